@@ -1,0 +1,363 @@
+"""Benchmark of the DeepThin compressed-layer hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Workload (N=1 default): BASELINE.json configs[1] ("config 2") — one DeepThin
+layer with straddling rows, in 440 -> out 2048, m_f 2816, n_f 320, rank 24,
+batch 4096 per GPU, bf16 operands / fp32 accumulate and fp32 output, on the
+general path (on-chip regeneration + tcgen05). A step is one forward of that
+batch. N GPUs = N ranks (torchrun), batch sharded: each rank runs its own
+4096 rows (weak scaling), no collective on the forward path.
+
+Prints ONE JSON line on rank 0. ``value`` = samples/s over all ranks from
+device-timed steps (CUDA events on the launching stream, max over ranks, L2
+flushed between steps). ``e2e`` = the same metric through the host-buffer
+C-ABI call (dt_session_forward: pinned host x -> device -> forward -> host y).
+``--impl reference`` times the reference algorithm's CPU port (oracle/, the
+reference's own route for rank > 1: decompress + matmul, kernel.py:313-319)
+on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # key: (q, r_dim, rank, n, m, batch, description)
+    "c2": (440, 2048, 24, 320, 2816, 4096,
+           "config2: DeepThin layer 440->2048 straddling rows (m_f 2816, n_f 320, r 24), "
+           "general path regen+tcgen05"),
+    "c1": (1024, 1024, 16, 256, 4096, 64,
+           "config1: DeepThin layer 1024->1024 reuse path (m_f 4096, n_f 256, r 16), fp32 FFMA"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback"
+
+
+def traffic_for(key):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled every 50 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        sm = [int(r[0]) for r in rows]
+        return {"sm_mhz": int(statistics.median(sm)), "sm_max_mhz": int(rows[0][1]),
+                "samples": len(rows), "reasons": reasons}
+
+    def __exit__(self, *a):
+        pass
+
+
+def dist_init():
+    import torch
+    import torch.distributed as tdist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not tdist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        tdist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def make_inputs(cfg, seed=0):
+    """BASELINE inputs: spawn_rngs(seed, 5) -> [xf, wf, bias, x, target], factors ~ N(0, 1/sqrt r)."""
+    import numpy as np
+    from paper_1802_06944_b200.core import sample_normal, spawn_rngs
+    q, r_dim, rank, n, m, batch, _ = cfg
+    rx, rw, rb, ri, _rt = spawn_rngs(seed, 5)
+    sd = 1.0 / math.sqrt(rank)
+    return dict(xf=sample_normal(rx, 0.0, sd, (m, rank)), wf=sample_normal(rw, 0.0, sd, (rank, n)),
+                bias=sample_normal(rb, 0.0, 0.01, (r_dim,)),
+                x=sample_normal(ri, 0.0, 1.0, (batch, q)).astype(np.float32))
+
+
+def cpu_reference_time(cfg, budget_s=12.0, rows=None):
+    """Time the reference algorithm's CPU port (oracle) on this host: samples/s, threads, sample."""
+    import numpy as np
+    threads = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    os.environ.setdefault("DEEPTHIN_THREADS", str(threads))
+    from oracle import deepthin_oracle as O
+    q, r_dim, rank, n, m, batch, _ = cfg
+    rows = rows or batch
+    d = make_inputs(cfg)
+    plan = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    xf, wf = d["xf"].astype(np.float32), d["wf"].astype(np.float32)
+    x = d["x"][:rows]
+    O.layer_forward(x, xf, wf, plan, d["bias"])  # warm
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        O.layer_forward(x, xf, wf, plan, d["bias"])   # decompress + matmul + bias (kernel.py:313-320)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return rows / med, threads, (f"{len(times)} calls of oracle.layer_forward on {rows} rows "
+                                 f"(fp32, median {med * 1e3:.1f} ms/call)")
+
+
+def run_reference(args, cfg, key):
+    rank, world, _ = dist_init()
+    if rank != 0:
+        return
+    # each "step" = one full-batch call on the host cores, bounded by the K/W counts
+    import numpy as np  # noqa: F401
+    budget = max(3.0, min(60.0, 0.05 * (args.steps + args.warmup) * 20))
+    sps, threads, sample = cpu_reference_time(cfg, budget_s=budget)
+    line = {"impl": "reference", "metric": "compressed-layer samples/sec", "value": round(sps, 3),
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(cfg[5] / sps * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg[6], "batch": cfg[5]},
+            "cpu_baseline": {"value": round(sps, 3), "unit": "samples/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(sps, 3), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg, key):
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    rank, world, local = dist_init()
+    torch.cuda.set_device(local)
+    import paper_1802_06944_b200 as D
+    from paper_1802_06944_b200 import _lib
+
+    q, r_dim, rank_r, n, m, batch, desc = cfg
+    plan = D.LayerPlan(q=q, r_dim=r_dim, rank=rank_r, m=m, n=n)
+    d = make_inputs(cfg, seed=0)
+    mma = "bf16" if key == "c2" else "ffma"
+    fp = D.FactorPair(d["xf"].astype(np.float32), d["wf"].astype(np.float32), plan)
+    bias = torch.tensor(d["bias"], dtype=torch.float32, device="cuda")
+    xdt = torch.bfloat16 if mma == "bf16" else torch.float32
+    x = torch.tensor(d["x"], device="cuda").to(xdt)
+    y = torch.empty((batch, r_dim), dtype=torch.float32, device="cuda")
+    code = _lib.DT_MMA_BF16 if mma == "bf16" else _lib.DT_MMA_FFMA
+    lib = _lib.lib()
+    ps = _lib.plan_struct(plan)
+    ws = torch.empty(max(256, lib.dt_forward_workspace_bytes(C.byref(ps), batch, code)),
+                     dtype=torch.uint8, device="cuda")
+    if mma == "bf16":
+        xf_d, wf_d = fp.bf16()
+        fdt = _lib.DT_BF16
+    else:
+        xf_d, wf_d, fdt = fp.xf, fp.wf, _lib.DT_F32
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step():
+        _lib.check(lib.dt_forward(C.byref(ps), batch, code, x.data_ptr(),
+                                  _lib.DT_BF16 if xdt == torch.bfloat16 else _lib.DT_F32,
+                                  xf_d.data_ptr(), wf_d.data_ptr(), fdt, bias.data_ptr(), 0, 0.0,
+                                  y.data_ptr(), _lib.DT_F32, ws.data_ptr(), ws.numel(), sh))
+
+    l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(max(2 * l2_bytes, 256 << 20), dtype=torch.uint8, device="cuda")
+
+    def l2_flush():
+        flush.fill_(1)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    # clock ramp + sampler (the sampler runs through warm-up and the timed region)
+    sampler = ClockSampler(local).__enter__()
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 0.5:
+        step()
+        l2_flush()
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+        l2_flush()
+    barrier()
+    n0 = lib.dt_launch_counter()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for s, e in ev:
+        l2_flush()
+        s.record(stream)
+        step()
+        e.record(stream)
+    barrier()
+    launches = (lib.dt_launch_counter() - n0)
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    samples = batch * world * args.steps
+    value = samples / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (one launch per step on this path)
+    bf16_peak, hbm_peak, peak_kind = peaks()
+    kernel_ms = statistics.mean(step_ms) / max(1, launches // max(1, args.steps))
+    if mma == "bf16":
+        flops = 2.0 * batch * q * r_dim                  # dense-equivalent per launch
+        achieved = flops / (kernel_ms * 1e-3) / 1e12
+        bytes_alg = batch * q * 2 + batch * r_dim * 4 + m * rank_r * 2 + rank_r * n * 2 + r_dim * 4
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_peak,
+                "unit": "TFLOP/s", "frac": round(achieved / bf16_peak, 4),
+                "traffic": traffic_for(key), "peak_source": f"{peak_kind} bf16_tflops (burst)",
+                "algorithmic_bytes": bytes_alg,
+                "hbm_gbs_at_algorithmic_bytes": round(bytes_alg / (kernel_ms * 1e-3) / 1e9, 1)}
+    else:
+        bytes_alg = 4 * (batch * q + batch * r_dim + m * rank_r + rank_r * n + r_dim)
+        achieved = bytes_alg / (kernel_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic_for(key),
+                "peak_source": f"{peak_kind} hbm_gbs"}
+
+    # e2e through the host-buffer C ABI (pinned host x in, host y out, every step)
+    sess = C.c_void_p()
+    _lib.check(lib.dt_session_create(C.byref(ps), code, d["xf"].astype(np.float32).ctypes.data,
+                                     d["wf"].astype(np.float32).ctypes.data,
+                                     d["bias"].astype(np.float32).ctypes.data, C.byref(sess)))
+    hx = torch.tensor(d["x"], dtype=torch.float32).pin_memory()
+    hy = torch.empty((batch, r_dim), dtype=torch.float32).pin_memory()
+    h2d, d2h = C.c_int64(), C.c_int64()
+
+    def e2e_step():
+        _lib.check(lib.dt_session_forward(sess, batch, hx.data_ptr(), 0, 0.0, hy.data_ptr(),
+                                          C.byref(h2d), C.byref(d2h)))
+
+    for _ in range(max(3, args.warmup)):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    e2e_value = samples / float(te.item())
+    lib.dt_session_destroy(sess)
+    # e2e parity spot check against the device path
+    ok = torch.allclose(hy.cuda(), y, rtol=0, atol=1e-3 * float(y.abs().max()))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, threads, sample = cpu_reference_time(cfg, budget_s=args.cpu_budget)
+        cpu = {"value": round(sps, 3), "unit": "samples/s", "cores": threads, "kind": "port",
+               "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "compressed-layer samples/sec", "value": round(value, 1), "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if mma == "bf16" else "f32", "data": "synthetic",
+            "config": {"workload": desc, "batch_per_gpu": batch, "global_batch": batch * world,
+                       "x_dtype": str(xdt).replace("torch.", ""), "y_dtype": "float32",
+                       "parallelism": f"dp{world} (batch-sharded replicas, no collective)",
+                       "l2": f"flushed between timed steps ({flush.numel() >> 20} MiB write)",
+                       "effective_tflops_dense_equiv": round(2.0 * batch * q * r_dim /
+                                                             (ms_per_step * 1e-3) / 1e12, 2)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 1), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
+                    "matches_device_path": bool(ok)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, args.config)
+    else:
+        run_ours(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    main()

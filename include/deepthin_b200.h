@@ -1,0 +1,158 @@
+/*
+ * deepthin_b200.h — C ABI of the B200-native DeepThin compressed-layer hot path.
+ *
+ * Notation is the reference's (deepthin, /root/reference/pkg/src/deepthin):
+ * a layer maps q inputs to r_dim outputs; its weight W (q x r_dim) is the
+ * column-major refill of v = (xf @ wf).ravel() with xf m x rank and wf
+ * rank x n (factor.py:1-9, 87-93). The trailing m*n - q*r_dim elements of v
+ * are discarded. y = x @ W + bias.
+ *
+ * Conventions
+ *  - Every device pointer is caller-owned (PyTorch allocates). Calls are
+ *    stream-ordered and asynchronous; none synchronises the host except the
+ *    dt_session_* host-buffer entry points.
+ *  - Matrices are dense row-major with the leading dimension equal to the
+ *    row length (x: batch x q, y: batch x r_dim, xf: m x rank, wf: rank x n).
+ *  - Return value is a dt_status; on failure dt_last_error() holds a
+ *    thread-local message. The Python shim maps DT_E_DIM → DimensionError,
+ *    DT_E_ARG → ArgumentError, DT_E_UNSUPPORTED → UnsupportedConfigurationError
+ *    (deepthin/errors.py:10-31), DT_E_CUDA → RuntimeError.
+ *  - Results are deterministic: no float atomics; every reduction has a
+ *    fixed order independent of launch geometry (kernel.py:264-266 analogue).
+ */
+#ifndef DEEPTHIN_B200_H
+#define DEEPTHIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *dt_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+/* Geometry of one compressed matrix — replaces planner.py:27-60 LayerPlan
+ * (q, r_dim, rank, m, n; validation m*n >= q*r_dim, all >= 1). */
+typedef struct {
+  int64_t q, r_dim, rank, m, n;
+} dt_plan;
+
+/* Derived geometry (factor.py:96-110, kernel.py:99-149). */
+typedef struct {
+  int64_t period;      /* n / gcd(n, q): columns per phase cycle            */
+  int64_t phase_count; /* min(period, r_dim)              (factor.py:108)   */
+  int64_t reuse;       /* 1 iff n | q: the factored-reuse path (a)          */
+  int64_t segments;    /* q / n on the reuse path, else 0                   */
+  int64_t tail;        /* m*n - q*r_dim discarded aux elements              */
+  int64_t rows_per_period; /* q / gcd(n, q): aux rows advanced per period   */
+} dt_plan_info;
+
+enum dt_status {
+  DT_OK = 0,
+  DT_E_DIM = 1,         /* DimensionError                  */
+  DT_E_ARG = 2,         /* ArgumentError                   */
+  DT_E_UNSUPPORTED = 3, /* UnsupportedConfigurationError   */
+  DT_E_CUDA = 4         /* CUDA launch / runtime failure   */
+};
+
+enum dt_dtype { DT_F32 = 0, DT_BF16 = 1 };
+
+/* Arithmetic of the contraction.
+ *  DT_MMA_FFMA: fp32 CUDA-core FFMA, fp32 operands (parity rtol 1e-5).
+ *  DT_MMA_BF16: tcgen05 kind::f16 tensor cores, bf16 operands, fp32 accumulate;
+ *               reuse-path partials stay fp32 (tf32 MMA) (parity rtol 2e-3).  */
+enum dt_mma { DT_MMA_FFMA = 0, DT_MMA_BF16 = 1 };
+
+/* kernel.py:39-48 (+ clipped ReLU and row softmax, used by BASELINE configs 3/4). */
+enum dt_act {
+  DT_ACT_IDENTITY = 0,
+  DT_ACT_RELU = 1,
+  DT_ACT_SIGMOID = 2,
+  DT_ACT_TANH = 3,
+  DT_ACT_CLIPPED_RELU = 4, /* min(max(z, 0), act_arg) */
+  DT_ACT_SOFTMAX = 5       /* row softmax (forward only) */
+};
+
+const char *dt_version(void);
+/* Thread-local message of the last failing call on this thread. */
+const char *dt_last_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+int64_t dt_launch_counter(void);
+
+/* ---- geometry (host-only, no GPU needed) ---------------------------------- */
+/* planner.py:38-47 LayerPlan.__post_init__ validation. */
+int dt_plan_validate(const dt_plan *plan);
+int dt_plan_query(const dt_plan *plan, dt_plan_info *info);
+/* factor.py:96-105 phase(col, plan). */
+int dt_phase(const dt_plan *plan, int64_t col, int64_t *out_phase);
+/* factor.py:74-84 relayout_index(flat, plan). */
+int dt_relayout_index(const dt_plan *plan, int64_t flat, int64_t *row, int64_t *col);
+/* kernel.py:184-205 predict_reuse(plan, batch): per-row distinct / total runs. */
+int dt_predict_reuse(const dt_plan *plan, int64_t batch, int64_t *distinct_runs,
+                     int64_t *total_runs);
+/* kernel.py:277-280 OpCount of the run-memoized algorithm over `batch` rows. */
+int dt_op_count(const dt_plan *plan, int64_t batch, int64_t *multiplies, int64_t *adds);
+
+/* ---- device compute --------------------------------------------------------- */
+/* Replaces factor.py:87-93 decompress(fp): W (q x r_dim, row-major fp32). */
+int dt_decompress(const dt_plan *plan, const float *xf, const float *wf, float *w,
+                  dt_stream stream);
+
+/* Round fp32 → bf16 (RNE); used to make the bf16 operand copies of factors. */
+int dt_cast_bf16(int64_t count, const float *src, uint16_t *dst, dt_stream stream);
+
+size_t dt_forward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma);
+
+/* Replaces kernel.py:222-293 fused_matmul and kernel.py:296-320 layer_forward:
+ * y = act(x @ W + bias) without materialising W.
+ *   x      batch x q, dtype x_dtype (DT_F32 or DT_BF16)
+ *   xf, wf fp32 masters (DT_MMA_FFMA) or bf16 copies (DT_MMA_BF16): f_dtype
+ *   bias   r_dim fp32, nullable (= zero)
+ *   y      batch x r_dim, dtype y_dtype
+ * Reuse path (n | q) and general path (straddling rows) are chosen from the plan. */
+int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x_dtype,
+               const void *xf, const void *wf, int f_dtype, const float *bias, int act,
+               float act_arg, void *y, int y_dtype, void *workspace, size_t workspace_bytes,
+               dt_stream stream);
+
+size_t dt_backward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma);
+
+/* Replaces grad.py:63-95 layer_backward: gradients through activation, bias,
+ * the contraction, the inverse re-layout (tail gets zero) and the factor product.
+ *   upstream batch x r_dim fp32 (dLoss/dy)
+ *   d_xf m x rank, d_wf rank x n, d_bias r_dim fp32 (d_bias nullable)
+ *   d_input batch x q fp32, nullable (skipped)
+ * Pre-activations are recomputed (grad.py:81-83) unless act == IDENTITY. */
+int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x_dtype,
+                const float *xf, const float *wf, const float *bias, int act, float act_arg,
+                const float *upstream, float *d_xf, float *d_wf, float *d_bias,
+                float *d_input, void *workspace, size_t workspace_bytes, dt_stream stream);
+
+/* grad.py:98-103 loss_and_grad("mse") for one shard of rows:
+ *   grad = 2 (y - t) / norm_count;  loss_sum[0] = sum (y - t)^2  (fp64, fixed order).
+ * norm_count is the GLOBAL y.size when the batch is sharded across ranks. */
+int dt_mse_grad(int64_t rows, int64_t cols, const float *y, const float *target,
+                double norm_count, float *grad, double *loss_sum, void *workspace,
+                size_t workspace_bytes, dt_stream stream);
+size_t dt_mse_workspace_bytes(int64_t rows, int64_t cols);
+
+/* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
+int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);
+
+/* ---- host-buffer entry points (the binding a numpy caller would use) -------- */
+/* A session owns device-resident copies of one layer's factors and bias — the
+ * analogue of FactorPair's private read-only copies (factor.py:42-50). */
+typedef struct dt_session dt_session;
+int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const float *wf_host,
+                      const float *bias_host, dt_session **out);
+/* Host x (batch x q fp32) → device, forward, device → host y (batch x r_dim
+ * fp32); synchronous. Returns the bytes moved in *h2d / *d2h when non-NULL. */
+int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int act,
+                       float act_arg, float *y_host, int64_t *h2d_bytes, int64_t *d2h_bytes);
+void dt_session_destroy(dt_session *s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEEPTHIN_B200_H */

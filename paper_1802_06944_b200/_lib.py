@@ -1,0 +1,106 @@
+"""ctypes binding of libdeepthin_b200.so (include/deepthin_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every compute call raises CudaError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import ArgumentError, CudaError, DimensionError, UnsupportedConfigurationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
+
+DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA = range(5)
+DT_F32, DT_BF16 = 0, 1
+DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
+ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
+
+# Every symbol the header declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "dt_version", "dt_last_error", "dt_launch_counter", "dt_plan_validate", "dt_plan_query", "dt_phase",
+    "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
+    "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
+    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_sgd_step", "dt_session_create",
+    "dt_session_forward", "dt_session_destroy",
+)
+
+
+class Plan(C.Structure):
+    _fields_ = [("q", C.c_int64), ("r_dim", C.c_int64), ("rank", C.c_int64),
+                ("m", C.c_int64), ("n", C.c_int64)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("period", C.c_int64), ("phase_count", C.c_int64), ("reuse", C.c_int64),
+                ("segments", C.c_int64), ("tail", C.c_int64), ("rows_per_period", C.c_int64)]
+
+
+_lib = None
+
+
+def _declare(lib):
+    P, I64, VP, F, D, SZ = C.POINTER(Plan), C.c_int64, C.c_void_p, C.c_float, C.c_double, C.c_size_t
+    i = C.c_int
+    sig = {
+        "dt_version": ([], C.c_char_p),
+        "dt_last_error": ([], C.c_char_p),
+        "dt_launch_counter": ([], I64),
+        "dt_plan_validate": ([P], i),
+        "dt_plan_query": ([P, C.POINTER(PlanInfo)], i),
+        "dt_phase": ([P, I64, C.POINTER(I64)], i),
+        "dt_relayout_index": ([P, I64, C.POINTER(I64), C.POINTER(I64)], i),
+        "dt_predict_reuse": ([P, I64, C.POINTER(I64), C.POINTER(I64)], i),
+        "dt_op_count": ([P, I64, C.POINTER(I64), C.POINTER(I64)], i),
+        "dt_decompress": ([P, VP, VP, VP, VP], i),
+        "dt_cast_bf16": ([I64, VP, VP, VP], i),
+        "dt_forward_workspace_bytes": ([P, I64, i], SZ),
+        "dt_forward": ([P, I64, i, VP, i, VP, VP, i, VP, i, F, VP, i, VP, SZ, VP], i),
+        "dt_backward_workspace_bytes": ([P, I64, i], SZ),
+        "dt_backward": ([P, I64, i, VP, i, VP, VP, VP, i, F, VP, VP, VP, VP, VP, VP, SZ, VP], i),
+        "dt_mse_workspace_bytes": ([I64, I64], SZ),
+        "dt_mse_grad": ([I64, I64, VP, VP, D, VP, VP, VP, SZ, VP], i),
+        "dt_sgd_step": ([I64, VP, VP, F, VP], i),
+        "dt_session_create": ([P, i, VP, VP, VP, C.POINTER(VP)], i),
+        "dt_session_forward": ([VP, I64, VP, i, F, VP, C.POINTER(I64), C.POINTER(I64)], i),
+        "dt_session_destroy": ([VP], None),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib():
+    """Load (once) and return the native library; raise CudaError if it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaError(
+                f"native library {LIB_PATH} is missing; build it with "
+                "`python -m paper_1802_06944_b200.build` (there is no CPU fallback)")
+        handle = C.CDLL(LIB_PATH)
+        _declare(handle)
+        _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Raise the reference exception type matching a dt_status."""
+    if rc == DT_OK:
+        return
+    msg = lib().dt_last_error().decode(errors="replace")
+    if rc == DT_E_DIM:
+        raise DimensionError(msg)
+    if rc == DT_E_ARG:
+        raise ArgumentError(msg)
+    if rc == DT_E_UNSUPPORTED:
+        raise UnsupportedConfigurationError(msg)
+    raise CudaError(msg or f"dt status {rc}")
+
+
+def plan_struct(plan) -> Plan:
+    return Plan(plan.q, plan.r_dim, plan.rank, plan.m, plan.n)

@@ -1,0 +1,418 @@
+// extern "C" entry points of libdeepthin_b200.so (declared in include/deepthin_b200.h).
+//
+// Validation and error conventions mirror the reference: shape problems are
+// DT_E_DIM (DimensionError), bad scalars DT_E_ARG (ArgumentError), an
+// unsupported configuration DT_E_UNSUPPORTED (UnsupportedConfigurationError)
+// — deepthin/errors.py:10-31, core.py:21-36, kernel.py:238-246, grad.py:74-79.
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "dt_internal.h"
+
+namespace dt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+// planner.py:38-47 (LayerPlan.__post_init__) plus the derived geometry of
+// factor.py:96-110 and kernel.py:102-106.
+int make_geo(const dt_plan *plan, Geo *g) {
+  if (!plan) {
+    set_error("plan is NULL");
+    return DT_E_ARG;
+  }
+  const char *names[5] = {"q", "r_dim", "rank", "m", "n"};
+  const int64_t vals[5] = {plan->q, plan->r_dim, plan->rank, plan->m, plan->n};
+  for (int i = 0; i < 5; ++i)
+    if (vals[i] < 1) {
+      set_error(std::string(names[i]) + " must be >= 1, got " + std::to_string(vals[i]));
+      return DT_E_ARG;
+    }
+  if (plan->m * plan->n < plan->q * plan->r_dim) {
+    set_error("m*n = " + std::to_string(plan->m * plan->n) + " must cover q*r_dim = " +
+              std::to_string(plan->q * plan->r_dim));
+    return DT_E_ARG;
+  }
+  g->q = plan->q;
+  g->r_dim = plan->r_dim;
+  g->rank = plan->rank;
+  g->m = plan->m;
+  g->n = plan->n;
+  const int64_t gc = std::gcd(plan->n, plan->q);
+  g->period = plan->n / gc;
+  g->phase_count = std::min(g->period, plan->r_dim);
+  g->rows_per_period = plan->q / gc;
+  g->tail = plan->m * plan->n - plan->q * plan->r_dim;
+  g->reuse = (plan->q % plan->n) == 0;
+  g->s = g->reuse ? plan->q / plan->n : 0;
+  return DT_OK;
+}
+
+}  // namespace dt
+
+using namespace dt;
+
+namespace {
+
+int check_dtype(int dt, const char *what) {
+  if (dt != DT_F32 && dt != DT_BF16) {
+    set_error(std::string(what) + ": unknown dtype " + std::to_string(dt));
+    return DT_E_ARG;
+  }
+  return DT_OK;
+}
+
+int check_act(int act) {
+  if (act < DT_ACT_IDENTITY || act > DT_ACT_SOFTMAX) {
+    set_error("unknown activation " + std::to_string(act));
+    return DT_E_ARG;
+  }
+  return DT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dt_version(void) { return "deepthin_b200 0.1.0 (sm_100a)"; }
+
+const char *dt_last_error(void) { return g_last_error.c_str(); }
+
+int64_t dt_launch_counter(void) { return launch_count(); }
+
+int dt_plan_validate(const dt_plan *plan) {
+  Geo g;
+  return make_geo(plan, &g);
+}
+
+int dt_plan_query(const dt_plan *plan, dt_plan_info *info) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  info->period = g.period;
+  info->phase_count = g.phase_count;
+  info->reuse = g.reuse ? 1 : 0;
+  info->segments = g.s;
+  info->tail = g.tail;
+  info->rows_per_period = g.rows_per_period;
+  return DT_OK;
+}
+
+int dt_phase(const dt_plan *plan, int64_t col, int64_t *out) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (col < 0 || col >= g.r_dim) {
+    set_error("col " + std::to_string(col) + " out of range for r_dim " + std::to_string(g.r_dim));
+    return DT_E_ARG;
+  }
+  *out = (col * g.q) % g.n;
+  return DT_OK;
+}
+
+int dt_relayout_index(const dt_plan *plan, int64_t flat, int64_t *row, int64_t *col) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (flat < 0 || flat >= g.q * g.r_dim) {
+    set_error("flat index " + std::to_string(flat) + " out of range for " + std::to_string(g.q) +
+              "x" + std::to_string(g.r_dim) + " target");
+    return DT_E_ARG;
+  }
+  *row = flat % g.q;
+  *col = flat / g.q;
+  return DT_OK;
+}
+
+// kernel.py:184-205: per phase slot t, runs = 1 + (p + q - 1) // n with p = t*q mod n.
+int dt_predict_reuse(const dt_plan *plan, int64_t batch, int64_t *distinct, int64_t *total) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (batch < 1) {
+    set_error("batch must be >= 1, got " + std::to_string(batch));
+    return DT_E_ARG;
+  }
+  int64_t d = 0, t = 0;
+  for (int64_t ph = 0; ph < g.phase_count; ++ph) {
+    const int64_t p = (ph * g.q) % g.n;
+    const int64_t runs = 1 + (p + g.q - 1) / g.n;
+    const int64_t cols = (g.r_dim - ph + g.period - 1) / g.period;
+    d += runs;
+    t += runs * cols;
+  }
+  *distinct = d;
+  *total = t;
+  return DT_OK;
+}
+
+// kernel.py:277-280: multiplies = B*(sum_len + total), adds = B*(sum_len - distinct) + B*(total - r_dim)
+// where sum_len is the summed length of the distinct runs (kernel.py:107-121).
+int dt_op_count(const dt_plan *plan, int64_t batch, int64_t *mul, int64_t *add) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  int64_t distinct, total;
+  if (int rc = dt_predict_reuse(plan, 1, &distinct, &total)) return rc;
+  int64_t sum_len = 0;
+  for (int64_t t = 0; t < g.phase_count; ++t) {
+    const int64_t p = (t * g.q) % g.n;
+    // run starts: 0, then n-p, n-p+n, ... < q; first run at wf offset p, others at 0
+    const int64_t first = std::min(g.n - p, g.q);
+    sum_len += first;
+    for (int64_t s = g.n - p; s < g.q; s += g.n) sum_len += std::min(g.n, g.q - s);
+  }
+  *mul = batch * (sum_len + total);
+  *add = batch * (sum_len - distinct) + batch * (total - g.r_dim);
+  return DT_OK;
+}
+
+int dt_decompress(const dt_plan *plan, const float *xf, const float *wf, float *w,
+                  dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  return launch_decompress(g, xf, wf, w, (cudaStream_t)stream);
+}
+
+int dt_cast_bf16(int64_t count, const float *src, uint16_t *dst, dt_stream stream) {
+  if (count < 0) {
+    set_error("count must be >= 0");
+    return DT_E_ARG;
+  }
+  return launch_cast_bf16(count, src, dst, (cudaStream_t)stream);
+}
+
+size_t dt_forward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) {
+  Geo g;
+  if (make_geo(plan, &g) || batch < 0) return 0;
+  if (mma == DT_MMA_BF16 && !g.reuse) return tc_general_ws(g, batch);
+  return ffma_forward_ws(g, batch);
+}
+
+int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x_dtype,
+               const void *xf, const void *wf, int f_dtype, const float *bias, int act,
+               float act_arg, void *y, int y_dtype, void *workspace, size_t workspace_bytes,
+               dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (batch < 0) {
+    set_error("batch must be >= 0");
+    return DT_E_DIM;
+  }
+  if (int rc = check_dtype(x_dtype, "x")) return rc;
+  if (int rc = check_dtype(y_dtype, "y")) return rc;
+  if (int rc = check_dtype(f_dtype, "factors")) return rc;
+  if (int rc = check_act(act)) return rc;
+  if (batch > 0 && (!x || !xf || !wf || !y)) {
+    set_error("NULL operand pointer");
+    return DT_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mma == DT_MMA_FFMA) {
+    if (f_dtype != DT_F32) {
+      set_error("the FFMA path takes fp32 factors");
+      return DT_E_ARG;
+    }
+    if (batch == 0) return DT_OK;
+    return ffma_forward(g, batch, x, x_dtype, (const float *)xf, (const float *)wf, bias, act,
+                        act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
+  }
+  if (mma == DT_MMA_BF16) {
+    if (f_dtype != DT_BF16) {
+      set_error("the bf16 tensor-core path takes bf16 factor copies (dt_cast_bf16)");
+      return DT_E_ARG;
+    }
+    if (g.reuse) {
+      set_error("bf16 tensor-core reuse path is not built yet");
+      return DT_E_UNSUPPORTED;
+    }
+    return tc_general_forward(g, batch, x, x_dtype, (const uint16_t *)xf, (const uint16_t *)wf,
+                              bias, act, act_arg, y, y_dtype, (char *)workspace, workspace_bytes,
+                              st);
+  }
+  set_error("unknown mma kind " + std::to_string(mma));
+  return DT_E_ARG;
+}
+
+size_t dt_backward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) {
+  Geo g;
+  if (make_geo(plan, &g) || batch < 0) return 0;
+  (void)mma;
+  return ffma_backward_ws(g, batch);
+}
+
+int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x_dtype,
+                const float *xf, const float *wf, const float *bias, int act, float act_arg,
+                const float *upstream, float *d_xf, float *d_wf, float *d_bias, float *d_input,
+                void *workspace, size_t workspace_bytes, dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (batch < 0) {
+    set_error("batch must be >= 0");
+    return DT_E_DIM;
+  }
+  if (int rc = check_dtype(x_dtype, "x")) return rc;
+  if (int rc = check_act(act)) return rc;
+  if (act == DT_ACT_SOFTMAX) {
+    set_error("softmax is forward-only (use the fused softmax cross-entropy gradient)");
+    return DT_E_UNSUPPORTED;
+  }
+  if (!xf || !wf || !d_xf || !d_wf || (batch > 0 && (!x || !upstream))) {
+    set_error("NULL operand pointer");
+    return DT_E_ARG;
+  }
+  if (mma != DT_MMA_FFMA && mma != DT_MMA_BF16) {
+    set_error("unknown mma kind " + std::to_string(mma));
+    return DT_E_ARG;
+  }
+  return ffma_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
+                       d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t dt_mse_workspace_bytes(int64_t rows, int64_t cols) { return mse_ws(rows, cols); }
+
+int dt_mse_grad(int64_t rows, int64_t cols, const float *y, const float *target,
+                double norm_count, float *grad, double *loss_sum, void *workspace,
+                size_t workspace_bytes, dt_stream stream) {
+  if (rows < 0 || cols < 0) {
+    set_error("negative shape");
+    return DT_E_DIM;
+  }
+  if (!(norm_count > 0)) {
+    set_error("norm_count must be > 0");
+    return DT_E_ARG;
+  }
+  return launch_mse_grad(rows, cols, y, target, norm_count, grad, loss_sum, (char *)workspace,
+                         workspace_bytes, (cudaStream_t)stream);
+}
+
+int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream) {
+  if (count < 0) {
+    set_error("count must be >= 0");
+    return DT_E_ARG;
+  }
+  if (!(lr > 0.f)) {
+    set_error("learning_rate must be > 0");
+    return DT_E_ARG;
+  }
+  return launch_sgd(count, param, grad, lr, (cudaStream_t)stream);
+}
+
+// ---- host-buffer sessions ---------------------------------------------------------------
+struct dt_session {
+  dt_plan plan;
+  Geo geo;
+  int mma;
+  float *xf = nullptr, *wf = nullptr, *bias = nullptr;
+  uint16_t *xf16 = nullptr, *wf16 = nullptr;
+  float *x = nullptr, *y = nullptr;
+  char *ws = nullptr;
+  size_t ws_bytes = 0;
+  int64_t cap_batch = 0;
+  cudaStream_t stream = nullptr;
+};
+
+static void session_free_io(dt_session *s) {
+  cudaFree(s->x);
+  cudaFree(s->y);
+  cudaFree(s->ws);
+  s->x = s->y = nullptr;
+  s->ws = nullptr;
+  s->cap_batch = 0;
+}
+
+int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const float *wf_host,
+                      const float *bias_host, dt_session **out) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (mma != DT_MMA_FFMA && mma != DT_MMA_BF16) {
+    set_error("unknown mma kind");
+    return DT_E_ARG;
+  }
+  dt_session *s = new dt_session();
+  s->plan = *plan;
+  s->geo = g;
+  s->mma = mma;
+  const size_t nx = (size_t)g.m * g.rank, nw = (size_t)g.rank * g.n;
+  cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&s->xf, nx * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->wf, nw * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->bias, (size_t)g.r_dim * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->xf16, nx * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&s->wf16, nw * 2);
+  if (e == cudaSuccess) e = cudaMemcpy(s->xf, xf_host, nx * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(s->wf, wf_host, nw * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    if (bias_host)
+      e = cudaMemcpy(s->bias, bias_host, (size_t)g.r_dim * 4, cudaMemcpyHostToDevice);
+    else
+      e = cudaMemset(s->bias, 0, (size_t)g.r_dim * 4);
+  }
+  if (e != cudaSuccess) {
+    set_error(std::string("session create: ") + cudaGetErrorString(e));
+    dt_session_destroy(s);
+    return DT_E_CUDA;
+  }
+  int rc = launch_cast_bf16((int64_t)nx, s->xf, s->xf16, s->stream);
+  if (!rc) rc = launch_cast_bf16((int64_t)nw, s->wf, s->wf16, s->stream);
+  if (!rc && cudaStreamSynchronize(s->stream) != cudaSuccess) rc = DT_E_CUDA;
+  if (rc) {
+    dt_session_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return DT_OK;
+}
+
+int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int act, float act_arg,
+                       float *y_host, int64_t *h2d, int64_t *d2h) {
+  if (!s) {
+    set_error("NULL session");
+    return DT_E_ARG;
+  }
+  if (batch < 0) {
+    set_error("batch must be >= 0");
+    return DT_E_DIM;
+  }
+  const Geo &g = s->geo;
+  if (batch > s->cap_batch) {
+    session_free_io(s);
+    size_t ws = dt_forward_workspace_bytes(&s->plan, batch, s->mma);
+    cudaError_t e = cudaMalloc(&s->x, (size_t)batch * g.q * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&s->y, (size_t)batch * g.r_dim * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&s->ws, ws ? ws : 256);
+    if (e != cudaSuccess) {
+      set_error(std::string("session alloc: ") + cudaGetErrorString(e));
+      session_free_io(s);
+      return DT_E_CUDA;
+    }
+    s->ws_bytes = ws;
+    s->cap_batch = batch;
+  }
+  const size_t xb = (size_t)batch * g.q * 4, yb = (size_t)batch * g.r_dim * 4;
+  DT_CUDA_CHECK(cudaMemcpyAsync(s->x, x_host, xb, cudaMemcpyHostToDevice, s->stream));
+  const bool tc = s->mma == DT_MMA_BF16;
+  int rc = dt_forward(&s->plan, batch, s->mma, s->x, DT_F32, tc ? (const void *)s->xf16 : s->xf,
+                      tc ? (const void *)s->wf16 : s->wf, tc ? DT_BF16 : DT_F32, s->bias, act,
+                      act_arg, s->y, DT_F32, s->ws, s->ws_bytes, (dt_stream)s->stream);
+  if (rc) return rc;
+  DT_CUDA_CHECK(cudaMemcpyAsync(y_host, s->y, yb, cudaMemcpyDeviceToHost, s->stream));
+  DT_CUDA_CHECK(cudaStreamSynchronize(s->stream));
+  if (h2d) *h2d = (int64_t)xb;
+  if (d2h) *d2h = (int64_t)yb;
+  return DT_OK;
+}
+
+void dt_session_destroy(dt_session *s) {
+  if (!s) return;
+  session_free_io(s);
+  cudaFree(s->xf);
+  cudaFree(s->wf);
+  cudaFree(s->bias);
+  cudaFree(s->xf16);
+  cudaFree(s->wf16);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+}  // extern "C"

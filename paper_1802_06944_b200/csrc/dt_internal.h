@@ -1,0 +1,64 @@
+// Internal declarations shared by the C-ABI translation unit and the kernel files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/deepthin_b200.h"
+
+namespace dt {
+
+// Thread-local error message behind dt_last_error().
+void set_error(const std::string &msg);
+
+// ---- geometry -------------------------------------------------------------
+struct Geo {
+  int64_t q, r_dim, rank, m, n;
+  int64_t period, phase_count, rows_per_period, tail;
+  bool reuse;
+  int64_t s;  // q / n on the reuse path
+};
+int make_geo(const dt_plan *plan, Geo *g);
+
+// ---- fp32 CUDA-core (FFMA) path: k_simt.cu -----------------------------------
+int ffma_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                 const float *wf, const float *bias, int act, float act_arg, void *y,
+                 int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st);
+size_t ffma_forward_ws(const Geo &g, int64_t batch);
+int ffma_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                  const float *wf, const float *bias, int act, float act_arg,
+                  const float *upstream, float *d_xf, float *d_wf, float *d_bias,
+                  float *d_input, char *ws, size_t ws_bytes, cudaStream_t st);
+size_t ffma_backward_ws(const Geo &g, int64_t batch);
+
+int launch_decompress(const Geo &g, const float *xf, const float *wf, float *w, cudaStream_t st);
+int launch_cast_bf16(int64_t count, const float *src, uint16_t *dst, cudaStream_t st);
+int launch_row_softmax(int64_t rows, int64_t cols, void *y, int y_dtype, cudaStream_t st);
+int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, double norm,
+                    float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st);
+size_t mse_ws(int64_t rows, int64_t cols);
+int launch_sgd(int64_t count, float *p, const float *g, float lr, cudaStream_t st);
+
+// ---- tcgen05 tensor-core path: k_tc_general.cu ---------------------------------
+int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
+                       const uint16_t *xf_bf16, const uint16_t *wf_bf16, const float *bias,
+                       int act, float act_arg, void *y, int y_dtype, char *ws, size_t ws_bytes,
+                       cudaStream_t st);
+size_t tc_general_ws(const Geo &g, int64_t batch);
+
+// Every kernel launch goes through check_launch, which also counts it (dt_launch_counter).
+int check_launch(const char *what);
+int64_t launch_count();
+
+}  // namespace dt
+
+#define DT_CUDA_CHECK(expr)                                                        \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      dt::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+      return DT_E_CUDA;                                                            \
+    }                                                                              \
+  } while (0)

@@ -1,0 +1,114 @@
+"""The compressed representation on the GPU (reference factor.py:23-110).
+
+A FactorPair owns private, device-resident fp32 copies of the factors (the
+reference's private read-only copies, factor.py:42-50) plus lazily cached
+bf16 operand copies for the tensor-core path (the analogue of the per-pair
+cached combine weights, kernel.py:157-164).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import as_device_matrix, device, sample_normal, stream_handle
+from .errors import ArgumentError, DimensionError
+from .planner import LayerPlan
+
+
+@dataclass(frozen=True)
+class FactorPair:
+    """Learnable factors (xf: m x rank, wf: rank x n) plus their plan; device-resident."""
+
+    xf: torch.Tensor
+    wf: torch.Tensor
+    plan: LayerPlan
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def __post_init__(self):
+        host = not isinstance(self.xf, torch.Tensor)
+        xf, _ = as_device_matrix(self.xf, name="xf", keep_bf16=False)
+        wf, _ = as_device_matrix(self.wf, name="wf", keep_bf16=False)
+        p = self.plan
+        if tuple(xf.shape) != (p.m, p.rank):
+            raise DimensionError(f"xf must be {p.m}x{p.rank}, got {xf.shape[0]}x{xf.shape[1]}")
+        if tuple(wf.shape) != (p.rank, p.n):
+            raise DimensionError(f"wf must be {p.rank}x{p.n}, got {wf.shape[0]}x{wf.shape[1]}")
+        # private copies: never alias (or later see edits to) the caller's buffers
+        object.__setattr__(self, "xf", xf.clone() if xf.data_ptr() == _ptr(self.xf) else xf)
+        object.__setattr__(self, "wf", wf.clone() if wf.data_ptr() == _ptr(self.wf) else wf)
+        self._cache["host"] = host
+
+    @property
+    def dtype(self):
+        return self.xf.dtype
+
+    @property
+    def from_numpy(self) -> bool:
+        return bool(self._cache.get("host", False))
+
+    def with_values(self, xf, wf) -> "FactorPair":
+        return FactorPair(xf=xf, wf=wf, plan=self.plan)
+
+    def bf16(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """bf16 (RNE) copies of the factors, made once per pair by dt_cast_bf16."""
+        if "bf16" not in self._cache:
+            lib = _lib.lib()
+            out = []
+            for t in (self.xf, self.wf):
+                o = torch.empty(t.shape, dtype=torch.bfloat16, device=t.device)
+                _lib.check(lib.dt_cast_bf16(t.numel(), t.data_ptr(), o.data_ptr(), stream_handle()))
+                out.append(o)
+            self._cache["bf16"] = tuple(out)
+        return self._cache["bf16"]
+
+
+def _ptr(a) -> int:
+    return a.data_ptr() if isinstance(a, torch.Tensor) else -1
+
+
+def init_factors(plan: LayerPlan, sigma: float, rng: np.random.Generator) -> FactorPair:
+    """factor.py:60-71: xf ~ N(0, sigma^2), wf ~ N(0, 1/rank), drawn on the host."""
+    if not sigma > 0:
+        raise ArgumentError(f"sigma must be > 0, got {sigma}")
+    xf = sample_normal(rng, 0.0, sigma, (plan.m, plan.rank))
+    wf = sample_normal(rng, 0.0, 1.0 / math.sqrt(plan.rank), (plan.rank, plan.n))
+    return FactorPair(xf=xf, wf=wf, plan=plan)
+
+
+def relayout_index(flat: int, plan: LayerPlan) -> tuple[int, int]:
+    """factor.py:74-84 via dt_relayout_index."""
+    row, col = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().dt_relayout_index(C.byref(_lib.plan_struct(plan)), int(flat),
+                                            C.byref(row), C.byref(col)))
+    return row.value, col.value
+
+
+def phase(col: int, plan: LayerPlan) -> int:
+    """factor.py:96-105 via dt_phase."""
+    out = C.c_int64()
+    _lib.check(_lib.lib().dt_phase(C.byref(_lib.plan_struct(plan)), int(col), C.byref(out)))
+    return out.value
+
+
+def phase_count(plan: LayerPlan) -> int:
+    """factor.py:108-110."""
+    return int(plan.info().phase_count)
+
+
+def decompress(fp: FactorPair):
+    """factor.py:87-93: materialise the dense q x r_dim W (fp32) on the GPU.
+
+    Debug/oracle helper — the forward and backward never call it. Returns a
+    numpy array when the pair was built from numpy, else a CUDA tensor.
+    """
+    p = fp.plan
+    w = torch.empty((p.q, p.r_dim), dtype=torch.float32, device=device())
+    _lib.check(_lib.lib().dt_decompress(C.byref(_lib.plan_struct(p)), fp.xf.data_ptr(),
+                                        fp.wf.data_ptr(), w.data_ptr(), stream_handle()))
+    return w.cpu().numpy() if fp.from_numpy else w

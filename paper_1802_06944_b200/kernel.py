@@ -1,0 +1,172 @@
+"""Fused forward on the compressed form (reference kernel.py:39-320), on the GPU.
+
+``fused_matmul`` / ``layer_forward`` keep the reference's names, argument
+meaning and errors, and route to the sm_100a kernels through dt_forward:
+
+* reuse path (n | q): every distinct run dot is computed once per input row
+  (P = x.view(B*s, n) @ wf^T) and combined with xf (scale-after-dot);
+* general path (straddling rows): W tiles are regenerated from the factors
+  on chip and contracted without W ever touching HBM.
+
+Deliberate extensions: every rank is fused (the reference's rank-1 limit,
+kernel.py:238-240, and its decompress fallback warning, :313-319, are
+lifted), and activations include clipped ReLU and row softmax (BASELINE
+configs 3/4). ``mma`` selects exact fp32 FFMA ("ffma", parity rtol 1e-5) or
+bf16 tcgen05 tensor cores with fp32 accumulation ("bf16", rtol 2e-3).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import as_device_matrix, as_device_vector, device, stream_handle, workspace
+from .errors import ArgumentError, DimensionError
+from .factor import FactorPair
+
+ACTIVATIONS = ("identity", "relu", "sigmoid", "tanh")
+EXTRA_ACTIVATIONS = ("clipped_relu", "softmax")
+
+
+@dataclass
+class OpCount:
+    """kernel.py:65-77 — counts of the canonical run-memoized algorithm."""
+
+    multiplies: int = 0
+    adds: int = 0
+
+
+@dataclass
+class ReuseTable:
+    """kernel.py:80-96 — hit/miss accounting (entries are not recorded on the GPU)."""
+
+    hits: int = 0
+    misses: int = 0
+    record_entries: bool = False
+    entries: dict = field(default_factory=dict)
+
+
+class ReusePrediction(tuple):
+    """(distinct_runs, total_runs) per input row (kernel.py:167-181)."""
+
+    __slots__ = ()
+
+    def __new__(cls, distinct_runs: int, total_runs: int):
+        return super().__new__(cls, (distinct_runs, total_runs))
+
+    @property
+    def distinct_runs(self) -> int:
+        return self[0]
+
+    @property
+    def total_runs(self) -> int:
+        return self[1]
+
+
+def predict_reuse(plan, batch: int = 1) -> ReusePrediction:
+    """kernel.py:184-205 via dt_predict_reuse."""
+    d, t = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().dt_predict_reuse(C.byref(_lib.plan_struct(plan)), int(batch),
+                                           C.byref(d), C.byref(t)))
+    return ReusePrediction(d.value, t.value)
+
+
+def op_count(plan, batch: int) -> OpCount:
+    mul, add = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().dt_op_count(C.byref(_lib.plan_struct(plan)), int(batch),
+                                      C.byref(mul), C.byref(add)))
+    return OpCount(multiplies=mul.value, adds=add.value)
+
+
+def _resolve_threads(threads):
+    """kernel.py:208-214 — accepted for signature parity; GPU results never depend on it."""
+    if threads is None:
+        env = os.environ.get("DEEPTHIN_THREADS")
+        threads = int(env) if env else 1
+    if threads < 1:
+        raise ArgumentError(f"threads must be >= 1, got {threads}")
+    return threads
+
+
+def _act_code(activation: str) -> int:
+    try:
+        return _lib.ACT_CODES[activation]
+    except KeyError:
+        raise ArgumentError(
+            f"unknown activation {activation!r}; expected one of "
+            f"{ACTIVATIONS + EXTRA_ACTIVATIONS}") from None
+
+
+def resolve_mma(mma, x: torch.Tensor, plan) -> int:
+    if mma is None:
+        mma = "bf16" if x.dtype == torch.bfloat16 else "ffma"
+    if mma not in ("ffma", "bf16"):
+        raise ArgumentError(f"mma must be 'ffma' or 'bf16', got {mma!r}")
+    return _lib.DT_MMA_BF16 if mma == "bf16" else _lib.DT_MMA_FFMA
+
+
+def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float, y: torch.Tensor,
+                 mma: int) -> None:
+    """Raw stream-ordered dt_forward on device tensors (no validation beyond the ABI's)."""
+    p = fp.plan
+    lib = _lib.lib()
+    ps = _lib.plan_struct(p)
+    batch = x.shape[0]
+    ws_bytes = lib.dt_forward_workspace_bytes(C.byref(ps), batch, mma)
+    ws = workspace(ws_bytes)
+    if mma == _lib.DT_MMA_BF16:
+        xf, wf = fp.bf16()
+        fdt = _lib.DT_BF16
+    else:
+        xf, wf, fdt = fp.xf, fp.wf, _lib.DT_F32
+    _lib.check(lib.dt_forward(
+        C.byref(ps), batch, mma, x.data_ptr(),
+        _lib.DT_BF16 if x.dtype == torch.bfloat16 else _lib.DT_F32,
+        xf.data_ptr(), wf.data_ptr(), fdt, bias.data_ptr() if bias is not None else None,
+        act, float(act_arg), y.data_ptr(),
+        _lib.DT_BF16 if y.dtype == torch.bfloat16 else _lib.DT_F32,
+        ws.data_ptr(), ws.numel(), stream_handle()))
+
+
+def _forward(x, fp: FactorPair, bias, activation, act_arg, mma, out_dtype):
+    xt, host = as_device_matrix(x, name="input")
+    p = fp.plan
+    if xt.shape[1] != p.q:
+        raise DimensionError(
+            f"cannot multiply {xt.shape[0]}x{xt.shape[1]} by compressed {p.q}x{p.r_dim}")
+    code = resolve_mma(mma, xt, p)
+    y = torch.empty((xt.shape[0], p.r_dim), dtype=out_dtype, device=device())
+    forward_into(xt, fp, bias, _act_code(activation), act_arg, y, code)
+    return (y.float().cpu().numpy() if host else y), xt.shape[0]
+
+
+def fused_matmul(x, fp: FactorPair, *, reuse: ReuseTable | None = None, threads: int | None = None,
+                 mma: str | None = None, out_dtype=torch.float32):
+    """kernel.py:222-293: Y = X @ decompress(fp) computed from the factors.
+
+    Returns (y, OpCount). OpCount / ReuseTable report the run-memoized
+    algorithm's counts exactly as the reference does (kernel.py:277-283).
+    """
+    _resolve_threads(threads)
+    y, batch = _forward(x, fp, None, "identity", 0.0, mma, out_dtype)
+    if reuse is not None:
+        pred = predict_reuse(fp.plan)
+        reuse.misses += pred.distinct_runs * batch
+        reuse.hits += pred.total_runs * batch - pred.distinct_runs * batch
+    return y, op_count(fp.plan, batch)
+
+
+def layer_forward(x, fp: FactorPair, bias, activation: str = "identity", *,
+                  threads: int | None = None, mma: str | None = None, act_arg: float = 20.0,
+                  out_dtype=torch.float32):
+    """kernel.py:296-320: activation(X @ W + bias), fused at every rank."""
+    _resolve_threads(threads)
+    _act_code(activation)
+    b = as_device_vector(bias, fp.plan.r_dim)
+    y, _ = _forward(x, fp, b, activation, act_arg, mma, out_dtype)
+    return y

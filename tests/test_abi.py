@@ -1,0 +1,132 @@
+"""CPU tests of the C-ABI library: it loads, exports every declared symbol, and its
+host-side geometry (no GPU needed) agrees with the pinned oracle and the
+reference's known answers."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import deepthin_oracle as O
+
+import paper_1802_06944_b200 as D
+from paper_1802_06944_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if fn.endswith(".h"):
+            text = open(os.path.join(ROOT, "include", fn)).read()
+            names |= set(re.findall(r"\b(dt_[a-z0-9_]+)\s*\(", text))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    declared = declared_functions()
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in lib.dt_version()
+
+
+def test_library_is_sm100a_only():
+    # the fatbin carries sm_100a SASS, no PTX for other arches
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out
+
+
+def test_plan_validation_matches_reference_rules():
+    with pytest.raises(D.ArgumentError):
+        D.LayerPlan(q=4, r_dim=4, rank=1, m=3, n=5)
+    with pytest.raises(D.ArgumentError):
+        D.LayerPlan(q=4, r_dim=0, rank=1, m=3, n=5)
+    p = D.LayerPlan(q=440, r_dim=2048, rank=24, m=2816, n=320)
+    assert p.achieved_ratio == pytest.approx(24 * (2816 + 320) / (440 * 2048))
+    assert not p.reuse_path and p.info().period == 8 and p.info().tail == 0
+
+
+def test_index_laws_match_golden(golden):
+    for row in golden["index_laws"]:
+        q, r_dim, n, m, pc, d, t = (int(v) for v in row[:7])
+        p = D.LayerPlan(q=q, r_dim=r_dim, rank=1, m=m, n=n)
+        assert D.phase_count(p) == pc
+        assert tuple(D.predict_reuse(p)) == (d, t)
+        assert [D.phase(int(c), p) for c in row[11:15]] == row[7:11].tolist()
+        info = p.info()
+        assert info.reuse == (q % n == 0)
+        assert info.tail == m * n - q * r_dim
+
+
+def test_relayout_and_errors(golden):
+    p = D.LayerPlan(q=7, r_dim=5, rank=1, m=7, n=5)
+    got = np.array([D.relayout_index(k, p) for k in range(35)])
+    assert np.array_equal(got, golden["relayout_7x5"])
+    with pytest.raises(D.ArgumentError):
+        D.relayout_index(35, p)
+    with pytest.raises(D.ArgumentError):
+        D.phase(5, p)
+
+
+def test_op_counts_match_oracle_and_reference(golden):
+    for i in range(16):
+        q, r_dim, rank, m, n = (int(v) for v in golden[f"fm{i}_plan"])
+        p = D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+        batch = golden[f"fm{i}_x"].shape[0]
+        hits, misses, mul, add = (int(v) for v in golden[f"fm{i}_counts"])
+        ops = D.op_count(p, batch)
+        assert (ops.multiplies, ops.adds) == (mul, add)
+        pred = D.predict_reuse(p, batch)
+        assert pred.distinct_runs * batch == misses
+        assert pred.total_runs * batch - misses == hits
+
+
+def test_baseline_config_geometry():
+    # c1/c3/c5 single phase (reuse); c2 period 8; c4-fc1 period 160, tail 128
+    c1 = D.baseline_plan(1024, 1024, 16, 256, 4096)
+    c2 = D.baseline_plan(440, 2048, 24, 320, 2816)
+    c4 = D.baseline_plan(494, 2048, 3, 320)
+    c5 = D.baseline_plan(8192, 8192, 64, 1024, 65536)
+    assert c1.reuse_path and c5.reuse_path and not c2.reuse_path and not c4.reuse_path
+    assert c4.m == 3162 and c4.info().period == 160 and c4.info().tail == 128
+    assert c2.info().phase_count == 8
+    assert tuple(D.predict_reuse(c2)) == (18, 4608)
+
+
+def test_status_mapping():
+    with pytest.raises(D.DimensionError):
+        _lib.check(_lib.DT_E_DIM)
+    with pytest.raises(D.UnsupportedConfigurationError):
+        _lib.check(_lib.DT_E_UNSUPPORTED)
+    with pytest.raises(D.CudaError):
+        _lib.check(_lib.DT_E_CUDA)
+
+
+def test_forward_rejects_bad_arguments_before_touching_the_gpu():
+    lib = _lib.lib()
+    ps = _lib.Plan(440, 2048, 24, 2816, 320)
+    rc = lib.dt_forward(C.byref(ps), 4, 7, None, 0, None, None, 0, None, 0, 0.0, None, 0, None, 0,
+                        None)
+    assert rc == _lib.DT_E_ARG
+    rc = lib.dt_forward(C.byref(ps), 4, 0, None, 0, None, None, 0, None, 99, 0.0, None, 0, None, 0,
+                        None)
+    assert rc == _lib.DT_E_ARG
+    bad = _lib.Plan(4, 4, 1, 3, 5)
+    assert lib.dt_forward(C.byref(bad), 1, 0, None, 0, None, None, 0, None, 0, 0.0, None, 0, None,
+                          0, None) == _lib.DT_E_ARG
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = D.LayerPlan(q=8, r_dim=8, rank=1, m=8, n=8)
+    with pytest.raises(D.CudaError):
+        D.FactorPair(np.ones((8, 1)), np.ones((1, 8)), p)

@@ -1,0 +1,106 @@
+"""GPU parity of the backward path (dt_backward), the MSE gradient and the SGD step."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import deepthin_oracle as O
+
+import paper_1802_06944_b200 as D
+
+pytestmark = pytest.mark.gpu
+
+ACTS = ("identity", "relu", "sigmoid", "tanh")
+F32_TOL = 1e-5
+
+
+def plan_of(arr):
+    q, r_dim, rank, m, n = (int(v) for v in arr)
+    return O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n), D.LayerPlan(q=q, r_dim=r_dim, rank=rank,
+                                                                       m=m, n=n)
+
+
+def test_backward_matches_reference_golden(golden):
+    for i in range(12):
+        _, p = plan_of(golden[f"lb{i}_plan"])
+        act = ACTS[int(golden[f"lb{i}_act"][0])]
+        fp = D.FactorPair(golden[f"lb{i}_xf"], golden[f"lb{i}_wf"], p)
+        gr = D.layer_backward(golden[f"lb{i}_x"], fp, golden[f"lb{i}_bias"], act,
+                              golden[f"lb{i}_up"])
+        for mine, key in ((gr.d_xf, "dxf"), (gr.d_wf, "dwf"), (gr.d_input, "dx"), (gr.d_bias, "db")):
+            assert O.rel_error(mine, golden[f"lb{i}_{key}"]) <= F32_TOL, (i, key)
+
+
+@pytest.mark.parametrize("key", ["t5s", "t2"])
+def test_training_geometry_gradients(golden, key):
+    op, p = plan_of(golden[f"{key}_plan"])
+    batch = golden[f"{key}_dx"].shape[0]
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, batch, seed=1).items()}
+    fp = D.FactorPair(d["xf"], d["wf"], p)
+    y = D.layer_forward(d["x"], fp, d["bias"], mma="ffma")
+    loss, dy = D.loss_and_grad("mse", y, d["target"])
+    assert loss == pytest.approx(float(golden[f"{key}_loss"][0]), rel=1e-5)
+    gr = D.layer_backward(d["x"], fp, d["bias"], "identity", dy)
+    for mine, k in ((gr.d_xf, "dxf"), (gr.d_wf, "dwf"), (gr.d_input, "dx"), (gr.d_bias, "db")):
+        assert O.rel_error(mine, golden[f"{key}_{k}"]) <= F32_TOL, k
+
+
+def test_discarded_tail_gets_zero_gradient():
+    # pkg/tests/test_grad.py:63-79 — m*n - q*r_dim = 2 tail elements
+    op = O.Plan(q=5, r_dim=2, rank=1, m=3, n=4)
+    xf, wf = O.init_factors(op, 0.7, O.make_rng(5))
+    x = O.make_rng(6).standard_normal((3, 5))
+    up = O.make_rng(7).standard_normal((3, 2))
+    fp = D.FactorPair(xf, wf, D.LayerPlan(q=5, r_dim=2, rank=1, m=3, n=4))
+    gr = D.layer_backward(x, fp, np.zeros(2), "identity", up)
+    d_aux = np.concatenate([(x.T @ up).T.ravel(), np.zeros(2)]).reshape(3, 4)
+    assert np.allclose(gr.d_xf, d_aux @ wf.T, atol=1e-5)
+    assert np.allclose(gr.d_wf, xf.T @ d_aux, atol=1e-5)
+
+
+def test_zero_upstream_and_shape_errors():
+    op = O.Plan(q=6, r_dim=5, rank=2, m=8, n=4)
+    xf, wf = O.init_factors(op, 0.7, O.make_rng(0))
+    fp = D.FactorPair(xf, wf, D.LayerPlan(q=6, r_dim=5, rank=2, m=8, n=4))
+    x = O.make_rng(1).standard_normal((3, 6))
+    gr = D.layer_backward(x, fp, np.zeros(5), "tanh", np.zeros((3, 5)))
+    for g in (gr.d_xf, gr.d_wf, gr.d_input, gr.d_bias):
+        assert not np.any(g)
+    with pytest.raises(D.DimensionError):
+        D.layer_backward(np.zeros((2, 6)), fp, np.zeros(5), "relu", np.zeros((3, 5)))
+
+
+def test_backward_deterministic():
+    op = O.Plan(q=440, r_dim=2048, rank=24, m=2816, n=320)
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, 300, seed=4).items()}
+    fp = D.FactorPair(d["xf"], d["wf"], D.LayerPlan(q=440, r_dim=2048, rank=24, m=2816, n=320))
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda")
+    up = torch.tensor(d["target"], dtype=torch.float32, device="cuda")
+    g1 = D.layer_backward(x, fp, d["bias"], "sigmoid", up)
+    g2 = D.layer_backward(x, fp, d["bias"], "sigmoid", up)
+    for a, b in ((g1.d_xf, g2.d_xf), (g1.d_wf, g2.d_wf), (g1.d_input, g2.d_input), (g1.d_bias, g2.d_bias)):
+        assert torch.equal(a, b)
+
+
+def test_train_step_update_matches_oracle():
+    # config-5-shaped reuse layer scaled down; one SGD step at lr 1e-3 (train.py:107-111)
+    op = O.Plan(q=512, r_dim=512, rank=8, m=4096, n=64)
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, 64, seed=2).items()}
+    layer = D.DeepThinLayer(D.LayerPlan(q=512, r_dim=512, rank=8, m=4096, n=64), d["xf"], d["wf"],
+                            d["bias"], mma="ffma")
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda")
+    t = torch.tensor(d["target"], dtype=torch.float32, device="cuda")
+    xf0, wf0, b0 = layer.fp.xf.clone(), layer.fp.wf.clone(), layer.bias.clone()
+    lsum = D.train_step(layer, x, t, lr=1e-3)
+    y = O.layer_forward(d["x"], d["xf"], d["wf"], op, d["bias"])
+    loss, dy = O.loss_and_grad("mse", y, d["target"])
+    gr = O.layer_backward(d["x"], d["xf"], d["wf"], op, d["bias"], "identity", dy)
+    assert float(lsum.item()) / y.size == pytest.approx(loss, rel=1e-5)
+    # check the gradients that drove the step (the post-step factors would pass trivially,
+    # SURVEY.md §7 hard part 6), then that the step applied exactly p - lr * g in fp32
+    assert O.rel_error(layer.d_xf, gr.d_xf) <= F32_TOL
+    assert O.rel_error(layer.d_wf, gr.d_wf) <= F32_TOL
+    assert O.rel_error(layer.d_bias, gr.d_bias) <= F32_TOL
+    for p0, p1, g in ((xf0, layer.fp.xf, layer.d_xf), (wf0, layer.fp.wf, layer.d_wf),
+                      (b0, layer.bias, layer.d_bias)):
+        assert torch.allclose(p1, p0 - 1e-3 * g, rtol=1e-6, atol=1e-12)

@@ -1,0 +1,187 @@
+"""GPU parity of the forward path (dt_forward) against the pinned oracle and golden vectors.
+
+Tolerances (BASELINE.json north_star), in the reference's metric rel_error =
+max|a-e| / max|e| (core.py:91-95):
+  * FFMA fp32 path            rel_error <= 1e-5
+  * bf16 tcgen05 path (fp32 accumulate) rel_error <= 2e-3, oracle fed the SAME
+    bf16-rounded inputs.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import deepthin_oracle as O
+
+import paper_1802_06944_b200 as D
+
+pytestmark = pytest.mark.gpu
+
+ACTS = ("identity", "relu", "sigmoid", "tanh")
+F32_TOL = 1e-5
+BF16_TOL = 2e-3
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def make_case(q, r_dim, rank, n, m, batch, seed=0, rnd=f32, bias_sd=0.01):
+    plan = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    d = {k: rnd(v) for k, v in O.baseline_inputs(plan, batch, seed=seed, bias_sd=bias_sd).items()}
+    fp = D.FactorPair(d["xf"], d["wf"], D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+    return plan, d, fp
+
+
+def gpu_x(a, dtype):
+    return torch.tensor(a, dtype=torch.float32, device="cuda").to(dtype)
+
+
+# ---- FFMA fp32 path -----------------------------------------------------------------
+
+def test_ffma_matches_reference_golden_small_plans(golden):
+    for i in range(16):
+        q, r_dim, rank, m, n = (int(v) for v in golden[f"lf{i}_plan"])
+        act = ACTS[int(golden[f"lf{i}_act"][0])]
+        fp = D.FactorPair(golden[f"lf{i}_xf"], golden[f"lf{i}_wf"],
+                          D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+        y = D.layer_forward(golden[f"lf{i}_x"], fp, golden[f"lf{i}_bias"], act, mma="ffma")
+        assert isinstance(y, np.ndarray)
+        assert O.rel_error(y, golden[f"lf{i}_y"]) <= F32_TOL, (i, q, r_dim, rank, n)
+
+
+def test_ffma_fused_matmul_golden_rank1(golden):
+    for i in range(16):
+        q, r_dim, rank, m, n = (int(v) for v in golden[f"fm{i}_plan"])
+        fp = D.FactorPair(golden[f"fm{i}_xf"], golden[f"fm{i}_wf"],
+                          D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+        table = D.ReuseTable()
+        y, ops = D.fused_matmul(golden[f"fm{i}_x"], fp, reuse=table)
+        assert O.rel_error(y, golden[f"fm{i}_y"]) <= F32_TOL
+        hits, misses, mul, add = (int(v) for v in golden[f"fm{i}_counts"])
+        assert (table.hits, table.misses, ops.multiplies, ops.adds) == (hits, misses, mul, add)
+
+
+@pytest.mark.parametrize("key", ["c1", "c2", "c4fc1", "c3l1"])
+def test_baseline_geometries_vs_reference_golden(golden, key):
+    q, r_dim, rank, m, n = (int(v) for v in golden[f"{key}_plan"])
+    rnd = f32 if key == "c1" else O.round_bf16
+    plan = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    d = {k: rnd(v) for k, v in O.baseline_inputs(plan, golden[f"{key}_x"].shape[0], 0).items()}
+    fp = D.FactorPair(d["xf"], d["wf"], D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+    y = D.layer_forward(d["x"], fp, d["bias"], "identity", mma="ffma")
+    assert O.rel_error(y, golden[f"{key}_y"]) <= F32_TOL
+
+
+def test_ffma_config1_full_batch():
+    # BASELINE config 1: q=r_dim=1024, m=4096, n=256, rank 16, batch 64 (reuse path), fp32
+    plan, d, fp = make_case(1024, 1024, 16, 256, 4096, 64)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(torch.tensor(d["x"], dtype=torch.float32, device="cuda"), fp, d["bias"],
+                        mma="ffma")
+    assert y.dtype == torch.float32 and y.shape == (64, 1024)
+    assert O.rel_error(y, ref) <= F32_TOL
+
+
+@pytest.mark.parametrize("geo", [(440, 2048, 24, 320, 2816, 256), (494, 2048, 3, 320, 3162, 100),
+                                 (300, 257, 2, 41, 1881, 37)])
+def test_ffma_general_path(geo):
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=3)
+    for act in ("identity", "relu", "tanh"):
+        ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], act)
+        y = D.layer_forward(d["x"], fp, d["bias"], act, mma="ffma")
+        assert O.rel_error(y, ref) <= F32_TOL, act
+
+
+def test_ffma_bf16_input_exact_products():
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 64, rnd=O.round_bf16)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="ffma")
+    assert O.rel_error(y, ref) <= F32_TOL
+
+
+# ---- bf16 tcgen05 general path ------------------------------------------------------------
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_tc_general_config2_full_batch(seed):
+    # BASELINE config 2: in 440 -> out 2048, m_f 2816, n_f 320, rank 24, batch 4096
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 4096, seed=seed, rnd=O.round_bf16)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
+    err = O.rel_error(y, ref)
+    assert err <= BF16_TOL, err
+
+
+@pytest.mark.parametrize("geo", [
+    (494, 2048, 3, 320, 3162, 300),    # config 4 fc1: period 160, tail 128, q % 8 != 0
+    (440, 2048, 3, 320, 2816, 1000),   # config 3 layer 0 (rank 3)
+    (300, 257, 2, 41, 1881, 129),      # odd everything, ragged r_dim and batch
+    (200, 100, 5, 7, 2858, 1),         # n odd (scalar scatter path), batch 1
+    (64, 600, 40, 48, 800, 260),       # rank 40 -> padded K of 48
+])
+def test_tc_general_geometries(geo):
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=5, rnd=O.round_bf16)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
+    assert O.rel_error(y, ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("act", ["relu", "sigmoid", "tanh", "clipped_relu", "softmax"])
+def test_tc_general_fused_activations(act):
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 384, seed=7, rnd=O.round_bf16, bias_sd=0.5)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    ref = O.apply_activation(act, ref, 2.0)
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], act, mma="bf16", act_arg=2.0)
+    assert O.rel_error(y, ref) <= BF16_TOL
+
+
+def test_tc_general_fp32_input_and_bf16_output():
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 512, seed=2, rnd=O.round_bf16)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(gpu_x(d["x"], torch.float32), fp, d["bias"], mma="bf16")
+    assert O.rel_error(y, ref) <= BF16_TOL
+    yb = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16",
+                         out_dtype=torch.bfloat16)
+    assert yb.dtype == torch.bfloat16
+    # bf16 output adds <= 2^-8 relative rounding on top of the operand rounding
+    assert O.rel_error(yb.float(), ref) <= BF16_TOL + 2 ** -8
+
+
+def test_tc_general_deterministic_and_shard_invariant():
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 4096, seed=9, rnd=O.round_bf16)
+    x = gpu_x(d["x"], torch.bfloat16)
+    b = d["bias"]
+    y1 = D.layer_forward(x, fp, b, mma="bf16")
+    y2 = D.layer_forward(x, fp, b, mma="bf16")
+    assert torch.equal(y1, y2)
+    # batch sharding (multi-GPU DP) must not change any row's bits
+    for lo, hi in ((0, 1024), (1024, 2048), (2048, 4096), (100, 357)):
+        ys = D.layer_forward(x[lo:hi].contiguous(), fp, b, mma="bf16")
+        assert torch.equal(ys, y1[lo:hi]), (lo, hi)
+
+
+def test_empty_batch_and_errors():
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 4, rnd=O.round_bf16)
+    for mma in ("ffma", "bf16"):
+        y = D.layer_forward(torch.zeros((0, 440), device="cuda", dtype=torch.bfloat16), fp, d["bias"],
+                            mma=mma)
+        assert y.shape == (0, 2048)
+    with pytest.raises(D.DimensionError):
+        D.layer_forward(torch.zeros((2, 441), device="cuda"), fp, d["bias"])
+    with pytest.raises(D.DimensionError):
+        D.layer_forward(torch.zeros((2, 440), device="cuda"), fp, np.zeros(7))
+    with pytest.raises(D.ArgumentError):
+        D.layer_forward(torch.zeros((2, 440), device="cuda"), fp, d["bias"], "gelu")
+    with pytest.raises(D.ArgumentError):
+        D.layer_forward(np.full((2, 440), np.nan), fp, d["bias"])
+
+
+def test_decompress_matches_oracle(golden):
+    for i in range(24):
+        q, r_dim, rank, m, n = (int(v) for v in golden[f"dec{i}_plan"])
+        fp = D.FactorPair(golden[f"dec{i}_xf"], golden[f"dec{i}_wf"],
+                          D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+        w = D.decompress(fp)
+        assert O.rel_error(w, golden[f"dec{i}_w"]) <= F32_TOL
