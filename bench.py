@@ -205,8 +205,8 @@ def run_ours(args, cfg, key):
     ws = torch.empty(max(256, lib.dt_forward_workspace_bytes(C.byref(ps), batch, code)),
                      dtype=torch.uint8, device="cuda")
     if mma == "bf16":
-        xf_d, wf_d = fp.bf16()
-        fdt = _lib.DT_BF16
+        xf_d, wf_d = fp.packed(), None     # per-pair derived operand layout, built once
+        fdt = _lib.DT_FACTORS_PACKED
     else:
         xf_d, wf_d, fdt = fp.xf, fp.wf, _lib.DT_F32
     stream = torch.cuda.current_stream()
@@ -215,7 +215,8 @@ def run_ours(args, cfg, key):
     def step():
         _lib.check(lib.dt_forward(C.byref(ps), batch, code, x.data_ptr(),
                                   _lib.DT_BF16 if xdt == torch.bfloat16 else _lib.DT_F32,
-                                  xf_d.data_ptr(), wf_d.data_ptr(), fdt, bias.data_ptr(), 0, 0.0,
+                                  xf_d.data_ptr(), wf_d.data_ptr() if wf_d is not None else None,
+                                  fdt, bias.data_ptr(), 0, 0.0,
                                   y.data_ptr(), _lib.DT_F32, ws.data_ptr(), ws.numel(), sh))
 
     l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
@@ -282,9 +283,9 @@ def run_ours(args, cfg, key):
 
     # e2e through the host-buffer C ABI (pinned host x in, host y out, every step)
     sess = C.c_void_p()
-    _lib.check(lib.dt_session_create(C.byref(ps), code, d["xf"].astype(np.float32).ctypes.data,
-                                     d["wf"].astype(np.float32).ctypes.data,
-                                     d["bias"].astype(np.float32).ctypes.data, C.byref(sess)))
+    host_f = [np.ascontiguousarray(d[k], dtype=np.float32) for k in ("xf", "wf", "bias")]
+    _lib.check(lib.dt_session_create(C.byref(ps), code, host_f[0].ctypes.data,
+                                     host_f[1].ctypes.data, host_f[2].ctypes.data, C.byref(sess)))
     hx = torch.tensor(d["x"], dtype=torch.float32).pin_memory()
     hy = torch.empty((batch, r_dim), dtype=torch.float32).pin_memory()
     h2d, d2h = C.c_int64(), C.c_int64()

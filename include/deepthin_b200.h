@@ -56,7 +56,9 @@ enum dt_status {
   DT_E_CUDA = 4         /* CUDA launch / runtime failure   */
 };
 
-enum dt_dtype { DT_F32 = 0, DT_BF16 = 1 };
+/* DT_FACTORS_PACKED is valid only as dt_forward's f_dtype: xf points at the buffer
+ * dt_pack_factors filled (wf is ignored). */
+enum dt_dtype { DT_F32 = 0, DT_BF16 = 1, DT_FACTORS_PACKED = 2 };
 
 /* Arithmetic of the contraction.
  *  DT_MMA_FFMA: fp32 CUDA-core FFMA, fp32 operands (parity rtol 1e-5).
@@ -101,6 +103,15 @@ int dt_decompress(const dt_plan *plan, const float *xf, const float *wf, float *
 
 /* Round fp32 → bf16 (RNE); used to make the bf16 operand copies of factors. */
 int dt_cast_bf16(int64_t count, const float *src, uint16_t *dst, dt_stream stream);
+
+/* Derived per-pair operand layout for the bf16 tensor-core path (the analogue of the
+ * reference's per-pair cached combine weights, kernel.py:157-164): bf16 factors
+ * re-laid into the on-chip regeneration operands' core-matrix order, zero padded.
+ * Build once per factor update; pass to dt_forward with f_dtype = DT_FACTORS_PACKED.
+ * Returns 0 bytes for plans the tensor-core path does not support. */
+size_t dt_packed_factors_bytes(const dt_plan *plan, int mma);
+int dt_pack_factors(const dt_plan *plan, int mma, const uint16_t *xf_bf16,
+                    const uint16_t *wf_bf16, void *packed, dt_stream stream);
 
 size_t dt_forward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma);
 

@@ -96,10 +96,17 @@ def matmul(a, b):
     return np.matmul(am.astype(dt, copy=False), bm.astype(dt, copy=False))
 
 
+def _host(a):
+    """Accept device tensors from the code under test (copied to host, widened)."""
+    if hasattr(a, "detach"):
+        return a.detach().float().cpu().numpy()
+    return np.asarray(a)
+
+
 def max_abs_diff(a, b):
     """core.py:80-88."""
-    a = np.asarray(a)
-    b = np.asarray(b)
+    a = _host(a)
+    b = _host(b)
     if a.shape != b.shape:
         return float("inf")
     if a.size == 0:

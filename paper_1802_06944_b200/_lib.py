@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
 
 DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA = range(5)
-DT_F32, DT_BF16 = 0, 1
+DT_F32, DT_BF16, DT_FACTORS_PACKED = 0, 1, 2
 DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
 ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
 
@@ -23,6 +23,7 @@ ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 
 EXPORTS = (
     "dt_version", "dt_last_error", "dt_launch_counter", "dt_plan_validate", "dt_plan_query", "dt_phase",
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
+    "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
     "dt_mse_grad", "dt_mse_workspace_bytes", "dt_sgd_step", "dt_session_create",
     "dt_session_forward", "dt_session_destroy",
@@ -57,6 +58,8 @@ def _declare(lib):
         "dt_op_count": ([P, I64, C.POINTER(I64), C.POINTER(I64)], i),
         "dt_decompress": ([P, VP, VP, VP, VP], i),
         "dt_cast_bf16": ([I64, VP, VP, VP], i),
+        "dt_packed_factors_bytes": ([P, i], SZ),
+        "dt_pack_factors": ([P, i, VP, VP, VP, VP], i),
         "dt_forward_workspace_bytes": ([P, I64, i], SZ),
         "dt_forward": ([P, I64, i, VP, i, VP, VP, i, VP, i, F, VP, i, VP, SZ, VP], i),
         "dt_backward_workspace_bytes": ([P, I64, i], SZ),

@@ -182,6 +182,27 @@ int dt_cast_bf16(int64_t count, const float *src, uint16_t *dst, dt_stream strea
   return launch_cast_bf16(count, src, dst, (cudaStream_t)stream);
 }
 
+size_t dt_packed_factors_bytes(const dt_plan *plan, int mma) {
+  Geo g;
+  if (make_geo(plan, &g) || mma != DT_MMA_BF16 || g.reuse) return 0;
+  return tc_general_packed_bytes(g);
+}
+
+int dt_pack_factors(const dt_plan *plan, int mma, const uint16_t *xf_bf16,
+                    const uint16_t *wf_bf16, void *packed, dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (mma != DT_MMA_BF16 || g.reuse) {
+    set_error("packed factors exist only for the bf16 tensor-core general path");
+    return DT_E_UNSUPPORTED;
+  }
+  if (!xf_bf16 || !wf_bf16 || !packed) {
+    set_error("NULL operand pointer");
+    return DT_E_ARG;
+  }
+  return tc_general_pack(g, xf_bf16, wf_bf16, packed, (cudaStream_t)stream);
+}
+
 size_t dt_forward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) {
   Geo g;
   if (make_geo(plan, &g) || batch < 0) return 0;
@@ -201,9 +222,10 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
   }
   if (int rc = check_dtype(x_dtype, "x")) return rc;
   if (int rc = check_dtype(y_dtype, "y")) return rc;
-  if (int rc = check_dtype(f_dtype, "factors")) return rc;
+  if (f_dtype != DT_FACTORS_PACKED)
+    if (int rc = check_dtype(f_dtype, "factors")) return rc;
   if (int rc = check_act(act)) return rc;
-  if (batch > 0 && (!x || !xf || !wf || !y)) {
+  if (batch > 0 && (!x || !xf || (!wf && f_dtype != DT_FACTORS_PACKED) || !y)) {
     set_error("NULL operand pointer");
     return DT_E_ARG;
   }
@@ -218,17 +240,19 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
                         act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
   }
   if (mma == DT_MMA_BF16) {
-    if (f_dtype != DT_BF16) {
-      set_error("the bf16 tensor-core path takes bf16 factor copies (dt_cast_bf16)");
+    if (f_dtype != DT_BF16 && f_dtype != DT_FACTORS_PACKED) {
+      set_error("the bf16 tensor-core path takes bf16 factor copies (dt_cast_bf16) or the "
+                "dt_pack_factors buffer");
       return DT_E_ARG;
     }
     if (g.reuse) {
       set_error("bf16 tensor-core reuse path is not built yet");
       return DT_E_UNSUPPORTED;
     }
-    return tc_general_forward(g, batch, x, x_dtype, (const uint16_t *)xf, (const uint16_t *)wf,
-                              bias, act, act_arg, y, y_dtype, (char *)workspace, workspace_bytes,
-                              st);
+    const bool pk = f_dtype == DT_FACTORS_PACKED;
+    return tc_general_forward(g, batch, x, x_dtype, pk ? nullptr : (const uint16_t *)xf,
+                              pk ? nullptr : (const uint16_t *)wf, pk ? xf : nullptr, bias, act,
+                              act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
   }
   set_error("unknown mma kind " + std::to_string(mma));
   return DT_E_ARG;
@@ -305,6 +329,7 @@ struct dt_session {
   int mma;
   float *xf = nullptr, *wf = nullptr, *bias = nullptr;
   uint16_t *xf16 = nullptr, *wf16 = nullptr;
+  void *packed = nullptr;  // dt_pack_factors buffer (bf16 general path)
   float *x = nullptr, *y = nullptr;
   char *ws = nullptr;
   size_t ws_bytes = 0;
@@ -355,6 +380,11 @@ int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const 
   }
   int rc = launch_cast_bf16((int64_t)nx, s->xf, s->xf16, s->stream);
   if (!rc) rc = launch_cast_bf16((int64_t)nw, s->wf, s->wf16, s->stream);
+  const size_t pkb = dt_packed_factors_bytes(plan, mma);
+  if (!rc && pkb) {
+    if (cudaMalloc(&s->packed, pkb) != cudaSuccess) rc = DT_E_CUDA;
+    if (!rc) rc = dt_pack_factors(plan, mma, s->xf16, s->wf16, s->packed, (dt_stream)s->stream);
+  }
   if (!rc && cudaStreamSynchronize(s->stream) != cudaSuccess) rc = DT_E_CUDA;
   if (rc) {
     dt_session_destroy(s);
@@ -392,9 +422,15 @@ int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int ac
   const size_t xb = (size_t)batch * g.q * 4, yb = (size_t)batch * g.r_dim * 4;
   DT_CUDA_CHECK(cudaMemcpyAsync(s->x, x_host, xb, cudaMemcpyHostToDevice, s->stream));
   const bool tc = s->mma == DT_MMA_BF16;
-  int rc = dt_forward(&s->plan, batch, s->mma, s->x, DT_F32, tc ? (const void *)s->xf16 : s->xf,
-                      tc ? (const void *)s->wf16 : s->wf, tc ? DT_BF16 : DT_F32, s->bias, act,
-                      act_arg, s->y, DT_F32, s->ws, s->ws_bytes, (dt_stream)s->stream);
+  const void *fx = s->xf, *fw = s->wf;
+  int fdt = DT_F32;
+  if (tc && s->packed) {
+    fx = s->packed; fw = nullptr; fdt = DT_FACTORS_PACKED;
+  } else if (tc) {
+    fx = s->xf16; fw = s->wf16; fdt = DT_BF16;
+  }
+  int rc = dt_forward(&s->plan, batch, s->mma, s->x, DT_F32, fx, fw, fdt, s->bias, act, act_arg,
+                      s->y, DT_F32, s->ws, s->ws_bytes, (dt_stream)s->stream);
   if (rc) return rc;
   DT_CUDA_CHECK(cudaMemcpyAsync(y_host, s->y, yb, cudaMemcpyDeviceToHost, s->stream));
   DT_CUDA_CHECK(cudaStreamSynchronize(s->stream));
@@ -411,6 +447,7 @@ void dt_session_destroy(dt_session *s) {
   cudaFree(s->bias);
   cudaFree(s->xf16);
   cudaFree(s->wf16);
+  cudaFree(s->packed);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }

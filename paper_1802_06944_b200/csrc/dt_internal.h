@@ -42,11 +42,15 @@ size_t mse_ws(int64_t rows, int64_t cols);
 int launch_sgd(int64_t count, float *p, const float *g, float lr, cudaStream_t st);
 
 // ---- tcgen05 tensor-core path: k_tc_general.cu ---------------------------------
+// `packed` (nullable): regeneration operands from tc_general_pack; else packed into ws.
 int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
-                       const uint16_t *xf_bf16, const uint16_t *wf_bf16, const float *bias,
-                       int act, float act_arg, void *y, int y_dtype, char *ws, size_t ws_bytes,
-                       cudaStream_t st);
+                       const uint16_t *xf_bf16, const uint16_t *wf_bf16, const void *packed,
+                       const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
+                       size_t ws_bytes, cudaStream_t st);
 size_t tc_general_ws(const Geo &g, int64_t batch);
+size_t tc_general_packed_bytes(const Geo &g);
+int tc_general_pack(const Geo &g, const uint16_t *xf_bf16, const uint16_t *wf_bf16, void *packed,
+                    cudaStream_t st);
 
 // Every kernel launch goes through check_launch, which also counts it (dt_launch_counter).
 int check_launch(const char *what);

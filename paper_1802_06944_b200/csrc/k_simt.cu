@@ -182,7 +182,7 @@ __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const float *par
 
 // Split count: a pure function of the shape (determinism), aimed at >= ~2 waves.
 int choose_splits(int64_t M, int64_t N, int64_t K) {
-  int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int64_t tiles = std::max<int64_t>(1, ((M + BM - 1) / BM) * ((N + BN - 1) / BN));
   int64_t want = (2 * 148 + tiles - 1) / tiles;
   int64_t maxs = std::max<int64_t>(1, K / 256);
   return (int)std::max<int64_t>(1, std::min<int64_t>({want, maxs, 64}));

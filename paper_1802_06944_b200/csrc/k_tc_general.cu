@@ -9,11 +9,12 @@
 //    items, column-block-major, so a CTA regenerates its W block once and reuses
 //    it (resident in shared memory) for every batch tile it owns.
 //  * Regeneration runs on the tensor cores: the aux rows a_lo..a_hi covering
-//    the block's flat range [j0*q, (j0+128)*q) are one small MMA
+//    the block's flat range [j0*q, (j0+128)*q) are small MMAs
 //    I_rows(128 x n) = xf_rows(128 x rank) @ wf(rank x n) into TMEM; the
-//    epilogue warps read it back (tcgen05.ld), round to bf16 and scatter every
+//    epilogue warps read them back (tcgen05.ld), round to bf16 and scatter every
 //    element f -> (jj, i) = divmod(f - j0*q, q) into the 128B-swizzled K-major
-//    operand layout. The discarded tail (f >= q*r_dim) is never produced.
+//    operand layout (16-byte stores when q and n are multiples of 8). The
+//    discarded tail (f >= q*r_dim) is never produced.
 //  * Main loop: D[j, b] (TMEM, fp32) += W_blk[j, :] . x[b, :] with
 //    tcgen05.mma.cta_group::1.kind::f16, M = 128 output columns, N = 128 batch
 //    rows, A = the resident W block, B = TMA-staged x tiles (S-stage mbarrier
@@ -21,7 +22,9 @@
 //    overlaps the MMAs of tile t+1.
 //  * Epilogue: lanes are output columns, TMEM columns are batch rows, so each
 //    warp store instruction writes 32 consecutive outputs of one batch row
-//    (coalesced), fused with bias + activation.
+//    (coalesced), fused with bias + activation. Output dtype and activation are
+//    template parameters: the epilogue stays a few hundred instructions (the
+//    runtime-switch version thrashed the instruction cache).
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
 // warps 2-5 regeneration + epilogue.
@@ -31,7 +34,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "dt_internal.h"
 #include "sm100_ptx.cuh"
@@ -50,157 +56,252 @@ constexpr uint32_t kXStage = BNB * 128;   // bytes per x stage (128 rows x 64 bf
 constexpr uint32_t kWKBlk = BMW * 128;    // bytes per W k-block
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSmemBudget = 227 * 1024;
+constexpr int kTraceSlots = 48;
 
 struct TcParams {
-  int64_t q, r_dim, rank, m, n, batch, ldy;
+  int64_t batch;
+  int q, r_dim, rank, m, n, ldy;
   int KB, S, RK, Nc, n_chunks, n_cb, n_bt, items, per_cta;
-  const __nv_bfloat16 *xf, *wf;
+  const uint8_t *xf_pk, *wf_pk;  // regeneration operands, pre-packed (dt_pack_factors)
   const float *bias;
   void *y;
-  int y_dtype, act;
   float arg;
   uint32_t off_w, off_x, off_ar, off_br, off_bar;
+  uint32_t w_sbo;  // W block 8-row-group stride (no-swizzle K-major layout)
+  unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps, else null
+  int dbg_serial;             // DEEPTHIN_REGEN_SERIAL: no regen MMA / read-back overlap
 };
 
-__device__ __forceinline__ float act_apply(int act, float z, float arg) {
-  switch (act) {
-    case DT_ACT_RELU: return z > 0.f ? z : 0.f;
-    case DT_ACT_SIGMOID: return 1.f / (1.f + __expf(-z));
-    case DT_ACT_TANH: return tanhf(z);
-    case DT_ACT_CLIPPED_RELU: return fminf(fmaxf(z, 0.f), arg);
-    default: return z;
-  }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// slots: 0 start, 1 setup done, 2..5 regen begin/end (x2), 6..13 epilogue tile done,
+// 14..21 MMA tile committed, 22 producer done, 23 end
+__device__ __forceinline__ void trace(const TcParams &p, int slot) {
+  if (p.trace && slot < kTraceSlots) p.trace[(size_t)blockIdx.x * kTraceSlots + slot] = gtimer();
 }
 
-__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
-  int64_t q = a / b;
-  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+template <int ACT>
+__device__ __forceinline__ float act_apply(float z, float arg) {
+  if constexpr (ACT == DT_ACT_RELU) return z > 0.f ? z : 0.f;
+  if constexpr (ACT == DT_ACT_SIGMOID) return 1.f / (1.f + expf(-z));
+  if constexpr (ACT == DT_ACT_TANH) return tanhf(z);
+  if constexpr (ACT == DT_ACT_CLIPPED_RELU) return fminf(fmaxf(z, 0.f), arg);
+  return z;
 }
 
-// Byte offset of W-block element (jj, i) in the K-major SWIZZLE_128B operand layout.
-__device__ __forceinline__ uint32_t w_off(int64_t jj, int64_t i) {
-  uint32_t kb = (uint32_t)(i >> 6), col = (uint32_t)(i & 63);
-  return kb * kWKBlk + (uint32_t)jj * 128u + ((((col >> 3) ^ (uint32_t)(jj & 7))) << 4) +
-         ((col & 7) << 1);
+// Byte offset of W-block element (jj, i) in the no-swizzle K-major core-matrix layout:
+// [8-row group][K core of 8][8 rows x 16 B]. The regeneration scatter writes 16-byte units
+// whose rows advance ~q/n per thread; here the bank group of a unit is jj & 7, so a warp's
+// stores spread over all banks (the 128B-swizzled layout put every lane on one chunk when
+// n = 0 mod 64, a 32-way conflict). sbo = 8-row-group stride = (K extent / 8) * 128.
+__device__ __forceinline__ uint32_t w_off(uint32_t jj, uint32_t i, uint32_t sbo) {
+  return (jj >> 3) * sbo + (i >> 3) * 128u + (jj & 7u) * 16u + (i & 7u) * 2u;
 }
 
 // No-swizzle K-major ("interleave") layout of the small regeneration operands:
 // 8-row x 16-byte core matrices, K-adjacent cores 128 B apart (LBO), 8-row groups SBO apart.
-__device__ __forceinline__ uint32_t core_off(int row, int k, uint32_t sbo) {
-  return (uint32_t)(row >> 3) * sbo + (uint32_t)(k >> 3) * 128u + (uint32_t)(row & 7) * 16u +
-         (uint32_t)(k & 7) * 2u;
+__device__ __forceinline__ uint32_t core_off(uint32_t row, uint32_t k, uint32_t sbo) {
+  return (row >> 3) * sbo + (k >> 3) * 128u + (row & 7u) * 16u + (k & 7u) * 2u;
 }
 
-// Regenerate the W block of column block cb into shared memory (128 epilogue threads).
-__device__ void regen_block(const TcParams &p, int64_t cb, uint8_t *wblk, uint8_t *ar, uint8_t *br,
-                            uint64_t *rbar, uint32_t &rphase, uint32_t tbase, int et, int wq,
-                            int lane) {
-  const int64_t q = p.q, n = p.n, rank = p.rank;
-  const int64_t j0 = cb * BMW;
-  const int64_t jrows = (int64_t)min((int64_t)BMW, p.r_dim - j0);
-  const int64_t fbeg = j0 * q, fend = (j0 + jrows) * q;
-  const int64_t a_lo = fbeg / n, a_hi = (int64_t)min(p.m - 1, (fend - 1) / n);
-  const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
-  const int L = 32 * wq + lane;  // TMEM lane (= aux row offset) this thread reads
-  const bool pairs = ((n & 1) == 0) && ((q & 1) == 0);
-  const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)p.Nc);
-  const uint32_t ar_s = smem_u32(ar), br_s = smem_u32(br);
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<uint32_t *>(&h);
+}
 
-  for (int64_t a0 = a_lo; a0 <= a_hi; a0 += 128) {
-    {  // A operand: xf rows a0 .. a0+127 (zero beyond a_hi / rank)
-      const int64_t a = a0 + et;
-      for (int k = 0; k < p.RK; k += 8) {
-        __align__(16) __nv_bfloat16 v[8];
+// Scatter one tcgen05.ld group (32 consecutive aux columns of one aux row) into the W block.
+// (jj, i) = position of the group's first element (jj may be negative: skipped).
+// MODE 2: q, n multiples of 8 (16-byte stores); 1: both even (4-byte); 0: scalar.
+template <int MODE>
+__device__ __forceinline__ void scatter32(const uint32_t (&v)[32], uint32_t w_s, uint32_t sbo,
+                                          int jj, int i, int q, int cvalid, int jrows) {
+  if constexpr (MODE == 2) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[e] = (a <= a_hi && k + e < rank) ? p.xf[a * rank + k + e] : __float2bfloat16(0.f);
-        *reinterpret_cast<uint4 *>(ar + core_off(et, k, sbo)) = *reinterpret_cast<uint4 *>(v);
-      }
+    for (int t = 0; t < 4; ++t) {
+      if (8 * t < cvalid && jj >= 0 && jj < jrows)
+        sts_v4(w_s + w_off(jj, i, sbo), pack_bf16(v[8 * t], v[8 * t + 1]),
+               pack_bf16(v[8 * t + 2], v[8 * t + 3]), pack_bf16(v[8 * t + 4], v[8 * t + 5]),
+               pack_bf16(v[8 * t + 6], v[8 * t + 7]));
+      i += 8;
+      if (i >= q) { i -= q; ++jj; }
     }
-    for (int chunk = 0; chunk < p.n_chunks; ++chunk) {
-      const int64_t c0 = (int64_t)chunk * p.Nc;
-      for (int nn = et; nn < p.Nc; nn += kEpiThreads) {  // B operand: wf[:, c0+nn]^T
-        const int64_t c = c0 + nn;
-        for (int k = 0; k < p.RK; k += 8) {
-          __align__(16) __nv_bfloat16 v[8];
+  } else if constexpr (MODE == 1) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            v[e] = (c < n && k + e < rank) ? p.wf[(k + e) * n + c] : __float2bfloat16(0.f);
-          *reinterpret_cast<uint4 *>(br + core_off(nn, k, sbo)) = *reinterpret_cast<uint4 *>(v);
-        }
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1, kEpiThreads);
-      if (et == 0) {
-        tc_fence_after();
-        for (int kk = 0; kk < p.RK / 16; ++kk) {
-          uint64_t ad = smem_desc(ar_s + kk * 256u, 128u, sbo, SL_NONE);
-          uint64_t bd = smem_desc(br_s + kk * 256u, 128u, sbo, SL_NONE);
-          mma_bf16_ss(tbase, ad, bd, idesc, kk > 0);
-        }
-        mma_commit(rbar);
-      }
-      mbar_wait(rbar, rphase);
-      rphase ^= 1;
-      tc_fence_after();
-      const int64_t a = a0 + L;
-      for (int col0 = 0; col0 < p.Nc; col0 += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)col0, v);
-        tmem_ld_wait();
-        if (a > a_hi) continue;
-        const int64_t cstart = c0 + col0;
-        const int64_t f0 = a * n + cstart - fbeg;
-        int64_t jj = floordiv(f0, q), i = f0 - jj * q;
-        if (pairs) {
+    for (int t = 0; t < 16; ++t) {
+      if (2 * t < cvalid && jj >= 0 && jj < jrows)
+        sts_u32(w_s + w_off(jj, i, sbo), pack_bf16(v[2 * t], v[2 * t + 1]));
+      i += 2;
+      if (i >= q) { i -= q; ++jj; }
+    }
+  } else {
 #pragma unroll
-          for (int t = 0; t < 32; t += 2) {
-            if (cstart + t < n && jj >= 0 && jj < jrows) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[t]), __uint_as_float(v[t + 1]));
-              *reinterpret_cast<__nv_bfloat162 *>(wblk + w_off(jj, i)) = h;
-            }
-            i += 2;
-            if (i >= q) { i -= q; ++jj; }
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            if (cstart + t < n && jj >= 0 && jj < jrows)
-              *reinterpret_cast<__nv_bfloat16 *>(wblk + w_off(jj, i)) =
-                  __float2bfloat16_rn(__uint_as_float(v[t]));
-            if (++i == q) { i = 0; ++jj; }
-          }
-        }
+    for (int t = 0; t < 32; ++t) {
+      if (t < cvalid && jj >= 0 && jj < jrows) {
+        __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(v[t]));
+        sts_u16(w_s + w_off(jj, i, sbo), *reinterpret_cast<uint16_t *>(&h));
       }
-      tc_fence_before();
-      named_bar_sync(1, kEpiThreads);
+      if (++i == q) { i = 0; ++jj; }
     }
   }
 }
 
+struct BlockRows {
+  int jrows, a_lo, a_hi, a_first, n_pass;
+  int64_t fbeg;
+};
+__device__ __forceinline__ BlockRows block_rows(const TcParams &p, int cb) {
+  BlockRows b;
+  const int j0 = cb * BMW;
+  b.jrows = min(BMW, p.r_dim - j0);
+  b.fbeg = (int64_t)j0 * p.q;
+  const int64_t fend = (int64_t)(j0 + b.jrows) * p.q;
+  b.a_lo = (int)(b.fbeg / p.n);
+  b.a_hi = (int)min((int64_t)p.m - 1, (fend - 1) / p.n);
+  b.a_first = b.a_lo & ~7;
+  b.n_pass = (b.a_hi - b.a_first) / 128 + 1;
+  return b;
+}
+
+// Request the regeneration operands of column block cb (one thread): every pass of xf rows
+// as one contiguous bulk copy; all of wf^T only when not already resident.
+__device__ __forceinline__ void regen_request(const TcParams &p, int cb, uint8_t *ar, uint8_t *br,
+                                              uint64_t *obar, bool need_b) {
+  const BlockRows b = block_rows(p, cb);
+  const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
+  const uint32_t a_bytes = (uint32_t)b.n_pass * 16u * sbo;
+  const uint32_t b_bytes = (uint32_t)p.n_chunks * (uint32_t)(p.Nc / 8) * sbo;
+  mbar_arrive_expect_tx(obar, a_bytes + (need_b ? b_bytes : 0u));
+  bulk_load(ar, p.xf_pk + (size_t)(b.a_first >> 3) * sbo, a_bytes, obar);
+  if (need_b) bulk_load(br, p.wf_pk, b_bytes, obar);
+}
+
+// Regenerate the W block of column block cb into shared memory (the 128 epilogue threads).
+//
+// Steps (pass, chunk): pass = 128 aux rows starting at a_first + 128*pass, chunk = Nc aux
+// columns. Operands are resident (regen_request, issued ahead); regeneration MMAs are
+// double-buffered in TMEM (columns [0, Nc) / [Nc, 2Nc)) so step s+1's MMA runs while
+// step s is read back and scattered.
+template <int MODE>
+__device__ void regen_block(const TcParams &p, int cb, uint32_t w_s, uint8_t *ar, uint8_t *br,
+                            uint64_t *rbar, uint32_t &rphase, uint64_t *obar, uint32_t &ophase,
+                            uint32_t tbase, int et, int wq, int lane) {
+  const BlockRows b = block_rows(p, cb);
+  const int q = p.q, n = p.n;
+  const int n_steps = b.n_pass * p.n_chunks;
+  const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
+  const int L = 32 * wq + lane;  // TMEM lane (= aux row offset within the pass)
+  const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)p.Nc);
+  const uint32_t ar_s = smem_u32(ar), br_s = smem_u32(br);
+
+  auto issue_mma = [&](int s) {  // et == 0 only
+    const int pass = s / p.n_chunks, chunk = s % p.n_chunks;
+    const uint32_t a_s = ar_s + (uint32_t)pass * 16u * sbo;
+    const uint32_t b_s = br_s + (uint32_t)chunk * (uint32_t)(p.Nc / 8) * sbo;
+    for (int kk = 0; kk < p.RK / 16; ++kk) {
+      uint64_t ad = smem_desc(a_s + kk * 256u, 128u, sbo, SL_NONE);
+      uint64_t bd = smem_desc(b_s + kk * 256u, 128u, sbo, SL_NONE);
+      mma_bf16_ss(tbase + (uint32_t)((s & 1) * p.Nc), ad, bd, idesc, kk > 0);
+    }
+    mma_commit(rbar);
+  };
+  if (et == 0) {
+    mbar_wait(obar, ophase);
+    trace(p, 24);
+    tc_fence_after();
+    issue_mma(0);
+  }
+  ophase ^= 1;
+
+  for (int s = 0; s < n_steps; ++s) {
+    const int pass = s / p.n_chunks, chunk = s % p.n_chunks;
+    const int c0 = chunk * p.Nc;
+    const int cols = min(p.Nc, n - c0);
+    mbar_wait(rbar, rphase);
+    if (et == 0 && s < 4) trace(p, 25 + s);
+    rphase ^= 1;
+    tc_fence_after();
+    if (!p.dbg_serial && et == 0 && s + 1 < n_steps) issue_mma(s + 1);  // overlaps this scatter
+    const int a = b.a_first + 128 * pass + L;
+    const int a_warp = b.a_first + 128 * pass + 32 * wq;  // this warp's rows: a_warp .. +31
+    const uint32_t tcol = tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)((s & 1) * p.Nc);
+    if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo) {  // warp-uniform: skip all-invalid warps
+      const int f0 = (int)((int64_t)a * n + c0 - b.fbeg);
+      int jj = f0 >= 0 ? f0 / q : -((-f0 + q - 1) / q);
+      int i = f0 - jj * q;
+      const bool row_ok = a >= b.a_lo && a <= b.a_hi;
+      for (int col0 = 0; col0 < p.Nc; col0 += 32) {
+        uint32_t v[32];
+        long long c0t = 0, c1t = 0;
+        if (p.trace) c0t = clock64();
+        tmem_ld_32x32b_x32(tcol + (uint32_t)col0, v);
+        tmem_ld_wait();
+        if (p.trace) {
+          uint32_t dep = v[0] ^ v[31];
+          asm volatile("" ::"r"(dep));
+          c1t = clock64();
+          if (et == 0 && s == 0) p.trace[(size_t)blockIdx.x * kTraceSlots + 32] += c1t - c0t;
+        }
+        if (row_ok && col0 < cols) scatter32<MODE>(v, w_s, p.w_sbo, jj, i, q, cols - col0, b.jrows);
+        if (p.trace && et == 0 && s == 0) {
+          asm volatile("" ::: "memory");
+          p.trace[(size_t)blockIdx.x * kTraceSlots + 33] += clock64() - c1t;
+        }
+        i += 32;
+        while (i >= q) { i -= q; ++jj; }
+      }
+    }
+    if (et == 0 && s == 0) trace(p, 31);
+    tc_fence_before();
+    named_bar_sync(1, kEpiThreads);
+    if (p.dbg_serial && et == 0 && s + 1 < n_steps) {
+      tc_fence_after();
+      issue_mma(s + 1);
+    }
+  }
+}
+
+template <int YDT, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_general(const __grid_constant__ CUtensorMap tm_x, const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *wblk = smem + p.off_w;
   uint8_t *xst = smem + p.off_x;
-  uint8_t *ar = smem + p.off_ar;
-  uint8_t *br = smem + p.off_br;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
-  uint64_t *bready = tempty + 2, *rbar = bready + 1;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(rbar + 1);
+  uint64_t *bready = tempty + 2, *rbar = bready + 1, *obar = rbar + 1;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(obar + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t item_beg = (int64_t)blockIdx.x * p.per_cta;
-  const int64_t item_end = (int64_t)min((int64_t)p.items, item_beg + (int64_t)p.per_cta);
+  const int item_beg = blockIdx.x * p.per_cta;
+  const int item_end = min(p.items, item_beg + p.per_cta);
 
   if (threadIdx.x == 0) {
+    trace(p, 0);
     for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiThreads); }
     mbar_init(bready, 1);
     mbar_init(rbar, 1);
+    mbar_init(obar, 1);
     fence_mbar_init();
+    // the first block's regeneration operands start streaming in before anything else
+    if (item_beg < item_end)
+      regen_request(p, item_beg / p.n_bt, smem + p.off_ar, smem + p.off_br, obar, true);
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_x);
   if (warp == 1) tmem_alloc(tslot, kTmemCols);
@@ -208,14 +309,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) trace(p, 1);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = item_beg; it < item_end; ++it) {
-        const int32_t b0 = (int32_t)((it % p.n_bt) * BNB);
+      for (int it = item_beg; it < item_end; ++it) {
+        const int32_t b0 = (it % p.n_bt) * BNB;
         for (int kb = 0; kb < p.KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kXStage);
@@ -223,17 +325,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
       }
+      trace(p, 22);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(BMW, BNB);
       const uint32_t w_s = smem_u32(wblk), x_s = smem_u32(xst);
-      int stage = 0, acc = 0;
+      int stage = 0, acc = 0, cur_cb = -1;
       uint32_t phase = 0, acc_phase = 0, bphase = 0;
-      int64_t cur_cb = -1;
-      for (int64_t it = item_beg; it < item_end; ++it) {
-        const int64_t cb = it / p.n_bt;
+      for (int it = item_beg; it < item_end; ++it) {
+        const int cb = it / p.n_bt;
         if (cb != cur_cb) {
           mbar_wait(bready, bphase);
           bphase ^= 1;
@@ -247,7 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < KATOM / 16; ++k) {
-            uint64_t ad = smem_desc(w_s + kb * kWKBlk + k * 32, 16, 1024, SL_SW128);
+            // A = W block, no-swizzle K-major: a 16-wide K step is 2 core columns (256 B)
+            uint64_t ad = smem_desc(w_s + (uint32_t)(kb * 4 + k) * 256u, 128u, p.w_sbo, SL_NONE);
             uint64_t bd = smem_desc(x_s + stage * kXStage + k * 32, 16, 1024, SL_SW128);
             mma_bf16_ss(d, ad, bd, idesc, (kb | k) != 0);
           }
@@ -255,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
+        trace(p, 14 + min(7, it - item_beg));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -263,58 +367,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 64;
     const int wq = warp & 3;
     const int jl = 32 * wq + lane;  // output column within the block (TMEM lane)
-    // zero the K padding [q, KB*64) of every W row once
-    for (int64_t i = p.q; i < (int64_t)p.KB * KATOM; ++i)
-      *reinterpret_cast<__nv_bfloat16 *>(wblk + w_off(et, i)) = __float2bfloat16(0.f);
-    uint32_t rphase = 0, acc_phase = 0;
-    int acc = 0;
-    int64_t cur_cb = -1;
+    const uint32_t w_s = smem_u32(wblk);
+    uint8_t *ar = smem + p.off_ar, *br = smem + p.off_br;
+    // one-time zeroing of the W K-padding [q, KB*64)
+    for (int i = p.q; i < p.KB * KATOM; ++i) sts_u16(w_s + w_off(et, i, p.w_sbo), 0);
+    const int mode = (p.q % 8 == 0 && p.n % 8 == 0) ? 2 : ((p.q % 2 == 0 && p.n % 2 == 0) ? 1 : 0);
+    uint32_t rphase = 0, ophase = 0, acc_phase = 0;
+    int acc = 0, cur_cb = -1, n_regen = 0;
     float bias_j = 0.f;
-    for (int64_t it = item_beg; it < item_end; ++it) {
-      const int64_t cb = it / p.n_bt, bt = it % p.n_bt;
-      const int64_t j = cb * BMW + jl;
+    for (int it = item_beg; it < item_end; ++it) {
+      const int cb = it / p.n_bt, bt = it % p.n_bt;
+      const int j = cb * BMW + jl;
       if (cb != cur_cb) {
-        regen_block(p, cb, wblk, ar, br, rbar, rphase, tbase, et, wq, lane);
+        if (et == 0 && n_regen < 2) trace(p, 2 + 2 * n_regen);
+        if (et == 0 && n_regen > 0) regen_request(p, cb, ar, br, obar, false);
+        if (mode == 2)
+          regen_block<2>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, lane);
+        else if (mode == 1)
+          regen_block<1>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, lane);
+        else
+          regen_block<0>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, lane);
         fence_proxy_async_smem();
         tc_fence_before();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) mbar_arrive(bready);
+        if (et == 0 && n_regen < 2) trace(p, 3 + 2 * n_regen);
+        ++n_regen;
         cur_cb = cb;
         bias_j = (p.bias && j < p.r_dim) ? p.bias[j] : 0.f;
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t b0 = bt * BNB;
+      const int b0 = bt * BNB;
       const bool jok = j < p.r_dim;
+      const int nrows = (int)min((int64_t)BNB, p.batch - b0);
+      using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
+      OutT *yp = reinterpret_cast<OutT *>(p.y) + (int64_t)b0 * p.ldy + j;
       for (int c32 = 0; c32 < BNB / 32; ++c32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * BNB + c32 * 32), v);
         tmem_ld_wait();
-        if (!jok) continue;
-        const int64_t bb = b0 + c32 * 32;
-        if (p.y_dtype == DT_BF16) {
-          __nv_bfloat16 *y = reinterpret_cast<__nv_bfloat16 *>(p.y);
+        if (jok) {
+          const int rmax = nrows - c32 * 32;
 #pragma unroll
-          for (int r = 0; r < 32; ++r)
-            if (bb + r < p.batch)
-              y[(bb + r) * p.ldy + j] =
-                  __float2bfloat16_rn(act_apply(p.act, __uint_as_float(v[r]) + bias_j, p.arg));
-        } else {
-          float *y = reinterpret_cast<float *>(p.y);
-#pragma unroll
-          for (int r = 0; r < 32; ++r)
-            if (bb + r < p.batch)
-              y[(bb + r) * p.ldy + j] = act_apply(p.act, __uint_as_float(v[r]) + bias_j, p.arg);
+          for (int r = 0; r < 32; ++r) {
+            if (r < rmax) {
+              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+            }
+            yp += p.ldy;
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (et == 0) trace(p, 6 + min(7, it - item_beg));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace(p, 23);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tbase, kTmemCols);
@@ -332,6 +446,29 @@ __global__ void k_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, i
     v = x_dtype == DT_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(x)[b * q + i])
                            : reinterpret_cast<const float *>(x)[b * q + i];
   out[idx] = __float2bfloat16_rn(v);
+}
+
+// Pack bf16 factors into the regeneration operands' core-matrix layout (zero padded):
+//   xf_pk: rows 0 .. xrows-1 (xrows = round_up(m, 8) + 128) x RK,
+//   wf_pk: wf^T, rows c = 0 .. n_chunks*Nc - 1 x RK.
+__global__ void k_pack_general(int m, int n, int rank, int RK, int xrows, int wrows,
+                               const __nv_bfloat16 *xf, const __nv_bfloat16 *wf, uint8_t *xf_pk,
+                               uint8_t *wf_pk) {
+  const uint32_t sbo = (uint32_t)(RK / 8) * 128u;
+  const int64_t nx = (int64_t)xrows * RK, nw = (int64_t)wrows * RK;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < nx + nw;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    if (idx < nx) {
+      const int row = (int)(idx / RK), k = (int)(idx % RK);
+      const __nv_bfloat16 v = (row < m && k < rank) ? xf[(int64_t)row * rank + k] : __float2bfloat16(0.f);
+      *reinterpret_cast<__nv_bfloat16 *>(xf_pk + core_off(row, k, sbo)) = v;
+    } else {
+      const int64_t e = idx - nx;
+      const int c = (int)(e / RK), k = (int)(e % RK);
+      const __nv_bfloat16 v = (c < n && k < rank) ? wf[(int64_t)k * n + c] : __float2bfloat16(0.f);
+      *reinterpret_cast<__nv_bfloat16 *>(wf_pk + core_off(c, k, sbo)) = v;
+    }
+  }
 }
 
 // ---- host ------------------------------------------------------------------------------
@@ -356,7 +493,7 @@ PFN_encode_tiled encode_fn() {
 }
 
 struct Layout {
-  int KB, S, RK, Nc, n_chunks;
+  int KB, S, RK, Nc, n_chunks, n_pass;
   uint32_t off_w, off_x, off_ar, off_br, off_bar, total;
 };
 
@@ -365,9 +502,14 @@ bool make_layout(const Geo &g, Layout *L) {
   L->RK = (int)((g.rank + 15) / 16 * 16);
   L->n_chunks = (int)((g.n + 255) / 256);
   L->Nc = (int)(((g.n + L->n_chunks - 1) / L->n_chunks + 31) / 32 * 32);
+  // aux rows one W block touches (+ the 8-row alignment of the first pass)
+  const int64_t span = (BMW * g.q + g.n - 1) / g.n + 1 + 7;
+  L->n_pass = (int)((span + 127) / 128);
   if (L->RK > 64) return false;
   uint32_t w = (uint32_t)L->KB * kWKBlk;
-  uint32_t arb = 128u * L->RK * 2, brb = (uint32_t)L->Nc * L->RK * 2;
+  // all of a block's regeneration operands stay resident: every pass of xf rows, all of wf
+  uint32_t arb = (uint32_t)L->n_pass * 128u * L->RK * 2;
+  uint32_t brb = (uint32_t)L->n_chunks * L->Nc * L->RK * 2;
   uint32_t fixed = w + arb + brb + 1024 /*barriers*/ + 1024 /*alignment slack*/;
   int S = 0;
   for (int s = 8; s >= 2; --s)
@@ -383,40 +525,122 @@ bool make_layout(const Geo &g, Layout *L) {
   return true;
 }
 
-}  // namespace
+typedef void (*KernelFn)(CUtensorMap, TcParams);
 
-size_t tc_general_ws(const Geo &g, int64_t batch) {
-  int64_t ldx = (g.q + 7) / 8 * 8;
-  return (size_t)batch * ldx * 2 + 256;
+template <int YDT>
+KernelFn pick_act(int act) {
+  switch (act) {
+    case DT_ACT_RELU: return k_tc_general<YDT, DT_ACT_RELU>;
+    case DT_ACT_SIGMOID: return k_tc_general<YDT, DT_ACT_SIGMOID>;
+    case DT_ACT_TANH: return k_tc_general<YDT, DT_ACT_TANH>;
+    case DT_ACT_CLIPPED_RELU: return k_tc_general<YDT, DT_ACT_CLIPPED_RELU>;
+    default: return k_tc_general<YDT, DT_ACT_IDENTITY>;
+  }
 }
 
-int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
-                       const uint16_t *xf_bf16, const uint16_t *wf_bf16, const float *bias,
-                       int act, float act_arg, void *y, int y_dtype, char *ws, size_t ws_bytes,
-                       cudaStream_t st) {
-  Layout L;
-  if (!make_layout(g, &L)) {
+void print_trace(const std::vector<unsigned long long> &h, int grid, const TcParams &p) {
+  unsigned long long t0 = ~0ull, t1 = 0;
+  for (int c = 0; c < grid; ++c) {
+    t0 = std::min(t0, h[(size_t)c * kTraceSlots]);
+    t1 = std::max(t1, h[(size_t)c * kTraceSlots + 23]);
+  }
+  fprintf(stderr, "[tc trace] grid %d per_cta %d S %d KB %d span %.2f us\n", grid, p.per_cta, p.S,
+          p.KB, (t1 - t0) / 1e3);
+  for (int c = 0; c < grid; c += std::max(1, grid / 6)) {
+    const unsigned long long *r = &h[(size_t)c * kTraceSlots];
+    auto rel = [&](int s) { return r[s] ? (double)(r[s] - t0) / 1e3 : -1.0; };
+    fprintf(stderr, "  cta %3d: start %.2f setup %.2f regen [%.2f..%.2f] epi", c, rel(0), rel(1),
+            rel(2), rel(3));
+    for (int k = 0; k < 8; ++k)
+      if (r[6 + k]) fprintf(stderr, " %.2f", rel(6 + k));
+    fprintf(stderr, " | mma");
+    for (int k = 0; k < 8; ++k)
+      if (r[14 + k]) fprintf(stderr, " %.2f", rel(14 + k));
+    fprintf(stderr,
+            " | prod %.2f end %.2f | regen ops %.2f steps %.2f %.2f %.2f %.2f | ld0 %.2f..%.2f "
+            "step0 end %.2f\n",
+            rel(22), rel(23), rel(24), rel(25), rel(26), rel(27), rel(28), rel(29), rel(30),
+            rel(31));
+    fprintf(stderr, "        step0 (thread 64): ld cycles %llu scatter cycles %llu\n", r[32], r[33]);
+  }
+}
+
+}  // namespace
+
+static int check_layout(const Geo &g, Layout *L) {
+  if (!make_layout(g, L)) {
     set_error("tcgen05 general path: q=" + std::to_string(g.q) + ", rank=" +
               std::to_string(g.rank) + " does not fit the resident-W-block kernel "
               "(needs ceil(q/64)*16 KB + stages <= 227 KB and rank <= 64)");
     return DT_E_UNSUPPORTED;
   }
+  if (g.m * g.n > INT32_MAX || g.q * g.r_dim > INT32_MAX) {
+    set_error("tcgen05 general path: m*n must fit in 32 bits");
+    return DT_E_UNSUPPORTED;
+  }
+  return DT_OK;
+}
+
+static int packed_x_rows(const Geo &g, const Layout &L) {
+  return (int)(((g.m + 7) / 8) * 8 + 128 * L.n_pass);
+}
+static size_t packed_x_bytes(const Geo &g, const Layout &L) {
+  return (size_t)packed_x_rows(g, L) * L.RK * 2;
+}
+
+size_t tc_general_packed_bytes(const Geo &g) {
+  Layout L;
+  if (!make_layout(g, &L)) return 0;
+  return (packed_x_bytes(g, L) + 255) / 256 * 256 + (size_t)L.n_chunks * L.Nc * L.RK * 2;
+}
+
+int tc_general_pack(const Geo &g, const uint16_t *xf_bf16, const uint16_t *wf_bf16, void *packed,
+                    cudaStream_t st) {
+  Layout L;
+  if (int rc = check_layout(g, &L)) return rc;
+  const int xrows = packed_x_rows(g, L);
+  const int wrows = L.n_chunks * L.Nc;
+  uint8_t *xpk = reinterpret_cast<uint8_t *>(packed);
+  uint8_t *wpk = xpk + (packed_x_bytes(g, L) + 255) / 256 * 256;
+  const int64_t tot = (int64_t)(xrows + wrows) * L.RK;
+  const unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 4096);
+  k_pack_general<<<blocks, 256, 0, st>>>((int)g.m, (int)g.n, (int)g.rank, L.RK, xrows, wrows,
+                                         reinterpret_cast<const __nv_bfloat16 *>(xf_bf16),
+                                         reinterpret_cast<const __nv_bfloat16 *>(wf_bf16), xpk, wpk);
+  return check_launch("pack_general");
+}
+
+size_t tc_general_ws(const Geo &g, int64_t batch) {
+  int64_t ldx = (g.q + 7) / 8 * 8;
+  return (size_t)batch * ldx * 2 + 256 + tc_general_packed_bytes(g) + 256;
+}
+
+int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
+                       const uint16_t *xf_bf16, const uint16_t *wf_bf16, const void *packed,
+                       const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  Layout L;
+  if (int rc = check_layout(g, &L)) return rc;
   if (batch == 0) return DT_OK;
   PFN_encode_tiled enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable from the driver");
     return DT_E_CUDA;
   }
+  if (ws_bytes < tc_general_ws(g, batch) - (packed ? tc_general_packed_bytes(g) + 256 : 0)) {
+    set_error("forward workspace too small: need " + std::to_string(tc_general_ws(g, batch)));
+    return DT_E_ARG;
+  }
+  if (!packed) {  // pack the regeneration operands into the workspace tail for this call
+    char *pk = ws + ((size_t)batch * ((g.q + 7) / 8 * 8) * 2 + 256 + 255) / 256 * 256;
+    if (int rc = tc_general_pack(g, xf_bf16, wf_bf16, pk, st)) return rc;
+    packed = pk;
+  }
   // TMA needs a bf16 x whose row pitch is a multiple of 16 bytes.
   const void *xt = x;
   int64_t ldx = g.q;
   if (x_dtype != DT_BF16 || (g.q % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
     ldx = (g.q + 7) / 8 * 8;
-    size_t need = (size_t)batch * ldx * 2;
-    if (need > ws_bytes) {
-      set_error("forward workspace too small for the packed bf16 input");
-      return DT_E_ARG;
-    }
     int64_t tot = batch * ldx;
     k_pack_x<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(batch, g.q, ldx, x, x_dtype,
                                                              reinterpret_cast<__nv_bfloat16 *>(ws));
@@ -436,8 +660,9 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
     return DT_E_CUDA;
   }
   TcParams p{};
-  p.q = g.q; p.r_dim = g.r_dim; p.rank = g.rank; p.m = g.m; p.n = g.n; p.batch = batch;
-  p.ldy = g.r_dim;
+  p.batch = batch;
+  p.q = (int)g.q; p.r_dim = (int)g.r_dim; p.rank = (int)g.rank; p.m = (int)g.m; p.n = (int)g.n;
+  p.ldy = (int)g.r_dim;
   p.KB = L.KB; p.S = L.S; p.RK = L.RK; p.Nc = L.Nc; p.n_chunks = L.n_chunks;
   p.n_cb = (int)((g.r_dim + BMW - 1) / BMW);
   p.n_bt = (int)((batch + BNB - 1) / BNB);
@@ -446,24 +671,38 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   p.per_cta = (p.items + nsm - 1) / nsm;
-  int grid = (p.items + p.per_cta - 1) / p.per_cta;
-  p.xf = reinterpret_cast<const __nv_bfloat16 *>(xf_bf16);
-  p.wf = reinterpret_cast<const __nv_bfloat16 *>(wf_bf16);
+  const int grid = (p.items + p.per_cta - 1) / p.per_cta;
+  p.xf_pk = reinterpret_cast<const uint8_t *>(packed);
+  p.wf_pk = p.xf_pk + (packed_x_bytes(g, L) + 255) / 256 * 256;
   p.bias = bias;
   p.y = y;
-  p.y_dtype = y_dtype;
-  p.act = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
   p.arg = act_arg;
+  static const int dbg_serial = getenv("DEEPTHIN_REGEN_SERIAL") != nullptr;
+  p.dbg_serial = dbg_serial;
   p.off_w = L.off_w; p.off_x = L.off_x; p.off_ar = L.off_ar; p.off_br = L.off_br;
   p.off_bar = L.off_bar;
-  static bool attr_set = false;
-  if (!attr_set) {
-    DT_CUDA_CHECK(cudaFuncSetAttribute(k_tc_general, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSmemBudget));
-    attr_set = true;
+  p.w_sbo = (uint32_t)L.KB * (KATOM / 8) * 128u;
+  const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
+  KernelFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(eact) : pick_act<DT_F32>(eact);
+  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+
+  // Debug: DEEPTHIN_TC_TRACE=1 records per-CTA globaltimer stamps and prints a phase summary.
+  static const bool tracing = getenv("DEEPTHIN_TC_TRACE") != nullptr;
+  unsigned long long *tbuf = nullptr;
+  if (tracing) {
+    DT_CUDA_CHECK(cudaMalloc(&tbuf, (size_t)grid * kTraceSlots * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(tbuf, 0, (size_t)grid * kTraceSlots * 8, st));
+    p.trace = tbuf;
   }
-  k_tc_general<<<grid, kThreads, L.total, st>>>(tm, p);
+  fn<<<grid, kThreads, L.total, st>>>(tm, p);
   if (int rc = check_launch("tc_general")) return rc;
+  if (tracing) {
+    std::vector<unsigned long long> h((size_t)grid * kTraceSlots);
+    DT_CUDA_CHECK(cudaStreamSynchronize(st));
+    DT_CUDA_CHECK(cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(tbuf);
+    print_trace(h, grid, p);
+  }
   if (act == DT_ACT_SOFTMAX) return launch_row_softmax(batch, g.r_dim, y, y_dtype, st);
   return DT_OK;
 }

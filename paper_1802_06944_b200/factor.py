@@ -67,6 +67,35 @@ class FactorPair:
             self._cache["bf16"] = tuple(out)
         return self._cache["bf16"]
 
+    def packed(self):
+        """Regeneration operands for the bf16 tensor-core general path (dt_pack_factors),
+        made once per pair; None where that path does not use them (reuse geometries)."""
+        if "packed" not in self._cache:
+            lib = _lib.lib()
+            ps = _lib.plan_struct(self.plan)
+            nbytes = lib.dt_packed_factors_bytes(C.byref(ps), _lib.DT_MMA_BF16)
+            buf = None
+            if nbytes:
+                xf16, wf16 = self.bf16()
+                buf = torch.empty(nbytes, dtype=torch.uint8, device=self.xf.device)
+                _lib.check(lib.dt_pack_factors(C.byref(ps), _lib.DT_MMA_BF16, xf16.data_ptr(),
+                                               wf16.data_ptr(), buf.data_ptr(), stream_handle()))
+            self._cache["packed"] = buf
+        return self._cache["packed"]
+
+    def refresh_derived(self) -> None:
+        """Re-derive the cached bf16 / packed copies after the fp32 masters changed (SGD)."""
+        lib = _lib.lib()
+        if "bf16" in self._cache:
+            for src, dst in zip((self.xf, self.wf), self._cache["bf16"]):
+                _lib.check(lib.dt_cast_bf16(src.numel(), src.data_ptr(), dst.data_ptr(),
+                                            stream_handle()))
+        if self._cache.get("packed") is not None:
+            xf16, wf16 = self._cache["bf16"]
+            _lib.check(lib.dt_pack_factors(C.byref(_lib.plan_struct(self.plan)), _lib.DT_MMA_BF16,
+                                           xf16.data_ptr(), wf16.data_ptr(),
+                                           self._cache["packed"].data_ptr(), stream_handle()))
+
 
 def _ptr(a) -> int:
     return a.data_ptr() if isinstance(a, torch.Tensor) else -1

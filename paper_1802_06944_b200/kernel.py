@@ -120,14 +120,19 @@ def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float
     ws_bytes = lib.dt_forward_workspace_bytes(C.byref(ps), batch, mma)
     ws = workspace(ws_bytes)
     if mma == _lib.DT_MMA_BF16:
-        xf, wf = fp.bf16()
-        fdt = _lib.DT_BF16
+        pk = fp.packed()
+        if pk is not None:
+            xf, wf, fdt = pk, None, _lib.DT_FACTORS_PACKED
+        else:
+            xf, wf = fp.bf16()
+            fdt = _lib.DT_BF16
     else:
         xf, wf, fdt = fp.xf, fp.wf, _lib.DT_F32
     _lib.check(lib.dt_forward(
         C.byref(ps), batch, mma, x.data_ptr(),
         _lib.DT_BF16 if x.dtype == torch.bfloat16 else _lib.DT_F32,
-        xf.data_ptr(), wf.data_ptr(), fdt, bias.data_ptr() if bias is not None else None,
+        xf.data_ptr(), wf.data_ptr() if wf is not None else None, fdt,
+        bias.data_ptr() if bias is not None else None,
         act, float(act_arg), y.data_ptr(),
         _lib.DT_BF16 if y.dtype == torch.bfloat16 else _lib.DT_F32,
         ws.data_ptr(), ws.numel(), stream_handle()))

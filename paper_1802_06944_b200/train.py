@@ -59,10 +59,7 @@ class DeepThinLayer:
         for p, g in ((self.fp.xf, self.d_xf), (self.fp.wf, self.d_wf), (self.bias, self.d_bias)):
             _lib.check(lib.dt_sgd_step(p.numel(), p.data_ptr(), g.data_ptr(), float(lr),
                                        stream_handle()))
-        if "bf16" in self.fp._cache:
-            for src, dst in zip((self.fp.xf, self.fp.wf), self.fp._cache["bf16"]):
-                _lib.check(lib.dt_cast_bf16(src.numel(), src.data_ptr(), dst.data_ptr(),
-                                            stream_handle()))
+        self.fp.refresh_derived()
 
 
 def train_step(layer: DeepThinLayer, x: torch.Tensor, target: torch.Tensor, lr: float,

@@ -37,6 +37,23 @@ def gpu_x(a, dtype):
     return torch.tensor(a, dtype=torch.float32, device="cuda").to(dtype)
 
 
+def bf16_emulated(d, plan, bias):
+    """The bf16 tensor-core contract emulated in f64: W rounded to bf16 (RNE), exact sums.
+
+    The kernel must match this up to fp32 accumulation order and the occasional
+    one-ulp bf16 double-rounding of a regenerated element."""
+    w = O.round_bf16(O.decompress(d["xf"], d["wf"], plan))
+    return d["x"] @ w + bias
+
+
+def check_activation(y_act, y_pre, act, arg=20.0):
+    """The fused activation epilogue, checked on the kernel's own pre-activations."""
+    pre = y_pre.detach().double().cpu().numpy() if hasattr(y_pre, "detach") else y_pre
+    want = O.apply_activation(act, pre, arg)
+    got = y_act.detach().double().cpu().numpy() if hasattr(y_act, "detach") else y_act
+    assert np.max(np.abs(got - want)) <= 1e-6 * max(1.0, np.max(np.abs(want))), act
+
+
 # ---- FFMA fp32 path -----------------------------------------------------------------
 
 def test_ffma_matches_reference_golden_small_plans(golden):
@@ -88,10 +105,16 @@ def test_ffma_config1_full_batch():
 def test_ffma_general_path(geo):
     q, r_dim, rank, n, m, batch = geo
     plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=3)
-    for act in ("identity", "relu", "tanh"):
-        ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], act)
-        y = D.layer_forward(d["x"], fp, d["bias"], act, mma="ffma")
-        assert O.rel_error(y, ref) <= F32_TOL, act
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(d["x"], fp, d["bias"], "identity", mma="ffma")
+    assert O.rel_error(y, ref) <= F32_TOL
+    # bounded activations shrink max|e| and would inflate rel_error; |act'| <= 1 so
+    # the absolute error stays within the pre-activation bound
+    for act in ("relu", "tanh", "sigmoid"):
+        ya = D.layer_forward(d["x"], fp, d["bias"], act, mma="ffma")
+        want = O.apply_activation(act, ref)
+        assert np.max(np.abs(ya - want)) <= F32_TOL * np.max(np.abs(ref)), act
+        check_activation(ya, y, act)
 
 
 def test_ffma_bf16_input_exact_products():
@@ -111,6 +134,7 @@ def test_tc_general_config2_full_batch(seed):
     y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
     err = O.rel_error(y, ref)
     assert err <= BF16_TOL, err
+    assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3
 
 
 @pytest.mark.parametrize("geo", [
@@ -125,16 +149,23 @@ def test_tc_general_geometries(geo):
     plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=5, rnd=O.round_bf16)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
     y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
-    assert O.rel_error(y, ref) <= BF16_TOL
+    # kernel correctness: tight against the bf16-rounded-W emulation
+    assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3
+    # the contract tolerance is a statistic over many outputs; a 100-output row can
+    # exceed it by chance from W's bf16 rounding alone
+    if batch * r_dim >= 10_000:
+        assert O.rel_error(y, ref) <= BF16_TOL
 
 
 @pytest.mark.parametrize("act", ["relu", "sigmoid", "tanh", "clipped_relu", "softmax"])
 def test_tc_general_fused_activations(act):
     plan, d, fp = make_case(440, 2048, 24, 320, 2816, 384, seed=7, rnd=O.round_bf16, bias_sd=0.5)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
-    ref = O.apply_activation(act, ref, 2.0)
-    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], act, mma="bf16", act_arg=2.0)
-    assert O.rel_error(y, ref) <= BF16_TOL
+    x = gpu_x(d["x"], torch.bfloat16)
+    pre = D.layer_forward(x, fp, d["bias"], "identity", mma="bf16")
+    assert O.rel_error(pre, ref) <= BF16_TOL          # the contraction (deterministic kernel)
+    y = D.layer_forward(x, fp, d["bias"], act, mma="bf16", act_arg=2.0)
+    check_activation(y, pre, act, 2.0)                # the fused epilogue on the same logits
 
 
 def test_tc_general_fp32_input_and_bf16_output():
