@@ -47,10 +47,14 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 192;
-constexpr int kEpiThreads = 128;
+// warps 0-1: TMA producer / MMA issuer; warps 2..: regeneration + epilogue, kParts warps per
+// TMEM lane quarter (warp % 4) splitting the columns between them (part = (warp - 2) / 4).
+constexpr int kParts = 3;
+constexpr int kEpiThreads = 128 * kParts;
+constexpr int kThreads = 64 + kEpiThreads;
 constexpr int BMW = 128;   // W rows (output columns) per block == UMMA M
-constexpr int BNB = 128;   // batch rows per tile == UMMA N
+constexpr int BNB = 256;   // batch rows per tile == UMMA N (N=256 runs the MMA at ~88% of
+                           // peak; N=128 is shared-memory-bound at ~60%, measured)
 constexpr int KATOM = 64;  // bf16 elements per 128-byte swizzle row
 constexpr uint32_t kXStage = BNB * 128;   // bytes per x stage (128 rows x 64 bf16)
 constexpr uint32_t kWKBlk = BMW * 128;    // bytes per W k-block
@@ -61,7 +65,8 @@ constexpr int kTraceSlots = 48;
 struct TcParams {
   int64_t batch;
   int q, r_dim, rank, m, n, ldy;
-  int KB, S, RK, Nc, n_chunks, n_cb, n_bt, items, per_cta;
+  int KB, S, S_ded, RK, Nc, n_chunks, n_cb, n_bt, items, per_cta;
+  int a_res;  // passes of xf rows resident at once (all, or 1 = streamed per pass)
   const uint8_t *xf_pk, *wf_pk;  // regeneration operands, pre-packed (dt_pack_factors)
   const float *bias;
   void *y;
@@ -70,6 +75,7 @@ struct TcParams {
   uint32_t w_sbo;  // W block 8-row-group stride (no-swizzle K-major layout)
   unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps, else null
   int dbg_serial;             // DEEPTHIN_REGEN_SERIAL: no regen MMA / read-back overlap
+  int dbg_regen;              // DEEPTHIN_DBG_REGEN: 1 skip scatter, 2 skip TMEM loads (timing only)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -130,23 +136,40 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
 template <int MODE>
 __device__ __forceinline__ void scatter32(const uint32_t (&v)[32], uint32_t w_s, uint32_t sbo,
                                           int jj, int i, int q, int cvalid, int jrows) {
+  // predicated stores (no per-store branch / reconvergence barrier)
   if constexpr (MODE == 2) {
+    // 16-byte units (i % 8 == 0): consecutive units of one W row are 128 B apart in the
+    // core-matrix layout; the address is recomputed only when the run wraps to the next row
+    uint32_t addr = w_s + w_off(jj, i, sbo);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      if (8 * t < cvalid && jj >= 0 && jj < jrows)
-        sts_v4(w_s + w_off(jj, i, sbo), pack_bf16(v[8 * t], v[8 * t + 1]),
-               pack_bf16(v[8 * t + 2], v[8 * t + 3]), pack_bf16(v[8 * t + 4], v[8 * t + 5]),
-               pack_bf16(v[8 * t + 6], v[8 * t + 7]));
+      const uint32_t ok = (8 * t < cvalid) & ((uint32_t)jj < (uint32_t)jrows);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+          "@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(addr),
+          "r"(pack_bf16(v[8 * t], v[8 * t + 1])), "r"(pack_bf16(v[8 * t + 2], v[8 * t + 3])),
+          "r"(pack_bf16(v[8 * t + 4], v[8 * t + 5])), "r"(pack_bf16(v[8 * t + 6], v[8 * t + 7])),
+          "r"(ok));
       i += 8;
-      if (i >= q) { i -= q; ++jj; }
+      addr += 128u;
+      if (i >= q) {
+        i -= q;
+        ++jj;
+        addr = w_s + w_off(jj, i, sbo);
+      }
     }
   } else if constexpr (MODE == 1) {
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-      if (2 * t < cvalid && jj >= 0 && jj < jrows)
-        sts_u32(w_s + w_off(jj, i, sbo), pack_bf16(v[2 * t], v[2 * t + 1]));
+      const uint32_t ok = (2 * t < cvalid) & (jj >= 0) & (jj < jrows);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(
+              w_s + w_off(jj, i, sbo)),
+          "r"(pack_bf16(v[2 * t], v[2 * t + 1])), "r"(ok));
       i += 2;
-      if (i >= q) { i -= q; ++jj; }
+      const bool wrap = i >= q;
+      i -= wrap ? q : 0;
+      jj += wrap;
     }
   } else {
 #pragma unroll
@@ -183,7 +206,7 @@ __device__ __forceinline__ void regen_request(const TcParams &p, int cb, uint8_t
                                               uint64_t *obar, bool need_b) {
   const BlockRows b = block_rows(p, cb);
   const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
-  const uint32_t a_bytes = (uint32_t)b.n_pass * 16u * sbo;
+  const uint32_t a_bytes = (uint32_t)min(b.n_pass, p.a_res) * 16u * sbo;
   const uint32_t b_bytes = (uint32_t)p.n_chunks * (uint32_t)(p.Nc / 8) * sbo;
   mbar_arrive_expect_tx(obar, a_bytes + (need_b ? b_bytes : 0u));
   bulk_load(ar, p.xf_pk + (size_t)(b.a_first >> 3) * sbo, a_bytes, obar);
@@ -199,7 +222,7 @@ __device__ __forceinline__ void regen_request(const TcParams &p, int cb, uint8_t
 template <int MODE>
 __device__ void regen_block(const TcParams &p, int cb, uint32_t w_s, uint8_t *ar, uint8_t *br,
                             uint64_t *rbar, uint32_t &rphase, uint64_t *obar, uint32_t &ophase,
-                            uint32_t tbase, int et, int wq, int lane) {
+                            uint32_t tbase, int et, int wq, int part, int lane) {
   const BlockRows b = block_rows(p, cb);
   const int q = p.q, n = p.n;
   const int n_steps = b.n_pass * p.n_chunks;
@@ -208,9 +231,10 @@ __device__ void regen_block(const TcParams &p, int cb, uint32_t w_s, uint8_t *ar
   const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)p.Nc);
   const uint32_t ar_s = smem_u32(ar), br_s = smem_u32(br);
 
+  const bool stream = p.a_res < b.n_pass;  // one pass of xf rows resident, reloaded per pass
   auto issue_mma = [&](int s) {  // et == 0 only
     const int pass = s / p.n_chunks, chunk = s % p.n_chunks;
-    const uint32_t a_s = ar_s + (uint32_t)pass * 16u * sbo;
+    const uint32_t a_s = ar_s + (stream ? 0u : (uint32_t)pass * 16u * sbo);
     const uint32_t b_s = br_s + (uint32_t)chunk * (uint32_t)(p.Nc / 8) * sbo;
     for (int kk = 0; kk < p.RK / 16; ++kk) {
       uint64_t ad = smem_desc(a_s + kk * 256u, 128u, sbo, SL_NONE);
@@ -235,42 +259,49 @@ __device__ void regen_block(const TcParams &p, int cb, uint32_t w_s, uint8_t *ar
     if (et == 0 && s < 4) trace(p, 25 + s);
     rphase ^= 1;
     tc_fence_after();
-    if (!p.dbg_serial && et == 0 && s + 1 < n_steps) issue_mma(s + 1);  // overlaps this scatter
+    // the next step's MMA goes to the other TMEM buffer and overlaps this read-back, unless it
+    // needs a streamed pass of xf rows that must first replace the current one
+    const bool next_new_pass = stream && (s + 1) % p.n_chunks == 0;
+    const bool early = !p.dbg_serial && !next_new_pass;
+    if (early && et == 0 && s + 1 < n_steps) issue_mma(s + 1);
     const int a = b.a_first + 128 * pass + L;
     const int a_warp = b.a_first + 128 * pass + 32 * wq;  // this warp's rows: a_warp .. +31
     const uint32_t tcol = tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)((s & 1) * p.Nc);
-    if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo) {  // warp-uniform: skip all-invalid warps
-      const int f0 = (int)((int64_t)a * n + c0 - b.fbeg);
+    if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo && p.dbg_regen != 3) {  // skip all-invalid warps
+      // this warp's column groups: part, part + kParts, ... (32 columns each); the next
+      // group's TMEM load is in flight while the current group is scattered
+      const int f0 = (int)((int64_t)a * n + c0 + 32 * part - b.fbeg);
       int jj = f0 >= 0 ? f0 / q : -((-f0 + q - 1) / q);
       int i = f0 - jj * q;
       const bool row_ok = a >= b.a_lo && a <= b.a_hi;
-      for (int col0 = 0; col0 < p.Nc; col0 += 32) {
+      for (int col0 = 32 * part; col0 < p.Nc; col0 += 32 * kParts) {
         uint32_t v[32];
-        long long c0t = 0, c1t = 0;
-        if (p.trace) c0t = clock64();
         tmem_ld_32x32b_x32(tcol + (uint32_t)col0, v);
         tmem_ld_wait();
-        if (p.trace) {
-          uint32_t dep = v[0] ^ v[31];
-          asm volatile("" ::"r"(dep));
-          c1t = clock64();
-          if (et == 0 && s == 0) p.trace[(size_t)blockIdx.x * kTraceSlots + 32] += c1t - c0t;
-        }
-        if (row_ok && col0 < cols) scatter32<MODE>(v, w_s, p.w_sbo, jj, i, q, cols - col0, b.jrows);
-        if (p.trace && et == 0 && s == 0) {
-          asm volatile("" ::: "memory");
-          p.trace[(size_t)blockIdx.x * kTraceSlots + 33] += clock64() - c1t;
-        }
-        i += 32;
+        if (row_ok && col0 < cols && p.dbg_regen != 1)
+          scatter32<MODE>(v, w_s, p.w_sbo, jj, i, q, cols - col0, b.jrows);
+        i += 32 * kParts;
         while (i >= q) { i -= q; ++jj; }
       }
     }
     if (et == 0 && s == 0) trace(p, 31);
     tc_fence_before();
     named_bar_sync(1, kEpiThreads);
-    if (p.dbg_serial && et == 0 && s + 1 < n_steps) {
-      tc_fence_after();
-      issue_mma(s + 1);
+    if (!early && s + 1 < n_steps) {
+      if (next_new_pass) {  // all MMAs reading the old pass are complete (rbar waited)
+        if (et == 0) {
+          const uint32_t bytes = 16u * sbo;
+          mbar_arrive_expect_tx(obar, bytes);
+          bulk_load(ar, p.xf_pk + (size_t)((b.a_first >> 3) + 16 * ((s + 1) / p.n_chunks)) * sbo,
+                    bytes, obar);
+          mbar_wait(obar, ophase);
+        }
+        ophase ^= 1;
+      }
+      if (et == 0) {
+        tc_fence_after();
+        issue_mma(s + 1);
+      }
     }
   }
 }
@@ -314,11 +345,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      int stage = 0;
+      int stage = 0, cur_cb = -1, n_cbs = 0;
       uint32_t phase = 0;
+      bool regen_pending = false;
       for (int it = item_beg; it < item_end; ++it) {
         const int32_t b0 = (it % p.n_bt) * BNB;
+        if (it / p.n_bt != cur_cb) {
+          cur_cb = it / p.n_bt;
+          ++n_cbs;
+          regen_pending = true;
+        }
         for (int kb = 0; kb < p.KB; ++kb) {
+          if (stage >= p.S_ded && regen_pending) {  // stage aliases the regen operands
+            mbar_wait(bready, (uint32_t)(n_cbs - 1) & 1u);
+            regen_pending = false;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kXStage);
           tma_load_2d(xst + (size_t)stage * kXStage, &tm_x, &full[stage], kb * KATOM, b0);
@@ -363,14 +404,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- regeneration + epilogue (warps 2-5) ----------------
+    // ---------------- regeneration + epilogue (warps 2-9) ----------------
     const int et = threadIdx.x - 64;
     const int wq = warp & 3;
+    const int part = (warp - 2) / 4;
     const int jl = 32 * wq + lane;  // output column within the block (TMEM lane)
     const uint32_t w_s = smem_u32(wblk);
     uint8_t *ar = smem + p.off_ar, *br = smem + p.off_br;
     // one-time zeroing of the W K-padding [q, KB*64)
-    for (int i = p.q; i < p.KB * KATOM; ++i) sts_u16(w_s + w_off(et, i, p.w_sbo), 0);
+    if (et < BMW)
+      for (int i = p.q; i < p.KB * KATOM; ++i) sts_u16(w_s + w_off(et, i, p.w_sbo), 0);
     const int mode = (p.q % 8 == 0 && p.n % 8 == 0) ? 2 : ((p.q % 2 == 0 && p.n % 2 == 0) ? 1 : 0);
     uint32_t rphase = 0, ophase = 0, acc_phase = 0;
     int acc = 0, cur_cb = -1, n_regen = 0;
@@ -382,11 +425,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (et == 0 && n_regen < 2) trace(p, 2 + 2 * n_regen);
         if (et == 0 && n_regen > 0) regen_request(p, cb, ar, br, obar, false);
         if (mode == 2)
-          regen_block<2>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, lane);
+          regen_block<2>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, part, lane);
         else if (mode == 1)
-          regen_block<1>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, lane);
+          regen_block<1>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, part, lane);
         else
-          regen_block<0>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, lane);
+          regen_block<0>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, part, lane);
         fence_proxy_async_smem();
         tc_fence_before();
         named_bar_sync(1, kEpiThreads);
@@ -402,12 +445,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool jok = j < p.r_dim;
       const int nrows = (int)min((int64_t)BNB, p.batch - b0);
       using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
-      OutT *yp = reinterpret_cast<OutT *>(p.y) + (int64_t)b0 * p.ldy + j;
-      for (int c32 = 0; c32 < BNB / 32; ++c32) {
+      for (int c32 = part; c32 < BNB / 32; c32 += kParts) {  // this part's 32-row groups
         uint32_t v[32];
         tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * BNB + c32 * 32), v);
         tmem_ld_wait();
         if (jok) {
+          OutT *yp = reinterpret_cast<OutT *>(p.y) + (int64_t)(b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - c32 * 32;
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
@@ -493,7 +536,7 @@ PFN_encode_tiled encode_fn() {
 }
 
 struct Layout {
-  int KB, S, RK, Nc, n_chunks, n_pass;
+  int KB, S, S_ded, RK, Nc, n_chunks, n_pass, a_res;
   uint32_t off_w, off_x, off_ar, off_br, off_bar, total;
 };
 
@@ -506,23 +549,40 @@ bool make_layout(const Geo &g, Layout *L) {
   const int64_t span = (BMW * g.q + g.n - 1) / g.n + 1 + 7;
   L->n_pass = (int)((span + 127) / 128);
   if (L->RK > 64) return false;
-  uint32_t w = (uint32_t)L->KB * kWKBlk;
-  // all of a block's regeneration operands stay resident: every pass of xf rows, all of wf
-  uint32_t arb = (uint32_t)L->n_pass * 128u * L->RK * 2;
-  uint32_t brb = (uint32_t)L->n_chunks * L->Nc * L->RK * 2;
-  uint32_t fixed = w + arb + brb + 1024 /*barriers*/ + 1024 /*alignment slack*/;
-  int S = 0;
-  for (int s = 8; s >= 2; --s)
-    if (fixed + (uint32_t)s * kXStage <= (uint32_t)kSmemBudget) { S = s; break; }
-  if (S == 0) return false;
-  L->S = S;
-  L->off_w = 0;
-  L->off_x = w;
-  L->off_ar = L->off_x + (uint32_t)S * kXStage;
-  L->off_br = L->off_ar + arb;
-  L->off_bar = (L->off_br + brb + 15) / 16 * 16;
-  L->total = L->off_bar + 512 + 1024;
-  return true;
+  const uint32_t w = (uint32_t)L->KB * kWKBlk;
+  const uint32_t fixed = w + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+  // Preferred: all of a block's regeneration operands resident (every pass of xf rows, all
+  // of wf). Fallback for very skinny n (many passes): one pass of xf rows, streamed.
+  for (int a_res : {L->n_pass, 1}) {
+    const uint32_t arb = (uint32_t)a_res * 128u * L->RK * 2;
+    const uint32_t brb = (uint32_t)L->n_chunks * L->Nc * L->RK * 2;
+    // The regeneration operands are only live while a W block is regenerated, so they
+    // alias the last x stages; the producer fills those stages only after that block's regen.
+    int S = 0;
+    for (int s = 8; s >= 2; --s)
+      if (fixed + (uint32_t)s * kXStage <= (uint32_t)kSmemBudget) { S = s; break; }
+    if (S == 0) return false;
+    const uint32_t xbytes = (uint32_t)S * kXStage;
+    const uint32_t ops = (arb + brb + 1023) / 1024 * 1024;
+    L->off_w = 0;
+    L->off_x = w;
+    if (ops > xbytes) {  // operands larger than the stage area: place them after it
+      if (fixed + xbytes + ops > (uint32_t)kSmemBudget) continue;
+      L->off_ar = L->off_x + xbytes;
+    } else {
+      L->off_ar = L->off_x + xbytes - ops;
+    }
+    L->S = S;
+    L->S_ded = (int)std::min<uint32_t>((uint32_t)S, (L->off_ar - L->off_x) / kXStage);
+    if (L->S_ded < 1) continue;
+    L->a_res = a_res;
+    L->off_br = L->off_ar + arb;
+    L->off_bar = std::max(L->off_x + xbytes, L->off_br + brb);
+    L->off_bar = (L->off_bar + 15) / 16 * 16;
+    L->total = L->off_bar + 512 + 1024;
+    if (L->total <= (uint32_t)kSmemBudget) return true;
+  }
+  return false;
 }
 
 typedef void (*KernelFn)(CUtensorMap, TcParams);
@@ -544,8 +604,8 @@ void print_trace(const std::vector<unsigned long long> &h, int grid, const TcPar
     t0 = std::min(t0, h[(size_t)c * kTraceSlots]);
     t1 = std::max(t1, h[(size_t)c * kTraceSlots + 23]);
   }
-  fprintf(stderr, "[tc trace] grid %d per_cta %d S %d KB %d span %.2f us\n", grid, p.per_cta, p.S,
-          p.KB, (t1 - t0) / 1e3);
+  fprintf(stderr, "[tc trace] grid %d per_cta %d S %d (dedicated %d) KB %d span %.2f us\n", grid,
+          p.per_cta, p.S, p.S_ded, p.KB, (t1 - t0) / 1e3);
   for (int c = 0; c < grid; c += std::max(1, grid / 6)) {
     const unsigned long long *r = &h[(size_t)c * kTraceSlots];
     auto rel = [&](int s) { return r[s] ? (double)(r[s] - t0) / 1e3 : -1.0; };
@@ -663,7 +723,8 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   p.batch = batch;
   p.q = (int)g.q; p.r_dim = (int)g.r_dim; p.rank = (int)g.rank; p.m = (int)g.m; p.n = (int)g.n;
   p.ldy = (int)g.r_dim;
-  p.KB = L.KB; p.S = L.S; p.RK = L.RK; p.Nc = L.Nc; p.n_chunks = L.n_chunks;
+  p.KB = L.KB; p.S = L.S; p.S_ded = L.S_ded; p.RK = L.RK; p.Nc = L.Nc; p.n_chunks = L.n_chunks;
+  p.a_res = L.a_res;
   p.n_cb = (int)((g.r_dim + BMW - 1) / BMW);
   p.n_bt = (int)((batch + BNB - 1) / BNB);
   p.items = p.n_cb * p.n_bt;
@@ -679,6 +740,8 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   p.arg = act_arg;
   static const int dbg_serial = getenv("DEEPTHIN_REGEN_SERIAL") != nullptr;
   p.dbg_serial = dbg_serial;
+  static const int dbg_regen = getenv("DEEPTHIN_DBG_REGEN") ? atoi(getenv("DEEPTHIN_DBG_REGEN")) : 0;
+  p.dbg_regen = dbg_regen;
   p.off_w = L.off_w; p.off_x = L.off_x; p.off_ar = L.off_ar; p.off_br = L.off_br;
   p.off_bar = L.off_bar;
   p.w_sbo = (uint32_t)L.KB * (KATOM / 8) * 128u;
