@@ -104,7 +104,9 @@ def _act_code(activation: str) -> int:
 
 def resolve_mma(mma, x: torch.Tensor, plan) -> int:
     if mma is None:
-        mma = "bf16" if x.dtype == torch.bfloat16 else "ffma"
+        # bf16 inputs take the tensor-core path where one exists (general geometries);
+        # reuse geometries run the FFMA kernel, which reads bf16 x directly
+        mma = "bf16" if (x.dtype == torch.bfloat16 and not plan.reuse_path) else "ffma"
     if mma not in ("ffma", "bf16"):
         raise ArgumentError(f"mma must be 'ffma' or 'bf16', got {mma!r}")
     return _lib.DT_MMA_BF16 if mma == "bf16" else _lib.DT_MMA_FFMA
