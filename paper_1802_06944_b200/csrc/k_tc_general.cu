@@ -49,7 +49,10 @@ using namespace ptx;
 
 // warps 0-1: TMA producer / MMA issuer; warps 2..: regeneration + epilogue, kParts warps per
 // TMEM lane quarter (warp % 4) splitting the columns between them (part = (warp - 2) / 4).
-constexpr int kParts = 3;
+#ifndef DT_TC_PARTS
+#define DT_TC_PARTS 3
+#endif
+constexpr int kParts = DT_TC_PARTS;
 constexpr int kEpiThreads = 128 * kParts;
 constexpr int kThreads = 64 + kEpiThreads;
 constexpr int BMW = 128;   // W rows (output columns) per block == UMMA M
@@ -67,6 +70,7 @@ struct TcParams {
   int q, r_dim, rank, m, n, ldy;
   int KB, S, S_ded, RK, Nc, n_chunks, n_cb, n_bt, items, per_cta;
   int a_res;  // passes of xf rows resident at once (all, or 1 = streamed per pass)
+  int csize;  // cluster size: CTAs sharing (multicasting) each x tile
   const uint8_t *xf_pk, *wf_pk;  // regeneration operands, pre-packed (dt_pack_factors)
   const float *bias;
   void *y;
@@ -138,25 +142,25 @@ __device__ __forceinline__ void scatter32(const uint32_t (&v)[32], uint32_t w_s,
                                           int jj, int i, int q, int cvalid, int jrows) {
   // predicated stores (no per-store branch / reconvergence barrier)
   if constexpr (MODE == 2) {
-    // 16-byte units (i % 8 == 0): consecutive units of one W row are 128 B apart in the
-    // core-matrix layout; the address is recomputed only when the run wraps to the next row
-    uint32_t addr = w_s + w_off(jj, i, sbo);
+    // 16-byte units (i % 8 == 0). A 32-element group wraps to the next W row at most once
+    // (q >= 32): units t < wrap stay in row jj (128 B apart in the core-matrix layout), the
+    // rest continue in row jj+1 from column i + 8*t - q. Every unit's address and predicate
+    // is computed independently (no serial chain across units).
+    const int wrap = (q - i + 7) >> 3;  // units left in row jj
+    const uint32_t a0 = w_s + w_off((uint32_t)jj, (uint32_t)i, sbo);
+    const uint32_t a1 = w_s + w_off((uint32_t)(jj + 1), (uint32_t)(i + 8 * wrap - q), sbo);
+    const bool r0 = (uint32_t)jj < (uint32_t)jrows, r1 = (uint32_t)(jj + 1) < (uint32_t)jrows;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const uint32_t ok = (8 * t < cvalid) & ((uint32_t)jj < (uint32_t)jrows);
+      const bool second = t >= wrap;
+      const uint32_t addr = second ? a1 + 128u * (uint32_t)(t - wrap) : a0 + 128u * (uint32_t)t;
+      const uint32_t ok = (8 * t < cvalid) & (second ? r1 : r0);
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
           "@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(addr),
           "r"(pack_bf16(v[8 * t], v[8 * t + 1])), "r"(pack_bf16(v[8 * t + 2], v[8 * t + 3])),
           "r"(pack_bf16(v[8 * t + 4], v[8 * t + 5])), "r"(pack_bf16(v[8 * t + 6], v[8 * t + 7])),
           "r"(ok));
-      i += 8;
-      addr += 128u;
-      if (i >= q) {
-        i -= q;
-        ++jj;
-        addr = w_s + w_off(jj, i, sbo);
-      }
     }
   } else if constexpr (MODE == 1) {
 #pragma unroll
@@ -213,73 +217,100 @@ __device__ __forceinline__ void regen_request(const TcParams &p, int cb, uint8_t
   if (need_b) bulk_load(br, p.wf_pk, b_bytes, obar);
 }
 
-// Regenerate the W block of column block cb into shared memory (the 128 epilogue threads).
-//
-// Steps (pass, chunk): pass = 128 aux rows starting at a_first + 128*pass, chunk = Nc aux
-// columns. Operands are resident (regen_request, issued ahead); regeneration MMAs are
-// double-buffered in TMEM (columns [0, Nc) / [Nc, 2Nc)) so step s+1's MMA runs while
-// step s is read back and scattered.
-template <int MODE>
-__device__ void regen_block(const TcParams &p, int cb, uint32_t w_s, uint8_t *ar, uint8_t *br,
-                            uint64_t *rbar, uint32_t &rphase, uint64_t *obar, uint32_t &ophase,
-                            uint32_t tbase, int et, int wq, int part, int lane) {
-  const BlockRows b = block_rows(p, cb);
-  const int q = p.q, n = p.n;
+// How many regeneration steps TMEM holds at once: the first `slots` steps' MMAs are issued
+// up front and each read-back frees a slot for step s + slots, so MMA -> commit -> mbarrier
+// round trips overlap the read-backs. A streamed pass of xf rows (very skinny n) must first
+// replace the resident one: one step at a time.
+__device__ __forceinline__ int regen_slots(const TcParams &p, const BlockRows &b) {
   const int n_steps = b.n_pass * p.n_chunks;
+  const bool stream = p.a_res < b.n_pass;
+  return (stream || p.dbg_serial) ? 1 : min(4, min(n_steps, 512 / p.Nc));
+}
+
+// Regeneration MMAs of column block cb — issued by the MMA warp's elected lane (issuing
+// tcgen05 from a lane of a divergent epilogue warp measured ~5x slower).
+// Steps (pass, chunk): pass = 128 aux rows from a_first + 128*pass, chunk = Nc aux columns.
+// rbar[slot]: MMA -> read-back ("step done"); rfree[slot]: read-back -> MMA ("slot free").
+__device__ void regen_issue(const TcParams &p, int cb, uint8_t *ar, uint8_t *br, uint64_t *rbar,
+                            uint64_t *rfree, uint32_t &fphase, uint64_t *obar, uint32_t &ophase,
+                            uint32_t tbase) {
+  const BlockRows b = block_rows(p, cb);
+  const int n_steps = b.n_pass * p.n_chunks;
+  const bool stream = p.a_res < b.n_pass;
+  const int slots = regen_slots(p, b);
   const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
-  const int L = 32 * wq + lane;  // TMEM lane (= aux row offset within the pass)
   const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)p.Nc);
   const uint32_t ar_s = smem_u32(ar), br_s = smem_u32(br);
-
-  const bool stream = p.a_res < b.n_pass;  // one pass of xf rows resident, reloaded per pass
-  auto issue_mma = [&](int s) {  // et == 0 only
-    const int pass = s / p.n_chunks, chunk = s % p.n_chunks;
+  mbar_wait(obar, ophase);  // operands landed (regen_request)
+  ophase ^= 1;
+  trace(p, 24);
+  for (int s = 0; s < n_steps; ++s) {
+    const int slot = s % slots, pass = s / p.n_chunks, chunk = s % p.n_chunks;
+    if (s >= slots) {  // the read-back of step s - slots has released this TMEM slot
+      mbar_wait(&rfree[slot], (fphase >> slot) & 1u);
+      fphase ^= 1u << slot;
+    }
+    if (stream && s > 0 && chunk == 0) {  // replace the resident pass of xf rows
+      const uint32_t bytes = 16u * sbo;
+      mbar_arrive_expect_tx(obar, bytes);
+      bulk_load(ar, p.xf_pk + (size_t)((b.a_first >> 3) + 16 * pass) * sbo, bytes, obar);
+      mbar_wait(obar, ophase);
+      ophase ^= 1;
+    }
+    tc_fence_after();
     const uint32_t a_s = ar_s + (stream ? 0u : (uint32_t)pass * 16u * sbo);
     const uint32_t b_s = br_s + (uint32_t)chunk * (uint32_t)(p.Nc / 8) * sbo;
     for (int kk = 0; kk < p.RK / 16; ++kk) {
       uint64_t ad = smem_desc(a_s + kk * 256u, 128u, sbo, SL_NONE);
       uint64_t bd = smem_desc(b_s + kk * 256u, 128u, sbo, SL_NONE);
-      mma_bf16_ss(tbase + (uint32_t)((s & 1) * p.Nc), ad, bd, idesc, kk > 0);
+      mma_bf16_ss(tbase + (uint32_t)(slot * p.Nc), ad, bd, idesc, kk > 0);
     }
-    mma_commit(rbar);
-  };
-  if (et == 0) {
-    mbar_wait(obar, ophase);
-    trace(p, 24);
-    tc_fence_after();
-    issue_mma(0);
+    mma_commit(&rbar[slot]);  // one mbarrier per TMEM slot: one phase in flight each
+    if (s == slots - 1) trace(p, 39);
   }
-  ophase ^= 1;
+}
 
+// Read back the regeneration steps of column block cb (the epilogue warps): TMEM -> bf16 ->
+// scatter of every element f -> (jj, i) = divmod(f - j0*q, q) into the W block.
+template <int MODE>
+__device__ void regen_readout(const TcParams &p, int cb, uint32_t w_s, uint64_t *rbar,
+                              uint32_t &rphase, uint64_t *rfree, uint32_t tbase, int et, int wq,
+                              int part, int lane) {
+  const BlockRows b = block_rows(p, cb);
+  const int q = p.q, n = p.n;
+  const int n_steps = b.n_pass * p.n_chunks;
+  const int slots = regen_slots(p, b);
+  const int L = 32 * wq + lane;  // TMEM lane (= aux row offset within the pass)
   for (int s = 0; s < n_steps; ++s) {
     const int pass = s / p.n_chunks, chunk = s % p.n_chunks;
     const int c0 = chunk * p.Nc;
     const int cols = min(p.Nc, n - c0);
-    mbar_wait(rbar, rphase);
+    const int slot = s % slots;
+    mbar_wait(&rbar[slot], (rphase >> slot) & 1u);  // one parity bit per slot
+    rphase ^= 1u << slot;
     if (et == 0 && s < 4) trace(p, 25 + s);
-    rphase ^= 1;
     tc_fence_after();
-    // the next step's MMA goes to the other TMEM buffer and overlaps this read-back, unless it
-    // needs a streamed pass of xf rows that must first replace the current one
-    const bool next_new_pass = stream && (s + 1) % p.n_chunks == 0;
-    const bool early = !p.dbg_serial && !next_new_pass;
-    if (early && et == 0 && s + 1 < n_steps) issue_mma(s + 1);
     const int a = b.a_first + 128 * pass + L;
     const int a_warp = b.a_first + 128 * pass + 32 * wq;  // this warp's rows: a_warp .. +31
-    const uint32_t tcol = tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)((s & 1) * p.Nc);
+    const uint32_t tcol = tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(slot * p.Nc);
     if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo && p.dbg_regen != 3) {  // skip all-invalid warps
-      // this warp's column groups: part, part + kParts, ... (32 columns each); the next
-      // group's TMEM load is in flight while the current group is scattered
+      // this warp's column groups: part, part + kParts, ... (32 columns each)
       const int f0 = (int)((int64_t)a * n + c0 + 32 * part - b.fbeg);
       int jj = f0 >= 0 ? f0 / q : -((-f0 + q - 1) / q);
       int i = f0 - jj * q;
       const bool row_ok = a >= b.a_lo && a <= b.a_hi;
-      for (int col0 = 32 * part; col0 < p.Nc; col0 += 32 * kParts) {
+      int g = 0;
+      for (int col0 = 32 * part; col0 < p.Nc; col0 += 32 * kParts, ++g) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tcol + (uint32_t)col0, v);
         tmem_ld_wait();
+        if (p.trace && et == 0 && s == 0 && g < 3) {
+          asm volatile("" ::"r"(v[0] ^ v[31]));
+          trace(p, 32 + 2 * g);
+        }
         if (row_ok && col0 < cols && p.dbg_regen != 1)
           scatter32<MODE>(v, w_s, p.w_sbo, jj, i, q, cols - col0, b.jrows);
+        if (p.trace && et == 0 && s == 0 && g < 3) trace(p, 33 + 2 * g);
         i += 32 * kParts;
         while (i >= q) { i -= q; ++jj; }
       }
@@ -287,22 +318,8 @@ __device__ void regen_block(const TcParams &p, int cb, uint32_t w_s, uint8_t *ar
     if (et == 0 && s == 0) trace(p, 31);
     tc_fence_before();
     named_bar_sync(1, kEpiThreads);
-    if (!early && s + 1 < n_steps) {
-      if (next_new_pass) {  // all MMAs reading the old pass are complete (rbar waited)
-        if (et == 0) {
-          const uint32_t bytes = 16u * sbo;
-          mbar_arrive_expect_tx(obar, bytes);
-          bulk_load(ar, p.xf_pk + (size_t)((b.a_first >> 3) + 16 * ((s + 1) / p.n_chunks)) * sbo,
-                    bytes, obar);
-          mbar_wait(obar, ophase);
-        }
-        ophase ^= 1;
-      }
-      if (et == 0) {
-        tc_fence_after();
-        issue_mma(s + 1);
-      }
-    }
+    if (et == 0 && s == 0) trace(p, 38);
+    if (et == 0 && s + slots < n_steps) mbar_arrive(&rfree[slot]);  // slot reusable
   }
 }
 
@@ -315,29 +332,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *xst = smem + p.off_x;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
-  uint64_t *bready = tempty + 2, *rbar = bready + 1, *obar = rbar + 1;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(obar + 1);
+  uint64_t *bready = tempty + 2, *rbar = bready + 1, *rfree = rbar + 4, *obar = rfree + 4;
+  uint64_t *cregen = obar + 1;  // "every CTA of my cluster finished regenerating this block"
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(cregen + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int item_beg = blockIdx.x * p.per_cta;
+  // Clusters of p.csize CTAs own consecutive column blocks and walk the same batch tiles:
+  // each CTA TMA-loads 1/csize of every x stage and multicasts it to the whole cluster.
+  // Work items are cluster items (column-block group, batch tile).
+  const uint32_t crank = p.csize > 1 ? cluster_ctarank() : 0u;
+  const uint16_t cmask = (uint16_t)((1u << p.csize) - 1u);
+  const int cid = blockIdx.x / p.csize;
+  const int item_beg = cid * p.per_cta;
   const int item_end = min(p.items, item_beg + p.per_cta);
+  auto cb_of = [&](int it) { return (it / p.n_bt) * p.csize + (int)crank; };
 
   if (threadIdx.x == 0) {
     trace(p, 0);
-    for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], p.csize); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiThreads); }
     mbar_init(bready, 1);
-    mbar_init(rbar, 1);
+    for (int s = 0; s < 4; ++s) { mbar_init(&rbar[s], 1); mbar_init(&rfree[s], 1); }
     mbar_init(obar, 1);
+    mbar_init(cregen, p.csize);
     fence_mbar_init();
     // the first block's regeneration operands start streaming in before anything else
     if (item_beg < item_end)
-      regen_request(p, item_beg / p.n_bt, smem + p.off_ar, smem + p.off_br, obar, true);
+      regen_request(p, cb_of(item_beg), smem + p.off_ar, smem + p.off_br, obar, true);
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_x);
   if (warp == 1) tmem_alloc(tslot, kTmemCols);
   tc_fence_before();
   __syncthreads();
+  if (p.csize > 1) cluster_sync();  // peers' barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) trace(p, 1);
@@ -348,37 +375,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0, cur_cb = -1, n_cbs = 0;
       uint32_t phase = 0;
       bool regen_pending = false;
+      const uint32_t slice_rows = BNB / p.csize, slice_bytes = kXStage / p.csize;
       for (int it = item_beg; it < item_end; ++it) {
         const int32_t b0 = (it % p.n_bt) * BNB;
-        if (it / p.n_bt != cur_cb) {
-          cur_cb = it / p.n_bt;
+        if (cb_of(it) != cur_cb) {
+          cur_cb = cb_of(it);
           ++n_cbs;
           regen_pending = true;
         }
         for (int kb = 0; kb < p.KB; ++kb) {
-          if (stage >= p.S_ded && regen_pending) {  // stage aliases the regen operands
-            mbar_wait(bready, (uint32_t)(n_cbs - 1) & 1u);
+          if ((stage >= p.S_ded || p.dbg_regen == 4) && regen_pending) {
+            // this stage aliases the regeneration operands of every CTA it multicasts into
+            mbar_wait_sleepy(cregen, (uint32_t)(n_cbs - 1) & 1u);
             regen_pending = false;
           }
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);  // consumed by every CTA of the cluster
           mbar_arrive_expect_tx(&full[stage], kXStage);
-          tma_load_2d(xst + (size_t)stage * kXStage, &tm_x, &full[stage], kb * KATOM, b0);
+          if (p.csize == 1)
+            tma_load_2d(xst + (size_t)stage * kXStage, &tm_x, &full[stage], kb * KATOM, b0);
+          else
+            tma_load_2d_mc(xst + (size_t)stage * kXStage + crank * slice_bytes, &tm_x,
+                           &full[stage], kb * KATOM, b0 + (int32_t)(crank * slice_rows), cmask);
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
       }
       trace(p, 22);
     }
+    __syncwarp();  // lanes 1-31 wait here: no lane reaches the aligned barriers below early
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(BMW, BNB);
       const uint32_t w_s = smem_u32(wblk), x_s = smem_u32(xst);
       int stage = 0, acc = 0, cur_cb = -1;
-      uint32_t phase = 0, acc_phase = 0, bphase = 0;
+      uint32_t phase = 0, acc_phase = 0, bphase = 0, fphase = 0, ophase = 0;
+      uint8_t *ar = smem + p.off_ar, *br = smem + p.off_br;
       for (int it = item_beg; it < item_end; ++it) {
-        const int cb = it / p.n_bt;
+        const int cb = cb_of(it);
         if (cb != cur_cb) {
-          mbar_wait(bready, bphase);
+          // regenerate this block's W on the tensor cores, then wait for the read-back
+          regen_issue(p, cb, ar, br, rbar, rfree, fphase, obar, ophase, tbase);
+          mbar_wait_sleepy(bready, bphase);
           bphase ^= 1;
           cur_cb = cb;
         }
@@ -395,7 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint64_t bd = smem_desc(x_s + stage * kXStage + k * 32, 16, 1024, SL_SW128);
             mma_bf16_ss(d, ad, bd, idesc, (kb | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          if (p.csize == 1)
+            mma_commit(&empty[stage]);
+          else  // every producer of the cluster multicasts into this stage
+            mma_commit_mc(&empty[stage], cmask);
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
@@ -403,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+    __syncwarp();  // reconverge before tcgen05.dealloc (.sync.aligned)
   } else {
     // ---------------- regeneration + epilogue (warps 2-9) ----------------
     const int et = threadIdx.x - 64;
@@ -414,26 +455,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     // one-time zeroing of the W K-padding [q, KB*64)
     if (et < BMW)
       for (int i = p.q; i < p.KB * KATOM; ++i) sts_u16(w_s + w_off(et, i, p.w_sbo), 0);
-    const int mode = (p.q % 8 == 0 && p.n % 8 == 0) ? 2 : ((p.q % 2 == 0 && p.n % 2 == 0) ? 1 : 0);
-    uint32_t rphase = 0, ophase = 0, acc_phase = 0;
+    const int mode = (p.q % 8 == 0 && p.n % 8 == 0 && p.q >= 32)
+                         ? 2
+                         : ((p.q % 2 == 0 && p.n % 2 == 0) ? 1 : 0);
+    uint32_t rphase = 0, acc_phase = 0;
     int acc = 0, cur_cb = -1, n_regen = 0;
     float bias_j = 0.f;
     for (int it = item_beg; it < item_end; ++it) {
-      const int cb = it / p.n_bt, bt = it % p.n_bt;
+      const int cb = cb_of(it), bt = it % p.n_bt;
       const int j = cb * BMW + jl;
       if (cb != cur_cb) {
         if (et == 0 && n_regen < 2) trace(p, 2 + 2 * n_regen);
         if (et == 0 && n_regen > 0) regen_request(p, cb, ar, br, obar, false);
         if (mode == 2)
-          regen_block<2>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, part, lane);
+          regen_readout<2>(p, cb, w_s, rbar, rphase, rfree, tbase, et, wq, part, lane);
         else if (mode == 1)
-          regen_block<1>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, part, lane);
+          regen_readout<1>(p, cb, w_s, rbar, rphase, rfree, tbase, et, wq, part, lane);
         else
-          regen_block<0>(p, cb, w_s, ar, br, rbar, rphase, obar, ophase, tbase, et, wq, part, lane);
+          regen_readout<0>(p, cb, w_s, rbar, rphase, rfree, tbase, et, wq, part, lane);
         fence_proxy_async_smem();
         tc_fence_before();
         named_bar_sync(1, kEpiThreads);
-        if (et == 0) mbar_arrive(bready);
+        if (et == 0) {
+          mbar_arrive(bready);
+          // every cluster CTA may now multicast x into the stages aliasing my operands
+          if (p.csize == 1)
+            mbar_arrive(cregen);
+          else
+            for (int r = 0; r < p.csize; ++r) mbar_arrive_remote(cregen, (uint32_t)r);
+        }
         if (et == 0 && n_regen < 2) trace(p, 3 + 2 * n_regen);
         ++n_regen;
         cur_cb = cb;
@@ -472,9 +522,311 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) trace(p, 23);
+  if (p.csize > 1) cluster_sync();  // no CTA leaves while peers may still signal / multicast to it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tbase, kTmemCols);
+  }
+}
+
+// =============================================================================================
+// CTA-pair variant (tcgen05 cta_group::2). A cluster of two CTAs owns two consecutive column
+// blocks (M = 256 output columns, 128 per CTA, each CTA regenerating its own W block) and
+// 256-row batch tiles of which each CTA TMA-loads 128 rows: per-SM x traffic halves and the
+// 2-SM MMA (256 x 256 x 16) runs at the full per-SM rate, with seven 16 KB x stages in flight.
+// The leader (cluster rank 0) issues every MMA — regeneration (M = 256: both CTAs' aux rows
+// against wf^T, whose N rows are split across the pair) and main loop — and its commits
+// multicast to both CTAs. Peer -> leader signals (operands landed, slot free, block
+// regenerated, accumulator drained) are remote mbarrier arrivals.
+// =============================================================================================
+
+__device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t crank) {
+  if (crank == 0)
+    mbar_arrive(bar);
+  else
+    mbar_arrive_remote(bar, 0);
+}
+
+// Steps of a pair regeneration: the pair's passes cover both CTAs' aux rows.
+__device__ __forceinline__ int pair_passes(const TcParams &p, int cb_leader) {
+  return max(block_rows(p, cb_leader).n_pass, block_rows(p, cb_leader + 1).n_pass);
+}
+
+// Own xf rows (every pass) and this CTA's half of each wf^T chunk (rows [crank*Nc/2, +Nc/2)).
+__device__ __forceinline__ void regen_request_pair(const TcParams &p, int cb, uint32_t crank,
+                                                   uint8_t *ar, uint8_t *br, uint64_t *obar,
+                                                   bool need_b) {
+  const BlockRows b = block_rows(p, cb);
+  const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
+  const uint32_t a_bytes = (uint32_t)pair_passes(p, cb - (int)crank) * 16u * sbo;
+  const uint32_t half = (uint32_t)(p.Nc / 16) * sbo;  // Nc/2 rows of one chunk
+  mbar_arrive_expect_tx(obar, a_bytes + (need_b ? half * (uint32_t)p.n_chunks : 0u));
+  bulk_load(ar, p.xf_pk + (size_t)(b.a_first >> 3) * sbo, a_bytes, obar);
+  if (need_b)
+    for (int ch = 0; ch < p.n_chunks; ++ch)
+      bulk_load(br + ch * half, p.wf_pk + (size_t)ch * 2u * half + crank * half, half, obar);
+}
+
+template <int MODE>
+__device__ void regen_readout_pair(const TcParams &p, int cb, uint32_t crank, uint32_t w_s,
+                                   uint64_t *rbar, uint32_t &rphase, uint64_t *rfree,
+                                   uint32_t tbase, int et, int wq, int part, int lane) {
+  const BlockRows b = block_rows(p, cb);
+  const int q = p.q, n = p.n;
+  const int n_steps = pair_passes(p, cb - (int)crank) * p.n_chunks;
+  const int slots = min(4, min(n_steps, 512 / p.Nc));
+  const int L = 32 * wq + lane;
+  for (int s = 0; s < n_steps; ++s) {
+    const int pass = s / p.n_chunks, chunk = s % p.n_chunks;
+    const int c0 = chunk * p.Nc;
+    const int cols = min(p.Nc, n - c0);
+    const int slot = s % slots;
+    mbar_wait(&rbar[slot], (rphase >> slot) & 1u);
+    rphase ^= 1u << slot;
+    if (et == 0 && s < 4) trace(p, 25 + s);
+    tc_fence_after();
+    const int a = b.a_first + 128 * pass + L;
+    const int a_warp = b.a_first + 128 * pass + 32 * wq;
+    const uint32_t tcol = tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(slot * p.Nc);
+    if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo) {
+      const int f0 = (int)((int64_t)a * n + c0 + 32 * part - b.fbeg);
+      int jj = f0 >= 0 ? f0 / q : -((-f0 + q - 1) / q);
+      int i = f0 - jj * q;
+      const bool row_ok = a >= b.a_lo && a <= b.a_hi;
+      for (int col0 = 32 * part; col0 < p.Nc; col0 += 32 * kParts) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tcol + (uint32_t)col0, v);
+        tmem_ld_wait();
+        if (row_ok && col0 < cols)
+          scatter32<MODE>(v, w_s, p.w_sbo, jj, i, q, cols - col0, b.jrows);
+        i += 32 * kParts;
+        while (i >= q) { i -= q; ++jj; }
+      }
+    }
+    tc_fence_before();
+    named_bar_sync(1, kEpiThreads);
+    if (et == 0 && s + slots < n_steps) arrive_leader(&rfree[slot], crank);
+  }
+}
+
+template <int YDT, int ACT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_general_pair(const __grid_constant__ CUtensorMap tm_x, const TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t *wblk = smem + p.off_w;
+  uint8_t *xst = smem + p.off_x;
+  uint8_t *ar = smem + p.off_ar, *br = smem + p.off_br;
+  const uint32_t stage_bytes = kXStage / 2;  // this CTA's 128 of the tile's 256 rows
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+  uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
+  uint64_t *bready = tempty + 2, *rbar = bready + 1, *rfree = rbar + 4, *obar = rfree + 4;
+  uint64_t *cregen = obar + 1, *pobar = cregen + 1;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(pobar + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int item_beg = (blockIdx.x / 2) * p.per_cta;
+  const int item_end = min(p.items, item_beg + p.per_cta);
+  auto cb_of = [&](int it) { return (it / p.n_bt) * 2 + (int)crank; };
+
+  if (threadIdx.x == 0) {
+    trace(p, 0);
+    for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2); }
+    mbar_init(bready, 2);
+    for (int s = 0; s < 4; ++s) { mbar_init(&rbar[s], 1); mbar_init(&rfree[s], 2); }
+    mbar_init(obar, 1);
+    mbar_init(cregen, 1);
+    mbar_init(pobar, 1);
+    fence_mbar_init();
+    if (item_beg < item_end) regen_request_pair(p, cb_of(item_beg), crank, ar, br, obar, true);
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_x);
+  if (warp == 1) tmem_alloc_pair(tslot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) trace(p, 1);
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own 128 rows of each tile) ----------------
+    if (lane == 0) {
+      int stage = 0, cur_cb = -1, n_cbs = 0;
+      uint32_t phase = 0;
+      bool regen_pending = false;
+      for (int it = item_beg; it < item_end; ++it) {
+        const int32_t b0 = (it % p.n_bt) * BNB + (int32_t)crank * (BNB / 2);
+        if (cb_of(it) != cur_cb) {
+          cur_cb = cb_of(it);
+          ++n_cbs;
+          regen_pending = true;
+        }
+        for (int kb = 0; kb < p.KB; ++kb) {
+          if (stage >= p.S_ded && regen_pending) {  // stage aliases my regeneration operands
+            mbar_wait_sleepy(cregen, (uint32_t)(n_cbs - 1) & 1u);
+            regen_pending = false;
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);  // both halves
+          tma_load_2d_pair(xst + (size_t)stage * stage_bytes, &tm_x, &full[stage], kb * KATOM, b0);
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+      }
+      trace(p, 22);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader only; 2-SM MMAs) ----------------
+      const uint32_t idesc = idesc_bf16_f32(2 * BMW, BNB);
+      const uint32_t idesc_r = idesc_bf16_f32(2 * BMW, (uint32_t)p.Nc);
+      const uint32_t w_s = smem_u32(wblk), x_s = smem_u32(xst);
+      const uint32_t ar_s = smem_u32(ar), br_s = smem_u32(br);
+      const uint32_t sbo = (uint32_t)(p.RK / 8) * 128u;
+      const uint32_t half = (uint32_t)(p.Nc / 16) * sbo;
+      int stage = 0, acc = 0, cur_cb = -1;
+      uint32_t phase = 0, acc_phase = 0, bphase = 0, fphase = 0, ophase = 0;
+      for (int it = item_beg; it < item_end; ++it) {
+        const int cb = cb_of(it);
+        if (cb != cur_cb) {
+          // regeneration of both W blocks: own operands + the peer's (relayed)
+          mbar_wait(obar, ophase);
+          mbar_wait(pobar, ophase);
+          ophase ^= 1;
+          trace(p, 24);
+          const int n_steps = pair_passes(p, cb) * p.n_chunks;
+          const int slots = min(4, min(n_steps, 512 / p.Nc));
+          for (int s = 0; s < n_steps; ++s) {
+            const int slot = s % slots, pass = s / p.n_chunks, chunk = s % p.n_chunks;
+            if (s >= slots) {
+              mbar_wait(&rfree[slot], (fphase >> slot) & 1u);
+              fphase ^= 1u << slot;
+            }
+            tc_fence_after();
+            for (int kk = 0; kk < p.RK / 16; ++kk) {
+              uint64_t ad = smem_desc(ar_s + (uint32_t)pass * 16u * sbo + kk * 256u, 128u, sbo, SL_NONE);
+              uint64_t bd = smem_desc(br_s + (uint32_t)chunk * half + kk * 256u, 128u, sbo, SL_NONE);
+              mma_bf16_ss_pair(tbase + (uint32_t)(slot * p.Nc), ad, bd, idesc_r, kk > 0);
+            }
+            mma_commit_pair(&rbar[slot]);
+          }
+          mbar_wait_sleepy(bready, bphase);  // both CTAs' W blocks are in shared memory
+          bphase ^= 1;
+          cur_cb = cb;
+        }
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * BNB);
+        for (int kb = 0; kb < p.KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < KATOM / 16; ++k) {
+            uint64_t ad = smem_desc(w_s + (uint32_t)(kb * 4 + k) * 256u, 128u, p.w_sbo, SL_NONE);
+            uint64_t bd = smem_desc(x_s + stage * stage_bytes + k * 32, 16, 1024, SL_SW128);
+            mma_bf16_ss_pair(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit_pair(&empty[stage]);
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc]);
+        trace(p, 14 + min(7, it - item_beg));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    } else if (lane == 0) {
+      // peer: relay "my regeneration operands landed" to the leader, once per block
+      int cur_cb = -1;
+      uint32_t ophase = 0;
+      for (int it = item_beg; it < item_end; ++it) {
+        if (cb_of(it) == cur_cb) continue;
+        cur_cb = cb_of(it);
+        mbar_wait_sleepy(obar, ophase);
+        ophase ^= 1;
+        mbar_arrive_remote(pobar, 0);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- regeneration read-back + epilogue (both CTAs) ----------------
+    const int et = threadIdx.x - 64;
+    const int wq = warp & 3;
+    const int part = (warp - 2) / 4;
+    const int jl = 32 * wq + lane;
+    const uint32_t w_s = smem_u32(wblk);
+    if (et < BMW)
+      for (int i = p.q; i < p.KB * KATOM; ++i) sts_u16(w_s + w_off(et, i, p.w_sbo), 0);
+    const int mode = (p.q % 8 == 0 && p.n % 8 == 0 && p.q >= 32)
+                         ? 2
+                         : ((p.q % 2 == 0 && p.n % 2 == 0) ? 1 : 0);
+    uint32_t rphase = 0, acc_phase = 0;
+    int acc = 0, cur_cb = -1, n_regen = 0;
+    float bias_j = 0.f;
+    for (int it = item_beg; it < item_end; ++it) {
+      const int cb = cb_of(it), bt = it % p.n_bt;
+      const int j = cb * BMW + jl;
+      if (cb != cur_cb) {
+        if (et == 0 && n_regen < 2) trace(p, 2 + 2 * n_regen);
+        if (et == 0 && n_regen > 0) regen_request_pair(p, cb, crank, ar, br, obar, false);
+        if (mode == 2)
+          regen_readout_pair<2>(p, cb, crank, w_s, rbar, rphase, rfree, tbase, et, wq, part, lane);
+        else if (mode == 1)
+          regen_readout_pair<1>(p, cb, crank, w_s, rbar, rphase, rfree, tbase, et, wq, part, lane);
+        else
+          regen_readout_pair<0>(p, cb, crank, w_s, rbar, rphase, rfree, tbase, et, wq, part, lane);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+          arrive_leader(bready, crank);  // the leader's MMAs read both W blocks
+          mbar_arrive(cregen);           // my producer may fill the aliased stages
+        }
+        if (et == 0 && n_regen < 2) trace(p, 3 + 2 * n_regen);
+        ++n_regen;
+        cur_cb = cb;
+        bias_j = (p.bias && j < p.r_dim) ? p.bias[j] : 0.f;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int b0 = bt * BNB;
+      const bool jok = j < p.r_dim;
+      const int nrows = (int)min((int64_t)BNB, p.batch - b0);
+      using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
+      for (int c32 = part; c32 < BNB / 32; c32 += kParts) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * BNB + c32 * 32), v);
+        tmem_ld_wait();
+        if (jok) {
+          OutT *yp = reinterpret_cast<OutT *>(p.y) + (int64_t)(b0 + 32 * c32) * p.ldy + j;
+          const int rmax = nrows - c32 * 32;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            if (r < rmax) {
+              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+            }
+            yp += p.ldy;
+          }
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(1, kEpiThreads);  // every TMEM read of this accumulator has completed
+      if (et == 0) arrive_leader(&tempty[acc], crank);
+      if (et == 0) trace(p, 6 + min(7, it - item_beg));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) trace(p, 23);
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tbase, kTmemCols);
   }
 }
 
@@ -540,7 +892,10 @@ struct Layout {
   uint32_t off_w, off_x, off_ar, off_br, off_bar, total;
 };
 
-bool make_layout(const Geo &g, Layout *L) {
+// pair: the cta_group::2 kernel (16 KB x stages = this CTA's half of a 256-row tile; half of
+// each wf^T chunk; all passes resident — no streamed fallback).
+bool make_layout(const Geo &g, Layout *L, bool pair = false) {
+  const uint32_t kStage = pair ? kXStage / 2 : kXStage;
   L->KB = (int)((g.q + KATOM - 1) / KATOM);
   L->RK = (int)((g.rank + 15) / 16 * 16);
   L->n_chunks = (int)((g.n + 255) / 256);
@@ -554,15 +909,16 @@ bool make_layout(const Geo &g, Layout *L) {
   // Preferred: all of a block's regeneration operands resident (every pass of xf rows, all
   // of wf). Fallback for very skinny n (many passes): one pass of xf rows, streamed.
   for (int a_res : {L->n_pass, 1}) {
+    if (pair && a_res != L->n_pass) break;
     const uint32_t arb = (uint32_t)a_res * 128u * L->RK * 2;
-    const uint32_t brb = (uint32_t)L->n_chunks * L->Nc * L->RK * 2;
+    const uint32_t brb = (uint32_t)L->n_chunks * L->Nc * L->RK * 2 / (pair ? 2 : 1);
     // The regeneration operands are only live while a W block is regenerated, so they
     // alias the last x stages; the producer fills those stages only after that block's regen.
     int S = 0;
     for (int s = 8; s >= 2; --s)
-      if (fixed + (uint32_t)s * kXStage <= (uint32_t)kSmemBudget) { S = s; break; }
+      if (fixed + (uint32_t)s * kStage <= (uint32_t)kSmemBudget) { S = s; break; }
     if (S == 0) return false;
-    const uint32_t xbytes = (uint32_t)S * kXStage;
+    const uint32_t xbytes = (uint32_t)S * kStage;
     const uint32_t ops = (arb + brb + 1023) / 1024 * 1024;
     L->off_w = 0;
     L->off_x = w;
@@ -573,7 +929,7 @@ bool make_layout(const Geo &g, Layout *L) {
       L->off_ar = L->off_x + xbytes - ops;
     }
     L->S = S;
-    L->S_ded = (int)std::min<uint32_t>((uint32_t)S, (L->off_ar - L->off_x) / kXStage);
+    L->S_ded = (int)std::min<uint32_t>((uint32_t)S, (L->off_ar - L->off_x) / kStage);
     if (L->S_ded < 1) continue;
     L->a_res = a_res;
     L->off_br = L->off_ar + arb;
@@ -598,11 +954,24 @@ KernelFn pick_act(int act) {
   }
 }
 
+template <int YDT>
+KernelFn pick_act_pair(int act) {
+  switch (act) {
+    case DT_ACT_RELU: return k_tc_general_pair<YDT, DT_ACT_RELU>;
+    case DT_ACT_SIGMOID: return k_tc_general_pair<YDT, DT_ACT_SIGMOID>;
+    case DT_ACT_TANH: return k_tc_general_pair<YDT, DT_ACT_TANH>;
+    case DT_ACT_CLIPPED_RELU: return k_tc_general_pair<YDT, DT_ACT_CLIPPED_RELU>;
+    default: return k_tc_general_pair<YDT, DT_ACT_IDENTITY>;
+  }
+}
+
 void print_trace(const std::vector<unsigned long long> &h, int grid, const TcParams &p) {
   unsigned long long t0 = ~0ull, t1 = 0;
   for (int c = 0; c < grid; ++c) {
     t0 = std::min(t0, h[(size_t)c * kTraceSlots]);
-    t1 = std::max(t1, h[(size_t)c * kTraceSlots + 23]);
+    // the last stamp of any role (slot 23 is taken right after a BAR.SYNC.DEFER_BLOCKING and
+    // can precede the epilogue's final stores)
+    for (int s = 0; s < kTraceSlots; ++s) t1 = std::max(t1, h[(size_t)c * kTraceSlots + s]);
   }
   fprintf(stderr, "[tc trace] grid %d per_cta %d S %d (dedicated %d) KB %d span %.2f us\n", grid,
           p.per_cta, p.S, p.S_ded, p.KB, (t1 - t0) / 1e3);
@@ -621,7 +990,10 @@ void print_trace(const std::vector<unsigned long long> &h, int grid, const TcPar
             "step0 end %.2f\n",
             rel(22), rel(23), rel(24), rel(25), rel(26), rel(27), rel(28), rel(29), rel(30),
             rel(31));
-    fprintf(stderr, "        step0 (thread 64): ld cycles %llu scatter cycles %llu\n", r[32], r[33]);
+    fprintf(stderr,
+            "        step0 (thread 64): ld0 %.3f sc0 %.3f ld1 %.3f sc1 %.3f ld2 %.3f sc2 %.3f "
+            "pre-bar %.3f post-bar %.3f | regen MMAs issued %.3f\n",
+            rel(32), rel(33), rel(34), rel(35), rel(36), rel(37), rel(31), rel(38), rel(39));
   }
 }
 
@@ -710,7 +1082,26 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)g.q, (cuuint64_t)batch};
   cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-  cuuint32_t box[2] = {KATOM, BNB};
+  // Cluster size: consecutive column blocks share every x tile through TMA multicast, so L2
+  // serves each x tile once per cluster instead of once per CTA (DEEPTHIN_TC_CLUSTER
+  // overrides; needs n_cb % csize == 0).
+  const int n_cb = (int)((g.r_dim + BMW - 1) / BMW);
+  // Preferred: the CTA-pair (cta_group::2) kernel when column blocks pair up and every
+  // regeneration pass fits (DEEPTHIN_TC_PAIR=0 disables).
+  static const int want_pair = getenv("DEEPTHIN_TC_PAIR") ? atoi(getenv("DEEPTHIN_TC_PAIR")) : 1;
+  Layout LP;
+  const bool pair = want_pair && n_cb % 2 == 0 && make_layout(g, &LP, true);
+  if (pair) L = LP;
+  static const int want_cluster =
+      getenv("DEEPTHIN_TC_CLUSTER") ? atoi(getenv("DEEPTHIN_TC_CLUSTER")) : 1;
+  int csize = 1;
+  if (pair) {
+    csize = 2;
+  } else {
+    for (int c : {4, 2})
+      if (c <= want_cluster && n_cb % c == 0) { csize = c; break; }
+  }
+  cuuint32_t box[2] = {KATOM, (cuuint32_t)(BNB / csize)};
   cuuint32_t estr[2] = {1, 1};
   CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(xt), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -725,14 +1116,16 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   p.ldy = (int)g.r_dim;
   p.KB = L.KB; p.S = L.S; p.S_ded = L.S_ded; p.RK = L.RK; p.Nc = L.Nc; p.n_chunks = L.n_chunks;
   p.a_res = L.a_res;
-  p.n_cb = (int)((g.r_dim + BMW - 1) / BMW);
+  p.n_cb = n_cb;
   p.n_bt = (int)((batch + BNB - 1) / BNB);
-  p.items = p.n_cb * p.n_bt;
+  p.csize = csize;
+  p.items = (n_cb / csize) * p.n_bt;  // cluster items: (column-block group, batch tile)
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  p.per_cta = (p.items + nsm - 1) / nsm;
-  const int grid = (p.items + p.per_cta - 1) / p.per_cta;
+  const int clusters = nsm / csize;
+  p.per_cta = (p.items + clusters - 1) / clusters;  // items per cluster
+  const int grid = ((p.items + p.per_cta - 1) / p.per_cta) * csize;
   p.xf_pk = reinterpret_cast<const uint8_t *>(packed);
   p.wf_pk = p.xf_pk + (packed_x_bytes(g, L) + 255) / 256 * 256;
   p.bias = bias;
@@ -746,7 +1139,8 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   p.off_bar = L.off_bar;
   p.w_sbo = (uint32_t)L.KB * (KATOM / 8) * 128u;
   const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
-  KernelFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(eact) : pick_act<DT_F32>(eact);
+  KernelFn fn = pair ? (y_dtype == DT_BF16 ? pick_act_pair<DT_BF16>(eact) : pick_act_pair<DT_F32>(eact))
+                     : (y_dtype == DT_BF16 ? pick_act<DT_BF16>(eact) : pick_act<DT_F32>(eact));
   DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
 
   // Debug: DEEPTHIN_TC_TRACE=1 records per-CTA globaltimer stamps and prints a phase summary.
@@ -757,7 +1151,23 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
     DT_CUDA_CHECK(cudaMemsetAsync(tbuf, 0, (size_t)grid * kTraceSlots * 8, st));
     p.trace = tbuf;
   }
-  fn<<<grid, kThreads, L.total, st>>>(tm, p);
+  if (csize == 1) {
+    fn<<<grid, kThreads, L.total, st>>>(tm, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm, p));
+  }
   if (int rc = check_launch("tc_general")) return rc;
   if (tracing) {
     std::vector<unsigned long long> h((size_t)grid * kTraceSlots);

@@ -32,11 +32,23 @@ __global__ void bench(int mode, int ksteps, int reps, long long *out) {
     uint32_t ph = 0;
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-      for (int ks = 0; ks < ksteps; ++ks) {
-        uint64_t ad = mode == 1 ? smem_desc(a_s + (ks / 4) * 16384 + (ks % 4) * 32, 16, 1024, SL_SW128)
-                                : smem_desc(a_s + ks * 256, 128, 7168, SL_NONE);
-        uint64_t bd = smem_desc(b_s + (ks % 4) * 32 + ((ks / 4) % 4) * 16384, 16, 1024, SL_SW128);
-        mma_bf16_ss(tbase + (r & 1) * 256, ad, bd, idesc, ks > 0);
+      if (mode >= 3) {
+        // regeneration-style: A (128 x 32) and B (160 x 32) no-swizzle K-major, SBO 512;
+        // mode 3: D at column (r % 3) * 160, mode 4: D at column (r & 1) * 256
+        const uint32_t idr = idesc_bf16_f32(128, 160);
+        const uint32_t dcol = mode == 3 ? (uint32_t)(r % 3) * 160u : (uint32_t)(r & 1) * 256u;
+        for (int ks = 0; ks < 2; ++ks) {
+          uint64_t ad = smem_desc(a_s + ks * 256, 128, 512, SL_NONE);
+          uint64_t bd = smem_desc(b_s + ks * 256, 128, 512, SL_NONE);
+          mma_bf16_ss(tbase + dcol, ad, bd, idr, ks > 0);
+        }
+      } else {
+        for (int ks = 0; ks < ksteps; ++ks) {
+          uint64_t ad = mode == 1 ? smem_desc(a_s + (ks / 4) * 16384 + (ks % 4) * 32, 16, 1024, SL_SW128)
+                                  : smem_desc(a_s + ks * 256, 128, 7168, SL_NONE);
+          uint64_t bd = smem_desc(b_s + (ks % 4) * 32 + ((ks / 4) % 4) * 16384, 16, 1024, SL_SW128);
+          mma_bf16_ss(tbase + (r & 1) * 256, ad, bd, idesc, ks > 0);
+        }
       }
       mma_commit(&bar);
       mbar_wait(&bar, ph);
@@ -54,14 +66,19 @@ int main() {
   long long *out;
   cudaMalloc(&out, 1024 * 8);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  for (int mode : {0, 1, 2}) {
+  for (int mode : {0, 1, 2, 3, 4}) {
     for (int grid : {1, 148}) {
-      const int ks = 28, reps = 200;
+      const int ks = mode >= 3 ? 2 : 28, reps = 200;
       bench<<<grid, 128, 220 * 1024>>>(mode, ks, reps, out);
       cudaError_t e = cudaDeviceSynchronize();
       long long c = 0;
       cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost);
       double per_mma = (double)c / (ks * reps);
+      if (mode >= 3) {
+        printf("mode %d grid %3d: %s  %.1f cycles per regen step (2 MMAs 128x160x16 + commit/wait)\n",
+               mode, grid, cudaGetErrorString(e), (double)c / reps);
+        continue;
+      }
       double N = mode == 2 ? 256 : 128;
       printf("mode %d grid %3d: %s  %.1f cycles/MMA (floor %.0f), %.0f MAC/cycle/SM\n", mode, grid,
              cudaGetErrorString(e), per_mma, 128 * N / 256, 128 * N * 16 / per_mma);
