@@ -211,10 +211,10 @@ def run_ours(args, cfg, key):
     ps = _lib.plan_struct(plan)
     ws = torch.empty(max(256, lib.dt_forward_workspace_bytes(C.byref(ps), batch, code)),
                      dtype=torch.uint8, device="cuda")
-    if mma == "bf16":
-        xf_d, wf_d = fp.packed(), None     # per-pair derived operand layout, built once
+    if mma == "bf16" and args.path == "fused":
+        xf_d, wf_d = fp.packed(), None     # the fused kernel's packed operands, built once
         fdt = _lib.DT_FACTORS_PACKED
-    else:
+    else:  # two-phase: W^T regenerated from the fp32 factors inside every step
         xf_d, wf_d, fdt = fp.xf, fp.wf, _lib.DT_F32
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -354,6 +354,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", default="two-phase", choices=["two-phase", "fused"],
+                    help="bf16 tensor-core path: two-phase (default) or the fused kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

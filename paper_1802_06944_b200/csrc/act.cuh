@@ -1,0 +1,18 @@
+// Fused activation of the forward epilogues (kernel.py activation set; softmax runs as a
+// separate row kernel). ACT is a template parameter so each epilogue stays branch-free.
+#pragma once
+
+#include "../../include/deepthin_b200.h"
+
+namespace dt {
+
+template <int ACT>
+__device__ __forceinline__ float act_apply(float z, float arg) {
+  if constexpr (ACT == DT_ACT_RELU) return z > 0.f ? z : 0.f;
+  if constexpr (ACT == DT_ACT_SIGMOID) return 1.f / (1.f + expf(-z));
+  if constexpr (ACT == DT_ACT_TANH) return tanhf(z);
+  if constexpr (ACT == DT_ACT_CLIPPED_RELU) return fminf(fmaxf(z, 0.f), arg);
+  return z;
+}
+
+}  // namespace dt

@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -206,7 +208,8 @@ int dt_pack_factors(const dt_plan *plan, int mma, const uint16_t *xf_bf16,
 size_t dt_forward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) {
   Geo g;
   if (make_geo(plan, &g) || batch < 0) return 0;
-  if (mma == DT_MMA_BF16 && !g.reuse) return tc_general_ws(g, batch);
+  if (mma == DT_MMA_BF16)  // two-phase path, or the fused kernel (general geometries)
+    return std::max(tc_gemm_ws(g, batch), g.reuse ? (size_t)0 : tc_general_ws(g, batch));
   return ffma_forward_ws(g, batch);
 }
 
@@ -240,19 +243,23 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
                         act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
   }
   if (mma == DT_MMA_BF16) {
-    if (f_dtype != DT_BF16 && f_dtype != DT_FACTORS_PACKED) {
-      set_error("the bf16 tensor-core path takes bf16 factor copies (dt_cast_bf16) or the "
-                "dt_pack_factors buffer");
-      return DT_E_ARG;
-    }
-    if (g.reuse) {
-      set_error("bf16 tensor-core reuse path is not built yet");
-      return DT_E_UNSUPPORTED;
-    }
+    // DT_FACTORS_PACKED: the fused single-kernel path (in-kernel W regeneration, general
+    // geometries only). DT_F32 / DT_BF16 factors: the two-phase path (W^T regenerated into
+    // the workspace, then the tcgen05 GEMM), any geometry. DEEPTHIN_TC_FUSED=1 routes bf16
+    // factors on general geometries to the fused kernel (comparison runs).
+    static const int want_fused = getenv("DEEPTHIN_TC_FUSED") ? atoi(getenv("DEEPTHIN_TC_FUSED")) : 0;
     const bool pk = f_dtype == DT_FACTORS_PACKED;
-    return tc_general_forward(g, batch, x, x_dtype, pk ? nullptr : (const uint16_t *)xf,
-                              pk ? nullptr : (const uint16_t *)wf, pk ? xf : nullptr, bias, act,
-                              act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
+    if (pk || (want_fused && f_dtype == DT_BF16 && !g.reuse)) {
+      if (g.reuse) {
+        set_error("packed factors exist only for general (straddling-row) geometries");
+        return DT_E_UNSUPPORTED;
+      }
+      return tc_general_forward(g, batch, x, x_dtype, pk ? nullptr : (const uint16_t *)xf,
+                                pk ? nullptr : (const uint16_t *)wf, pk ? xf : nullptr, bias, act,
+                                act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
+    }
+    return tc_gemm_forward(g, batch, x, x_dtype, xf, wf, f_dtype, bias, act, act_arg, y, y_dtype,
+                           (char *)workspace, workspace_bytes, st);
   }
   set_error("unknown mma kind " + std::to_string(mma));
   return DT_E_ARG;
@@ -380,7 +387,9 @@ int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const 
   }
   int rc = launch_cast_bf16((int64_t)nx, s->xf, s->xf16, s->stream);
   if (!rc) rc = launch_cast_bf16((int64_t)nw, s->wf, s->wf16, s->stream);
-  const size_t pkb = dt_packed_factors_bytes(plan, mma);
+  // The fused kernel's packed operands, only for DEEPTHIN_TC_FUSED comparison runs; the
+  // default bf16 path regenerates W^T from the fp32 factors each call.
+  const size_t pkb = getenv("DEEPTHIN_TC_FUSED") ? dt_packed_factors_bytes(plan, mma) : 0;
   if (!rc && pkb) {
     if (cudaMalloc(&s->packed, pkb) != cudaSuccess) rc = DT_E_CUDA;
     if (!rc) rc = dt_pack_factors(plan, mma, s->xf16, s->wf16, s->packed, (dt_stream)s->stream);
@@ -426,8 +435,6 @@ int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int ac
   int fdt = DT_F32;
   if (tc && s->packed) {
     fx = s->packed; fw = nullptr; fdt = DT_FACTORS_PACKED;
-  } else if (tc) {
-    fx = s->xf16; fw = s->wf16; fdt = DT_BF16;
   }
   int rc = dt_forward(&s->plan, batch, s->mma, s->x, DT_F32, fx, fw, fdt, s->bias, act, act_arg,
                       s->y, DT_F32, s->ws, s->ws_bytes, (dt_stream)s->stream);

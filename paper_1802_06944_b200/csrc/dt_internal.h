@@ -1,6 +1,7 @@
 // Internal declarations shared by the C-ABI translation unit and the kernel files.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -51,6 +52,22 @@ size_t tc_general_ws(const Geo &g, int64_t batch);
 size_t tc_general_packed_bytes(const Geo &g);
 int tc_general_pack(const Geo &g, const uint16_t *xf_bf16, const uint16_t *wf_bf16, void *packed,
                     cudaStream_t st);
+
+// x (fp32 or bf16, pitch q) -> bf16 with pitch ldx (>= q, zero padded), for TMA.
+int launch_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, int x_dtype, void *out,
+                  cudaStream_t st);
+// 2-D tiled tensor map (dtype DT_BF16 / DT_F32), optional 128-byte swizzle.
+int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
+                         uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                         bool swizzle128);
+
+// ---- two-phase tensor-core path: k_tc_gemm.cu ---------------------------------------
+// W^T (r_dim x round_up(q, 8), bf16) regenerated from the factors (f_dtype DT_F32 or DT_BF16)
+// into the workspace, then a persistent tcgen05 GEMM y = act(x W + bias). Any geometry.
+int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, const void *xf,
+                    const void *wf, int f_dtype, const float *bias, int act, float act_arg,
+                    void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st);
+size_t tc_gemm_ws(const Geo &g, int64_t batch);
 
 // Every kernel launch goes through check_launch, which also counts it (dt_launch_counter).
 int check_launch(const char *what);

@@ -1,0 +1,766 @@
+// Two-phase tensor-core forward — the default bf16 path for every geometry (kernel.py:222-293
+// computes the same y = act(x @ W + b) on the CPU; W is factor.py:87-93's re-layout of
+// I = xf @ wf).
+//
+// Phase 1, k_regen_wt: W^T (r_dim x ldw bf16, ldw = round_up(q, 8)) from the factors. Row j of
+// W^T is the flat slice I.ravel()[j*q : (j+1)*q] (factor.py:87-93), so with ldw == q the
+// buffer IS I.ravel()[:q*r_dim] and each thread stores its 8 consecutive outputs as one
+// 16-byte write. W^T is 2*q*r_dim bytes — 1.8 MB at BASELINE config 2 — so it lives in L2
+// between the two phases; the layer's parameters in HBM stay the factors.
+//
+// Phase 2, k_tc_gemm: persistent warp-specialised tcgen05 GEMM, launched with programmatic
+// dependent launch so its prologue (barriers, TMEM, descriptor prefetch, the first x stages)
+// overlaps phase 1. Tile = 128 output columns (UMMA M, TMEM lanes) x 256 batch rows (UMMA N);
+// operands arrive by TMA in 128B-swizzled K-major layout (W^T resident per column block with
+// x multicast across a cluster, or both streamed; see GemmParams) through an S-deep mbarrier
+// stage ring. Accumulators double-buffer in TMEM (2 x 256
+// columns) so the epilogue of tile t overlaps the MMAs of tile t+1. Epilogue: lanes are output
+// columns and TMEM columns batch rows, so every warp store writes 32 consecutive outputs of
+// one batch row (coalesced), fused with bias + activation.
+//
+// Roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (one lane), warps 2.. epilogue.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <vector>
+
+#include "act.cuh"
+#include "dt_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dt {
+namespace {
+
+using namespace ptx;
+
+constexpr int GM = 128;  // output columns per tile (UMMA M)
+constexpr int GN = 256;  // batch rows per tile (UMMA N; N = 256 runs the MMA at ~88% of peak)
+constexpr int GK = 64;   // K per stage: one 128-byte swizzle row of bf16
+constexpr uint32_t kABytes = GM * GK * 2;  // one W^T k-block (16 KB)
+constexpr uint32_t kXBytes = GN * GK * 2;  // one x k-block (32 KB)
+#ifndef DT_GEMM_EPI_WARPS
+#define DT_GEMM_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = DT_GEMM_EPI_WARPS;  // multiple of 4 (one per TMEM lane quarter)
+constexpr int kEpiParts = kEpiWarps / 4;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kSmemMax = 227 * 1024;
+constexpr int kTrace = 48;
+static_assert(kEpiWarps % 4 == 0, "epilogue warps cover the 4 TMEM lane quarters");
+
+// Two operand schedules:
+//  * wres (W resident, K <= 512): a cluster of csize CTAs owns csize consecutive column blocks;
+//    each CTA loads its W^T block once (KB x 16 KB) and the cluster walks batch tiles together,
+//    each CTA TMA-loading 1/csize of every x stage and multicasting it to the whole cluster —
+//    L2 serves every x tile once per cluster. (Streaming both operands per tile moved 10.5
+//    bytes of operands per output through L2, which capped the kernel at the L2 throughput.)
+//  * stream (larger K): W^T and x k-blocks both stream through the stage ring, csize = 1.
+// Work items are (column group, batch tile), column-group-major; cluster c takes the balanced
+// contiguous range [c*items/ncl, (c+1)*items/ncl), so a cluster changes W block at most a few
+// times.
+struct GemmParams {
+  int64_t batch;
+  int r_dim, ldy, KB, n_jb, n_bt, n_jg, items, ncl;
+  int wres, csize, S;
+  uint32_t off_x, stage_bytes, off_bar;
+  const float *bias;
+  void *y;
+  float arg;
+  unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps
+};
+
+__device__ __forceinline__ void gtrace(const GemmParams &p, int slot) {
+  if (p.trace && slot < kTrace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.trace[(size_t)blockIdx.x * kTrace + slot] = t;
+  }
+}
+
+// ---- phase 1 --------------------------------------------------------------------------------
+template <typename FT>
+__device__ __forceinline__ float ldf(const FT *p) {
+  if constexpr (std::is_same<FT, float>::value)
+    return __ldg(p);
+  else
+    return __bfloat162float(*p);
+}
+
+// CTA tile: RG_R aux rows x RG_C aux columns of I = xf @ wf, the factors staged through shared
+// memory RG_K ranks at a time (coalesced loads, all in flight together; xf transposed so a
+// thread's 8 rows at one rank are 32 contiguous bytes). Thread: 8 consecutive rows
+// (RG_E * warp ..) x 4 consecutive columns (4 * lane ..): per rank one 128-bit load of wf (a
+// warp reads 512 distinct bytes) and one broadcast 128-bit load of xf feed 16 FMAs. Only rows
+// a < a_rows = ceil(q*r_dim / n) feed W (the tail of I past q*r_dim is discarded, factor.py:91).
+constexpr int RG_R = 32, RG_C = 128, RG_K = 32;
+constexpr int RG_E = RG_R / 8;  // rows per thread (8 warps)
+
+template <typename FT>
+__global__ void __launch_bounds__(256) k_regen_wt(int64_t q, int64_t r_dim, int rank, int n,
+                                                  int a_rows, int64_t ldw, const FT *xf,
+                                                  const FT *wf, __nv_bfloat16 *wt) {
+  griddep_launch_dependents();  // the GEMM may start its prologue now
+  __shared__ __align__(16) float xt[RG_K][RG_R + 4];  // +4: the transposing stores are 4-way, not 32-way, conflicted
+  __shared__ __align__(16) float ws[RG_K][RG_C];
+  const int tid = threadIdx.x, lane = tid % 32, wrp = tid / 32;
+  const int a0 = blockIdx.x * RG_R, c0 = blockIdx.y * RG_C;
+  float acc[RG_E][4];
+#pragma unroll
+  for (int e = 0; e < RG_E; ++e)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[e][c] = 0.f;
+  for (int k0 = 0; k0 < rank; k0 += RG_K) {
+    const int kc = min(RG_K, rank - k0);
+    // every load of the chunk issued before the first shared-memory store (one latency)
+    constexpr int NX = RG_R * RG_K / 256, NW = RG_K * RG_C / 256;
+    float xv[NX], wv[NW];
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const int e = tid + 256 * u, r = e / RG_K, k = e % RG_K;
+      xv[u] = (a0 + r < a_rows && k < kc) ? ldf(xf + (int64_t)(a0 + r) * rank + k0 + k) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int e = tid + 256 * u, k = e / RG_C, c = e % RG_C;
+      wv[u] = (k < kc && c0 + c < n) ? ldf(wf + (int64_t)(k0 + k) * n + c0 + c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const int e = tid + 256 * u;
+      xt[e % RG_K][e / RG_K] = xv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int e = tid + 256 * u;
+      ws[e / RG_C][e % RG_C] = wv[u];
+    }
+    __syncthreads();
+    // 8 ranks per unrolled group (the staged chunk is zero-padded to a multiple of 8): the
+    // shared loads of later ranks issue ahead of the FMAs of earlier ones
+    for (int k8 = 0; k8 < kc; k8 += 8) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = k8 + kk;
+        const float4 w4 = *reinterpret_cast<const float4 *>(&ws[k][4 * lane]);
+        const float4 x4 = *reinterpret_cast<const float4 *>(&xt[k][RG_E * wrp]);
+        const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
+        const float xk[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+        for (int e = 0; e < RG_E; ++e)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[e][c] = fmaf(xk[e], wk[c], acc[e][c]);
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t total = q * r_dim;
+  const bool flat = ldw == q && (n & 3) == 0;  // W^T == I.ravel(): 8-byte stores
+  const int cc = c0 + 4 * lane;
+  if (cc >= n) return;
+#pragma unroll
+  for (int e = 0; e < RG_E; ++e) {
+    const int a = a0 + RG_E * wrp + e;
+    if (a >= a_rows) continue;
+    const int64_t f0 = (int64_t)a * n + cc;
+    if (flat && f0 + 4 <= total) {
+      __nv_bfloat162 v0 = __floats2bfloat162_rn(acc[e][0], acc[e][1]);
+      __nv_bfloat162 v1 = __floats2bfloat162_rn(acc[e][2], acc[e][3]);
+      *reinterpret_cast<uint2 *>(wt + f0) =
+          make_uint2(*reinterpret_cast<uint32_t *>(&v0), *reinterpret_cast<uint32_t *>(&v1));
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int64_t f = f0 + c;
+        if (cc + c < n && f < total) {
+          const int64_t j = f / q, i = f - j * q;
+          wt[j * ldw + i] = __float2bfloat16_rn(acc[e][c]);
+        }
+      }
+    }
+  }
+}
+
+// ---- phase 2 --------------------------------------------------------------------------------
+template <int YDT, int ACT>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+              const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+  uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
+  uint64_t *wfull = tempty + 2, *wfree = wfull + 1;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(wfree + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int cs = p.csize;
+  const uint32_t crank = cs > 1 ? cluster_ctarank() : 0u;
+  const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
+  const int cid = (int)blockIdx.x / cs;
+  const int beg = (int)((int64_t)cid * p.items / p.ncl);
+  const int end = (int)((int64_t)(cid + 1) * p.items / p.ncl);
+  // item -> (column block, first batch row)
+  auto jb_of = [&](int it) { return (it / p.n_bt) * cs + (int)crank; };
+  auto b0_of = [&](int it) { return (it % p.n_bt) * GN; };
+
+  if (threadIdx.x == 0) {
+    gtrace(p, 0);
+    for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cs); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kEpiWarps); }
+    mbar_init(wfull, 1);
+    mbar_init(wfree, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tm_w); tma_prefetch_desc(&tm_x); }
+  if (warp == 1) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  if (cs > 1) cluster_sync();  // peers' barriers initialised before any multicast lands
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) gtrace(p, 1);
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint32_t slice_rows = GN / cs, slice_bytes = kXBytes / cs;
+      int stage = 0, jg_cur = -1, u = 0;
+      uint32_t phase = 0, wf_phase = 0;
+      // x does not depend on phase 1: the first stages' x loads go out before griddep_wait.
+      const int pre = min(p.S, p.KB);
+      for (int it = beg; it < end; ++it) {
+        const int jg = it / p.n_bt, j0 = jb_of(it) * GM, b0 = b0_of(it);
+        if (p.wres && jg != jg_cur && jg_cur >= 0) {  // next W block: old one fully consumed
+          mbar_wait(wfree, wf_phase);
+          wf_phase ^= 1;
+          mbar_arrive_expect_tx(wfull, (uint32_t)p.KB * kABytes);
+          for (int kb = 0; kb < p.KB; ++kb)
+            tma_load_2d(smem + kb * kABytes, &tm_w, wfull, kb * GK, j0);
+        }
+        for (int kb = 0; kb < p.KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);  // every cluster CTA released this stage
+          if (u < 10) gtrace(p, 34 + u);
+          uint8_t *st = smem + p.off_x + stage * p.stage_bytes;
+          mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
+          uint8_t *xdst = p.wres ? st : st + kABytes;
+          if (cs == 1)
+            tma_load_2d(xdst, &tm_x, &full[stage], kb * GK, b0);
+          else
+            tma_load_2d_mc(xdst + crank * slice_bytes, &tm_x, &full[stage], kb * GK,
+                           b0 + (int)(crank * slice_rows), cmask);
+          if (!p.wres && u >= pre) tma_load_2d(st, &tm_w, &full[stage], kb * GK, j0);
+          ++u;
+          if (u == pre) {  // W^T is phase 1's output
+            griddep_wait();
+            gtrace(p, 2);
+            if (p.wres) {
+              mbar_arrive_expect_tx(wfull, (uint32_t)p.KB * kABytes);
+              for (int k = 0; k < p.KB; ++k)
+                tma_load_2d(smem + k * kABytes, &tm_w, wfull, k * GK, j0);
+            } else {
+              for (int v = 0; v < pre; ++v)  // the W halves of the stages already in flight
+                tma_load_2d(smem + p.off_x + v * p.stage_bytes, &tm_w, &full[v], v * GK, j0);
+            }
+          }
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+        jg_cur = jg;
+      }
+      gtrace(p, 3);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(GM, GN);
+      const uint32_t s0 = smem_u32(smem);
+      int stage = 0, acc = 0, jg_cur = -1;
+      uint32_t phase = 0, aphase = 0, wphase = 0;
+      for (int it = beg; it < end; ++it) {
+        const int jg = it / p.n_bt;
+        if (p.wres && jg != jg_cur) {  // this W block landed
+          mbar_wait(wfull, wphase);
+          wphase ^= 1;
+          jg_cur = jg;
+        }
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * GN);
+        for (int kb = 0; kb < p.KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          if (it == beg) gtrace(p, 20 + kb);
+          tc_fence_after();
+          const uint32_t st = s0 + p.off_x + (uint32_t)stage * p.stage_bytes;
+          const uint32_t a_s = p.wres ? s0 + (uint32_t)kb * kABytes : st;
+          const uint32_t b_s = p.wres ? st : st + kABytes;
+#pragma unroll
+          for (int k = 0; k < GK / 16; ++k)
+            mma_bf16_ss(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
+                        smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
+          if (cs == 1)
+            mma_commit(&empty[stage]);
+          else  // every producer of the cluster multicasts into this stage
+            mma_commit_mc(&empty[stage], cmask);
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        if (p.wres && it + 1 < end && (it + 1) / p.n_bt != jg) mma_commit(wfree);
+        gtrace(p, 4 + min(it - beg, 7));
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue ----------------
+    const int wq = warp & 3;          // TMEM lane quarter this warp may read
+    const int part = (warp - 2) / 4;  // which 32-row groups of the tile
+    using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int it = beg; it < end; ++it) {
+      const int j = jb_of(it) * GM + 32 * wq + lane;
+      const int64_t b0 = b0_of(it);
+      const bool jok = j < p.r_dim;
+      const float bias_j = (p.bias && jok) ? __ldg(p.bias + j) : 0.f;
+      const int nrows = (int)min((int64_t)GN, p.batch - b0);
+      mbar_wait(&tfull[acc], aphase);
+      if (threadIdx.x == 64 && it - beg < 2) gtrace(p, 44 + (it - beg));
+      tc_fence_after();
+      for (int c32 = part; c32 < GN / 32; c32 += kEpiParts) {
+        if (32 * c32 >= nrows) break;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
+        tmem_ld_wait();
+        if (jok) {
+          OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
+          const int rmax = nrows - 32 * c32;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            if (r < rmax) {
+              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+            }
+            yp += p.ldy;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);  // this warp's TMEM reads are done
+      if (threadIdx.x == 64) gtrace(p, 12 + min(it - beg, 7));
+      if (threadIdx.x == kGemmThreads - 32 && it - beg < 2) gtrace(p, 46 + (it - beg));
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (cs > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+// ---- phase 2, CTA-pair variant (tcgen05 cta_group::2) ---------------------------------------
+// A cluster of two CTAs owns two consecutive column blocks (UMMA M = 256: each CTA's W^T block
+// resident in its own shared memory, loaded once per column group, one mbarrier per k-block so
+// the first MMAs need not wait for the whole block) and walks 256-row batch tiles, each CTA
+// TMA-loading its 128-row half of every x k-block (16 KB stages, S ~ 7 deep). The leader
+// (cluster rank 0) issues every MMA (M = 256, N = 256) and its commits multicast to both CTAs;
+// each CTA's TMEM holds its own 128 columns x 256 rows. Per SM this halves the x bytes per
+// output of the single-CTA schedule and doubles the stages in flight, with no multicast copy.
+constexpr uint32_t kXHalf = (GN / 2) * GK * 2;  // one CTA's half of an x k-block (16 KB)
+constexpr int kMaxKB = 8;
+
+__device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t crank) {
+  if (crank == 0)
+    mbar_arrive(bar);
+  else
+    mbar_arrive_remote(bar, 0);
+}
+
+template <int YDT, int ACT>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_tc_gemm_pair(const __grid_constant__ CUtensorMap tm_w,
+                   const __grid_constant__ CUtensorMap tm_x, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+  uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
+  uint64_t *wfull = tempty + 2, *wfree = wfull + kMaxKB;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(wfree + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int cid = (int)blockIdx.x / 2;
+  const int beg = (int)((int64_t)cid * p.items / p.ncl);
+  const int end = (int)((int64_t)(cid + 1) * p.items / p.ncl);
+  auto jb_of = [&](int it) { return (it / p.n_bt) * 2 + (int)crank; };
+  auto b0_of = [&](int it) { return (it % p.n_bt) * GN; };
+
+  if (threadIdx.x == 0) {
+    gtrace(p, 0);
+    for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * kEpiWarps); }
+    for (int k = 0; k < kMaxKB; ++k) mbar_init(&wfull[k], 1);
+    mbar_init(wfree, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tm_w); tma_prefetch_desc(&tm_x); }
+  if (warp == 1) tmem_alloc_pair(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers initialised before any pair TMA / commit lands
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) gtrace(p, 1);
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own W block, own half of each x tile) -------
+    if (lane == 0) {
+      auto load_w = [&](int j0) {
+        for (int kb = 0; kb < p.KB; ++kb) {
+          if (leader) mbar_arrive_expect_tx(&wfull[kb], 2 * kABytes);
+          tma_load_2d_pair(smem + kb * kABytes, &tm_w, &wfull[kb], kb * GK, j0);
+        }
+      };
+      int stage = 0, jg_cur = -1, u = 0;
+      uint32_t phase = 0, wf_phase = 0;
+      const int pre = min(p.S, p.KB);
+      for (int it = beg; it < end; ++it) {
+        const int jg = it / p.n_bt, j0 = jb_of(it) * GM;
+        const int xb0 = b0_of(it) + (int)crank * (GN / 2);
+        if (jg != jg_cur && jg_cur >= 0) {  // next W block once the MMAs on the old one retired
+          mbar_wait(wfree, wf_phase);
+          wf_phase ^= 1;
+          load_w(j0);
+        }
+        for (int kb = 0; kb < p.KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (u < 10) gtrace(p, 34 + u);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kXHalf);
+          tma_load_2d_pair(smem + p.off_x + stage * kXHalf, &tm_x, &full[stage], kb * GK, xb0);
+          if (++u == pre) {  // W^T is phase 1's output: x prefetch first, then wait for it
+            griddep_wait();
+            gtrace(p, 2);
+            load_w(j0);
+          }
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+        jg_cur = jg;
+      }
+      gtrace(p, 3);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (lane == 0 && leader) {
+      const uint32_t idesc = idesc_bf16_f32(2 * GM, GN);
+      const uint32_t s0 = smem_u32(smem);
+      int stage = 0, acc = 0, jg_cur = -1;
+      uint32_t phase = 0, aphase = 0, wphase = 0;
+      for (int it = beg; it < end; ++it) {
+        const int jg = it / p.n_bt;
+        const bool first_of_group = jg != jg_cur;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * GN);
+        for (int kb = 0; kb < p.KB; ++kb) {
+          if (first_of_group) mbar_wait(&wfull[kb], wphase);  // both CTAs' W k-block landed
+          mbar_wait(&full[stage], phase);
+          if (it == beg) gtrace(p, 20 + kb);
+          tc_fence_after();
+          const uint32_t a_s = s0 + (uint32_t)kb * kABytes;
+          const uint32_t b_s = s0 + p.off_x + (uint32_t)stage * kXHalf;
+#pragma unroll
+          for (int k = 0; k < GK / 16; ++k)
+            mma_bf16_ss_pair(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
+                             smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
+          mma_commit_pair(&empty[stage]);  // frees the stage in both CTAs
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+        if (first_of_group) { wphase ^= 1; jg_cur = jg; }
+        mma_commit_pair(&tfull[acc]);
+        if (it + 1 < end && (it + 1) / p.n_bt != jg) mma_commit_pair(wfree);
+        gtrace(p, 4 + min(it - beg, 7));
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (both CTAs: own 128 columns x 256 rows) ----------------
+    const int wq = warp & 3;
+    const int part = (warp - 2) / 4;
+    using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int it = beg; it < end; ++it) {
+      const int j = jb_of(it) * GM + 32 * wq + lane;
+      const int64_t b0 = b0_of(it);
+      const bool jok = j < p.r_dim;
+      const float bias_j = (p.bias && jok) ? __ldg(p.bias + j) : 0.f;
+      const int nrows = (int)min((int64_t)GN, p.batch - b0);
+      mbar_wait(&tfull[acc], aphase);
+      if (threadIdx.x == 64 && it - beg < 2) gtrace(p, 44 + (it - beg));
+      tc_fence_after();
+      for (int c32 = part; c32 < GN / 32; c32 += kEpiParts) {
+        if (32 * c32 >= nrows) break;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
+        tmem_ld_wait();
+        if (jok) {
+          OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
+          const int rmax = nrows - 32 * c32;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            if (r < rmax) {
+              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+            }
+            yp += p.ldy;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&tempty[acc], crank);  // the leader's MMAs reuse it
+      if (threadIdx.x == 64) gtrace(p, 12 + min(it - beg, 7));
+      if (threadIdx.x == kGemmThreads - 32 && it - beg < 2) gtrace(p, 46 + (it - beg));
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal it
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tbase, 512);
+  }
+}
+
+typedef void (*GemmFn)(CUtensorMap, CUtensorMap, GemmParams);
+
+template <int YDT>
+GemmFn pick_gemm(int act, bool pair) {
+  if (pair) switch (act) {
+      case DT_ACT_RELU: return k_tc_gemm_pair<YDT, DT_ACT_RELU>;
+      case DT_ACT_SIGMOID: return k_tc_gemm_pair<YDT, DT_ACT_SIGMOID>;
+      case DT_ACT_TANH: return k_tc_gemm_pair<YDT, DT_ACT_TANH>;
+      case DT_ACT_CLIPPED_RELU: return k_tc_gemm_pair<YDT, DT_ACT_CLIPPED_RELU>;
+      default: return k_tc_gemm_pair<YDT, DT_ACT_IDENTITY>;
+    }
+  switch (act) {
+    case DT_ACT_RELU: return k_tc_gemm<YDT, DT_ACT_RELU>;
+    case DT_ACT_SIGMOID: return k_tc_gemm<YDT, DT_ACT_SIGMOID>;
+    case DT_ACT_TANH: return k_tc_gemm<YDT, DT_ACT_TANH>;
+    case DT_ACT_CLIPPED_RELU: return k_tc_gemm<YDT, DT_ACT_CLIPPED_RELU>;
+    default: return k_tc_gemm<YDT, DT_ACT_IDENTITY>;
+  }
+}
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+void print_gemm_trace(const std::vector<unsigned long long> &h, int grid, int n_tiles) {
+  unsigned long long t0 = ~0ull, t1 = 0;
+  for (int c = 0; c < grid; ++c) {
+    if (h[(size_t)c * kTrace]) t0 = std::min(t0, h[(size_t)c * kTrace]);
+    for (int s = 0; s < kTrace; ++s) t1 = std::max(t1, h[(size_t)c * kTrace + s]);
+  }
+  fprintf(stderr, "[gemm trace] grid %d items %d span %.2f us\n", grid, n_tiles, (t1 - t0) / 1e3);
+  for (int c = 0; c < grid; c += std::max(1, grid / 6)) {
+    const unsigned long long *r = &h[(size_t)c * kTrace];
+    auto rel = [&](int s) { return r[s] ? (double)(r[s] - t0) / 1e3 : -1.0; };
+    fprintf(stderr, "  cta %3d: start %.2f setup %.2f W-ready %.2f prod-done %.2f | mma", c, rel(0),
+            rel(1), rel(2), rel(3));
+    for (int k = 0; k < 8; ++k)
+      if (r[4 + k]) fprintf(stderr, " %.2f", rel(4 + k));
+    fprintf(stderr, " | epi");
+    for (int k = 0; k < 8; ++k)
+      if (r[12 + k]) fprintf(stderr, " %.2f", rel(12 + k));
+    fprintf(stderr, "\n        first tile full[kb]:");
+    for (int k = 0; k < 14; ++k)
+      if (r[20 + k]) fprintf(stderr, " %.2f", rel(20 + k));
+    fprintf(stderr, " | epi-start %.2f %.2f last-warp-done %.2f %.2f", rel(44), rel(45), rel(46),
+            rel(47));
+    fprintf(stderr, " | producer empty-ok[u]:");
+    for (int k = 0; k < 10; ++k)
+      if (r[34 + k]) fprintf(stderr, " %.2f", rel(34 + k));
+    fprintf(stderr, "\n");
+  }
+}
+
+}  // namespace
+
+size_t tc_gemm_ws(const Geo &g, int64_t batch) {
+  const int64_t ldw = round_up(g.q, 8);
+  return (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
+}
+
+int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, const void *xf,
+                    const void *wf, int f_dtype, const float *bias, int act, float act_arg,
+                    void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st) {
+  if (batch == 0) return DT_OK;
+  if (f_dtype != DT_F32 && f_dtype != DT_BF16) {
+    set_error("two-phase tensor-core path: factors must be DT_F32 or DT_BF16");
+    return DT_E_ARG;
+  }
+  if (g.m * g.n > INT32_MAX || g.r_dim > INT32_MAX / 2) {
+    set_error("two-phase tensor-core path: m*n must fit in 32 bits");
+    return DT_E_UNSUPPORTED;
+  }
+  if (ws_bytes < tc_gemm_ws(g, batch)) {
+    set_error("forward workspace too small: need " + std::to_string(tc_gemm_ws(g, batch)));
+    return DT_E_ARG;
+  }
+  const int64_t ldw = round_up(g.q, 8);
+  __nv_bfloat16 *wt = reinterpret_cast<__nv_bfloat16 *>(ws);
+  char *xws = ws + round_up(g.r_dim * ldw * 2, 256);
+
+  // TMA needs a bf16 x whose base and row pitch are 16-byte aligned.
+  const void *xt = x;
+  int64_t ldx = g.q;
+  if (x_dtype != DT_BF16 || (g.q % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
+    ldx = ldw;
+    if (int rc = launch_pack_x(batch, g.q, ldx, x, x_dtype, xws, st)) return rc;
+    xt = xws;
+  }
+
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  GemmParams p{};
+  const int64_t n_bt = (batch + GN - 1) / GN;
+  const int64_t n_jb = (g.r_dim + GM - 1) / GM;
+  p.KB = (int)((g.q + GK - 1) / GK);
+  // operand schedule + shared-memory layout (see GemmParams)
+  const uint32_t kFixed = 256 /*barriers*/ + 1024 /*alignment slack*/;
+  const uint32_t wbytes = (uint32_t)p.KB * kABytes;
+  static const int want_cs = getenv("DEEPTHIN_GEMM_CLUSTER") ? atoi(getenv("DEEPTHIN_GEMM_CLUSTER")) : 4;
+  static const int want_wres = getenv("DEEPTHIN_GEMM_WRES") ? atoi(getenv("DEEPTHIN_GEMM_WRES")) : 1;
+  static const int want_pair = getenv("DEEPTHIN_GEMM_PAIR") ? atoi(getenv("DEEPTHIN_GEMM_PAIR")) : 1;
+  bool pair = false;
+  if (want_pair && n_jb >= 2 && p.KB <= kMaxKB &&
+      wbytes + 4 * kXHalf + kFixed <= (uint32_t)kSmemMax) {
+    pair = true;
+    p.wres = 1;
+    p.stage_bytes = kXHalf;
+    p.off_x = wbytes;
+    p.S = (int)std::min<uint32_t>(8, (kSmemMax - kFixed - wbytes) / kXHalf);
+    p.csize = 2;
+  } else if (want_wres && p.KB <= 8 && wbytes + 3 * kXBytes + kFixed <= (uint32_t)kSmemMax) {
+    p.wres = 1;
+    p.stage_bytes = kXBytes;
+    p.off_x = wbytes;
+    p.S = (int)std::min<uint32_t>(6, (kSmemMax - kFixed - wbytes) / kXBytes);
+    p.csize = 1;
+    for (int c : {4, 2})
+      if (c <= want_cs && n_jb >= c) { p.csize = c; break; }
+  } else {
+    p.wres = 0;
+    p.stage_bytes = kABytes + kXBytes;
+    p.off_x = 0;
+    p.S = (int)std::min<uint32_t>(6, (kSmemMax - kFixed) / p.stage_bytes);
+    p.csize = 1;
+  }
+  p.off_bar = p.off_x + (uint32_t)p.S * p.stage_bytes;
+  const uint32_t smem_bytes = p.off_bar + kFixed;
+  const int64_t n_jg = (n_jb + p.csize - 1) / p.csize;
+  if (n_jg * n_bt > INT32_MAX / 2) {
+    set_error("two-phase tensor-core path: too many tiles");
+    return DT_E_UNSUPPORTED;
+  }
+  p.n_jb = (int)n_jb;
+  p.n_bt = (int)n_bt;
+  p.n_jg = (int)n_jg;
+  p.items = (int)(n_jg * n_bt);
+  p.ncl = std::min(p.items, nsm / p.csize);
+  const int grid = p.ncl * p.csize;
+  static const bool tracing = getenv("DEEPTHIN_TC_TRACE") != nullptr;
+  unsigned long long *tbuf = nullptr;
+  if (tracing) {
+    DT_CUDA_CHECK(cudaMalloc(&tbuf, (size_t)grid * kTrace * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(tbuf, 0, (size_t)grid * kTrace * 8, st));
+  }
+
+  // DEEPTHIN_DBG_PHASE=1 / 2: launch only phase 1 / phase 2 (timing experiments only — the
+  // output is wrong).
+  static const int dbg_phase = getenv("DEEPTHIN_DBG_PHASE") ? atoi(getenv("DEEPTHIN_DBG_PHASE")) : 0;
+
+  // phase 1
+  const int64_t a_rows = (g.q * g.r_dim + g.n - 1) / g.n;
+  const dim3 rgrid((unsigned)((a_rows + RG_R - 1) / RG_R), (unsigned)((g.n + RG_C - 1) / RG_C));
+  if (dbg_phase == 2) {
+  } else if (f_dtype == DT_F32)
+    k_regen_wt<float><<<rgrid, 256, 0, st>>>(g.q, g.r_dim, (int)g.rank, (int)g.n, (int)a_rows, ldw,
+                                             reinterpret_cast<const float *>(xf),
+                                             reinterpret_cast<const float *>(wf), wt);
+  else
+    k_regen_wt<__nv_bfloat16><<<rgrid, 256, 0, st>>>(
+        g.q, g.r_dim, (int)g.rank, (int)g.n, (int)a_rows, ldw,
+        reinterpret_cast<const __nv_bfloat16 *>(xf), reinterpret_cast<const __nv_bfloat16 *>(wf), wt);
+  if (dbg_phase != 2)
+    if (int rc = check_launch("regen_wt")) return rc;
+  if (dbg_phase == 1) return DT_OK;
+
+  // phase 2
+  CUtensorMap tm_w, tm_x;
+  if (int rc = encode_tensor_map_2d(&tm_w, DT_BF16, wt, (uint64_t)g.q, (uint64_t)g.r_dim,
+                                    (uint64_t)ldw * 2, GK, GM, true))
+    return rc;
+  if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(xt), (uint64_t)g.q,
+                                    (uint64_t)batch, (uint64_t)ldx * 2, GK, GN / p.csize, true))
+    return rc;
+  p.batch = batch;
+  p.r_dim = (int)g.r_dim;
+  p.ldy = (int)g.r_dim;
+  p.trace = tbuf;
+  p.bias = bias;
+  p.y = y;
+  p.arg = act_arg;
+  const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
+  GemmFn fn = y_dtype == DT_BF16 ? pick_gemm<DT_BF16>(eact, pair) : pick_gemm<DT_F32>(eact, pair);
+  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+
+  static const int use_pdl = getenv("DEEPTHIN_PDL") ? atoi(getenv("DEEPTHIN_PDL")) : 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (use_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (p.csize > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)p.csize;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_w, tm_x, p));
+  if (int rc = check_launch("tc_gemm")) return rc;
+  if (tracing) {
+    std::vector<unsigned long long> h((size_t)grid * kTrace);
+    DT_CUDA_CHECK(cudaStreamSynchronize(st));
+    DT_CUDA_CHECK(cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(tbuf);
+    print_gemm_trace(h, grid, p.items);
+  }
+  if (act == DT_ACT_SOFTMAX) return launch_row_softmax(batch, g.r_dim, y, y_dtype, st);
+  return DT_OK;
+}
+
+}  // namespace dt

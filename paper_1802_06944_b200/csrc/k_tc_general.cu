@@ -39,6 +39,7 @@
 #include <mutex>
 #include <vector>
 
+#include "act.cuh"
 #include "dt_internal.h"
 #include "sm100_ptx.cuh"
 
@@ -91,15 +92,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // 14..21 MMA tile committed, 22 producer done, 23 end
 __device__ __forceinline__ void trace(const TcParams &p, int slot) {
   if (p.trace && slot < kTraceSlots) p.trace[(size_t)blockIdx.x * kTraceSlots + slot] = gtimer();
-}
-
-template <int ACT>
-__device__ __forceinline__ float act_apply(float z, float arg) {
-  if constexpr (ACT == DT_ACT_RELU) return z > 0.f ? z : 0.f;
-  if constexpr (ACT == DT_ACT_SIGMOID) return 1.f / (1.f + expf(-z));
-  if constexpr (ACT == DT_ACT_TANH) return tanhf(z);
-  if constexpr (ACT == DT_ACT_CLIPPED_RELU) return fminf(fmaxf(z, 0.f), arg);
-  return z;
 }
 
 // Byte offset of W-block element (jj, i) in the no-swizzle K-major core-matrix layout:
@@ -1177,6 +1169,38 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
     print_trace(h, grid, p);
   }
   if (act == DT_ACT_SOFTMAX) return launch_row_softmax(batch, g.r_dim, y, y_dtype, st);
+  return DT_OK;
+}
+
+int launch_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, int x_dtype, void *out,
+                  cudaStream_t st) {
+  const int64_t tot = batch * ldx;
+  if (tot == 0) return DT_OK;
+  k_pack_x<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(batch, q, ldx, x, x_dtype,
+                                                           reinterpret_cast<__nv_bfloat16 *>(out));
+  return check_launch("pack_x");
+}
+
+int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
+                         uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                         bool swizzle128) {
+  PFN_encode_tiled enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return DT_E_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(tm, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                    2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+    return DT_E_CUDA;
+  }
   return DT_OK;
 }
 

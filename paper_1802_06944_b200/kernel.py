@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .core import as_device_matrix, as_device_vector, device, stream_handle, workspace
-from .errors import ArgumentError, DimensionError
+from .errors import ArgumentError, DimensionError, UnsupportedConfigurationError
 from .factor import FactorPair
 
 ACTIVATIONS = ("identity", "relu", "sigmoid", "tanh")
@@ -104,30 +104,31 @@ def _act_code(activation: str) -> int:
 
 def resolve_mma(mma, x: torch.Tensor, plan) -> int:
     if mma is None:
-        # bf16 inputs take the tensor-core path where one exists (general geometries);
-        # reuse geometries run the FFMA kernel, which reads bf16 x directly
-        mma = "bf16" if (x.dtype == torch.bfloat16 and not plan.reuse_path) else "ffma"
+        # bf16 inputs take the tensor-core path (any geometry); fp32 inputs the FFMA path
+        mma = "bf16" if x.dtype == torch.bfloat16 else "ffma"
     if mma not in ("ffma", "bf16"):
-        raise ArgumentError(f"mma must be 'ffma' or 'bf16', got {mma!r}")
+        raise ArgumentError(f"mma must be 'ffma', 'bf16' or 'bf16_fused', got {mma!r}")
     return _lib.DT_MMA_BF16 if mma == "bf16" else _lib.DT_MMA_FFMA
 
 
 def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float, y: torch.Tensor,
-                 mma: int) -> None:
-    """Raw stream-ordered dt_forward on device tensors (no validation beyond the ABI's)."""
+                 mma: int, fused: bool = False) -> None:
+    """Raw stream-ordered dt_forward on device tensors (no validation beyond the ABI's).
+
+    bf16 tensor-core path: by default the two-phase kernels (W^T regenerated from the fp32
+    factors, then the tcgen05 GEMM); ``fused=True`` runs the single fused kernel on the
+    packed bf16 factors (general geometries only)."""
     p = fp.plan
     lib = _lib.lib()
     ps = _lib.plan_struct(p)
     batch = x.shape[0]
     ws_bytes = lib.dt_forward_workspace_bytes(C.byref(ps), batch, mma)
     ws = workspace(ws_bytes)
-    if mma == _lib.DT_MMA_BF16:
-        pk = fp.packed()
-        if pk is not None:
-            xf, wf, fdt = pk, None, _lib.DT_FACTORS_PACKED
-        else:
-            xf, wf = fp.bf16()
-            fdt = _lib.DT_BF16
+    if mma == _lib.DT_MMA_BF16 and fused:
+        xf, wf, fdt = fp.packed(), None, _lib.DT_FACTORS_PACKED
+        if xf is None:
+            raise UnsupportedConfigurationError(
+                "the fused tensor-core kernel needs a general (straddling-row) geometry")
     else:
         xf, wf, fdt = fp.xf, fp.wf, _lib.DT_F32
     _lib.check(lib.dt_forward(
@@ -146,9 +147,10 @@ def _forward(x, fp: FactorPair, bias, activation, act_arg, mma, out_dtype):
     if xt.shape[1] != p.q:
         raise DimensionError(
             f"cannot multiply {xt.shape[0]}x{xt.shape[1]} by compressed {p.q}x{p.r_dim}")
-    code = resolve_mma(mma, xt, p)
+    fused = mma == "bf16_fused"  # the single fused kernel (comparison / its own tests)
+    code = resolve_mma("bf16" if fused else mma, xt, p)
     y = torch.empty((xt.shape[0], p.r_dim), dtype=out_dtype, device=device())
-    forward_into(xt, fp, bias, _act_code(activation), act_arg, y, code)
+    forward_into(xt, fp, bias, _act_code(activation), act_arg, y, code, fused=fused)
     return (y.float().cpu().numpy() if host else y), xt.shape[0]
 
 

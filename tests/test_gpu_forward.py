@@ -124,31 +124,41 @@ def test_ffma_bf16_input_exact_products():
     assert O.rel_error(y, ref) <= F32_TOL
 
 
-# ---- bf16 tcgen05 general path ------------------------------------------------------------
+# ---- bf16 tcgen05 paths ----------------------------------------------------------------
+# "bf16": two-phase (W^T regenerated into L2-resident workspace, then the tcgen05 GEMM), any
+# geometry. "bf16_fused": the single kernel regenerating W blocks in shared memory (general
+# geometries only).
+TC_PATHS = ["bf16", "bf16_fused"]
 
+
+@pytest.mark.parametrize("path", TC_PATHS)
 @pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
-def test_tc_general_config2_full_batch(seed):
+def test_tc_config2_full_batch(seed, path):
     # BASELINE config 2: in 440 -> out 2048, m_f 2816, n_f 320, rank 24, batch 4096
     plan, d, fp = make_case(440, 2048, 24, 320, 2816, 4096, seed=seed, rnd=O.round_bf16)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
-    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma=path)
     err = O.rel_error(y, ref)
     assert err <= BF16_TOL, err
     assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3
 
 
-@pytest.mark.parametrize("geo", [
+GENERAL_GEOS = [
     (494, 2048, 3, 320, 3162, 300),    # config 4 fc1: period 160, tail 128, q % 8 != 0
     (440, 2048, 3, 320, 2816, 1000),   # config 3 layer 0 (rank 3)
     (300, 257, 2, 41, 1881, 129),      # odd everything, ragged r_dim and batch
     (200, 100, 5, 7, 2858, 1),         # n odd (scalar scatter path), batch 1
     (64, 600, 40, 48, 800, 260),       # rank 40 -> padded K of 48
-])
-def test_tc_general_geometries(geo):
+]
+
+
+@pytest.mark.parametrize("path", TC_PATHS)
+@pytest.mark.parametrize("geo", GENERAL_GEOS)
+def test_tc_general_geometries(geo, path):
     q, r_dim, rank, n, m, batch = geo
     plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=5, rnd=O.round_bf16)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
-    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma=path)
     # kernel correctness: tight against the bf16-rounded-W emulation
     assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3
     # the contract tolerance is a statistic over many outputs; a 100-output row can
@@ -157,45 +167,77 @@ def test_tc_general_geometries(geo):
         assert O.rel_error(y, ref) <= BF16_TOL
 
 
+@pytest.mark.parametrize("geo", [
+    (1024, 1024, 16, 256, 4096, 512),  # BASELINE config 1 (reuse: n | q)
+    (1024, 1024, 16, 256, 4096, 1),    # config 1, batch 1
+    (512, 1536, 72, 128, 6144, 700),   # reuse, rank 72 > 64 (two-phase only)
+    (96, 130, 4, 32, 390, 257),        # reuse, ragged r_dim / batch, q % 64 != 0
+    (1000, 300, 8, 125, 2400, 33),     # reuse with n % 8 != 0 (scalar W^T stores)
+    (13, 17, 3, 5, 45, 9),             # tiny: q < 16, K padded by TMA zero fill
+])
+def test_tc_two_phase_reuse_and_edge_geometries(geo):
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=11, rnd=O.round_bf16)
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
+    assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3
+    if batch * r_dim >= 10_000:
+        assert O.rel_error(y, ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("path", TC_PATHS)
 @pytest.mark.parametrize("act", ["relu", "sigmoid", "tanh", "clipped_relu", "softmax"])
-def test_tc_general_fused_activations(act):
+def test_tc_fused_activations(act, path):
     plan, d, fp = make_case(440, 2048, 24, 320, 2816, 384, seed=7, rnd=O.round_bf16, bias_sd=0.5)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
     x = gpu_x(d["x"], torch.bfloat16)
-    pre = D.layer_forward(x, fp, d["bias"], "identity", mma="bf16")
+    pre = D.layer_forward(x, fp, d["bias"], "identity", mma=path)
     assert O.rel_error(pre, ref) <= BF16_TOL          # the contraction (deterministic kernel)
-    y = D.layer_forward(x, fp, d["bias"], act, mma="bf16", act_arg=2.0)
+    y = D.layer_forward(x, fp, d["bias"], act, mma=path, act_arg=2.0)
     check_activation(y, pre, act, 2.0)                # the fused epilogue on the same logits
 
 
-def test_tc_general_fp32_input_and_bf16_output():
+@pytest.mark.parametrize("path", TC_PATHS)
+def test_tc_fp32_input_and_bf16_output(path):
     plan, d, fp = make_case(440, 2048, 24, 320, 2816, 512, seed=2, rnd=O.round_bf16)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
-    y = D.layer_forward(gpu_x(d["x"], torch.float32), fp, d["bias"], mma="bf16")
+    y = D.layer_forward(gpu_x(d["x"], torch.float32), fp, d["bias"], mma=path)
     assert O.rel_error(y, ref) <= BF16_TOL
-    yb = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16",
+    yb = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma=path,
                          out_dtype=torch.bfloat16)
     assert yb.dtype == torch.bfloat16
     # bf16 output adds <= 2^-8 relative rounding on top of the operand rounding
     assert O.rel_error(yb.float(), ref) <= BF16_TOL + 2 ** -8
 
 
-def test_tc_general_deterministic_and_shard_invariant():
+def test_tc_two_phase_agrees_with_fused():
+    # Both paths round W to bf16 and accumulate x . W in fp32. W's fp32 pre-rounding values
+    # come from different summation orders (FFMA vs tcgen05), so an element near a bf16
+    # rounding boundary can differ by one ulp (2^-8 relative) between the paths.
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 1024, seed=3, rnd=O.round_bf16)
+    x = gpu_x(d["x"], torch.bfloat16)
+    a = D.layer_forward(x, fp, d["bias"], mma="bf16")
+    b = D.layer_forward(x, fp, d["bias"], mma="bf16_fused")
+    assert O.rel_error(a, b.double().cpu().numpy()) <= 1e-3
+
+
+@pytest.mark.parametrize("path", TC_PATHS)
+def test_tc_deterministic_and_shard_invariant(path):
     plan, d, fp = make_case(440, 2048, 24, 320, 2816, 4096, seed=9, rnd=O.round_bf16)
     x = gpu_x(d["x"], torch.bfloat16)
     b = d["bias"]
-    y1 = D.layer_forward(x, fp, b, mma="bf16")
-    y2 = D.layer_forward(x, fp, b, mma="bf16")
+    y1 = D.layer_forward(x, fp, b, mma=path)
+    y2 = D.layer_forward(x, fp, b, mma=path)
     assert torch.equal(y1, y2)
     # batch sharding (multi-GPU DP) must not change any row's bits
     for lo, hi in ((0, 1024), (1024, 2048), (2048, 4096), (100, 357)):
-        ys = D.layer_forward(x[lo:hi].contiguous(), fp, b, mma="bf16")
+        ys = D.layer_forward(x[lo:hi].contiguous(), fp, b, mma=path)
         assert torch.equal(ys, y1[lo:hi]), (lo, hi)
 
 
 def test_empty_batch_and_errors():
     plan, d, fp = make_case(440, 2048, 24, 320, 2816, 4, rnd=O.round_bf16)
-    for mma in ("ffma", "bf16"):
+    for mma in ("ffma", "bf16", "bf16_fused"):
         y = D.layer_forward(torch.zeros((0, 440), device="cuda", dtype=torch.bfloat16), fp, d["bias"],
                             mma=mma)
         assert y.shape == (0, 2048)
