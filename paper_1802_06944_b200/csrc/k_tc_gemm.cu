@@ -30,6 +30,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "act.cuh"
 #include "dt_internal.h"
 #include "sm100_ptx.cuh"
@@ -54,6 +56,20 @@ constexpr int kSmemMax = 227 * 1024;
 constexpr int kTrace = 48;
 static_assert(kEpiWarps % 4 == 0, "epilogue warps cover the 4 TMEM lane quarters");
 
+// Phase-1 tile geometry (see regen_tile) and arguments.
+constexpr int RG_R = 32, RG_C = 128, RG_K = 32;  // standalone tile: 32 rows x 128 columns
+constexpr int RG_RMAX = 64;                       // fused kernel: up to 64-row tiles
+struct RegenArgs {
+  int64_t q, r_dim, ldw;
+  int rank, n, a_rows, f_dtype;
+  const void *xf, *wf;
+  __nv_bfloat16 *wt;
+};
+struct RegenSmem {
+  float xt[RG_K][RG_RMAX + 4];  // +4: the transposing stores are 4-way, not 32-way, conflicted
+  float ws[RG_K][RG_C];
+};
+
 // Two operand schedules:
 //  * wres (W resident, K <= 512): a cluster of csize CTAs owns csize consecutive column blocks;
 //    each CTA loads its W^T block once (KB x 16 KB) and the cluster walks batch tiles together,
@@ -67,13 +83,34 @@ static_assert(kEpiWarps % 4 == 0, "epilogue warps cover the 4 TMEM lane quarters
 struct GemmParams {
   int64_t batch;
   int r_dim, ldy, KB, n_jb, n_bt, n_jg, items, ncl;
+  int cpj;  // clusters per column group (> 0: every cluster stays in one group), else 0
   int wres, csize, S;
   uint32_t off_x, stage_bytes, off_bar;
   const float *bias;
   void *y;
   float arg;
+  // fused (cooperative launch): phase 1 runs inside the GEMM kernel on the epilogue warps of
+  // every CTA (tiles rg_ux x rg_uy), then a grid-wide barrier, then the GEMM
+  int fused, rg_ux, rg_uy, rg_rows;
+  uint32_t off_rg;  // phase-1 staging (the W block area, or x stages not yet in flight)
+  RegenArgs rg;
+  int dbg;  // DEEPTHIN_DBG_GEMM (timing experiments only): 1 skip y stores, 2 x loads after the first S stages skipped, 4 skip TMEM loads
   unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps
 };
+
+// Items of cluster cid. With cpj > 0 clusters per column group, each cluster takes a balanced
+// share of one group's batch tiles, so its W block is loaded once; else balanced contiguous
+// ranges of the group-major item order (a range may cross a group: the W block is reloaded).
+__device__ __forceinline__ void item_range(const GemmParams &p, int cid, int &beg, int &end) {
+  if (p.cpj > 0) {
+    const int jg = cid / p.cpj, sub = cid % p.cpj;
+    beg = jg * p.n_bt + (int)((int64_t)sub * p.n_bt / p.cpj);
+    end = jg * p.n_bt + (int)((int64_t)(sub + 1) * p.n_bt / p.cpj);
+  } else {
+    beg = (int)((int64_t)cid * p.items / p.ncl);
+    end = (int)((int64_t)(cid + 1) * p.items / p.ncl);
+  }
+}
 
 __device__ __forceinline__ void gtrace(const GemmParams &p, int slot) {
   if (p.trace && slot < kTrace) {
@@ -98,18 +135,19 @@ __device__ __forceinline__ float ldf(const FT *p) {
 // (RG_E * warp ..) x 4 consecutive columns (4 * lane ..): per rank one 128-bit load of wf (a
 // warp reads 512 distinct bytes) and one broadcast 128-bit load of xf feed 16 FMAs. Only rows
 // a < a_rows = ceil(q*r_dim / n) feed W (the tail of I past q*r_dim is discarded, factor.py:91).
-constexpr int RG_R = 32, RG_C = 128, RG_K = 32;
-constexpr int RG_E = RG_R / 8;  // rows per thread (8 warps)
 
-template <typename FT>
-__global__ void __launch_bounds__(256) k_regen_wt(int64_t q, int64_t r_dim, int rank, int n,
-                                                  int a_rows, int64_t ldw, const FT *xf,
-                                                  const FT *wf, __nv_bfloat16 *wt) {
-  griddep_launch_dependents();  // the GEMM may start its prologue now
-  __shared__ __align__(16) float xt[RG_K][RG_R + 4];  // +4: the transposing stores are 4-way, not 32-way, conflicted
-  __shared__ __align__(16) float ws[RG_K][RG_C];
-  const int tid = threadIdx.x, lane = tid % 32, wrp = tid / 32;
-  const int a0 = blockIdx.x * RG_R, c0 = blockIdx.y * RG_C;
+// One regeneration tile (row block bx, column block by) by 256 threads (tid 0..255); `sync`
+// is the barrier over those threads.
+template <typename FT, int R, typename Sync>
+__device__ __forceinline__ void regen_tile(const RegenArgs &g, int tid, int bx, int by,
+                                           RegenSmem &sm, Sync sync) {
+  constexpr int RG_E = R / 8;  // rows per thread (8 warps)
+  static_assert(R % 32 == 0 && R <= RG_RMAX, "tile rows");
+  const FT *xf = reinterpret_cast<const FT *>(g.xf);
+  const FT *wf = reinterpret_cast<const FT *>(g.wf);
+  const int lane = tid % 32, wrp = tid / 32;
+  const int a0 = bx * R, c0 = by * RG_C;
+  const int rank = g.rank, n = g.n, a_rows = g.a_rows;
   float acc[RG_E][4];
 #pragma unroll
   for (int e = 0; e < RG_E; ++e)
@@ -118,7 +156,7 @@ __global__ void __launch_bounds__(256) k_regen_wt(int64_t q, int64_t r_dim, int 
   for (int k0 = 0; k0 < rank; k0 += RG_K) {
     const int kc = min(RG_K, rank - k0);
     // every load of the chunk issued before the first shared-memory store (one latency)
-    constexpr int NX = RG_R * RG_K / 256, NW = RG_K * RG_C / 256;
+    constexpr int NX = R * RG_K / 256, NW = RG_K * RG_C / 256;
     float xv[NX], wv[NW];
 #pragma unroll
     for (int u = 0; u < NX; ++u) {
@@ -130,37 +168,41 @@ __global__ void __launch_bounds__(256) k_regen_wt(int64_t q, int64_t r_dim, int 
       const int e = tid + 256 * u, k = e / RG_C, c = e % RG_C;
       wv[u] = (k < kc && c0 + c < n) ? ldf(wf + (int64_t)(k0 + k) * n + c0 + c) : 0.f;
     }
+    sync();  // the previous chunk / tile is done with the staging buffers
 #pragma unroll
     for (int u = 0; u < NX; ++u) {
       const int e = tid + 256 * u;
-      xt[e % RG_K][e / RG_K] = xv[u];
+      sm.xt[e % RG_K][e / RG_K] = xv[u];
     }
 #pragma unroll
     for (int u = 0; u < NW; ++u) {
       const int e = tid + 256 * u;
-      ws[e / RG_C][e % RG_C] = wv[u];
+      sm.ws[e / RG_C][e % RG_C] = wv[u];
     }
-    __syncthreads();
+    sync();
     // 8 ranks per unrolled group (the staged chunk is zero-padded to a multiple of 8): the
     // shared loads of later ranks issue ahead of the FMAs of earlier ones
     for (int k8 = 0; k8 < kc; k8 += 8) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const int k = k8 + kk;
-        const float4 w4 = *reinterpret_cast<const float4 *>(&ws[k][4 * lane]);
-        const float4 x4 = *reinterpret_cast<const float4 *>(&xt[k][RG_E * wrp]);
+        const float4 w4 = *reinterpret_cast<const float4 *>(&sm.ws[k][4 * lane]);
         const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
-        const float xk[4] = {x4.x, x4.y, x4.z, x4.w};
+        float xk[RG_E];
+#pragma unroll
+        for (int h = 0; h < RG_E / 4; ++h) {
+          const float4 x4 = *reinterpret_cast<const float4 *>(&sm.xt[k][RG_E * wrp + 4 * h]);
+          xk[4 * h] = x4.x; xk[4 * h + 1] = x4.y; xk[4 * h + 2] = x4.z; xk[4 * h + 3] = x4.w;
+        }
 #pragma unroll
         for (int e = 0; e < RG_E; ++e)
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[e][c] = fmaf(xk[e], wk[c], acc[e][c]);
       }
     }
-    __syncthreads();
   }
-  const int64_t total = q * r_dim;
-  const bool flat = ldw == q && (n & 3) == 0;  // W^T == I.ravel(): 8-byte stores
+  const int64_t q = g.q, total = q * g.r_dim;
+  const bool flat = g.ldw == q && (n & 3) == 0;  // W^T == I.ravel(): 8-byte stores
   const int cc = c0 + 4 * lane;
   if (cc >= n) return;
 #pragma unroll
@@ -171,7 +213,7 @@ __global__ void __launch_bounds__(256) k_regen_wt(int64_t q, int64_t r_dim, int 
     if (flat && f0 + 4 <= total) {
       __nv_bfloat162 v0 = __floats2bfloat162_rn(acc[e][0], acc[e][1]);
       __nv_bfloat162 v1 = __floats2bfloat162_rn(acc[e][2], acc[e][3]);
-      *reinterpret_cast<uint2 *>(wt + f0) =
+      *reinterpret_cast<uint2 *>(g.wt + f0) =
           make_uint2(*reinterpret_cast<uint32_t *>(&v0), *reinterpret_cast<uint32_t *>(&v1));
     } else {
 #pragma unroll
@@ -179,11 +221,21 @@ __global__ void __launch_bounds__(256) k_regen_wt(int64_t q, int64_t r_dim, int 
         const int64_t f = f0 + c;
         if (cc + c < n && f < total) {
           const int64_t j = f / q, i = f - j * q;
-          wt[j * ldw + i] = __float2bfloat16_rn(acc[e][c]);
+          g.wt[j * g.ldw + i] = __float2bfloat16_rn(acc[e][c]);
         }
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_regen_wt(const RegenArgs g) {
+  griddep_launch_dependents();  // the GEMM may start its prologue now
+  __shared__ __align__(16) RegenSmem sm;
+  auto sync = [] { __syncthreads(); };
+  if (g.f_dtype == DT_F32)
+    regen_tile<float, RG_R>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm, sync);
+  else
+    regen_tile<__nv_bfloat16, RG_R>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm, sync);
 }
 
 // ---- phase 2 --------------------------------------------------------------------------------
@@ -202,8 +254,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t crank = cs > 1 ? cluster_ctarank() : 0u;
   const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
   const int cid = (int)blockIdx.x / cs;
-  const int beg = (int)((int64_t)cid * p.items / p.ncl);
-  const int end = (int)((int64_t)(cid + 1) * p.items / p.ncl);
+  int beg, end;
+  item_range(p, cid, beg, end);
   // item -> (column block, first batch row)
   auto jb_of = [&](int it) { return (it / p.n_bt) * cs + (int)crank; };
   auto b0_of = [&](int it) { return (it % p.n_bt) * GN; };
@@ -334,9 +386,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int c32 = part; c32 < GN / 32; c32 += kEpiParts) {
         if (32 * c32 >= nrows) break;
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
-        tmem_ld_wait();
-        if (jok) {
+        if (p.dbg & 4) {
+          for (int r = 0; r < 32; ++r) v[r] = 0;
+        } else {
+          tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
+          tmem_ld_wait();
+        }
+        if (jok && !(p.dbg & 1)) {
           OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - 32 * c32;
 #pragma unroll
@@ -399,8 +455,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
   const int cid = (int)blockIdx.x / 2;
-  const int beg = (int)((int64_t)cid * p.items / p.ncl);
-  const int end = (int)((int64_t)(cid + 1) * p.items / p.ncl);
+  int beg, end;
+  item_range(p, cid, beg, end);
   auto jb_of = [&](int it) { return (it / p.n_bt) * 2 + (int)crank; };
   auto b0_of = [&](int it) { return (it % p.n_bt) * GN; };
 
@@ -421,40 +477,94 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) gtrace(p, 1);
 
+  // ---------------- TMA producer state (warp 0, lane 0) ----------------
+  // Issue order for the first column group: the first x stages before W^T is known to be
+  // ready (they do not depend on phase 1), then W^T k-blocks interleaved one ahead of the
+  // x stages (W0 W1 x2 W2 x3 ...), so the first MMAs wait for ~3 k-blocks of operands, not for
+  // the whole W block queued behind the x prefetch (operand delivery is L2-throughput-bound).
+  const bool producer = warp == 0 && lane == 0;
+  int pstage = 0, pu = 0, w_next = p.KB, w_j0 = 0;
+  uint32_t pphase = 0;
+  const int pre = min(2, min(p.S, p.KB));
+  auto issue_w = [&](int upto) {
+    for (; w_next < min(upto, p.KB); ++w_next) {
+      if (leader) mbar_arrive_expect_tx(&wfull[w_next], 2 * kABytes);
+      tma_load_2d_pair(smem + w_next * kABytes, &tm_w, &wfull[w_next], w_next * GK, w_j0);
+    }
+  };
+  auto issue_x = [&](int it, int kb) {
+    const int xb0 = b0_of(it) + (int)crank * (GN / 2);
+    if ((p.dbg & 2) && pu >= p.S) {  // timing experiment: stale x, no L2 traffic
+      if (leader) mbar_arrive(&full[pstage]);
+    } else {
+      if (leader) mbar_arrive_expect_tx(&full[pstage], 2 * kXHalf);
+      tma_load_2d_pair(smem + p.off_x + pstage * kXHalf, &tm_x, &full[pstage], kb * GK, xb0);
+    }
+    ++pu;
+    if (++pstage == p.S) { pstage = 0; pphase ^= 1; }
+  };
+  if (producer && beg < end)
+    for (int kb = 0; kb < pre; ++kb) issue_x(beg, kb);  // fresh stages: no empty wait
+
+  if (p.fused) {
+    // ---------------- phase 1 inside the kernel: W^T tiles on the epilogue warps ----------
+    if (warp >= 2) {
+      RegenSmem &rs = *reinterpret_cast<RegenSmem *>(smem + p.off_rg);  // no TMA lands here yet
+      auto sync = [] { named_bar_sync(1, 256); };
+      const int n_units = p.rg_ux * p.rg_uy;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int bx = u % p.rg_ux, by = u / p.rg_ux, t = threadIdx.x - 64;
+        if (p.rg_rows == 64) {
+          if (p.rg.f_dtype == DT_F32) regen_tile<float, 64>(p.rg, t, bx, by, rs, sync);
+          else regen_tile<__nv_bfloat16, 64>(p.rg, t, bx, by, rs, sync);
+        } else {
+          if (p.rg.f_dtype == DT_F32) regen_tile<float, 32>(p.rg, t, bx, by, rs, sync);
+          else regen_tile<__nv_bfloat16, 32>(p.rg, t, bx, by, rs, sync);
+        }
+      }
+      fence_proxy_async_global();  // W^T stores -> the TMA reads of every CTA
+      fence_proxy_async_smem();    // staging stores -> the W block TMA writes to the same bytes
+    }
+    if (threadIdx.x == 64) gtrace(p, 42);
+    cooperative_groups::this_grid().sync();
+    if (threadIdx.x == 0) gtrace(p, 43);
+  }
+
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs: own W block, own half of each x tile) -------
     if (lane == 0) {
-      auto load_w = [&](int j0) {
-        for (int kb = 0; kb < p.KB; ++kb) {
-          if (leader) mbar_arrive_expect_tx(&wfull[kb], 2 * kABytes);
-          tma_load_2d_pair(smem + kb * kABytes, &tm_w, &wfull[kb], kb * GK, j0);
-        }
-      };
-      int stage = 0, jg_cur = -1, u = 0;
-      uint32_t phase = 0, wf_phase = 0;
-      const int pre = min(p.S, p.KB);
+      int jg_cur = -1;
+      uint32_t wf_phase = 0;
       for (int it = beg; it < end; ++it) {
         const int jg = it / p.n_bt, j0 = jb_of(it) * GM;
-        const int xb0 = b0_of(it) + (int)crank * (GN / 2);
         if (jg != jg_cur && jg_cur >= 0) {  // next W block once the MMAs on the old one retired
+          issue_w(p.KB);
           mbar_wait(wfree, wf_phase);
           wf_phase ^= 1;
-          load_w(j0);
+          w_next = 0;
+          w_j0 = j0;
+          issue_w(p.KB);
         }
-        for (int kb = 0; kb < p.KB; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (u < 10) gtrace(p, 34 + u);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kXHalf);
-          tma_load_2d_pair(smem + p.off_x + stage * kXHalf, &tm_x, &full[stage], kb * GK, xb0);
-          if (++u == pre) {  // W^T is phase 1's output: x prefetch first, then wait for it
+        if (it == beg) {  // W^T is phase 1's output
+          if (p.fused)
+            fence_proxy_async_global();
+          else
             griddep_wait();
-            gtrace(p, 2);
-            load_w(j0);
-          }
-          if (++stage == p.S) { stage = 0; phase ^= 1; }
+          gtrace(p, 2);
+          w_next = 0;
+          w_j0 = j0;
+          issue_w(2);
+        }
+        for (int kb = it == beg ? pre : 0; kb < p.KB; ++kb) {
+          issue_w(pu - pre + 3);
+          if (pstage == 0 && pu >= p.S) issue_w(p.KB);  // before the first wait on a stage
+          mbar_wait(&empty[pstage], pphase ^ 1);
+          if (pu < 8) gtrace(p, 34 + pu);
+          issue_x(it, kb);
         }
         jg_cur = jg;
       }
+      issue_w(p.KB);
       gtrace(p, 3);
     }
     __syncwarp();
@@ -512,9 +622,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int c32 = part; c32 < GN / 32; c32 += kEpiParts) {
         if (32 * c32 >= nrows) break;
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
-        tmem_ld_wait();
-        if (jok) {
+        if (p.dbg & 4) {
+          for (int r = 0; r < 32; ++r) v[r] = 0;
+        } else {
+          tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
+          tmem_ld_wait();
+        }
+        if (jok && !(p.dbg & 1)) {
           OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - 32 * c32;
 #pragma unroll
@@ -574,11 +688,33 @@ void print_gemm_trace(const std::vector<unsigned long long> &h, int grid, int n_
     for (int s = 0; s < kTrace; ++s) t1 = std::max(t1, h[(size_t)c * kTrace + s]);
   }
   fprintf(stderr, "[gemm trace] grid %d items %d span %.2f us\n", grid, n_tiles, (t1 - t0) / 1e3);
-  for (int c = 0; c < grid; c += std::max(1, grid / 6)) {
+  {  // per-CTA start / end distribution
+    std::vector<double> st, en;
+    for (int c = 0; c < grid; ++c) {
+      const unsigned long long *r = &h[(size_t)c * kTrace];
+      unsigned long long e = 0;
+      for (int s = 0; s < kTrace; ++s) e = std::max(e, r[s]);
+      st.push_back((r[0] - t0) / 1e3);
+      en.push_back((e - t0) / 1e3);
+    }
+    std::sort(st.begin(), st.end());
+    std::sort(en.begin(), en.end());
+    auto q = [&](const std::vector<double> &v, double f) { return v[(size_t)(f * (v.size() - 1))]; };
+    fprintf(stderr, "  CTA start min/med/p90/max %.2f %.2f %.2f %.2f | end min/med/p90/max %.2f %.2f %.2f %.2f\n",
+            q(st, 0), q(st, .5), q(st, .9), q(st, 1), q(en, 0), q(en, .5), q(en, .9), q(en, 1));
+  }
+  std::vector<int> show;
+  for (int c = 0; c < grid; c += std::max(1, grid / 6)) show.push_back(c);
+  for (int c = 0; c < grid; ++c) {  // plus the three latest-finishing CTAs
+    unsigned long long e = 0;
+    for (int s = 0; s < kTrace; ++s) e = std::max(e, h[(size_t)c * kTrace + s]);
+    if (e + 1500 >= t1 && show.size() < 10) show.push_back(c);
+  }
+  for (int c : show) {
     const unsigned long long *r = &h[(size_t)c * kTrace];
     auto rel = [&](int s) { return r[s] ? (double)(r[s] - t0) / 1e3 : -1.0; };
-    fprintf(stderr, "  cta %3d: start %.2f setup %.2f W-ready %.2f prod-done %.2f | mma", c, rel(0),
-            rel(1), rel(2), rel(3));
+    fprintf(stderr, "  cta %3d: start %.2f setup %.2f regen-done %.2f gsync %.2f W-ready %.2f prod-done %.2f | mma",
+            c, rel(0), rel(1), rel(42), rel(43), rel(2), rel(3));
     for (int k = 0; k < 8; ++k)
       if (r[4 + k]) fprintf(stderr, " %.2f", rel(4 + k));
     fprintf(stderr, " | epi");
@@ -590,7 +726,7 @@ void print_gemm_trace(const std::vector<unsigned long long> &h, int grid, int n_
     fprintf(stderr, " | epi-start %.2f %.2f last-warp-done %.2f %.2f", rel(44), rel(45), rel(46),
             rel(47));
     fprintf(stderr, " | producer empty-ok[u]:");
-    for (int k = 0; k < 10; ++k)
+    for (int k = 0; k < 8; ++k)
       if (r[34 + k]) fprintf(stderr, " %.2f", rel(34 + k));
     fprintf(stderr, "\n");
   }
@@ -681,6 +817,9 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   p.n_jg = (int)n_jg;
   p.items = (int)(n_jg * n_bt);
   p.ncl = std::min(p.items, nsm / p.csize);
+  // whole column groups per cluster when every group gets at least one cluster (no W reloads)
+  p.cpj = p.ncl >= p.n_jg ? std::min(p.ncl / p.n_jg, p.n_bt) : 0;
+  if (p.cpj > 0) p.ncl = p.cpj * p.n_jg;
   const int grid = p.ncl * p.csize;
   static const bool tracing = getenv("DEEPTHIN_TC_TRACE") != nullptr;
   unsigned long long *tbuf = nullptr;
@@ -692,24 +831,19 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   // DEEPTHIN_DBG_PHASE=1 / 2: launch only phase 1 / phase 2 (timing experiments only — the
   // output is wrong).
   static const int dbg_phase = getenv("DEEPTHIN_DBG_PHASE") ? atoi(getenv("DEEPTHIN_DBG_PHASE")) : 0;
+  // DEEPTHIN_GEMM_FUSED=1: phase 1 inside the (cooperatively launched) pair kernel, a grid
+  // barrier between the phases (a refused cooperative launch falls back to two kernels).
+  // Measured slower than the two-kernel form at BASELINE config 2 (20.2 vs 18.7 us/step: the
+  // grid barrier ~1.6 us and one 64-row tile per CTA ~3.3 us), so off by default.
+  static const int want_fused = getenv("DEEPTHIN_GEMM_FUSED") ? atoi(getenv("DEEPTHIN_GEMM_FUSED")) : 0;
 
-  // phase 1
   const int64_t a_rows = (g.q * g.r_dim + g.n - 1) / g.n;
   const dim3 rgrid((unsigned)((a_rows + RG_R - 1) / RG_R), (unsigned)((g.n + RG_C - 1) / RG_C));
-  if (dbg_phase == 2) {
-  } else if (f_dtype == DT_F32)
-    k_regen_wt<float><<<rgrid, 256, 0, st>>>(g.q, g.r_dim, (int)g.rank, (int)g.n, (int)a_rows, ldw,
-                                             reinterpret_cast<const float *>(xf),
-                                             reinterpret_cast<const float *>(wf), wt);
-  else
-    k_regen_wt<__nv_bfloat16><<<rgrid, 256, 0, st>>>(
-        g.q, g.r_dim, (int)g.rank, (int)g.n, (int)a_rows, ldw,
-        reinterpret_cast<const __nv_bfloat16 *>(xf), reinterpret_cast<const __nv_bfloat16 *>(wf), wt);
-  if (dbg_phase != 2)
-    if (int rc = check_launch("regen_wt")) return rc;
-  if (dbg_phase == 1) return DT_OK;
+  RegenArgs rg;
+  rg.q = g.q; rg.r_dim = g.r_dim; rg.ldw = ldw;
+  rg.rank = (int)g.rank; rg.n = (int)g.n; rg.a_rows = (int)a_rows; rg.f_dtype = f_dtype;
+  rg.xf = xf; rg.wf = wf; rg.wt = wt;
 
-  // phase 2
   CUtensorMap tm_w, tm_x;
   if (int rc = encode_tensor_map_2d(&tm_w, DT_BF16, wt, (uint64_t)g.q, (uint64_t)g.r_dim,
                                     (uint64_t)ldw * 2, GK, GM, true))
@@ -721,9 +855,16 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   p.r_dim = (int)g.r_dim;
   p.ldy = (int)g.r_dim;
   p.trace = tbuf;
+  static const int dbg_gemm = getenv("DEEPTHIN_DBG_GEMM") ? atoi(getenv("DEEPTHIN_DBG_GEMM")) : 0;
+  p.dbg = dbg_gemm;
   p.bias = bias;
   p.y = y;
   p.arg = act_arg;
+  p.rg = rg;
+  // fused phase 1: 64-row tiles when that makes one tile per CTA, else 32-row tiles
+  p.rg_rows = ((a_rows + 63) / 64) * rgrid.y <= (int64_t)grid ? 64 : 32;
+  p.rg_ux = (int)((a_rows + p.rg_rows - 1) / p.rg_rows);
+  p.rg_uy = (int)rgrid.y;
   const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
   GemmFn fn = y_dtype == DT_BF16 ? pick_gemm<DT_BF16>(eact, pair) : pick_gemm<DT_F32>(eact, pair);
   DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
@@ -734,23 +875,55 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  int na = 0;
-  if (use_pdl) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
+  cudaLaunchAttribute attr[3];
+  auto launch = [&](bool fused) {
+    int na = 0;
+    if (fused) {
+      attr[na].id = cudaLaunchAttributeCooperative;
+      attr[na].val.cooperative = 1;
+      ++na;
+    } else if (use_pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (p.csize > 1) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = (unsigned)p.csize;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    p.fused = fused ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, tm_w, tm_x, p);
+  };
+  // phase-1 staging inside the fused kernel: the W block area, else x stages past the ones
+  // prefetched during phase 1
+  const uint32_t pre_stages = (uint32_t)std::min(2, std::min(p.S, p.KB));
+  p.off_rg = wbytes >= sizeof(RegenSmem) ? 0u : p.off_x + pre_stages * p.stage_bytes;
+  const bool rg_fits = p.off_rg + sizeof(RegenSmem) <= p.off_bar;
+  bool done = false;
+  if (pair && want_fused && rg_fits && dbg_phase == 0) {
+    const cudaError_t e = launch(true);
+    if (e == cudaSuccess) {
+      done = true;
+    } else if (e == cudaErrorCooperativeLaunchTooLarge) {
+      (void)cudaGetLastError();  // not all CTAs co-resident right now: two kernels instead
+    } else {
+      set_error(std::string("tc_gemm (fused) launch: ") + cudaGetErrorString(e));
+      return DT_E_CUDA;
+    }
   }
-  if (p.csize > 1) {
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = (unsigned)p.csize;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
+  if (!done) {
+    if (dbg_phase != 2) {
+      k_regen_wt<<<rgrid, 256, 0, st>>>(rg);
+      if (int rc = check_launch("regen_wt")) return rc;
+    }
+    if (dbg_phase == 1) return DT_OK;
+    DT_CUDA_CHECK(launch(false));
   }
-  cfg.attrs = attr;
-  cfg.numAttrs = na;
-  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_w, tm_x, p));
   if (int rc = check_launch("tc_gemm")) return rc;
   if (tracing) {
     std::vector<unsigned long long> h((size_t)grid * kTrace);
