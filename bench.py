@@ -264,24 +264,47 @@ def run_ours(args, cfg, key):
     samples = batch * world * args.steps
     value = samples / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (one launch per step on this path)
+    # Roofline of the dominant kernel, timed live: dt_profile_kernel_events brackets each launch
+    # of it (the phase-2 tcgen05 GEMM on the bf16 path; the whole FFMA forward on the fp32
+    # path) with CUDA events on the launching stream, over K more steps of the same loop.
     bf16_peak, hbm_peak, peak_kind = peaks()
-    kernel_ms = statistics.mean(step_ms) / max(1, launches // max(1, args.steps))
+    evb = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    eva = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for e in evb + eva:
+        e.record(stream)  # torch creates the cudaEvent_t lazily, at the first record
+    barrier()
+    arr_b = (C.c_void_p * args.steps)(*[e.cuda_event for e in evb])
+    arr_a = (C.c_void_p * args.steps)(*[e.cuda_event for e in eva])
+    assert all(arr_b) and all(arr_a)
+    _lib.check(lib.dt_profile_kernel_events(arr_b, arr_a, args.steps))
+    for _ in range(args.steps):
+        step()
+    _lib.check(lib.dt_profile_kernel_events(None, None, 0))
+    barrier()
+    kernel_ms = statistics.mean(b.elapsed_time(a) for b, a in zip(evb, eva))
     if mma == "bf16":
-        flops = 2.0 * batch * q * r_dim                  # dense-equivalent per launch
-        achieved = flops / (kernel_ms * 1e-3) / 1e12
-        bytes_alg = batch * q * 2 + batch * r_dim * 4 + m * rank_r * 2 + rank_r * n * 2 + r_dim * 4
-        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_peak,
-                "unit": "TFLOP/s", "frac": round(achieved / bf16_peak, 4),
-                "traffic": traffic_for(key), "peak_source": f"{peak_kind} bf16_tflops (burst)",
+        # phase-2 GEMM per launch: reads x (bf16) and W^T (bf16, L2-resident from phase 1) once,
+        # writes y (fp32); HBM-bound at this shape (bytes/peak_bw > flops/peak_flops)
+        bytes_alg = batch * q * 2 + r_dim * q * 2 + batch * r_dim * 4 + r_dim * 4
+        flops = 2.0 * batch * q * r_dim
+        achieved = bytes_alg / (kernel_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic_for(key),
+                "peak_source": f"{peak_kind} hbm_gbs",
+                "kernel": "k_tc_gemm_pair (phase 2)", "kernel_us": round(kernel_ms * 1e3, 3),
+                "kernel_share_of_step": round(kernel_ms / ms_per_step, 3),
                 "algorithmic_bytes": bytes_alg,
-                "hbm_gbs_at_algorithmic_bytes": round(bytes_alg / (kernel_ms * 1e-3) / 1e9, 1)}
+                "tensor_tflops": round(flops / (kernel_ms * 1e-3) / 1e12, 1),
+                "tensor_frac": round(flops / (kernel_ms * 1e-3) / 1e12 / bf16_peak, 4)}
     else:
         bytes_alg = 4 * (batch * q + batch * r_dim + m * rank_r + rank_r * n + r_dim)
         achieved = bytes_alg / (kernel_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": traffic_for(key),
-                "peak_source": f"{peak_kind} hbm_gbs"}
+                "peak_source": f"{peak_kind} hbm_gbs", "kernel": "ffma forward",
+                "kernel_us": round(kernel_ms * 1e3, 3),
+                "kernel_share_of_step": round(kernel_ms / ms_per_step, 3),
+                "algorithmic_bytes": bytes_alg}
 
     # e2e through the host-buffer C ABI (pinned host x in, host y out, every step)
     sess = C.c_void_p()

@@ -81,6 +81,12 @@ const char *dt_version(void);
 const char *dt_last_error(void);
 /* Number of kernels this library has launched in this process (all threads). */
 int64_t dt_launch_counter(void);
+/* Profiling hook (this thread): the next n launches of the forward's dominant kernel (the
+ * tcgen05 GEMM of the bf16 path; the whole FFMA forward on the fp32 path) are bracketed by
+ * cudaEventRecord(before[i]) / cudaEventRecord(after[i]) on their stream. n = 0 disarms.
+ * Events are cudaEvent_t handles created by the caller. No reference counterpart: used by
+ * bench.py for the roofline of the dominant kernel. */
+int dt_profile_kernel_events(void *const *before, void *const *after, int n);
 
 /* ---- geometry (host-only, no GPU needed) ---------------------------------- */
 /* planner.py:38-47 LayerPlan.__post_init__ validation. */

@@ -77,7 +77,21 @@ int check_act(int act) {
   return DT_OK;
 }
 
+thread_local void *const *g_prof_before = nullptr;
+thread_local void *const *g_prof_after = nullptr;
+thread_local int g_prof_n = 0, g_prof_used = 0;
+
 }  // namespace
+
+void dt::profile_next(cudaEvent_t *before, cudaEvent_t *after) {
+  if (g_prof_used < g_prof_n) {
+    *before = (cudaEvent_t)g_prof_before[g_prof_used];
+    *after = (cudaEvent_t)g_prof_after[g_prof_used];
+    ++g_prof_used;
+  } else {
+    *before = *after = nullptr;
+  }
+}
 
 extern "C" {
 
@@ -86,6 +100,18 @@ const char *dt_version(void) { return "deepthin_b200 0.1.0 (sm_100a)"; }
 const char *dt_last_error(void) { return g_last_error.c_str(); }
 
 int64_t dt_launch_counter(void) { return launch_count(); }
+
+int dt_profile_kernel_events(void *const *before, void *const *after, int n) {
+  if (n < 0 || (n > 0 && (!before || !after))) {
+    set_error("dt_profile_kernel_events: n >= 0 event pairs");
+    return DT_E_ARG;
+  }
+  g_prof_before = before;
+  g_prof_after = after;
+  g_prof_n = n;
+  g_prof_used = 0;
+  return DT_OK;
+}
 
 int dt_plan_validate(const dt_plan *plan) {
   Geo g;
@@ -239,8 +265,13 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
       return DT_E_ARG;
     }
     if (batch == 0) return DT_OK;
-    return ffma_forward(g, batch, x, x_dtype, (const float *)xf, (const float *)wf, bias, act,
-                        act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
+    cudaEvent_t eb, ea;
+    profile_next(&eb, &ea);
+    if (eb) DT_CUDA_CHECK(cudaEventRecord(eb, st));
+    int rc = ffma_forward(g, batch, x, x_dtype, (const float *)xf, (const float *)wf, bias, act,
+                          act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
+    if (ea && rc == DT_OK) DT_CUDA_CHECK(cudaEventRecord(ea, st));
+    return rc;
   }
   if (mma == DT_MMA_BF16) {
     // DT_FACTORS_PACKED: the fused single-kernel path (in-kernel W regeneration, general

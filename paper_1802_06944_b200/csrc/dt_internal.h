@@ -69,6 +69,10 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
                     void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st);
 size_t tc_gemm_ws(const Geo &g, int64_t batch);
 
+// dt_profile_kernel_events: events to record around the next dominant-kernel launch on this
+// thread (both null when disarmed / exhausted).
+void profile_next(cudaEvent_t *before, cudaEvent_t *after);
+
 // Every kernel launch goes through check_launch, which also counts it (dt_launch_counter).
 int check_launch(const char *what);
 int64_t launch_count();

@@ -904,8 +904,11 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   const uint32_t pre_stages = (uint32_t)std::min(2, std::min(p.S, p.KB));
   p.off_rg = wbytes >= sizeof(RegenSmem) ? 0u : p.off_x + pre_stages * p.stage_bytes;
   const bool rg_fits = p.off_rg + sizeof(RegenSmem) <= p.off_bar;
+  cudaEvent_t ev_b, ev_a;  // dt_profile_kernel_events: bracket the GEMM launch
+  profile_next(&ev_b, &ev_a);
   bool done = false;
   if (pair && want_fused && rg_fits && dbg_phase == 0) {
+    if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
     const cudaError_t e = launch(true);
     if (e == cudaSuccess) {
       done = true;
@@ -922,8 +925,10 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
       if (int rc = check_launch("regen_wt")) return rc;
     }
     if (dbg_phase == 1) return DT_OK;
+    if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
     DT_CUDA_CHECK(launch(false));
   }
+  if (ev_a) DT_CUDA_CHECK(cudaEventRecord(ev_a, st));
   if (int rc = check_launch("tc_gemm")) return rc;
   if (tracing) {
     std::vector<unsigned long long> h((size_t)grid * kTrace);
