@@ -164,7 +164,10 @@ typedef struct dt_session dt_session;
 int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const float *wf_host,
                       const float *bias_host, dt_session **out);
 /* Host x (batch x q fp32) → device, forward, device → host y (batch x r_dim
- * fp32); synchronous. Returns the bytes moved in *h2d / *d2h when non-NULL. */
+ * fp32); synchronous. Internally the rows go in chunks (DEEPTHIN_SESSION_CHUNK_ROWS, default
+ * 1024) alternating between two streams, so H2D, compute and D2H of neighbouring chunks
+ * overlap; pinned host buffers make the copies asynchronous. Returns the bytes moved in
+ * *h2d / *d2h when non-NULL. */
 int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int act,
                        float act_arg, float *y_host, int64_t *h2d_bytes, int64_t *d2h_bytes);
 void dt_session_destroy(dt_session *s);

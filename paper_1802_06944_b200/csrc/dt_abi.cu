@@ -361,27 +361,42 @@ int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_str
 }
 
 // ---- host-buffer sessions ---------------------------------------------------------------
+// Host-buffer sessions. A call is split into row chunks that alternate between two streams:
+// chunk c's H2D copy, forward and D2H copy are ordered on stream c % 2, so the two copy
+// directions and the kernels of neighbouring chunks overlap (PCIe is the bottleneck of this
+// entry point: at config 2 the fp32 y read-back is 33.5 MB per call).
+constexpr int kSessionStreams = 2;
 struct dt_session {
   dt_plan plan;
   Geo geo;
   int mma;
   float *xf = nullptr, *wf = nullptr, *bias = nullptr;
   uint16_t *xf16 = nullptr, *wf16 = nullptr;
-  void *packed = nullptr;  // dt_pack_factors buffer (bf16 general path)
+  void *packed = nullptr;  // dt_pack_factors buffer (DEEPTHIN_TC_FUSED comparison runs only)
   float *x = nullptr, *y = nullptr;
-  char *ws = nullptr;
+  char *ws[kSessionStreams] = {nullptr, nullptr};
   size_t ws_bytes = 0;
-  int64_t cap_batch = 0;
-  cudaStream_t stream = nullptr;
+  int64_t cap_batch = 0, cap_chunk = 0;
+  cudaStream_t stream = nullptr;  // stream 0 of the pipeline
+  cudaStream_t stream2 = nullptr;
 };
 
 static void session_free_io(dt_session *s) {
   cudaFree(s->x);
   cudaFree(s->y);
-  cudaFree(s->ws);
+  for (auto &w : s->ws) cudaFree(w), w = nullptr;
   s->x = s->y = nullptr;
-  s->ws = nullptr;
-  s->cap_batch = 0;
+  s->cap_batch = s->cap_chunk = 0;
+}
+
+// Rows per chunk: DEEPTHIN_SESSION_CHUNK_ROWS, else 1024 (a multiple of the GEMM's 256-row
+// batch tile), never fewer than 4 chunks' worth of overlap when the batch allows.
+static int64_t session_chunk_rows(int64_t batch) {
+  static const int64_t env = getenv("DEEPTHIN_SESSION_CHUNK_ROWS")
+                                 ? atoll(getenv("DEEPTHIN_SESSION_CHUNK_ROWS"))
+                                 : 0;
+  if (env > 0) return std::min(env, std::max<int64_t>(batch, 1));
+  return std::min<int64_t>(std::max<int64_t>(batch, 1), 1024);
 }
 
 int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const float *wf_host,
@@ -398,6 +413,7 @@ int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const 
   s->mma = mma;
   const size_t nx = (size_t)g.m * g.rank, nw = (size_t)g.rank * g.n;
   cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&s->xf, nx * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->wf, nw * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->bias, (size_t)g.r_dim * 4);
@@ -445,12 +461,14 @@ int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int ac
     return DT_E_DIM;
   }
   const Geo &g = s->geo;
-  if (batch > s->cap_batch) {
+  const int64_t chunk = session_chunk_rows(batch);
+  if (batch > s->cap_batch || chunk > s->cap_chunk) {
     session_free_io(s);
-    size_t ws = dt_forward_workspace_bytes(&s->plan, batch, s->mma);
-    cudaError_t e = cudaMalloc(&s->x, (size_t)batch * g.q * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&s->y, (size_t)batch * g.r_dim * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&s->ws, ws ? ws : 256);
+    const size_t ws = dt_forward_workspace_bytes(&s->plan, chunk, s->mma);
+    cudaError_t e = cudaMalloc(&s->x, (size_t)std::max<int64_t>(batch, 1) * g.q * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&s->y, (size_t)std::max<int64_t>(batch, 1) * g.r_dim * 4);
+    for (auto &w : s->ws)
+      if (e == cudaSuccess) e = cudaMalloc(&w, ws ? ws : 256);
     if (e != cudaSuccess) {
       set_error(std::string("session alloc: ") + cudaGetErrorString(e));
       session_free_io(s);
@@ -458,22 +476,31 @@ int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int ac
     }
     s->ws_bytes = ws;
     s->cap_batch = batch;
+    s->cap_chunk = chunk;
   }
-  const size_t xb = (size_t)batch * g.q * 4, yb = (size_t)batch * g.r_dim * 4;
-  DT_CUDA_CHECK(cudaMemcpyAsync(s->x, x_host, xb, cudaMemcpyHostToDevice, s->stream));
   const bool tc = s->mma == DT_MMA_BF16;
   const void *fx = s->xf, *fw = s->wf;
   int fdt = DT_F32;
   if (tc && s->packed) {
     fx = s->packed; fw = nullptr; fdt = DT_FACTORS_PACKED;
   }
-  int rc = dt_forward(&s->plan, batch, s->mma, s->x, DT_F32, fx, fw, fdt, s->bias, act, act_arg,
-                      s->y, DT_F32, s->ws, s->ws_bytes, (dt_stream)s->stream);
-  if (rc) return rc;
-  DT_CUDA_CHECK(cudaMemcpyAsync(y_host, s->y, yb, cudaMemcpyDeviceToHost, s->stream));
-  DT_CUDA_CHECK(cudaStreamSynchronize(s->stream));
-  if (h2d) *h2d = (int64_t)xb;
-  if (d2h) *d2h = (int64_t)yb;
+  cudaStream_t st[kSessionStreams] = {s->stream, s->stream2};
+  int c = 0;
+  for (int64_t r0 = 0; r0 < batch; r0 += chunk, ++c) {
+    const int64_t rows = std::min(chunk, batch - r0);
+    cudaStream_t cs = st[c % kSessionStreams];
+    float *xd = s->x + r0 * g.q, *yd = s->y + r0 * g.r_dim;
+    DT_CUDA_CHECK(cudaMemcpyAsync(xd, x_host + r0 * g.q, (size_t)rows * g.q * 4,
+                                  cudaMemcpyHostToDevice, cs));
+    int rc = dt_forward(&s->plan, rows, s->mma, xd, DT_F32, fx, fw, fdt, s->bias, act, act_arg, yd,
+                        DT_F32, s->ws[c % kSessionStreams], s->ws_bytes, (dt_stream)cs);
+    if (rc) return rc;
+    DT_CUDA_CHECK(cudaMemcpyAsync(y_host + r0 * g.r_dim, yd, (size_t)rows * g.r_dim * 4,
+                                  cudaMemcpyDeviceToHost, cs));
+  }
+  for (auto cs : st) DT_CUDA_CHECK(cudaStreamSynchronize(cs));
+  if (h2d) *h2d = batch * g.q * 4;
+  if (d2h) *d2h = batch * g.r_dim * 4;
   return DT_OK;
 }
 
@@ -487,6 +514,7 @@ void dt_session_destroy(dt_session *s) {
   cudaFree(s->wf16);
   cudaFree(s->packed);
   if (s->stream) cudaStreamDestroy(s->stream);
+  if (s->stream2) cudaStreamDestroy(s->stream2);
   delete s;
 }
 

@@ -822,17 +822,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// x (fp32 or bf16, row stride q) -> bf16 with row stride ldx (zero padded).
+// x (fp32 or bf16, row stride q) -> bf16 with row stride ldx (zero padded). One thread per 8
+// output elements (one 16-byte store); two 16-byte fp32 loads when the source row is aligned.
 __global__ void k_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, int x_dtype,
                          __nv_bfloat16 *out) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= batch * ldx) return;
-  int64_t b = idx / ldx, i = idx % ldx;
-  float v = 0.f;
-  if (i < q)
-    v = x_dtype == DT_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(x)[b * q + i])
-                           : reinterpret_cast<const float *>(x)[b * q + i];
-  out[idx] = __float2bfloat16_rn(v);
+  const int64_t per_row = ldx / 8;  // ldx is a multiple of 8
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= batch * per_row) return;
+  const int64_t b = idx / per_row, i0 = (idx - b * per_row) * 8;
+  float v[8];
+  const bool vec = x_dtype == DT_F32 && i0 + 8 <= q && ((q & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  if (vec) {
+    const float4 *src = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(x) + b * q + i0);
+    const float4 a = __ldg(src), c = __ldg(src + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int64_t i = i0 + e;
+      v[e] = i >= q ? 0.f
+             : x_dtype == DT_BF16
+                 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(x)[b * q + i])
+                 : reinterpret_cast<const float *>(x)[b * q + i];
+    }
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+    w[h] = *reinterpret_cast<uint32_t *>(&t);
+  }
+  *reinterpret_cast<uint4 *>(out + b * ldx + i0) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // Pack bf16 factors into the regeneration operands' core-matrix layout (zero padded):
@@ -1066,8 +1087,8 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   if (x_dtype != DT_BF16 || (g.q % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
     ldx = (g.q + 7) / 8 * 8;
     int64_t tot = batch * ldx;
-    k_pack_x<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(batch, g.q, ldx, x, x_dtype,
-                                                             reinterpret_cast<__nv_bfloat16 *>(ws));
+    k_pack_x<<<(unsigned)((tot / 8 + 255) / 256), 256, 0, st>>>(batch, g.q, ldx, x, x_dtype,
+                                                                 reinterpret_cast<__nv_bfloat16 *>(ws));
     if (int rc = check_launch("pack_x")) return rc;
     xt = ws;
   }
@@ -1176,8 +1197,12 @@ int launch_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, int x_dt
                   cudaStream_t st) {
   const int64_t tot = batch * ldx;
   if (tot == 0) return DT_OK;
-  k_pack_x<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(batch, q, ldx, x, x_dtype,
-                                                           reinterpret_cast<__nv_bfloat16 *>(out));
+  if (ldx % 8 != 0) {
+    set_error("pack_x: ldx must be a multiple of 8");
+    return DT_E_ARG;
+  }
+  k_pack_x<<<(unsigned)((tot / 8 + 255) / 256), 256, 0, st>>>(batch, q, ldx, x, x_dtype,
+                                                               reinterpret_cast<__nv_bfloat16 *>(out));
   return check_launch("pack_x");
 }
 
