@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 
 #include "dt_internal.h"
 
@@ -341,6 +342,153 @@ struct Carver {
   }
 };
 
+
+// ---- reuse path, small batch: the two factored contractions in one kernel ------------------
+// kernel.py:1-16 with one phase (n | q, s = q/n): column j of W is aux rows j*s .. j*s+s-1, so
+//   P[b, seg, r] = sum_c x[b, seg*n + c] * wf[r, c]        (each distinct run dot once)
+//   y[b, j]      = sum_{k < s*rank} P[b, k] * xf_flat[j*s*rank + k] + bias[j]
+// A CTA owns one batch row x RC output columns (many small CTAs: the work is latency-bound, so
+// parallelism beats reuse; the row's P is recomputed per column tile, s*rank*n FMAs). Every
+// global operand it needs (the x row, wf, the XF2 tile) is staged into shared memory with
+// cp.async first — all copies in flight at once — then P (warp-shuffle reductions in a fixed
+// order) and the outputs (sequential s*rank-long dots) run from shared memory. Exact fp32
+// FFMA; per-row results do not depend on the batch split.
+
+// rows x cols (row stride src_ld) -> shared (row stride dst_ld), zero padded to `cols_pad`.
+// fp32 sources go through cp.async (no register staging: every copy of the CTA is in flight at
+// once); other types through registers. Call cp_async_wait_all() + a barrier before reading.
+__device__ __forceinline__ void cp_async4(float *dst, const float *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async16(float *dst, const float *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void stage_rows(float *dst, int dst_ld, const T *src, int64_t src_ld,
+                                           int rows, int rows_valid, int cols, int cols_pad) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (std::is_same<T, float>::value) {
+    if ((cols & 3) == 0 && (cols_pad & 3) == 0 && (dst_ld & 3) == 0 && (src_ld & 3) == 0 &&
+        ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      const int c4 = cols_pad / 4;
+      for (int e = threadIdx.x; e < rows * c4; e += 256) {  // 16-byte copies
+        const int r = e / c4, c = (e - r * c4) * 4;
+        const bool ok = r < rows_valid && c < cols;
+        cp_async16(dst + r * dst_ld + c, ok ? src + (int64_t)r * src_ld + c : src, ok);
+      }
+      return;
+    }
+  }
+  for (int r = warp; r < rows; r += 8) {
+    const bool rok = r < rows_valid;
+    for (int c = lane; c < cols_pad; c += 32) {
+      const bool ok = rok && c < cols;
+      if constexpr (std::is_same<T, float>::value)
+        cp_async4(dst + r * dst_ld + c, ok ? src + (int64_t)r * src_ld + c : src, ok);
+      else
+        dst[r * dst_ld + c] = ok ? (float)src[(int64_t)r * src_ld + c] : 0.f;
+    }
+  }
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(256) k_reuse_small(int64_t batch, int64_t q, int64_t r_dim,
+                                                     int rank, int64_t n, int s, int RC,
+                                                     const XT *x, const float *xf, const float *wf,
+                                                     const float *bias, int act, float act_arg,
+                                                     void *y, int y_dtype) {
+  extern __shared__ float sm[];
+  // rows padded to a multiple of 4 floats + 4: 16-byte-aligned for cp.async, and the padding
+  // staggers the banks of consecutive rows
+  const int SR = s * rank, SRP = (SR + 3) / 4 * 4 + 4;
+  const int NP = ((int)n + 3) / 4 * 4 + 4, QP = ((int)q + 3) / 4 * 4;
+  float *Xs = sm;                    // q (this CTA's batch row)
+  float *Ws = Xs + QP;               // rank x NP
+  float *X2 = Ws + rank * NP;        // RC x SRP
+  float *Ps = X2 + RC * SRP;         // SR
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = blockIdx.x, j0 = (int64_t)blockIdx.y * RC;
+  // 1) stage the x row, wf, the XF2 tile (rows j0.. of xf viewed r_dim x SR)
+  stage_rows(Xs, (int)q, x + b * q, q, 1, 1, (int)q, (int)q);
+  stage_rows(Ws, NP, wf, n, rank, rank, (int)n, (int)n);
+  stage_rows(X2, SRP, xf + j0 * SR, SR, RC, (int)(r_dim - j0 < RC ? r_dim - j0 : RC), SR, SR);
+  cp_async_wait_all();
+  __syncthreads();
+  // 2) P[seg*rank + r] = x[seg*n : (seg+1)*n] . wf[r, :]: a warp per dot, lanes along the segment,
+  //    two dots per warp in flight, fixed-order shuffle reduction
+  for (int d0 = warp; d0 < SR; d0 += 16) {
+    const int d1 = d0 + 8;
+    const float *x0 = Xs + (d0 / rank) * (int)n, *w0 = Ws + (d0 % rank) * NP;
+    const float *x1 = Xs + (d1 < SR ? d1 / rank : 0) * (int)n, *w1 = Ws + (d1 < SR ? d1 % rank : 0) * NP;
+    float a0 = 0.f, a1 = 0.f;
+    for (int c = lane; c < (int)n; c += 32) {
+      a0 = fmaf(x0[c], w0[c], a0);
+      a1 = fmaf(x1[c], w1[c], a1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (lane == 0) {
+      Ps[d0] = a0;
+      if (d1 < SR) Ps[d1] = a1;
+    }
+  }
+  __syncthreads();
+  // 3) outputs j0 + jj: a thread per column, sequential SR-long dot, 4 partial sums
+  for (int jj = tid; jj < RC; jj += 256) {
+    const int64_t j = j0 + jj;
+    if (j >= r_dim) break;
+    const float *xr = X2 + jj * SRP;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int k = 0;
+    for (; k + 4 <= SR; k += 4)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) acc[kk] = fmaf(Ps[k + kk], xr[k + kk], acc[kk]);
+    for (; k < SR; ++k) acc[0] = fmaf(Ps[k], xr[k], acc[0]);
+    float v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + (bias ? __ldg(bias + j) : 0.f);
+    v = act_apply(act, v, act_arg);
+    if (y_dtype == DT_BF16)
+      reinterpret_cast<__nv_bfloat16 *>(y)[b * r_dim + j] = __float2bfloat16_rn(v);
+    else
+      reinterpret_cast<float *>(y)[b * r_dim + j] = v;
+  }
+}
+
+// Launches k_reuse_small when the shape suits it (small batch, rank <= 64, tiles fit in
+// shared memory); returns false to let the caller take the GEMM route.
+template <typename XT>
+static bool reuse_small(const Geo &g, int64_t batch, const XT *x, const float *xf, const float *wf,
+                        const float *bias, int act, float act_arg, void *y, int y_dtype,
+                        cudaStream_t st, int *rc) {
+  const int SR = (int)(g.s * g.rank);
+  if (!g.reuse || batch > 512 || g.rank > 64 || SR > 4096 || batch > 65535) return false;
+  auto smem_for = [&](int rc) {
+    return (size_t)((g.q + 3) / 4 * 4 + g.rank * ((g.n + 3) / 4 * 4 + 4) +
+                    rc * ((SR + 3) / 4 * 4 + 4) + SR) * 4;
+  };
+  int RC = 256;
+  while (RC > 32 && smem_for(RC) > 100 * 1024) RC /= 2;
+  const size_t smem = smem_for(RC);
+  if (smem > 100 * 1024) return false;
+  const dim3 grid((unsigned)batch, (unsigned)((g.r_dim + RC - 1) / RC));
+  cudaFuncSetAttribute(k_reuse_small<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_reuse_small<XT><<<grid, 256, smem, st>>>(batch, g.q, g.r_dim, (int)g.rank, g.n, (int)g.s, RC,
+                                             x, xf, wf, bias, act, act_arg, y, y_dtype);
+  *rc = check_launch("reuse_small");
+  return true;
+}
+
 }  // namespace
 
 std::atomic<int64_t> g_launches{0};
@@ -395,6 +543,16 @@ static int ffma_forward_t(const Geo &g, int64_t batch, XL xl, const float *xf, c
   EpiStore out{y, g.r_dim, bias, sm_act, act_arg, y_dtype};
   int rc;
   if (g.reuse) {
+    if (batch > 0) {  // small batches: both contractions in one kernel
+      int src = 0;
+      const bool done =
+          reuse_small(g, batch, xl.p, xf, wf, bias, sm_act, act_arg, y, y_dtype, st, &src);
+      if (done) {
+        if (src) return src;
+        if (act == DT_ACT_SOFTMAX) return launch_row_softmax(batch, g.r_dim, y, y_dtype, st);
+        return DT_OK;
+      }
+    }
     // stage 1: P[(b*s + k), r] = sum_c x[b, k*n + c] * wf[r, c]   (one dot per distinct run)
     MatF32 wfT{wf, 1, g.n};  // (k=c, n=r) -> wf[r*n + c]
     EpiStore pst{P, g.rank, nullptr, DT_ACT_IDENTITY, 0.f, DT_F32};

@@ -93,6 +93,10 @@ struct GemmParams {
   // every CTA (tiles rg_ux x rg_uy), then a grid-wide barrier, then the GEMM
   int fused, rg_ux, rg_uy, rg_rows;
   uint32_t off_rg;  // phase-1 staging (the W block area, or x stages not yet in flight)
+  // wgen: no phase 1 — each pair CTA generates its own W^T block in shared memory from the
+  // factors (p.rg.xf / p.rg.wf), staged at off_fs (x stages not in flight yet)
+  int wgen;
+  uint32_t off_fs;
   RegenArgs rg;
   int dbg;  // DEEPTHIN_DBG_GEMM (timing experiments only): 1 skip y stores, 2 x loads after the first S stages skipped, 4 skip TMEM loads
   unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps
@@ -423,6 +427,230 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ---- in-CTA W block generation (p.wgen) ------------------------------------------------------
+// W^T rows [j0, j0 + 128) of one column block, bf16, written straight into the 128B-swizzled
+// K-major A-operand layout in shared memory, so no dense W exists outside the SM. The aux rows
+// a_lo..a_hi that cover the block's flat range [j0*q, (j0+128)*q) are I = xf @ wf products on
+// the warp-level tensor-core path (mma.sync m16n8k8, tf32 operands rounded from the fp32
+// factors — bf16-valued factors are exact — fp32 accumulate), each accumulator element scattered
+// to (j, i) = divmod(a*n + c - j0*q, q) (factor.py:87-93). Factor operands are staged as fp32
+// through shared memory with strides that make the fragment reads bank-conflict-free.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
+                                                 uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// byte offset of W-block element (j, i): 64-column k-blocks of 128 rows x 128 B, 16-byte chunks
+// XOR-swizzled by (row mod 8) — the layout TMA SWIZZLE_128B produces for the GEMM's A operand
+__device__ __forceinline__ uint32_t wsw_off(uint32_t j, uint32_t i) {
+  return (i >> 6) * kABytes + j * 128u + ((((i >> 3) & 7u) ^ (j & 7u)) << 4) + (i & 7u) * 2u;
+}
+struct WgenGeo {  // host-computed staging geometry for one plan
+  int n_ks, xs_stride, ws_stride, max_mt;
+};
+__host__ __device__ inline WgenGeo wgen_geo(int q, int rank, int n) {
+  WgenGeo w;
+  w.n_ks = (rank + 7) / 8;
+  w.xs_stride = 8 * w.n_ks + 4;  // = 4 mod 8: the 8 fragment rows hit distinct bank quads
+  const int n_nt = (n + 7) / 8;
+  w.ws_stride = 8 * (n_nt + 1 + ((n_nt + 1) % 2 == 0 ? 1 : 0));  // /8 odd: conflict-free
+  // aux rows one 128-column block touches, rounded up to whole 16-row tiles
+  const int64_t rows = ((int64_t)GM * q + n - 1) / n + 1;
+  w.max_mt = (int)((rows + 15) / 16);
+  return w;
+}
+__host__ __device__ inline uint32_t wgen_stage_bytes(int q, int rank, int n) {
+  const WgenGeo w = wgen_geo(q, rank, n);
+  return (uint32_t)(w.max_mt * 16 * w.xs_stride + w.n_ks * 8 * w.ws_stride) * 4u;
+}
+
+// Integer work here is latency-bound (8 warps, 2 per scheduler): the loops are division-free
+// (warp-per-row staging, the flat offset of a row split once per m-tile and advanced by +8
+// per n-tile) and two n-tiles are in flight per iteration.
+template <typename FT>
+__device__ void wgen_block(const GemmParams &p, int j0, uint8_t *smem, int tid) {
+  const RegenArgs &g = p.rg;
+  const int q = (int)g.q, n = g.n, rank = g.rank;
+  const int jrows = max(0, min(GM, (int)g.r_dim - j0));
+  const int KP = p.KB * GK;
+  const WgenGeo wg = wgen_geo(q, rank, n);
+  const int w = tid / 32, lane = tid % 32;
+  // 1) zeros: the K padding [q8, KP) of every row (q8 = q rounded down to 8), rows >= jrows
+  {
+    const int q8 = q & ~7;
+    for (int j = tid >> 3; j < GM; j += 32) {  // 8 threads per row
+      const int i_start = j >= jrows ? 0 : q8;
+      for (int i8 = i_start + 8 * (tid & 7); i8 < KP; i8 += 64) {
+        if (j >= jrows || i8 >= q) {
+          *reinterpret_cast<uint4 *>(smem + wsw_off(j, i8)) = make_uint4(0, 0, 0, 0);
+        } else {  // the unit straddling q: only its tail
+          for (int i = q; i < i8 + 8; ++i) *reinterpret_cast<uint16_t *>(smem + wsw_off(j, i)) = 0;
+        }
+      }
+    }
+  }
+  if (tid == 0) gtrace(p, 28);
+  if (jrows == 0) return;
+  const int f_lo = j0 * q, f_span = jrows * q;  // flat range of the block (< 2^31: host check)
+  const int a_lo = f_lo / n, a_hi = (f_lo + f_span - 1) / n;
+  const int n_mt = (a_hi - a_lo + 16) / 16, n_nt = (n + 7) / 8, n_ks = wg.n_ks;
+  const int XS = wg.xs_stride, WS = wg.ws_stride;
+  uint32_t *xs = reinterpret_cast<uint32_t *>(smem + p.off_fs);  // tf32 bit patterns
+  uint32_t *ws = xs + wg.max_mt * 16 * XS;
+  // 2) stage xf rows a_lo.. (n_mt*16 x n_ks*8) and wf (n_ks*8 x n_nt*8) as tf32, zero padded;
+  //    a warp per row, lanes along the contiguous dimension, loads batched ahead of the stores
+  const FT *xf = reinterpret_cast<const FT *>(g.xf);
+  const FT *wf = reinterpret_cast<const FT *>(g.wf);
+  const int kx = n_ks * 8, cx = n_nt * 8;
+  {
+    constexpr int B = 8;
+    const int rows = n_mt * 16;
+    for (int r0 = w; r0 < rows; r0 += 8 * B) {
+      float v[B][2];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int r = r0 + 8 * u, a = a_lo + r;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = lane + 32 * h;
+          v[u][h] = (r < rows && a <= a_hi && k < rank) ? ldf(xf + (int64_t)a * rank + k) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int r = r0 + 8 * u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = lane + 32 * h;
+          if (r < rows && k < kx) xs[r * XS + k] = to_tf32(v[u][h]);
+        }
+      }
+    }
+    for (int k = w; k < kx; k += 8) {
+      const bool kok = k < rank;
+      for (int c0 = 0; c0 < cx; c0 += 32 * B) {
+        float v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int c = c0 + lane + 32 * u;
+          v[u] = (kok && c < n) ? ldf(wf + (int64_t)k * n + c) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int c = c0 + lane + 32 * u;
+          if (c < cx) ws[k * WS + c] = to_tf32(v[u]);
+        }
+      }
+    }
+  }
+  named_bar_sync(1, 256);
+  if (tid == 0) gtrace(p, 29);
+  // 3) tensor-core products + scatter; warp w owns n-tiles w, w+8, ... (two per iteration)
+  const int gr = lane >> 2, tq = lane & 3;
+  // 8 consecutive columns of a row land on 8 consecutive, 16-byte-aligned elements of one W
+  // row: the quad's four bf16 pairs are gathered into one lane and stored as 16 bytes
+  const bool vec8 = (q % 8) == 0 && (n % 8) == 0 && (f_lo % 8) == 0;
+  auto split = [&](int rel, int &j, int &i) {  // rel >= 0
+    j = rel / q;
+    i = rel - j * q;
+  };
+  auto put1 = [&](int rel, uint16_t hb) {  // one element at flat offset rel (any range)
+    if (rel < 0 || rel >= f_span) return;
+    int j, i;
+    split(rel, j, i);
+    *reinterpret_cast<uint16_t *>(smem + wsw_off(j, i)) = hb;
+  };
+  // this lane's store row for the vector path: quad lane 0 stores row g, lane 1 row g + 8
+  const int my_half = tq == 1 ? 8 : 0;
+  for (int mt = 0; mt < n_mt; ++mt) {
+    uint32_t af[8][4];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      if (ks < n_ks) {
+        const uint32_t *xr = xs + (mt * 16 + gr) * XS + ks * 8 + tq;
+        af[ks][0] = xr[0];
+        af[ks][1] = xr[8 * XS];
+        af[ks][2] = xr[4];
+        af[ks][3] = xr[8 * XS + 4];
+      }
+    }
+    const int ra = a_lo + mt * 16 + gr;
+    const int rel_g = ra * n - f_lo, rel_g8 = (ra + 8) * n - f_lo;
+    // the vector path's row: flat offset at column 0, split once; advanced per n-tile below
+    const int my_row = ra + my_half, my_rel0 = my_half ? rel_g8 : rel_g;
+    const bool my_rowok = my_row <= a_hi;
+    int jv = 0, iv = 0;
+    if (my_rel0 >= 0) split(my_rel0, jv, iv);
+    for (int nt0 = w; nt0 < n_nt; nt0 += 16) {
+      float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      const bool second = nt0 + 8 < n_nt;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        if (ks < n_ks) {
+          const uint32_t *wr = ws + (ks * 8 + tq) * WS + nt0 * 8 + gr;
+          mma_m16n8k8_tf32(d[0], af[ks], wr[0], wr[4 * WS]);
+          if (second) mma_m16n8k8_tf32(d[1], af[ks], wr[64], wr[4 * WS + 64]);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !second) break;
+        const int nt = nt0 + 8 * h, c0 = nt * 8;
+        if (vec8 && c0 + 8 <= n) {
+          __nv_bfloat162 hg = __floats2bfloat162_rn(d[h][0], d[h][1]);
+          __nv_bfloat162 hg8 = __floats2bfloat162_rn(d[h][2], d[h][3]);
+          const uint32_t w0 = *reinterpret_cast<uint32_t *>(&hg);
+          const uint32_t w8 = *reinterpret_cast<uint32_t *>(&hg8);
+          uint32_t u[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t a0 = __shfl_sync(0xffffffffu, w0, (lane & ~3) + k);
+            const uint32_t a8 = __shfl_sync(0xffffffffu, w8, (lane & ~3) + k);
+            u[k] = my_half ? a8 : a0;
+          }
+          if (tq < 2 && my_rowok) {
+            const int rel = my_rel0 + c0;
+            if (rel >= 0 && rel + 8 <= f_span) {
+              int j = jv, i = iv + c0;  // advance the row's split by c0 (c0 < n)
+              if (my_rel0 < 0) split(rel, j, i);
+              while (i >= q) { i -= q; ++j; }
+              *reinterpret_cast<uint4 *>(smem + wsw_off(j, i)) = make_uint4(u[0], u[1], u[2], u[3]);
+            } else {  // the block's first / last row: element-wise
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t word = u[e >> 1];
+                put1(rel + e, (uint16_t)(e & 1 ? word >> 16 : word & 0xFFFFu));
+              }
+            }
+          }
+        } else {
+          const int c = c0 + 2 * tq;
+          auto hb = [](float v) {
+            __nv_bfloat16 t = __float2bfloat16_rn(v);
+            return *reinterpret_cast<uint16_t *>(&t);
+          };
+          if (c < n) {
+            if (ra <= a_hi) put1(rel_g + c, hb(d[h][0]));
+            if (ra + 8 <= a_hi) put1(rel_g8 + c, hb(d[h][2]));
+          }
+          if (c + 1 < n) {
+            if (ra <= a_hi) put1(rel_g + c + 1, hb(d[h][1]));
+            if (ra + 8 <= a_hi) put1(rel_g8 + c + 1, hb(d[h][3]));
+          }
+        }
+      }
+    }
+  }
+  if (tid == 0) gtrace(p, 30);
+}
+
 // ---- phase 2, CTA-pair variant (tcgen05 cta_group::2) ---------------------------------------
 // A cluster of two CTAs owns two consecutive column blocks (UMMA M = 256: each CTA's W^T block
 // resident in its own shared memory, loaded once per column group, one mbarrier per k-block so
@@ -449,8 +677,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
-  uint64_t *wfull = tempty + 2, *wfree = wfull + kMaxKB;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(wfree + 1);
+  uint64_t *wfull = tempty + 2, *wfree = wfull + kMaxKB, *wgen_done = wfree + 1;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(wgen_done + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
@@ -465,7 +693,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * kEpiWarps); }
     for (int k = 0; k < kMaxKB; ++k) mbar_init(&wfull[k], 1);
+    if (p.wgen) mbar_init(&wfull[0], 2);  // both CTAs generated their W block (leader's copy)
     mbar_init(wfree, 1);
+    mbar_init(wgen_done, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch_desc(&tm_w); tma_prefetch_desc(&tm_x); }
@@ -530,6 +760,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (threadIdx.x == 0) gtrace(p, 43);
   }
 
+  if (p.wgen && warp >= 2 && beg < end) {
+    // ---------------- W block generated in shared memory (epilogue warps) ----------------
+    if (p.rg.f_dtype == DT_F32)
+      wgen_block<float>(p, jb_of(beg) * GM, smem, threadIdx.x - 64);
+    else
+      wgen_block<__nv_bfloat16>(p, jb_of(beg) * GM, smem, threadIdx.x - 64);
+    fence_proxy_async_smem();  // generic-proxy W stores -> the tensor cores' operand reads
+    named_bar_sync(1, 256);
+    if (threadIdx.x == 64) {
+      gtrace(p, 42);
+      mbar_arrive(wgen_done);             // the factor staging area may take x stages now
+      arrive_leader(&wfull[0], crank);    // the leader's MMAs read both CTAs' W blocks
+    }
+  }
+
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs: own W block, own half of each x tile) -------
     if (lane == 0) {
@@ -545,7 +790,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           w_j0 = j0;
           issue_w(p.KB);
         }
-        if (it == beg) {  // W^T is phase 1's output
+        if (it == beg && p.wgen) {  // stages past `pre` hold the factor staging until then
+          mbar_wait(wgen_done, 0);
+          gtrace(p, 2);
+        } else if (it == beg) {  // W^T is phase 1's output
           if (p.fused)
             fence_proxy_async_global();
           else
@@ -582,7 +830,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t d = tbase + (uint32_t)(acc * GN);
         for (int kb = 0; kb < p.KB; ++kb) {
-          if (first_of_group) mbar_wait(&wfull[kb], wphase);  // both CTAs' W k-block landed
+          if (first_of_group && (!p.wgen || kb == 0))  // both CTAs' W k-block (or block) ready
+            mbar_wait(&wfull[kb], wphase);
           mbar_wait(&full[stage], phase);
           if (it == beg) gtrace(p, 20 + kb);
           tc_fence_after();
@@ -713,8 +962,8 @@ void print_gemm_trace(const std::vector<unsigned long long> &h, int grid, int n_
   for (int c : show) {
     const unsigned long long *r = &h[(size_t)c * kTrace];
     auto rel = [&](int s) { return r[s] ? (double)(r[s] - t0) / 1e3 : -1.0; };
-    fprintf(stderr, "  cta %3d: start %.2f setup %.2f regen-done %.2f gsync %.2f W-ready %.2f prod-done %.2f | mma",
-            c, rel(0), rel(1), rel(42), rel(43), rel(2), rel(3));
+    fprintf(stderr, "  cta %3d: start %.2f setup %.2f wgen zero/stage/mma %.2f %.2f %.2f regen-done %.2f gsync %.2f W-ready %.2f prod-done %.2f | mma",
+            c, rel(0), rel(1), rel(28), rel(29), rel(30), rel(42), rel(43), rel(2), rel(3));
     for (int k = 0; k < 8; ++k)
       if (r[4 + k]) fprintf(stderr, " %.2f", rel(4 + k));
     fprintf(stderr, " | epi");
@@ -835,7 +1084,7 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   // barrier between the phases (a refused cooperative launch falls back to two kernels).
   // Measured slower than the two-kernel form at BASELINE config 2 (20.2 vs 18.7 us/step: the
   // grid barrier ~1.6 us and one 64-row tile per CTA ~3.3 us), so off by default.
-  static const int want_fused = getenv("DEEPTHIN_GEMM_FUSED") ? atoi(getenv("DEEPTHIN_GEMM_FUSED")) : 0;
+  const int want_fused = getenv("DEEPTHIN_GEMM_FUSED") ? atoi(getenv("DEEPTHIN_GEMM_FUSED")) : 0;
 
   const int64_t a_rows = (g.q * g.r_dim + g.n - 1) / g.n;
   const dim3 rgrid((unsigned)((a_rows + RG_R - 1) / RG_R), (unsigned)((g.n + RG_C - 1) / RG_C));
@@ -882,7 +1131,7 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
       attr[na].id = cudaLaunchAttributeCooperative;
       attr[na].val.cooperative = 1;
       ++na;
-    } else if (use_pdl) {
+    } else if (use_pdl && !p.wgen) {  // (wgen: nothing to overlap, and no griddep wait)
       attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[na].val.programmaticStreamSerializationAllowed = 1;
       ++na;
@@ -902,12 +1151,27 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   // phase-1 staging inside the fused kernel: the W block area, else x stages past the ones
   // prefetched during phase 1
   const uint32_t pre_stages = (uint32_t)std::min(2, std::min(p.S, p.KB));
+  // DEEPTHIN_GEMM_WGEN=1: every CTA generates its own W^T block in shared memory (no phase-1
+  // kernel, no W^T outside the SM). Needs one column group per cluster (cpj > 0), rank <= 64
+  // and the factor staging to fit in the x stages not prefetched. Measured slower than the
+  // two-kernel form at config 2 (~40 vs 20.7 us/step): the per-element scatter is
+  // instruction-latency-bound on 8 warps and its one-pass code runs from a cold I-cache.
+  const int want_wgen = getenv("DEEPTHIN_GEMM_WGEN") ? atoi(getenv("DEEPTHIN_GEMM_WGEN")) : 0;
+  p.off_fs = p.off_x + pre_stages * p.stage_bytes;
+  p.wgen = (pair && want_wgen && p.cpj > 0 && g.rank <= 64 && dbg_phase == 0 &&
+            p.off_fs + wgen_stage_bytes((int)g.q, (int)g.rank, (int)g.n) <= p.off_bar)
+               ? 1
+               : 0;
   p.off_rg = wbytes >= sizeof(RegenSmem) ? 0u : p.off_x + pre_stages * p.stage_bytes;
   const bool rg_fits = p.off_rg + sizeof(RegenSmem) <= p.off_bar;
   cudaEvent_t ev_b, ev_a;  // dt_profile_kernel_events: bracket the GEMM launch
   profile_next(&ev_b, &ev_a);
   bool done = false;
-  if (pair && want_fused && rg_fits && dbg_phase == 0) {
+  if (p.wgen) {
+    if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
+    DT_CUDA_CHECK(launch(false));
+    done = true;
+  } else if (pair && want_fused && rg_fits && dbg_phase == 0) {
     if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
     const cudaError_t e = launch(true);
     if (e == cudaSuccess) {

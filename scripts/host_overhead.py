@@ -11,22 +11,24 @@ import torch
 import paper_1802_06944_b200 as D
 from paper_1802_06944_b200 import _lib
 
-q, r_dim, rank, n, m, batch = 440, 2048, 24, 320, 2816, 4096
+import os
+q, r_dim, rank, n, m, batch = (1024, 1024, 16, 256, 4096, 64) if os.environ.get("HO_C1") else (440, 2048, 24, 320, 2816, 4096)
+MMA = _lib.DT_MMA_FFMA if os.environ.get("HO_FFMA") else _lib.DT_MMA_BF16
 plan = D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
 rng = np.random.default_rng(0)
 fp = D.FactorPair(rng.standard_normal((m, rank)) / 5, rng.standard_normal((rank, n)) / 5, plan)
-x = torch.randn(batch, q, device="cuda").to(torch.bfloat16)
+x = torch.randn(batch, q, device="cuda").to(torch.float32 if MMA == _lib.DT_MMA_FFMA else torch.bfloat16)
 y = torch.empty(batch, r_dim, device="cuda")
 b = torch.zeros(r_dim, device="cuda")
 lib = _lib.lib()
 ps = _lib.plan_struct(plan)
-ws = torch.empty(lib.dt_forward_workspace_bytes(C.byref(ps), batch, _lib.DT_MMA_BF16), dtype=torch.uint8,
+ws = torch.empty(lib.dt_forward_workspace_bytes(C.byref(ps), batch, MMA), dtype=torch.uint8,
                  device="cuda")
 sh = torch.cuda.current_stream().cuda_stream
 
 
 def call():
-    lib.dt_forward(C.byref(ps), batch, _lib.DT_MMA_BF16, x.data_ptr(), _lib.DT_BF16, fp.xf.data_ptr(),
+    lib.dt_forward(C.byref(ps), batch, MMA, x.data_ptr(), _lib.DT_F32 if MMA == _lib.DT_MMA_FFMA else _lib.DT_BF16, fp.xf.data_ptr(),
                    fp.wf.data_ptr(), _lib.DT_F32, b.data_ptr(), 0, 0.0, y.data_ptr(), _lib.DT_F32,
                    ws.data_ptr(), ws.numel(), sh)
 
@@ -52,7 +54,7 @@ with torch.cuda.stream(s):
     g_ok = True
     with torch.cuda.graph(g, stream=s):
         for _ in range(10):
-            lib.dt_forward(C.byref(ps), batch, _lib.DT_MMA_BF16, x.data_ptr(), _lib.DT_BF16,
+            lib.dt_forward(C.byref(ps), batch, MMA, x.data_ptr(), _lib.DT_F32 if MMA == _lib.DT_MMA_FFMA else _lib.DT_BF16,
                            fp.xf.data_ptr(), fp.wf.data_ptr(), _lib.DT_F32, b.data_ptr(), 0, 0.0,
                            y.data_ptr(), _lib.DT_F32, ws.data_ptr(), ws.numel(), s.cuda_stream)
 torch.cuda.synchronize()

@@ -288,3 +288,16 @@ def test_session_host_buffers_match_device_path():
             assert np.array_equal(y, ref)
         else:               # split-K partitioning follows the chunk shape
             assert O.rel_error(y, ref) <= 1e-6
+
+
+@pytest.mark.parametrize("variant", ["DEEPTHIN_GEMM_WGEN", "DEEPTHIN_GEMM_FUSED"])
+def test_tc_alternative_pair_schedules(variant, monkeypatch):
+    # the in-CTA W generation (no W^T outside the SM) and the cooperative fused phase 1 are
+    # opt-in schedules of the same pair kernel: same contract as the default
+    monkeypatch.setenv(variant, "1")
+    for geo in [(440, 2048, 24, 320, 2816, 1024), (494, 2048, 3, 320, 3162, 300),
+                (1024, 1024, 16, 256, 4096, 512), (300, 257, 2, 41, 1881, 129)]:
+        q, r_dim, rank, n, m, batch = geo
+        plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=6, rnd=O.round_bf16)
+        y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
+        assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3, geo
