@@ -243,10 +243,13 @@ __global__ void __launch_bounds__(256) k_regen_wt(const RegenArgs g) {
 }
 
 // ---- phase 2 --------------------------------------------------------------------------------
-template <int YDT, int ACT>
+// EL: 0 = bf16 operands (kind::f16, 64 elements per 128-byte k-block), 1 = fp32 operands
+// (kind::tf32, 32 elements per k-block). Shared-memory bytes and descriptors are identical.
+template <int YDT, int ACT, int EL>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const GemmParams p) {
+  constexpr int GKE = EL ? 32 : 64;  // elements per 128-byte k-block
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           wf_phase ^= 1;
           mbar_arrive_expect_tx(wfull, (uint32_t)p.KB * kABytes);
           for (int kb = 0; kb < p.KB; ++kb)
-            tma_load_2d(smem + kb * kABytes, &tm_w, wfull, kb * GK, j0);
+            tma_load_2d(smem + kb * kABytes, &tm_w, wfull, kb * GKE, j0);
         }
         for (int kb = 0; kb < p.KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);  // every cluster CTA released this stage
@@ -305,11 +308,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
           uint8_t *xdst = p.wres ? st : st + kABytes;
           if (cs == 1)
-            tma_load_2d(xdst, &tm_x, &full[stage], kb * GK, b0);
+            tma_load_2d(xdst, &tm_x, &full[stage], kb * GKE, b0);
           else
-            tma_load_2d_mc(xdst + crank * slice_bytes, &tm_x, &full[stage], kb * GK,
+            tma_load_2d_mc(xdst + crank * slice_bytes, &tm_x, &full[stage], kb * GKE,
                            b0 + (int)(crank * slice_rows), cmask);
-          if (!p.wres && u >= pre) tma_load_2d(st, &tm_w, &full[stage], kb * GK, j0);
+          if (!p.wres && u >= pre) tma_load_2d(st, &tm_w, &full[stage], kb * GKE, j0);
           ++u;
           if (u == pre) {  // W^T is phase 1's output
             griddep_wait();
@@ -317,10 +320,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (p.wres) {
               mbar_arrive_expect_tx(wfull, (uint32_t)p.KB * kABytes);
               for (int k = 0; k < p.KB; ++k)
-                tma_load_2d(smem + k * kABytes, &tm_w, wfull, k * GK, j0);
+                tma_load_2d(smem + k * kABytes, &tm_w, wfull, k * GKE, j0);
             } else {
               for (int v = 0; v < pre; ++v)  // the W halves of the stages already in flight
-                tma_load_2d(smem + p.off_x + v * p.stage_bytes, &tm_w, &full[v], v * GK, j0);
+                tma_load_2d(smem + p.off_x + v * p.stage_bytes, &tm_w, &full[v], v * GKE, j0);
             }
           }
           if (++stage == p.S) { stage = 0; phase ^= 1; }
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(GM, GN);
+      const uint32_t idesc = idesc_f32acc(GM, GN, EL ? 2 : 1);
       const uint32_t s0 = smem_u32(smem);
       int stage = 0, acc = 0, jg_cur = -1;
       uint32_t phase = 0, aphase = 0, wphase = 0;
@@ -356,8 +359,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b_s = p.wres ? st : st + kABytes;
 #pragma unroll
           for (int k = 0; k < GK / 16; ++k)
-            mma_bf16_ss(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
-                        smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
+            if constexpr (EL)
+              mma_tf32_ss(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
+                          smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
+            else
+              mma_bf16_ss(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
+                          smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
           if (cs == 1)
             mma_commit(&empty[stage]);
           else  // every producer of the cluster multicasts into this stage
@@ -669,10 +676,11 @@ __device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t crank) {
     mbar_arrive_remote(bar, 0);
 }
 
-template <int YDT, int ACT>
+template <int YDT, int ACT, int EL>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_tc_gemm_pair(const __grid_constant__ CUtensorMap tm_w,
                    const __grid_constant__ CUtensorMap tm_x, const GemmParams p) {
+  constexpr int GKE = EL ? 32 : 64;  // elements per 128-byte k-block
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
@@ -719,7 +727,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   auto issue_w = [&](int upto) {
     for (; w_next < min(upto, p.KB); ++w_next) {
       if (leader) mbar_arrive_expect_tx(&wfull[w_next], 2 * kABytes);
-      tma_load_2d_pair(smem + w_next * kABytes, &tm_w, &wfull[w_next], w_next * GK, w_j0);
+      tma_load_2d_pair(smem + w_next * kABytes, &tm_w, &wfull[w_next], w_next * GKE, w_j0);
     }
   };
   auto issue_x = [&](int it, int kb) {
@@ -728,7 +736,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (leader) mbar_arrive(&full[pstage]);
     } else {
       if (leader) mbar_arrive_expect_tx(&full[pstage], 2 * kXHalf);
-      tma_load_2d_pair(smem + p.off_x + pstage * kXHalf, &tm_x, &full[pstage], kb * GK, xb0);
+      tma_load_2d_pair(smem + p.off_x + pstage * kXHalf, &tm_x, &full[pstage], kb * GKE, xb0);
     }
     ++pu;
     if (++pstage == p.S) { pstage = 0; pphase ^= 1; }
@@ -819,7 +827,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (lane == 0 && leader) {
-      const uint32_t idesc = idesc_bf16_f32(2 * GM, GN);
+      const uint32_t idesc = idesc_f32acc(2 * GM, GN, EL ? 2 : 1);
       const uint32_t s0 = smem_u32(smem);
       int stage = 0, acc = 0, jg_cur = -1;
       uint32_t phase = 0, aphase = 0, wphase = 0;
@@ -839,8 +847,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b_s = s0 + p.off_x + (uint32_t)stage * kXHalf;
 #pragma unroll
           for (int k = 0; k < GK / 16; ++k)
-            mma_bf16_ss_pair(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
-                             smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
+            if constexpr (EL)
+              mma_tf32_ss_pair(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
+                               smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
+            else
+              mma_bf16_ss_pair(d, smem_desc(a_s + k * 32, 16, 1024, SL_SW128),
+                               smem_desc(b_s + k * 32, 16, 1024, SL_SW128), idesc, (kb | k) != 0);
           mma_commit_pair(&empty[stage]);  // frees the stage in both CTAs
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
@@ -910,22 +922,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 typedef void (*GemmFn)(CUtensorMap, CUtensorMap, GemmParams);
 
-template <int YDT>
-GemmFn pick_gemm(int act, bool pair) {
+template <int YDT, int EL>
+GemmFn pick_gemm_el(int act, bool pair) {
   if (pair) switch (act) {
-      case DT_ACT_RELU: return k_tc_gemm_pair<YDT, DT_ACT_RELU>;
-      case DT_ACT_SIGMOID: return k_tc_gemm_pair<YDT, DT_ACT_SIGMOID>;
-      case DT_ACT_TANH: return k_tc_gemm_pair<YDT, DT_ACT_TANH>;
-      case DT_ACT_CLIPPED_RELU: return k_tc_gemm_pair<YDT, DT_ACT_CLIPPED_RELU>;
-      default: return k_tc_gemm_pair<YDT, DT_ACT_IDENTITY>;
+      case DT_ACT_RELU: return k_tc_gemm_pair<YDT, DT_ACT_RELU, EL>;
+      case DT_ACT_SIGMOID: return k_tc_gemm_pair<YDT, DT_ACT_SIGMOID, EL>;
+      case DT_ACT_TANH: return k_tc_gemm_pair<YDT, DT_ACT_TANH, EL>;
+      case DT_ACT_CLIPPED_RELU: return k_tc_gemm_pair<YDT, DT_ACT_CLIPPED_RELU, EL>;
+      default: return k_tc_gemm_pair<YDT, DT_ACT_IDENTITY, EL>;
     }
   switch (act) {
-    case DT_ACT_RELU: return k_tc_gemm<YDT, DT_ACT_RELU>;
-    case DT_ACT_SIGMOID: return k_tc_gemm<YDT, DT_ACT_SIGMOID>;
-    case DT_ACT_TANH: return k_tc_gemm<YDT, DT_ACT_TANH>;
-    case DT_ACT_CLIPPED_RELU: return k_tc_gemm<YDT, DT_ACT_CLIPPED_RELU>;
-    default: return k_tc_gemm<YDT, DT_ACT_IDENTITY>;
+    case DT_ACT_RELU: return k_tc_gemm<YDT, DT_ACT_RELU, EL>;
+    case DT_ACT_SIGMOID: return k_tc_gemm<YDT, DT_ACT_SIGMOID, EL>;
+    case DT_ACT_TANH: return k_tc_gemm<YDT, DT_ACT_TANH, EL>;
+    case DT_ACT_CLIPPED_RELU: return k_tc_gemm<YDT, DT_ACT_CLIPPED_RELU, EL>;
+    default: return k_tc_gemm<YDT, DT_ACT_IDENTITY, EL>;
   }
+}
+GemmFn pick_gemm(int y_dtype, int act, bool pair, int el) {
+  if (el)
+    return y_dtype == DT_BF16 ? pick_gemm_el<DT_BF16, 1>(act, pair) : pick_gemm_el<DT_F32, 1>(act, pair);
+  return y_dtype == DT_BF16 ? pick_gemm_el<DT_BF16, 0>(act, pair) : pick_gemm_el<DT_F32, 0>(act, pair);
 }
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -983,47 +1000,35 @@ void print_gemm_trace(const std::vector<unsigned long long> &h, int grid, int n_
 
 }  // namespace
 
-size_t tc_gemm_ws(const Geo &g, int64_t batch) {
-  const int64_t ldw = round_up(g.q, 8);
-  return (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
-}
+// One phase-2 launch: y[rows x cols] (pitch ldy) = act(x[rows x K] @ wt[cols x K]^T + bias),
+// bf16 operands with 16-byte-aligned pitches, fp32 accumulation. `rg` non-null: wt is the output
+// of the phase-1 regeneration described by rg, launched here first (PDL / fused / wgen
+// schedules apply); null: wt is ready in memory.
+struct GemmCall {
+  const void *x;
+  int64_t ldx, rows, K;
+  const void *wt;
+  int64_t ldw, cols;
+  const float *bias;
+  int act;
+  float act_arg;
+  void *y;
+  int64_t ldy;
+  int y_dtype;
+  const RegenArgs *rg;
+  bool profile;  // the forward's dominant kernel: dt_profile_kernel_events brackets it
+  int el = 0;    // operand element type: 0 bf16 (kind::f16), 1 fp32 (kind::tf32)
+};
 
-int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, const void *xf,
-                    const void *wf, int f_dtype, const float *bias, int act, float act_arg,
-                    void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st) {
-  if (batch == 0) return DT_OK;
-  if (f_dtype != DT_F32 && f_dtype != DT_BF16) {
-    set_error("two-phase tensor-core path: factors must be DT_F32 or DT_BF16");
-    return DT_E_ARG;
-  }
-  if (g.m * g.n > INT32_MAX || g.r_dim > INT32_MAX / 2) {
-    set_error("two-phase tensor-core path: m*n must fit in 32 bits");
-    return DT_E_UNSUPPORTED;
-  }
-  if (ws_bytes < tc_gemm_ws(g, batch)) {
-    set_error("forward workspace too small: need " + std::to_string(tc_gemm_ws(g, batch)));
-    return DT_E_ARG;
-  }
-  const int64_t ldw = round_up(g.q, 8);
-  __nv_bfloat16 *wt = reinterpret_cast<__nv_bfloat16 *>(ws);
-  char *xws = ws + round_up(g.r_dim * ldw * 2, 256);
-
-  // TMA needs a bf16 x whose base and row pitch are 16-byte aligned.
-  const void *xt = x;
-  int64_t ldx = g.q;
-  if (x_dtype != DT_BF16 || (g.q % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
-    ldx = ldw;
-    if (int rc = launch_pack_x(batch, g.q, ldx, x, x_dtype, xws, st)) return rc;
-    xt = xws;
-  }
-
+static int run_gemm(const GemmCall &c, cudaStream_t st) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   GemmParams p{};
-  const int64_t n_bt = (batch + GN - 1) / GN;
-  const int64_t n_jb = (g.r_dim + GM - 1) / GM;
-  p.KB = (int)((g.q + GK - 1) / GK);
+  const int64_t n_bt = (c.rows + GN - 1) / GN;
+  const int64_t n_jb = (c.cols + GM - 1) / GM;
+  const int gke = c.el ? 32 : 64;  // elements per 128-byte k-block
+  p.KB = (int)((c.K + gke - 1) / gke);
   // operand schedule + shared-memory layout (see GemmParams)
   const uint32_t kFixed = 256 /*barriers*/ + 1024 /*alignment slack*/;
   const uint32_t wbytes = (uint32_t)p.KB * kABytes;
@@ -1045,8 +1050,8 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
     p.off_x = wbytes;
     p.S = (int)std::min<uint32_t>(6, (kSmemMax - kFixed - wbytes) / kXBytes);
     p.csize = 1;
-    for (int c : {4, 2})
-      if (c <= want_cs && n_jb >= c) { p.csize = c; break; }
+    for (int cs : {4, 2})
+      if (cs <= want_cs && n_jb >= cs) { p.csize = cs; break; }
   } else {
     p.wres = 0;
     p.stage_bytes = kABytes + kXBytes;
@@ -1057,8 +1062,8 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   p.off_bar = p.off_x + (uint32_t)p.S * p.stage_bytes;
   const uint32_t smem_bytes = p.off_bar + kFixed;
   const int64_t n_jg = (n_jb + p.csize - 1) / p.csize;
-  if (n_jg * n_bt > INT32_MAX / 2) {
-    set_error("two-phase tensor-core path: too many tiles");
+  if (n_jg * n_bt > INT32_MAX / 2 || c.cols > INT32_MAX / 2 || c.ldy > INT32_MAX) {
+    set_error("tensor-core GEMM: too many tiles");
     return DT_E_UNSUPPORTED;
   }
   p.n_jb = (int)n_jb;
@@ -1086,36 +1091,35 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   // grid barrier ~1.6 us and one 64-row tile per CTA ~3.3 us), so off by default.
   const int want_fused = getenv("DEEPTHIN_GEMM_FUSED") ? atoi(getenv("DEEPTHIN_GEMM_FUSED")) : 0;
 
-  const int64_t a_rows = (g.q * g.r_dim + g.n - 1) / g.n;
-  const dim3 rgrid((unsigned)((a_rows + RG_R - 1) / RG_R), (unsigned)((g.n + RG_C - 1) / RG_C));
-  RegenArgs rg;
-  rg.q = g.q; rg.r_dim = g.r_dim; rg.ldw = ldw;
-  rg.rank = (int)g.rank; rg.n = (int)g.n; rg.a_rows = (int)a_rows; rg.f_dtype = f_dtype;
-  rg.xf = xf; rg.wf = wf; rg.wt = wt;
-
   CUtensorMap tm_w, tm_x;
-  if (int rc = encode_tensor_map_2d(&tm_w, DT_BF16, wt, (uint64_t)g.q, (uint64_t)g.r_dim,
-                                    (uint64_t)ldw * 2, GK, GM, true))
+  const int tdt = c.el ? DT_F32 : DT_BF16, esz = c.el ? 4 : 2;
+  if (int rc = encode_tensor_map_2d(&tm_w, tdt, const_cast<void *>(c.wt), (uint64_t)c.K,
+                                    (uint64_t)c.cols, (uint64_t)c.ldw * esz, gke, GM, true))
     return rc;
-  if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(xt), (uint64_t)g.q,
-                                    (uint64_t)batch, (uint64_t)ldx * 2, GK, GN / p.csize, true))
+  if (int rc = encode_tensor_map_2d(&tm_x, tdt, const_cast<void *>(c.x), (uint64_t)c.K,
+                                    (uint64_t)c.rows, (uint64_t)c.ldx * esz, gke, GN / p.csize, true))
     return rc;
-  p.batch = batch;
-  p.r_dim = (int)g.r_dim;
-  p.ldy = (int)g.r_dim;
+  p.batch = c.rows;
+  p.r_dim = (int)c.cols;
+  p.ldy = (int)c.ldy;
   p.trace = tbuf;
   static const int dbg_gemm = getenv("DEEPTHIN_DBG_GEMM") ? atoi(getenv("DEEPTHIN_DBG_GEMM")) : 0;
   p.dbg = dbg_gemm;
-  p.bias = bias;
-  p.y = y;
-  p.arg = act_arg;
-  p.rg = rg;
-  // fused phase 1: 64-row tiles when that makes one tile per CTA, else 32-row tiles
-  p.rg_rows = ((a_rows + 63) / 64) * rgrid.y <= (int64_t)grid ? 64 : 32;
-  p.rg_ux = (int)((a_rows + p.rg_rows - 1) / p.rg_rows);
-  p.rg_uy = (int)rgrid.y;
-  const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
-  GemmFn fn = y_dtype == DT_BF16 ? pick_gemm<DT_BF16>(eact, pair) : pick_gemm<DT_F32>(eact, pair);
+  p.bias = c.bias;
+  p.y = c.y;
+  p.arg = c.act_arg;
+  dim3 rgrid(1, 1);
+  if (c.rg) {
+    const RegenArgs &rg = *c.rg;
+    rgrid = dim3((unsigned)((rg.a_rows + RG_R - 1) / RG_R), (unsigned)((rg.n + RG_C - 1) / RG_C));
+    p.rg = rg;
+    // fused phase 1: 64-row tiles when that makes one tile per CTA, else 32-row tiles
+    p.rg_rows = ((rg.a_rows + 63) / 64) * (int64_t)rgrid.y <= (int64_t)grid ? 64 : 32;
+    p.rg_ux = (int)((rg.a_rows + p.rg_rows - 1) / p.rg_rows);
+    p.rg_uy = (int)rgrid.y;
+  }
+  const int eact = c.act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : c.act;
+  GemmFn fn = pick_gemm(c.y_dtype, eact, pair, c.el);
   DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
 
   static const int use_pdl = getenv("DEEPTHIN_PDL") ? atoi(getenv("DEEPTHIN_PDL")) : 1;
@@ -1131,7 +1135,7 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
       attr[na].id = cudaLaunchAttributeCooperative;
       attr[na].val.cooperative = 1;
       ++na;
-    } else if (use_pdl && !p.wgen) {  // (wgen: nothing to overlap, and no griddep wait)
+    } else if (use_pdl && c.rg && !p.wgen) {  // overlap the prologue with phase 1
       attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[na].val.programmaticStreamSerializationAllowed = 1;
       ++na;
@@ -1158,20 +1162,20 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   // instruction-latency-bound on 8 warps and its one-pass code runs from a cold I-cache.
   const int want_wgen = getenv("DEEPTHIN_GEMM_WGEN") ? atoi(getenv("DEEPTHIN_GEMM_WGEN")) : 0;
   p.off_fs = p.off_x + pre_stages * p.stage_bytes;
-  p.wgen = (pair && want_wgen && p.cpj > 0 && g.rank <= 64 && dbg_phase == 0 &&
-            p.off_fs + wgen_stage_bytes((int)g.q, (int)g.rank, (int)g.n) <= p.off_bar)
+  p.wgen = (c.rg && !c.el && pair && want_wgen && p.cpj > 0 && c.rg->rank <= 64 && dbg_phase == 0 &&
+            p.off_fs + wgen_stage_bytes((int)c.rg->q, c.rg->rank, c.rg->n) <= p.off_bar)
                ? 1
                : 0;
   p.off_rg = wbytes >= sizeof(RegenSmem) ? 0u : p.off_x + pre_stages * p.stage_bytes;
   const bool rg_fits = p.off_rg + sizeof(RegenSmem) <= p.off_bar;
-  cudaEvent_t ev_b, ev_a;  // dt_profile_kernel_events: bracket the GEMM launch
-  profile_next(&ev_b, &ev_a);
+  cudaEvent_t ev_b = nullptr, ev_a = nullptr;  // dt_profile_kernel_events: bracket the GEMM
+  if (c.profile) profile_next(&ev_b, &ev_a);
   bool done = false;
   if (p.wgen) {
     if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
     DT_CUDA_CHECK(launch(false));
     done = true;
-  } else if (pair && want_fused && rg_fits && dbg_phase == 0) {
+  } else if (c.rg && pair && want_fused && rg_fits && dbg_phase == 0) {
     if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
     const cudaError_t e = launch(true);
     if (e == cudaSuccess) {
@@ -1184,11 +1188,11 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
     }
   }
   if (!done) {
-    if (dbg_phase != 2) {
-      k_regen_wt<<<rgrid, 256, 0, st>>>(rg);
+    if (c.rg && dbg_phase != 2) {
+      k_regen_wt<<<rgrid, 256, 0, st>>>(*c.rg);
       if (int rc = check_launch("regen_wt")) return rc;
     }
-    if (dbg_phase == 1) return DT_OK;
+    if (c.rg && dbg_phase == 1) return DT_OK;
     if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
     DT_CUDA_CHECK(launch(false));
   }
@@ -1201,8 +1205,100 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
     cudaFree(tbuf);
     print_gemm_trace(h, grid, p.items);
   }
-  if (act == DT_ACT_SOFTMAX) return launch_row_softmax(batch, g.r_dim, y, y_dtype, st);
+  if (c.act == DT_ACT_SOFTMAX) return launch_row_softmax(c.rows, c.cols, c.y, c.y_dtype, st);
   return DT_OK;
+}
+
+// Factored reuse forward on the tensor cores (n | q, s = q/n; kernel.py:1-16 with one phase):
+//   P  (B*s x rank) = x.view(B*s, n) @ wf^T        GEMM 1: bf16 operands, fp32 P
+//   y  (B x r_dim)  = P.view(B, s*rank) @ XF2^T    GEMM 2: kind::tf32 on the fp32 P and the
+//                                                  fp32 master xf viewed (r_dim x s*rank)
+// 2*B*s*rank*(n + r_dim) flops instead of the dense 2*B*q*r_dim, and no intermediate bf16
+// rounding (P stays fp32; rounding it to bf16 measured 2.5e-3 rel_error at config 1 — over the
+// 2e-3 contract — while tf32 products keep the two-GEMM error at the operand-rounding level).
+// Needs aligned views: n % 8 == 0 (bf16 rows), s*rank % 4 == 0 (fp32 rows); fp32 factors.
+static bool reuse_factored_ok(const Geo &g) {
+  const int want = getenv("DEEPTHIN_REUSE_FACTORED") ? atoi(getenv("DEEPTHIN_REUSE_FACTORED")) : 1;
+  return want && g.reuse && g.n % 8 == 0 && (g.s * g.rank) % 4 == 0;
+}
+static size_t reuse_factored_ws(const Geo &g, int64_t batch) {
+  return (size_t)round_up(g.rank * g.n * 2, 256) + (size_t)round_up(batch * g.s * g.rank * 4, 256) +
+         (size_t)round_up(batch * g.q * 2, 256);
+}
+
+size_t tc_gemm_ws(const Geo &g, int64_t batch) {
+  const int64_t ldw = round_up(g.q, 8);
+  const size_t two_phase =
+      (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
+  return std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0);
+}
+
+int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, const void *xf,
+                    const void *wf, int f_dtype, const float *bias, int act, float act_arg,
+                    void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st) {
+  if (batch == 0) return DT_OK;
+  if (f_dtype != DT_F32 && f_dtype != DT_BF16) {
+    set_error("tensor-core path: factors must be DT_F32 or DT_BF16");
+    return DT_E_ARG;
+  }
+  if (g.m * g.n > INT32_MAX || g.r_dim > INT32_MAX / 2) {
+    set_error("tensor-core path: m*n must fit in 32 bits");
+    return DT_E_UNSUPPORTED;
+  }
+  if (ws_bytes < tc_gemm_ws(g, batch)) {
+    set_error("forward workspace too small: need " + std::to_string(tc_gemm_ws(g, batch)));
+    return DT_E_ARG;
+  }
+
+  if (reuse_factored_ok(g) && f_dtype == DT_F32) {
+    // ---- factored reuse path: two GEMMs ----
+    char *cur = ws;
+    auto take = [&](int64_t bytes) {
+      char *r = cur;
+      cur += round_up(bytes, 256);
+      return r;
+    };
+    char *wf16 = take(g.rank * g.n * 2);
+    float *P = reinterpret_cast<float *>(take(batch * g.s * g.rank * 4));
+    char *x_ws = take(batch * g.q * 2);
+    if (int rc = launch_cast_bf16(g.rank * g.n, reinterpret_cast<const float *>(wf),
+                                  reinterpret_cast<uint16_t *>(wf16), st))
+      return rc;
+    const void *xt = x;
+    if (x_dtype != DT_BF16 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
+      if (int rc = launch_pack_x(batch, g.q, g.q, x, x_dtype, x_ws, st)) return rc;
+      xt = x_ws;
+    }
+    const int64_t SR = g.s * g.rank;
+    GemmCall c1{xt, g.n, batch * g.s, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
+                P, g.rank, DT_F32, nullptr, false, 0};
+    if (int rc = run_gemm(c1, st)) return rc;
+    GemmCall c2{P, SR, batch, SR, xf, SR, g.r_dim, bias, act, act_arg,
+                y, g.r_dim, y_dtype, nullptr, true, 1};
+    return run_gemm(c2, st);
+  }
+
+  // ---- two-phase: W^T regenerated into the workspace, then the GEMM ----
+  const int64_t ldw = round_up(g.q, 8);
+  __nv_bfloat16 *wt = reinterpret_cast<__nv_bfloat16 *>(ws);
+  char *xws = ws + round_up(g.r_dim * ldw * 2, 256);
+  // TMA needs a bf16 x whose base and row pitch are 16-byte aligned.
+  const void *xt = x;
+  int64_t ldx = g.q;
+  if (x_dtype != DT_BF16 || (g.q % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
+    ldx = ldw;
+    if (int rc = launch_pack_x(batch, g.q, ldx, x, x_dtype, xws, st)) return rc;
+    xt = xws;
+  }
+  RegenArgs rg;
+  rg.q = g.q; rg.r_dim = g.r_dim; rg.ldw = ldw;
+  rg.rank = (int)g.rank; rg.n = (int)g.n;
+  rg.a_rows = (int)((g.q * g.r_dim + g.n - 1) / g.n);
+  rg.f_dtype = f_dtype;
+  rg.xf = xf; rg.wf = wf; rg.wt = wt;
+  GemmCall c{xt, ldx, batch, g.q, wt, ldw, g.r_dim, bias, act, act_arg,
+             y, g.r_dim, y_dtype, &rg, true};
+  return run_gemm(c, st);
 }
 
 }  // namespace dt

@@ -46,6 +46,31 @@ def bf16_emulated(d, plan, bias):
     return d["x"] @ w + bias
 
 
+def factored_path(plan):
+    """The bf16 tensor-core path computes reuse geometries in factored form when the views are
+    16-byte aligned (k_tc_gemm.cu reuse_factored_ok)."""
+    if plan.q % plan.n:
+        return False
+    s = plan.q // plan.n
+    return plan.n % 8 == 0 and (s * plan.rank) % 4 == 0
+
+
+def bf16_factored_emulated(d, plan, bias):
+    """The factored reuse contract in f64: P = x.view(B*s, n) @ wf^T (bf16 operands, fp32 P),
+    then y = P.view(B, s*rank) @ XF2^T + bias on tf32 products, XF2 = xf.view(r_dim, s*rank).
+    With bf16-valued inputs the only rounding left is P's tf32 rounding (2^-11 relative)."""
+    x, xf, wf = d["x"], d["xf"], d["wf"]
+    s = plan.q // plan.n
+    b = x.shape[0]
+    p = (x.reshape(b * s, plan.n) @ wf.T).reshape(b, s * plan.rank)
+    xf2 = xf[: plan.r_dim * s].reshape(plan.r_dim, s * plan.rank)
+    return p @ xf2.T + bias
+
+
+def bf16_contract(d, plan, bias):
+    return bf16_factored_emulated(d, plan, bias) if factored_path(plan) else bf16_emulated(d, plan, bias)
+
+
 def check_activation(y_act, y_pre, act, arg=20.0):
     """The fused activation epilogue, checked on the kernel's own pre-activations."""
     pre = y_pre.detach().double().cpu().numpy() if hasattr(y_pre, "detach") else y_pre
@@ -175,12 +200,13 @@ def test_tc_general_geometries(geo, path):
     (1000, 300, 8, 125, 2400, 33),     # reuse with n % 8 != 0 (scalar W^T stores)
     (13, 17, 3, 5, 45, 9),             # tiny: q < 16, K padded by TMA zero fill
 ])
-def test_tc_two_phase_reuse_and_edge_geometries(geo):
+def test_tc_reuse_and_edge_geometries(geo):
+    # reuse geometries with aligned views take the factored two-GEMM form, the rest two-phase
     q, r_dim, rank, n, m, batch = geo
     plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=11, rnd=O.round_bf16)
     ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
     y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
-    assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3
+    assert O.rel_error(y, bf16_contract(d, plan, d["bias"])) <= 1e-3
     if batch * r_dim >= 10_000:
         assert O.rel_error(y, ref) <= BF16_TOL
 
@@ -300,4 +326,4 @@ def test_tc_alternative_pair_schedules(variant, monkeypatch):
         q, r_dim, rank, n, m, batch = geo
         plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=6, rnd=O.round_bf16)
         y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
-        assert O.rel_error(y, bf16_emulated(d, plan, d["bias"])) <= 1e-3, geo
+        assert O.rel_error(y, bf16_contract(d, plan, d["bias"])) <= 1e-3, geo
