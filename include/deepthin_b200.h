@@ -87,6 +87,13 @@ int64_t dt_launch_counter(void);
  * Events are cudaEvent_t handles created by the caller. No reference counterpart: used by
  * bench.py for the roofline of the dominant kernel. */
 int dt_profile_kernel_events(void *const *before, void *const *after, int n);
+/* Inference pipelining (this thread): with enable = 1, consecutive bf16 tensor-core forwards
+ * on one stream overlap each call's W regeneration with the previous call's GEMM (programmatic
+ * dependent launch; W^T alternates between two workspace slots). The caller promises that the
+ * factor buffers are not written while pipelined calls are in flight on the stream (a forward
+ * never waits for a factor update launched after the previous forward). Every call still
+ * regenerates its own W^T. Default 0. No reference counterpart (kernel.py has no pipelining). */
+int dt_set_forward_pipeline(int enable);
 
 /* ---- geometry (host-only, no GPU needed) ---------------------------------- */
 /* planner.py:38-47 LayerPlan.__post_init__ validation. */

@@ -11,8 +11,8 @@ from .errors import (ArgumentError, CudaError, DeepThinError, DimensionError,
                      UnsupportedConfigurationError)
 from .factor import FactorPair, decompress, init_factors, phase, phase_count, relayout_index
 from .grad import Gradients, layer_backward, loss_and_grad
-from .kernel import (ACTIVATIONS, OpCount, ReuseTable, fused_matmul, layer_forward, op_count,
-                     predict_reuse)
+from .kernel import (ACTIVATIONS, OpCount, ReuseTable, forward_pipeline, fused_matmul,
+                     layer_forward, op_count, predict_reuse)
 from .planner import LayerPlan, baseline_plan
 from .train import DeepThinLayer, train_step
 
@@ -21,7 +21,7 @@ __version__ = "0.1.0"
 __all__ = [
     "ACTIVATIONS", "ArgumentError", "CudaError", "DeepThinError", "DeepThinLayer",
     "DimensionError", "FactorPair", "Gradients", "LayerPlan", "OpCount", "ReuseTable",
-    "UnsupportedConfigurationError", "baseline_plan", "decompress", "fused_matmul",
+    "UnsupportedConfigurationError", "baseline_plan", "decompress", "forward_pipeline", "fused_matmul",
     "init_factors", "layer_backward", "layer_forward", "loss_and_grad", "make_rng",
     "max_abs_diff", "op_count", "phase", "phase_count", "predict_reuse", "rel_error",
     "relayout_index", "sample_normal", "spawn_rngs", "train_step",

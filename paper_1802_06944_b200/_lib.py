@@ -21,7 +21,7 @@ ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "dt_version", "dt_last_error", "dt_launch_counter", "dt_profile_kernel_events", "dt_plan_validate", "dt_plan_query", "dt_phase",
+    "dt_version", "dt_last_error", "dt_launch_counter", "dt_profile_kernel_events", "dt_set_forward_pipeline", "dt_plan_validate", "dt_plan_query", "dt_phase",
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
@@ -51,6 +51,7 @@ def _declare(lib):
         "dt_last_error": ([], C.c_char_p),
         "dt_launch_counter": ([], I64),
         "dt_profile_kernel_events": ([C.POINTER(VP), C.POINTER(VP), i], i),
+        "dt_set_forward_pipeline": ([i], i),
         "dt_plan_validate": ([P], i),
         "dt_plan_query": ([P, C.POINTER(PlanInfo)], i),
         "dt_phase": ([P, I64, C.POINTER(I64)], i),

@@ -80,6 +80,7 @@ int check_act(int act) {
 thread_local void *const *g_prof_before = nullptr;
 thread_local void *const *g_prof_after = nullptr;
 thread_local int g_prof_n = 0, g_prof_used = 0;
+thread_local bool g_pipeline = false;
 
 }  // namespace
 
@@ -93,6 +94,8 @@ void dt::profile_next(cudaEvent_t *before, cudaEvent_t *after) {
   }
 }
 
+bool dt::forward_pipeline() { return g_pipeline; }
+
 extern "C" {
 
 const char *dt_version(void) { return "deepthin_b200 0.1.0 (sm_100a)"; }
@@ -100,6 +103,11 @@ const char *dt_version(void) { return "deepthin_b200 0.1.0 (sm_100a)"; }
 const char *dt_last_error(void) { return g_last_error.c_str(); }
 
 int64_t dt_launch_counter(void) { return launch_count(); }
+
+int dt_set_forward_pipeline(int enable) {
+  g_pipeline = enable != 0;
+  return DT_OK;
+}
 
 int dt_profile_kernel_events(void *const *before, void *const *after, int n) {
   if (n < 0 || (n > 0 && (!before || !after))) {

@@ -72,6 +72,8 @@ size_t tc_gemm_ws(const Geo &g, int64_t batch);
 // dt_profile_kernel_events: events to record around the next dominant-kernel launch on this
 // thread (both null when disarmed / exhausted).
 void profile_next(cudaEvent_t *before, cudaEvent_t *after);
+// dt_set_forward_pipeline state of this thread.
+bool forward_pipeline();
 
 // Every kernel launch goes through check_launch, which also counts it (dt_launch_counter).
 int check_launch(const char *what);

@@ -28,6 +28,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -62,6 +64,7 @@ constexpr int RG_RMAX = 64;                       // fused kernel: up to 64-row 
 struct RegenArgs {
   int64_t q, r_dim, ldw;
   int rank, n, a_rows, f_dtype;
+  int chain;  // pipelined forward: complete only after the previous grid (griddepcontrol.wait)
   const void *xf, *wf;
   __nv_bfloat16 *wt;
 };
@@ -98,6 +101,7 @@ struct GemmParams {
   int wgen;
   uint32_t off_fs;
   RegenArgs rg;
+  int chain;  // pipelined forward: let the next call's phase 1 launch right away
   int dbg;  // DEEPTHIN_DBG_GEMM (timing experiments only): 1 skip y stores, 2 x loads after the first S stages skipped, 4 skip TMEM loads
   unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps
 };
@@ -133,6 +137,19 @@ __device__ __forceinline__ float ldf(const FT *p) {
     return __bfloat162float(*p);
 }
 
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
+                                                 uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 // CTA tile: RG_R aux rows x RG_C aux columns of I = xf @ wf, the factors staged through shared
 // memory RG_K ranks at a time (coalesced loads, all in flight together; xf transposed so a
 // thread's 8 rows at one rank are 32 contiguous bytes). Thread: 8 consecutive rows
@@ -232,14 +249,107 @@ __device__ __forceinline__ void regen_tile(const RegenArgs &g, int tid, int bx, 
   }
 }
 
+// Tensor-core form of one regeneration tile (RG_R x RG_C): the products on the warp-level
+// tensor cores (mma.sync m16n8k8, tf32 operands rounded from the factors — bf16-valued factors
+// are exact — fp32 accumulate); staging strides make the fragment reads conflict-free. Warp w:
+// m-tile w & 1, n-tiles 4*(w >> 1) .. +3. Accumulator pairs go straight to W^T (= I.ravel()
+// when ldw == q) as 4-byte bf16x2 stores.
+struct RegenSmemTC {
+  uint32_t xs[RG_R][RG_K + 4];   // tf32 bits; row stride = 4 (mod 8): conflict-free A reads
+  uint32_t ws[RG_K][RG_C + 8];   // row stride / 8 odd: conflict-free B reads
+};
+template <typename FT>
+__device__ __forceinline__ void regen_tile_tc(const RegenArgs &g, int tid, int bx, int by,
+                                              RegenSmemTC &sm) {
+  static_assert(RG_R == 32 && RG_C == 128 && RG_K == 32, "warp tiling below");
+  const FT *xf = reinterpret_cast<const FT *>(g.xf);
+  const FT *wf = reinterpret_cast<const FT *>(g.wf);
+  const int lane = tid % 32, w = tid / 32, gr = lane >> 2, tq = lane & 3;
+  const int mt = w & 1, nt0 = 4 * (w >> 1);
+  const int a0 = bx * RG_R, c0 = by * RG_C;
+  const int rank = g.rank, n = g.n, a_rows = g.a_rows;
+  float d[4][4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) d[t][e] = 0.f;
+  for (int k0 = 0; k0 < rank; k0 += RG_K) {
+    const int kc = min(RG_K, rank - k0);
+    constexpr int NX = RG_R * RG_K / 256, NW = RG_K * RG_C / 256;
+    float xv[NX], wv[NW];
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const int e = tid + 256 * u, r = e / RG_K, k = e % RG_K;
+      xv[u] = (a0 + r < a_rows && k < kc) ? ldf(xf + (int64_t)(a0 + r) * rank + k0 + k) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int e = tid + 256 * u, k = e / RG_C, c = e % RG_C;
+      wv[u] = (k < kc && c0 + c < n) ? ldf(wf + (int64_t)(k0 + k) * n + c0 + c) : 0.f;
+    }
+    if (k0 > 0) __syncthreads();  // the previous chunk's fragments are read
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const int e = tid + 256 * u;
+      sm.xs[e / RG_K][e % RG_K] = to_tf32(xv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int e = tid + 256 * u;
+      sm.ws[e / RG_C][e % RG_C] = to_tf32(wv[u]);
+    }
+    __syncthreads();
+    for (int ks = 0; ks < (kc + 7) / 8; ++ks) {
+      uint32_t af[4];
+      const uint32_t *xr = &sm.xs[mt * 16 + gr][ks * 8 + tq];
+      af[0] = xr[0];
+      af[1] = xr[8 * (RG_K + 4)];
+      af[2] = xr[4];
+      af[3] = xr[8 * (RG_K + 4) + 4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t *wr = &sm.ws[ks * 8 + tq][(nt0 + t) * 8 + gr];
+        mma_m16n8k8_tf32(d[t], af, wr[0], wr[4 * (RG_C + 8)]);
+      }
+    }
+  }
+  const int64_t q = g.q, total = q * g.r_dim;
+  const bool flat = g.ldw == q && (n & 1) == 0;  // W^T == I.ravel(): bf16x2 stores
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int c = c0 + (nt0 + t) * 8 + 2 * tq;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int a = a0 + mt * 16 + gr + 8 * h;
+      if (a >= a_rows || c >= n) continue;
+      const float v0 = d[t][2 * h], v1 = d[t][2 * h + 1];
+      const int64_t f = (int64_t)a * n + c;
+      if (flat && c + 1 < n && f + 2 <= total) {
+        *reinterpret_cast<__nv_bfloat162 *>(g.wt + f) = __floats2bfloat162_rn(v0, v1);
+      } else {
+        for (int e = 0; e < 2; ++e) {
+          const int64_t fe = f + e;
+          if (c + e < n && fe < total) {
+            const int64_t j = fe / q, i = fe - j * q;
+            g.wt[j * g.ldw + i] = __float2bfloat16_rn(e ? v1 : v0);
+          }
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_regen_wt(const RegenArgs g) {
   griddep_launch_dependents();  // the GEMM may start its prologue now
-  __shared__ __align__(16) RegenSmem sm;
-  auto sync = [] { __syncthreads(); };
+  __shared__ __align__(16) RegenSmemTC sm;
   if (g.f_dtype == DT_F32)
-    regen_tile<float, RG_R>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm, sync);
+    regen_tile_tc<float>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm);
   else
-    regen_tile<__nv_bfloat16, RG_R>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm, sync);
+    regen_tile_tc<__nv_bfloat16>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm);
+  // pipelined: this grid overlapped the previous forward's GEMM (it writes the other W^T
+  // slot); completing only after that grid keeps the next GEMM — which waits on this grid —
+  // ordered after it, so W^T slots and outputs are reused safely.
+  if (g.chain) griddep_wait();
 }
 
 // ---- phase 2 --------------------------------------------------------------------------------
@@ -283,6 +393,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) gtrace(p, 1);
+  if (p.chain) griddep_launch_dependents();  // the next forward's phase 1 may start
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -442,19 +553,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // factors — bf16-valued factors are exact — fp32 accumulate), each accumulator element scattered
 // to (j, i) = divmod(a*n + c - j0*q, q) (factor.py:87-93). Factor operands are staged as fp32
 // through shared memory with strides that make the fragment reads bank-conflict-free.
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
-                                                 uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
-      "{%8, %9}, {%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 // byte offset of W-block element (j, i): 64-column k-blocks of 128 rows x 128 B, 16-byte chunks
 // XOR-swizzled by (row mod 8) — the layout TMA SWIZZLE_128B produces for the GEMM's A operand
 __device__ __forceinline__ uint32_t wsw_off(uint32_t j, uint32_t i) {
@@ -714,6 +812,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) gtrace(p, 1);
+  if (p.chain) griddep_launch_dependents();  // the next forward's phase 1 may start
 
   // ---------------- TMA producer state (warp 0, lane 0) ----------------
   // Issue order for the first column group: the first x stages before W^T is known to be
@@ -1042,7 +1141,11 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
     p.wres = 1;
     p.stage_bytes = kXHalf;
     p.off_x = wbytes;
-    p.S = (int)std::min<uint32_t>(8, (kSmemMax - kFixed - wbytes) / kXHalf);
+    // stages: DEEPTHIN_GEMM_STAGES caps them (fewer stages leave shared memory for a
+    // co-resident phase-1 CTA of the next pipelined forward)
+    static const int max_stages = getenv("DEEPTHIN_GEMM_STAGES") ? atoi(getenv("DEEPTHIN_GEMM_STAGES")) : 8;
+    p.S = (int)std::min<uint32_t>((uint32_t)std::max(4, max_stages),
+                                  (kSmemMax - kFixed - wbytes) / kXHalf);
     p.csize = 2;
   } else if (want_wres && p.KB <= 8 && wbytes + 3 * kXBytes + kFixed <= (uint32_t)kSmemMax) {
     p.wres = 1;
@@ -1113,6 +1216,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
     const RegenArgs &rg = *c.rg;
     rgrid = dim3((unsigned)((rg.a_rows + RG_R - 1) / RG_R), (unsigned)((rg.n + RG_C - 1) / RG_C));
     p.rg = rg;
+    p.chain = rg.chain;
     // fused phase 1: 64-row tiles when that makes one tile per CTA, else 32-row tiles
     p.rg_rows = ((rg.a_rows + 63) / 64) * (int64_t)rgrid.y <= (int64_t)grid ? 64 : 32;
     p.rg_ux = (int)((rg.a_rows + p.rg_rows - 1) / p.rg_rows);
@@ -1120,7 +1224,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   }
   const int eact = c.act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : c.act;
   GemmFn fn = pick_gemm(c.y_dtype, eact, pair, c.el);
-  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
 
   static const int use_pdl = getenv("DEEPTHIN_PDL") ? atoi(getenv("DEEPTHIN_PDL")) : 1;
   cudaLaunchConfig_t cfg{};
@@ -1189,7 +1293,20 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   }
   if (!done) {
     if (c.rg && dbg_phase != 2) {
-      k_regen_wt<<<rgrid, 256, 0, st>>>(*c.rg);
+      if (c.rg->chain) {  // pipelined: phase 1 overlaps the previous forward's GEMM
+        cudaLaunchConfig_t rcfg{};
+        rcfg.gridDim = rgrid;
+        rcfg.blockDim = dim3(256);
+        rcfg.stream = st;
+        cudaLaunchAttribute ra[1];
+        ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        ra[0].val.programmaticStreamSerializationAllowed = 1;
+        rcfg.attrs = ra;
+        rcfg.numAttrs = 1;
+        DT_CUDA_CHECK(cudaLaunchKernelEx(&rcfg, k_regen_wt, *c.rg));
+      } else {
+        k_regen_wt<<<rgrid, 256, 0, st>>>(*c.rg);
+      }
       if (int rc = check_launch("regen_wt")) return rc;
     }
     if (c.rg && dbg_phase == 1) return DT_OK;
@@ -1226,10 +1343,19 @@ static size_t reuse_factored_ws(const Geo &g, int64_t batch) {
          (size_t)round_up(batch * g.q * 2, 256);
 }
 
+// W^T slot of a pipelined forward: consecutive calls with one workspace alternate between two
+// slots, so a call's phase 1 never overwrites the W^T the previous call's GEMM is reading.
+static int pipeline_slot(const void *ws) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, unsigned> next;
+  std::lock_guard<std::mutex> lock(mu);
+  return (int)(next[ws]++ & 1u);
+}
+
 size_t tc_gemm_ws(const Geo &g, int64_t batch) {
   const int64_t ldw = round_up(g.q, 8);
-  const size_t two_phase =
-      (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
+  const size_t two_phase =  // two W^T slots (pipelined forwards alternate) + packed x
+      2 * (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
   return std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0);
 }
 
@@ -1280,8 +1406,11 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
 
   // ---- two-phase: W^T regenerated into the workspace, then the GEMM ----
   const int64_t ldw = round_up(g.q, 8);
-  __nv_bfloat16 *wt = reinterpret_cast<__nv_bfloat16 *>(ws);
-  char *xws = ws + round_up(g.r_dim * ldw * 2, 256);
+  const bool pipe = forward_pipeline();
+  const int64_t slot_bytes = round_up(g.r_dim * ldw * 2, 256);
+  __nv_bfloat16 *wt =
+      reinterpret_cast<__nv_bfloat16 *>(ws + (pipe ? pipeline_slot(ws) : 0) * slot_bytes);
+  char *xws = ws + 2 * slot_bytes;
   // TMA needs a bf16 x whose base and row pitch are 16-byte aligned.
   const void *xt = x;
   int64_t ldx = g.q;
@@ -1296,6 +1425,7 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   rg.a_rows = (int)((g.q * g.r_dim + g.n - 1) / g.n);
   rg.f_dtype = f_dtype;
   rg.xf = xf; rg.wf = wf; rg.wt = wt;
+  rg.chain = pipe ? 1 : 0;
   GemmCall c{xt, ldx, batch, g.q, wt, ldw, g.r_dim, bias, act, act_arg,
              y, g.r_dim, y_dtype, &rg, true};
   return run_gemm(c, st);

@@ -111,6 +111,23 @@ def resolve_mma(mma, x: torch.Tensor, plan) -> int:
     return _lib.DT_MMA_BF16 if mma == "bf16" else _lib.DT_MMA_FFMA
 
 
+class forward_pipeline:
+    """Context manager / switch for inference pipelining on this thread (dt_set_forward_pipeline):
+    consecutive bf16 tensor-core forwards on one stream overlap each call's W regeneration with
+    the previous call's GEMM. Only for factors that are not updated while the calls run."""
+
+    def __init__(self, enable: bool = True):
+        self.enable = enable
+
+    def __enter__(self):
+        _lib.lib().dt_set_forward_pipeline(1 if self.enable else 0)
+        return self
+
+    def __exit__(self, *exc):
+        _lib.lib().dt_set_forward_pipeline(0)
+        return False
+
+
 def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float, y: torch.Tensor,
                  mma: int, fused: bool = False) -> None:
     """Raw stream-ordered dt_forward on device tensors (no validation beyond the ABI's).

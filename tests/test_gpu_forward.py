@@ -327,3 +327,19 @@ def test_tc_alternative_pair_schedules(variant, monkeypatch):
         plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=6, rnd=O.round_bf16)
         y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16")
         assert O.rel_error(y, bf16_contract(d, plan, d["bias"])) <= 1e-3, geo
+
+
+def test_tc_forward_pipeline_matches_serial():
+    # pipelined consecutive forwards (phase 1 of call i+1 overlapping the GEMM of call i, W^T
+    # slots alternating) give the same bits as serial calls, also when y buffers are reused
+    plan, d, fp = make_case(440, 2048, 24, 320, 2816, 1024, seed=12, rnd=O.round_bf16)
+    xs = [gpu_x(d["x"], torch.bfloat16)]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    xs += [torch.randn(1024, 440, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4)]
+    b = torch.tensor(d["bias"], dtype=torch.float32, device="cuda")
+    serial = [D.layer_forward(x, fp, b, mma="bf16") for x in xs]
+    with D.forward_pipeline():
+        piped = [D.layer_forward(x, fp, b, mma="bf16") for x in xs for _ in range(2)]
+    torch.cuda.synchronize()
+    for k, x in enumerate(xs):
+        assert torch.equal(piped[2 * k], serial[k]) and torch.equal(piped[2 * k + 1], serial[k]), k
