@@ -307,7 +307,7 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
 size_t dt_backward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) {
   Geo g;
   if (make_geo(plan, &g) || batch < 0) return 0;
-  (void)mma;
+  if (mma == DT_MMA_BF16 && tc_backward_ok(g)) return tc_backward_ws(g, batch);
   return ffma_backward_ws(g, batch);
 }
 
@@ -335,6 +335,11 @@ int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int 
     set_error("unknown mma kind " + std::to_string(mma));
     return DT_E_ARG;
   }
+  // bf16 / tf32 tensor cores for reuse geometries (factored); every other case runs the exact
+  // fp32 FFMA backward
+  if (mma == DT_MMA_BF16 && tc_backward_ok(g))
+    return tc_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
+                       d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
   return ffma_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
                        d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
 }

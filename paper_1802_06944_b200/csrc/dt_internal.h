@@ -41,6 +41,12 @@ int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, 
                     float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st);
 size_t mse_ws(int64_t rows, int64_t cols);
 int launch_sgd(int64_t count, float *p, const float *g, float lr, cudaStream_t st);
+int launch_act_grad(int64_t count, const float *up, const float *pre, int act, float act_arg,
+                    float *out, cudaStream_t st);
+// fixed-order column sums of a rows x cols fp32 matrix (partials in `part`, colsum_ws bytes)
+size_t colsum_ws(int64_t rows, int64_t cols);
+int launch_colsum(int64_t rows, int64_t cols, const float *g, float *out, float *part,
+                  cudaStream_t st);
 
 // ---- tcgen05 tensor-core path: k_tc_general.cu ---------------------------------
 // `packed` (nullable): regeneration operands from tc_general_pack; else packed into ws.
@@ -68,6 +74,14 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
                     const void *wf, int f_dtype, const float *bias, int act, float act_arg,
                     void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st);
 size_t tc_gemm_ws(const Geo &g, int64_t batch);
+// Tensor-core backward of reuse geometries in factored form (cuBLASLt for the plain GEMMs over
+// transposed views); returns DT_E_UNSUPPORTED when the geometry does not qualify.
+bool tc_backward_ok(const Geo &g);
+int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                const float *wf, const float *bias, int act, float act_arg,
+                const float *upstream, float *d_xf, float *d_wf, float *d_bias, float *d_input,
+                char *ws, size_t ws_bytes, cudaStream_t st);
+size_t tc_backward_ws(const Geo &g, int64_t batch);
 
 // dt_profile_kernel_events: events to record around the next dominant-kernel launch on this
 // thread (both null when disarmed / exhausted).

@@ -295,15 +295,32 @@ __global__ void k_row_softmax(int64_t cols, void *y, int dtype) {
 }
 
 // MSE: grad = 2 (y - t) / norm; per-block fp64 partial sums of squares, fixed order.
-__global__ void k_mse(int64_t count, const float *y, const float *t, double scale, float *grad,
-                      double *part) {
+// grad.py:98-103 (mse): grad = 2 (y - t) / norm, per-block fp64 partial sums of (y - t)^2.
+// Grid-stride over float4 groups with a grid size that depends only on `count`, so every
+// partial has a fixed summation order (deterministic loss); HBM-bound (y, t read; grad written).
+constexpr int kMseBlocks = 1184;  // 8 per SM
+__global__ void __launch_bounds__(256) k_mse(int64_t count, const float *y, const float *t,
+                                             double scale, float *grad, double *part) {
   __shared__ double red[256];
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
-  if (idx < count) {
-    float d = y[idx] - t[idx];
-    grad[idx] = (float)(scale * (double)d);
-    sq = (double)d * (double)d;
+  const int64_t n4 = count / 4, stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(t) |
+                     reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+  if (vec) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 a = reinterpret_cast<const float4 *>(y)[i];
+      const float4 b = reinterpret_cast<const float4 *>(t)[i];
+      const float d0 = a.x - b.x, d1 = a.y - b.y, d2 = a.z - b.z, d3 = a.w - b.w;
+      reinterpret_cast<float4 *>(grad)[i] =
+          make_float4((float)(scale * d0), (float)(scale * d1), (float)(scale * d2), (float)(scale * d3));
+      sq += (double)d0 * d0 + (double)d1 * d1 + (double)d2 * d2 + (double)d3 * d3;
+    }
+  }
+  for (int64_t i = (vec ? 4 * n4 : 0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    const float d = y[i] - t[i];
+    grad[i] = (float)(scale * (double)d);
+    sq += (double)d * (double)d;
   }
   red[threadIdx.x] = sq;
   __syncthreads();
@@ -313,12 +330,19 @@ __global__ void k_mse(int64_t count, const float *y, const float *t, double scal
   }
   if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
-__global__ void k_sum_f64(int64_t count, const double *part, double *out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int64_t i = 0; i < count; ++i) s += part[i];
-    out[0] = s;
+
+// fixed-order sum of `count` fp64 partials (one block)
+__global__ void __launch_bounds__(256) k_sum_f64(int64_t count, const double *part, double *out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[0] = red[0];
 }
 
 __global__ void k_sgd(int64_t count, float *p, const float *g, float lr) {
@@ -688,6 +712,25 @@ int ffma_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const
 }
 
 // ---- small launchers ------------------------------------------------------------------
+int launch_act_grad(int64_t count, const float *up, const float *pre, int act, float act_arg,
+                    float *out, cudaStream_t st) {
+  if (count == 0) return DT_OK;
+  k_act_grad<<<blocks_for(count), 256, 0, st>>>(count, up, pre, act, act_arg, out);
+  return check_launch("act_grad");
+}
+size_t colsum_ws(int64_t rows, int64_t cols) {
+  return (size_t)std::max<int64_t>(1, (rows + 255) / 256) * cols * sizeof(float);
+}
+int launch_colsum(int64_t rows, int64_t cols, const float *g, float *out, float *part,
+                  cudaStream_t st) {
+  const int chunks = (int)std::max<int64_t>(1, (rows + 255) / 256);
+  dim3 grid(blocks_for(cols), (unsigned)chunks);
+  k_colsum_partial<<<grid, 256, 0, st>>>(rows, cols, 256, g, part);
+  if (int rc = check_launch("colsum")) return rc;
+  k_colsum_final<<<blocks_for(cols), 256, 0, st>>>(cols, chunks, part, out);
+  return check_launch("colsum_final");
+}
+
 int launch_decompress(const Geo &g, const float *xf, const float *wf, float *w, cudaStream_t st) {
   int64_t tot = g.q * g.r_dim;
   k_decompress<<<blocks_for(tot), 256, 0, st>>>(g.q, g.r_dim, g.rank, g.n, xf, wf, w);
@@ -706,9 +749,10 @@ int launch_row_softmax(int64_t rows, int64_t cols, void *y, int y_dtype, cudaStr
   return check_launch("row_softmax");
 }
 
-size_t mse_ws(int64_t rows, int64_t cols) {
-  return (size_t)blocks_for(rows * cols) * sizeof(double);
+static unsigned mse_blocks(int64_t count) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(kMseBlocks, (count + 1023) / 1024));
 }
+size_t mse_ws(int64_t rows, int64_t cols) { return (size_t)mse_blocks(rows * cols) * sizeof(double); }
 
 int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, double norm,
                     float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st) {
@@ -717,11 +761,11 @@ int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, 
     set_error("mse workspace too small");
     return DT_E_ARG;
   }
-  unsigned nb = blocks_for(count);
+  const unsigned nb = mse_blocks(count);
   k_mse<<<nb, 256, 0, st>>>(count, y, t, 2.0 / norm, grad, reinterpret_cast<double *>(ws));
   if (int rc = check_launch("mse")) return rc;
   if (loss_sum) {
-    k_sum_f64<<<1, 32, 0, st>>>(nb, reinterpret_cast<double *>(ws), loss_sum);
+    k_sum_f64<<<1, 256, 0, st>>>(nb, reinterpret_cast<double *>(ws), loss_sum);
     return check_launch("mse_sum");
   }
   return DT_OK;

@@ -104,3 +104,32 @@ def test_train_step_update_matches_oracle():
     for p0, p1, g in ((xf0, layer.fp.xf, layer.d_xf), (wf0, layer.fp.wf, layer.d_wf),
                       (b0, layer.bias, layer.d_bias)):
         assert torch.allclose(p1, p0 - 1e-3 * g, rtol=1e-6, atol=1e-12)
+
+
+BF16_TOL = 2e-3
+
+
+@pytest.mark.parametrize("geo", [
+    (1024, 1024, 16, 256, 4096, 512),   # config 1 geometry (reuse)
+    (512, 1536, 64, 128, 6144, 300),    # config-5-like rank 64, ragged batch
+    (2048, 2048, 3, 256, 16384, 128),   # config 3 hidden layer (rank 3, s*rank = 24)
+    (96, 130, 4, 32, 400, 70),          # discarded tail (m*n > q*r_dim), s*rank = 12
+])
+@pytest.mark.parametrize("act", ["identity", "tanh"])
+def test_tc_backward_reuse_factored(geo, act):
+    # the tensor-core backward of reuse geometries (factored; cuBLASLt tf32 / bf16 hi+lo for the
+    # plain GEMMs over transposed views) against the oracle fed the same bf16-rounded inputs
+    q, r_dim, rank, n, m, batch = geo
+    op = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, batch, seed=4, bias_sd=0.3).items()}
+    fp = D.FactorPair(d["xf"], d["wf"], D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+    up = O.round_bf16(O.make_rng(9).standard_normal((batch, r_dim)))
+    ref = O.layer_backward(d["x"], d["xf"], d["wf"], op, d["bias"], act, up)
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda").to(torch.bfloat16)
+    gr = D.layer_backward(x, fp, d["bias"], act, up, mma="bf16")
+    for mine, want, k in ((gr.d_xf, ref.d_xf, "dxf"), (gr.d_wf, ref.d_wf, "dwf"),
+                          (gr.d_input, ref.d_input, "dx"), (gr.d_bias, ref.d_bias, "db")):
+        assert O.rel_error(mine, want) <= BF16_TOL, (k, O.rel_error(mine, want))
+    # the discarded tail of I (rows >= r_dim*s of xf) receives exactly zero gradient
+    s = q // n
+    assert not torch.any(gr.d_xf[r_dim * s:]).item()
