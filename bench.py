@@ -40,6 +40,9 @@ CONFIGS = {
            "general path regen+tcgen05"),
     "c1": (1024, 1024, 16, 256, 4096, 64,
            "config1: DeepThin layer 1024->1024 reuse path (m_f 4096, n_f 256, r 16), fp32 FFMA"),
+    "c5": (8192, 8192, 64, 1024, 65536, 8192,
+           "config5: DeepThin layer 8192->8192 training step (m_f 65536, n_f 1024, r 64), reuse path "
+           "factored on tensor cores: forward + MSE + backward + grad all-reduce + SGD"),
 }
 
 
@@ -167,8 +170,13 @@ def run_reference(args, cfg, key):
     # each "step" = one full-batch call on the host cores, bounded by the K/W counts
     import numpy as np  # noqa: F401
     budget = max(3.0, min(60.0, 0.05 * (args.steps + args.warmup) * 20))
-    sps, threads, sample = cpu_reference_time(cfg, budget_s=budget)
-    line = {"impl": "reference", "metric": "compressed-layer samples/sec", "value": round(sps, 3),
+    if key == "c5":
+        c = cpu_train_time(cfg)
+        sps, threads, sample = c["value"], c["cores"], c["sample"]
+    else:
+        sps, threads, sample = cpu_reference_time(cfg, budget_s=budget)
+    metric = "compressed-layer training samples/sec" if key == "c5" else "compressed-layer samples/sec"
+    line = {"impl": "reference", "metric": metric, "value": round(sps, 3),
             "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(cfg[5] / sps * 1e3, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -178,6 +186,148 @@ def run_reference(args, cfg, key):
             "e2e": {"value": round(sps, 3), "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_train(args, cfg, key):
+    """BASELINE config 5: one SGD training step per GPU on its 8192-row shard (weak scaling;
+    global batch = 8192 x N), forward + MSE gradient (normalised by the global element count)
+    + backward + all-reduce of [d_xf | d_wf | d_bias] (NCCL when N > 1) + SGD on fp32 masters."""
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    rank, world, local = dist_init()
+    torch.cuda.set_device(local)
+    import paper_1802_06944_b200 as D
+    from paper_1802_06944_b200 import _lib
+    from paper_1802_06944_b200.grad import mse_grad_into
+
+    q, r_dim, rank_r, n, m, batch, desc = cfg
+    plan = D.LayerPlan(q=q, r_dim=r_dim, rank=rank_r, m=m, n=n)
+    # seeded synthetic inputs with the BASELINE distributions (factors N(0, 1/sqrt r) stddev,
+    # x and target N(0, 1)); generated on the device (c5 arrays are GBs in numpy f64)
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    sd = 1.0 / math.sqrt(rank_r)
+    xf = (torch.randn(m, rank_r, device="cuda", generator=gen) * sd).cpu().numpy()
+    wf = (torch.randn(rank_r, n, device="cuda", generator=gen) * sd).cpu().numpy()
+    bias = (torch.randn(r_dim, device="cuda", generator=gen) * 0.01).cpu().numpy()
+    layer = D.DeepThinLayer(plan, xf, wf, bias, mma="bf16")
+    x = torch.randn(batch, q, device="cuda", generator=gen).to(torch.bfloat16)
+    tgt = torch.randn(batch, r_dim, device="cuda", generator=gen)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    group = tdist.group.WORLD if world > 1 else None
+    lib = _lib.lib()
+
+    def step():
+        D.train_step(layer, x, tgt, 1e-4, global_rows=batch * world, group=group, loss_out=loss)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local).__enter__()
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    n0 = lib.dt_launch_counter()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    launches = lib.dt_launch_counter() - n0
+    clocks = sampler.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = batch * world * args.steps / (total_ms / 1e3)
+    bf16_peak, hbm_peak, peak_kind = peaks()
+    # SURVEY.md §8(d) config 5 per GPU: factored flops 4*B*q*r + 6*B*r_dim*(q/n)*r, compulsory
+    # bytes ~748 MB -> tensor-bound (133 us at peak vs 116 us of HBM)
+    flops = 4.0 * batch * q * rank_r + 6.0 * batch * r_dim * (q // n) * rank_r
+    achieved = flops / (ms * 1e-3) / 1e12
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": bf16_peak, "unit": "TFLOP/s",
+            "frac": round(achieved / bf16_peak, 4), "traffic": None,
+            "peak_source": f"{peak_kind} bf16_tflops (burst)", "kernel": "whole training step",
+            "kernel_us": round(ms * 1e3, 2), "factored_flops_per_step": flops,
+            "dense_equiv_tflops": round(4.0 * batch * q * r_dim / (ms * 1e-3) / 1e12, 1)}
+    # e2e: host (pinned) x and target -> device every step, loss read back every step
+    hx = x.cpu().pin_memory()
+    ht = tgt.cpu().pin_memory()
+    hl = torch.empty(1, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        x.copy_(hx, non_blocking=True)
+        tgt.copy_(ht, non_blocking=True)
+        step()
+        hl.copy_(loss, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(e2e_steps):
+        e2e_step()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    e2e_value = batch * world * e2e_steps / float(te.item())
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_train_time(cfg)
+    if rank == 0:
+        line = {
+            "metric": "compressed-layer training samples/sec", "value": round(value, 1),
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": desc, "batch_per_gpu": batch, "global_batch": batch * world,
+                       "x_dtype": "bfloat16", "parallelism": f"dp{world} (grad all-reduce)",
+                       "l2": "inputs (x 128 MiB bf16, target 256 MiB fp32) larger than L2"},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 1), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(hx.numel() * 2 + ht.numel() * 4),
+                    "d2h_bytes_per_step": 8},
+            "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def cpu_train_time(cfg, rows=256):
+    """Reference training step (oracle port: decompress, matmul, MSE, layer_backward) on a
+    `rows`-row sample of the config-5 shard, scaled to samples/s."""
+    import numpy as np
+    threads = len(os.sched_getaffinity(0))
+    from oracle import deepthin_oracle as O
+    q, r_dim, rank, n, m, batch, _ = cfg
+    plan = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    rng = np.random.default_rng(0)
+    sd = 1.0 / math.sqrt(rank)
+    xf = (rng.standard_normal((m, rank)) * sd).astype(np.float32)
+    wf = (rng.standard_normal((rank, n)) * sd).astype(np.float32)
+    b = np.zeros(r_dim, dtype=np.float32)
+    x = rng.standard_normal((rows, q)).astype(np.float32)
+    t = rng.standard_normal((rows, r_dim)).astype(np.float32)
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        y = O.layer_forward(x, xf, wf, plan, b)
+        _, gy = O.loss_and_grad("mse", y, t)
+        O.layer_backward(x, xf, wf, plan, b, "identity", gy)
+        times.append(time.perf_counter() - t0)
+    med = min(times)
+    return {"value": round(rows / med, 3), "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"oracle forward + MSE + layer_backward on {rows} of the {batch} rows "
+                      f"(best of 2: {med:.2f} s)"}
 
 
 def run_ours(args, cfg, key):
@@ -394,6 +544,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg, args.config)
+    elif args.config == "c5":
+        run_train(args, cfg, args.config)
     else:
         run_ours(args, cfg, args.config)
 
