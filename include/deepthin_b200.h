@@ -161,6 +161,17 @@ int dt_mse_grad(int64_t rows, int64_t cols, const float *y, const float *target,
                 size_t workspace_bytes, dt_stream stream);
 size_t dt_mse_workspace_bytes(int64_t rows, int64_t cols);
 
+/* Fused forward + MSE gradient, identity activation (grad.py:98-103 applied to
+ * kernel.py:296-320's output without materialising y): grad = 2 (x W + b - target) /
+ * norm_count (fp32, batch x r_dim) and loss_sum[0] = sum (y - target)^2 (fp64, fixed order).
+ * bf16 tensor-core path (x bf16 or fp32, fp32 factors); the MSE runs in the final GEMM's
+ * epilogue. */
+size_t dt_forward_mse_workspace_bytes(const dt_plan *plan, int64_t batch);
+int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtype, const float *xf,
+                   const float *wf, const float *bias, const float *target, double norm_count,
+                   float *grad, double *loss_sum, void *workspace, size_t workspace_bytes,
+                   dt_stream stream);
+
 /* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);
 

@@ -25,7 +25,7 @@ EXPORTS = (
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
-    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_sgd_step", "dt_session_create",
+    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_sgd_step", "dt_session_create",
     "dt_session_forward", "dt_session_destroy",
 )
 
@@ -52,6 +52,8 @@ def _declare(lib):
         "dt_launch_counter": ([], I64),
         "dt_profile_kernel_events": ([C.POINTER(VP), C.POINTER(VP), i], i),
         "dt_set_forward_pipeline": ([i], i),
+        "dt_forward_mse_workspace_bytes": ([P, I64], SZ),
+        "dt_forward_mse": ([P, I64, VP, i, VP, VP, VP, VP, D, VP, VP, VP, SZ, VP], i),
         "dt_plan_validate": ([P], i),
         "dt_plan_query": ([P, C.POINTER(PlanInfo)], i),
         "dt_phase": ([P, I64, C.POINTER(I64)], i),

@@ -344,6 +344,35 @@ int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int 
                        d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
+size_t dt_forward_mse_workspace_bytes(const dt_plan *plan, int64_t batch) {
+  Geo g;
+  if (make_geo(plan, &g) || batch < 0) return 0;
+  return tc_forward_mse_ws(g, batch);
+}
+
+int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtype, const float *xf,
+                   const float *wf, const float *bias, const float *target, double norm_count,
+                   float *grad, double *loss_sum, void *workspace, size_t workspace_bytes,
+                   dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (batch < 0) {
+    set_error("batch must be >= 0");
+    return DT_E_DIM;
+  }
+  if (int rc = check_dtype(x_dtype, "x")) return rc;
+  if (!(norm_count > 0)) {
+    set_error("norm_count must be > 0");
+    return DT_E_ARG;
+  }
+  if (batch > 0 && (!x || !xf || !wf || !target || !grad)) {
+    set_error("NULL operand pointer");
+    return DT_E_ARG;
+  }
+  return tc_forward_mse(g, batch, x, x_dtype, xf, wf, bias, target, 2.0 / norm_count, grad,
+                        loss_sum, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 size_t dt_mse_workspace_bytes(int64_t rows, int64_t cols) { return mse_ws(rows, cols); }
 
 int dt_mse_grad(int64_t rows, int64_t cols, const float *y, const float *target,

@@ -74,6 +74,13 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
                     const void *wf, int f_dtype, const float *bias, int act, float act_arg,
                     void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st);
 size_t tc_gemm_ws(const Geo &g, int64_t batch);
+// Forward with the MSE gradient fused into the final GEMM's epilogue (identity activation):
+// grad = scale * (x W + b - target), loss_sum = fixed-order fp64 sum of squared errors.
+int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                   const float *wf, const float *bias, const float *target, double scale,
+                   float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st);
+size_t tc_forward_mse_ws(const Geo &g, int64_t batch);
+int launch_sum_f64(int64_t count, const double *part, double *out, cudaStream_t st);
 // Tensor-core backward of reuse geometries in factored form (cuBLASLt for the plain GEMMs over
 // transposed views); returns DT_E_UNSUPPORTED when the geometry does not qualify.
 bool tc_backward_ok(const Geo &g);

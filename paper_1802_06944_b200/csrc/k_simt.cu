@@ -771,6 +771,11 @@ int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, 
   return DT_OK;
 }
 
+int launch_sum_f64(int64_t count, const double *part, double *out, cudaStream_t st) {
+  k_sum_f64<<<1, 256, 0, st>>>(count, part, out);
+  return check_launch("sum_f64");
+}
+
 int launch_sgd(int64_t count, float *p, const float *g, float lr, cudaStream_t st) {
   if (count == 0) return DT_OK;
   k_sgd<<<blocks_for(count), 256, 0, st>>>(count, p, g, lr);

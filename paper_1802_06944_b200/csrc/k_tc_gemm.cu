@@ -52,6 +52,7 @@ constexpr uint32_t kXBytes = GN * GK * 2;  // one x k-block (32 KB)
 #ifndef DT_GEMM_EPI_WARPS
 #define DT_GEMM_EPI_WARPS 8
 #endif
+constexpr int YDT_MSE = 7;  // epilogue "output type": the fused MSE gradient (see GemmParams)
 constexpr int kEpiWarps = DT_GEMM_EPI_WARPS;  // multiple of 4 (one per TMEM lane quarter)
 constexpr int kEpiParts = kEpiWarps / 4;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
@@ -93,6 +94,12 @@ struct GemmParams {
   const float *bias;
   void *y;
   float arg;
+  // YDT == YDT_MSE epilogue: y holds grad = scale * (z - target) (fp32), and every epilogue
+  // warp writes the fp64 sum of (z - target)^2 over its share of a tile to
+  // loss_part[(item * csize + crank) * kEpiWarps + warp - 2]
+  const float *target;
+  double scale;
+  double *loss_part;
   // fused (cooperative launch): phase 1 runs inside the GEMM kernel on the epilogue warps of
   // every CTA (tiles rg_ux x rg_uy), then a grid-wide barrier, then the GEMM
   int fused, rg_ux, rg_uy, rg_rows;
@@ -497,6 +504,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
     int acc = 0;
     uint32_t aphase = 0;
+    double sq = 0.0;  // YDT_MSE: this thread's share of the tile's squared error
     for (int it = beg; it < end; ++it) {
       const int j = jb_of(it) * GM + 32 * wq + lane;
       const int64_t b0 = b0_of(it);
@@ -518,15 +526,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (jok && !(p.dbg & 1)) {
           OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - 32 * c32;
+          if constexpr (YDT == YDT_MSE) {  // grad = scale * (z - t), sum (z - t)^2
+            // fp32 per element (fp64 math per element made this epilogue the bottleneck), the
+            // 32-row chunk's fp32 sum folded into the thread's fp64 total in a fixed order
+            const float *tp = p.target + (b0 + 32 * c32) * p.ldy + j;
+            const float sc = (float)p.scale;
+            float tv[32];
 #pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            if (r < rmax) {
-              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
-              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+            for (int r = 0; r < 32; ++r) tv[r] = r < rmax ? __ldg(tp + (int64_t)r * p.ldy) : 0.f;
+            float csq = 0.f;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              if (r < rmax) {
+                const float dz = (__uint_as_float(v[r]) + bias_j) - tv[r];
+                *yp = sc * dz;
+                csq = fmaf(dz, dz, csq);
+              }
+              yp += p.ldy;
             }
-            yp += p.ldy;
+            sq += (double)csq;
+          } else {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              if (r < rmax) {
+                const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+                if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+              }
+              yp += p.ldy;
+            }
           }
         }
+      }
+      if constexpr (YDT == YDT_MSE) {  // fixed-order warp reduction -> one partial per warp
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) p.loss_part[((int64_t)it * cs + crank) * kEpiWarps + (warp - 2)] = sq;
+        sq = 0.0;
       }
       tc_fence_before();
       __syncwarp();
@@ -971,6 +1006,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
     int acc = 0;
     uint32_t aphase = 0;
+    double sq = 0.0;  // YDT_MSE: this thread's share of the tile's squared error
     for (int it = beg; it < end; ++it) {
       const int j = jb_of(it) * GM + 32 * wq + lane;
       const int64_t b0 = b0_of(it);
@@ -992,15 +1028,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (jok && !(p.dbg & 1)) {
           OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - 32 * c32;
+          if constexpr (YDT == YDT_MSE) {  // grad = scale * (z - t), sum (z - t)^2
+            // fp32 per element (fp64 math per element made this epilogue the bottleneck), the
+            // 32-row chunk's fp32 sum folded into the thread's fp64 total in a fixed order
+            const float *tp = p.target + (b0 + 32 * c32) * p.ldy + j;
+            const float sc = (float)p.scale;
+            float tv[32];
 #pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            if (r < rmax) {
-              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
-              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+            for (int r = 0; r < 32; ++r) tv[r] = r < rmax ? __ldg(tp + (int64_t)r * p.ldy) : 0.f;
+            float csq = 0.f;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              if (r < rmax) {
+                const float dz = (__uint_as_float(v[r]) + bias_j) - tv[r];
+                *yp = sc * dz;
+                csq = fmaf(dz, dz, csq);
+              }
+              yp += p.ldy;
             }
-            yp += p.ldy;
+            sq += (double)csq;
+          } else {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              if (r < rmax) {
+                const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+                if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+              }
+              yp += p.ldy;
+            }
           }
         }
+      }
+      if constexpr (YDT == YDT_MSE) {  // fixed-order warp reduction -> one partial per warp
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) p.loss_part[((int64_t)it * 2 + crank) * kEpiWarps + (warp - 2)] = sq;
+        sq = 0.0;
       }
       tc_fence_before();
       __syncwarp();
@@ -1040,6 +1103,10 @@ GemmFn pick_gemm_el(int act, bool pair) {
   }
 }
 GemmFn pick_gemm(int y_dtype, int act, bool pair, int el) {
+  if (y_dtype == YDT_MSE) {  // identity activation only
+    if (el) return pair ? k_tc_gemm_pair<YDT_MSE, DT_ACT_IDENTITY, 1> : k_tc_gemm<YDT_MSE, DT_ACT_IDENTITY, 1>;
+    return pair ? k_tc_gemm_pair<YDT_MSE, DT_ACT_IDENTITY, 0> : k_tc_gemm<YDT_MSE, DT_ACT_IDENTITY, 0>;
+  }
   if (el)
     return y_dtype == DT_BF16 ? pick_gemm_el<DT_BF16, 1>(act, pair) : pick_gemm_el<DT_F32, 1>(act, pair);
   return y_dtype == DT_BF16 ? pick_gemm_el<DT_BF16, 0>(act, pair) : pick_gemm_el<DT_F32, 0>(act, pair);
@@ -1118,6 +1185,11 @@ struct GemmCall {
   const RegenArgs *rg;
   bool profile;  // the forward's dominant kernel: dt_profile_kernel_events brackets it
   int el = 0;    // operand element type: 0 bf16 (kind::f16), 1 fp32 (kind::tf32)
+  // y_dtype == YDT_MSE: fused MSE gradient against `target`, partials into loss_part
+  const float *target = nullptr;
+  double scale = 0.0;
+  double *loss_part = nullptr;
+  int64_t *n_part = nullptr;  // out: number of partials written
 };
 
 static int run_gemm(const GemmCall &c, cudaStream_t st) {
@@ -1212,6 +1284,13 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   p.bias = c.bias;
   p.y = c.y;
   p.arg = c.act_arg;
+  p.target = c.target;
+  p.scale = c.scale;
+  p.loss_part = c.loss_part;
+  if (c.n_part) *c.n_part = (int64_t)p.items * p.csize * kEpiWarps;
+  if (c.loss_part)
+    DT_CUDA_CHECK(cudaMemsetAsync(c.loss_part, 0,
+                                  (size_t)p.items * p.csize * kEpiWarps * sizeof(double), st));
   dim3 rgrid(1, 1);
   if (c.rg) {
     const RegenArgs &rg = *c.rg;
@@ -1360,10 +1439,63 @@ size_t tc_gemm_ws(const Geo &g, int64_t batch) {
   return std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0);
 }
 
+struct MseArgs {
+  const float *target;
+  double scale;
+  double *loss_sum;
+  double *part;  // workspace for the per-warp partials
+};
+static int64_t mse_parts_bound(const Geo &g, int64_t batch) {
+  return ((g.r_dim + GM - 1) / GM + 2) * ((batch + GN - 1) / GN) * kEpiWarps;
+}
+
+static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dtype,
+                           const void *xf, const void *wf, int f_dtype, const float *bias,
+                           int act, float act_arg, void *y, int y_dtype, char *ws,
+                           size_t ws_bytes, cudaStream_t st, const MseArgs *mse);
+
 int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, const void *xf,
                     const void *wf, int f_dtype, const float *bias, int act, float act_arg,
                     void *y, int y_dtype, char *ws, size_t ws_bytes, cudaStream_t st) {
+  return tc_forward_impl(g, batch, x, x_dtype, xf, wf, f_dtype, bias, act, act_arg, y, y_dtype,
+                         ws, ws_bytes, st, nullptr);
+}
+
+size_t tc_forward_mse_ws(const Geo &g, int64_t batch) {
+  return tc_gemm_ws(g, batch) + (size_t)round_up(mse_parts_bound(g, batch) * 8, 256);
+}
+
+int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                   const float *wf, const float *bias, const float *target, double scale,
+                   float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < tc_forward_mse_ws(g, batch)) {
+    set_error("forward+mse workspace too small: need " + std::to_string(tc_forward_mse_ws(g, batch)));
+    return DT_E_ARG;
+  }
+  if (batch == 0) {
+    if (loss_sum) DT_CUDA_CHECK(cudaMemsetAsync(loss_sum, 0, sizeof(double), st));
+    return DT_OK;
+  }
+  const size_t base = tc_gemm_ws(g, batch);
+  MseArgs m{target, scale, loss_sum, reinterpret_cast<double *>(ws + base)};
+  return tc_forward_impl(g, batch, x, x_dtype, xf, wf, DT_F32, bias, DT_ACT_IDENTITY, 0.f, grad,
+                         YDT_MSE, ws, base, st, &m);
+}
+
+static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dtype,
+                           const void *xf, const void *wf, int f_dtype, const float *bias,
+                           int act, float act_arg, void *y, int y_dtype, char *ws,
+                           size_t ws_bytes, cudaStream_t st, const MseArgs *mse) {
   if (batch == 0) return DT_OK;
+  int64_t n_part = 0;
+  auto finish_mse = [&](int rc) {
+    if (rc || !mse) return rc;
+    if (n_part > mse_parts_bound(g, batch)) {
+      set_error("mse partials exceed the workspace bound");
+      return (int)DT_E_ARG;
+    }
+    return mse->loss_sum ? launch_sum_f64(n_part, mse->part, mse->loss_sum, st) : (int)DT_OK;
+  };
   if (f_dtype != DT_F32 && f_dtype != DT_BF16) {
     set_error("tensor-core path: factors must be DT_F32 or DT_BF16");
     return DT_E_ARG;
@@ -1402,7 +1534,11 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
     if (int rc = run_gemm(c1, st)) return rc;
     GemmCall c2{P, SR, batch, SR, xf, SR, g.r_dim, bias, act, act_arg,
                 y, g.r_dim, y_dtype, nullptr, true, 1};
-    return run_gemm(c2, st);
+    if (mse) {
+      c2.target = mse->target; c2.scale = mse->scale; c2.loss_part = mse->part;
+      c2.n_part = &n_part;
+    }
+    return finish_mse(run_gemm(c2, st));
   }
 
   // ---- two-phase: W^T regenerated into the workspace, then the GEMM ----
@@ -1429,7 +1565,11 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   rg.chain = pipe ? 1 : 0;
   GemmCall c{xt, ldx, batch, g.q, wt, ldw, g.r_dim, bias, act, act_arg,
              y, g.r_dim, y_dtype, &rg, true};
-  return run_gemm(c, st);
+  if (mse) {
+    c.target = mse->target; c.scale = mse->scale; c.loss_part = mse->part;
+    c.n_part = &n_part;
+  }
+  return finish_mse(run_gemm(c, st));
 }
 
 

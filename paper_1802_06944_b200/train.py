@@ -46,6 +46,26 @@ class DeepThinLayer:
         forward_into(x, self.fp, self.bias, self.act, self.act_arg, y, self.mma)
         return y
 
+    def forward_mse(self, x: torch.Tensor, target: torch.Tensor, norm_count: float,
+                    loss_out: torch.Tensor) -> torch.Tensor:
+        """Forward + MSE gradient in one pass (dt_forward_mse, identity activation, bf16 path):
+        returns grad = 2 (y - target) / norm_count; loss_out[0] = sum (y - target)^2. y itself
+        is never written (grad.py:98-103 fused into the contraction's epilogue)."""
+        self._x = x
+        lib = _lib.lib()
+        ps = _lib.plan_struct(self.plan)
+        batch = x.shape[0]
+        from .core import workspace
+        ws = workspace(lib.dt_forward_mse_workspace_bytes(C.byref(ps), batch))
+        g = torch.empty((batch, self.plan.r_dim), dtype=torch.float32, device=x.device)
+        tgt = target.contiguous().float()
+        _lib.check(lib.dt_forward_mse(
+            C.byref(ps), batch, x.data_ptr(), _lib.DT_BF16 if x.dtype == torch.bfloat16 else _lib.DT_F32,
+            self.fp.xf.data_ptr(), self.fp.wf.data_ptr(), self.bias.data_ptr(), tgt.data_ptr(),
+            float(norm_count), g.data_ptr(), loss_out.data_ptr(), ws.data_ptr(), ws.numel(),
+            stream_handle()))
+        return g
+
     def backward(self, upstream: torch.Tensor, need_input_grad: bool = False):
         d_in = (torch.empty((self._x.shape[0], self.plan.q), dtype=torch.float32, device=self._x.device)
                 if need_input_grad else None)
@@ -65,11 +85,15 @@ class DeepThinLayer:
 def train_step(layer: DeepThinLayer, x: torch.Tensor, target: torch.Tensor, lr: float,
                global_rows: int | None = None, group=None, loss_out: torch.Tensor | None = None):
     """One SGD step on this rank's shard; returns the local sum of squared errors (fp64 device)."""
-    y = layer.forward(x)
     rows = global_rows if global_rows is not None else x.shape[0]
-    g = torch.empty_like(y)
-    ls = loss_out if loss_out is not None else torch.empty(1, dtype=torch.float64, device=y.device)
-    mse_grad_into(y, target, g, float(rows * layer.plan.r_dim), ls)
+    ls = loss_out if loss_out is not None else torch.empty(1, dtype=torch.float64, device=x.device)
+    norm = float(rows * layer.plan.r_dim)
+    if layer.mma == _lib.DT_MMA_BF16 and layer.activation == "identity":
+        g = layer.forward_mse(x, target, norm, ls)   # MSE fused into the forward epilogue
+    else:
+        y = layer.forward(x)
+        g = torch.empty_like(y)
+        mse_grad_into(y, target, g, norm, ls)
     layer.backward(g)
     allreduce_grads(layer.grad_flat, group)
     layer.step(lr)

@@ -17,7 +17,7 @@ for _ in range(3):
     D.train_step(layer, x, t, 1e-3)
 torch.cuda.synchronize()
 e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-K = 10
+K = int(os.environ.get("K", 10))
 tot = [0.0] * 4
 for _ in range(K):
     e[0].record()

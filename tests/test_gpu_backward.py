@@ -133,3 +133,27 @@ def test_tc_backward_reuse_factored(geo, act):
     # the discarded tail of I (rows >= r_dim*s of xf) receives exactly zero gradient
     s = q // n
     assert not torch.any(gr.d_xf[r_dim * s:]).item()
+
+
+@pytest.mark.parametrize("geo", [
+    (8192 // 8, 1024, 16, 128, 8192, 700),   # reuse (factored GEMM 2 epilogue)
+    (440, 2048, 24, 320, 2816, 600),         # general (two-phase GEMM epilogue)
+])
+def test_forward_mse_fused_matches_separate(geo):
+    # dt_forward_mse: the MSE gradient in the final GEMM's epilogue equals forward + mse_grad,
+    # and its fp64 loss is the same sum (the oracle's loss on the kernel's own outputs)
+    q, r_dim, rank, n, m, batch = geo
+    op = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, batch, seed=8).items()}
+    p = D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    layer = D.DeepThinLayer(p, d["xf"], d["wf"], d["bias"], mma="bf16")
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda").to(torch.bfloat16)
+    t = torch.tensor(d["target"], dtype=torch.float32, device="cuda")
+    norm = float(batch * r_dim)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    g = layer.forward_mse(x, t, norm, loss)
+    y = layer.forward(x)
+    want_g = (2.0 / norm) * (y.double() - t.double())
+    assert torch.allclose(g.double(), want_g, rtol=0, atol=1e-6 * float(want_g.abs().max()))
+    want_loss = float(((y.double() - t.double()) ** 2).sum())
+    assert float(loss.item()) == pytest.approx(want_loss, rel=1e-6)  # fp32 chunk sums
