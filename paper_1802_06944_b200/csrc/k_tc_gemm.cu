@@ -545,6 +545,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               yp += p.ldy;
             }
             sq += (double)csq;
+          } else if (rmax >= 32) {  // full chunk: no per-row predicate, pointer bumps only
+            const int64_t ld = p.ldy;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+              yp += ld;
+            }
           } else {
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
@@ -1047,6 +1055,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               yp += p.ldy;
             }
             sq += (double)csq;
+          } else if (rmax >= 32) {  // full chunk: no per-row predicate, pointer bumps only
+            const int64_t ld = p.ldy;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
+              yp += ld;
+            }
           } else {
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
@@ -1196,6 +1212,8 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static const int max_sm = getenv("DEEPTHIN_GEMM_MAXSM") ? atoi(getenv("DEEPTHIN_GEMM_MAXSM")) : 0;
+  if (max_sm > 0) nsm = std::min(nsm, max_sm);
   GemmParams p{};
   const int64_t n_bt = (c.rows + GN - 1) / GN;
   const int64_t n_jb = (c.cols + GM - 1) / GM;
