@@ -53,12 +53,13 @@ enum dt_status {
   DT_E_DIM = 1,         /* DimensionError                  */
   DT_E_ARG = 2,         /* ArgumentError                   */
   DT_E_UNSUPPORTED = 3, /* UnsupportedConfigurationError   */
-  DT_E_CUDA = 4         /* CUDA launch / runtime failure   */
+  DT_E_CUDA = 4,        /* CUDA launch / runtime failure   */
+  DT_E_FORMAT = 5       /* ModelFormatError (dt_model_parse; details in dt_format_error) */
 };
 
 /* DT_FACTORS_PACKED is valid only as dt_forward's f_dtype: xf points at the buffer
  * dt_pack_factors filled (wf is ignored). */
-enum dt_dtype { DT_F32 = 0, DT_BF16 = 1, DT_FACTORS_PACKED = 2 };
+enum dt_dtype { DT_F32 = 0, DT_BF16 = 1, DT_FACTORS_PACKED = 2, DT_F64 = 3 /* dt_unpack_values */ };
 
 /* Arithmetic of the contraction.
  *  DT_MMA_FFMA: fp32 CUDA-core FFMA, fp32 operands (parity rtol 1e-5).
@@ -189,6 +190,62 @@ int dt_session_create(const dt_plan *plan, int mma, const float *xf_host, const 
 int dt_session_forward(dt_session *s, int64_t batch, const float *x_host, int act,
                        float act_arg, float *y_host, int64_t *h2d_bytes, int64_t *d2h_bytes);
 void dt_session_destroy(dt_session *s);
+
+/* ---- .dthn model image (reference model_io.py:1-224) ------------------------- */
+/* Host-only parse of a serialized model held in memory: validates the image exactly as
+ * deserialize does (model_io.py:141-210, same checks in the same order, same failing byte
+ * offsets) and indexes it in place — names, metadata strings and payloads are reported as byte
+ * offsets into the image, nothing is copied. Records are written up to meta_cap / layer_cap
+ * (either may be 0); hdr->meta_read / hdr->layers_read count the records the parse started,
+ * including a partial one at the failure point (unread spans have length -1), so a caller
+ * sizes its arrays with a first call at cap 0. Returns DT_OK, or DT_E_FORMAT with *err set. */
+typedef struct { int64_t offset, length; } dt_span;
+typedef struct { dt_span key, value; } dt_model_meta;
+typedef struct {
+  uint32_t version, layer_count;
+  uint64_t payload_bytes;
+  double target_ratio;
+  uint32_t meta_count, reserved;
+  int64_t meta_read, layers_read;
+} dt_model_header;
+typedef struct {
+  dt_span name;
+  dt_plan plan;        /* u64 fields of the file (values above INT64_MAX wrap) */
+  int32_t dtype_code;  /* 0 float32, 1 float64 */
+  int32_t floor_hit;
+  int64_t bias_len;
+  int64_t xf_offset, wf_offset, bias_offset; /* payload byte offsets into the image */
+} dt_model_layer;
+enum dt_format_kind {
+  DT_FMT_OK = 0,
+  DT_FMT_TRUNCATED = 1,        /* need/have bytes while reading `what`                 */
+  DT_FMT_BAD_MAGIC = 2,
+  DT_FMT_BAD_VERSION = 3,      /* need = version                                      */
+  DT_FMT_PAYLOAD_MISMATCH = 4, /* need = declared payload, have = actual              */
+  DT_FMT_BAD_DTYPE = 5,        /* need = code                                         */
+  DT_FMT_INVALID_PLAN = 6,     /* layer = index (its plan is in the layer record)     */
+  DT_FMT_TRAILING = 7          /* need = trailing byte count                          */
+};
+enum dt_format_what {
+  DT_WHAT_HEADER = 0, DT_WHAT_META_COUNT, DT_WHAT_META_KEY_LEN, DT_WHAT_META_KEY,
+  DT_WHAT_META_VALUE_LEN, DT_WHAT_META_VALUE, DT_WHAT_NAME_LEN, DT_WHAT_NAME, DT_WHAT_PLAN,
+  DT_WHAT_FLAGS, DT_WHAT_BIAS_LEN, DT_WHAT_XF, DT_WHAT_WF, DT_WHAT_BIAS
+};
+typedef struct {
+  int32_t kind, what;
+  int64_t offset; /* the failing byte offset (ModelFormatError.offset) */
+  int64_t layer;  /* layer (or metadata item) index, -1 when none      */
+  int64_t need, have;
+} dt_format_error;
+int dt_model_parse(const void *image, size_t size, dt_model_header *hdr, dt_model_meta *meta,
+                   int64_t meta_cap, dt_model_layer *layers, int64_t layer_cap,
+                   dt_format_error *err);
+
+/* Device-side payload decode: `count` little-endian values of src_dtype (DT_F32 / DT_F64) at
+ * any byte alignment (a payload inside a device copy of the image) -> aligned fp32 `dst`
+ * (float64 rounded to nearest even), plus the bf16 (RNE) copy when dst_bf16 is non-NULL. */
+int dt_unpack_values(int64_t count, const void *src, int src_dtype, float *dst,
+                     uint16_t *dst_bf16, dt_stream stream);
 
 #ifdef __cplusplus
 }

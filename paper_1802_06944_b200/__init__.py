@@ -7,21 +7,27 @@ backed by hand-written sm_100a kernels behind a C ABI
 """
 
 from .core import make_rng, max_abs_diff, rel_error, sample_normal, spawn_rngs
-from .errors import (ArgumentError, CudaError, DeepThinError, DimensionError,
+from .errors import (ArgumentError, CudaError, DeepThinError, DimensionError, ModelFormatError,
                      UnsupportedConfigurationError)
 from .factor import FactorPair, decompress, init_factors, phase, phase_count, relayout_index
 from .grad import Gradients, layer_backward, loss_and_grad
 from .kernel import (ACTIVATIONS, OpCount, ReuseTable, forward_pipeline, fused_matmul,
                      layer_forward, op_count, predict_reuse)
-from .planner import LayerPlan, baseline_plan
+from .model import DeviceModel
+from .model_io import (CompressedModel, deserialize, expected_file_size, load_model, save_model,
+                       serialize)
+from .planner import LayerPlan, NetworkPlan, baseline_plan
 from .train import DeepThinLayer, train_step
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ACTIVATIONS", "ArgumentError", "CudaError", "DeepThinError", "DeepThinLayer",
-    "DimensionError", "FactorPair", "Gradients", "LayerPlan", "OpCount", "ReuseTable",
-    "UnsupportedConfigurationError", "baseline_plan", "decompress", "forward_pipeline", "fused_matmul",
+    "ACTIVATIONS", "ArgumentError", "CompressedModel", "CudaError", "DeepThinError",
+    "DeepThinLayer", "DeviceModel", "DimensionError", "FactorPair", "Gradients", "LayerPlan",
+    "ModelFormatError", "NetworkPlan", "OpCount", "ReuseTable",
+    "UnsupportedConfigurationError", "baseline_plan", "decompress", "deserialize",
+    "expected_file_size", "forward_pipeline", "fused_matmul", "load_model", "save_model",
+    "serialize",
     "init_factors", "layer_backward", "layer_forward", "loss_and_grad", "make_rng",
     "max_abs_diff", "op_count", "phase", "phase_count", "predict_reuse", "rel_error",
     "relayout_index", "sample_normal", "spawn_rngs", "train_step",

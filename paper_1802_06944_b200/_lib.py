@@ -14,8 +14,8 @@ from .errors import ArgumentError, CudaError, DimensionError, UnsupportedConfigu
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
 
-DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA = range(5)
-DT_F32, DT_BF16, DT_FACTORS_PACKED = 0, 1, 2
+DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA, DT_E_FORMAT = range(6)
+DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64 = 0, 1, 2, 3
 DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
 ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
 
@@ -26,7 +26,7 @@ EXPORTS = (
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
     "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_sgd_step", "dt_session_create",
-    "dt_session_forward", "dt_session_destroy",
+    "dt_session_forward", "dt_session_destroy", "dt_model_parse", "dt_unpack_values",
 )
 
 
@@ -39,6 +39,38 @@ class PlanInfo(C.Structure):
     _fields_ = [("period", C.c_int64), ("phase_count", C.c_int64), ("reuse", C.c_int64),
                 ("segments", C.c_int64), ("tail", C.c_int64), ("rows_per_period", C.c_int64)]
 
+
+class Span(C.Structure):
+    _fields_ = [("offset", C.c_int64), ("length", C.c_int64)]
+
+
+class ModelMeta(C.Structure):
+    _fields_ = [("key", Span), ("value", Span)]
+
+
+class ModelHeader(C.Structure):
+    _fields_ = [("version", C.c_uint32), ("layer_count", C.c_uint32),
+                ("payload_bytes", C.c_uint64), ("target_ratio", C.c_double),
+                ("meta_count", C.c_uint32), ("reserved", C.c_uint32),
+                ("meta_read", C.c_int64), ("layers_read", C.c_int64)]
+
+
+class ModelLayer(C.Structure):
+    _fields_ = [("name", Span), ("plan", Plan), ("dtype_code", C.c_int32),
+                ("floor_hit", C.c_int32), ("bias_len", C.c_int64), ("xf_offset", C.c_int64),
+                ("wf_offset", C.c_int64), ("bias_offset", C.c_int64)]
+
+
+class FormatError(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("what", C.c_int32), ("offset", C.c_int64),
+                ("layer", C.c_int64), ("need", C.c_int64), ("have", C.c_int64)]
+
+
+(DT_FMT_OK, DT_FMT_TRUNCATED, DT_FMT_BAD_MAGIC, DT_FMT_BAD_VERSION, DT_FMT_PAYLOAD_MISMATCH,
+ DT_FMT_BAD_DTYPE, DT_FMT_INVALID_PLAN, DT_FMT_TRAILING) = range(8)
+(DT_WHAT_HEADER, DT_WHAT_META_COUNT, DT_WHAT_META_KEY_LEN, DT_WHAT_META_KEY,
+ DT_WHAT_META_VALUE_LEN, DT_WHAT_META_VALUE, DT_WHAT_NAME_LEN, DT_WHAT_NAME, DT_WHAT_PLAN,
+ DT_WHAT_FLAGS, DT_WHAT_BIAS_LEN, DT_WHAT_XF, DT_WHAT_WF, DT_WHAT_BIAS) = range(14)
 
 _lib = None
 
@@ -74,6 +106,9 @@ def _declare(lib):
         "dt_session_create": ([P, i, VP, VP, VP, C.POINTER(VP)], i),
         "dt_session_forward": ([VP, I64, VP, i, F, VP, C.POINTER(I64), C.POINTER(I64)], i),
         "dt_session_destroy": ([VP], None),
+        "dt_model_parse": ([VP, SZ, C.POINTER(ModelHeader), C.POINTER(ModelMeta), I64,
+                            C.POINTER(ModelLayer), I64, C.POINTER(FormatError)], i),
+        "dt_unpack_values": ([I64, VP, i, VP, VP, VP], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -150,6 +150,12 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+// fp32 bits -> tf32 hi (RNA) + tf32 lo (the RNA of the remainder): hi + lo carries ~21 bits
+__device__ __forceinline__ void split_tf32(uint32_t bits, uint32_t &hi, uint32_t &lo) {
+  const float v = __uint_as_float(bits);
+  hi = to_tf32(v);
+  lo = to_tf32(v - __uint_as_float(hi));
+}
 __device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
                                                  uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -263,7 +269,7 @@ __device__ __forceinline__ void regen_tile(const RegenArgs &g, int tid, int bx, 
 // m-tile w & 1, n-tiles 4*(w >> 1) .. +3. Accumulator pairs go straight to W^T (= I.ravel()
 // when ldw == q) as 4-byte bf16x2 stores.
 struct RegenSmemTC {
-  uint32_t xs[RG_R][RG_K + 4];   // tf32 bits; row stride = 4 (mod 8): conflict-free A reads
+  uint32_t xs[RG_R][RG_K + 4];   // fp32 bits (split to tf32 hi/lo at fragment load); row stride = 4 (mod 8): conflict-free A reads
   uint32_t ws[RG_K][RG_C + 8];   // row stride / 8 odd: conflict-free B reads
 };
 template <typename FT>
@@ -296,28 +302,37 @@ __device__ __forceinline__ void regen_tile_tc(const RegenArgs &g, int tid, int b
       wv[u] = (k < kc && c0 + c < n) ? ldf(wf + (int64_t)(k0 + k) * n + c0 + c) : 0.f;
     }
     if (k0 > 0) __syncthreads();  // the previous chunk's fragments are read
+    // smem keeps the raw fp32 bits; fragments are split at load time
 #pragma unroll
     for (int u = 0; u < NX; ++u) {
       const int e = tid + 256 * u;
-      sm.xs[e / RG_K][e % RG_K] = to_tf32(xv[u]);
+      sm.xs[e / RG_K][e % RG_K] = __float_as_uint(xv[u]);
     }
 #pragma unroll
     for (int u = 0; u < NW; ++u) {
       const int e = tid + 256 * u;
-      sm.ws[e / RG_C][e % RG_C] = to_tf32(wv[u]);
+      sm.ws[e / RG_C][e % RG_C] = __float_as_uint(wv[u]);
     }
     __syncthreads();
     for (int ks = 0; ks < (kc + 7) / 8; ++ks) {
-      uint32_t af[4];
+      uint32_t ah[4], al[4];
       const uint32_t *xr = &sm.xs[mt * 16 + gr][ks * 8 + tq];
-      af[0] = xr[0];
-      af[1] = xr[8 * (RG_K + 4)];
-      af[2] = xr[4];
-      af[3] = xr[8 * (RG_K + 4) + 4];
+      const uint32_t araw[4] = {xr[0], xr[8 * (RG_K + 4)], xr[4], xr[8 * (RG_K + 4) + 4]};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) split_tf32(araw[i], ah[i], al[i]);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const uint32_t *wr = &sm.ws[ks * 8 + tq][(nt0 + t) * 8 + gr];
-        mma_m16n8k8_tf32(d[t], af, wr[0], wr[4 * (RG_C + 8)]);
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(wr[0], bh0, bl0);
+        split_tf32(wr[4 * (RG_C + 8)], bh1, bl1);
+        if constexpr (std::is_same<FT, float>::value) {
+          // split TF32: hi*lo + lo*hi + hi*hi, ~fp32-accurate products, so the bf16 W^T is
+          // the RNE of the (near-)exact W — the rounding the bf16 contract states
+          mma_m16n8k8_tf32(d[t], ah, bl0, bl1);
+          mma_m16n8k8_tf32(d[t], al, bh0, bh1);
+        }
+        mma_m16n8k8_tf32(d[t], ah, bh0, bh1);  // bf16 factors: exact in tf32, lo == 0
       }
     }
   }

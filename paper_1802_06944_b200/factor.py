@@ -44,6 +44,26 @@ class FactorPair:
         object.__setattr__(self, "wf", wf.clone() if wf.data_ptr() == _ptr(self.wf) else wf)
         self._cache["host"] = host
 
+    @classmethod
+    def adopt(cls, xf: torch.Tensor, wf: torch.Tensor, plan: LayerPlan,
+              bf16: tuple | None = None) -> "FactorPair":
+        """Take ownership of freshly made contiguous fp32 CUDA factors (no private copy: the
+        caller hands them over), optionally with their bf16 operand copies."""
+        if tuple(xf.shape) != (plan.m, plan.rank) or tuple(wf.shape) != (plan.rank, plan.n):
+            raise DimensionError(f"factors {tuple(xf.shape)} / {tuple(wf.shape)} do not match "
+                                 f"the plan ({plan.m}x{plan.rank}, {plan.rank}x{plan.n})")
+        for t in (xf, wf):
+            if t.dtype != torch.float32 or t.device.type != "cuda" or not t.is_contiguous():
+                raise ArgumentError("adopted factors must be contiguous fp32 CUDA tensors")
+        fp = cls.__new__(cls)
+        object.__setattr__(fp, "xf", xf)
+        object.__setattr__(fp, "wf", wf)
+        object.__setattr__(fp, "plan", plan)
+        object.__setattr__(fp, "_cache", {"host": False})
+        if bf16 is not None:
+            fp._cache["bf16"] = tuple(bf16)
+        return fp
+
     @property
     def dtype(self):
         return self.xf.dtype

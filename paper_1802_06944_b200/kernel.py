@@ -129,18 +129,20 @@ class forward_pipeline:
 
 
 def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float, y: torch.Tensor,
-                 mma: int, fused: bool = False) -> None:
+                 mma: int, fused: bool = False, ws: torch.Tensor | None = None) -> None:
     """Raw stream-ordered dt_forward on device tensors (no validation beyond the ABI's).
 
     bf16 tensor-core path: by default the two-phase kernels (W^T regenerated from the fp32
     factors, then the tcgen05 GEMM); ``fused=True`` runs the single fused kernel on the
-    packed bf16 factors (general geometries only)."""
+    packed bf16 factors (general geometries only). ``ws``: a caller-owned workspace (grown
+    here when too small); by default a fresh one per call."""
     p = fp.plan
     lib = _lib.lib()
     ps = _lib.plan_struct(p)
     batch = x.shape[0]
     ws_bytes = lib.dt_forward_workspace_bytes(C.byref(ps), batch, mma)
-    ws = workspace(ws_bytes)
+    if ws is None or ws.numel() < ws_bytes:
+        ws = workspace(ws_bytes)
     if mma == _lib.DT_MMA_BF16 and fused:
         xf, wf, fdt = fp.packed(), None, _lib.DT_FACTORS_PACKED
         if xf is None:

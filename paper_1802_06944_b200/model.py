@@ -1,0 +1,122 @@
+"""Device-resident compressed network loaded from a ``.dthn`` image.
+
+``DeviceModel`` is what ``CompressedModel.to_device`` returns (reference CompressedModel,
+model_io.py:46-63, whose layers the reference runs one ``layer_forward`` at a time,
+kernel.py:296-320). Loading is B200-first:
+
+* the serialized image goes to HBM in ONE pinned host→device copy (``h2d_bytes``);
+* every payload is decoded on the GPU by ``dt_unpack_values`` straight out of the device image
+  (unaligned little-endian float32/float64 → aligned fp32 masters, plus the bf16 operand copies
+  the tensor-core path reads), then the image is released — no host-side conversion;
+* the forward chains the layers on one stream with bf16 intermediates on the tensor-core path
+  (fp32 on the FFMA path), each layer with its own workspace so consecutive layers pipeline
+  (``forward_pipeline``: layer i+1's W regeneration overlaps layer i's GEMM; the regeneration
+  reads only the layer's own factors, never the activations in flight).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import as_device_matrix, device, stream_handle
+from .errors import ArgumentError, DimensionError
+from .factor import FactorPair
+from .kernel import _act_code, forward_into, forward_pipeline
+
+
+class DeviceModel:
+    """A multi-layer DeepThin network whose factors live in HBM.
+
+    activations: one name for every layer, or one per layer (default "identity"); act_args:
+    the clipped-ReLU ceiling per layer (default 20.0, as layer_forward). mma: "bf16" (tcgen05
+    tensor cores, bf16 intermediates) or "ffma" (fp32 CUDA cores, fp32 intermediates).
+    """
+
+    def __init__(self, model, activations=None, *, mma: str = "bf16", act_args=None,
+                 pipeline: bool = True):
+        if mma not in ("bf16", "ffma"):
+            raise ArgumentError(f"mma must be 'bf16' or 'ffma', got {mma!r}")
+        image, index = model.image()
+        count = len(index)
+        if activations is None or isinstance(activations, str):
+            activations = [activations or "identity"] * count
+        if act_args is None or isinstance(act_args, (int, float)):
+            act_args = [20.0 if act_args is None else float(act_args)] * count
+        if len(activations) != count or len(act_args) != count:
+            raise ArgumentError(f"need one activation / act_arg per layer ({count})")
+        plans = [plan for _, plan in model.plans.layers]
+        for i in range(1, count):
+            if plans[i].q != plans[i - 1].r_dim:
+                raise DimensionError(
+                    f"layer {model.layer_names[i]!r} takes {plans[i].q} inputs but "
+                    f"{model.layer_names[i - 1]!r} produces {plans[i - 1].r_dim}")
+        self.names = model.layer_names
+        self.mma = mma
+        self.pipeline = pipeline
+        self.codes = [_act_code(a) for a in activations]
+        self.act_args = [float(a) for a in act_args]
+
+        dev = device()
+        staging = torch.empty(len(image), dtype=torch.uint8, pin_memory=True)
+        staging.numpy()[:] = np.frombuffer(image, dtype=np.uint8)
+        img = staging.to(dev, non_blocking=True)
+        self.h2d_bytes = len(image)
+        lib, st, base = _lib.lib(), stream_handle(), img.data_ptr()
+        want16 = mma == "bf16"
+
+        def unpack(offset, shape, code):
+            out = torch.empty(shape, dtype=torch.float32, device=dev)
+            out16 = torch.empty(shape, dtype=torch.bfloat16, device=dev) if want16 else None
+            _lib.check(lib.dt_unpack_values(
+                out.numel(), base + offset, _lib.DT_F64 if code == 1 else _lib.DT_F32,
+                out.data_ptr(), out16.data_ptr() if out16 is not None else None, st))
+            return out, out16
+
+        self.factors, self.biases = [], []
+        for rec, plan in zip(index, plans):
+            xf, xf16 = unpack(rec.xf_offset, (plan.m, plan.rank), rec.dtype_code)
+            wf, wf16 = unpack(rec.wf_offset, (plan.rank, plan.n), rec.dtype_code)
+            bias, _ = unpack(rec.bias_offset, (rec.bias_len,), rec.dtype_code)
+            if rec.bias_len != plan.r_dim:
+                raise DimensionError(f"bias length {rec.bias_len} != output width {plan.r_dim}")
+            self.factors.append(FactorPair.adopt(xf, wf, plan, (xf16, wf16) if want16 else None))
+            self.biases.append(bias)
+        torch.cuda.current_stream().synchronize()  # the image (and staging) can go now
+        del img, staging
+        self._ws = [None] * count
+
+    @property
+    def plans(self):
+        return [fp.plan for fp in self.factors]
+
+    def forward(self, x, out_dtype=torch.float32):
+        """y = act_L(... act_1(x W_1 + b_1) ... W_L + b_L). Host (numpy) input returns a host
+        array; a CUDA tensor returns a CUDA tensor (stream-ordered, no sync)."""
+        xt, host = as_device_matrix(x, name="input")
+        if xt.shape[1] != self.factors[0].plan.q:
+            raise DimensionError(f"input has {xt.shape[1]} columns, the first layer takes "
+                                 f"{self.factors[0].plan.q}")
+        code = _lib.DT_MMA_BF16 if self.mma == "bf16" else _lib.DT_MMA_FFMA
+        mid = torch.bfloat16 if self.mma == "bf16" else torch.float32
+        lib = _lib.lib()
+        batch = xt.shape[0]
+        last = len(self.factors) - 1
+        with forward_pipeline(self.pipeline and self.mma == "bf16"):
+            for i, (fp, bias) in enumerate(zip(self.factors, self.biases)):
+                need = lib.dt_forward_workspace_bytes(C.byref(_lib.plan_struct(fp.plan)), batch,
+                                                      code)
+                if self._ws[i] is None or self._ws[i].numel() < need:
+                    self._ws[i] = torch.empty(max(need, 256), dtype=torch.uint8,
+                                              device=xt.device)
+                y = torch.empty((batch, fp.plan.r_dim), device=xt.device,
+                                dtype=out_dtype if i == last else mid)
+                forward_into(xt, fp, bias, self.codes[i], self.act_args[i], y, code,
+                             ws=self._ws[i])
+                xt = y
+        return xt.float().cpu().numpy() if host else xt
+
+    __call__ = forward

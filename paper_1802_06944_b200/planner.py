@@ -56,6 +56,25 @@ class LayerPlan:
         return self.q % self.n == 0
 
 
+@dataclass(frozen=True)
+class NetworkPlan:
+    """Per-layer plans of a network (reference planner.py:63-77): ordered (name, LayerPlan)
+    pairs, the target and achieved whole-network ratios, the layers that hit their accuracy
+    floor, and the dense bias counts the achieved ratio includes."""
+
+    layers: tuple
+    target_ratio: float
+    achieved_total_ratio: float
+    floor_hits: tuple
+    bias_counts: tuple = ()
+
+    def plan_for(self, name: str) -> LayerPlan:
+        found = [plan for layer_name, plan in self.layers if layer_name == name]
+        if not found:
+            raise KeyError(name)
+        return found[0]
+
+
 def baseline_plan(in_features: int, out_features: int, rank: int, n_f: int, m_f: int | None = None):
     """Build a plan from BASELINE.json notation (n=in, m=out, n_f, m_f, r)."""
     m = m_f if m_f is not None else -(-(in_features * out_features) // n_f)

@@ -1,0 +1,160 @@
+"""GPU parity of the .dthn loader → device-resident network.
+
+The network is the reference-serialized golden model (tests/golden/dthn.npz: fc0 12→40 rank 2
+general path, fc1 40→40 rank 3 reuse path, out 40→9 rank 1 reuse path) plus a BASELINE-config-3
+shaped network built here. Checks:
+  * decoding on the device is exact: fp32 masters == the stored values rounded by numpy
+    (float64 → float32 RNE), bf16 copies == RNE of those;
+  * FFMA network forward vs the oracle's layer chain (kernel.py:296-320 per layer, f64) on the
+    fp32-rounded factors: rel_error <= 1e-5;
+  * bf16 network forward vs the bf16 contract per layer, emulated in f64 with bf16
+    intermediates (what the device chain stores between layers): rel_error <= 4e-3 for the
+    3-layer chain (2e-3 per layer, north_star; an intermediate that lands on the other side of
+    a bf16 rounding boundary carries one bf16 ulp into the next layer);
+  * pipelined (PDL) and serial chains agree bit for bit.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import deepthin_oracle as O
+
+import paper_1802_06944_b200 as D
+from paper_1802_06944_b200 import model_io as mi
+from test_gpu_forward import bf16_contract
+
+pytestmark = pytest.mark.gpu
+
+ACTS = ["tanh", "relu", "identity"]
+
+
+@pytest.fixture(scope="module")
+def dthn():
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "dthn.npz"))
+
+
+def oplan(p):
+    return O.Plan(q=p.q, r_dim=p.r_dim, rank=p.rank, m=p.m, n=p.n)
+
+
+def oracle_chain(model, x, acts, *, factor_round, inter_round=None, contract=None):
+    h = x
+    for i, ((_, p), fp, b) in enumerate(zip(model.plans.layers, model.factors, model.biases)):
+        d = {"x": h, "xf": factor_round(fp.xf), "wf": factor_round(fp.wf)}
+        bias = np.asarray(b, dtype=np.float32).astype(np.float64)
+        if contract is None:
+            h = O.layer_forward(h, d["xf"], d["wf"], oplan(p), bias, acts[i])
+        else:
+            h = O.apply_activation(acts[i], contract(d, oplan(p), bias))
+        if inter_round is not None and i + 1 < len(model.factors):
+            h = inter_round(h)
+    return h
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("tag", ["f32", "f64"])
+def test_device_decode_is_exact(dthn, tag):
+    model = mi.deserialize(dthn[f"{tag}_bytes"].tobytes())
+    dm = model.to_device(ACTS, mma="bf16")
+    assert dm.h2d_bytes == len(dthn[f"{tag}_bytes"])
+    for fp, dfp, b, db in zip(model.factors, dm.factors, model.biases, dm.biases):
+        for host, dev in ((fp.xf, dfp.xf), (fp.wf, dfp.wf), (b, db)):
+            want = np.asarray(host).astype(np.float32)
+            assert np.array_equal(dev.cpu().numpy(), want.reshape(dev.shape))
+        for dev, dev16 in zip((dfp.xf, dfp.wf), dfp.bf16()):
+            assert torch.equal(dev16, dev.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("tag", ["f32", "f64"])
+def test_ffma_network_matches_oracle_chain(dthn, tag):
+    model = mi.deserialize(dthn[f"{tag}_bytes"].tobytes())
+    dm = model.to_device(ACTS, mma="ffma")
+    x = np.random.default_rng(3).standard_normal((200, 12))
+    y = dm.forward(x)
+    assert isinstance(y, np.ndarray) and y.shape == (200, 9)
+    want = oracle_chain(model, f32(x), ACTS, factor_round=f32)
+    assert O.rel_error(y, want) <= 1e-5
+
+
+def test_bf16_network_matches_contract_chain(dthn):
+    model = mi.deserialize(dthn["f64_bytes"].tobytes())
+    dm = model.to_device(ACTS, mma="bf16")
+    x = O.round_bf16(np.random.default_rng(4).standard_normal((300, 12)))
+    y = dm.forward(torch.tensor(x, dtype=torch.bfloat16, device="cuda"))
+    assert y.dtype == torch.float32 and tuple(y.shape) == (300, 9)
+    # every golden layer takes the two-phase path: W regenerated from the fp32 masters, then
+    # rounded to bf16 (the contract bf16_emulated states); the factors themselves stay fp32
+    want = oracle_chain(model, x, ACTS, factor_round=f32, inter_round=O.round_bf16,
+                        contract=bf16_contract)
+    assert O.rel_error(y.double().cpu().numpy(), want) <= 4e-3
+
+
+def config3_like(scale_out=3000, hidden=2048, layers=3, seed=0):
+    """BASELINE config 3's layer geometry (440 → hidden sigmoid ... → 3000 softmax, n_f = 256
+    where it divides the input width else 320, rank 3), fewer hidden layers."""
+    rng = np.random.default_rng(seed)
+    dims = [440] + [hidden] * layers + [scale_out]
+    entries, factors, biases = [], [], []
+    for i in range(len(dims) - 1):
+        q, r_dim = dims[i], dims[i + 1]
+        n = 256 if q % 256 == 0 else 320
+        m = -(-(q * r_dim) // n)
+        plan = D.LayerPlan(q=q, r_dim=r_dim, rank=3, m=m, n=n)
+        entries.append((f"fc{i}", plan))
+        # bf16-valued factors: the factored reuse layers read wf as bf16 and xf as tf32, so
+        # the contract emulation needs no extra factor rounding
+        factors.append(mi.StoredFactors(
+            O.round_bf16(rng.normal(0, 3 ** -0.5, (m, 3))).astype(np.float32),
+            O.round_bf16(rng.normal(0, 3 ** -0.5, (3, n))).astype(np.float32), plan))
+        biases.append(rng.normal(0, 0.01, r_dim).astype(np.float32))
+    plans = D.NetworkPlan(layers=tuple(entries), target_ratio=0.01, achieved_total_ratio=0.0,
+                          floor_hits=())
+    return mi.CompressedModel(plans=plans, factors=factors, biases=biases)
+
+
+def test_config3_shaped_network_bf16_and_pipeline():
+    """Parity on the logits (identity head); the softmax head separately. Softmax turns an
+    absolute logit error into a relative probability error (dp/p = dz), so a relative-to-max
+    bound on probabilities would measure the logits' magnitude, not the kernels."""
+    model = mi.deserialize(mi.serialize(config3_like()))
+    x = O.round_bf16(np.random.default_rng(5).standard_normal((512, 440)))
+    xt = torch.tensor(x, dtype=torch.bfloat16, device="cuda")
+    logits_acts = ["sigmoid"] * 3 + ["identity"]
+    serial = model.to_device(logits_acts, mma="bf16", pipeline=False)
+    piped = model.to_device(logits_acts, mma="bf16")
+    y0 = serial.forward(xt)
+    y1 = piped.forward(xt)
+    y2 = piped.forward(xt)  # second call: the first layer's W^T slot alternates
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1) and torch.equal(y1, y2)
+    logits = y0.double().cpu().numpy()
+    want = oracle_chain(model, x, logits_acts, factor_round=f32, inter_round=O.round_bf16,
+                        contract=bf16_contract)
+    assert O.rel_error(logits, want) <= 4e-3
+    probs = model.to_device(["sigmoid"] * 3 + ["softmax"], mma="bf16").forward(xt)
+    got = probs.double().cpu().numpy()
+    assert np.allclose(got.sum(axis=1), 1.0, atol=1e-5)
+    assert np.max(np.abs(got - O.apply_activation("softmax", logits))) <= 1e-6
+
+
+def test_chain_and_argument_errors(dthn):
+    model = mi.deserialize(dthn["f32_bytes"].tobytes())
+    with pytest.raises(D.ArgumentError):
+        model.to_device(["relu"], mma="bf16")
+    with pytest.raises(D.ArgumentError):
+        model.to_device(ACTS, mma="tf32")
+    broken = mi.CompressedModel(plans=D.NetworkPlan(
+        layers=(model.plans.layers[1], model.plans.layers[0]), target_ratio=0.5,
+        achieved_total_ratio=0.0, floor_hits=()),  # 40 -> 40 then a 12-input layer
+        factors=[model.factors[1], model.factors[0]], biases=[model.biases[1], model.biases[0]])
+    with pytest.raises(D.DimensionError):
+        broken.to_device("relu")
+    dm = model.to_device(ACTS, mma="ffma")
+    with pytest.raises(D.DimensionError):
+        dm.forward(np.zeros((4, 13)))
