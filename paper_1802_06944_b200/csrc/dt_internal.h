@@ -67,6 +67,16 @@ int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner,
                          uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
                          bool swizzle128);
 
+// ---- row-tile tensor-core forward for reuse geometries: k_tc_rows.cu ------------------
+// One persistent kernel: P = x_seg @ wf^T (bf16, TMEM) -> tf32 A operand -> y = act(P XF2^T + b),
+// TMA-stored. A prep kernel writes the bf16 wf and the K-padded XF2 into ws (tc_rows_ws bytes).
+// Softmax is not fused (caller post-pass).
+bool tc_rows_ok(const Geo &g, int x_dtype, int y_dtype);
+size_t tc_rows_ws(const Geo &g);
+int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
+                    const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
+                    cudaStream_t st);
+
 // ---- two-phase tensor-core path: k_tc_gemm.cu ---------------------------------------
 // W^T (r_dim x round_up(q, 8), bf16) regenerated from the factors (f_dtype DT_F32 or DT_BF16)
 // into the workspace, then a persistent tcgen05 GEMM y = act(x W + bias). Any geometry.

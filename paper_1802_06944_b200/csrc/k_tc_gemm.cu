@@ -1469,7 +1469,8 @@ size_t tc_gemm_ws(const Geo &g, int64_t batch) {
   const int64_t ldw = round_up(g.q, 8);
   const size_t two_phase =  // two W^T slots (pipelined forwards alternate) + packed x
       2 * (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
-  return std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0);
+  return std::max(std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0),
+                  tc_rows_ws(g));
 }
 
 struct MseArgs {
@@ -1550,6 +1551,16 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
       cur += round_up(bytes, 256);
       return r;
     };
+    // one-kernel row-tile form (k_tc_rows.cu) when the geometry and operands allow it
+    if (!mse && tc_rows_ok(g, x_dtype, y_dtype) && ((reinterpret_cast<uintptr_t>(x) |
+        reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0) {
+      const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
+      if (int rc = tc_rows_forward(g, batch, x, reinterpret_cast<const float *>(wf),
+                                   reinterpret_cast<const float *>(xf), bias, eact, act_arg, y,
+                                   y_dtype, ws, st))
+        return rc;
+      return act == DT_ACT_SOFTMAX ? launch_row_softmax(batch, g.r_dim, y, y_dtype, st) : DT_OK;
+    }
     char *wf16 = take(g.rank * g.n * 2);
     float *P = reinterpret_cast<float *>(take(batch * g.s * g.rank * 4));
     char *x_ws = take(batch * g.q * 2);

@@ -1,0 +1,672 @@
+// Row-tile tensor-core forward for reuse geometries (n_f | q): the factored DeepThin layer in
+// ONE persistent kernel, batch rows on the MMA M axis, output written through TMA stores.
+//
+// Reference: kernel.py:1-16 / 99-164 (the reuse identity: every output column reads s = q/n
+// whole rows of I = xf @ wf, so each distinct run dot x_seg . wf[k] is computed once) and
+// kernel.py:296-320 (layer_forward = act(x W + b)). In BASELINE notation, per 128-row tile:
+//
+//   phase A:  P[b, seg, k] = sum_t x[b, seg*n + t] * wf[k, t]        (bf16 x bf16 -> fp32, TMEM)
+//   phase B:  y[b, j] = act(sum_{seg,k} xf[j*s + seg, k] * P[b, seg, k] + bias[j])
+//             = act(P2[b, :] . XF2[j, :] + bias[j]),  XF2 = xf viewed (r_dim x s*rank)
+//             (kind::tf32 on the fp32 P and the fp32 master xf, fp32 accumulate)
+//
+// No W and no P ever touch HBM: per row the kernel reads q bf16 inputs and writes r_dim
+// outputs, so it is HBM-bound (config 3: 8 KB per row per 2048-wide layer, ~13 flop/B).
+//
+// A cluster of cs CTAs (8 when s allows) shares each 128-row tile: CTA c contracts only
+// segments c, c+cs, ... (so x is read from HBM exactly once and every SM streams), broadcasts
+// its P values into the tf32 A operand of every cluster CTA through distributed shared memory,
+// then computes and stores output chunks c, c+cs, ... Clusters are persistent over tiles.
+//
+// Warp roles (480 threads, one CTA per SM):
+//   warp 0  TMA producer of x k-blocks (128 rows x 64 bf16, SW128) into a 4-deep ring
+//   warp 1  TMA producer of XF2 chunks (128 output columns x 32 fp32, SW128), 2-deep ring
+//   warp 2  TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 3-6  P exchange: P (TMEM) -> tf32 A operand of every cluster CTA (DSMEM stores)
+//   warps 7-14 epilogue: D chunks (TMEM, double-buffered 2 x 128 columns) -> bias +
+//           activation -> bf16/fp32 -> swizzled shared staging -> TMA store (each warp its
+//           own 32 rows x 128 B boxes).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "act.cuh"
+#include "dt_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dt {
+namespace {
+
+using namespace ptx;
+
+constexpr int kTM = 128;           // batch rows per tile (UMMA M = TMEM lanes)
+constexpr int kNc = 128;           // output columns per D chunk (UMMA N of phase B)
+constexpr int kXSMax = 8;          // x ring depth cap (the launcher sizes it to the smem left)
+constexpr int kBS = 2;             // XF2 chunk ring depth (resident when a CTA has <= 2 chunks)
+constexpr int kPW = 4;             // P-exchange warps (one per TMEM lane quarter)
+constexpr int kEpi = 8;            // epilogue warps (two per TMEM lane quarter)
+constexpr int kRowsThreads = 32 * (3 + kPW + kEpi);
+constexpr uint32_t kXBytes = kTM * 128;   // 128 rows x 64 bf16
+constexpr uint32_t kBBytes = kNc * 128;   // 128 columns x 32 fp32
+constexpr uint32_t kA2Bytes = kTM * 128;  // 128 rows x 32 fp32 (k2 <= 32)
+constexpr uint32_t kOutBox = 32 * 128;    // one warp's 32 rows x 128 B staging box
+constexpr uint32_t kDCol = 256;           // TMEM column of the first D buffer (P below it)
+// A2 descriptor strides (see a2n_off)
+constexpr uint32_t kA2Lbo = 2048, kA2Sbo = 128;
+
+struct RowsParams {
+  int64_t batch;
+  int r_dim, n_tiles, s, nkb, np, rank, rp, k2, n_chunks, cs, xs, pcols;
+  const float *bias;
+  void *y;
+  float arg;
+  uint32_t off_x, off_a2, off_wf, off_b, off_out, off_bar;
+  unsigned long long *trace;  // DEEPTHIN_ROWS_TRACE: globaltimer stamps of cluster 0
+};
+
+constexpr int kTr = 64;  // trace slots per CTA
+__device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
+  if (p.trace && blockIdx.x < 8 && slot < kTr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * kTr + slot] = t;
+  }
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Epilogue activations of the tensor-core path (contract rel_error <= 2e-3): MUFU tanh.approx
+// (max rel. error 2^-11) — one MUFU op per element instead of ex2 + rcp + Newton steps.
+template <int ACT>
+__device__ __forceinline__ float act_fast(float z, float arg) {
+  if constexpr (ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f);
+  if constexpr (ACT == DT_ACT_TANH) return tanh_fast(z);
+  return act_apply<ACT>(z, arg);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c,
+                                             uint32_t &d) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ void st_global_v4(void *ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+// No-swizzle K-major layout of the 128-row x k2 tf32 A operand: core matrices of 8 rows x 16 B
+// (4 K values); M-adjacent core matrices 128 B apart (SBO), K-adjacent 2 KB apart (LBO) — so
+// every 4-K column block of all 128 rows is one contiguous 2 KB run (bulk-copyable).
+__device__ __forceinline__ uint32_t a2n_off(int row, int kk) {
+  return (uint32_t)(kk >> 2) * 2048u + (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u +
+         (uint32_t)(kk & 3) * 4u;
+}
+// shared::cta -> shared::cluster bulk copy, completion counted on the destination's mbarrier
+__device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                         uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+      : "memory");
+}
+
+// Cluster of cs CTAs per 128-row tile. CTA c of the cluster:
+//   * loads and contracts only its own segments seg = c, c + cs, ... (x read once from HBM);
+//   * pushes its P values (rank per segment per row, padded to rp) into the tf32 A operand of
+//     every cluster CTA with shared->shared bulk copies (A2 double-buffered by tile parity);
+//   * computes and stores its own output chunks ch = c, c + cs, ... (128 columns each).
+// Tiles are strided over the clusters (persistent); the MMA issuer runs phase A of tile i+1
+// before phase B of tile i (P double-buffered in TMEM), so the exchange latency is hidden.
+template <int YDT, int ACT>
+__global__ void __launch_bounds__(kRowsThreads, 1)
+    k_tc_rows_reuse(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_wf,
+                    const __grid_constant__ CUtensorMap tm_xf2, const __grid_constant__ CUtensorMap tm_y,
+                    const RowsParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+  uint64_t *x_full = bars, *x_empty = bars + kXSMax;
+  uint64_t *b_full = bars + 2 * kXSMax, *b_empty = b_full + kBS;
+  uint64_t *d_full = b_empty + kBS, *d_empty = d_full + 2;
+  uint64_t *a2_full = d_empty + 2, *a2_free = a2_full + 2;
+  uint64_t *p_full = a2_free + 2, *wf_full = p_full + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(wf_full + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int cs = p.cs;
+  const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
+  const int cid = (int)blockIdx.x / cs, ncl = (int)gridDim.x / cs;
+  const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
+  const int my_chunks = crank < p.n_chunks ? (p.n_chunks - crank + cs - 1) / cs : 0;
+  const bool b_res = my_chunks <= kBS;  // XF2 chunks loaded once, resident for every tile
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.xs; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < kBS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], kEpi);
+      mbar_init(&a2_full[i], 1);   // local arm (expect_tx of the peers' bytes)
+      mbar_init(&a2_free[i], cs);  // every cluster CTA's MMAs on this buffer done
+      mbar_init(&p_full[i], 1);
+    }
+    mbar_init(wf_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_wf);
+    tma_prefetch_desc(&tm_xf2);
+    tma_prefetch_desc(&tm_y);
+  }
+  if (warp == 2) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  if (cs > 1) cluster_sync();  // peers' barriers initialised before any remote copy/arrive
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) rtrace(p, 0);
+  // Everything below reads buffers an earlier kernel on the stream may write (x is the previous
+  // layer's output; factors/bias may come from an SGD step): wait for it, let the next start.
+  griddep_wait();
+  griddep_launch_dependents();
+
+  const int n = p.nkb * 64;
+  if (warp == 0) {
+    // ---------------- x producer: this CTA's segments of each tile ----------------
+    if (lane == 0) {
+      // wf (rank x n bf16, rows rank..np-1 zero-filled by TMA) stays resident: nkb blocks of
+      // np rows x 128 B
+      uint8_t *wf_s = smem + p.off_wf;
+      mbar_arrive_expect_tx(wf_full, (uint32_t)(p.nkb * p.np * 128));
+      for (int kb = 0; kb < p.nkb; ++kb)
+        tma_load_2d(wf_s + kb * p.np * 128, &tm_wf, wf_full, kb * 64, 0);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = cid; t < p.n_tiles; t += ncl)
+        for (int seg = crank; seg < p.s; seg += cs)
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(&x_empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&x_full[st], kXBytes);
+            tma_load_2d(smem + p.off_x + st * kXBytes, &tm_x, &x_full[st], seg * n + kb * 64, t * kTM);
+            if (++st == p.xs) { st = 0; ph ^= 1; }
+          }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- XF2 chunk producer: this CTA's output chunks ----------------
+    if (lane == 0) {
+      if (b_res) {
+        int i = 0;
+        for (int c = crank; c < p.n_chunks; c += cs, ++i) {
+          mbar_arrive_expect_tx(&b_full[i], kBBytes);
+          tma_load_2d(smem + p.off_b + i * kBBytes, &tm_xf2, &b_full[i], 0, c * kNc);
+        }
+      } else {
+        int st = 0;
+        uint32_t ph = 0;
+        for (int t = cid; t < p.n_tiles; t += ncl)
+          for (int c = crank; c < p.n_chunks; c += cs) {
+            mbar_wait(&b_empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&b_full[st], kBBytes);
+            tma_load_2d(smem + p.off_b + st * kBBytes, &tm_xf2, &b_full[st], 0, c * kNc);
+            if (++st == kBS) { st = 0; ph ^= 1; }
+          }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t s0 = smem_u32(smem);
+      const uint32_t wf_s = s0 + p.off_wf;
+      const uint32_t idA = idesc_f32acc(kTM, (uint32_t)p.np, 1);
+      const uint32_t idB = idesc_f32acc(kTM, kNc, 2);
+      mbar_wait(wf_full, 0);
+      const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
+      int xs = 0, bs = 0, db = 0;
+      uint32_t xph = 0, bph = 0, dph = 0;
+      for (int i = 0; i <= ntl; ++i) {
+        if (i < ntl) {
+          // phase A of tile i into P[i & 1] (read out by the P warps before they armed
+          // a2_full of tile i-2, which phase B of tile i-2 below waited on)
+          const uint32_t pc = tbase + (uint32_t)((i & 1) * p.pcols);
+          int j = 0;
+          for (int seg = crank; seg < p.s; seg += cs, ++j) {
+            const uint32_t d = pc + (uint32_t)(j * p.np);
+            for (int kb = 0; kb < p.nkb; ++kb) {
+              mbar_wait(&x_full[xs], xph);
+              if (kb == 0 && j == 0) rtrace(p, 1 + 4 * min(i, 7));
+              tc_fence_after();
+              const uint32_t a = s0 + p.off_x + (uint32_t)xs * kXBytes;
+              const uint32_t b = wf_s + (uint32_t)(kb * p.np * 128);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(d, smem_desc(a + k * 32, 16, 1024, SL_SW128),
+                            smem_desc(b + k * 32, 16, 1024, SL_SW128), idA, (kb | k) != 0);
+              mma_commit(&x_empty[xs]);
+              if (++xs == p.xs) { xs = 0; xph ^= 1; }
+            }
+          }
+          mma_commit(&p_full[i & 1]);
+        }
+        if (i >= 1) {
+          // phase B of tile i-1: every cluster CTA's P landed in A2[(i-1) & 1]
+          const int tb = i - 1, ab = tb & 1;
+          mbar_wait_cluster(&a2_full[ab], (uint32_t)(tb >> 1) & 1u);
+          rtrace(p, 2 + 4 * min(tb, 7));
+          tc_fence_after();
+          const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)ab * kA2Bytes;
+          int ci = 0;
+          for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
+            const int slot = b_res ? ci : bs;
+            mbar_wait(&b_full[slot], b_res ? 0u : bph);
+            mbar_wait(&d_empty[db], dph ^ 1);
+            tc_fence_after();
+            const uint32_t d = tbase + kDCol + (uint32_t)(db * kNc);
+            const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
+            for (int k = 0; k < p.k2 / 8; ++k)
+              mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
+                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
+            if (!b_res) {
+              mma_commit(&b_empty[bs]);
+              if (++bs == kBS) { bs = 0; bph ^= 1; }
+            }
+            mma_commit(&d_full[db]);
+            if (++db == 2) { db = 0; dph ^= 1; }
+          }
+          // this CTA's reads of A2[ab] are done when these MMAs complete: tell every writer
+          if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 3 + kPW) {
+    // ---------------- P exchange: TMEM -> tf32 A operand of every cluster CTA ----------------
+    const int sp = warp & 3, row = 32 * sp + lane;
+    const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
+    const uint32_t a2_local = smem_u32(smem) + p.off_a2;
+    for (int b = 0; b < 2; ++b)  // K padding of the tf32 operand (never overwritten)
+      for (int kk = p.s * p.rp; kk < p.k2; kk += 4)
+        st_shared_v4(a2_local + (uint32_t)b * kA2Bytes + a2n_off(row, kk), 0u, 0u, 0u, 0u);
+    uint32_t it = 0;
+    for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
+      const int ab = (int)(it & 1);
+      mbar_wait(&p_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+      mbar_wait(&a2_free[ab], ((it >> 1) & 1) ^ 1);  // all readers of tile it-2 finished
+      const bool trp = false;
+      if (trp) rtrace(p, 44 + 4 * (int)it);
+      const uint32_t a2b = a2_local + (uint32_t)ab * kA2Bytes;
+      // own P values (rank padded to rp with zeros) into this CTA's A2[ab], one 16-byte store
+      // per 4 K values
+      int j = 0;
+      for (int seg = crank; seg < p.s; seg += cs, ++j) {
+        for (int g = 0; g < p.np; g += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(ab * p.pcols + j * p.np + g), v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k0 = 0; k0 < 32; k0 += 4) {
+            if (g + k0 < p.rp) {
+              uint32_t w[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) w[i] = (g + k0 + i < p.rank) ? v[k0 + i] : 0u;
+              st_shared_v4(a2b + a2n_off(row, seg * p.rp + g + k0), w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      }
+      if (trp) rtrace(p, 45 + 4 * (int)it);
+      tc_fence_before();
+      fence_proxy_async_smem();  // visible to the local MMAs and to the bulk-copy engine
+      named_bar_sync(1, 32 * kPW);
+      if (warp == 3) {
+        // lane r (1..cs-1) pushes this CTA's blocks into peer (crank + r) % cs, completion
+        // counted on the peer's a2_full[ab]; lane 0 arms the local barrier for the peers' bytes
+        if (lane >= 1 && lane < cs) {
+          const uint32_t peer = (uint32_t)((crank + lane) % cs);
+          const uint32_t bar = mapa_shared(smem_u32(&a2_full[ab]), peer);
+          for (int seg = crank; seg < p.s; seg += cs)
+            for (int c4 = seg * p.rp / 4; c4 < (seg + 1) * p.rp / 4; ++c4) {
+              const uint32_t src = a2b + (uint32_t)c4 * 2048u;
+              bulk_s2c(mapa_shared(src, peer), src, 2048u, bar);
+            }
+        }
+        if (lane == 0) {
+          const int own = ((p.s - crank + cs - 1) / cs) * (p.rp / 4);
+          mbar_arrive_expect_tx(&a2_full[ab], (uint32_t)(p.s * p.rp / 4 - own) * 2048u);
+        }
+        if (trp) rtrace(p, 46 + 4 * (int)it);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int sp = warp & 3;           // TMEM lane quarter this warp may access
+    const int e = warp - 3 - kPW;      // 0..7
+    const int half = e / 4;            // which 64 columns of each 128-column chunk
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
+    constexpr int E = YDT == DT_BF16 ? 2 : 4;
+    constexpr int UC = 128 / E;        // output columns per 128-byte store box
+    const uint32_t out_s = s0 + p.off_out + (uint32_t)e * kOutBox;
+    int db = 0;
+    uint32_t dph = 0, it = 0;
+    for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
+      const int64_t row0 = (int64_t)t * kTM + 32 * sp;
+      for (int c = crank; c < p.n_chunks; c += cs) {
+        mbar_wait(&d_full[db], dph);
+        if (warp == 3 + kPW && c == crank) rtrace(p, 3 + 4 * (int)min(it, 7u));
+        tc_fence_after();
+        const int tsl = 44 + 8 * (int)(it * 2 + (c - crank) / cs) ;
+        const bool tre = warp == 3 + kPW && lane == 0 && it < 1;
+        {
+          const int h = half;
+          if (tre) rtrace(p, tsl + 4 * h);
+          const int col0 = c * kNc + 64 * h;
+          uint32_t v[64];
+          tmem_ld_32x32b_x32(tbase + lane_t + kDCol + (uint32_t)(db * kNc + 64 * h),
+                             *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_ld_32x32b_x32(tbase + lane_t + kDCol + (uint32_t)(db * kNc + 64 * h + 32),
+                             *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[db]);
+          if (tre) rtrace(p, tsl + 4 * h + 1);
+          if (col0 < p.r_dim) {
+          // bias + activation in fp32
+          // bias: one coalesced load per 32 columns, broadcast by shuffles (per-element
+          // broadcast loads serialise on their latency)
+          float blo = 0.f, bhi = 0.f;
+          if (p.bias) {
+            if (col0 + lane < p.r_dim) blo = __ldg(p.bias + col0 + lane);
+            if (col0 + 32 + lane < p.r_dim) bhi = __ldg(p.bias + col0 + 32 + lane);
+          }
+          float o[64];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            o[i] = act_fast<ACT>(__uint_as_float(v[i]) + __shfl_sync(0xffffffffu, blo, i), p.arg);
+            o[i + 32] = act_fast<ACT>(__uint_as_float(v[i + 32]) + __shfl_sync(0xffffffffu, bhi, i), p.arg);
+          }
+          if (tre) rtrace(p, tsl + 4 * h + 2);
+          // 64 columns = 64*E bytes per row = (E/2) boxes of 32 rows x 128 B: pack into the
+          // warp's swizzled staging box (conflict-free), read it back 4 rows per instruction
+          // (8 lanes per 128-byte row) and store full lines with st.global.v4
+#pragma unroll
+          for (int u = 0; u < E / 2; ++u) {
+            if (col0 + u * UC >= p.r_dim) break;
+            const uint32_t rb = out_s + (uint32_t)lane * 128u;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              uint32_t w0, w1, w2, w3;
+              if constexpr (E == 2) {
+                const float *f = o + ch * 8;
+                w0 = pack_bf16(f[0], f[1]); w1 = pack_bf16(f[2], f[3]);
+                w2 = pack_bf16(f[4], f[5]); w3 = pack_bf16(f[6], f[7]);
+              } else {
+                const float *f = o + u * 32 + ch * 4;
+                w0 = __float_as_uint(f[0]); w1 = __float_as_uint(f[1]);
+                w2 = __float_as_uint(f[2]); w3 = __float_as_uint(f[3]);
+              }
+              st_shared_v4(rb + ((uint32_t)(ch ^ (lane & 7)) << 4), w0, w1, w2, w3);
+            }
+            __syncwarp();
+            const int ch = lane & 7;
+            const int cb = col0 + u * UC + ch * (16 / E);  // first column of this lane's 16 B
+            uint32_t w[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 4 * i + (lane >> 3);
+              ld_shared_v4(out_s + (uint32_t)r * 128u + ((uint32_t)(ch ^ (r & 7)) << 4), w[i][0],
+                           w[i][1], w[i][2], w[i][3]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 4 * i + (lane >> 3);
+              if (row0 + r < p.batch && cb < p.r_dim)
+                st_global_v4(reinterpret_cast<uint8_t *>(p.y) + ((row0 + r) * p.r_dim + cb) * E, w[i][0],
+                             w[i][1], w[i][2], w[i][3]);
+            }
+            __syncwarp();
+          }
+          }
+          if (tre) rtrace(p, tsl + 4 * h + 3);
+        }
+        if (++db == 2) { db = 0; dph ^= 1; }
+      }
+    }
+    if (warp == 3 + kPW) rtrace(p, 40);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (cs > 1) cluster_sync();  // no CTA leaves while peers may still copy into / arrive on it
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
+
+template <int YDT>
+RowsFn pick_act(int act) {
+  switch (act) {
+    case DT_ACT_RELU: return k_tc_rows_reuse<YDT, DT_ACT_RELU>;
+    case DT_ACT_SIGMOID: return k_tc_rows_reuse<YDT, DT_ACT_SIGMOID>;
+    case DT_ACT_TANH: return k_tc_rows_reuse<YDT, DT_ACT_TANH>;
+    case DT_ACT_CLIPPED_RELU: return k_tc_rows_reuse<YDT, DT_ACT_CLIPPED_RELU>;
+    default: return k_tc_rows_reuse<YDT, DT_ACT_IDENTITY>;
+  }
+}
+
+int g_nsm() {
+  static int nsm = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return nsm;
+}
+
+}  // namespace
+
+// Cluster size: CTAs sharing one row tile (segments and output chunks split among them).
+static int rows_cluster(const Geo &g) {
+  static const int want = getenv("DEEPTHIN_ROWS_CS") ? atoi(getenv("DEEPTHIN_ROWS_CS")) : 8;
+  for (int cs : {8, 4, 2})
+    if (cs <= want && g.s % cs == 0) return cs;
+  return 1;
+}
+
+// Geometries the row-tile kernel takes: reuse (n | q), 64-aligned segments, the padded rank's
+// wf block resident (<= 32 KB), s * round_up(rank, 4) <= 32 (one 128-byte tf32 K atom),
+// TMA-legal output pitch.
+bool tc_rows_ok(const Geo &g, int x_dtype, int y_dtype) {
+  static const int want = getenv("DEEPTHIN_ROWS") ? atoi(getenv("DEEPTHIN_ROWS")) : 1;
+  if (!want || !g.reuse || g.n % 64 != 0 || x_dtype != DT_BF16) return false;
+  const int64_t np = (g.rank + 15) / 16 * 16;
+  const int64_t rp = (g.rank + 3) / 4 * 4;
+  if (g.s * rp > 32 || (g.s / rows_cluster(g)) * np > 128) return false;
+  if ((g.n / 64) * np * 128 > 32 * 1024) return false;
+  const int E = y_dtype == DT_BF16 ? 2 : 4;
+  if ((g.r_dim * E) % 16 != 0) return false;
+  return true;
+}
+
+static int64_t rows_k2(const Geo &g) { return (g.s * ((g.rank + 3) / 4 * 4) + 7) / 8 * 8; }
+
+size_t tc_rows_ws(const Geo &g) {
+  if (!g.reuse) return 0;
+  return (size_t)((g.rank * g.n * 2 + 255) / 256 * 256) + (size_t)((g.r_dim * rows_k2(g) * 4 + 255) / 256 * 256);
+}
+
+namespace {
+// Per-call operand prep (the analogue of the reference's per-pair derived copies,
+// kernel.py:157-164): wf -> bf16, and XF2 re-laid with each segment's rank values padded to rp
+// (zeros), K padded to k2: XF2p[j, seg*rp + k] = xf[j*s + seg, k].
+__global__ void k_rows_prep(int64_t wf_count, const float *wf, __nv_bfloat16 *wf16, int r_dim, int s,
+                            int rank, int rp, int k2, const float *xf, float *xf2p) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int64_t tot = wf_count + (int64_t)r_dim * k2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < wf_count) {
+      wf16[i] = __float2bfloat16_rn(wf[i]);
+    } else {
+      const int64_t e = i - wf_count;
+      const int64_t j = e / k2;
+      const int kk = (int)(e - j * k2), seg = kk / rp, k = kk - seg * rp;
+      xf2p[e] = (seg < s && k < rank) ? xf[(j * s + seg) * rank + k] : 0.f;
+    }
+  }
+}
+}  // namespace
+
+int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
+                    const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
+                    cudaStream_t st) {
+  if (batch == 0) return DT_OK;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15) ||
+      (reinterpret_cast<uintptr_t>(ws) & 255)) {
+    set_error("row-tile kernel: operands must be 16-byte aligned");
+    return DT_E_ARG;
+  }
+  RowsParams p{};
+  p.batch = batch;
+  p.r_dim = (int)g.r_dim;
+  p.n_tiles = (int)((batch + kTM - 1) / kTM);
+  p.s = (int)g.s;
+  p.nkb = (int)(g.n / 64);
+  p.np = (int)((g.rank + 15) / 16 * 16);
+  p.rank = (int)g.rank;
+  p.rp = (int)((g.rank + 3) / 4 * 4);
+  p.k2 = (int)rows_k2(g);
+  p.n_chunks = (int)((g.r_dim + kNc - 1) / kNc);
+  p.cs = rows_cluster(g);
+  p.bias = bias;
+  p.y = y;
+  p.arg = act_arg;
+  // shared memory: x ring | A2 x 2 | wf | XF2 ring | output staging | barriers
+  p.pcols = (int)((g.s / p.cs) * p.np);
+  // shared memory: A2 x 2 | wf | XF2 ring | output staging | x ring (what is left) | barriers
+  const uint32_t wf_bytes = (uint32_t)(p.nkb * p.np * 128);
+  p.off_a2 = 0;
+  p.off_wf = 2 * kA2Bytes;
+  p.off_b = (p.off_wf + wf_bytes + 1023) & ~1023u;
+  p.off_out = p.off_b + kBS * kBBytes;
+  p.off_x = p.off_out + kEpi * kOutBox;
+  constexpr uint32_t kSmemMax = 227 * 1024, kTail = 512 + 1024;
+  p.xs = (int)std::min<uint32_t>(kXSMax, (kSmemMax - kTail - p.off_x) / kXBytes);
+  p.off_bar = p.off_x + (uint32_t)p.xs * kXBytes;
+  const uint32_t smem_bytes = p.off_bar + kTail;
+
+  __nv_bfloat16 *wf16 = reinterpret_cast<__nv_bfloat16 *>(ws);
+  float *xf2p = reinterpret_cast<float *>(ws + (g.rank * g.n * 2 + 255) / 256 * 256);
+  {
+    const int64_t tot = g.rank * g.n + g.r_dim * (int64_t)p.k2;
+    cudaLaunchConfig_t pc{};
+    pc.gridDim = dim3((unsigned)std::min<int64_t>((tot + 255) / 256, 4 * g_nsm()));
+    pc.blockDim = dim3(256);
+    pc.stream = st;
+    cudaLaunchAttribute pa[1];
+    pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pa[0].val.programmaticStreamSerializationAllowed = 1;
+    pc.attrs = pa;
+    pc.numAttrs = 1;
+    DT_CUDA_CHECK(cudaLaunchKernelEx(&pc, k_rows_prep, (int64_t)(g.rank * g.n), wf, wf16,
+                                     (int)g.r_dim, (int)g.s, (int)g.rank, p.rp, p.k2, xf, xf2p));
+    if (int rc = check_launch("rows_prep")) return rc;
+  }
+
+  CUtensorMap tm_x, tm_wf, tm_xf2, tm_y;
+  if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(x), (uint64_t)g.q,
+                                    (uint64_t)batch, (uint64_t)g.q * 2, 64, kTM, true))
+    return rc;
+  if (int rc = encode_tensor_map_2d(&tm_wf, DT_BF16, wf16, (uint64_t)g.n, (uint64_t)g.rank,
+                                    (uint64_t)g.n * 2, 64, (uint32_t)p.np, true))
+    return rc;
+  if (int rc = encode_tensor_map_2d(&tm_xf2, DT_F32, xf2p, (uint64_t)p.k2, (uint64_t)g.r_dim,
+                                    (uint64_t)p.k2 * 4, 32, kNc, true))
+    return rc;
+  const int E = y_dtype == DT_BF16 ? 2 : 4;
+  if (int rc = encode_tensor_map_2d(&tm_y, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
+                                    (uint64_t)g.r_dim * E, 128 / E, 32, true))
+    return rc;
+
+  RowsFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(act) : pick_act<DT_F32>(act);
+  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kRowsThreads);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = (unsigned)p.cs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  // persistent: as many clusters as fit at once (each loops over row tiles)
+  static int max_cl[9] = {0};
+  if (!max_cl[p.cs]) {
+    if (p.cs > 1)
+      DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    cfg.gridDim = dim3((unsigned)(p.cs * 64));
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl <= 0) {
+      (void)cudaGetLastError();
+      ncl = g_nsm() / p.cs;
+    }
+    max_cl[p.cs] = ncl;
+  }
+  const int ncl = std::max(1, std::min(p.n_tiles, max_cl[p.cs]));
+  cfg.gridDim = dim3((unsigned)(ncl * p.cs));
+  static const bool tracing = getenv("DEEPTHIN_ROWS_TRACE") != nullptr;
+  if (tracing) {
+    DT_CUDA_CHECK(cudaMalloc(&p.trace, 8 * kTr * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 8 * kTr * 8, st));
+  }
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, tm_y, p));
+  if (tracing) {
+    unsigned long long h[8 * kTr];
+    DT_CUDA_CHECK(cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    DT_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFree(p.trace);
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < 8 * kTr; ++i) if (h[i] && h[i] < t0) t0 = h[i];
+    fprintf(stderr, "rows trace: grid %d clusters x %d, tiles %d, chunks %d, s %d\n", ncl, p.cs,
+            p.n_tiles, p.n_chunks, p.s);
+    for (int b = 0; b < std::min(8, ncl * p.cs); ++b) {
+      fprintf(stderr, " cta %d:", b);
+      for (int i = 0; i < kTr; ++i)
+        if (h[b * kTr + i]) fprintf(stderr, " %d:%.2f", i, (h[b * kTr + i] - t0) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+  }
+  return check_launch("tc_rows_reuse");
+}
+
+}  // namespace dt

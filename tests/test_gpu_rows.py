@@ -1,0 +1,79 @@
+"""GPU parity of the row-tile reuse kernel (k_tc_rows.cu): the factored DeepThin layer in one
+persistent tcgen05 kernel (P = x_seg @ wf^T in TMEM -> tf32 A operand -> y = act(P XF2^T + b),
+TMA-stored). It serves bf16 inputs on reuse geometries (n | q) with n % 64 == 0 and
+s * rank <= 32 — BASELINE config 3's hidden/output layers and config 4's FC layers.
+
+Bounds (rel_error = max|a-e| / max|e|, core.py:91-95):
+  * <= 1e-3 against the factored bf16 contract emulated in f64 (the only rounding left is P's
+    and xf's tf32 truncation);
+  * <= 2e-3 against the oracle's layer_forward (kernel.py:296-320) on the same bf16 inputs;
+  * activations on the kernel's own logits: sigmoid/tanh use MUFU tanh.approx (max relative
+    error 2^-11), so |act - oracle act(logits)| <= 6e-4 absolute (fp32 output).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import deepthin_oracle as O
+
+import paper_1802_06944_b200 as D
+from test_gpu_forward import bf16_factored_emulated, gpu_x, make_case
+
+pytestmark = pytest.mark.gpu
+
+GEOS = [
+    # q, r_dim, rank, n, m, batch
+    (2048, 2048, 3, 256, 16384, 1000),   # config 3 hidden layer, ragged batch
+    (2048, 3000, 3, 256, 24000, 300),    # config 3 output layer (3000 = 23.4 chunks)
+    (512, 640, 4, 64, 5120, 129),        # s * rank = 32 (full tf32 atom)
+    (128, 96, 2, 64, 192, 77),           # s * rank = 4 -> K padded to 8
+    (2048, 2048, 1, 256, 16384, 5),      # rank 1 (the reference's fused_matmul case)
+]
+
+
+@pytest.mark.parametrize("geo", GEOS)
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+def test_rows_reuse_matches_contract_and_oracle(geo, out):
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=21, rnd=O.round_bf16, bias_sd=0.1)
+    y = D.layer_forward(gpu_x(d["x"], torch.bfloat16), fp, d["bias"], mma="bf16", out_dtype=out)
+    assert y.dtype == out
+    got = y.double().cpu().numpy()
+    extra = 2 ** -8 if out == torch.bfloat16 else 0.0
+    assert O.rel_error(got, bf16_factored_emulated(d, plan, d["bias"])) <= 1e-3 + extra
+    ref = O.layer_forward(d["x"], d["xf"], d["wf"], plan, d["bias"], "identity")
+    assert O.rel_error(got, ref) <= 2e-3 + extra
+
+
+@pytest.mark.parametrize("act", ["relu", "sigmoid", "tanh", "clipped_relu", "softmax"])
+def test_rows_activations(act):
+    plan, d, fp = make_case(2048, 2048, 3, 256, 16384, 256, seed=4, rnd=O.round_bf16, bias_sd=0.5)
+    x = gpu_x(d["x"], torch.bfloat16)
+    pre = D.layer_forward(x, fp, d["bias"], "identity", mma="bf16")
+    y = D.layer_forward(x, fp, d["bias"], act, mma="bf16", act_arg=2.0)
+    want = O.apply_activation(act, pre.double().cpu().numpy(), 2.0)
+    err = np.max(np.abs(y.double().cpu().numpy() - want))
+    assert err <= (6e-4 if act in ("sigmoid", "tanh") else 1e-6), (act, err)
+
+
+def test_rows_deterministic_and_shard_invariant():
+    plan, d, fp = make_case(2048, 2048, 3, 256, 16384, 2048, seed=5, rnd=O.round_bf16)
+    x = gpu_x(d["x"], torch.bfloat16)
+    y1 = D.layer_forward(x, fp, d["bias"], "sigmoid", mma="bf16", out_dtype=torch.bfloat16)
+    y2 = D.layer_forward(x, fp, d["bias"], "sigmoid", mma="bf16", out_dtype=torch.bfloat16)
+    assert torch.equal(y1, y2)
+    for lo, hi in ((0, 128), (128, 1024), (1000, 2048), (77, 300)):
+        ys = D.layer_forward(x[lo:hi].contiguous(), fp, d["bias"], "sigmoid", mma="bf16",
+                             out_dtype=torch.bfloat16)
+        assert torch.equal(ys, y1[lo:hi]), (lo, hi)
+
+
+def test_rows_large_batch_persistent_tiles():
+    # more 128-row tiles than SMs: every CTA loops over several tiles (ring/TMEM phase reuse)
+    plan, d, fp = make_case(512, 640, 4, 64, 5120, 148 * 128 * 2 + 50, seed=6, rnd=O.round_bf16)
+    x = gpu_x(d["x"], torch.bfloat16)
+    pre = D.layer_forward(x, fp, d["bias"], "identity", mma="bf16")
+    assert O.rel_error(pre, bf16_factored_emulated(d, plan, d["bias"])) <= 1e-3
+    y = D.layer_forward(x, fp, d["bias"], "tanh", mma="bf16")
+    assert np.max(np.abs(y.double().cpu().numpy() - np.tanh(pre.double().cpu().numpy()))) <= 6e-4
