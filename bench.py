@@ -40,6 +40,12 @@ CONFIGS = {
            "general path regen+tcgen05"),
     "c1": (1024, 1024, 16, 256, 4096, 64,
            "config1: DeepThin layer 1024->1024 reuse path (m_f 4096, n_f 256, r 16), fp32 FFMA"),
+    # config 3: the network (440 -> 6 x 2048 sigmoid -> 3000 softmax, rank 3), global batch
+    # 16384 sharded over the ranks (strong scaling); q/r_dim/... describe its widest layer
+    "c3": (2048, 2048, 3, 256, 16384, 16384,
+           "config3: 7-layer DeepThin acoustic-model network 440 -> 6x2048 (sigmoid) -> 3000 "
+           "(softmax), rank 3 (~1% of the dense parameters), n_f 256 (320 for the 440-wide input), "
+           "bf16, batch 16384 frames"),
     "c5": (8192, 8192, 64, 1024, 65536, 8192,
            "config5: DeepThin layer 8192->8192 training step (m_f 65536, n_f 1024, r 64), reuse path "
            "factored on tensor cores: forward + MSE + backward + grad all-reduce + SGD"),
@@ -173,13 +179,16 @@ def run_reference(args, cfg, key):
     if key == "c5":
         c = cpu_train_time(cfg)
         sps, threads, sample = c["value"], c["cores"], c["sample"]
+    elif key == "c3":
+        sps, threads, sample = cpu_network_time(budget_s=budget)
     else:
         sps, threads, sample = cpu_reference_time(cfg, budget_s=budget)
-    metric = "compressed-layer training samples/sec" if key == "c5" else "compressed-layer samples/sec"
+    metric = {"c5": "compressed-layer training samples/sec",
+              "c3": "compressed-network samples/sec"}.get(key, "compressed-layer samples/sec")
     line = {"impl": "reference", "metric": metric, "value": round(sps, 3),
             "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(cfg[5] / sps * 1e3, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if key == "c3" else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg[6], "batch": cfg[5]},
             "cpu_baseline": {"value": round(sps, 3), "unit": "samples/s", "cores": threads,
                              "kind": "port", "sample": sample},
@@ -525,6 +534,225 @@ def run_ours(args, cfg, key):
         tdist.destroy_process_group()
 
 
+C3_DIMS = [440] + [2048] * 6 + [3000]
+C3_ACTS = ["sigmoid"] * 6 + ["softmax"]
+
+
+def c3_layers(rank=3):
+    """Config-3 layer geometry: n_f = 256 where it divides the input width, else 320;
+    m_f = ceil(q * r_dim / n_f) (the smallest m_f covering the layer); rank 3 for ~1% of the
+    dense parameters (1.04-1.19% per layer)."""
+    out = []
+    for q, r_dim in zip(C3_DIMS[:-1], C3_DIMS[1:]):
+        n = 256 if q % 256 == 0 else 320
+        out.append((q, r_dim, rank, n, -(-(q * r_dim) // n)))
+    return out
+
+
+def c3_params(seed=0):
+    """Seeded factors per layer (spawn_rngs children [xf, wf, bias] per layer, factors
+    N(0, stddev 1/sqrt(r)), bias N(0, 0.01)) — the BASELINE distributions."""
+    import numpy as np
+    from paper_1802_06944_b200.core import sample_normal, spawn_rngs
+    layers = c3_layers()
+    rngs = spawn_rngs(seed, 3 * len(layers) + 1)
+    params = []
+    for i, (q, r_dim, rank, n, m) in enumerate(layers):
+        sd = 1.0 / math.sqrt(rank)
+        params.append((sample_normal(rngs[3 * i], 0.0, sd, (m, rank)).astype(np.float32),
+                       sample_normal(rngs[3 * i + 1], 0.0, sd, (rank, n)).astype(np.float32),
+                       sample_normal(rngs[3 * i + 2], 0.0, 0.01, (r_dim,)).astype(np.float32)))
+    return layers, params, rngs[-1]
+
+
+def cpu_network_time(budget_s=12.0, rows=512):
+    """The reference's own route for the network on the host cores: per layer
+    layer_forward (decompress + matmul + bias, kernel.py:296-320) then the activation, in f64."""
+    import numpy as np
+    threads = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    from oracle import deepthin_oracle as O
+    layers, params, rx = c3_params()
+    from paper_1802_06944_b200.core import sample_normal
+    x = sample_normal(rx, 0.0, 1.0, (rows, C3_DIMS[0]))
+
+    def fwd():
+        h = x
+        for (q, r_dim, rank, n, m), (xf, wf, b), act in zip(layers, params, C3_ACTS):
+            h = O.apply_activation(act, O.layer_forward(h, xf, wf, O.Plan(q=q, r_dim=r_dim, rank=rank,
+                                                                          m=m, n=n), b))
+        return h
+
+    fwd()
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        fwd()
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return rows / med, threads, (f"{len(times)} forwards of the 7-layer network (oracle.layer_forward "
+                                 f"+ activation per layer, f64) on {rows} rows, median "
+                                 f"{med * 1e3:.1f} ms")
+
+
+def run_network(args, cfg, key):
+    """Config 3: one step = the 7-layer network forward of this rank's batch shard (strong
+    scaling: global batch 16384 / world), bf16 activations, tcgen05 kernels."""
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    rank, world, local = dist_init()
+    torch.cuda.set_device(local)
+    import paper_1802_06944_b200 as D
+    from paper_1802_06944_b200 import _lib
+    from paper_1802_06944_b200 import model_io as mi
+    from paper_1802_06944_b200.core import sample_normal
+
+    layers, params, rx = c3_params()
+    entries, factors, biases = [], [], []
+    for i, ((q, r_dim, rk, n, m), (xf, wf, b)) in enumerate(zip(layers, params)):
+        plan = D.LayerPlan(q=q, r_dim=r_dim, rank=rk, m=m, n=n)
+        entries.append((f"fc{i}", plan))
+        factors.append(mi.StoredFactors(xf, wf, plan))
+        biases.append(b)
+    model = mi.CompressedModel(plans=D.NetworkPlan(layers=tuple(entries), target_ratio=0.01,
+                                                   achieved_total_ratio=0.0, floor_hits=()),
+                               factors=factors, biases=biases)
+    dm = model.to_device(C3_ACTS, mma="bf16")
+    gbatch = cfg[5]
+    batch = gbatch // world
+    x_all = sample_normal(rx, 0.0, 1.0, (gbatch, C3_DIMS[0])).astype(np.float32)
+    x_host = torch.tensor(x_all[rank * batch:(rank + 1) * batch]).to(torch.bfloat16)
+    xs = [x_host.cuda() for _ in range(2)]
+    stream = torch.cuda.current_stream()
+    lib = _lib.lib()
+    counter = [0]
+
+    def step():
+        y = dm.forward(xs[counter[0] % 2], out_dtype=torch.bfloat16)
+        counter[0] += 1
+        return y
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local).__enter__()
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 0.5:
+        step()
+        torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    n0 = lib.dt_launch_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        y = step()
+    ev1.record(stream)
+    barrier()
+    launches = lib.dt_launch_counter() - n0
+    clocks = sampler.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = gbatch * args.steps / (total_ms / 1e3)
+    net_bytes = sum(2 * batch * (q + r) for q, r in zip(C3_DIMS[:-1], C3_DIMS[1:]))
+
+    # roofline of the dominant kernel: the row-tile reuse kernel (6 of the 7 layers), every
+    # launch bracketed by CUDA events on the launching stream over K more steps
+    bf16_peak, hbm_peak, peak_kind = peaks()
+    nl = 6 * args.steps
+    evb = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
+    eva = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
+    for e in evb + eva:
+        e.record(stream)
+    barrier()
+    arr_b = (C.c_void_p * nl)(*[e.cuda_event for e in evb])
+    arr_a = (C.c_void_p * nl)(*[e.cuda_event for e in eva])
+    _lib.check(lib.dt_profile_kernel_kind(_lib.DT_PROF_ROWS))
+    _lib.check(lib.dt_profile_kernel_events(arr_b, arr_a, nl))
+    for _ in range(args.steps):
+        step()
+    _lib.check(lib.dt_profile_kernel_events(None, None, 0))
+    _lib.check(lib.dt_profile_kernel_kind(_lib.DT_PROF_ANY))
+    barrier()
+    kms = [b.elapsed_time(a) for b, a in zip(evb, eva)]
+    reuse = [(q, r, rk, n, m) for (q, r, rk, n, m) in layers if q % n == 0]
+    per_launch = [batch * (q + r) * 2 + r * (q // n) * 4 * 4 + rk * n * 4 + r * 4
+                  for (q, r, rk, n, m) in reuse]
+    bytes_alg = sum(per_launch[i % 6] for i in range(nl))
+    achieved = bytes_alg / (sum(kms) * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "traffic": traffic_for(key),
+            "peak_source": f"{peak_kind} hbm_gbs",
+            "kernel": "k_tc_rows_reuse (row-tile reuse kernel, layers 1-6)",
+            "kernel_us": round(statistics.mean(kms) * 1e3, 3),
+            "kernel_share_of_step": round(sum(kms) / args.steps / ms_per_step, 3),
+            "algorithmic_bytes": int(statistics.mean(per_launch))}
+
+    # e2e through the public API: pinned host x -> device -> DeviceModel.forward -> pinned host y
+    hx = x_host.pin_memory()
+    hy = torch.empty((batch, C3_DIMS[-1]), dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        xd = hx.to("cuda", non_blocking=True)
+        yd = dm.forward(xd, out_dtype=torch.bfloat16)
+        hy.copy_(yd, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(3):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    e2e_value = gbatch * args.steps / float(te.item())
+    ok = torch.equal(hy.cuda(), y)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, threads, sample = cpu_network_time(budget_s=args.cpu_budget)
+        cpu = {"value": round(sps, 3), "unit": "samples/s", "cores": threads, "kind": "port",
+               "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": "compressed-network samples/sec", "value": round(value, 1),
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg[6], "global_batch": gbatch, "batch_per_gpu": batch,
+                       "parallelism": f"dp{world} (batch-sharded, no collective)",
+                       "activation_bytes_per_step": net_bytes,
+                       "hbm_gbs_whole_step": round(net_bytes / (ms_per_step * 1e-3) / 1e9, 1),
+                       "l2": (f"activations {2 * batch * 2048 >> 20} MiB per hidden layer, "
+                              f"{net_bytes >> 20} MiB per step >> 126 MiB L2 (no flush needed)"),
+                       "effective_tflops_dense_equiv": round(sum(
+                           2.0 * batch * q * r for q, r in zip(C3_DIMS[:-1], C3_DIMS[1:])) /
+                           (ms_per_step * 1e-3) / 1e12, 2)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 1), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(hx.numel() * 2),
+                    "d2h_bytes_per_step": int(hy.numel() * 2), "matches_device_path": bool(ok)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -546,6 +774,8 @@ def main():
         run_reference(args, cfg, args.config)
     elif args.config == "c5":
         run_train(args, cfg, args.config)
+    elif args.config == "c3":
+        run_network(args, cfg, args.config)
     else:
         run_ours(args, cfg, args.config)
 

@@ -88,6 +88,10 @@ int64_t dt_launch_counter(void);
  * Events are cudaEvent_t handles created by the caller. No reference counterpart: used by
  * bench.py for the roofline of the dominant kernel. */
 int dt_profile_kernel_events(void *const *before, void *const *after, int n);
+/* Which launches dt_profile_kernel_events brackets (this thread): DT_PROF_ANY (default), the
+ * two-phase GEMM / FFMA forward (DT_PROF_GEMM), or the row-tile reuse kernel (DT_PROF_ROWS). */
+enum { DT_PROF_ANY = 0, DT_PROF_GEMM = 1, DT_PROF_ROWS = 2 };
+int dt_profile_kernel_kind(int kind);
 /* Inference pipelining (this thread): with enable = 1, consecutive bf16 tensor-core forwards
  * on one stream overlap each call's W regeneration with the previous call's GEMM (programmatic
  * dependent launch; W^T alternates between two workspace slots). The caller promises that the

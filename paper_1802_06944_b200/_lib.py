@@ -17,11 +17,12 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
 DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA, DT_E_FORMAT = range(6)
 DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64 = 0, 1, 2, 3
 DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
+DT_PROF_ANY, DT_PROF_GEMM, DT_PROF_ROWS = 0, 1, 2
 ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "dt_version", "dt_last_error", "dt_launch_counter", "dt_profile_kernel_events", "dt_set_forward_pipeline", "dt_plan_validate", "dt_plan_query", "dt_phase",
+    "dt_version", "dt_last_error", "dt_launch_counter", "dt_profile_kernel_events", "dt_profile_kernel_kind", "dt_set_forward_pipeline", "dt_plan_validate", "dt_plan_query", "dt_phase",
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
@@ -83,6 +84,7 @@ def _declare(lib):
         "dt_last_error": ([], C.c_char_p),
         "dt_launch_counter": ([], I64),
         "dt_profile_kernel_events": ([C.POINTER(VP), C.POINTER(VP), i], i),
+        "dt_profile_kernel_kind": ([i], i),
         "dt_set_forward_pipeline": ([i], i),
         "dt_forward_mse_workspace_bytes": ([P, I64], SZ),
         "dt_forward_mse": ([P, I64, VP, i, VP, VP, VP, VP, D, VP, VP, VP, SZ, VP], i),

@@ -79,13 +79,13 @@ int check_act(int act) {
 
 thread_local void *const *g_prof_before = nullptr;
 thread_local void *const *g_prof_after = nullptr;
-thread_local int g_prof_n = 0, g_prof_used = 0;
+thread_local int g_prof_n = 0, g_prof_used = 0, g_prof_kind = 0;
 thread_local bool g_pipeline = false;
 
 }  // namespace
 
-void dt::profile_next(cudaEvent_t *before, cudaEvent_t *after) {
-  if (g_prof_used < g_prof_n) {
+void dt::profile_next(cudaEvent_t *before, cudaEvent_t *after, int kind) {
+  if (g_prof_used < g_prof_n && (g_prof_kind == 0 || g_prof_kind == kind)) {
     *before = (cudaEvent_t)g_prof_before[g_prof_used];
     *after = (cudaEvent_t)g_prof_after[g_prof_used];
     ++g_prof_used;
@@ -106,6 +106,15 @@ int64_t dt_launch_counter(void) { return launch_count(); }
 
 int dt_set_forward_pipeline(int enable) {
   g_pipeline = enable != 0;
+  return DT_OK;
+}
+
+int dt_profile_kernel_kind(int kind) {
+  if (kind < DT_PROF_ANY || kind > DT_PROF_ROWS) {
+    set_error("dt_profile_kernel_kind: unknown kind " + std::to_string(kind));
+    return DT_E_ARG;
+  }
+  g_prof_kind = kind;
   return DT_OK;
 }
 
@@ -274,7 +283,7 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
     }
     if (batch == 0) return DT_OK;
     cudaEvent_t eb, ea;
-    profile_next(&eb, &ea);
+    profile_next(&eb, &ea, DT_PROF_GEMM);
     if (eb) DT_CUDA_CHECK(cudaEventRecord(eb, st));
     int rc = ffma_forward(g, batch, x, x_dtype, (const float *)xf, (const float *)wf, bias, act,
                           act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);

@@ -102,7 +102,7 @@ size_t tc_backward_ws(const Geo &g, int64_t batch);
 
 // dt_profile_kernel_events: events to record around the next dominant-kernel launch on this
 // thread (both null when disarmed / exhausted).
-void profile_next(cudaEvent_t *before, cudaEvent_t *after);
+void profile_next(cudaEvent_t *before, cudaEvent_t *after, int kind);
 // dt_set_forward_pipeline state of this thread.
 bool forward_pipeline();
 

@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int64_t ld = p.ldy;
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
               if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               yp += ld;
             }
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
               if (r < rmax) {
-                const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+                const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
                 if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               }
               yp += p.ldy;
@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int64_t ld = p.ldy;
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
               if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               yp += ld;
             }
@@ -1082,7 +1082,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
               if (r < rmax) {
-                const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+                const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
                 if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               }
               yp += p.ldy;
@@ -1386,7 +1386,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   p.off_rg = wbytes >= sizeof(RegenSmem) ? 0u : p.off_x + pre_stages * p.stage_bytes;
   const bool rg_fits = p.off_rg + sizeof(RegenSmem) <= p.off_bar;
   cudaEvent_t ev_b = nullptr, ev_a = nullptr;  // dt_profile_kernel_events: bracket the GEMM
-  if (c.profile) profile_next(&ev_b, &ev_a);
+  if (c.profile) profile_next(&ev_b, &ev_a, DT_PROF_GEMM);
   bool done = false;
   if (p.wgen) {
     if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));

@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
             if (r < rmax) {
-              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
               if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
             }
             yp += p.ldy;
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
             if (r < rmax) {
-              const float o = act_apply<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
               if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
             }
             yp += p.ldy;

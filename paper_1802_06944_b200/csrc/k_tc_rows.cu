@@ -75,18 +75,19 @@ __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
   }
 }
 
-__device__ __forceinline__ float tanh_fast(float x) {
+__device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// Epilogue activations of the tensor-core path (contract rel_error <= 2e-3): MUFU tanh.approx
-// (max rel. error 2^-11) — one MUFU op per element instead of ex2 + rcp + Newton steps.
-template <int ACT>
-__device__ __forceinline__ float act_fast(float z, float arg) {
-  if constexpr (ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f);
-  if constexpr (ACT == DT_ACT_TANH) return tanh_fast(z);
-  return act_apply<ACT>(z, arg);
+// bf16 outputs: one MUFU op per element (tanh.approx, relative error 2^-11: <= 2.5e-4 absolute
+// on a sigmoid, below the bf16 output's own rounding of up to 2^-9 relative); fp32 outputs:
+// act_fast (ex2 + rcp, ~1e-7).
+template <int YDT, int ACT>
+__device__ __forceinline__ float act_out(float z, float arg) {
+  if constexpr (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f);
+  if constexpr (YDT == DT_BF16 && ACT == DT_ACT_TANH) return tanh_approx(z);
+  return act_fast<ACT>(z, arg);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -403,8 +404,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           float o[64];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            o[i] = act_fast<ACT>(__uint_as_float(v[i]) + __shfl_sync(0xffffffffu, blo, i), p.arg);
-            o[i + 32] = act_fast<ACT>(__uint_as_float(v[i + 32]) + __shfl_sync(0xffffffffu, bhi, i), p.arg);
+            o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]) + __shfl_sync(0xffffffffu, blo, i), p.arg);
+            o[i + 32] = act_out<YDT, ACT>(__uint_as_float(v[i + 32]) + __shfl_sync(0xffffffffu, bhi, i), p.arg);
           }
           if (tre) rtrace(p, tsl + 4 * h + 2);
           // 64 columns = 64*E bytes per row = (E/2) boxes of 32 rows x 128 B: pack into the
@@ -649,7 +650,11 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
     DT_CUDA_CHECK(cudaMalloc(&p.trace, 8 * kTr * 8));
     DT_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 8 * kTr * 8, st));
   }
+  cudaEvent_t ev_b = nullptr, ev_a = nullptr;  // dt_profile_kernel_events
+  profile_next(&ev_b, &ev_a, DT_PROF_ROWS);
+  if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
   DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, tm_y, p));
+  if (ev_a) DT_CUDA_CHECK(cudaEventRecord(ev_a, st));
   if (tracing) {
     unsigned long long h[8 * kTr];
     DT_CUDA_CHECK(cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st));

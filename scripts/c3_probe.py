@@ -60,7 +60,7 @@ for i, fp in enumerate(dm.factors):
     lib = D._lib.lib()
     need = lib.dt_forward_workspace_bytes(C.byref(D._lib.plan_struct(fp.plan)), B, code)
     ws = torch.empty(max(need, 256), dtype=torch.uint8, device="cuda")
-    tl = timeit(lambda k: forward_into(xi[k % 4], fp, bias, _act_code("sigmoid"), 20.0, yi[k % 4],
+    tl = timeit(lambda k: forward_into(xi[k % 4], fp, bias, _act_code(os.environ.get("LACT", "sigmoid")), 20.0, yi[k % 4],
                                        code, ws=ws))
     by = 2 * B * (q + r)
     print(f"layer {i} {q}->{r} reuse={fp.plan.reuse_path}: {tl:.1f} us, {by / tl / 1e3:.0f} GB/s "
