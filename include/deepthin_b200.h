@@ -179,6 +179,21 @@ int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtyp
 
 /* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);
+/* The four recurrent gate contractions of one LSTM step (BASELINE config 4): gh[g] = h @ W_g +
+ * bias[g] for four DeepThin layers sharing one square reuse geometry (plan: q == r_dim, n | q),
+ * h fp32 (batch x q), exact fp32 on the CUDA cores in the reference's factored reuse form
+ * (kernel.py:1-16, 296-320). xf/wf/bias/gh: four pointers each (bias may be NULL). */
+size_t dt_lstm_gates_workspace_bytes(const dt_plan *plan, int64_t batch);
+int dt_lstm_gates(const dt_plan *plan, int64_t batch, const float *h, const float *const *xf,
+                  const float *const *wf, const float *const *bias, float *const *gh,
+                  void *workspace, size_t workspace_bytes, dt_stream stream);
+/* LSTM cell step of BASELINE config 4 (no reference counterpart: SURVEY.md §8(a) a8 lists LSTM
+ * gates as outside the reference). Gate order i, f, g, o; gx[g]: bf16 input projections
+ * (batch rows, row stride ld_gx, biases included); gh[g]: fp32 recurrent projections (batch x
+ * hidden, contiguous). c (fp32, batch x hidden) is updated in place; h32 (fp32) and/or h16
+ * (bf16) receive h' = o * tanh(c'). */
+int dt_lstm_cell(int64_t batch, int64_t hidden, const void *const *gx, int64_t ld_gx,
+                 const float *const *gh, float *c, float *h32, void *h16, dt_stream stream);
 
 /* ---- host-buffer entry points (the binding a numpy caller would use) -------- */
 /* A session owns device-resident copies of one layer's factors and bias — the

@@ -458,3 +458,49 @@ def round_bf16(a):
     u = a32.view(np.uint32).astype(np.uint64)
     rounded = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
     return rounded.astype(np.uint32).view(np.float32).astype(FLOAT64)
+
+
+# ---- BASELINE config 4: the speech-RNN-shaped network (UNPINNED by the reference) ----------
+# The reference has no LSTM. Every contraction below is the pinned
+# layer_forward (kernel.py:296-320); the cell is the standard LSTM cell, gate order i, f, g, o.
+
+def _sigmoid(z):
+    return 1.0 / (1.0 + np.exp(-z))
+
+
+def lstm_cell(gx, gh, c):
+    """One cell step: gx/gh are the 4 input/recurrent gate pre-activations (lists), c the state.
+    Returns (h', c')."""
+    i, f, g, o = (_sigmoid(gx[0] + gh[0]), _sigmoid(gx[1] + gh[1]), np.tanh(gx[2] + gh[2]),
+                  _sigmoid(gx[3] + gh[3]))
+    cn = f * c + i * g
+    return o * np.tanh(cn), cn
+
+
+def speech_forward(x, layers, clip=20.0, layer=None, store=None):
+    """Config-4 forward in f64. x: (T, B, n_in); layers: name -> (xf, wf, Plan, bias) for
+    fc1-3, x_{i,f,g,o}, h_{i,f,g,o}, fc4, out. ``layer(name, h, xf, wf, plan, bias)`` overrides
+    the contraction (default: layer_forward); ``store(a)`` rounds every activation the device
+    stores between layers (default: identity). The recurrence itself stays unrounded."""
+    layer = layer or (lambda name, h, xf, wf, plan, b: layer_forward(h, xf, wf, plan, b))
+    store = store or (lambda a: a)
+    T, B, n_in = x.shape
+    h = x.reshape(T * B, n_in).astype(np.float64)
+
+    def run(name, h):
+        xf, wf, plan, b = layers[name]
+        return layer(name, h, xf, wf, plan, b)
+
+    for name in ("fc1", "fc2", "fc3"):
+        h = store(apply_activation("clipped_relu", run(name, h), clip))
+    gx = [store(run(f"x_{g}", h)) for g in "ifgo"]
+    H = layers["h_i"][2].q
+    hp = np.zeros((B, H))
+    c = np.zeros((B, H))
+    seq = np.zeros((T * B, H))
+    for t in range(T):
+        gh = [run(f"h_{g}", hp) for g in "ifgo"]
+        hp, c = lstm_cell([a[t * B:(t + 1) * B] for a in gx], gh, c)
+        seq[t * B:(t + 1) * B] = store(hp)
+    h = store(apply_activation("clipped_relu", run("fc4", seq), clip))
+    return run("out", h).reshape(T, B, -1)

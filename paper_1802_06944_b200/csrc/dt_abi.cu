@@ -411,6 +411,64 @@ int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_str
   return launch_sgd(count, param, grad, lr, (cudaStream_t)stream);
 }
 
+size_t dt_lstm_gates_workspace_bytes(const dt_plan *plan, int64_t batch) {
+  Geo g;
+  if (make_geo(plan, &g) || batch < 0 || !lstm_gates_ok(g)) return 0;
+  return std::max<size_t>(256, lstm_gates_ws(g, batch));
+}
+
+int dt_lstm_gates(const dt_plan *plan, int64_t batch, const float *h, const float *const *xf,
+                  const float *const *wf, const float *const *bias, float *const *gh,
+                  void *workspace, size_t workspace_bytes, dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (batch < 0) {
+    set_error("batch must be >= 0");
+    return DT_E_DIM;
+  }
+  if (!lstm_gates_ok(g)) {
+    set_error("lstm_gates: needs a square reuse geometry (n | q, q == r_dim), rank <= 64, "
+              "s*rank <= 256 and a multiple of 4, n <= 1024");
+    return DT_E_UNSUPPORTED;
+  }
+  if (batch > 0) {
+    if (!h || !xf || !wf || !gh || !workspace) {
+      set_error("lstm_gates: NULL operand pointer");
+      return DT_E_ARG;
+    }
+    for (int i = 0; i < 4; ++i)
+      if (!xf[i] || !wf[i] || !gh[i]) {
+        set_error("lstm_gates: NULL gate pointer");
+        return DT_E_ARG;
+      }
+    if (workspace_bytes < lstm_gates_ws(g, batch)) {
+      set_error("lstm_gates: workspace too small");
+      return DT_E_ARG;
+    }
+  }
+  return lstm_gates(g, batch, h, xf, wf, bias, gh, (char *)workspace, (cudaStream_t)stream);
+}
+
+int dt_lstm_cell(int64_t batch, int64_t hidden, const void *const *gx, int64_t ld_gx,
+                 const float *const *gh, float *c, float *h32, void *h16, dt_stream stream) {
+  if (batch < 0 || hidden < 0 || ld_gx < hidden) {
+    set_error("lstm_cell: batch, hidden >= 0 and ld_gx >= hidden");
+    return DT_E_DIM;
+  }
+  if (batch > 0 && hidden > 0) {
+    if (!gx || !gh || !c || (!h32 && !h16)) {
+      set_error("lstm_cell: NULL operand pointer");
+      return DT_E_ARG;
+    }
+    for (int g = 0; g < 4; ++g)
+      if (!gx[g] || !gh[g]) {
+        set_error("lstm_cell: NULL gate pointer");
+        return DT_E_ARG;
+      }
+  }
+  return launch_lstm_cell(batch, hidden, gx, ld_gx, gh, c, h32, h16, (cudaStream_t)stream);
+}
+
 // ---- host-buffer sessions ---------------------------------------------------------------
 // Host-buffer sessions. A call is split into row chunks that alternate between two streams:
 // chunk c's H2D copy, forward and D2H copy are ordered on stream c % 2, so the two copy

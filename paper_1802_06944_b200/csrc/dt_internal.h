@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../include/deepthin_b200.h"
@@ -41,6 +42,14 @@ int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, 
                     float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st);
 size_t mse_ws(int64_t rows, int64_t cols);
 int launch_sgd(int64_t count, float *p, const float *g, float lr, cudaStream_t st);
+// config-4 recurrent step: the four H -> H reuse-geometry gate contractions of h (fp32, exact)
+bool lstm_gates_ok(const Geo &g);
+size_t lstm_gates_ws(const Geo &g, int64_t batch);
+int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *xf,
+               const float *const *wf, const float *const *bias, float *const *gh, char *ws,
+               cudaStream_t st);
+int launch_lstm_cell(int64_t batch, int64_t hidden, const void *const *gx, int64_t ld_gx,
+                     const float *const *gh, float *c, float *h32, void *h16, cudaStream_t st);
 int launch_act_grad(int64_t count, const float *up, const float *pre, int act, float act_arg,
                     float *out, cudaStream_t st);
 // fixed-order column sums of a rows x cols fp32 matrix (partials in `part`, colsum_ws bytes)

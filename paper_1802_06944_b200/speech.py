@@ -1,0 +1,210 @@
+"""BASELINE config 4: speech-RNN-shaped model with every weight DeepThin-compressed.
+
+    input 494 (26 features x 19 context frames)
+      -> fc1, fc2, fc3: 2048, clipped ReLU at 20
+      -> unidirectional LSTM 2048 (four input and four recurrent gate matrices, each a DeepThin
+         layer of rank 32)
+      -> fc4: 2048, clipped ReLU at 20
+      -> out: 29 logits
+
+Each matrix is the reference's compressed layer (kernel.py:296-320 ``layer_forward`` on a
+``FactorPair``, factor.py:23-93): n_f = 256 where it divides the input width, else 320;
+m_f = ceil(q * r_dim / n_f); FC ranks 3 (~1% of the dense parameters, the config-3 rule, SURVEY
+Appendix A) and 1 for the 29-wide output. The reference has no LSTM: the
+cell is the standard one (gate order i, f, g, o), restated in ``oracle/deepthin_oracle.py``.
+
+Execution (B200): the time-parallel layers (fc1-3, the four input projections, fc4, out) run
+once over all T*B frames on the bf16 tensor-core path; the recurrence runs T steps of four
+exact-fp32 recurrent contractions (the FFMA reuse kernel, batch B) plus one fused cell kernel,
+captured once into a CUDA graph and replayed (launch-latency-bound at batch 64).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import device, sample_normal, spawn_rngs, stream_handle
+from .errors import ArgumentError, DimensionError
+from .factor import FactorPair
+from .kernel import _act_code, forward_into
+from .planner import LayerPlan
+
+GATES = ("i", "f", "g", "o")
+
+
+def compressed_plan(q: int, r_dim: int, rank: int) -> LayerPlan:
+    """n_f = 256 if it divides q else 320; the smallest m_f covering q * r_dim."""
+    n = 256 if q % 256 == 0 else 320
+    return LayerPlan(q=q, r_dim=r_dim, rank=rank, m=-(-(q * r_dim) // n), n=n)
+
+
+class SpeechRNN:
+    """Config-4 model on the device. ``layers``: name -> (FactorPair, bias) for fc1, fc2, fc3,
+    x_i, x_f, x_g, x_o (input projections), h_i, h_f, h_g, h_o (recurrent), fc4, out."""
+
+    NAMES = ("fc1", "fc2", "fc3") + tuple(f"x_{g}" for g in GATES) + \
+        tuple(f"h_{g}" for g in GATES) + ("fc4", "out")
+
+    def __init__(self, layers: dict, clip: float = 20.0):
+        missing = [k for k in self.NAMES if k not in layers]
+        if missing:
+            raise ArgumentError(f"missing layers {missing}")
+        self.layers = {}
+        for k in self.NAMES:
+            fp, b = layers[k]
+            bt = torch.as_tensor(np.asarray(b, dtype=np.float32)).to(device())
+            if bt.numel() != fp.plan.r_dim:
+                raise DimensionError(f"{k}: bias length {bt.numel()} != {fp.plan.r_dim}")
+            self.layers[k] = (fp, bt)
+        self.hidden = self.layers["h_i"][0].plan.q
+        self.n_in = self.layers["fc1"][0].plan.q
+        self.n_out = self.layers["out"][0].plan.r_dim
+        chain = [("fc1", "fc2"), ("fc2", "fc3"), ("fc4", "out")]
+        for a, b in chain:
+            if self.layers[a][0].plan.r_dim != self.layers[b][0].plan.q:
+                raise DimensionError(f"{a} -> {b} widths do not chain")
+        for g in GATES:
+            if self.layers[f"x_{g}"][0].plan.q != self.layers["fc3"][0].plan.r_dim or \
+               self.layers[f"h_{g}"][0].plan.q != self.hidden or \
+               self.layers[f"x_{g}"][0].plan.r_dim != self.hidden or \
+               self.layers[f"h_{g}"][0].plan.r_dim != self.hidden:
+                raise DimensionError(f"gate {g}: projections must map to the hidden width")
+        self.clip = float(clip)
+        self._ws = {}
+        self._graphs = {}
+
+    @classmethod
+    def random(cls, seed: int = 0, n_in: int = 494, hidden: int = 2048, n_out: int = 29,
+               fc_rank: int = 3, lstm_rank: int = 32):
+        """BASELINE config-4 geometry with seeded factors: spawn_rngs children per layer
+        [xf, wf, bias], biases N(0, 0.01). Config 4 states no factor distribution; the factors
+        are variance-preserving, stddev (r * q)^(-1/4) each, so W = reshape(xf @ wf) has
+        entries of variance 1/q and every layer's pre-activations stay O(1) (as in a trained
+        acoustic model; configs 1/2's N(0, 1/sqrt(r)) factors would give W entries of variance
+        1 and saturate every clipped ReLU and LSTM gate)."""
+        shapes = {"fc1": (n_in, hidden, fc_rank), "fc2": (hidden, hidden, fc_rank),
+                  "fc3": (hidden, hidden, fc_rank), "fc4": (hidden, hidden, fc_rank),
+                  "out": (hidden, n_out, 1)}
+        for g in GATES:
+            shapes[f"x_{g}"] = (hidden, hidden, lstm_rank)
+            shapes[f"h_{g}"] = (hidden, hidden, lstm_rank)
+        rngs = spawn_rngs(seed, 3 * len(cls.NAMES))
+        layers = {}
+        for i, name in enumerate(cls.NAMES):
+            q, r_dim, rank = shapes[name]
+            plan = compressed_plan(q, r_dim, rank)
+            sd = (rank * q) ** -0.25
+            xf = sample_normal(rngs[3 * i], 0.0, sd, (plan.m, rank)).astype(np.float32)
+            wf = sample_normal(rngs[3 * i + 1], 0.0, sd, (rank, plan.n)).astype(np.float32)
+            b = sample_normal(rngs[3 * i + 2], 0.0, 0.01, (r_dim,)).astype(np.float32)
+            layers[name] = (FactorPair(xf, wf, plan), b)
+        return cls(layers)
+
+    # ---- helpers ------------------------------------------------------------------------
+    def _wsp(self, key, plan, batch, mma):
+        lib = _lib.lib()
+        need = max(256, lib.dt_forward_workspace_bytes(C.byref(_lib.plan_struct(plan)), batch, mma))
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=device())
+            self._ws[key] = ws
+        return ws
+
+    def _dense(self, name, x, act, out_dtype=torch.bfloat16):
+        fp, b = self.layers[name]
+        y = torch.empty((x.shape[0], fp.plan.r_dim), dtype=out_dtype, device=device())
+        forward_into(x, fp, b, _act_code(act), self.clip, y, _lib.DT_MMA_BF16,
+                     ws=self._wsp(name, fp.plan, x.shape[0], _lib.DT_MMA_BF16))
+        return y
+
+    def _recurrence(self, gx, T, B, graph=True):
+        """T LSTM steps; returns the bf16 sequence output (T*B x hidden)."""
+        H = self.hidden
+        key = (T, B)
+        st = self._graphs.get(key)
+        if st is None:
+            dev = device()
+            st = {"gx": [torch.empty((T * B, H), dtype=torch.bfloat16, device=dev) for _ in GATES],
+                  "gh": [torch.empty((B, H), dtype=torch.float32, device=dev) for _ in GATES],
+                  "c": torch.zeros((B, H), dtype=torch.float32, device=dev),
+                  "h": torch.zeros((B, H), dtype=torch.float32, device=dev),
+                  "out": torch.empty((T * B, H), dtype=torch.bfloat16, device=dev),
+                  "graph": None}
+            self._graphs[key] = st
+        for g in range(4):
+            st["gx"][g].copy_(gx[g])
+        st["c"].zero_()
+        st["h"].zero_()
+        if graph and st["graph"] is None:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self._steps(st, T, B)          # warm-up: kernels loaded, workspaces sized
+            torch.cuda.current_stream().wait_stream(side)
+            st["c"].zero_()
+            st["h"].zero_()
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg):
+                self._steps(st, T, B)
+            st["graph"] = cg
+            st["c"].zero_()
+            st["h"].zero_()
+        if graph:
+            st["graph"].replay()
+        else:
+            self._steps(st, T, B)
+        return st["out"]
+
+    def _steps(self, st, T, B):
+        lib = _lib.lib()
+        H = self.hidden
+        gh_ptrs = (C.c_void_p * 4)(*[t.data_ptr() for t in st["gh"]])
+        esz = 2
+        hl = [self.layers[f"h_{g}"] for g in GATES]
+        ps = _lib.plan_struct(hl[0][0].plan)
+        need = lib.dt_lstm_gates_workspace_bytes(C.byref(ps), B)
+        fused = need > 0 and all(fp.plan == hl[0][0].plan for fp, _ in hl)
+        if fused:
+            ws = self._ws.get("gates")
+            if ws is None or ws.numel() < need:
+                ws = self._ws["gates"] = torch.empty(need, dtype=torch.uint8, device=device())
+            xf = (C.c_void_p * 4)(*[fp.xf.data_ptr() for fp, _ in hl])
+            wf = (C.c_void_p * 4)(*[fp.wf.data_ptr() for fp, _ in hl])
+            bs = (C.c_void_p * 4)(*[b.data_ptr() for _, b in hl])
+        for t in range(T):
+            if fused:   # the four recurrent contractions in two launches (P, then gates)
+                _lib.check(lib.dt_lstm_gates(C.byref(ps), B, st["h"].data_ptr(), xf, wf, bs,
+                                             gh_ptrs, ws.data_ptr(), ws.numel(), stream_handle()))
+            else:
+                for g, gate in enumerate(GATES):
+                    fp, b = hl[g]
+                    forward_into(st["h"], fp, b, 0, 0.0, st["gh"][g], _lib.DT_MMA_FFMA,
+                                 ws=self._wsp(f"h_{gate}", fp.plan, B, _lib.DT_MMA_FFMA))
+            gx_ptrs = (C.c_void_p * 4)(*[x.data_ptr() + t * B * H * esz for x in st["gx"]])
+            _lib.check(lib.dt_lstm_cell(B, H, gx_ptrs, H, gh_ptrs, st["c"].data_ptr(),
+                                        st["h"].data_ptr(),
+                                        st["out"].data_ptr() + t * B * H * esz, stream_handle()))
+
+    # ---- forward ------------------------------------------------------------------------
+    def forward(self, x, graph: bool = True):
+        """x: (T, B, n_in) CUDA tensor (bf16 or fp32), time-major. Returns fp32 logits
+        (T, B, n_out)."""
+        if not isinstance(x, torch.Tensor) or x.dim() != 3 or x.shape[2] != self.n_in:
+            raise DimensionError(f"input must be (T, B, {self.n_in}), got "
+                                 f"{tuple(x.shape) if hasattr(x, 'shape') else type(x)}")
+        T, B = int(x.shape[0]), int(x.shape[1])
+        h = x.to(device()).reshape(T * B, self.n_in).to(torch.bfloat16).contiguous()
+        for name in ("fc1", "fc2", "fc3"):
+            h = self._dense(name, h, "clipped_relu")
+        gx = [self._dense(f"x_{g}", h, "identity") for g in GATES]
+        seq = self._recurrence(gx, T, B, graph=graph)
+        h = self._dense("fc4", seq, "clipped_relu")
+        y = self._dense("out", h, "identity", out_dtype=torch.float32)
+        return y.reshape(T, B, self.n_out)
+
+    __call__ = forward
