@@ -46,12 +46,11 @@ constexpr int kNc = 128;           // output columns per D chunk (UMMA N of phas
 constexpr int kXSMax = 8;          // x ring depth cap (the launcher sizes it to the smem left)
 constexpr int kBS = 2;             // XF2 chunk ring depth (resident when a CTA has <= 2 chunks)
 constexpr int kPW = 4;             // P-exchange warps (one per TMEM lane quarter)
-constexpr int kEpi = 8;            // epilogue warps (two per TMEM lane quarter)
+constexpr int kEpi = 16;           // epilogue warps (four per TMEM lane quarter)
 constexpr int kRowsThreads = 32 * (3 + kPW + kEpi);
 constexpr uint32_t kXBytes = kTM * 128;   // 128 rows x 64 bf16
 constexpr uint32_t kBBytes = kNc * 128;   // 128 columns x 32 fp32
 constexpr uint32_t kA2Bytes = kTM * 128;  // 128 rows x 32 fp32 (k2 <= 32)
-constexpr uint32_t kOutBox = 32 * 128;    // one warp's 32 rows x 128 B staging box
 constexpr uint32_t kDCol = 256;           // TMEM column of the first D buffer (P below it)
 // A2 descriptor strides (see a2n_off)
 constexpr uint32_t kA2Lbo = 2048, kA2Sbo = 128;
@@ -62,6 +61,7 @@ struct RowsParams {
   const float *bias;
   void *y;
   float arg;
+  int bslot;  // K slot carrying the bias (P = 1 there, XF2p = bias * scale), -1: epilogue adds it
   uint32_t off_x, off_a2, off_wf, off_b, off_out, off_bar;
   unsigned long long *trace;  // DEEPTHIN_ROWS_TRACE: globaltimer stamps of cluster 0
 };
@@ -85,7 +85,8 @@ __device__ __forceinline__ float tanh_approx(float x) {
 // act_fast (ex2 + rcp, ~1e-7).
 template <int YDT, int ACT>
 __device__ __forceinline__ float act_out(float z, float arg) {
-  if constexpr (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f);
+  // the launcher pre-scales XF2p and the bias by 1/2 for this case: z here is already z/2
+  if constexpr (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_approx(z), 0.5f);
   if constexpr (YDT == DT_BF16 && ACT == DT_ACT_TANH) return tanh_approx(z);
   return act_fast<ACT>(z, arg);
 }
@@ -305,7 +306,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const uint32_t a2_local = smem_u32(smem) + p.off_a2;
     for (int b = 0; b < 2; ++b)  // K padding of the tf32 operand (never overwritten)
       for (int kk = p.s * p.rp; kk < p.k2; kk += 4)
-        st_shared_v4(a2_local + (uint32_t)b * kA2Bytes + a2n_off(row, kk), 0u, 0u, 0u, 0u);
+        st_shared_v4(a2_local + (uint32_t)b * kA2Bytes + a2n_off(row, kk),
+                     kk == p.bslot ? 0x3f800000u : 0u, 0u, 0u, 0u);
     uint32_t it = 0;
     for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
       const int ab = (int)(it & 1);
@@ -328,7 +330,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             if (g + k0 < p.rp) {
               uint32_t w[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) w[i] = (g + k0 + i < p.rank) ? v[k0 + i] : 0u;
+              for (int i = 0; i < 4; ++i)
+                w[i] = (g + k0 + i < p.rank) ? v[k0 + i]
+                       : (seg == 0 && g + k0 + i == p.bslot) ? 0x3f800000u : 0u;  // 1.0f
               st_shared_v4(a2b + a2n_off(row, seg * p.rp + g + k0), w[0], w[1], w[2], w[3]);
             }
           }
@@ -360,14 +364,18 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
+    // 16 warps: four per TMEM lane quarter, each owning 32 of the chunk's 128 columns
     const int sp = warp & 3;           // TMEM lane quarter this warp may access
-    const int e = warp - 3 - kPW;      // 0..7
-    const int half = e / 4;            // which 64 columns of each 128-column chunk
+    const int e = warp - 3 - kPW;      // 0..15
+    const int qc = e / 4;              // which 32 columns of each 128-column chunk
     const uint32_t s0 = smem_u32(smem);
     const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
     constexpr int E = YDT == DT_BF16 ? 2 : 4;
-    constexpr int UC = 128 / E;        // output columns per 128-byte store box
-    const uint32_t out_s = s0 + p.off_out + (uint32_t)e * kOutBox;
+    constexpr int RB = 32 * E;         // bytes per row of this warp's 32 columns (64 or 128)
+    constexpr int LPR = RB / 16;       // lanes per row when storing (4 or 8)
+    constexpr int RPI = 32 / LPR;      // rows per store instruction (8 or 4)
+    constexpr int SWM = RB / 16 - 1;   // swizzle mask over the row's 16-byte chunks
+    const uint32_t out_s = s0 + p.off_out + (uint32_t)e * (32u * RB);
     int db = 0;
     uint32_t dph = 0, it = 0;
     for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
@@ -376,82 +384,63 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         mbar_wait(&d_full[db], dph);
         if (warp == 3 + kPW && c == crank) rtrace(p, 3 + 4 * (int)min(it, 7u));
         tc_fence_after();
-        const int tsl = 44 + 8 * (int)(it * 2 + (c - crank) / cs) ;
-        const bool tre = warp == 3 + kPW && lane == 0 && it < 1;
-        {
-          const int h = half;
-          if (tre) rtrace(p, tsl + 4 * h);
-          const int col0 = c * kNc + 64 * h;
-          uint32_t v[64];
-          tmem_ld_32x32b_x32(tbase + lane_t + kDCol + (uint32_t)(db * kNc + 64 * h),
-                             *reinterpret_cast<uint32_t(*)[32]>(v));
-          tmem_ld_32x32b_x32(tbase + lane_t + kDCol + (uint32_t)(db * kNc + 64 * h + 32),
-                             *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[db]);
-          if (tre) rtrace(p, tsl + 4 * h + 1);
-          if (col0 < p.r_dim) {
-          // bias + activation in fp32
-          // bias: one coalesced load per 32 columns, broadcast by shuffles (per-element
-          // broadcast loads serialise on their latency)
-          float blo = 0.f, bhi = 0.f;
-          if (p.bias) {
-            if (col0 + lane < p.r_dim) blo = __ldg(p.bias + col0 + lane);
-            if (col0 + 32 + lane < p.r_dim) bhi = __ldg(p.bias + col0 + 32 + lane);
-          }
-          float o[64];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]) + __shfl_sync(0xffffffffu, blo, i), p.arg);
-            o[i + 32] = act_out<YDT, ACT>(__uint_as_float(v[i + 32]) + __shfl_sync(0xffffffffu, bhi, i), p.arg);
-          }
-          if (tre) rtrace(p, tsl + 4 * h + 2);
-          // 64 columns = 64*E bytes per row = (E/2) boxes of 32 rows x 128 B: pack into the
-          // warp's swizzled staging box (conflict-free), read it back 4 rows per instruction
-          // (8 lanes per 128-byte row) and store full lines with st.global.v4
-#pragma unroll
-          for (int u = 0; u < E / 2; ++u) {
-            if (col0 + u * UC >= p.r_dim) break;
-            const uint32_t rb = out_s + (uint32_t)lane * 128u;
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-              uint32_t w0, w1, w2, w3;
-              if constexpr (E == 2) {
-                const float *f = o + ch * 8;
-                w0 = pack_bf16(f[0], f[1]); w1 = pack_bf16(f[2], f[3]);
-                w2 = pack_bf16(f[4], f[5]); w3 = pack_bf16(f[6], f[7]);
-              } else {
-                const float *f = o + u * 32 + ch * 4;
-                w0 = __float_as_uint(f[0]); w1 = __float_as_uint(f[1]);
-                w2 = __float_as_uint(f[2]); w3 = __float_as_uint(f[3]);
-              }
-              st_shared_v4(rb + ((uint32_t)(ch ^ (lane & 7)) << 4), w0, w1, w2, w3);
-            }
-            __syncwarp();
-            const int ch = lane & 7;
-            const int cb = col0 + u * UC + ch * (16 / E);  // first column of this lane's 16 B
-            uint32_t w[8][4];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = 4 * i + (lane >> 3);
-              ld_shared_v4(out_s + (uint32_t)r * 128u + ((uint32_t)(ch ^ (r & 7)) << 4), w[i][0],
-                           w[i][1], w[i][2], w[i][3]);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = 4 * i + (lane >> 3);
-              if (row0 + r < p.batch && cb < p.r_dim)
-                st_global_v4(reinterpret_cast<uint8_t *>(p.y) + ((row0 + r) * p.r_dim + cb) * E, w[i][0],
-                             w[i][1], w[i][2], w[i][3]);
-            }
-            __syncwarp();
-          }
-          }
-          if (tre) rtrace(p, tsl + 4 * h + 3);
-        }
+        const int col0 = c * kNc + 32 * qc;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_t + kDCol + (uint32_t)(db * kNc + 32 * qc), v);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[db]);
         if (++db == 2) { db = 0; dph ^= 1; }
+        if (col0 >= p.r_dim) continue;
+        float o[32];
+        if (p.bias && p.bslot < 0) {
+          constexpr float bsc = (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) ? 0.5f : 1.f;
+          const float bl = col0 + lane < p.r_dim ? bsc * __ldg(p.bias + col0 + lane) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]) + __shfl_sync(0xffffffffu, bl, i), p.arg);
+        } else {  // bias folded into the tf32 contraction (or absent)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]), p.arg);
+        }
+        // this lane's row (RB bytes) into the warp's swizzled staging box, then read back
+        // RPI rows per instruction (LPR lanes per row) and store whole rows with st.global.v4
+        const uint32_t rb = out_s + (uint32_t)lane * RB;
+#pragma unroll
+        for (int ch = 0; ch < RB / 16; ++ch) {
+          uint32_t w0, w1, w2, w3;
+          if constexpr (E == 2) {
+            const float *f = o + ch * 8;
+            w0 = pack_bf16(f[0], f[1]); w1 = pack_bf16(f[2], f[3]);
+            w2 = pack_bf16(f[4], f[5]); w3 = pack_bf16(f[6], f[7]);
+          } else {
+            const float *f = o + ch * 4;
+            w0 = __float_as_uint(f[0]); w1 = __float_as_uint(f[1]);
+            w2 = __float_as_uint(f[2]); w3 = __float_as_uint(f[3]);
+          }
+          const int sw = E == 2 ? ((lane >> 1) & SWM) : (lane & SWM);
+          st_shared_v4(rb + ((uint32_t)(ch ^ sw) << 4), w0, w1, w2, w3);
+        }
+        __syncwarp();
+        const int ch = lane % LPR;
+        const int cb = col0 + ch * (16 / E);  // first column of this lane's 16 bytes
+        uint32_t w[RPI == 8 ? 4 : 8][4];
+#pragma unroll
+        for (int i = 0; i < 32 / RPI; ++i) {
+          const int r = RPI * i + lane / LPR;
+          const int sw = E == 2 ? ((r >> 1) & SWM) : (r & SWM);
+          ld_shared_v4(out_s + (uint32_t)r * RB + ((uint32_t)(ch ^ sw) << 4), w[i][0], w[i][1],
+                       w[i][2], w[i][3]);
+        }
+#pragma unroll
+        for (int i = 0; i < 32 / RPI; ++i) {
+          const int r = RPI * i + lane / LPR;
+          if (row0 + r < p.batch && cb < p.r_dim)
+            st_global_v4(reinterpret_cast<uint8_t *>(p.y) + ((row0 + r) * p.r_dim + cb) * E, w[i][0],
+                         w[i][1], w[i][2], w[i][3]);
+        }
+        __syncwarp();
       }
     }
     if (warp == 3 + kPW) rtrace(p, 40);
@@ -526,7 +515,8 @@ namespace {
 // kernel.py:157-164): wf -> bf16, and XF2 re-laid with each segment's rank values padded to rp
 // (zeros), K padded to k2: XF2p[j, seg*rp + k] = xf[j*s + seg, k].
 __global__ void k_rows_prep(int64_t wf_count, const float *wf, __nv_bfloat16 *wf16, int r_dim, int s,
-                            int rank, int rp, int k2, const float *xf, float *xf2p) {
+                            int rank, int rp, int k2, const float *xf, float *xf2p, const float *bias,
+                            int bslot, float scale) {
   griddep_wait();
   griddep_launch_dependents();
   const int64_t tot = wf_count + (int64_t)r_dim * k2;
@@ -538,7 +528,9 @@ __global__ void k_rows_prep(int64_t wf_count, const float *wf, __nv_bfloat16 *wf
       const int64_t e = i - wf_count;
       const int64_t j = e / k2;
       const int kk = (int)(e - j * k2), seg = kk / rp, k = kk - seg * rp;
-      xf2p[e] = (seg < s && k < rank) ? xf[(j * s + seg) * rank + k] : 0.f;
+      float v = (seg < s && k < rank) ? xf[(j * s + seg) * rank + k] : 0.f;
+      if (kk == bslot) v = bias ? bias[j] : 0.f;
+      xf2p[e] = v * scale;
     }
   }
 }
@@ -568,6 +560,10 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.bias = bias;
   p.y = y;
   p.arg = act_arg;
+  // a zero K slot for the bias: the rank padding of segment 0, else an all-zero pad chunk
+  p.bslot = !bias ? -1 : (g.rank < p.rp ? (int)g.rank : (p.k2 > g.s * p.rp ? (int)(g.s * p.rp) : -1));
+  // bf16 sigmoid runs as 1/2 + tanh(z/2)/2: the contraction (and bias) pre-scaled by 1/2
+  const float scale = (y_dtype == DT_BF16 && act == DT_ACT_SIGMOID) ? 0.5f : 1.f;
   // shared memory: x ring | A2 x 2 | wf | XF2 ring | output staging | barriers
   p.pcols = (int)((g.s / p.cs) * p.np);
   // shared memory: A2 x 2 | wf | XF2 ring | output staging | x ring (what is left) | barriers
@@ -576,7 +572,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.off_wf = 2 * kA2Bytes;
   p.off_b = (p.off_wf + wf_bytes + 1023) & ~1023u;
   p.off_out = p.off_b + kBS * kBBytes;
-  p.off_x = p.off_out + kEpi * kOutBox;
+  p.off_x = p.off_out + kEpi * 32u * 32u * (uint32_t)(y_dtype == DT_BF16 ? 2 : 4);
   constexpr uint32_t kSmemMax = 227 * 1024, kTail = 512 + 1024;
   p.xs = (int)std::min<uint32_t>(kXSMax, (kSmemMax - kTail - p.off_x) / kXBytes);
   p.off_bar = p.off_x + (uint32_t)p.xs * kXBytes;
@@ -596,7 +592,8 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
     pc.attrs = pa;
     pc.numAttrs = 1;
     DT_CUDA_CHECK(cudaLaunchKernelEx(&pc, k_rows_prep, (int64_t)(g.rank * g.n), wf, wf16,
-                                     (int)g.r_dim, (int)g.s, (int)g.rank, p.rp, p.k2, xf, xf2p));
+                                     (int)g.r_dim, (int)g.s, (int)g.rank, p.rp, p.k2, xf, xf2p, bias,
+                                     p.bslot, scale));
     if (int rc = check_launch("rows_prep")) return rc;
   }
 

@@ -240,3 +240,42 @@ def test_bf16_rounding_is_rne():
     assert got[3] == -2.5
     assert abs(got[4] - 1e-3) <= 1e-3 * 2 ** -8
     assert math.isclose(O.round_bf16(np.array([3.0]))[0], 3.0)
+
+
+def test_oracle_lstm_cell_known_answer():
+    """oracle.lstm_cell (config 4, unpinned by the reference): gate order i, f, g, o; with all
+    pre-activations 0: i = f = o = 1/2, g = 0 -> c' = c/2, h' = tanh(c/2)/2."""
+    z = [np.zeros((2, 3))] * 4
+    c = np.array([[1.0, -2.0, 0.5], [0.0, 4.0, -1.0]])
+    h, cn = O.lstm_cell(z, z, c)
+    assert np.allclose(cn, c / 2) and np.allclose(h, np.tanh(c / 2) / 2)
+    # saturated gates: i = o = 1, f = 0, g = tanh(large) = 1 -> c' = 1, h' = tanh(1)
+    big = [np.full((1, 1), 50.0), np.full((1, 1), -50.0), np.full((1, 1), 50.0), np.full((1, 1), 50.0)]
+    h, cn = O.lstm_cell(big, [np.zeros((1, 1))] * 4, np.full((1, 1), 7.0))
+    assert np.allclose(cn, 1.0) and np.allclose(h, np.tanh(1.0))
+
+
+def test_oracle_speech_forward_is_layer_forward_chain():
+    """speech_forward with T = 1 and zero initial state equals the explicit chain of
+    layer_forward calls (kernel.py:296-320) and one cell step."""
+    rng = np.random.default_rng(0)
+    def lay(q, r_dim, rank, n):
+        m = -(-(q * r_dim) // n)
+        p = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+        return (rng.normal(0, 0.5, (m, rank)), rng.normal(0, 0.5, (rank, n)), p, rng.normal(0, 0.1, r_dim))
+    layers = {"fc1": lay(6, 8, 2, 3), "fc2": lay(8, 8, 1, 4), "fc3": lay(8, 8, 1, 4),
+              "fc4": lay(8, 8, 1, 4), "out": lay(8, 5, 1, 4)}
+    for g in "ifgo":
+        layers[f"x_{g}"] = lay(8, 8, 2, 4)
+        layers[f"h_{g}"] = lay(8, 8, 2, 4)
+    x = rng.standard_normal((1, 3, 6))
+    y = O.speech_forward(x, layers, clip=1.5)
+    lf = lambda name, h: O.layer_forward(h, *layers[name])
+    h = x[0]
+    for name in ("fc1", "fc2", "fc3"):
+        h = O.apply_activation("clipped_relu", lf(name, h), 1.5)
+    gx = [lf(f"x_{g}", h) for g in "ifgo"]
+    gh = [lf(f"h_{g}", np.zeros((3, 8))) for g in "ifgo"]
+    hs, _ = O.lstm_cell(gx, gh, np.zeros((3, 8)))
+    want = lf("out", O.apply_activation("clipped_relu", lf("fc4", hs), 1.5))
+    assert np.allclose(y[0], want, rtol=0, atol=1e-12)
