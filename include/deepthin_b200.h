@@ -59,7 +59,8 @@ enum dt_status {
 
 /* DT_FACTORS_PACKED is valid only as dt_forward's f_dtype: xf points at the buffer
  * dt_pack_factors filled (wf is ignored). */
-enum dt_dtype { DT_F32 = 0, DT_BF16 = 1, DT_FACTORS_PACKED = 2, DT_F64 = 3 /* dt_unpack_values */ };
+enum dt_dtype { DT_F32 = 0, DT_BF16 = 1, DT_FACTORS_PACKED = 2, DT_F64 = 3 /* dt_unpack_values */,
+               DT_FACTORS_ROWS = 4 /* dt_rows_prepare output, dt_forward f_dtype */ };
 
 /* Arithmetic of the contraction.
  *  DT_MMA_FFMA: fp32 CUDA-core FFMA, fp32 operands (parity rtol 1e-5).
@@ -179,6 +180,15 @@ int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtyp
 
 /* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);
+/* Row-tile reuse kernel operands derived once per factor pair (the analogue of the reference's
+ * per-pair derived-weight cache, kernel.py:157-164): bf16 wf and the K-padded XF2 with the bias
+ * and the bf16-sigmoid pre-scale folded in. dt_rows_prepared_bytes returns 0 when the geometry
+ * (n_f | q, n_f % 64 == 0, s * round_up(rank, 4) <= 32) or the dtypes do not take that kernel.
+ * Pass the buffer to dt_forward as xf with f_dtype = DT_FACTORS_ROWS (wf ignored) and the SAME
+ * act, y_dtype and bias as here; rebuild it after the factors or the bias change. */
+size_t dt_rows_prepared_bytes(const dt_plan *plan, int x_dtype, int y_dtype);
+int dt_rows_prepare(const dt_plan *plan, int act, int y_dtype, const float *xf, const float *wf,
+                    const float *bias, void *out, dt_stream stream);
 /* The four recurrent gate contractions of one LSTM step (BASELINE config 4): gh[g] = h @ W_g +
  * bias[g] for four DeepThin layers sharing one square reuse geometry (plan: q == r_dim, n | q),
  * h fp32 (batch x q), exact fp32 on the CUDA cores in the reference's factored reuse form

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
 
 DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA, DT_E_FORMAT = range(6)
-DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64 = 0, 1, 2, 3
+DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64, DT_FACTORS_ROWS = 0, 1, 2, 3, 4
 DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
 DT_PROF_ANY, DT_PROF_GEMM, DT_PROF_ROWS = 0, 1, 2
 ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
@@ -26,7 +26,7 @@ EXPORTS = (
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
-    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_sgd_step", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_cell", "dt_session_create",
+    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_sgd_step", "dt_rows_prepared_bytes", "dt_rows_prepare", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_cell", "dt_session_create",
     "dt_session_forward", "dt_session_destroy", "dt_model_parse", "dt_unpack_values",
 )
 
@@ -105,6 +105,8 @@ def _declare(lib):
         "dt_mse_workspace_bytes": ([I64, I64], SZ),
         "dt_mse_grad": ([I64, I64, VP, VP, D, VP, VP, VP, SZ, VP], i),
         "dt_sgd_step": ([I64, VP, VP, F, VP], i),
+        "dt_rows_prepared_bytes": ([P, i, i], SZ),
+        "dt_rows_prepare": ([P, i, i, VP, VP, VP, VP, VP], i),
         "dt_lstm_gates_workspace_bytes": ([P, I64], SZ),
         "dt_lstm_gates": ([P, I64, VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP), C.POINTER(VP), VP, SZ, VP], i),
         "dt_lstm_cell": ([I64, I64, C.POINTER(VP), I64, C.POINTER(VP), VP, VP, VP, VP], i),

@@ -268,10 +268,10 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
   }
   if (int rc = check_dtype(x_dtype, "x")) return rc;
   if (int rc = check_dtype(y_dtype, "y")) return rc;
-  if (f_dtype != DT_FACTORS_PACKED)
+  if (f_dtype != DT_FACTORS_PACKED && f_dtype != DT_FACTORS_ROWS)
     if (int rc = check_dtype(f_dtype, "factors")) return rc;
   if (int rc = check_act(act)) return rc;
-  if (batch > 0 && (!x || !xf || (!wf && f_dtype != DT_FACTORS_PACKED) || !y)) {
+  if (batch > 0 && (!x || !xf || (!wf && f_dtype != DT_FACTORS_PACKED && f_dtype != DT_FACTORS_ROWS) || !y)) {
     set_error("NULL operand pointer");
     return DT_E_ARG;
   }
@@ -289,6 +289,27 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
                           act_arg, y, y_dtype, (char *)workspace, workspace_bytes, st);
     if (ea && rc == DT_OK) DT_CUDA_CHECK(cudaEventRecord(ea, st));
     return rc;
+  }
+  if (mma == DT_MMA_BF16 && f_dtype == DT_FACTORS_ROWS) {
+    // operands prepared once per factor pair by dt_rows_prepare: the row-tile kernel alone
+    if (!tc_rows_ok(g, x_dtype, y_dtype) ||
+        ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+          reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(xf)) & 15) != 0) {
+      set_error("DT_FACTORS_ROWS: geometry/operands not eligible for the row-tile kernel "
+                "(dt_rows_prepared_bytes == 0) or misaligned pointers");
+      return DT_E_UNSUPPORTED;
+    }
+    if (batch == 0) return DT_OK;
+    const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
+    if (int rc = tc_rows_forward(g, batch, x, nullptr, nullptr, bias, eact, act_arg, y, y_dtype,
+                                 (char *)const_cast<void *>(xf), (cudaStream_t)stream, true))
+      return rc;
+    return act == DT_ACT_SOFTMAX ? launch_row_softmax(batch, g.r_dim, y, y_dtype, (cudaStream_t)stream)
+                                 : DT_OK;
+  }
+  if (f_dtype == DT_FACTORS_ROWS) {
+    set_error("DT_FACTORS_ROWS operands are for the bf16 tensor-core path");
+    return DT_E_ARG;
   }
   if (mma == DT_MMA_BF16) {
     // DT_FACTORS_PACKED: the fused single-kernel path (in-kernel W regeneration, general
@@ -409,6 +430,30 @@ int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_str
     return DT_E_ARG;
   }
   return launch_sgd(count, param, grad, lr, (cudaStream_t)stream);
+}
+
+size_t dt_rows_prepared_bytes(const dt_plan *plan, int x_dtype, int y_dtype) {
+  Geo g;
+  if (make_geo(plan, &g) || !tc_rows_ok(g, x_dtype, y_dtype)) return 0;
+  return tc_rows_ws(g);
+}
+
+int dt_rows_prepare(const dt_plan *plan, int act, int y_dtype, const float *xf, const float *wf,
+                    const float *bias, void *out, dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (int rc = check_act(act)) return rc;
+  if (int rc = check_dtype(y_dtype, "y")) return rc;
+  if (!tc_rows_ok(g, DT_BF16, y_dtype)) {
+    set_error("dt_rows_prepare: geometry not eligible for the row-tile kernel");
+    return DT_E_UNSUPPORTED;
+  }
+  if (!xf || !wf || !out || (reinterpret_cast<uintptr_t>(out) & 255)) {
+    set_error("dt_rows_prepare: NULL operand or output not 256-byte aligned");
+    return DT_E_ARG;
+  }
+  const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
+  return tc_rows_prepare(g, wf, xf, bias, eact, y_dtype, (char *)out, (cudaStream_t)stream);
 }
 
 size_t dt_lstm_gates_workspace_bytes(const dt_plan *plan, int64_t batch) {

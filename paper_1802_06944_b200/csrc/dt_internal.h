@@ -82,9 +82,12 @@ int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner,
 // Softmax is not fused (caller post-pass).
 bool tc_rows_ok(const Geo &g, int x_dtype, int y_dtype);
 size_t tc_rows_ws(const Geo &g);
+// prepared: ws already holds the operands tc_rows_prepare derived (same bias / act / y_dtype)
 int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
                     const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
-                    cudaStream_t st);
+                    cudaStream_t st, bool prepared = false);
+int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float *bias, int act,
+                    int y_dtype, char *ws, cudaStream_t st);
 
 // ---- two-phase tensor-core path: k_tc_gemm.cu ---------------------------------------
 // W^T (r_dim x round_up(q, 8), bf16) regenerated from the factors (f_dtype DT_F32 or DT_BF16)

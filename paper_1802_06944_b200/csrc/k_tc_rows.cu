@@ -536,9 +536,31 @@ __global__ void k_rows_prep(int64_t wf_count, const float *wf, __nv_bfloat16 *wf
 }
 }  // namespace
 
+int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float *bias, int act,
+                    int y_dtype, char *ws, cudaStream_t st) {
+  const int rp = (int)((g.rank + 3) / 4 * 4), k2 = (int)rows_k2(g);
+  const int bslot = !bias ? -1 : (g.rank < rp ? (int)g.rank : (k2 > g.s * rp ? (int)(g.s * rp) : -1));
+  const float scale = (y_dtype == DT_BF16 && act == DT_ACT_SIGMOID) ? 0.5f : 1.f;
+  __nv_bfloat16 *wf16 = reinterpret_cast<__nv_bfloat16 *>(ws);
+  float *xf2p = reinterpret_cast<float *>(ws + (g.rank * g.n * 2 + 255) / 256 * 256);
+  const int64_t tot = g.rank * g.n + g.r_dim * (int64_t)k2;
+  cudaLaunchConfig_t pc{};
+  pc.gridDim = dim3((unsigned)std::min<int64_t>((tot + 255) / 256, 4 * g_nsm()));
+  pc.blockDim = dim3(256);
+  pc.stream = st;
+  cudaLaunchAttribute pa[1];
+  pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pa[0].val.programmaticStreamSerializationAllowed = 1;
+  pc.attrs = pa;
+  pc.numAttrs = 1;
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&pc, k_rows_prep, (int64_t)(g.rank * g.n), wf, wf16, (int)g.r_dim,
+                                   (int)g.s, (int)g.rank, rp, k2, xf, xf2p, bias, bslot, scale));
+  return check_launch("rows_prep");
+}
+
 int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
                     const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool prepared) {
   if (batch == 0) return DT_OK;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15) ||
       (reinterpret_cast<uintptr_t>(ws) & 255)) {
@@ -580,22 +602,9 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
 
   __nv_bfloat16 *wf16 = reinterpret_cast<__nv_bfloat16 *>(ws);
   float *xf2p = reinterpret_cast<float *>(ws + (g.rank * g.n * 2 + 255) / 256 * 256);
-  {
-    const int64_t tot = g.rank * g.n + g.r_dim * (int64_t)p.k2;
-    cudaLaunchConfig_t pc{};
-    pc.gridDim = dim3((unsigned)std::min<int64_t>((tot + 255) / 256, 4 * g_nsm()));
-    pc.blockDim = dim3(256);
-    pc.stream = st;
-    cudaLaunchAttribute pa[1];
-    pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pa[0].val.programmaticStreamSerializationAllowed = 1;
-    pc.attrs = pa;
-    pc.numAttrs = 1;
-    DT_CUDA_CHECK(cudaLaunchKernelEx(&pc, k_rows_prep, (int64_t)(g.rank * g.n), wf, wf16,
-                                     (int)g.r_dim, (int)g.s, (int)g.rank, p.rp, p.k2, xf, xf2p, bias,
-                                     p.bslot, scale));
-    if (int rc = check_launch("rows_prep")) return rc;
-  }
+  // operands derived once per factor pair (dt_rows_prepare) or here, per call
+  if (!prepared)
+    if (int rc = tc_rows_prepare(g, wf, xf, bias, act, y_dtype, ws, st)) return rc;
 
   CUtensorMap tm_x, tm_wf, tm_xf2, tm_y;
   if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(x), (uint64_t)g.q,

@@ -103,6 +103,26 @@ class FactorPair:
             self._cache["packed"] = buf
         return self._cache["packed"]
 
+    def rows_prepared(self, bias, act: int, y_dtype: int):
+        """Row-tile reuse kernel operands (dt_rows_prepare: bf16 wf, K-padded XF2 with the bias
+        and the activation pre-scale folded in), derived once per (pair, bias, activation,
+        output dtype) like the reference's per-pair derived weights (kernel.py:157-164).
+        None when the geometry does not take that kernel."""
+        key = ("rows", act, y_dtype, bias.data_ptr() if bias is not None else 0)
+        if key not in self._cache:
+            lib = _lib.lib()
+            ps = _lib.plan_struct(self.plan)
+            nbytes = lib.dt_rows_prepared_bytes(C.byref(ps), _lib.DT_BF16, y_dtype)
+            buf = None
+            if nbytes:
+                buf = torch.empty(nbytes, dtype=torch.uint8, device=self.xf.device)
+                _lib.check(lib.dt_rows_prepare(C.byref(ps), act, y_dtype, self.xf.data_ptr(),
+                                               self.wf.data_ptr(),
+                                               bias.data_ptr() if bias is not None else None,
+                                               buf.data_ptr(), stream_handle()))
+            self._cache[key] = (buf, bias)
+        return self._cache[key][0]
+
     def refresh_derived(self) -> None:
         """Re-derive the cached bf16 / packed copies after the fp32 masters changed (SGD)."""
         lib = _lib.lib()
@@ -110,6 +130,13 @@ class FactorPair:
             for src, dst in zip((self.xf, self.wf), self._cache["bf16"]):
                 _lib.check(lib.dt_cast_bf16(src.numel(), src.data_ptr(), dst.data_ptr(),
                                             stream_handle()))
+        for key in [k for k in self._cache if isinstance(k, tuple) and k[0] == "rows"]:
+            buf, bias = self._cache[key]
+            if buf is not None:
+                _lib.check(lib.dt_rows_prepare(
+                    C.byref(_lib.plan_struct(self.plan)), key[1], key[2], self.xf.data_ptr(),
+                    self.wf.data_ptr(), bias.data_ptr() if bias is not None else None,
+                    buf.data_ptr(), stream_handle()))
         if self._cache.get("packed") is not None:
             xf16, wf16 = self._cache["bf16"]
             _lib.check(lib.dt_pack_factors(C.byref(_lib.plan_struct(self.plan)), _lib.DT_MMA_BF16,

@@ -129,7 +129,8 @@ class forward_pipeline:
 
 
 def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float, y: torch.Tensor,
-                 mma: int, fused: bool = False, ws: torch.Tensor | None = None) -> None:
+                 mma: int, fused: bool = False, ws: torch.Tensor | None = None,
+                 cached: bool = False) -> None:
     """Raw stream-ordered dt_forward on device tensors (no validation beyond the ABI's).
 
     bf16 tensor-core path: by default the two-phase kernels (W^T regenerated from the fp32

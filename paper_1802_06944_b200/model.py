@@ -115,7 +115,7 @@ class DeviceModel:
                 y = torch.empty((batch, fp.plan.r_dim), device=xt.device,
                                 dtype=out_dtype if i == last else mid)
                 forward_into(xt, fp, bias, self.codes[i], self.act_args[i], y, code,
-                             ws=self._ws[i])
+                             ws=self._ws[i], cached=True)
                 xt = y
         return xt.float().cpu().numpy() if host else xt
 

@@ -119,7 +119,7 @@ class SpeechRNN:
         fp, b = self.layers[name]
         y = torch.empty((x.shape[0], fp.plan.r_dim), dtype=out_dtype, device=device())
         forward_into(x, fp, b, _act_code(act), self.clip, y, _lib.DT_MMA_BF16,
-                     ws=self._wsp(name, fp.plan, x.shape[0], _lib.DT_MMA_BF16))
+                     ws=self._wsp(name, fp.plan, x.shape[0], _lib.DT_MMA_BF16), cached=True)
         return y
 
     def _recurrence(self, gx, T, B, graph=True):

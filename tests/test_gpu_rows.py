@@ -77,3 +77,26 @@ def test_rows_large_batch_persistent_tiles():
     assert O.rel_error(pre, bf16_factored_emulated(d, plan, d["bias"])) <= 1e-3
     y = D.layer_forward(x, fp, d["bias"], "tanh", mma="bf16")
     assert np.max(np.abs(y.double().cpu().numpy() - np.tanh(pre.double().cpu().numpy()))) <= 1e-6
+
+
+@pytest.mark.parametrize("act,out", [("sigmoid", torch.bfloat16), ("identity", torch.float32),
+                                     ("tanh", torch.bfloat16)])
+def test_rows_prepared_operands_equal_per_call(act, out):
+    """dt_rows_prepare + dt_forward(DT_FACTORS_ROWS) (operands derived once per pair) gives the
+    per-call path's bits; refresh_derived picks up changed factors."""
+    from paper_1802_06944_b200 import _lib
+    from paper_1802_06944_b200.kernel import _act_code, forward_into
+    plan, d, fp = make_case(2048, 2048, 3, 256, 16384, 300, seed=8, rnd=O.round_bf16)
+    x = gpu_x(d["x"], torch.bfloat16)
+    b = torch.tensor(d["bias"], dtype=torch.float32, device="cuda")
+    y0 = torch.empty((300, 2048), dtype=out, device="cuda")
+    y1 = torch.empty_like(y0)
+    forward_into(x, fp, b, _act_code(act), 20.0, y0, _lib.DT_MMA_BF16)
+    forward_into(x, fp, b, _act_code(act), 20.0, y1, _lib.DT_MMA_BF16, cached=True)
+    assert fp.rows_prepared(b, _act_code(act), _lib.DT_BF16 if out == torch.bfloat16 else _lib.DT_F32) is not None
+    assert torch.equal(y0, y1)
+    fp.xf.mul_(0.5)
+    fp.refresh_derived()
+    forward_into(x, fp, b, _act_code(act), 20.0, y0, _lib.DT_MMA_BF16)
+    forward_into(x, fp, b, _act_code(act), 20.0, y1, _lib.DT_MMA_BF16, cached=True)
+    assert torch.equal(y0, y1)
