@@ -103,6 +103,8 @@ int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, cons
                    float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st);
 size_t tc_forward_mse_ws(const Geo &g, int64_t batch);
 int launch_sum_f64(int64_t count, const double *part, double *out, cudaStream_t st);
+// fixed-order fp64 sum of (g * inv)^2 (part: mse_ws(1, count) bytes), out nullable
+int launch_sumsq(int64_t count, const float *g, double inv, double *part, double *out, cudaStream_t st);
 // Tensor-core backward of reuse geometries in factored form (cuBLASLt for the plain GEMMs over
 // transposed views); returns DT_E_UNSUPPORTED when the geometry does not qualify.
 bool tc_backward_ok(const Geo &g);

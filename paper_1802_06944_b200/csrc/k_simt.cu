@@ -405,6 +405,31 @@ __global__ void __launch_bounds__(256) k_mse(int64_t count, const float *y, cons
 }
 
 // fixed-order sum of `count` fp64 partials (one block)
+// fixed-order fp64 partial sums of (g * inv)^2 (the MSE loss recovered from its gradient)
+__global__ void __launch_bounds__(256) k_sumsq(int64_t count, const float *g, double inv, double *part) {
+  __shared__ double red[256];
+  double sq = 0.0;
+  const int64_t n4 = count / 4, stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+  if (vec)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 a = reinterpret_cast<const float4 *>(g)[i];
+      const double d0 = a.x * inv, d1 = a.y * inv, d2 = a.z * inv, d3 = a.w * inv;
+      sq += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+    }
+  for (int64_t i = (vec ? 4 * n4 : 0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    const double d = g[i] * inv;
+    sq += d * d;
+  }
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
 __global__ void __launch_bounds__(256) k_sum_f64(int64_t count, const double *part, double *out) {
   __shared__ double red[256];
   double s = 0.0;
@@ -856,6 +881,15 @@ int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, 
     return check_launch("mse_sum");
   }
   return DT_OK;
+}
+
+int launch_sumsq(int64_t count, const float *g, double inv, double *part, double *out, cudaStream_t st) {
+  const unsigned nb = mse_blocks(count);
+  k_sumsq<<<nb, 256, 0, st>>>(count, g, inv, part);
+  if (int rc = check_launch("sumsq")) return rc;
+  if (!out) return DT_OK;
+  k_sum_f64<<<1, 256, 0, st>>>(nb, part, out);
+  return check_launch("sumsq_sum");
 }
 
 int launch_sum_f64(int64_t count, const double *part, double *out, cudaStream_t st) {

@@ -1483,6 +1483,23 @@ static int64_t mse_parts_bound(const Geo &g, int64_t batch) {
   return ((g.r_dim + GM - 1) / GM + 2) * ((batch + GN - 1) / GN) * kEpiWarps;
 }
 
+namespace {
+int lt_gemm_ep(cudaStream_t st, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+               const float *B, int64_t ldb, const float *C, float *D, int64_t ldd, float alpha,
+               float beta, const float *bias, void *ws, size_t ws_bytes);
+__global__ void k_scale_vec(int64_t n, const float *a, float s, float *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a ? s * a[i] : 0.f;
+}
+constexpr size_t kLtWsFwd = 32u << 20;
+// the MSE through cuBLASLt's epilogue (C = target) once the tf32 GEMM is large enough that the
+// stream-scheduled single-CTA tf32 kernel is L2-operand-bound (config 5: K = s*rank = 512)
+bool mse_lt_ok(const Geo &g, int64_t batch) {
+  static const int want = getenv("DEEPTHIN_MSE_LT") ? atoi(getenv("DEEPTHIN_MSE_LT")) : 1;
+  return want && g.s * g.rank >= 256 && batch >= 1024 && g.r_dim >= 1024;
+}
+}  // namespace
+
 static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dtype,
                            const void *xf, const void *wf, int f_dtype, const float *bias,
                            int act, float act_arg, void *y, int y_dtype, char *ws,
@@ -1496,7 +1513,8 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
 }
 
 size_t tc_forward_mse_ws(const Geo &g, int64_t batch) {
-  return tc_gemm_ws(g, batch) + (size_t)round_up(mse_parts_bound(g, batch) * 8, 256);
+  return tc_gemm_ws(g, batch) + (size_t)round_up(mse_parts_bound(g, batch) * 8, 256) +
+         (size_t)round_up(g.r_dim * 4, 256) + (size_t)round_up(1184 * 8, 256) + kLtWsFwd;
 }
 
 int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
@@ -1576,6 +1594,23 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     GemmCall c1{xt, g.n, batch * g.s, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
                 P, g.rank, DT_F32, nullptr, false, 0};
     if (int rc = run_gemm(c1, st)) return rc;
+    if (mse && mse_lt_ok(g, batch)) {
+      // grad = scale * (P XF2^T + b - t) in one cuBLASLt tf32 GEMM: alpha = scale, C = target,
+      // beta = -scale, bias epilogue with scale * b; then the fixed-order fp64 loss from grad
+      char *tail = reinterpret_cast<char *>(mse->part) + round_up(mse_parts_bound(g, batch) * 8, 256);
+      float *bs = reinterpret_cast<float *>(tail);
+      double *sq_part = reinterpret_cast<double *>(tail + round_up(g.r_dim * 4, 256));
+      void *lws = tail + round_up(g.r_dim * 4, 256) + round_up(1184 * 8, 256);
+      const float sc = (float)mse->scale;
+      k_scale_vec<<<(unsigned)((g.r_dim + 255) / 256), 256, 0, st>>>(g.r_dim, bias, sc, bs);
+      if (int rc = check_launch("scale_vec")) return rc;
+      if (int rc = lt_gemm_ep(st, batch, g.r_dim, SR, P, SR, reinterpret_cast<const float *>(xf), SR,
+                              mse->target, reinterpret_cast<float *>(y), g.r_dim, sc, -sc, bs, lws,
+                              kLtWsFwd))
+        return rc;
+      return launch_sumsq(batch * g.r_dim, reinterpret_cast<const float *>(y), 1.0 / mse->scale,
+                          sq_part, mse->loss_sum, st);
+    }
     GemmCall c2{P, SR, batch, SR, xf, SR, g.r_dim, bias, act, act_arg,
                 y, g.r_dim, y_dtype, nullptr, true, 1};
     if (mse) {
@@ -1704,6 +1739,61 @@ int lt_gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, const void *A, boo
 
 constexpr size_t kLtWs = 32u << 20;
 
+}  // namespace
+
+namespace {
+// Row-major D[M x N] (ldd) = alpha * A[M x K] (lda) @ B^T (B stored N x K, ldb) + beta * C + bias
+// (bias over the N columns; C same layout as D, nullable with beta = 0), tf32 compute.
+int lt_gemm_ep(cudaStream_t st, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+               const float *B, int64_t ldb, const float *C, float *D, int64_t ldd, float alpha,
+               float beta, const float *bias, void *ws, size_t ws_bytes) {
+  cublasLtHandle_t h = lt_handle();
+  if (!h) {
+    set_error("cublasLtCreate failed");
+    return DT_E_CUDA;
+  }
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  cublasLtMatmulPreference_t pref = nullptr;
+  cublasStatus_t e = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F);
+  // column-major: D^T (N x M) = B (N x K, i.e. B^T stored K x N -> op T) * A^T (K x M, op N)
+  const cublasOperation_t opa = CUBLAS_OP_T, opb = CUBLAS_OP_N;
+  if (e == CUBLAS_STATUS_SUCCESS)
+    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &opa, sizeof(opa));
+  if (e == CUBLAS_STATUS_SUCCESS)
+    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &opb, sizeof(opb));
+  if (e == CUBLAS_STATUS_SUCCESS && bias) {
+    const cublasLtEpilogue_t ep = CUBLASLT_EPILOGUE_BIAS;
+    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &ep, sizeof(ep));
+    if (e == CUBLAS_STATUS_SUCCESS)
+      e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
+  }
+  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&la, CUDA_R_32F, K, N, ldb);
+  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&lb, CUDA_R_32F, K, M, lda);
+  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, N, M, ldd);
+  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatmulPreferenceCreate(&pref);
+  if (e == CUBLAS_STATUS_SUCCESS)
+    e = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                             &ws_bytes, sizeof(ws_bytes));
+  cublasLtMatmulHeuristicResult_t heur{};
+  int found = 0;
+  if (e == CUBLAS_STATUS_SUCCESS)
+    e = cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, lc, pref, 1, &heur, &found);
+  if (e == CUBLAS_STATUS_SUCCESS && found > 0)
+    e = cublasLtMatmul(h, op, &alpha, B, la, A, lb, &beta, C ? C : D, lc, D, lc, &heur.algo, ws,
+                       ws_bytes, st);
+  int rc = DT_OK;
+  if (e != CUBLAS_STATUS_SUCCESS || found == 0) {
+    set_error("cuBLASLt matmul (epilogue) failed (status " + std::to_string((int)e) + ")");
+    rc = DT_E_CUDA;
+  }
+  if (pref) cublasLtMatmulPreferenceDestroy(pref);
+  if (lc) cublasLtMatrixLayoutDestroy(lc);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (op) cublasLtMatmulDescDestroy(op);
+  return rc;
+}
 }  // namespace
 
 bool tc_backward_ok(const Geo &g) {

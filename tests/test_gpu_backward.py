@@ -157,3 +157,26 @@ def test_forward_mse_fused_matches_separate(geo):
     assert torch.allclose(g.double(), want_g, rtol=0, atol=1e-6 * float(want_g.abs().max()))
     want_loss = float(((y.double() - t.double()) ** 2).sum())
     assert float(loss.item()) == pytest.approx(want_loss, rel=1e-6)  # fp32 chunk sums
+
+
+def test_forward_mse_cublaslt_epilogue_large():
+    """Config-5-like factored geometry (s*rank = 512): the MSE runs through cuBLASLt's tf32 GEMM
+    with C = target and the bias epilogue, then a fixed-order fp64 loss from the gradient.
+    Checked against the oracle's forward on the same bf16 inputs (tf32 contract 2e-3 on the
+    gradient's pre-image) and against its own loss definition."""
+    q = r_dim = 2048; rank = 64; n = 256; m = q * r_dim // n; batch = 1024
+    op = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, batch, seed=3).items()}
+    p = D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    layer = D.DeepThinLayer(p, d["xf"], d["wf"], d["bias"], mma="bf16")
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda").to(torch.bfloat16)
+    t = torch.tensor(d["target"], dtype=torch.float32, device="cuda")
+    norm = float(batch * r_dim)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    g = layer.forward_mse(x, t, norm, loss)
+    z = O.layer_forward(d["x"], d["xf"], d["wf"], op, d["bias"])
+    got_z = g.double().cpu().numpy() * norm / 2.0 + d["target"]
+    assert O.rel_error(got_z, z) <= 2e-3
+    want_loss = float(((g.double() * norm / 2.0) ** 2).sum())
+    assert float(loss.item()) == pytest.approx(want_loss, rel=1e-9)
+    assert float(loss.item()) == pytest.approx(float(((z - d["target"]) ** 2).sum()), rel=2e-3)
