@@ -197,6 +197,14 @@ size_t dt_lstm_gates_workspace_bytes(const dt_plan *plan, int64_t batch);
 int dt_lstm_gates(const dt_plan *plan, int64_t batch, const float *h, const float *const *xf,
                   const float *const *wf, const float *const *bias, float *const *gh,
                   void *workspace, size_t workspace_bytes, dt_stream stream);
+/* The whole LSTM recurrence of BASELINE config 4 in one persistent cooperative kernel: for
+ * t < T, gates = gx[g][t] + h_{t-1} @ W_g + bias[g] (the dt_lstm_gates contractions, exact fp32),
+ * then the dt_lstm_cell update; h_{-1} = c_{-1} = 0. gx[g]: bf16, T*batch x q (time-major rows);
+ * out: bf16 T*batch x q (the h sequence). batch <= 64. */
+size_t dt_lstm_sequence_workspace_bytes(const dt_plan *plan, int64_t batch);
+int dt_lstm_sequence(const dt_plan *plan, int64_t T, int64_t batch, const void *const *gx,
+                     const float *const *xf, const float *const *wf, const float *const *bias,
+                     void *out, void *workspace, size_t workspace_bytes, dt_stream stream);
 /* LSTM cell step of BASELINE config 4 (no reference counterpart: SURVEY.md §8(a) a8 lists LSTM
  * gates as outside the reference). Gate order i, f, g, o; gx[g]: bf16 input projections
  * (batch rows, row stride ld_gx, biases included); gh[g]: fp32 recurrent projections (batch x

@@ -494,6 +494,42 @@ int dt_lstm_gates(const dt_plan *plan, int64_t batch, const float *h, const floa
   return lstm_gates(g, batch, h, xf, wf, bias, gh, (char *)workspace, (cudaStream_t)stream);
 }
 
+size_t dt_lstm_sequence_workspace_bytes(const dt_plan *plan, int64_t batch) {
+  Geo g;
+  if (make_geo(plan, &g) || !lstm_seq_ok(g, batch)) return 0;
+  return lstm_seq_ws(g, batch);
+}
+
+int dt_lstm_sequence(const dt_plan *plan, int64_t T, int64_t batch, const void *const *gx,
+                     const float *const *xf, const float *const *wf, const float *const *bias,
+                     void *out, void *workspace, size_t workspace_bytes, dt_stream stream) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return rc;
+  if (T < 0 || batch < 0) {
+    set_error("lstm_sequence: T, batch >= 0");
+    return DT_E_DIM;
+  }
+  if (T == 0 || batch == 0) return DT_OK;
+  if (!lstm_seq_ok(g, batch)) {
+    set_error("lstm_sequence: needs batch <= 64 and a square reuse geometry dt_lstm_gates takes");
+    return DT_E_UNSUPPORTED;
+  }
+  if (!gx || !xf || !wf || !out || !workspace) {
+    set_error("lstm_sequence: NULL operand pointer");
+    return DT_E_ARG;
+  }
+  for (int i = 0; i < 4; ++i)
+    if (!gx[i] || !xf[i] || !wf[i]) {
+      set_error("lstm_sequence: NULL gate pointer");
+      return DT_E_ARG;
+    }
+  if (workspace_bytes < lstm_seq_ws(g, batch)) {
+    set_error("lstm_sequence: workspace too small");
+    return DT_E_ARG;
+  }
+  return lstm_seq(g, T, batch, gx, xf, wf, bias, out, (char *)workspace, (cudaStream_t)stream);
+}
+
 int dt_lstm_cell(int64_t batch, int64_t hidden, const void *const *gx, int64_t ld_gx,
                  const float *const *gh, float *c, float *h32, void *h16, dt_stream stream) {
   if (batch < 0 || hidden < 0 || ld_gx < hidden) {

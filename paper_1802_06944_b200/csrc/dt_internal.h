@@ -48,6 +48,11 @@ size_t lstm_gates_ws(const Geo &g, int64_t batch);
 int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *xf,
                const float *const *wf, const float *const *bias, float *const *gh, char *ws,
                cudaStream_t st);
+// the whole recurrence (T steps, batch <= 64) in one cooperative persistent kernel
+bool lstm_seq_ok(const Geo &g, int64_t batch);
+size_t lstm_seq_ws(const Geo &g, int64_t batch);
+int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, const float *const *xf,
+             const float *const *wf, const float *const *bias, void *out, char *ws, cudaStream_t st);
 int launch_lstm_cell(int64_t batch, int64_t hidden, const void *const *gx, int64_t ld_gx,
                      const float *const *gh, float *c, float *h32, void *h16, cudaStream_t st);
 int launch_act_grad(int64_t count, const float *up, const float *pre, int act, float act_arg,

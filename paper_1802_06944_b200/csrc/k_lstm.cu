@@ -8,6 +8,9 @@
 // written in fp32 (next step's recurrent input) and bf16 (the sequence output).
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "dt_internal.h"
 
 namespace dt {
@@ -205,6 +208,261 @@ int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *
   if (int rc = check_launch("lstm_gates_p")) return rc;
   k_gates_y<<<dim3((unsigned)((H + 63) / 64), 4), 256, smy, st>>>(batch, H, K2, P, a);
   return check_launch("lstm_gates_y");
+}
+
+}  // namespace dt
+
+// =============================================================================================
+// The whole LSTM recurrence in ONE persistent kernel (config 4): T steps, two grid-wide
+// barriers per step, no host launches inside the loop. Work units (all exact fp32 FFMA):
+//   phase A, unit (gate g, segment seg, 16-row group rg):
+//     h[rows, seg cols] = cell(gx[t-1], gh, c) for t > 0 (0 at t = 0); gate 0's unit also
+//     writes c' (double-buffered) and the bf16 sequence output; then
+//     P_g[rows, seg*R + k] = h[rows, seg cols] . wf_g[k, :]
+//   phase B, unit (gate g, 64-column block): gh_g[:, cols] = P_g @ XF2_g[cols]^T + b_hg
+// After the last step one more phase A computes h[T-1]. Same arithmetic (and summation order)
+// as k_gates_p / k_gates_y / k_lstm_cell.
+// =============================================================================================
+namespace dt {
+namespace {
+
+struct SeqArgs {
+  const float *xf[4], *wf[4], *bias[4];
+  const __nv_bfloat16 *gx[4];  // T*B x H each (biases of the input projections included)
+  float *gh;                   // 4 x B x H
+  float *P;                    // 4 x B x K2
+  float *c;                    // 2 x B x H (double-buffered)
+  __nv_bfloat16 *out;          // T*B x H
+  unsigned *bar;               // grid barrier counter (zeroed before launch)
+  unsigned long long *trace;   // DEEPTHIN_LSTM_TRACE: globaltimer stamps (block 0, first steps)
+  int T, B, H, n, R, s, K2;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// grid-wide barrier: monotone counter, the k-th barrier completes at k * gridDim.x arrivals
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_gpu(bar) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float sigm_(float z) { return 1.f / (1.f + expf(-z)); }
+
+__global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
+  extern __shared__ float sm[];
+  const int B = a.B, H = a.H, n = a.n, R = a.R, K2 = a.K2;
+  const int npad = n + 1, kp = K2 + 4;
+  const int rgs = (B + 15) / 16;
+  const int unitsA = 4 * a.s * rgs, unitsB = 4 * ((H + 63) / 64);
+  // one phase-A and one phase-B unit per CTA when the grid covers them: their factor operands
+  // (wf_g, and the 64-column XF2_g block) stay resident in shared memory for all T steps
+  float *hs = sm, *ws = hs + 16 * npad, *ps = ws + R * npad;
+  ps += (4 - ((ps - sm) & 3)) & 3;  // 16-byte alignment for the float4 tiles
+  float *xs = ps + 64 * kp;
+  const bool resA = unitsA <= (int)gridDim.x, resB = unitsB <= (int)gridDim.x;
+  auto wf_of = [&](int g) { return g == 0 ? a.wf[0] : g == 1 ? a.wf[1] : g == 2 ? a.wf[2] : a.wf[3]; };
+  auto xf_of = [&](int g) { return g == 0 ? a.xf[0] : g == 1 ? a.xf[1] : g == 2 ? a.xf[2] : a.xf[3]; };
+  if (resA && (int)blockIdx.x < unitsA) stage_rows(ws, npad, wf_of((int)blockIdx.x / (a.s * rgs)), n, R, n);
+  if (resB && (int)blockIdx.x < unitsB) {
+    const int g = (int)blockIdx.x / ((H + 63) / 64), j0 = ((int)blockIdx.x % ((H + 63) / 64)) * 64;
+    stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, min(64, H - j0), K2);
+  }
+  unsigned target = 0;
+  auto stamp = [&](int t, int k) {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 8) {
+      unsigned long long v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      a.trace[t * 4 + k] = v;
+    }
+  };
+  for (int t = 0; t <= a.T; ++t) {
+    // ---------------- phase A: cell of step t-1 (rows x one segment) then P of step t ----------
+    const float *cprev = a.c + (size_t)((t + 1) & 1) * B * H;
+    float *cnext = a.c + (size_t)(t & 1) * B * H;
+    for (int u = blockIdx.x; u < unitsA; u += gridDim.x) {
+      const int g = u / (a.s * rgs), seg = (u / rgs) % a.s, rg = u % rgs;
+      const int b0 = rg * 16, nb = min(16, B - b0);
+      __syncthreads();
+      // h rows of this segment: gate pre-activations of 8 elements per thread loaded together
+      for (int i0 = threadIdx.x; i0 < nb * n; i0 += 8 * blockDim.x) {
+        float z[8][4], cp[8];
+        size_t ev[8], gv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int i = min(i0 + v * (int)blockDim.x, nb * n - 1);
+          const int b = i / n, j = seg * n + i % n;
+          ev[v] = (size_t)(b0 + b) * H + j;
+          gv[v] = ((size_t)(t > 0 ? t - 1 : 0) * B + b0 + b) * H + j;
+        }
+        if (t > 0) {
+          const size_t BH = (size_t)B * H;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              z[v][q] = __bfloat162float(a.gx[q == 0 ? 0 : q == 1 ? 1 : q == 2 ? 2 : 3][gv[v]]) + a.gh[q * BH + ev[v]];
+            cp[v] = cprev[ev[v]];
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int i = i0 + v * (int)blockDim.x;
+          if (i < nb * n) {
+            float h = 0.f;
+            if (t > 0) {
+              const float cn = sigm_(z[v][1]) * cp[v] + sigm_(z[v][0]) * tanhf(z[v][2]);
+              h = sigm_(z[v][3]) * tanhf(cn);
+              if (g == 0) {
+                cnext[ev[v]] = cn;
+                a.out[gv[v]] = __float2bfloat16_rn(h);
+              }
+            }
+            hs[(i / n) * npad + i % n] = h;
+          }
+        }
+      }
+      if (t == a.T) continue;  // the final cell only
+      if (!resA) {
+        __syncthreads();
+        stage_rows(ws, npad, wf_of(g), n, R, n);
+      }
+      __syncthreads();
+      for (int o = threadIdx.x; o < nb * R; o += blockDim.x) {
+        const int b = o / R, k = o % R;
+        const float *hr = hs + b * npad, *wr = ws + k * npad;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int tt = 0; tt < n; tt += 4) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[v] = fmaf(hr[tt + v], wr[tt + v], acc[v]);
+        }
+        a.P[((size_t)g * B + b0 + b) * K2 + seg * R + k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
+    }
+    if (t == a.T) break;
+    stamp(t, 0);
+    grid_barrier(a.bar, target);
+    stamp(t, 1);
+    // ---------------- phase B: gh_g[:, 64-column block] = P_g XF2_g^T + b ----------------
+    for (int u = blockIdx.x; u < unitsB; u += gridDim.x) {
+      const int g = u / ((H + 63) / 64), j0 = (u % ((H + 63) / 64)) * 64, nj = min(64, H - j0);
+      const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
+      __syncthreads();
+      if (!resB) stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, nj, K2);
+      stage_rows(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2);
+      __syncthreads();
+      const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+      float acc[4][4] = {};
+      for (int kk = 0; kk < K2; kk += 4) {
+        float4 pv[4], xv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) pv[r] = *reinterpret_cast<const float4 *>(ps + (tr * 4 + r) * kp + kk);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) xv[c] = *reinterpret_cast<const float4 *>(xs + (tc + 16 * c) * kp + kk);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc[r][c] = fmaf(pv[r].x, xv[c].x, acc[r][c]);
+            acc[r][c] = fmaf(pv[r].y, xv[c].y, acc[r][c]);
+            acc[r][c] = fmaf(pv[r].z, xv[c].z, acc[r][c]);
+            acc[r][c] = fmaf(pv[r].w, xv[c].w, acc[r][c]);
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int b = tr * 4 + r;
+        if (b >= B) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = tc + 16 * c;
+          if (j < nj) a.gh[((size_t)g * B + b) * H + j0 + j] = acc[r][c] + (bg ? bg[j0 + j] : 0.f);
+        }
+      }
+    }
+    stamp(t, 2);
+    grid_barrier(a.bar, target);
+    stamp(t, 3);
+  }
+}
+
+}  // namespace
+
+bool lstm_seq_ok(const Geo &g, int64_t batch) {
+  return lstm_gates_ok(g) && batch >= 1 && batch <= 64 && g.n <= 1024 &&
+         ((size_t)(16 + g.rank) * (g.n + 1) + 4 + (size_t)128 * (g.s * g.rank + 4)) * 4 <= 227 * 1024;
+}
+size_t lstm_seq_ws(const Geo &g, int64_t batch) {
+  return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * g.s * g.rank * 4 + (size_t)2 * batch * g.q * 4 + 256;
+}
+
+int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, const float *const *xf,
+             const float *const *wf, const float *const *bias, void *out, char *ws, cudaStream_t st) {
+  if (T == 0 || batch == 0) return DT_OK;
+  SeqArgs a;
+  for (int i = 0; i < 4; ++i) {
+    a.xf[i] = xf[i]; a.wf[i] = wf[i]; a.bias[i] = bias ? bias[i] : nullptr;
+    a.gx[i] = reinterpret_cast<const __nv_bfloat16 *>(gx[i]);
+  }
+  a.T = (int)T; a.B = (int)batch; a.H = (int)g.q; a.n = (int)g.n; a.R = (int)g.rank;
+  a.s = (int)g.s; a.K2 = (int)(g.s * g.rank);
+  char *cur = ws;
+  a.gh = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * g.q * 4;
+  a.P = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * a.K2 * 4;
+  a.c = reinterpret_cast<float *>(cur); cur += (size_t)2 * batch * g.q * 4;
+  a.bar = reinterpret_cast<unsigned *>(cur);
+  a.out = reinterpret_cast<__nv_bfloat16 *>(out);
+  // c(-1) = 0 lives in buffer 1 (read at t = 1 as cprev = c[(t+1)&1]... step 0's cell is skipped)
+  DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));
+  DT_CUDA_CHECK(cudaMemsetAsync(a.bar, 0, 256, st));
+  const size_t smem = ((size_t)(16 + a.R) * (a.n + 1) + 4 + (size_t)128 * (a.K2 + 4)) * 4;
+  static bool attr = false;
+  if (!attr) {
+    DT_CUDA_CHECK(cudaFuncSetAttribute(k_lstm_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int unitsA = 4 * a.s * ((a.B + 15) / 16), unitsB = 4 * ((a.H + 63) / 64);
+  const int grid = std::min(nsm, std::max(unitsA, unitsB));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: grid barriers are safe
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static const bool tracing = getenv("DEEPTHIN_LSTM_TRACE") != nullptr;
+  a.trace = nullptr;
+  if (tracing) {
+    DT_CUDA_CHECK(cudaMalloc(&a.trace, 32 * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 32 * 8, st));
+  }
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_lstm_seq, a));
+  if (tracing) {
+    unsigned long long h[32];
+    DT_CUDA_CHECK(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    DT_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFree(a.trace);
+    for (int t = 0; t < 8; ++t)
+      fprintf(stderr, "lstm step %d: A %.2f  bar1 %.2f  B %.2f  bar2 %.2f us\n", t,
+              t ? (h[t * 4] - h[t * 4 - 1]) * 1e-3 : 0.0, (h[t * 4 + 1] - h[t * 4]) * 1e-3,
+              (h[t * 4 + 2] - h[t * 4 + 1]) * 1e-3, (h[t * 4 + 3] - h[t * 4 + 2]) * 1e-3);
+  }
+  return check_launch("lstm_seq");
 }
 
 }  // namespace dt

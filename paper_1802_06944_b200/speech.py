@@ -15,8 +15,10 @@ cell is the standard one (gate order i, f, g, o), restated in ``oracle/deepthin_
 
 Execution (B200): the time-parallel layers (fc1-3, the four input projections, fc4, out) run
 once over all T*B frames on the bf16 tensor-core path; the recurrence runs T steps of four
-exact-fp32 recurrent contractions (the FFMA reuse kernel, batch B) plus one fused cell kernel,
-captured once into a CUDA graph and replayed (launch-latency-bound at batch 64).
+exact-fp32 recurrent contractions plus the cell, all T steps inside ONE persistent cooperative
+kernel (dt_lstm_sequence: two grid barriers per step, no host launches in the loop); the
+per-step form (dt_lstm_gates + dt_lstm_cell captured into a CUDA graph) remains for larger
+batches.
 """
 
 from __future__ import annotations
@@ -122,6 +124,27 @@ class SpeechRNN:
                      ws=self._wsp(name, fp.plan, x.shape[0], _lib.DT_MMA_BF16), cached=True)
         return y
 
+    def _sequence(self, gx, T, B):
+        """The whole recurrence in one persistent kernel (dt_lstm_sequence); None when the
+        geometry / batch does not take it."""
+        lib = _lib.lib()
+        hl = [self.layers[f"h_{g}"] for g in GATES]
+        if not all(fp.plan == hl[0][0].plan for fp, _ in hl):
+            return None
+        ps = _lib.plan_struct(hl[0][0].plan)
+        need = lib.dt_lstm_sequence_workspace_bytes(C.byref(ps), B)
+        if need == 0:
+            return None
+        ws = self._ws.get("seq")
+        if ws is None or ws.numel() < need:
+            ws = self._ws["seq"] = torch.empty(need, dtype=torch.uint8, device=device())
+        out = torch.empty((T * B, self.hidden), dtype=torch.bfloat16, device=device())
+        P = lambda ts: (C.c_void_p * 4)(*[t.data_ptr() for t in ts])
+        _lib.check(lib.dt_lstm_sequence(C.byref(ps), T, B, P(gx), P([fp.xf for fp, _ in hl]),
+                                        P([fp.wf for fp, _ in hl]), P([b for _, b in hl]),
+                                        out.data_ptr(), ws.data_ptr(), ws.numel(), stream_handle()))
+        return out
+
     def _recurrence(self, gx, T, B, graph=True):
         """T LSTM steps; returns the bf16 sequence output (T*B x hidden)."""
         H = self.hidden
@@ -191,9 +214,10 @@ class SpeechRNN:
                                         st["out"].data_ptr() + t * B * H * esz, stream_handle()))
 
     # ---- forward ------------------------------------------------------------------------
-    def forward(self, x, graph: bool = True):
+    def forward(self, x, graph: bool = True, persistent: bool = True):
         """x: (T, B, n_in) CUDA tensor (bf16 or fp32), time-major. Returns fp32 logits
-        (T, B, n_out)."""
+        (T, B, n_out). The recurrence runs as one persistent kernel (``persistent``, batch <= 64)
+        or as a CUDA graph of per-step launches (``graph``) or eagerly."""
         if not isinstance(x, torch.Tensor) or x.dim() != 3 or x.shape[2] != self.n_in:
             raise DimensionError(f"input must be (T, B, {self.n_in}), got "
                                  f"{tuple(x.shape) if hasattr(x, 'shape') else type(x)}")
@@ -202,7 +226,9 @@ class SpeechRNN:
         for name in ("fc1", "fc2", "fc3"):
             h = self._dense(name, h, "clipped_relu")
         gx = [self._dense(f"x_{g}", h, "identity") for g in GATES]
-        seq = self._recurrence(gx, T, B, graph=graph)
+        seq = self._sequence(gx, T, B) if persistent else None
+        if seq is None:
+            seq = self._recurrence(gx, T, B, graph=graph)
         h = self._dense("fc4", seq, "clipped_relu")
         y = self._dense("out", h, "identity", out_dtype=torch.float32)
         return y.reshape(T, B, self.n_out)

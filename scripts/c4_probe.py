@@ -16,6 +16,9 @@ for _ in range(3):
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
 print(f"forward T={T} B={B}: {ms:.2f} ms, {T * B / ms * 1e3 / 1e6:.3f} M frames/s")
+y2 = m.forward(x, persistent=False)
+torch.cuda.synchronize()
+print("persistent == graph:", bool(torch.equal(y, y2)))
 st = m._graphs[(T, B)]
 e0.record()
 for _ in range(3):

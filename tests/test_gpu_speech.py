@@ -76,10 +76,15 @@ def test_speech_graph_equals_eager_and_repeats(model):
     m, _ = model
     T, B = 7, 4
     x = torch.randn(T, B, 494, device="cuda").to(torch.bfloat16)
-    y1 = m.forward(x, graph=True)
-    y2 = m.forward(x, graph=True)   # replay of the captured recurrence
-    y3 = m.forward(x, graph=False)
+    y1 = m.forward(x, graph=True, persistent=False)
+    y2 = m.forward(x, graph=True, persistent=False)   # replay of the captured recurrence
+    y3 = m.forward(x, graph=False, persistent=False)
+    y4 = m.forward(x)                                 # the persistent one-kernel recurrence
+    y5 = m.forward(x)
     assert torch.equal(y1, y2) and torch.equal(y1, y3)
+    assert torch.equal(y4, y5)
+    # same arithmetic and summation order as the per-step kernels
+    assert torch.equal(y1, y4)
 
 
 def test_lstm_gates_match_oracle(model):
