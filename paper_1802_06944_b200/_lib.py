@@ -12,7 +12,7 @@ import os
 from .errors import ArgumentError, CudaError, DimensionError, UnsupportedConfigurationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
+LIB_PATH = os.environ.get("DEEPTHIN_LIB") or os.path.join(_HERE, "_lib", "libdeepthin_b200.so")
 
 DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA, DT_E_FORMAT = range(6)
 DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64, DT_FACTORS_ROWS = 0, 1, 2, 3, 4

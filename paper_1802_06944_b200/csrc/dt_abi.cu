@@ -300,12 +300,8 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
       return DT_E_UNSUPPORTED;
     }
     if (batch == 0) return DT_OK;
-    const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
-    if (int rc = tc_rows_forward(g, batch, x, nullptr, nullptr, bias, eact, act_arg, y, y_dtype,
-                                 (char *)const_cast<void *>(xf), (cudaStream_t)stream, true))
-      return rc;
-    return act == DT_ACT_SOFTMAX ? launch_row_softmax(batch, g.r_dim, y, y_dtype, (cudaStream_t)stream)
-                                 : DT_OK;
+    return tc_rows_forward(g, batch, x, nullptr, nullptr, bias, act, act_arg, y, y_dtype,
+                           (char *)const_cast<void *>(xf), (cudaStream_t)stream, true);
   }
   if (f_dtype == DT_FACTORS_ROWS) {
     set_error("DT_FACTORS_ROWS operands are for the bf16 tensor-core path");

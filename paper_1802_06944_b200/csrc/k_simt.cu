@@ -330,14 +330,13 @@ __global__ void __launch_bounds__(256) k_softmax_warp(int64_t rows, int cols, vo
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float ms = mx * l2e;
     float sum = 0.f;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (lane + 32 * c < nch) {
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-          v[c][k] = exp2f(fmaf(v[c][k], l2e, -ms));
+          v[c][k] = exp2f((v[c][k] - mx) * l2e);  // the difference first: exact near the max
           sum += v[c][k];
         }
       }

@@ -45,7 +45,10 @@ namespace {
 using namespace ptx;
 
 constexpr int GM = 128;  // output columns per tile (UMMA M)
-constexpr int GN = 256;  // batch rows per tile (UMMA N; N = 256 runs the MMA at ~88% of peak)
+#ifndef DT_GEMM_GN
+#define DT_GEMM_GN 256
+#endif
+constexpr int GN = DT_GEMM_GN;  // batch rows per tile (UMMA N; N = 256 runs the MMA at ~88% of peak)
 constexpr int GK = 64;   // K per stage: one 128-byte swizzle row of bf16
 constexpr uint32_t kABytes = GM * GK * 2;  // one W^T k-block (16 KB)
 constexpr uint32_t kXBytes = GN * GK * 2;  // one x k-block (32 KB)
@@ -1259,7 +1262,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
     p.off_x = wbytes;
     p.S = (int)std::min<uint32_t>(6, (kSmemMax - kFixed - wbytes) / kXBytes);
     p.csize = 1;
-    for (int cs : {4, 2})
+    for (int cs : {16, 8, 4, 2})
       if (cs <= want_cs && n_jb >= cs) { p.csize = cs; break; }
   } else {
     p.wres = 0;
@@ -1338,6 +1341,8 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   const int eact = c.act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : c.act;
   GemmFn fn = pick_gemm(c.y_dtype, eact, pair, c.el);
   DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  if (p.csize > 8)
+    DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 
   static const int use_pdl = getenv("DEEPTHIN_PDL") ? atoi(getenv("DEEPTHIN_PDL")) : 1;
   cudaLaunchConfig_t cfg{};
@@ -1572,12 +1577,10 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     // one-kernel row-tile form (k_tc_rows.cu) when the geometry and operands allow it
     if (!mse && tc_rows_ok(g, x_dtype, y_dtype) && ((reinterpret_cast<uintptr_t>(x) |
         reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0) {
-      const int eact = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
-      if (int rc = tc_rows_forward(g, batch, x, reinterpret_cast<const float *>(wf),
-                                   reinterpret_cast<const float *>(xf), bias, eact, act_arg, y,
-                                   y_dtype, ws, st))
-        return rc;
-      return act == DT_ACT_SOFTMAX ? launch_row_softmax(batch, g.r_dim, y, y_dtype, st) : DT_OK;
+      // (softmax: fused into the epilogue when it fits, else a post pass inside)
+      return tc_rows_forward(g, batch, x, reinterpret_cast<const float *>(wf),
+                             reinterpret_cast<const float *>(xf), bias, act, act_arg, y, y_dtype,
+                             ws, st);
     }
     char *wf16 = take(g.rank * g.n * 2);
     float *P = reinterpret_cast<float *>(take(batch * g.s * g.rank * 4));

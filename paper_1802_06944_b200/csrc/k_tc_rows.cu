@@ -61,6 +61,8 @@ struct RowsParams {
   const float *bias;
   void *y;
   float arg;
+  int softmax;         // fused row softmax over the full output width (see the epilogue)
+  uint32_t off_sm;     // softmax: 2 x cs x 128 (max, sum) partials
   int bslot;  // K slot carrying the bias (P = 1 there, XF2p = bias * scale), -1: epilogue adds it
   uint32_t off_x, off_a2, off_wf, off_b, off_out, off_bar;
   unsigned long long *trace;  // DEEPTHIN_ROWS_TRACE: globaltimer stamps of cluster 0
@@ -89,6 +91,12 @@ __device__ __forceinline__ float act_out(float z, float arg) {
   if constexpr (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_approx(z), 0.5f);
   if constexpr (YDT == DT_BF16 && ACT == DT_ACT_TANH) return tanh_approx(z);
   return act_fast<ACT>(z, arg);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -149,7 +157,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   uint64_t *d_full = b_empty + kBS, *d_empty = d_full + 2;
   uint64_t *a2_full = d_empty + 2, *a2_free = a2_full + 2;
   uint64_t *p_full = a2_free + 2, *wf_full = p_full + 2;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(wf_full + 1);
+  uint64_t *sm_full = wf_full + 1;  // softmax partials of every cluster CTA landed (2, by tile)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(sm_full + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int cs = p.cs;
   const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
@@ -169,6 +178,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       mbar_init(&p_full[i], 1);
     }
     mbar_init(wf_full, 1);
+    mbar_init(&sm_full[0], 1);
+    mbar_init(&sm_full[1], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -276,12 +287,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           tc_fence_after();
           const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)ab * kA2Bytes;
           int ci = 0;
+          if (p.softmax) {  // the whole tile's chunks live in TMEM together (row softmax)
+            mbar_wait(&d_empty[0], dph ^ 1);
+            tc_fence_after();
+          }
           for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
             const int slot = b_res ? ci : bs;
             mbar_wait(&b_full[slot], b_res ? 0u : bph);
-            mbar_wait(&d_empty[db], dph ^ 1);
+            if (!p.softmax) mbar_wait(&d_empty[db], dph ^ 1);
             tc_fence_after();
-            const uint32_t d = tbase + kDCol + (uint32_t)(db * kNc);
+            const uint32_t d = p.softmax ? tbase + 128u + (uint32_t)(ci * kNc)
+                                         : tbase + kDCol + (uint32_t)(db * kNc);
             const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
             for (int k = 0; k < p.k2 / 8; ++k)
               mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
@@ -290,8 +306,14 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
               mma_commit(&b_empty[bs]);
               if (++bs == kBS) { bs = 0; bph ^= 1; }
             }
-            mma_commit(&d_full[db]);
-            if (++db == 2) { db = 0; dph ^= 1; }
+            if (!p.softmax) {
+              mma_commit(&d_full[db]);
+              if (++db == 2) { db = 0; dph ^= 1; }
+            }
+          }
+          if (p.softmax) {
+            mma_commit(&d_full[0]);
+            dph ^= 1;
           }
           // this CTA's reads of A2[ab] are done when these MMAs complete: tell every writer
           if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
@@ -364,6 +386,155 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
+    if (p.softmax) {
+      // Fused row softmax (the output layer of config 3): the tile's chunks of this CTA sit in
+      // TMEM together. Pass 1: per-row (max, sum exp) over this warp's 32 columns of each chunk,
+      // combined over the CTA's four column warps through shared memory, then over the cluster:
+      // each CTA bulk-copies its 128 (max, sum) pairs into every peer (completion counted on the
+      // peer's sm_full), and every CTA combines the cs partials in rank order. Pass 2: reload,
+      // p = exp(z - M) / L, bf16 out. Fixed reduction order: deterministic.
+      const int sp = warp & 3, e = warp - 3 - kPW, qc = e / 4, row = 32 * sp + lane;
+      const uint32_t s0 = smem_u32(smem);
+      const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
+      constexpr int E = YDT == DT_BF16 ? 2 : 4;
+      constexpr int RB = 32 * E, LPR = RB / 16, RPI = 32 / LPR, SWM = RB / 16 - 1;
+      const uint32_t out_s = s0 + p.off_out + (uint32_t)e * (32u * RB);
+      float2 *red = reinterpret_cast<float2 *>(smem + p.off_out + kEpi * 32u * RB);  // [4][128]
+      const float l2e = 1.4426950408889634f;
+      uint32_t it = 0;
+      for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
+        const int sb = (int)(it & 1);
+        float2 *part = reinterpret_cast<float2 *>(smem + p.off_sm) + sb * cs * kTM;  // [cs][128]
+        mbar_wait(&d_full[0], it & 1);
+        tc_fence_after();
+        // pass 1: per chunk e = 2^((z - m_c) log2 e) written back over z in TMEM, with the
+        // chunk's (m_c, l_c); one MUFU op per element
+        float mc[3] = {-INFINITY, -INFINITY, -INFINITY}, lc[3] = {0.f, 0.f, 0.f};
+        int ci = 0;
+        for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
+          const int col0 = c * kNc + 32 * qc;
+          const uint32_t ta = tbase + lane_t + 128u + (uint32_t)(ci * kNc + 32 * qc);
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(ta, v);
+          tmem_ld_wait();
+          const int nv = min(32, p.r_dim - col0);
+          float cm = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nv) cm = fmaxf(cm, __uint_as_float(v[i]));
+          float cl = 0.f;
+          if (nv > 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float ev = i < nv ? ex2_approx((__uint_as_float(v[i]) - cm) * l2e) : 0.f;
+              cl += ev;
+              v[i] = __float_as_uint(ev);
+            }
+            tmem_st_32x32b_x32(ta, v);
+          }
+          if (ci < 3) { mc[ci] = cm; lc[ci] = cl; }
+        }
+        tmem_st_wait();
+        float m = -INFINITY, l = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) m = fmaxf(m, mc[k]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (mc[k] > -INFINITY) l += lc[k] * ex2_approx((mc[k] - m) * l2e);
+        red[qc * kTM + row] = make_float2(m, l);
+        named_bar_sync(2, 32 * kEpi);
+        if (qc == 0) {  // the CTA's partial for this row, column warps in order
+          float M = -INFINITY, L = 0.f;
+          for (int k = 0; k < 4; ++k) {
+            const float2 q = red[k * kTM + row];
+            if (q.x > -INFINITY) {
+              const float nm = fmaxf(M, q.x);
+              L = L * exp2f((M - nm) * l2e) + q.y * exp2f((q.x - nm) * l2e);
+              M = nm;
+            }
+          }
+          part[crank * kTM + row] = make_float2(M, L);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(2, 32 * kEpi);
+        if (warp == 3 + kPW) {
+          if (lane >= 1 && lane < cs) {
+            const uint32_t peer = (uint32_t)((crank + lane) % cs);
+            const uint32_t src = smem_u32(part + crank * kTM);
+            bulk_s2c(mapa_shared(src, peer), src, kTM * 8u,
+                     mapa_shared(smem_u32(&sm_full[sb]), peer));
+          }
+          if (lane == 0) mbar_arrive_expect_tx(&sm_full[sb], (uint32_t)(cs - 1) * kTM * 8u);
+          __syncwarp();
+        }
+        mbar_wait_cluster(&sm_full[sb], (it >> 1) & 1);
+        float M = -INFINITY, L = 0.f;
+        for (int k = 0; k < cs; ++k) {
+          const float2 q = part[k * kTM + row];
+          if (q.x > -INFINITY) {
+            const float nm = fmaxf(M, q.x);
+            L = L * exp2f((M - nm) * l2e) + q.y * exp2f((q.x - nm) * l2e);
+            M = nm;
+          }
+        }
+        const float inv = 1.f / L;
+        float fc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) fc[k] = mc[k] > -INFINITY ? ex2_approx((mc[k] - M) * l2e) * inv : 0.f;
+        // pass 2: p = e * 2^((m_c - M) log2 e) / L
+        const int64_t row0 = (int64_t)t * kTM + 32 * sp;
+        ci = 0;
+        for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
+          const int col0 = c * kNc + 32 * qc;
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tbase + lane_t + 128u + (uint32_t)(ci * kNc + 32 * qc), v);
+          tmem_ld_wait();
+          if (col0 >= p.r_dim) continue;
+          const float f = fc[ci < 3 ? ci : 2];
+          float o[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f;
+          const uint32_t rb = out_s + (uint32_t)lane * RB;
+#pragma unroll
+          for (int ch = 0; ch < RB / 16; ++ch) {
+            uint32_t w0, w1, w2, w3;
+            if constexpr (E == 2) {
+              const float *f = o + ch * 8;
+              w0 = pack_bf16(f[0], f[1]); w1 = pack_bf16(f[2], f[3]);
+              w2 = pack_bf16(f[4], f[5]); w3 = pack_bf16(f[6], f[7]);
+            } else {
+              const float *f = o + ch * 4;
+              w0 = __float_as_uint(f[0]); w1 = __float_as_uint(f[1]);
+              w2 = __float_as_uint(f[2]); w3 = __float_as_uint(f[3]);
+            }
+            const int sw = E == 2 ? ((lane >> 1) & SWM) : (lane & SWM);
+            st_shared_v4(rb + ((uint32_t)(ch ^ sw) << 4), w0, w1, w2, w3);
+          }
+          __syncwarp();
+          const int chl = lane % LPR;
+          const int cb = col0 + chl * (16 / E);
+          uint32_t w[RPI == 8 ? 4 : 8][4];
+#pragma unroll
+          for (int i = 0; i < 32 / RPI; ++i) {
+            const int r = RPI * i + lane / LPR;
+            const int sw = E == 2 ? ((r >> 1) & SWM) : (r & SWM);
+            ld_shared_v4(out_s + (uint32_t)r * RB + ((uint32_t)(chl ^ sw) << 4), w[i][0], w[i][1],
+                         w[i][2], w[i][3]);
+          }
+#pragma unroll
+          for (int i = 0; i < 32 / RPI; ++i) {
+            const int r = RPI * i + lane / LPR;
+            if (row0 + r < p.batch && cb < p.r_dim)
+              st_global_v4(reinterpret_cast<uint8_t *>(p.y) + ((row0 + r) * p.r_dim + cb) * E, w[i][0],
+                           w[i][1], w[i][2], w[i][3]);
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[0]);
+      }
+    } else {
     // 16 warps: four per TMEM lane quarter, each owning 32 of the chunk's 128 columns
     const int sp = warp & 3;           // TMEM lane quarter this warp may access
     const int e = warp - 3 - kPW;      // 0..15
@@ -444,6 +615,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       }
     }
     if (warp == 3 + kPW) rtrace(p, 40);
+    }
   }
 
   tc_fence_before();
@@ -584,10 +756,21 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.arg = act_arg;
   // a zero K slot for the bias: the rank padding of segment 0, else an all-zero pad chunk
   p.bslot = !bias ? -1 : (g.rank < p.rp ? (int)g.rank : (p.k2 > g.s * p.rp ? (int)(g.s * p.rp) : -1));
+  p.pcols = (int)((g.s / p.cs) * p.np);
+  // row softmax fused into the epilogue when every CTA's chunks of a tile fit in TMEM next to
+  // P (<= 3 chunks, 2 * pcols <= 128) and the bias rides in the contraction; else a post pass
+  const bool want_sm = act == DT_ACT_SOFTMAX;
+  // Opt-in (DEEPTHIN_ROWS_SOFTMAX=1, read per call): with every chunk of a tile held in TMEM
+  // there is no D double buffering, so tile t+1's MMAs wait for tile t's whole two-pass
+  // epilogue and its cluster exchange (~9.5 us per tile at config 3's output layer vs ~4 us
+  // for logits + the separate register softmax kernel) — measured slower end to end.
+  const char *fenv = getenv("DEEPTHIN_ROWS_SOFTMAX");
+  const int fuse_sm = fenv ? atoi(fenv) : 0;
+  p.softmax = (want_sm && fuse_sm && (p.n_chunks + p.cs - 1) / p.cs <= 3 && 2 * p.pcols <= 128 &&
+               (!bias || p.bslot >= 0)) ? 1 : 0;
+  if (want_sm) act = DT_ACT_IDENTITY;
   // bf16 sigmoid runs as 1/2 + tanh(z/2)/2: the contraction (and bias) pre-scaled by 1/2
   const float scale = (y_dtype == DT_BF16 && act == DT_ACT_SIGMOID) ? 0.5f : 1.f;
-  // shared memory: x ring | A2 x 2 | wf | XF2 ring | output staging | barriers
-  p.pcols = (int)((g.s / p.cs) * p.np);
   // shared memory: A2 x 2 | wf | XF2 ring | output staging | x ring (what is left) | barriers
   const uint32_t wf_bytes = (uint32_t)(p.nkb * p.np * 128);
   p.off_a2 = 0;
@@ -595,6 +778,12 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.off_b = (p.off_wf + wf_bytes + 1023) & ~1023u;
   p.off_out = p.off_b + kBS * kBBytes;
   p.off_x = p.off_out + kEpi * 32u * 32u * (uint32_t)(y_dtype == DT_BF16 ? 2 : 4);
+  if (p.softmax) {  // [4][128] column-warp partials, then 2 x cs x 128 cluster partials
+    p.off_x += 4 * kTM * 8;
+    p.off_sm = p.off_x;
+    p.off_x += 2u * (uint32_t)p.cs * kTM * 8;
+    p.off_x = (p.off_x + 1023) & ~1023u;
+  }
   constexpr uint32_t kSmemMax = 227 * 1024, kTail = 512 + 1024;
   p.xs = (int)std::min<uint32_t>(kXSMax, (kSmemMax - kTail - p.off_x) / kXBytes);
   p.off_bar = p.off_x + (uint32_t)p.xs * kXBytes;
@@ -677,7 +866,8 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
       fprintf(stderr, "\n");
     }
   }
-  return check_launch("tc_rows_reuse");
+  if (int rc = check_launch("tc_rows_reuse")) return rc;
+  return want_sm && !p.softmax ? launch_row_softmax(batch, g.r_dim, y, y_dtype, st) : DT_OK;
 }
 
 }  // namespace dt

@@ -100,3 +100,25 @@ def test_rows_prepared_operands_equal_per_call(act, out):
     forward_into(x, fp, b, _act_code(act), 20.0, y0, _lib.DT_MMA_BF16)
     forward_into(x, fp, b, _act_code(act), 20.0, y1, _lib.DT_MMA_BF16, cached=True)
     assert torch.equal(y0, y1)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+def test_rows_fused_softmax_output_layer(out, fused, monkeypatch):
+    """Config 3's output layer (2048 -> 3000, 3 chunks per cluster CTA): the row softmax runs in
+    the epilogue with a cluster-wide (max, sum) reduction. Checked against the oracle's softmax
+    of the kernel's own logits (identity launch of the same kernel), ragged batch."""
+    monkeypatch.setenv("DEEPTHIN_ROWS_SOFTMAX", fused)  # fused epilogue / separate row kernel
+    plan, d, fp = make_case(2048, 3000, 3, 256, 24000, 333, seed=12, rnd=O.round_bf16, bias_sd=0.5)
+    x = gpu_x(d["x"], torch.bfloat16)
+    logits = D.layer_forward(x, fp, d["bias"], "identity", mma="bf16").double().cpu().numpy()
+    if fused == "0" and out == torch.bfloat16:
+        logits = O.round_bf16(logits)  # the separate pass reads the bf16 logits back
+    want = O.apply_activation("softmax", logits)
+    y = D.layer_forward(x, fp, d["bias"], "softmax", mma="bf16", out_dtype=out)
+    got = y.double().cpu().numpy()
+    tol = 1e-6 + (2 ** -8 * want if out == torch.bfloat16 else 2e-6 * want)
+    assert np.all(np.abs(got - want) <= tol)
+    assert np.allclose(got.sum(axis=1), 1.0, atol=1e-5 if out == torch.float32 else 2e-2)
+    y2 = D.layer_forward(x, fp, d["bias"], "softmax", mma="bf16", out_dtype=out)
+    assert torch.equal(y, y2)
