@@ -104,6 +104,65 @@ __device__ __forceinline__ void stage_rows(float *dst, int sp, const float *src,
   }
 }
 
+// 64 x 64 output tile D[b][j] = sum_kk ps[b][kk] * xs[j][kk] (row pitch kp floats) on the tensor
+// cores: mma.sync m16n8k8 tf32 in the 3xTF32 form (lo*hi + hi*lo + hi*hi with hi = RNA(x),
+// lo = RNA(x - hi)): ~fp32 accuracy at a fraction of the FFMA instruction count. 8 warps, warp w
+// owns rows 16*(w%4).. and columns 32*(w/4).. (4 n-tiles of 8). acc[nt][4]: m16n8 fragments.
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void tile64_3xtf32(const float *ps, const float *xs, int kp, int K2,
+                                              float (&acc)[4][4]) {
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32, gid = lane >> 2, tig = lane & 3;
+  const int r0 = 16 * (w & 3), c0 = 32 * (w >> 2);
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
+  for (int kk = 0; kk < K2; kk += 8) {
+    const float av[4] = {ps[(r0 + gid) * kp + kk + tig], ps[(r0 + gid + 8) * kp + kk + tig],
+                         ps[(r0 + gid) * kp + kk + tig + 4], ps[(r0 + gid + 8) * kp + kk + tig + 4]};
+    uint32_t ah[4], al[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ah[i] = tf32_rna(av[i]);
+      al[i] = tf32_rna(av[i] - __uint_as_float(ah[i]));
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const float *xr = xs + (c0 + nt * 8 + gid) * kp + kk;
+      const float bv0 = xr[tig], bv1 = xr[tig + 4];
+      const uint32_t bh0 = tf32_rna(bv0), bh1 = tf32_rna(bv1);
+      const uint32_t bl0 = tf32_rna(bv0 - __uint_as_float(bh0)), bl1 = tf32_rna(bv1 - __uint_as_float(bh1));
+      mma_tf32(acc[nt], al, bh0, bh1);
+      mma_tf32(acc[nt], ah, bl0, bl1);
+      mma_tf32(acc[nt], ah, bh0, bh1);
+    }
+  }
+}
+// store the tile's fragments: D[b][j] + bias -> out[(b0 + b) * ld + j0 + j] (b < nb, j < nj)
+__device__ __forceinline__ void tile64_store(const float (&acc)[4][4], float *out, int64_t ld,
+                                             int64_t b0, int nb, int j0, int nj, const float *bias) {
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32, gid = lane >> 2, tig = lane & 3;
+  const int r0 = 16 * (w & 3), c0 = 32 * (w >> 2);
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int b = r0 + gid + (i >= 2 ? 8 : 0), j = c0 + nt * 8 + 2 * tig + (i & 1);
+      if (b < nb && j < nj) out[(b0 + b) * ld + j0 + j] = acc[nt][i] + (bias ? bias[j0 + j] : 0.f);
+    }
+}
+
 // one CTA per (segment, gate, 16-row block): h[rows, seg] and wf_g in shared memory; each
 // thread two outputs, four interleaved partial sums (fixed order)
 __global__ void __launch_bounds__(256) k_gates_p(int64_t batch, int H, int n, int R, const float *h,
@@ -142,39 +201,16 @@ __global__ void __launch_bounds__(256) k_gates_y(int64_t batch, int H, int K2, c
   const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
   float *ghg = g == 0 ? a.gh[0] : g == 1 ? a.gh[1] : g == 2 ? a.gh[2] : a.gh[3];
   stage_rows(xs, kp, xfg + (int64_t)j0 * K2, K2, nj, K2);
-  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;  // rows tr*4.., cols tc + 16*c
   for (int64_t b0 = 0; b0 < batch; b0 += kGB) {
     const int nb = (int)(batch - b0 < kGB ? batch - b0 : kGB);
     __syncthreads();
     stage_rows(ps, kp, P + ((int64_t)g * batch + b0) * K2, K2, nb, K2);
+    for (int i = nb * kp + threadIdx.x; i < kGB * kp; i += blockDim.x) ps[i] = 0.f;  // pad rows
+    for (int i = nj * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) xs[i] = 0.f;
     __syncthreads();
-    float acc[4][4] = {};
-    for (int kk = 0; kk < K2; kk += 4) {
-      float4 pv[4], xv[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) pv[r] = *reinterpret_cast<const float4 *>(ps + (tr * 4 + r) * kp + kk);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) xv[c] = *reinterpret_cast<const float4 *>(xs + (tc + 16 * c) * kp + kk);
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          acc[r][c] = fmaf(pv[r].x, xv[c].x, acc[r][c]);
-          acc[r][c] = fmaf(pv[r].y, xv[c].y, acc[r][c]);
-          acc[r][c] = fmaf(pv[r].z, xv[c].z, acc[r][c]);
-          acc[r][c] = fmaf(pv[r].w, xv[c].w, acc[r][c]);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int b = tr * 4 + r;
-      if (b >= nb) continue;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int j = tc + 16 * c;
-        if (j < nj) ghg[(b0 + b) * H + j0 + j] = acc[r][c] + (bg ? bg[j0 + j] : 0.f);
-      }
-    }
+    float acc[4][4];
+    tile64_3xtf32(ps, xs, kp, K2, acc);
+    tile64_store(acc, ghg, H, b0, nb, j0, nj, bg);
   }
 }
 
@@ -182,7 +218,7 @@ __global__ void __launch_bounds__(256) k_gates_y(int64_t batch, int H, int K2, c
 
 bool lstm_gates_ok(const Geo &g) {
   return g.reuse && g.q == g.r_dim && g.rank <= 64 && g.s * g.rank <= 256 &&
-         (g.s * g.rank) % 4 == 0 && g.n <= 1024 && g.n % 4 == 0;
+         (g.s * g.rank) % 8 == 0 && g.n <= 1024 && g.n % 4 == 0;
 }
 size_t lstm_gates_ws(const Geo &g, int64_t batch) { return (size_t)(4 * batch * g.s * g.rank * 4); }
 
@@ -231,7 +267,8 @@ struct SeqArgs {
   const __nv_bfloat16 *gx[4];  // T*B x H each (biases of the input projections included)
   float *gh;                   // 4 x B x H
   float *P;                    // 4 x B x K2
-  float *c;                    // 2 x B x H (double-buffered)
+  float *c;                    // B x H cell state
+  float *h;                    // B x H hidden state (fp32, the recurrent contractions' input)
   __nv_bfloat16 *out;          // T*B x H
   unsigned *bar;               // grid barrier counter (zeroed before launch)
   unsigned long long *trace;   // DEEPTHIN_LSTM_TRACE: globaltimer stamps (block 0, first steps)
@@ -263,20 +300,23 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
   const int B = a.B, H = a.H, n = a.n, R = a.R, K2 = a.K2;
   const int npad = n + 1, kp = K2 + 4;
   const int rgs = (B + 15) / 16;
-  const int unitsA = 4 * a.s * rgs, unitsB = 4 * ((H + 63) / 64);
-  // one phase-A and one phase-B unit per CTA when the grid covers them: their factor operands
+  const int unitsP = 4 * a.s * rgs, unitsB = 4 * ((H + 63) / 64);
+  const int64_t BH = (int64_t)B * H;
+  // one P unit and one gate-tile unit per CTA when the grid covers them: their factor operands
   // (wf_g, and the 64-column XF2_g block) stay resident in shared memory for all T steps
   float *hs = sm, *ws = hs + 16 * npad, *ps = ws + R * npad;
-  ps += (4 - ((ps - sm) & 3)) & 3;  // 16-byte alignment for the float4 tiles
+  ps += (4 - ((ps - sm) & 3)) & 3;  // 16-byte alignment for the staged tiles
   float *xs = ps + 64 * kp;
-  const bool resA = unitsA <= (int)gridDim.x, resB = unitsB <= (int)gridDim.x;
+  const bool resP = unitsP <= (int)gridDim.x, resB = unitsB <= (int)gridDim.x;
   auto wf_of = [&](int g) { return g == 0 ? a.wf[0] : g == 1 ? a.wf[1] : g == 2 ? a.wf[2] : a.wf[3]; };
   auto xf_of = [&](int g) { return g == 0 ? a.xf[0] : g == 1 ? a.xf[1] : g == 2 ? a.xf[2] : a.xf[3]; };
-  if (resA && (int)blockIdx.x < unitsA) stage_rows(ws, npad, wf_of((int)blockIdx.x / (a.s * rgs)), n, R, n);
-  if (resB && (int)blockIdx.x < unitsB) {
-    const int g = (int)blockIdx.x / ((H + 63) / 64), j0 = ((int)blockIdx.x % ((H + 63) / 64)) * 64;
-    stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, min(64, H - j0), K2);
-  }
+  auto stage_xs = [&](int u) {
+    const int g = u / ((H + 63) / 64), j0 = (u % ((H + 63) / 64)) * 64, nj = min(64, H - j0);
+    stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, nj, K2);
+    for (int i = nj * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) xs[i] = 0.f;
+  };
+  if (resP && (int)blockIdx.x < unitsP) stage_rows(ws, npad, wf_of((int)blockIdx.x / (a.s * rgs)), n, R, n);
+  if (resB && (int)blockIdx.x < unitsB) stage_xs((int)blockIdx.x);
   unsigned target = 0;
   auto stamp = [&](int t, int k) {
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 8) {
@@ -285,57 +325,30 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       a.trace[t * 4 + k] = v;
     }
   };
-  for (int t = 0; t <= a.T; ++t) {
-    // ---------------- phase A: cell of step t-1 (rows x one segment) then P of step t ----------
-    const float *cprev = a.c + (size_t)((t + 1) & 1) * B * H;
-    float *cnext = a.c + (size_t)(t & 1) * B * H;
-    for (int u = blockIdx.x; u < unitsA; u += gridDim.x) {
+  // phase C: the cell of step t (all of B x H, grid-strided; each element owned by one thread)
+  auto cell = [&](int t) {
+    const size_t gxo0 = (size_t)t * BH;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < BH;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const float zi = __bfloat162float(a.gx[0][gxo0 + e]) + a.gh[e];
+      const float zf = __bfloat162float(a.gx[1][gxo0 + e]) + a.gh[BH + e];
+      const float zg = __bfloat162float(a.gx[2][gxo0 + e]) + a.gh[2 * BH + e];
+      const float zo = __bfloat162float(a.gx[3][gxo0 + e]) + a.gh[3 * BH + e];
+      const float cn = sigm_(zf) * a.c[e] + sigm_(zi) * tanhf(zg);
+      const float hn = sigm_(zo) * tanhf(cn);
+      a.c[e] = cn;
+      a.h[e] = hn;
+      a.out[gxo0 + e] = __float2bfloat16_rn(hn);
+    }
+  };
+  for (int t = 0; t < a.T; ++t) {
+    // ---------------- phase P: P_g[rows, seg*R + k] = h[rows, seg] . wf_g[k, :] ----------------
+    for (int u = blockIdx.x; u < unitsP; u += gridDim.x) {
       const int g = u / (a.s * rgs), seg = (u / rgs) % a.s, rg = u % rgs;
       const int b0 = rg * 16, nb = min(16, B - b0);
       __syncthreads();
-      // h rows of this segment: gate pre-activations of 8 elements per thread loaded together
-      for (int i0 = threadIdx.x; i0 < nb * n; i0 += 8 * blockDim.x) {
-        float z[8][4], cp[8];
-        size_t ev[8], gv[8];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const int i = min(i0 + v * (int)blockDim.x, nb * n - 1);
-          const int b = i / n, j = seg * n + i % n;
-          ev[v] = (size_t)(b0 + b) * H + j;
-          gv[v] = ((size_t)(t > 0 ? t - 1 : 0) * B + b0 + b) * H + j;
-        }
-        if (t > 0) {
-          const size_t BH = (size_t)B * H;
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              z[v][q] = __bfloat162float(a.gx[q == 0 ? 0 : q == 1 ? 1 : q == 2 ? 2 : 3][gv[v]]) + a.gh[q * BH + ev[v]];
-            cp[v] = cprev[ev[v]];
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const int i = i0 + v * (int)blockDim.x;
-          if (i < nb * n) {
-            float h = 0.f;
-            if (t > 0) {
-              const float cn = sigm_(z[v][1]) * cp[v] + sigm_(z[v][0]) * tanhf(z[v][2]);
-              h = sigm_(z[v][3]) * tanhf(cn);
-              if (g == 0) {
-                cnext[ev[v]] = cn;
-                a.out[gv[v]] = __float2bfloat16_rn(h);
-              }
-            }
-            hs[(i / n) * npad + i % n] = h;
-          }
-        }
-      }
-      if (t == a.T) continue;  // the final cell only
-      if (!resA) {
-        __syncthreads();
-        stage_rows(ws, npad, wf_of(g), n, R, n);
-      }
+      if (!resP) stage_rows(ws, npad, wf_of(g), n, R, n);
+      stage_rows(hs, npad, a.h + (size_t)b0 * H + seg * n, H, nb, n);
       __syncthreads();
       for (int o = threadIdx.x; o < nb * R; o += blockDim.x) {
         const int b = o / R, k = o % R;
@@ -348,48 +361,25 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
         a.P[((size_t)g * B + b0 + b) * K2 + seg * R + k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
     }
-    if (t == a.T) break;
     stamp(t, 0);
     grid_barrier(a.bar, target);
-    stamp(t, 1);
-    // ---------------- phase B: gh_g[:, 64-column block] = P_g XF2_g^T + b ----------------
+    // ---------------- phase G: gh_g[:, 64-column block] = P_g XF2_g^T + b (3xTF32 mma) -----------
     for (int u = blockIdx.x; u < unitsB; u += gridDim.x) {
       const int g = u / ((H + 63) / 64), j0 = (u % ((H + 63) / 64)) * 64, nj = min(64, H - j0);
       const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
       __syncthreads();
-      if (!resB) stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, nj, K2);
+      if (!resB) stage_xs(u);
       stage_rows(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2);
+      for (int i = B * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) ps[i] = 0.f;
       __syncthreads();
-      const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
-      float acc[4][4] = {};
-      for (int kk = 0; kk < K2; kk += 4) {
-        float4 pv[4], xv[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) pv[r] = *reinterpret_cast<const float4 *>(ps + (tr * 4 + r) * kp + kk);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) xv[c] = *reinterpret_cast<const float4 *>(xs + (tc + 16 * c) * kp + kk);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            acc[r][c] = fmaf(pv[r].x, xv[c].x, acc[r][c]);
-            acc[r][c] = fmaf(pv[r].y, xv[c].y, acc[r][c]);
-            acc[r][c] = fmaf(pv[r].z, xv[c].z, acc[r][c]);
-            acc[r][c] = fmaf(pv[r].w, xv[c].w, acc[r][c]);
-          }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int b = tr * 4 + r;
-        if (b >= B) continue;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int j = tc + 16 * c;
-          if (j < nj) a.gh[((size_t)g * B + b) * H + j0 + j] = acc[r][c] + (bg ? bg[j0 + j] : 0.f);
-        }
-      }
+      float acc[4][4];
+      tile64_3xtf32(ps, xs, kp, K2, acc);
+      tile64_store(acc, a.gh + (size_t)g * BH, H, 0, B, j0, nj, bg);
     }
+    stamp(t, 1);
+    grid_barrier(a.bar, target);
     stamp(t, 2);
+    cell(t);
     grid_barrier(a.bar, target);
     stamp(t, 3);
   }
@@ -403,6 +393,7 @@ bool lstm_seq_ok(const Geo &g, int64_t batch) {
 }
 size_t lstm_seq_ws(const Geo &g, int64_t batch) {
   return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * g.s * g.rank * 4 + (size_t)2 * batch * g.q * 4 + 256;
+  // gh (4 B H) | P (4 B K2) | c, h (2 B H) | barrier
 }
 
 int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, const float *const *xf,
@@ -418,11 +409,11 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   char *cur = ws;
   a.gh = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * g.q * 4;
   a.P = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * a.K2 * 4;
-  a.c = reinterpret_cast<float *>(cur); cur += (size_t)2 * batch * g.q * 4;
+  a.c = reinterpret_cast<float *>(cur); cur += (size_t)batch * g.q * 4;
+  a.h = reinterpret_cast<float *>(cur); cur += (size_t)batch * g.q * 4;
   a.bar = reinterpret_cast<unsigned *>(cur);
   a.out = reinterpret_cast<__nv_bfloat16 *>(out);
-  // c(-1) = 0 lives in buffer 1 (read at t = 1 as cprev = c[(t+1)&1]... step 0's cell is skipped)
-  DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));
+  DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));  // c(-1) = h(-1) = 0
   DT_CUDA_CHECK(cudaMemsetAsync(a.bar, 0, 256, st));
   const size_t smem = ((size_t)(16 + a.R) * (a.n + 1) + 4 + (size_t)128 * (a.K2 + 4)) * 4;
   static bool attr = false;
@@ -433,8 +424,8 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int unitsA = 4 * a.s * ((a.B + 15) / 16), unitsB = 4 * ((a.H + 63) / 64);
-  const int grid = std::min(nsm, std::max(unitsA, unitsB));
+  const int unitsP = 4 * a.s * ((a.B + 15) / 16), unitsB = 4 * ((a.H + 63) / 64);
+  const int grid = std::min(nsm, std::max(unitsP, unitsB));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(256);
@@ -458,7 +449,7 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
     DT_CUDA_CHECK(cudaStreamSynchronize(st));
     cudaFree(a.trace);
     for (int t = 0; t < 8; ++t)
-      fprintf(stderr, "lstm step %d: A %.2f  bar1 %.2f  B %.2f  bar2 %.2f us\n", t,
+      fprintf(stderr, "lstm step %d: P %.2f  bar+G %.2f  bar %.2f  cell+bar %.2f us\n", t,
               t ? (h[t * 4] - h[t * 4 - 1]) * 1e-3 : 0.0, (h[t * 4 + 1] - h[t * 4]) * 1e-3,
               (h[t * 4 + 2] - h[t * 4 + 1]) * 1e-3, (h[t * 4 + 3] - h[t * 4 + 2]) * 1e-3);
   }
