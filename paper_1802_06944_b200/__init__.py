@@ -7,7 +7,8 @@ backed by hand-written sm_100a kernels behind a C ABI
 """
 
 from .core import make_rng, max_abs_diff, rel_error, sample_normal, spawn_rngs
-from .errors import (ArgumentError, CudaError, DeepThinError, DimensionError, ModelFormatError,
+from .errors import (ArgumentError, CudaError, DeepThinError, DimensionError, InfeasiblePlanError,
+                     ModelFormatError,
                      UnsupportedConfigurationError)
 from .factor import FactorPair, decompress, init_factors, phase, phase_count, relayout_index
 from .grad import Gradients, layer_backward, loss_and_grad
@@ -16,7 +17,8 @@ from .kernel import (ACTIVATIONS, OpCount, ReuseTable, forward_pipeline, fused_m
 from .model import DeviceModel
 from .model_io import (CompressedModel, deserialize, expected_file_size, load_model, save_model,
                        serialize)
-from .planner import LayerPlan, NetworkPlan, baseline_plan
+from .planner import (LayerPlan, NetworkPlan, baseline_plan, feasible_n_range, lower_bound_ratio,
+                      plan_layer)
 from .train import DeepThinLayer, train_step
 
 __version__ = "0.1.0"
