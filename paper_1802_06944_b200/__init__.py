@@ -19,7 +19,7 @@ from .model_io import (CompressedModel, deserialize, expected_file_size, load_mo
                        serialize)
 from .planner import (LayerPlan, NetworkPlan, baseline_plan, feasible_n_range, lower_bound_ratio,
                       plan_layer)
-from .train import DeepThinLayer, train_step
+from .train import DeepThinLayer, TrainConfig, clip_gradients, evaluate, sgd_train, train_step
 
 __version__ = "0.1.0"
 
@@ -33,4 +33,6 @@ __all__ = [
     "init_factors", "layer_backward", "layer_forward", "loss_and_grad", "make_rng",
     "max_abs_diff", "op_count", "phase", "phase_count", "predict_reuse", "rel_error",
     "relayout_index", "sample_normal", "spawn_rngs", "train_step",
+    "InfeasiblePlanError", "TrainConfig", "clip_gradients", "evaluate", "feasible_n_range",
+    "lower_bound_ratio", "plan_layer", "sgd_train",
 ]

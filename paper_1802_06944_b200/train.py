@@ -10,15 +10,17 @@ inverse re-layout, all-reduce, SGD (train.py:107-111).
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
-from .core import as_device_vector, device, stream_handle
+from .core import as_device_vector, device, make_rng, stream_handle
+from .errors import ArgumentError
 from .dist import allreduce_grads
 from .factor import FactorPair
-from .grad import backward_into, mse_grad_into
+from .grad import backward_into, loss_and_grad, mse_grad_into
 from .kernel import _act_code, forward_into
 from .planner import LayerPlan
 
@@ -73,6 +75,10 @@ class DeepThinLayer:
                       self.d_wf, self.d_bias, d_in, self.mma)
         return d_in
 
+    def grad_buffers(self):
+        """train.py:226-227: the gradient buffers the global-norm clip sees."""
+        return [self.d_xf, self.d_wf, self.d_bias]
+
     def step(self, lr: float) -> None:
         """train.py:107-111 + :221: SGD on the fp32 masters, then refresh bf16 operand copies."""
         lib = _lib.lib()
@@ -98,3 +104,88 @@ def train_step(layer: DeepThinLayer, x: torch.Tensor, target: torch.Tensor, lr: 
     allreduce_grads(layer.grad_flat, group)
     layer.step(lr)
     return ls
+
+
+# ---- multi-layer SGD trainer on the device (reference train.py:305-357) ----
+
+LOSSES = ("mse", "softmax_cross_entropy")
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """grad.py:31-51: learning rate, epochs, batch size, shuffle seed, loss, global-norm clip."""
+
+    learning_rate: float
+    epochs: int
+    batch_size: int
+    seed: int
+    loss: str = "mse"
+    clip_norm: float | None = None
+
+    def __post_init__(self):
+        if not self.learning_rate > 0:
+            raise ArgumentError(f"learning_rate must be > 0, got {self.learning_rate}")
+        if self.epochs < 1 or self.batch_size < 1:
+            raise ArgumentError("epochs and batch_size must be >= 1")
+        if self.loss not in LOSSES:
+            raise ArgumentError(f"loss must be one of {LOSSES}, got {self.loss!r}")
+        if self.clip_norm is not None and not self.clip_norm > 0:
+            raise ArgumentError(f"clip_norm must be > 0, got {self.clip_norm}")
+
+
+def clip_gradients(layers, clip_norm) -> None:
+    """train.py:318-327 on the device: global L2 norm over every layer's gradient buffers
+    (fp64, fixed order), all buffers scaled by clip/norm when norm > clip and finite. No host
+    synchronisation: the scale is computed and applied on the device."""
+    if clip_norm is None:
+        return
+    bufs = [b for layer in layers for b in layer.grad_buffers()]
+    total = torch.stack([(b.double() * b.double()).sum() for b in bufs]).sum()
+    norm = torch.sqrt(total)
+    scale = torch.where(torch.isfinite(norm) & (norm > clip_norm), clip_norm / norm,
+                        torch.ones_like(norm)).float()
+    for layer in layers:
+        layer.grad_flat.mul_(scale)
+
+
+def _forward_all(layers, x):
+    for layer in layers:
+        x = layer.forward(x)
+    return x
+
+
+def evaluate(layers, x, target, loss: str) -> float:
+    """train.py:296-301: the validation loss of the chained layers."""
+    return loss_and_grad(loss, _forward_all(layers, x), target)[0]
+
+
+def sgd_train(layers, train_data, val_data, cfg: TrainConfig):
+    """train.py:305-357 on the device: per epoch a seeded shuffle (make_rng(seed ^ 0x5DEE9),
+    the reference's stream), minibatch forward through every DeepThinLayer, loss gradient,
+    backward through the inverse re-layouts (input gradients chained), global-norm clip, SGD on
+    the fp32 masters. Returns [(epoch, train_loss, val_loss)] with diverged losses as inf."""
+    x_train, y_train = (torch.as_tensor(np.asarray(a, dtype=np.float32)).to(device())
+                        if not isinstance(a, torch.Tensor) else a for a in train_data)
+    x_val, y_val = (torch.as_tensor(np.asarray(a, dtype=np.float32)).to(device())
+                    if not isinstance(a, torch.Tensor) else a for a in val_data)
+    shuffle_rng = make_rng(cfg.seed ^ 0x5DEE9)
+    history = []
+    for epoch in range(1, cfg.epochs + 1):
+        order = torch.as_tensor(shuffle_rng.permutation(len(x_train)), device=device())
+        epoch_loss, batches = 0.0, 0
+        for start in range(0, len(order), cfg.batch_size):
+            idx = order[start:start + cfg.batch_size]
+            out = _forward_all(layers, x_train[idx])
+            loss, g = loss_and_grad(cfg.loss, out, y_train[idx])
+            for i, layer in enumerate(reversed(layers)):
+                g = layer.backward(g, need_input_grad=i + 1 < len(layers))
+            clip_gradients(layers, cfg.clip_norm)
+            for layer in layers:
+                layer.step(cfg.learning_rate)
+            epoch_loss += loss
+            batches += 1
+        train_loss = epoch_loss / batches
+        val_loss = evaluate(layers, x_val, y_val, cfg.loss)
+        history.append((epoch, train_loss if np.isfinite(train_loss) else float("inf"),
+                        val_loss if np.isfinite(val_loss) else float("inf")))
+    return history
