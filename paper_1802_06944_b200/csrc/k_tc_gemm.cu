@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int64_t ld = p.ldy;
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-              const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
               if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               yp += ld;
             }
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
               if (r < rmax) {
-                const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+                const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
                 if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               }
               yp += p.ldy;
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int64_t ld = p.ldy;
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-              const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+              const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
               if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               yp += ld;
             }
@@ -1085,7 +1085,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
               if (r < rmax) {
-                const float o = act_fast<ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
+                const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[r]) + bias_j, p.arg);
                 if constexpr (YDT == DT_BF16) *yp = __float2bfloat16_rn(o); else *yp = o;
               }
               yp += p.ldy;

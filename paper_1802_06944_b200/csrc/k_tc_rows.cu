@@ -77,20 +77,12 @@ __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
   }
 }
 
-__device__ __forceinline__ float tanh_approx(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// bf16 outputs: one MUFU op per element (tanh.approx, relative error 2^-11: <= 2.5e-4 absolute
-// on a sigmoid, below the bf16 output's own rounding of up to 2^-9 relative); fp32 outputs:
-// act_fast (ex2 + rcp, ~1e-7).
+// bf16 outputs: one MUFU op per element (act.cuh tanh_approx); the launcher pre-scales XF2p and
+// the bias by 1/2 for the bf16 sigmoid, so z here is already z/2
 template <int YDT, int ACT>
 __device__ __forceinline__ float act_out(float z, float arg) {
-  // the launcher pre-scales XF2p and the bias by 1/2 for this case: z here is already z/2
   if constexpr (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_approx(z), 0.5f);
-  if constexpr (YDT == DT_BF16 && ACT == DT_ACT_TANH) return tanh_approx(z);
-  return act_fast<ACT>(z, arg);
+  return act_out_bf16<YDT, ACT>(z, arg);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
