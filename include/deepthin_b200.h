@@ -189,6 +189,16 @@ int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_str
 size_t dt_rows_prepared_bytes(const dt_plan *plan, int x_dtype, int y_dtype);
 int dt_rows_prepare(const dt_plan *plan, int act, int y_dtype, const float *xf, const float *wf,
                     const float *bias, void *out, dt_stream stream);
+/* Layer chaining of consecutive row-tile layers (this thread, the NEXT dt_forward with
+ * DT_FACTORS_ROWS only): instead of waiting for the whole previous kernel, the launch loads
+ * 128-row tile t of x once ((unsigned *)wait_flags)[t] >= wait_target, and its epilogue warps
+ * add 1 to ((unsigned *)post_flags)[t] (release) after storing their part of tile t —
+ * dt_rows_posts_per_tile(plan) additions per tile per launch. wait_flags / post_flags may be
+ * NULL. The caller keeps the flags monotone across calls (targets grow by the producer's posts
+ * per tile each forward) and must not let a layer write a buffer that an earlier, still
+ * running layer reads in rows it has not finished (three rotating activation buffers). */
+int dt_rows_chain(const void *wait_flags, unsigned wait_target, void *post_flags);
+int dt_rows_posts_per_tile(const dt_plan *plan);
 /* The four recurrent gate contractions of one LSTM step (BASELINE config 4): gh[g] = h @ W_g +
  * bias[g] for four DeepThin layers sharing one square reuse geometry (plan: q == r_dim, n | q),
  * h fp32 (batch x q), exact fp32 on the CUDA cores in the reference's factored reuse form

@@ -428,6 +428,18 @@ int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_str
   return launch_sgd(count, param, grad, lr, (cudaStream_t)stream);
 }
 
+int dt_rows_chain(const void *wait_flags, unsigned wait_target, void *post_flags) {
+  rows_chain(reinterpret_cast<const unsigned *>(wait_flags), wait_target,
+             reinterpret_cast<unsigned *>(post_flags));
+  return DT_OK;
+}
+
+int dt_rows_posts_per_tile(const dt_plan *plan) {
+  Geo g;
+  if (make_geo(plan, &g)) return 0;
+  return rows_posts_per_tile(g);
+}
+
 size_t dt_rows_prepared_bytes(const dt_plan *plan, int x_dtype, int y_dtype) {
   Geo g;
   if (make_geo(plan, &g) || !tc_rows_ok(g, x_dtype, y_dtype)) return 0;

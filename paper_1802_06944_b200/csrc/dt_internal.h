@@ -91,6 +91,9 @@ size_t tc_rows_ws(const Geo &g);
 int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
                     const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
                     cudaStream_t st, bool prepared = false);
+// layer chaining for the next tc_rows_forward on this thread (prepared operands only)
+void rows_chain(const unsigned *wait, unsigned target, unsigned *post);
+int rows_posts_per_tile(const Geo &g);
 int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float *bias, int act,
                     int y_dtype, char *ws, cudaStream_t st);
 

@@ -66,7 +66,22 @@ struct RowsParams {
   int bslot;  // K slot carrying the bias (P = 1 there, XF2p = bias * scale), -1: epilogue adds it
   uint32_t off_x, off_a2, off_wf, off_b, off_out, off_bar;
   unsigned long long *trace;  // DEEPTHIN_ROWS_TRACE: globaltimer stamps of cluster 0
+  // layer chaining (dt_rows_chain): x row tile t is loaded once wait_flags[t] >= wait_target
+  // (the previous layer's epilogue warps post to it) instead of after the whole previous grid;
+  // this layer's epilogue warps post their finished tiles to post_flags
+  const unsigned *wait_flags;
+  unsigned wait_target;
+  unsigned *post_flags;
 };
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 constexpr int kTr = 64;  // trace slots per CTA
 __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
@@ -189,7 +204,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   if (threadIdx.x == 0) rtrace(p, 0);
   // Everything below reads buffers an earlier kernel on the stream may write (x is the previous
   // layer's output; factors/bias may come from an SGD step): wait for it, let the next start.
-  griddep_wait();
+  // (chained layers wait per row tile on the previous layer's flags instead, in the x producer)
+  if (!p.wait_flags) griddep_wait();
   griddep_launch_dependents();
 
   const int n = p.nkb * 64;
@@ -204,7 +220,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tma_load_2d(wf_s + kb * p.np * 128, &tm_wf, wf_full, kb * 64, 0);
       int st = 0;
       uint32_t ph = 0;
-      for (int t = cid; t < p.n_tiles; t += ncl)
+      for (int t = cid; t < p.n_tiles; t += ncl) {
+        if (p.wait_flags) {  // rows of tile t written (and released) by the previous layer
+          uint32_t spins = 0;
+          while (ld_acquire_u32(p.wait_flags + t) < p.wait_target) {
+            if (++spins == (1u << 28)) {
+              printf("deepthin: layer-chain flag timeout (tile %d)\n", t);
+              __trap();
+            }
+          }
+          fence_proxy_async_global();  // the TMA (async proxy) reads below see those writes
+        }
         for (int seg = crank; seg < p.s; seg += cs)
           for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(&x_empty[st], ph ^ 1);
@@ -212,6 +238,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             tma_load_2d(smem + p.off_x + st * kXBytes, &tm_x, &x_full[st], seg * n + kb * 64, t * kTM);
             if (++st == p.xs) { st = 0; ph ^= 1; }
           }
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -605,6 +632,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         __syncwarp();
       }
+      if (p.post_flags) {  // this warp's stores of tile t are done: release them to the next layer
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          red_release_add(p.post_flags + t, 1u);
+        }
+      }
     }
     if (warp == 3 + kPW) rtrace(p, 40);
     }
@@ -722,6 +756,19 @@ int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float 
   return check_launch("rows_prep");
 }
 
+namespace {
+thread_local const unsigned *g_chain_wait = nullptr;
+thread_local unsigned g_chain_target = 0;
+thread_local unsigned *g_chain_post = nullptr;
+}  // namespace
+
+void rows_chain(const unsigned *wait, unsigned target, unsigned *post) {
+  g_chain_wait = wait;
+  g_chain_target = target;
+  g_chain_post = post;
+}
+int rows_posts_per_tile(const Geo &g) { return rows_cluster(g) * kEpi; }
+
 int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
                     const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
                     cudaStream_t st, bool prepared) {
@@ -746,6 +793,15 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.bias = bias;
   p.y = y;
   p.arg = act_arg;
+  // one-shot chain request (dt_rows_chain), honoured only with prepared operands (a per-call
+  // prep kernel would itself be the dependency)
+  if (prepared) {
+    p.wait_flags = g_chain_wait;
+    p.wait_target = g_chain_target;
+    p.post_flags = g_chain_post;
+  }
+  g_chain_wait = nullptr;
+  g_chain_post = nullptr;
   // a zero K slot for the bias: the rank padding of segment 0, else an all-zero pad chunk
   p.bslot = !bias ? -1 : (g.rank < p.rp ? (int)g.rank : (p.k2 > g.s * p.rp ? (int)(g.s * p.rp) : -1));
   p.pcols = (int)((g.s / p.cs) * p.np);

@@ -88,6 +88,11 @@ class DeviceModel:
         torch.cuda.current_stream().synchronize()  # the image (and staging) can go now
         del img, staging
         self._ws = [None] * count
+        # per-row-tile layer chaining (see forward): exact, but measured no faster at config 3
+        # (its clusters of 8 only launch on SMs the previous layer's clusters free, which all
+        # finish within ~one tile of each other), and it costs host time: off by default
+        self.chain = False
+        self._chain_key = None
 
     @property
     def plans(self):
@@ -105,6 +110,18 @@ class DeviceModel:
         lib = _lib.lib()
         batch = xt.shape[0]
         last = len(self.factors) - 1
+        # Row-tile layers with prepared operands chain on per-row-tile flags (dt_rows_chain):
+        # layer i+1 loads rows layer i has finished while layer i still runs, so intermediate
+        # activations rotate over three persistent buffers (a layer never overwrites rows an
+        # earlier, still-running layer reads).
+        ydt = lambda i: out_dtype if i == last else mid
+        rows = [code == _lib.DT_MMA_BF16 and self.chain and
+                fp.rows_prepared(b, c, _lib.DT_BF16 if ydt(i) == torch.bfloat16 else _lib.DT_F32)
+                is not None and (i > 0 or xt.dtype == torch.bfloat16)
+                for i, (fp, b, c) in enumerate(zip(self.factors, self.biases, self.codes))]
+        bufs = flags = None
+        if any(rows[i] and rows[i - 1] for i in range(1, last + 1)):
+            bufs, flags = self._chain_state(batch, mid)
         with forward_pipeline(self.pipeline and self.mma == "bf16"):
             for i, (fp, bias) in enumerate(zip(self.factors, self.biases)):
                 need = lib.dt_forward_workspace_bytes(C.byref(_lib.plan_struct(fp.plan)), batch,
@@ -112,11 +129,37 @@ class DeviceModel:
                 if self._ws[i] is None or self._ws[i].numel() < need:
                     self._ws[i] = torch.empty(max(need, 256), dtype=torch.uint8,
                                               device=xt.device)
-                y = torch.empty((batch, fp.plan.r_dim), device=xt.device,
-                                dtype=out_dtype if i == last else mid)
+                if bufs is not None and i < last:
+                    y = bufs[(i + 1) % 3][: batch * fp.plan.r_dim].view(batch, fp.plan.r_dim)
+                else:
+                    y = torch.empty((batch, fp.plan.r_dim), device=xt.device, dtype=ydt(i))
+                if bufs is not None and rows[i]:
+                    wait = target = 0
+                    if i > 0 and rows[i - 1]:
+                        wait = flags[i - 1].data_ptr()
+                        target = self._epoch * self._posts[i - 1]
+                    post = flags[i].data_ptr() if i < last and rows[i + 1] else None
+                    _lib.check(lib.dt_rows_chain(wait or None, target, post))
                 forward_into(xt, fp, bias, self.codes[i], self.act_args[i], y, code,
                              ws=self._ws[i], cached=True)
                 xt = y
+        if bufs is not None:
+            self._epoch += 1
         return xt.float().cpu().numpy() if host else xt
+
+    def _chain_state(self, batch, mid):
+        """Three rotating activation buffers and per-layer tile flags for this batch size."""
+        key = (batch, mid)
+        if self._chain_key != key:
+            width = max(fp.plan.r_dim for fp in self.factors)
+            dev = self.factors[0].xf.device
+            self._bufs = [torch.empty(batch * width, dtype=mid, device=dev) for _ in range(3)]
+            tiles = -(-batch // 128)
+            self._flags = [torch.zeros(tiles, dtype=torch.int32, device=dev) for _ in self.factors]
+            self._posts = [_lib.lib().dt_rows_posts_per_tile(C.byref(_lib.plan_struct(fp.plan)))
+                           for fp in self.factors]
+            self._epoch = 1
+            self._chain_key = key
+        return self._bufs, self._flags
 
     __call__ = forward

@@ -158,3 +158,22 @@ def test_chain_and_argument_errors(dthn):
     dm = model.to_device(ACTS, mma="ffma")
     with pytest.raises(D.DimensionError):
         dm.forward(np.zeros((4, 13)))
+
+
+def test_row_tile_layer_chaining_is_exact():
+    """Chained row-tile layers (per-tile flags, dt_rows_chain, three rotating activation
+    buffers) give the unchained chain's bits, across repeated forwards (monotone flag epochs)
+    and a second batch size."""
+    model = mi.deserialize(mi.serialize(config3_like(layers=4)))
+    acts = ["sigmoid"] * 4 + ["softmax"]
+    dm = model.to_device(acts, mma="bf16")
+    for rows in (1000, 384):
+        x = torch.randn(rows, 440, device="cuda").to(torch.bfloat16)
+        dm.chain = False
+        want = dm.forward(x, out_dtype=torch.bfloat16).clone()
+        dm.chain = True
+        for _ in range(3):
+            got = dm.forward(x, out_dtype=torch.bfloat16)
+            torch.cuda.synchronize()
+            assert torch.equal(got, want)
+        dm.chain = False
