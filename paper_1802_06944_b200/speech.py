@@ -226,6 +226,7 @@ class SpeechRNN:
         for name in ("fc1", "fc2", "fc3"):
             h = self._dense(name, h, "clipped_relu")
         gx = [self._dense(f"x_{g}", h, "identity") for g in GATES]
+        self._last_gx = gx  # kept for measurement (bench.py times the recurrence alone)
         seq = self._sequence(gx, T, B) if persistent else None
         if seq is None:
             seq = self._recurrence(gx, T, B, graph=graph)
