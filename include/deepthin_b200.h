@@ -158,6 +158,13 @@ int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int 
                 const float *xf, const float *wf, const float *bias, int act, float act_arg,
                 const float *upstream, float *d_xf, float *d_wf, float *d_bias,
                 float *d_input, void *workspace, size_t workspace_bytes, dt_stream stream);
+/* dt_backward with p_in (nullable): the P that dt_forward_mse_ex kept for these x and factors
+ * (tensor-core backward of reuse geometries only). d_bias may be NULL to skip the column sums
+ * (already produced by dt_forward_mse_ex). */
+int dt_backward_ex(const dt_plan *plan, int64_t batch, int mma, const void *x, int x_dtype,
+                   const float *xf, const float *wf, const float *bias, int act, float act_arg,
+                   const float *upstream, float *d_xf, float *d_wf, float *d_bias, float *d_input,
+                   const float *p_in, void *workspace, size_t workspace_bytes, dt_stream stream);
 
 /* grad.py:98-103 loss_and_grad("mse") for one shard of rows:
  *   grad = 2 (y - t) / norm_count;  loss_sum[0] = sum (y - t)^2  (fp64, fixed order).
@@ -177,6 +184,15 @@ int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtyp
                    const float *wf, const float *bias, const float *target, double norm_count,
                    float *grad, double *loss_sum, void *workspace, size_t workspace_bytes,
                    dt_stream stream);
+/* dt_forward_mse plus two outputs for the step that follows (both nullable):
+ *   d_bias (r_dim fp32): the column sums of grad (grad.py:85), computed in the loss pass;
+ *   p_out (dt_forward_p_bytes bytes, reuse geometries only): the factored forward's
+ *     P = x.view(B*s, n) @ wf^T (fp32), for dt_backward_ex to reuse instead of recomputing. */
+size_t dt_forward_p_bytes(const dt_plan *plan, int64_t batch);
+int dt_forward_mse_ex(const dt_plan *plan, int64_t batch, const void *x, int x_dtype,
+                      const float *xf, const float *wf, const float *bias, const float *target,
+                      double norm_count, float *grad, double *loss_sum, float *d_bias,
+                      float *p_out, void *workspace, size_t workspace_bytes, dt_stream stream);
 
 /* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);

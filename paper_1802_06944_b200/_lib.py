@@ -26,7 +26,7 @@ EXPORTS = (
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
-    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_sgd_step", "dt_rows_prepared_bytes", "dt_rows_prepare", "dt_rows_chain", "dt_rows_posts_per_tile", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_sequence_workspace_bytes", "dt_lstm_sequence", "dt_lstm_cell", "dt_session_create",
+    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_forward_mse_ex", "dt_forward_p_bytes", "dt_backward_ex", "dt_sgd_step", "dt_rows_prepared_bytes", "dt_rows_prepare", "dt_rows_chain", "dt_rows_posts_per_tile", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_sequence_workspace_bytes", "dt_lstm_sequence", "dt_lstm_cell", "dt_session_create",
     "dt_session_forward", "dt_session_destroy", "dt_model_parse", "dt_unpack_values",
 )
 
@@ -88,6 +88,8 @@ def _declare(lib):
         "dt_set_forward_pipeline": ([i], i),
         "dt_forward_mse_workspace_bytes": ([P, I64], SZ),
         "dt_forward_mse": ([P, I64, VP, i, VP, VP, VP, VP, D, VP, VP, VP, SZ, VP], i),
+        "dt_forward_mse_ex": ([P, I64, VP, i, VP, VP, VP, VP, D, VP, VP, VP, VP, VP, SZ, VP], i),
+        "dt_forward_p_bytes": ([P, I64], SZ),
         "dt_plan_validate": ([P], i),
         "dt_plan_query": ([P, C.POINTER(PlanInfo)], i),
         "dt_phase": ([P, I64, C.POINTER(I64)], i),
@@ -102,6 +104,7 @@ def _declare(lib):
         "dt_forward": ([P, I64, i, VP, i, VP, VP, i, VP, i, F, VP, i, VP, SZ, VP], i),
         "dt_backward_workspace_bytes": ([P, I64, i], SZ),
         "dt_backward": ([P, I64, i, VP, i, VP, VP, VP, i, F, VP, VP, VP, VP, VP, VP, SZ, VP], i),
+        "dt_backward_ex": ([P, I64, i, VP, i, VP, VP, VP, i, F, VP, VP, VP, VP, VP, VP, VP, SZ, VP], i),
         "dt_mse_workspace_bytes": ([I64, I64], SZ),
         "dt_mse_grad": ([I64, I64, VP, VP, D, VP, VP, VP, SZ, VP], i),
         "dt_sgd_step": ([I64, VP, VP, F, VP], i),

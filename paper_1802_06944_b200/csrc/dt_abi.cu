@@ -341,6 +341,14 @@ int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int 
                 const float *xf, const float *wf, const float *bias, int act, float act_arg,
                 const float *upstream, float *d_xf, float *d_wf, float *d_bias, float *d_input,
                 void *workspace, size_t workspace_bytes, dt_stream stream) {
+  return dt_backward_ex(plan, batch, mma, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf,
+                        d_wf, d_bias, d_input, nullptr, workspace, workspace_bytes, stream);
+}
+
+int dt_backward_ex(const dt_plan *plan, int64_t batch, int mma, const void *x, int x_dtype,
+                   const float *xf, const float *wf, const float *bias, int act, float act_arg,
+                   const float *upstream, float *d_xf, float *d_wf, float *d_bias, float *d_input,
+                   const float *p_in, void *workspace, size_t workspace_bytes, dt_stream stream) {
   Geo g;
   if (int rc = make_geo(plan, &g)) return rc;
   if (batch < 0) {
@@ -365,7 +373,12 @@ int dt_backward(const dt_plan *plan, int64_t batch, int mma, const void *x, int 
   // fp32 FFMA backward
   if (mma == DT_MMA_BF16 && tc_backward_ok(g))
     return tc_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
-                       d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
+                       d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream,
+                       p_in);
+  if (p_in) {
+    set_error("backward: a kept P applies to the tensor-core backward of reuse geometries only");
+    return DT_E_UNSUPPORTED;
+  }
   return ffma_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
                        d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
 }
@@ -380,6 +393,20 @@ int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtyp
                    const float *wf, const float *bias, const float *target, double norm_count,
                    float *grad, double *loss_sum, void *workspace, size_t workspace_bytes,
                    dt_stream stream) {
+  return dt_forward_mse_ex(plan, batch, x, x_dtype, xf, wf, bias, target, norm_count, grad,
+                           loss_sum, nullptr, nullptr, workspace, workspace_bytes, stream);
+}
+
+size_t dt_forward_p_bytes(const dt_plan *plan, int64_t batch) {
+  Geo g;
+  if (make_geo(plan, &g) || batch < 0 || !tc_backward_ok(g)) return 0;
+  return (size_t)batch * g.s * g.rank * 4;
+}
+
+int dt_forward_mse_ex(const dt_plan *plan, int64_t batch, const void *x, int x_dtype,
+                      const float *xf, const float *wf, const float *bias, const float *target,
+                      double norm_count, float *grad, double *loss_sum, float *d_bias,
+                      float *p_out, void *workspace, size_t workspace_bytes, dt_stream stream) {
   Geo g;
   if (int rc = make_geo(plan, &g)) return rc;
   if (batch < 0) {
@@ -396,7 +423,8 @@ int dt_forward_mse(const dt_plan *plan, int64_t batch, const void *x, int x_dtyp
     return DT_E_ARG;
   }
   return tc_forward_mse(g, batch, x, x_dtype, xf, wf, bias, target, 2.0 / norm_count, grad,
-                        loss_sum, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
+                        loss_sum, (char *)workspace, workspace_bytes, (cudaStream_t)stream, d_bias,
+                        p_out);
 }
 
 size_t dt_mse_workspace_bytes(int64_t rows, int64_t cols) { return mse_ws(rows, cols); }

@@ -108,10 +108,14 @@ size_t tc_gemm_ws(const Geo &g, int64_t batch);
 // grad = scale * (x W + b - target), loss_sum = fixed-order fp64 sum of squared errors.
 int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
                    const float *wf, const float *bias, const float *target, double scale,
-                   float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st);
+                   float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st,
+                   float *d_bias = nullptr, float *p_out = nullptr);
 size_t tc_forward_mse_ws(const Geo &g, int64_t batch);
 int launch_sum_f64(int64_t count, const double *part, double *out, cudaStream_t st);
 // fixed-order fp64 sum of (g * inv)^2 (part: mse_ws(1, count) bytes), out nullable
+// one pass over g (rows x cols): column sums into out (fixed order) and sum (g*inv)^2 into loss
+int launch_colsum_sumsq(int64_t rows, int64_t cols, const float *g, double inv, float *out,
+                        float *cpart, double *sq_part, double *loss, cudaStream_t st);
 int launch_sumsq(int64_t count, const float *g, double inv, double *part, double *out, cudaStream_t st);
 // Tensor-core backward of reuse geometries in factored form (cuBLASLt for the plain GEMMs over
 // transposed views); returns DT_E_UNSUPPORTED when the geometry does not qualify.
@@ -119,7 +123,7 @@ bool tc_backward_ok(const Geo &g);
 int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
                 const float *wf, const float *bias, int act, float act_arg,
                 const float *upstream, float *d_xf, float *d_wf, float *d_bias, float *d_input,
-                char *ws, size_t ws_bytes, cudaStream_t st);
+                char *ws, size_t ws_bytes, cudaStream_t st, const float *p_in = nullptr);
 size_t tc_backward_ws(const Geo &g, int64_t batch);
 
 // dt_profile_kernel_events: events to record around the next dominant-kernel launch on this

@@ -248,6 +248,32 @@ __global__ void k_colsum_partial(int64_t rows, int64_t cols, int64_t rows_per_ch
   for (int64_t r = r0; r < r1; ++r) s += g[r * cols + j];
   part[(int64_t)blockIdx.y * cols + j] = s;
 }
+// column partial sums (as k_colsum_partial) fused with a fixed-order fp64 sum of (g*inv)^2
+__global__ void __launch_bounds__(256) k_colsum_sq_partial(int64_t rows, int64_t cols, int64_t rpc,
+                                                           const float *g, double inv, float *part,
+                                                           double *sq_part) {
+  __shared__ double red[256];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * rpc, r1 = min(rows, r0 + rpc);
+  float s = 0.f;
+  double q = 0.0;
+  if (j < cols) {
+    for (int64_t r = r0; r < r1; ++r) {
+      const float v = g[r * cols + j];
+      s += v;
+      const double d = v * inv;
+      q += d * d;
+    }
+    part[(int64_t)blockIdx.y * cols + j] = s;
+  }
+  red[threadIdx.x] = q;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sq_part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = red[0];
+}
 __global__ void k_colsum_final(int64_t cols, int chunks, const float *part, float *out) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cols) return;
@@ -880,6 +906,23 @@ int launch_mse_grad(int64_t rows, int64_t cols, const float *y, const float *t, 
     return check_launch("mse_sum");
   }
   return DT_OK;
+}
+
+int launch_colsum_sumsq(int64_t rows, int64_t cols, const float *g, double inv, float *out,
+                        float *cpart, double *sq_part, double *loss, cudaStream_t st) {
+  const int chunks = (int)std::max<int64_t>(1, (rows + 255) / 256);
+  dim3 grid(blocks_for(cols), (unsigned)chunks);
+  if ((int64_t)grid.x * grid.y > 1184) {  // the sq partials share the sumsq partial buffer
+    set_error("colsum_sumsq: too many blocks for the partial buffer");
+    return DT_E_UNSUPPORTED;
+  }
+  k_colsum_sq_partial<<<grid, 256, 0, st>>>(rows, cols, 256, g, inv, cpart, sq_part);
+  if (int rc = check_launch("colsum_sumsq")) return rc;
+  k_colsum_final<<<blocks_for(cols), 256, 0, st>>>(cols, chunks, cpart, out);
+  if (int rc = check_launch("colsum_final")) return rc;
+  if (!loss) return DT_OK;
+  k_sum_f64<<<1, 256, 0, st>>>((int64_t)grid.x * grid.y, sq_part, loss);
+  return check_launch("sumsq_sum");
 }
 
 int launch_sumsq(int64_t count, const float *g, double inv, double *part, double *out, cudaStream_t st) {

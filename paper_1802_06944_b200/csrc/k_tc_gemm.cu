@@ -1482,7 +1482,9 @@ struct MseArgs {
   const float *target;
   double scale;
   double *loss_sum;
-  double *part;  // workspace for the per-warp partials
+  double *part;     // workspace for the per-warp partials
+  float *d_bias;    // nullable: the column sums of grad (grad.py:85) in the loss pass
+  float *p_out;     // nullable: keep P (B x s*rank fp32) for the backward
 };
 static int64_t mse_parts_bound(const Geo &g, int64_t batch) {
   return ((g.r_dim + GM - 1) / GM + 2) * ((batch + GN - 1) / GN) * kEpiWarps;
@@ -1519,12 +1521,18 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
 
 size_t tc_forward_mse_ws(const Geo &g, int64_t batch) {
   return tc_gemm_ws(g, batch) + (size_t)round_up(mse_parts_bound(g, batch) * 8, 256) +
-         (size_t)round_up(g.r_dim * 4, 256) + (size_t)round_up(1184 * 8, 256) + kLtWsFwd;
+         (size_t)round_up(g.r_dim * 4, 256) + (size_t)round_up(1184 * 8, 256) + kLtWsFwd +
+         (size_t)round_up(colsum_ws(batch, g.r_dim), 256);
 }
 
 int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
                    const float *wf, const float *bias, const float *target, double scale,
-                   float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st) {
+                   float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st,
+                   float *d_bias, float *p_out) {
+  if (p_out && !(reuse_factored_ok(g))) {
+    set_error("forward_mse: P is kept only on reuse geometries (factored path)");
+    return DT_E_UNSUPPORTED;
+  }
   if (ws_bytes < tc_forward_mse_ws(g, batch)) {
     set_error("forward+mse workspace too small: need " + std::to_string(tc_forward_mse_ws(g, batch)));
     return DT_E_ARG;
@@ -1534,9 +1542,15 @@ int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, cons
     return DT_OK;
   }
   const size_t base = tc_gemm_ws(g, batch);
-  MseArgs m{target, scale, loss_sum, reinterpret_cast<double *>(ws + base)};
-  return tc_forward_impl(g, batch, x, x_dtype, xf, wf, DT_F32, bias, DT_ACT_IDENTITY, 0.f, grad,
-                         YDT_MSE, ws, base, st, &m);
+  MseArgs m{target, scale, loss_sum, reinterpret_cast<double *>(ws + base), d_bias, p_out};
+  int rc = tc_forward_impl(g, batch, x, x_dtype, xf, wf, DT_F32, bias, DT_ACT_IDENTITY, 0.f, grad,
+                           YDT_MSE, ws, base, st, &m);
+  if (rc == DT_OK && m.d_bias) {  // paths without the fused column sums: a separate pass
+    char *tail = ws + base + round_up(mse_parts_bound(g, batch) * 8, 256) + round_up(g.r_dim * 4, 256) +
+                 round_up(1184 * 8, 256);
+    rc = launch_colsum(batch, g.r_dim, grad, d_bias, reinterpret_cast<float *>(tail), st);
+  }
+  return rc;
 }
 
 static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dtype,
@@ -1594,6 +1608,7 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
       xt = x_ws;
     }
     const int64_t SR = g.s * g.rank;
+    if (mse && mse->p_out) P = mse->p_out;  // kept for the backward (dt_backward_ex)
     GemmCall c1{xt, g.n, batch * g.s, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
                 P, g.rank, DT_F32, nullptr, false, 0};
     if (int rc = run_gemm(c1, st)) return rc;
@@ -1611,6 +1626,16 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
                               mse->target, reinterpret_cast<float *>(y), g.r_dim, sc, -sc, bs, lws,
                               kLtWsFwd))
         return rc;
+      if (mse->d_bias) {  // one pass over grad: column sums (d_bias) and the loss
+        float *cpart = reinterpret_cast<float *>(reinterpret_cast<char *>(lws) + kLtWsFwd);
+        const int rc = launch_colsum_sumsq(batch, g.r_dim, reinterpret_cast<const float *>(y),
+                                           1.0 / mse->scale, mse->d_bias, cpart, sq_part,
+                                           mse->loss_sum, st);
+        if (rc != DT_E_UNSUPPORTED) {
+          const_cast<MseArgs *>(mse)->d_bias = nullptr;  // done (no separate pass)
+          return rc;
+        }
+      }
       return launch_sumsq(batch * g.r_dim, reinterpret_cast<const float *>(y), 1.0 / mse->scale,
                           sq_part, mse->loss_sum, st);
     }
@@ -1816,7 +1841,7 @@ size_t tc_backward_ws(const Geo &g, int64_t batch) {
 int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
                 const float *wf, const float *bias, int act, float act_arg,
                 const float *up, float *d_xf, float *d_wf, float *d_bias, float *d_input,
-                char *ws, size_t ws_bytes, cudaStream_t st) {
+                char *ws, size_t ws_bytes, cudaStream_t st, const float *p_in) {
   if (!tc_backward_ok(g)) {
     set_error("tensor-core backward: reuse geometries with n % 8 == 0 and s*rank % 4 == 0");
     return DT_E_UNSUPPORTED;
@@ -1871,9 +1896,13 @@ int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const f
     xt = x16;
   }
   if (int rc = launch_cast_bf16(g.rank * g.n, wf, reinterpret_cast<uint16_t *>(wf16), st)) return rc;
-  GemmCall c1{xt, g.n, Bs, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
-              P, g.rank, DT_F32, nullptr, false, 0};
-  if (int rc = run_gemm(c1, st)) return rc;
+  if (p_in) {  // P kept by the forward (dt_forward_mse_ex)
+    P = const_cast<float *>(p_in);
+  } else {
+    GemmCall c1{xt, g.n, Bs, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
+                P, g.rank, DT_F32, nullptr, false, 0};
+    if (int rc = run_gemm(c1, st)) return rc;
+  }
   // dXF2 (r_dim x SR) = g^T @ P'  -> d_xf's first r_dim*s rows; the discarded tail gets 0
   if (int rc = lt_gemm(st, g.r_dim, SR, batch, gp, true, g.r_dim, P, false, SR, d_xf, SR,
                        CUDA_R_32F, 0.f, ltws, kLtWs))

@@ -35,20 +35,22 @@ class Gradients:
 
 def backward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float,
                   upstream: torch.Tensor, d_xf: torch.Tensor, d_wf: torch.Tensor,
-                  d_bias: torch.Tensor | None, d_input: torch.Tensor | None, mma: int) -> None:
-    """Raw stream-ordered dt_backward on device tensors."""
+                  d_bias: torch.Tensor | None, d_input: torch.Tensor | None, mma: int,
+                  p_in: torch.Tensor | None = None) -> None:
+    """Raw stream-ordered dt_backward(_ex) on device tensors; p_in: the P the forward kept."""
     p = fp.plan
     lib = _lib.lib()
     ps = _lib.plan_struct(p)
     batch = x.shape[0]
     ws = workspace(lib.dt_backward_workspace_bytes(C.byref(ps), batch, mma))
-    _lib.check(lib.dt_backward(
+    _lib.check(lib.dt_backward_ex(
         C.byref(ps), batch, mma, x.data_ptr(),
         _lib.DT_BF16 if x.dtype == torch.bfloat16 else _lib.DT_F32,
         fp.xf.data_ptr(), fp.wf.data_ptr(), bias.data_ptr() if bias is not None else None,
         act, float(act_arg), upstream.data_ptr(), d_xf.data_ptr(), d_wf.data_ptr(),
         d_bias.data_ptr() if d_bias is not None else None,
         d_input.data_ptr() if d_input is not None else None,
+        p_in.data_ptr() if p_in is not None else None,
         ws.data_ptr(), ws.numel(), stream_handle()))
 
 

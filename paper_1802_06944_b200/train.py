@@ -44,15 +44,18 @@ class DeepThinLayer:
 
     def forward(self, x: torch.Tensor, out_dtype=torch.float32) -> torch.Tensor:
         self._x = x
+        self._p = None
         y = torch.empty((x.shape[0], self.plan.r_dim), dtype=out_dtype, device=x.device)
         forward_into(x, self.fp, self.bias, self.act, self.act_arg, y, self.mma)
         return y
 
     def forward_mse(self, x: torch.Tensor, target: torch.Tensor, norm_count: float,
-                    loss_out: torch.Tensor) -> torch.Tensor:
+                    loss_out: torch.Tensor, keep_for_backward: bool = False) -> torch.Tensor:
         """Forward + MSE gradient in one pass (dt_forward_mse, identity activation, bf16 path):
         returns grad = 2 (y - target) / norm_count; loss_out[0] = sum (y - target)^2. y itself
-        is never written (grad.py:98-103 fused into the contraction's epilogue)."""
+        is never written (grad.py:98-103 fused into the contraction's epilogue).
+        keep_for_backward (reuse geometries): the loss pass also produces d_bias (grad.py:85)
+        and the forward's P is kept, so the next backward() skips both (dt_forward_mse_ex)."""
         self._x = x
         lib = _lib.lib()
         ps = _lib.plan_struct(self.plan)
@@ -61,18 +64,27 @@ class DeepThinLayer:
         ws = workspace(lib.dt_forward_mse_workspace_bytes(C.byref(ps), batch))
         g = torch.empty((batch, self.plan.r_dim), dtype=torch.float32, device=x.device)
         tgt = target.contiguous().float()
-        _lib.check(lib.dt_forward_mse(
+        self._p = None
+        pbytes = lib.dt_forward_p_bytes(C.byref(ps), batch) if keep_for_backward else 0
+        if pbytes:
+            self._p = torch.empty(pbytes // 4, dtype=torch.float32, device=x.device)
+        _lib.check(lib.dt_forward_mse_ex(
             C.byref(ps), batch, x.data_ptr(), _lib.DT_BF16 if x.dtype == torch.bfloat16 else _lib.DT_F32,
             self.fp.xf.data_ptr(), self.fp.wf.data_ptr(), self.bias.data_ptr(), tgt.data_ptr(),
-            float(norm_count), g.data_ptr(), loss_out.data_ptr(), ws.data_ptr(), ws.numel(),
+            float(norm_count), g.data_ptr(), loss_out.data_ptr(),
+            self.d_bias.data_ptr() if self._p is not None else None,
+            self._p.data_ptr() if self._p is not None else None, ws.data_ptr(), ws.numel(),
             stream_handle()))
         return g
 
     def backward(self, upstream: torch.Tensor, need_input_grad: bool = False):
         d_in = (torch.empty((self._x.shape[0], self.plan.q), dtype=torch.float32, device=self._x.device)
                 if need_input_grad else None)
+        kept = getattr(self, "_p", None)  # forward_mse(keep_for_backward=True): P and d_bias done
         backward_into(self._x, self.fp, self.bias, self.act, self.act_arg, upstream, self.d_xf,
-                      self.d_wf, self.d_bias, d_in, self.mma)
+                      self.d_wf, None if kept is not None else self.d_bias, d_in, self.mma,
+                      p_in=kept)
+        self._p = None
         return d_in
 
     def grad_buffers(self):
@@ -95,7 +107,9 @@ def train_step(layer: DeepThinLayer, x: torch.Tensor, target: torch.Tensor, lr: 
     ls = loss_out if loss_out is not None else torch.empty(1, dtype=torch.float64, device=x.device)
     norm = float(rows * layer.plan.r_dim)
     if layer.mma == _lib.DT_MMA_BF16 and layer.activation == "identity":
-        g = layer.forward_mse(x, target, norm, ls)   # MSE fused into the forward epilogue
+        # MSE fused into the forward; its loss pass also yields d_bias, and P is kept for the
+        # backward (reuse geometries: config 5)
+        g = layer.forward_mse(x, target, norm, ls, keep_for_backward=layer.plan.reuse_path)
     else:
         y = layer.forward(x)
         g = torch.empty_like(y)

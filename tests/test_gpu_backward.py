@@ -180,3 +180,28 @@ def test_forward_mse_cublaslt_epilogue_large():
     want_loss = float(((g.double() * norm / 2.0) ** 2).sum())
     assert float(loss.item()) == pytest.approx(want_loss, rel=1e-9)
     assert float(loss.item()) == pytest.approx(float(((z - d["target"]) ** 2).sum()), rel=2e-3)
+
+
+@pytest.mark.parametrize("geo", [
+    (2048, 2048, 64, 256, 16384, 1024),   # config-5-like: cuBLASLt MSE, fused colsum + loss pass
+    (1024, 1024, 16, 128, 8192, 300),     # factored path, our GEMM-2 MSE epilogue
+])
+def test_forward_mse_keep_for_backward_is_exact(geo):
+    """dt_forward_mse_ex keeps P and produces d_bias in the loss pass; dt_backward_ex reuses
+    them: the gradients equal the recomputing path's bits, the loss agrees to fp64 rounding."""
+    q, r_dim, rank, n, m, batch = geo
+    op = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, batch, seed=5).items()}
+    p = D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda").to(torch.bfloat16)
+    t = torch.tensor(d["target"], dtype=torch.float32, device="cuda")
+    out = []
+    for keep in (False, True):
+        layer = D.DeepThinLayer(p, d["xf"], d["wf"], d["bias"], mma="bf16")
+        loss = torch.empty(1, dtype=torch.float64, device="cuda")
+        g = layer.forward_mse(x, t, float(batch * r_dim), loss, keep_for_backward=keep)
+        layer.backward(g)
+        out.append((g.clone(), layer.grad_flat.clone(), float(loss.item())))
+    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][1], out[1][1])
+    assert out[1][2] == pytest.approx(out[0][2], rel=1e-12)
