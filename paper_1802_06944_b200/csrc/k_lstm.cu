@@ -83,6 +83,9 @@ struct GateArgs {
 
 // Stage `rows` x `cols` fp32 (cols % 4 == 0, row pitch `ld` floats) from global into shared
 // memory (row pitch `sp` floats): 8 float4 loads in flight per thread before the stores.
+// COHERENT: L2-only loads (ld.global.cg) for data other CTAs write during the same kernel (the
+// persistent recurrence's P and h); otherwise the read-only path.
+template <bool COHERENT = false>
 __device__ __forceinline__ void stage_rows(float *dst, int sp, const float *src, int64_t ld, int rows,
                                            int cols) {
   const int c4 = cols / 4, n4 = rows * c4;
@@ -91,7 +94,10 @@ __device__ __forceinline__ void stage_rows(float *dst, int sp, const float *src,
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int i = i0 + u * blockDim.x;
-      if (i < n4) v[u] = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)(i / c4) * ld) + i % c4);
+      if (i < n4) {
+        const float4 *a4 = reinterpret_cast<const float4 *>(src + (int64_t)(i / c4) * ld) + i % c4;
+        v[u] = COHERENT ? __ldcg(a4) : __ldg(a4);
+      }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -105,13 +111,14 @@ __device__ __forceinline__ void stage_rows(float *dst, int sp, const float *src,
 }
 
 // 64 x 64 output tile D[b][j] = sum_kk ps[b][kk] * xs[j][kk] (row pitch kp floats) on the tensor
-// cores: mma.sync m16n8k8 tf32 in the 3xTF32 form (lo*hi + hi*lo + hi*hi with hi = RNA(x),
-// lo = RNA(x - hi)): ~fp32 accuracy at a fraction of the FFMA instruction count. 8 warps, warp w
-// owns rows 16*(w%4).. and columns 32*(w/4).. (4 n-tiles of 8). acc[nt][4]: m16n8 fragments.
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+// cores: mma.sync m16n8k8 tf32 in the 3xTF32 form (lo*hi + hi*lo + hi*hi), x = hi + lo split
+// exactly by masking the low 13 mantissa bits (integer ops: cvt.rna.tf32 runs at a quarter of
+// the ALU rate and made this tile conversion-bound); the MMA truncates lo to tf32, leaving
+// ~2^-20 relative error per product. 8 warps, warp w owns rows 16*(w%4).. and columns
+// 32*(w/4).. (4 n-tiles of 8). acc[nt][4]: m16n8 fragments.
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -133,16 +140,14 @@ __device__ __forceinline__ void tile64_3xtf32(const float *ps, const float *xs, 
                          ps[(r0 + gid) * kp + kk + tig + 4], ps[(r0 + gid + 8) * kp + kk + tig + 4]};
     uint32_t ah[4], al[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      ah[i] = tf32_rna(av[i]);
-      al[i] = tf32_rna(av[i] - __uint_as_float(ah[i]));
-    }
+    for (int i = 0; i < 4; ++i) split_tf32(av[i], ah[i], al[i]);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const float *xr = xs + (c0 + nt * 8 + gid) * kp + kk;
       const float bv0 = xr[tig], bv1 = xr[tig + 4];
-      const uint32_t bh0 = tf32_rna(bv0), bh1 = tf32_rna(bv1);
-      const uint32_t bl0 = tf32_rna(bv0 - __uint_as_float(bh0)), bl1 = tf32_rna(bv1 - __uint_as_float(bh1));
+      uint32_t bh0, bh1, bl0, bl1;
+      split_tf32(bv0, bh0, bl0);
+      split_tf32(bv1, bh1, bl1);
       mma_tf32(acc[nt], al, bh0, bh1);
       mma_tf32(acc[nt], ah, bl0, bl1);
       mma_tf32(acc[nt], ah, bh0, bh1);
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(256) k_gates_p(int64_t batch, int H, int n, in
   const int seg = blockIdx.x, g = blockIdx.y, s = H / n, K2 = s * R;
   const int64_t b0 = (int64_t)blockIdx.z * kPB;
   const int nb = (int)(batch - b0 < kPB ? batch - b0 : kPB);
-  const int npad = n + 1;  // conflict-free row reads across k
+  const int npad = n + 4;  // 16-byte rows; float4 reads across k hit distinct bank quads
   float *hs = sm, *ws = sm + kPB * npad;
   const float *wfg = g == 0 ? a.wf[0] : g == 1 ? a.wf[1] : g == 2 ? a.wf[2] : a.wf[3];
   stage_rows(ws, npad, wfg, n, R, n);
@@ -181,9 +186,13 @@ __global__ void __launch_bounds__(256) k_gates_p(int64_t batch, int H, int n, in
     const int b = o / R, k = o % R;
     const float *hr = hs + b * npad, *wr = ws + k * npad;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int t = 0; t < n; t += 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fmaf(hr[t + u], wr[t + u], acc[u]);
+    for (int t = 0; t < n; t += 4) {  // same sums as element-wise, a quarter of the loads
+      const float4 hv = *reinterpret_cast<const float4 *>(hr + t);
+      const float4 wv = *reinterpret_cast<const float4 *>(wr + t);
+      acc[0] = fmaf(hv.x, wv.x, acc[0]);
+      acc[1] = fmaf(hv.y, wv.y, acc[1]);
+      acc[2] = fmaf(hv.z, wv.z, acc[2]);
+      acc[3] = fmaf(hv.w, wv.w, acc[3]);
     }
     P[((int64_t)g * batch + b0 + b) * K2 + seg * R + k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
@@ -232,7 +241,7 @@ int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *
   }
   const int H = (int)g.q, n = (int)g.n, R = (int)g.rank, s = (int)g.s, K2 = s * R;
   float *P = reinterpret_cast<float *>(ws);
-  const size_t smp = (size_t)(kPB + R) * (n + 1) * 4;
+  const size_t smp = (size_t)(kPB + R) * (n + 4) * 4;
   const size_t smy = (size_t)(kGB + 64) * (K2 + 4) * 4;
   static bool attr = false;
   if (!attr) {
@@ -298,7 +307,7 @@ __device__ __forceinline__ float sigm_(float z) { return 1.f / (1.f + expf(-z));
 __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
   extern __shared__ float sm[];
   const int B = a.B, H = a.H, n = a.n, R = a.R, K2 = a.K2;
-  const int npad = n + 1, kp = K2 + 4;
+  const int npad = n + 4, kp = K2 + 4;
   const int rgs = (B + 15) / 16;
   const int unitsP = 4 * a.s * rgs, unitsB = 4 * ((H + 63) / 64);
   const int64_t BH = (int64_t)B * H;
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 8) {
       unsigned long long v;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-      a.trace[t * 4 + k] = v;
+      a.trace[t * 6 + k] = v;
     }
   };
   // phase C: the cell of step t (all of B x H, grid-strided; each element owned by one thread)
@@ -348,40 +357,46 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       const int b0 = rg * 16, nb = min(16, B - b0);
       __syncthreads();
       if (!resP) stage_rows(ws, npad, wf_of(g), n, R, n);
-      stage_rows(hs, npad, a.h + (size_t)b0 * H + seg * n, H, nb, n);
+      stage_rows<true>(hs, npad, a.h + (size_t)b0 * H + seg * n, H, nb, n);
       __syncthreads();
       for (int o = threadIdx.x; o < nb * R; o += blockDim.x) {
         const int b = o / R, k = o % R;
         const float *hr = hs + b * npad, *wr = ws + k * npad;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int tt = 0; tt < n; tt += 4) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[v] = fmaf(hr[tt + v], wr[tt + v], acc[v]);
+          const float4 hv = *reinterpret_cast<const float4 *>(hr + tt);
+          const float4 wv = *reinterpret_cast<const float4 *>(wr + tt);
+          acc[0] = fmaf(hv.x, wv.x, acc[0]);
+          acc[1] = fmaf(hv.y, wv.y, acc[1]);
+          acc[2] = fmaf(hv.z, wv.z, acc[2]);
+          acc[3] = fmaf(hv.w, wv.w, acc[3]);
         }
         a.P[((size_t)g * B + b0 + b) * K2 + seg * R + k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
     }
     stamp(t, 0);
     grid_barrier(a.bar, target);
+    stamp(t, 1);
     // ---------------- phase G: gh_g[:, 64-column block] = P_g XF2_g^T + b (3xTF32 mma) -----------
     for (int u = blockIdx.x; u < unitsB; u += gridDim.x) {
       const int g = u / ((H + 63) / 64), j0 = (u % ((H + 63) / 64)) * 64, nj = min(64, H - j0);
       const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
       __syncthreads();
       if (!resB) stage_xs(u);
-      stage_rows(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2);
+      stage_rows<true>(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2);
       for (int i = B * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) ps[i] = 0.f;
       __syncthreads();
       float acc[4][4];
       tile64_3xtf32(ps, xs, kp, K2, acc);
       tile64_store(acc, a.gh + (size_t)g * BH, H, 0, B, j0, nj, bg);
     }
-    stamp(t, 1);
-    grid_barrier(a.bar, target);
     stamp(t, 2);
-    cell(t);
     grid_barrier(a.bar, target);
     stamp(t, 3);
+    cell(t);
+    stamp(t, 4);
+    grid_barrier(a.bar, target);
+    stamp(t, 5);
   }
 }
 
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
 
 bool lstm_seq_ok(const Geo &g, int64_t batch) {
   return lstm_gates_ok(g) && batch >= 1 && batch <= 64 && g.n <= 1024 &&
-         ((size_t)(16 + g.rank) * (g.n + 1) + 4 + (size_t)128 * (g.s * g.rank + 4)) * 4 <= 227 * 1024;
+         ((size_t)(16 + g.rank) * (g.n + 4) + 4 + (size_t)128 * (g.s * g.rank + 4)) * 4 <= 227 * 1024;
 }
 size_t lstm_seq_ws(const Geo &g, int64_t batch) {
   return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * g.s * g.rank * 4 + (size_t)2 * batch * g.q * 4 + 256;
@@ -415,7 +430,7 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   a.out = reinterpret_cast<__nv_bfloat16 *>(out);
   DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));  // c(-1) = h(-1) = 0
   DT_CUDA_CHECK(cudaMemsetAsync(a.bar, 0, 256, st));
-  const size_t smem = ((size_t)(16 + a.R) * (a.n + 1) + 4 + (size_t)128 * (a.K2 + 4)) * 4;
+  const size_t smem = ((size_t)(16 + a.R) * (a.n + 4) + 4 + (size_t)128 * (a.K2 + 4)) * 4;
   static bool attr = false;
   if (!attr) {
     DT_CUDA_CHECK(cudaFuncSetAttribute(k_lstm_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -439,19 +454,20 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   static const bool tracing = getenv("DEEPTHIN_LSTM_TRACE") != nullptr;
   a.trace = nullptr;
   if (tracing) {
-    DT_CUDA_CHECK(cudaMalloc(&a.trace, 32 * 8));
-    DT_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 32 * 8, st));
+    DT_CUDA_CHECK(cudaMalloc(&a.trace, 48 * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 48 * 8, st));
   }
   DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_lstm_seq, a));
   if (tracing) {
-    unsigned long long h[32];
+    unsigned long long h[48];
     DT_CUDA_CHECK(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st));
     DT_CUDA_CHECK(cudaStreamSynchronize(st));
     cudaFree(a.trace);
     for (int t = 0; t < 8; ++t)
-      fprintf(stderr, "lstm step %d: P %.2f  bar+G %.2f  bar %.2f  cell+bar %.2f us\n", t,
-              t ? (h[t * 4] - h[t * 4 - 1]) * 1e-3 : 0.0, (h[t * 4 + 1] - h[t * 4]) * 1e-3,
-              (h[t * 4 + 2] - h[t * 4 + 1]) * 1e-3, (h[t * 4 + 3] - h[t * 4 + 2]) * 1e-3);
+      fprintf(stderr, "lstm step %d: P %.2f  bar %.2f  G %.2f  bar %.2f  cell %.2f  bar %.2f us\n", t,
+              t ? (h[t * 6] - h[t * 6 - 1]) * 1e-3 : 0.0, (h[t * 6 + 1] - h[t * 6]) * 1e-3,
+              (h[t * 6 + 2] - h[t * 6 + 1]) * 1e-3, (h[t * 6 + 3] - h[t * 6 + 2]) * 1e-3,
+              (h[t * 6 + 4] - h[t * 6 + 3]) * 1e-3, (h[t * 6 + 5] - h[t * 6 + 4]) * 1e-3);
   }
   return check_launch("lstm_seq");
 }
