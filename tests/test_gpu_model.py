@@ -177,3 +177,18 @@ def test_row_tile_layer_chaining_is_exact():
             torch.cuda.synchronize()
             assert torch.equal(got, want)
         dm.chain = False
+
+
+def test_graph_forward_equals_eager():
+    """DeviceModel.forward(graph=True): the captured layer chain replays the eager bits."""
+    model = mi.deserialize(mi.serialize(config3_like(layers=3)))
+    dm = model.to_device(["sigmoid"] * 3 + ["softmax"], mma="bf16")
+    x = torch.randn(700, 440, device="cuda").to(torch.bfloat16)
+    want = dm.forward(x, out_dtype=torch.bfloat16).clone()
+    for _ in range(3):
+        got = dm.forward(x, out_dtype=torch.bfloat16, graph=True)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
+    x.copy_(torch.randn(700, 440, device="cuda").to(torch.bfloat16))  # same buffer, new data
+    want2 = dm.forward(x, out_dtype=torch.bfloat16)
+    assert torch.equal(dm.forward(x, out_dtype=torch.bfloat16, graph=True), want2)
