@@ -1696,6 +1696,24 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
 // =============================================================================================
 namespace {
 
+// H (rows x r fp32) -> H2 (rows x 2r bf16): row i = [hi(H[i, :]) | lo(H[i, :])] (one GEMM then
+// contracts both halves against x in a single read of x)
+__global__ void k_split_bf16_rows(int64_t rows, int r, const float *src, __nv_bfloat16 *h2) {
+  const int64_t count = rows * r;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / r, k = i - row * r;
+    const float v = src[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    h2[row * 2 * r + k] = h;
+    h2[row * 2 * r + r + k] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+__global__ void k_add_halves(int64_t count, const float *d2, float *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = d2[i] + d2[count + i];
+}
+
 __global__ void k_split_bf16(int64_t count, const float *src, __nv_bfloat16 *hi, __nv_bfloat16 *lo) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1835,7 +1853,8 @@ size_t tc_backward_ws(const Geo &g, int64_t batch) {
          (size_t)round_up(batch * SR * 2, 256) * 2 /*H hi, lo*/ +
          (size_t)round_up(g.rank * g.n * 2, 256) + (size_t)round_up(batch * g.q * 2, 256) +
          (size_t)round_up(colsum_ws(batch, g.r_dim), 256) +
-         std::max(tc_gemm_ws(g, batch), ffma_forward_ws(g, batch)) + kLtWs;
+         std::max(tc_gemm_ws(g, batch), ffma_forward_ws(g, batch)) + kLtWs +
+         (size_t)round_up(2 * g.rank * g.n * 4, 256);
 }
 
 int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
@@ -1869,6 +1888,8 @@ int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const f
   float *H = reinterpret_cast<float *>(take(batch * SR * 4));
   __nv_bfloat16 *Hhi = reinterpret_cast<__nv_bfloat16 *>(take(batch * SR * 2));
   __nv_bfloat16 *Hlo = reinterpret_cast<__nv_bfloat16 *>(take(batch * SR * 2));
+  (void)Hlo;  // second half of the [hi | lo] operand that starts at Hhi
+  float *d2buf = reinterpret_cast<float *>(take(2 * g.rank * g.n * 4));
   char *wf16 = take(g.rank * g.n * 2);
   char *x16 = take(batch * g.q * 2);
   float *cpart = reinterpret_cast<float *>(take(colsum_ws(batch, g.r_dim)));
@@ -1914,16 +1935,18 @@ int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const f
   if (int rc = lt_gemm(st, batch, SR, g.r_dim, gp, false, g.r_dim, xf, false, SR, H, SR, CUDA_R_32F,
                        0.f, ltws, kLtWs))
     return rc;
-  // d_wf (rank x n) = H'^T @ x'  with H = hi + lo in bf16 (two accumulating GEMMs)
-  k_split_bf16<<<std::min<int64_t>((batch * SR + 255) / 256, 4096), 256, 0, st>>>(batch * SR, H,
-                                                                                 Hhi, Hlo);
-  if (int rc = check_launch("split_bf16")) return rc;
-  if (int rc = lt_gemm(st, g.rank, g.n, Bs, Hhi, true, g.rank, xt, false, g.n, d_wf, g.n,
+  // d_wf (rank x n) = H'^T @ x'  with H = hi + lo in bf16: one GEMM over [hi | lo] (2*rank
+  // rows, x read once), then the two halves added (fixed order hi + lo)
+  __nv_bfloat16 *H2 = Hhi;  // Bs x 2*rank bf16: spans the adjacent Hhi and Hlo regions
+  float *D2 = d2buf;        // 2*rank x n fp32
+  k_split_bf16_rows<<<std::min<int64_t>((batch * SR + 255) / 256, 4096), 256, 0, st>>>(Bs, (int)g.rank,
+                                                                                    H, H2);
+  if (int rc = check_launch("split_bf16_rows")) return rc;
+  if (int rc = lt_gemm(st, 2 * g.rank, g.n, Bs, H2, true, 2 * g.rank, xt, false, g.n, D2, g.n,
                        CUDA_R_16BF, 0.f, ltws, kLtWs))
     return rc;
-  if (int rc = lt_gemm(st, g.rank, g.n, Bs, Hlo, true, g.rank, xt, false, g.n, d_wf, g.n,
-                       CUDA_R_16BF, 1.f, ltws, kLtWs))
-    return rc;
+  k_add_halves<<<(unsigned)((g.rank * g.n + 255) / 256), 256, 0, st>>>(g.rank * g.n, D2, d_wf);
+  if (int rc = check_launch("add_halves")) return rc;
   // d_input (B*s x n) = H' @ wf
   if (d_input)
     if (int rc = lt_gemm(st, Bs, g.n, g.rank, H, false, g.rank, wf, false, g.n, d_input, g.n,
