@@ -29,17 +29,29 @@ class DeepThinLayer:
     def __init__(self, plan: LayerPlan, xf, wf, bias=None, activation: str = "identity",
                  mma: str = "bf16", act_arg: float = 20.0):
         self.plan = plan
-        self.fp = FactorPair(xf, wf, plan)
-        self.bias = as_device_vector(np.zeros(plan.r_dim) if bias is None else bias, plan.r_dim).clone()
+        # fp32 masters in ONE flat buffer [xf | wf | bias] (256-byte aligned segments) laid out
+        # like grad_flat, so the SGD step is a single launch over both flat buffers
+        src = FactorPair(xf, wf, plan)
+        nx, nw = plan.m * plan.rank, plan.rank * plan.n
+        ox, ow, ob = 0, -(-nx // 64) * 64, 0
+        ob = ow + -(-nw // 64) * 64
+        total = ob + -(-plan.r_dim // 64) * 64
+        self.param_flat = torch.zeros(total, dtype=torch.float32, device=device())
+        self.grad_flat = torch.zeros(total, dtype=torch.float32, device=device())
+        self.param_flat[ox:ox + nx].copy_(src.xf.reshape(-1))
+        self.param_flat[ow:ow + nw].copy_(src.wf.reshape(-1))
+        b = as_device_vector(np.zeros(plan.r_dim) if bias is None else bias, plan.r_dim)
+        self.param_flat[ob:ob + plan.r_dim].copy_(b)
+        self.fp = FactorPair.adopt(self.param_flat[ox:ox + nx].view(plan.m, plan.rank),
+                                   self.param_flat[ow:ow + nw].view(plan.rank, plan.n), plan)
+        self.bias = self.param_flat[ob:ob + plan.r_dim]
+        self.d_xf = self.grad_flat[ox:ox + nx].view(plan.m, plan.rank)
+        self.d_wf = self.grad_flat[ow:ow + nw].view(plan.rank, plan.n)
+        self.d_bias = self.grad_flat[ob:ob + plan.r_dim]
         self.activation = activation
         self.act = _act_code(activation)
         self.act_arg = act_arg
         self.mma = _lib.DT_MMA_BF16 if mma == "bf16" else _lib.DT_MMA_FFMA
-        nx, nw = plan.m * plan.rank, plan.rank * plan.n
-        self.grad_flat = torch.zeros(nx + nw + plan.r_dim, dtype=torch.float32, device=device())
-        self.d_xf = self.grad_flat[:nx].view(plan.m, plan.rank)
-        self.d_wf = self.grad_flat[nx:nx + nw].view(plan.rank, plan.n)
-        self.d_bias = self.grad_flat[nx + nw:]
         self._x = None
 
     def forward(self, x: torch.Tensor, out_dtype=torch.float32) -> torch.Tensor:
@@ -94,9 +106,8 @@ class DeepThinLayer:
     def step(self, lr: float) -> None:
         """train.py:107-111 + :221: SGD on the fp32 masters, then refresh bf16 operand copies."""
         lib = _lib.lib()
-        for p, g in ((self.fp.xf, self.d_xf), (self.fp.wf, self.d_wf), (self.bias, self.d_bias)):
-            _lib.check(lib.dt_sgd_step(p.numel(), p.data_ptr(), g.data_ptr(), float(lr),
-                                       stream_handle()))
+        _lib.check(lib.dt_sgd_step(self.param_flat.numel(), self.param_flat.data_ptr(),
+                                   self.grad_flat.data_ptr(), float(lr), stream_handle()))
         self.fp.refresh_derived()
 
 
