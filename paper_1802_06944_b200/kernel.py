@@ -136,11 +136,22 @@ def forward_into(x: torch.Tensor, fp: FactorPair, bias, act: int, act_arg: float
     bf16 tensor-core path: by default the two-phase kernels (W^T regenerated from the fp32
     factors, then the tcgen05 GEMM); ``fused=True`` runs the single fused kernel on the
     packed bf16 factors (general geometries only). ``ws``: a caller-owned workspace (grown
-    here when too small); by default a fresh one per call."""
+    here when too small); by default a fresh one per call. ``cached``: the caller keeps the
+    factors and bias constant between calls, so the row-tile kernel's derived operands are
+    built once per pair (FactorPair.rows_prepared) and the call launches that kernel alone."""
     p = fp.plan
     lib = _lib.lib()
     ps = _lib.plan_struct(p)
     batch = x.shape[0]
+    if cached and mma == _lib.DT_MMA_BF16 and not fused and x.dtype == torch.bfloat16:
+        ydt = _lib.DT_BF16 if y.dtype == torch.bfloat16 else _lib.DT_F32
+        prep = fp.rows_prepared(bias, act, ydt)
+        if prep is not None:
+            _lib.check(lib.dt_forward(
+                C.byref(ps), batch, mma, x.data_ptr(), _lib.DT_BF16, prep.data_ptr(), None,
+                _lib.DT_FACTORS_ROWS, bias.data_ptr() if bias is not None else None, act,
+                float(act_arg), y.data_ptr(), ydt, None, 0, stream_handle()))
+            return
     ws_bytes = lib.dt_forward_workspace_bytes(C.byref(ps), batch, mma)
     if ws is None or ws.numel() < ws_bytes:
         ws = workspace(ws_bytes)

@@ -122,3 +122,21 @@ def test_rows_fused_softmax_output_layer(out, fused, monkeypatch):
     assert np.allclose(got.sum(axis=1), 1.0, atol=1e-5 if out == torch.float32 else 2e-2)
     y2 = D.layer_forward(x, fp, d["bias"], "softmax", mma="bf16", out_dtype=out)
     assert torch.equal(y, y2)
+
+
+def test_prepared_path_launches_only_the_row_kernel():
+    """cached=True really takes the prepared-operand route: one launch per call (no prep)."""
+    from paper_1802_06944_b200 import _lib
+    from paper_1802_06944_b200.kernel import _act_code, forward_into
+    plan, d, fp = make_case(2048, 2048, 3, 256, 16384, 256, seed=2, rnd=O.round_bf16)
+    x = gpu_x(d["x"], torch.bfloat16)
+    b = torch.tensor(d["bias"], dtype=torch.float32, device="cuda")
+    y = torch.empty((256, 2048), dtype=torch.bfloat16, device="cuda")
+    lib = _lib.lib()
+    forward_into(x, fp, b, _act_code("sigmoid"), 0.0, y, _lib.DT_MMA_BF16, cached=True)  # prepares
+    n0 = lib.dt_launch_counter()
+    forward_into(x, fp, b, _act_code("sigmoid"), 0.0, y, _lib.DT_MMA_BF16, cached=True)
+    assert lib.dt_launch_counter() - n0 == 1
+    n0 = lib.dt_launch_counter()
+    forward_into(x, fp, b, _act_code("sigmoid"), 0.0, y, _lib.DT_MMA_BF16)
+    assert lib.dt_launch_counter() - n0 == 2   # per-call prep + the row kernel
