@@ -88,9 +88,10 @@ class DeviceModel:
         torch.cuda.current_stream().synchronize()  # the image (and staging) can go now
         del img, staging
         self._ws = [None] * count
-        # per-row-tile layer chaining (see forward): exact, but measured no faster at config 3
-        # (its clusters of 8 only launch on SMs the previous layer's clusters free, which all
-        # finish within ~one tile of each other), and it costs host time: off by default
+        # per-row-tile layer chaining (see forward): exact, but measured slower at config 3
+        # (351 vs 323 us per forward: its clusters of 8 only launch on SMs the previous layer's
+        # clusters free, which all finish within ~one tile of each other, and the x producer
+        # then polls flags instead of a single grid dependency): off by default
         self.chain = False
         self._chain_key = None
 
