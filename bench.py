@@ -654,6 +654,7 @@ def run_network(args, cfg, key):
 
     # our kernels per forward (counted on an eager forward: graph replays bypass the host-side
     # launch counter, the same kernels run inside them)
+    dm.forward(xs[0], out_dtype=torch.bfloat16)  # first call also prepares the operands
     n0 = lib.dt_launch_counter()
     dm.forward(xs[0], out_dtype=torch.bfloat16)
     per_forward = lib.dt_launch_counter() - n0
