@@ -1,7 +1,7 @@
 """Stage-by-stage comparison of SpeechRNN against the f64 contract emulation (debug)."""
 import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np, torch
 from oracle import deepthin_oracle as O
 from test_gpu_speech import build, contract_layer
