@@ -123,6 +123,33 @@ def test_forward_rejects_bad_arguments_before_touching_the_gpu():
                           0, None) == _lib.DT_E_ARG
 
 
+def test_new_entry_points_validate_before_touching_the_gpu():
+    """Geometry / argument checks of the row-tile, LSTM and training entry points run on the
+    host (no device work for a rejected call)."""
+    lib = _lib.lib()
+    reuse = _lib.Plan(2048, 2048, 3, 16384, 256)      # row-tile geometry (config 3)
+    general = _lib.Plan(440, 2048, 24, 2816, 320)     # straddling rows
+    assert lib.dt_rows_prepared_bytes(C.byref(reuse), _lib.DT_BF16, _lib.DT_BF16) > 0
+    assert lib.dt_rows_prepared_bytes(C.byref(general), _lib.DT_BF16, _lib.DT_BF16) == 0
+    assert lib.dt_rows_prepared_bytes(C.byref(reuse), _lib.DT_F32, _lib.DT_BF16) == 0  # bf16 x only
+    assert lib.dt_rows_prepare(C.byref(general), 0, _lib.DT_BF16, None, None, None, None, None) \
+        == _lib.DT_E_UNSUPPORTED
+    assert lib.dt_rows_prepare(C.byref(reuse), 0, _lib.DT_BF16, None, None, None, None, None) \
+        == _lib.DT_E_ARG
+    assert lib.dt_rows_posts_per_tile(C.byref(reuse)) == 8 * 16
+    lstm = _lib.Plan(2048, 2048, 32, 16384, 256)
+    assert lib.dt_lstm_sequence_workspace_bytes(C.byref(lstm), 64) > 0
+    assert lib.dt_lstm_sequence_workspace_bytes(C.byref(lstm), 65) == 0   # batch <= 64
+    assert lib.dt_lstm_gates_workspace_bytes(C.byref(general), 8) == 0    # square reuse only
+    P4 = C.c_void_p * 4
+    assert lib.dt_lstm_sequence(C.byref(lstm), 10, 65, P4(), P4(), P4(), P4(), None, None, 0,
+                                None) == _lib.DT_E_UNSUPPORTED
+    assert lib.dt_lstm_cell(4, 8, None, 4, None, None, None, None, None) == _lib.DT_E_DIM  # ld < hidden
+    assert lib.dt_forward_p_bytes(C.byref(reuse), 128) == 128 * 8 * 3 * 4
+    assert lib.dt_forward_p_bytes(C.byref(general), 128) == 0
+    assert lib.dt_profile_kernel_kind(7) == _lib.DT_E_ARG
+
+
 def test_no_cpu_fallback_without_gpu():
     import torch
     if torch.cuda.is_available():
