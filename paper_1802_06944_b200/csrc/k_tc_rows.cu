@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 
@@ -154,7 +155,7 @@ __device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta,
 template <int YDT, int ACT>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     k_tc_rows_reuse(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_wf,
-                    const __grid_constant__ CUtensorMap tm_xf2, const __grid_constant__ CUtensorMap tm_y,
+                    const __grid_constant__ CUtensorMap tm_xf2,
                     const RowsParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -193,7 +194,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     tma_prefetch_desc(&tm_x);
     tma_prefetch_desc(&tm_wf);
     tma_prefetch_desc(&tm_xf2);
-    tma_prefetch_desc(&tm_y);
   }
   if (warp == 2) tmem_alloc(tslot, 512);
   tc_fence_before();
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   }
 }
 
-using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
+using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
 
 template <int YDT>
 RowsFn pick_act(int act) {
@@ -843,7 +843,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   if (!prepared)
     if (int rc = tc_rows_prepare(g, wf, xf, bias, act, y_dtype, ws, st)) return rc;
 
-  CUtensorMap tm_x, tm_wf, tm_xf2, tm_y;
+  CUtensorMap tm_x, tm_wf, tm_xf2;
   if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(x), (uint64_t)g.q,
                                     (uint64_t)batch, (uint64_t)g.q * 2, 64, kTM, true))
     return rc;
@@ -853,13 +853,15 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   if (int rc = encode_tensor_map_2d(&tm_xf2, DT_F32, xf2p, (uint64_t)p.k2, (uint64_t)g.r_dim,
                                     (uint64_t)p.k2 * 4, 32, kNc, true))
     return rc;
-  const int E = y_dtype == DT_BF16 ? 2 : 4;
-  if (int rc = encode_tensor_map_2d(&tm_y, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
-                                    (uint64_t)g.r_dim * E, 128 / E, 32, true))
-    return rc;
-
   RowsFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(act) : pick_act<DT_F32>(act);
-  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  {  // the opt-in shared-memory size once per kernel instance (host cost per call otherwise)
+    thread_local std::unordered_map<const void *, uint32_t> set_smem;
+    uint32_t &have = set_smem[reinterpret_cast<const void *>(fn)];
+    if (have < smem_bytes) {
+      DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+      have = smem_bytes;
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kRowsThreads);
   cfg.dynamicSmemBytes = smem_bytes;
@@ -896,7 +898,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   cudaEvent_t ev_b = nullptr, ev_a = nullptr;  // dt_profile_kernel_events
   profile_next(&ev_b, &ev_a, DT_PROF_ROWS);
   if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
-  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, tm_y, p));
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, p));
   if (ev_a) DT_CUDA_CHECK(cudaEventRecord(ev_a, st));
   if (tracing) {
     unsigned long long h[8 * kTr];
