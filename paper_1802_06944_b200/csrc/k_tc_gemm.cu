@@ -1580,6 +1580,16 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     return DT_E_ARG;
   }
 
+  // one-kernel row-tile form (k_tc_rows.cu) when the geometry and operands allow it; it pads
+  // each segment's rank to 4, so it also serves reuse geometries whose s*rank % 4 != 0
+  if (f_dtype == DT_F32 && !mse && tc_rows_ok(g, x_dtype, y_dtype) &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+        reinterpret_cast<uintptr_t>(bias)) & 15) == 0) {
+    // (softmax: fused into the epilogue when it fits, else a post pass inside)
+    return tc_rows_forward(g, batch, x, reinterpret_cast<const float *>(wf),
+                           reinterpret_cast<const float *>(xf), bias, act, act_arg, y, y_dtype,
+                           ws, st);
+  }
   if (reuse_factored_ok(g) && f_dtype == DT_F32) {
     // ---- factored reuse path: two GEMMs ----
     char *cur = ws;
@@ -1588,14 +1598,6 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
       cur += round_up(bytes, 256);
       return r;
     };
-    // one-kernel row-tile form (k_tc_rows.cu) when the geometry and operands allow it
-    if (!mse && tc_rows_ok(g, x_dtype, y_dtype) && ((reinterpret_cast<uintptr_t>(x) |
-        reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0) {
-      // (softmax: fused into the epilogue when it fits, else a post pass inside)
-      return tc_rows_forward(g, batch, x, reinterpret_cast<const float *>(wf),
-                             reinterpret_cast<const float *>(xf), bias, act, act_arg, y, y_dtype,
-                             ws, st);
-    }
     char *wf16 = take(g.rank * g.n * 2);
     float *P = reinterpret_cast<float *>(take(batch * g.s * g.rank * 4));
     char *x_ws = take(batch * g.q * 2);

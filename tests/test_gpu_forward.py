@@ -46,13 +46,24 @@ def bf16_emulated(d, plan, bias):
     return d["x"] @ w + bias
 
 
-def factored_path(plan):
+def factored_path(plan, y_dtype=torch.float32):
     """The bf16 tensor-core path computes reuse geometries in factored form when the views are
-    16-byte aligned (k_tc_gemm.cu reuse_factored_ok)."""
+    16-byte aligned (k_tc_gemm.cu reuse_factored_ok) or the row-tile kernel takes them (bf16 x,
+    k_tc_rows.cu tc_rows_ok, which pads each segment's rank and so has no s*rank % 4 rule)."""
     if plan.q % plan.n:
         return False
     s = plan.q // plan.n
-    return plan.n % 8 == 0 and (s * plan.rank) % 4 == 0
+    if plan.n % 8 == 0 and (s * plan.rank) % 4 == 0:
+        return True
+    return rows_path(plan, y_dtype)
+
+
+def rows_path(plan, y_dtype=torch.float32):
+    import ctypes as C
+    from paper_1802_06944_b200 import _lib
+    ps = _lib.plan_struct(plan)
+    yd = _lib.DT_BF16 if y_dtype == torch.bfloat16 else _lib.DT_F32
+    return _lib.lib().dt_rows_prepared_bytes(C.byref(ps), _lib.DT_BF16, yd) > 0
 
 
 def bf16_factored_emulated(d, plan, bias):
@@ -67,8 +78,9 @@ def bf16_factored_emulated(d, plan, bias):
     return p @ xf2.T + bias
 
 
-def bf16_contract(d, plan, bias):
-    return bf16_factored_emulated(d, plan, bias) if factored_path(plan) else bf16_emulated(d, plan, bias)
+def bf16_contract(d, plan, bias, y_dtype=torch.float32):
+    return (bf16_factored_emulated(d, plan, bias) if factored_path(plan, y_dtype)
+            else bf16_emulated(d, plan, bias))
 
 
 def check_activation(y_act, y_pre, act, arg=20.0):

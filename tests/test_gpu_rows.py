@@ -18,7 +18,7 @@ import torch
 from oracle import deepthin_oracle as O
 
 import paper_1802_06944_b200 as D
-from test_gpu_forward import bf16_factored_emulated, gpu_x, make_case
+from test_gpu_forward import bf16_factored_emulated, gpu_x, make_case, rows_path
 
 pytestmark = pytest.mark.gpu
 
@@ -140,3 +140,31 @@ def test_prepared_path_launches_only_the_row_kernel():
     n0 = lib.dt_launch_counter()
     forward_into(x, fp, b, _act_code("sigmoid"), 0.0, y, _lib.DT_MMA_BF16)
     assert lib.dt_launch_counter() - n0 == 2   # per-call prep + the row kernel
+
+
+def _random_rows_geometries(count=10, seed=2024):
+    """Seeded random reuse geometries inside the row-tile envelope: n in {64, 128, 256, 320},
+    s * round_up(rank, 4) <= 32, r_dim a multiple of 8 (16-byte bf16 rows), ragged batch."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        n = int(rng.choice([64, 128, 256, 320]))
+        rank = int(rng.integers(1, 9))
+        rp = -(-rank // 4) * 4
+        s = int(rng.choice([s for s in (1, 2, 4, 8) if s * rp <= 32]))
+        q, r_dim = s * n, 8 * int(rng.integers(1, 400))
+        m = -(-(q * r_dim) // n) + int(rng.integers(0, 5))   # sometimes a discarded tail
+        out.append((q, r_dim, rank, n, m, int(rng.integers(1, 700))))
+    return out
+
+
+@pytest.mark.parametrize("geo", _random_rows_geometries())
+def test_rows_random_geometries(geo):
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=3, rnd=O.round_bf16, bias_sd=0.2)
+    x = gpu_x(d["x"], torch.bfloat16)
+    for out in (torch.float32, torch.bfloat16):
+        assert rows_path(plan, out), geo  # s * rank % 4 != 0 included: rank padded per segment
+        y = D.layer_forward(x, fp, d["bias"], mma="bf16", out_dtype=out).double().cpu().numpy()
+        extra = 2 ** -8 if out == torch.bfloat16 else 0.0
+        assert O.rel_error(y, bf16_factored_emulated(d, plan, d["bias"])) <= 1e-3 + extra, geo
