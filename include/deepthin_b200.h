@@ -217,14 +217,14 @@ int dt_rows_chain(const void *wait_flags, unsigned wait_target, void *post_flags
 int dt_rows_posts_per_tile(const dt_plan *plan);
 /* The four recurrent gate contractions of one LSTM step (BASELINE config 4): gh[g] = h @ W_g +
  * bias[g] for four DeepThin layers sharing one square reuse geometry (plan: q == r_dim, n | q),
- * h fp32 (batch x q), exact fp32 on the CUDA cores in the reference's factored reuse form
+ * h fp32 (batch x q), 3xTF32 tensor-core tiles (~fp32 accuracy, fixed order) in the reference's factored reuse form
  * (kernel.py:1-16, 296-320). xf/wf/bias/gh: four pointers each (bias may be NULL). */
 size_t dt_lstm_gates_workspace_bytes(const dt_plan *plan, int64_t batch);
 int dt_lstm_gates(const dt_plan *plan, int64_t batch, const float *h, const float *const *xf,
                   const float *const *wf, const float *const *bias, float *const *gh,
                   void *workspace, size_t workspace_bytes, dt_stream stream);
 /* The whole LSTM recurrence of BASELINE config 4 in one persistent cooperative kernel: for
- * t < T, gates = gx[g][t] + h_{t-1} @ W_g + bias[g] (the dt_lstm_gates contractions, exact fp32),
+ * t < T, gates = gx[g][t] + h_{t-1} @ W_g + bias[g] (the dt_lstm_gates contractions, 3xTF32 ~fp32),
  * then the dt_lstm_cell update; h_{-1} = c_{-1} = 0. gx[g]: bf16, T*batch x q (time-major rows);
  * out: bf16 T*batch x q (the h sequence). batch <= 64. */
 size_t dt_lstm_sequence_workspace_bytes(const dt_plan *plan, int64_t batch);

@@ -64,7 +64,7 @@ int launch_lstm_cell(int64_t batch, int64_t hidden, const void *const *gx, int64
 
 // =============================================================================================
 // The four recurrent gate contractions of one LSTM step (config 4: h (batch x H, fp32) through
-// four reuse-geometry DeepThin layers H -> H), exact fp32 on the CUDA cores, factored exactly
+// four reuse-geometry DeepThin layers H -> H), fp32-accurate (3xTF32 mma.sync tiles), factored exactly
 // like the reuse path (kernel.py:1-16):
 //   k_gates_p:  P_g[b, seg*R + k] = sum_t h[b, seg*n + t] * wf_g[k, t]        (grid: s x 4)
 //   k_gates_y:  gh_g[b, j] = sum_kk P_g[b, kk] * xf_g[j*s*R + kk] + bias_g[j]   (grid: H/64 x 4)
@@ -141,17 +141,21 @@ __device__ __forceinline__ void tile64_3xtf32(const float *ps, const float *xs, 
     uint32_t ah[4], al[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) split_tf32(av[i], ah[i], al[i]);
+    uint32_t bh[4][2], bl[4][2];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const float *xr = xs + (c0 + nt * 8 + gid) * kp + kk;
-      const float bv0 = xr[tig], bv1 = xr[tig + 4];
-      uint32_t bh0, bh1, bl0, bl1;
-      split_tf32(bv0, bh0, bl0);
-      split_tf32(bv1, bh1, bl1);
-      mma_tf32(acc[nt], al, bh0, bh1);
-      mma_tf32(acc[nt], ah, bl0, bl1);
-      mma_tf32(acc[nt], ah, bh0, bh1);
+      split_tf32(xr[tig], bh[nt][0], bl[nt][0]);
+      split_tf32(xr[tig + 4], bh[nt][1], bl[nt][1]);
     }
+    // the three passes each sweep the four n-tiles, so consecutive MMAs are independent (an
+    // accumulator's three products stay in the same order: lo*hi, hi*lo, hi*hi)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[nt], al, bh[nt][0], bh[nt][1]);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[nt], ah, bl[nt][0], bl[nt][1]);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[nt], ah, bh[nt][0], bh[nt][1]);
   }
 }
 // store the tile's fragments: D[b][j] + bias -> out[(b0 + b) * ld + j0 + j] (b < nb, j < nj)
@@ -168,34 +172,87 @@ __device__ __forceinline__ void tile64_store(const float (&acc)[4][4], float *ou
     }
 }
 
-// one CTA per (segment, gate, 16-row block): h[rows, seg] and wf_g in shared memory; each
-// thread two outputs, four interleaved partial sums (fixed order)
+// Segment-dot tile of the P phase on the tensor cores (3xTF32, as tile64_3xtf32):
+//   P[b][k] = sum_t hs[b][t] * ws[k][t],  b < 16, k < R8 (<= 64, rows >= R zero), t < n8
+// (row pitch npad = n8 + 4: conflict-free fragment loads). Warp w takes k-steps w, w + 8, ... for
+// every n-tile; the 8 warp partials land in red[w][16][R8] and p_tile_sum adds them in warp order.
+// Per CTA this reads 8x less shared memory than one-dot-per-thread FFMA, which was
+// shared-memory-bandwidth bound.
+__device__ __forceinline__ int lstm_npad(int n) { return (n + 7) / 8 * 8 + 4; }
+__device__ __forceinline__ void p_tile_3xtf32(const float *hs, const float *ws, int npad, int n8, int R8,
+                                              float *red) {
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32, gid = lane >> 2, tig = lane & 3;
+  const int ntiles = R8 / 8;
+  float acc[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
+  for (int kk = 8 * w; kk < n8; kk += 64) {
+    const float av[4] = {hs[gid * npad + kk + tig], hs[(gid + 8) * npad + kk + tig],
+                         hs[gid * npad + kk + tig + 4], hs[(gid + 8) * npad + kk + tig + 4]};
+    uint32_t ah[4], al[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_tf32(av[i], ah[i], al[i]);
+    uint32_t bh[8][2], bl[8][2];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+      if (nt < ntiles) {
+        const float *wr = ws + (nt * 8 + gid) * npad + kk;
+        split_tf32(wr[tig], bh[nt][0], bl[nt][0]);
+        split_tf32(wr[tig + 4], bh[nt][1], bl[nt][1]);
+      }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+      if (nt < ntiles) mma_tf32(acc[nt], al, bh[nt][0], bh[nt][1]);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+      if (nt < ntiles) mma_tf32(acc[nt], ah, bl[nt][0], bl[nt][1]);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+      if (nt < ntiles) mma_tf32(acc[nt], ah, bh[nt][0], bh[nt][1]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+    if (nt < ntiles)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        red[(w * 16 + gid + (i >= 2 ? 8 : 0)) * R8 + nt * 8 + 2 * tig + (i & 1)] = acc[nt][i];
+}
+// out[b * ldo + k] = sum over warps of red (fixed order), b < nb, k < R (after a __syncthreads)
+__device__ __forceinline__ void p_tile_sum(const float *red, int R8, int R, int nb, float *out, int64_t ldo) {
+  for (int o = threadIdx.x; o < nb * R; o += blockDim.x) {
+    const int b = o / R, k = o % R;
+    float v = red[b * R8 + k];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += red[(w * 16 + b) * R8 + k];
+    out[(int64_t)b * ldo + k] = v;
+  }
+}
+// zero a staged operand before its first use: the padding rows/columns the MMAs read
+__device__ __forceinline__ void zero_smem(float *p, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) p[i] = 0.f;
+}
+
+// one CTA per (segment, gate, 16-row block): h[rows, seg] and wf_g in shared memory, the
+// segment dots on the tensor cores (p_tile_3xtf32)
 __global__ void __launch_bounds__(256) k_gates_p(int64_t batch, int H, int n, int R, const float *h,
                                                  GateArgs a, float *P) {
   extern __shared__ float sm[];
   const int seg = blockIdx.x, g = blockIdx.y, s = H / n, K2 = s * R;
   const int64_t b0 = (int64_t)blockIdx.z * kPB;
   const int nb = (int)(batch - b0 < kPB ? batch - b0 : kPB);
-  const int npad = n + 4;  // 16-byte rows; float4 reads across k hit distinct bank quads
-  float *hs = sm, *ws = sm + kPB * npad;
+  const int npad = lstm_npad(n), n8 = (n + 7) / 8 * 8, R8 = (R + 7) / 8 * 8;
+  float *hs = sm, *ws = hs + kPB * npad, *red = ws + R8 * npad;
   const float *wfg = g == 0 ? a.wf[0] : g == 1 ? a.wf[1] : g == 2 ? a.wf[2] : a.wf[3];
+  zero_smem(sm, (kPB + R8) * npad);
+  __syncthreads();
   stage_rows(ws, npad, wfg, n, R, n);
   stage_rows(hs, npad, h + b0 * H + seg * n, H, nb, n);
   __syncthreads();
-  for (int o = threadIdx.x; o < nb * R; o += blockDim.x) {
-    const int b = o / R, k = o % R;
-    const float *hr = hs + b * npad, *wr = ws + k * npad;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int t = 0; t < n; t += 4) {  // same sums as element-wise, a quarter of the loads
-      const float4 hv = *reinterpret_cast<const float4 *>(hr + t);
-      const float4 wv = *reinterpret_cast<const float4 *>(wr + t);
-      acc[0] = fmaf(hv.x, wv.x, acc[0]);
-      acc[1] = fmaf(hv.y, wv.y, acc[1]);
-      acc[2] = fmaf(hv.z, wv.z, acc[2]);
-      acc[3] = fmaf(hv.w, wv.w, acc[3]);
-    }
-    P[((int64_t)g * batch + b0 + b) * K2 + seg * R + k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-  }
+  p_tile_3xtf32(hs, ws, npad, n8, R8, red);
+  __syncthreads();
+  p_tile_sum(red, R8, R, nb, P + ((int64_t)g * batch + b0) * K2 + seg * R, K2);
 }
 
 // one CTA per (64-column block, gate); each thread 4 rows x 4 columns of the block
@@ -241,7 +298,8 @@ int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *
   }
   const int H = (int)g.q, n = (int)g.n, R = (int)g.rank, s = (int)g.s, K2 = s * R;
   float *P = reinterpret_cast<float *>(ws);
-  const size_t smp = (size_t)(kPB + R) * (n + 4) * 4;
+  const int R8 = (R + 7) / 8 * 8;
+  const size_t smp = ((size_t)(kPB + R8) * ((n + 7) / 8 * 8 + 4) + (size_t)8 * 16 * R8) * 4;
   const size_t smy = (size_t)(kGB + 64) * (K2 + 4) * 4;
   static bool attr = false;
   if (!attr) {
@@ -258,15 +316,14 @@ int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *
 }  // namespace dt
 
 // =============================================================================================
-// The whole LSTM recurrence in ONE persistent kernel (config 4): T steps, two grid-wide
-// barriers per step, no host launches inside the loop. Work units (all exact fp32 FFMA):
-//   phase A, unit (gate g, segment seg, 16-row group rg):
-//     h[rows, seg cols] = cell(gx[t-1], gh, c) for t > 0 (0 at t = 0); gate 0's unit also
-//     writes c' (double-buffered) and the bf16 sequence output; then
-//     P_g[rows, seg*R + k] = h[rows, seg cols] . wf_g[k, :]
-//   phase B, unit (gate g, 64-column block): gh_g[:, cols] = P_g @ XF2_g[cols]^T + b_hg
-// After the last step one more phase A computes h[T-1]. Same arithmetic (and summation order)
-// as k_gates_p / k_gates_y / k_lstm_cell.
+// The whole LSTM recurrence in ONE persistent kernel (config 4): T steps, three grid-wide
+// barriers per step, no host launches inside the loop. Work units (3xTF32 tiles, fp32 cell):
+//   phase P, unit (gate g, segment seg, 16-row group rg):
+//     P_g[rows, seg*R + k] = h[rows, seg cols] . wf_g[k, :]        (p_tile_3xtf32)
+//   phase G, unit (gate g, 64-column block): gh_g[:, cols] = P_g @ XF2_g[cols]^T + b_hg
+//   phase C: the cell over all of B x H (c, h in place; the bf16 sequence output)
+// Same arithmetic (and summation order) as k_gates_p / k_gates_y / k_lstm_cell, so the
+// per-step form gives the same bits.
 // =============================================================================================
 namespace dt {
 namespace {
@@ -307,13 +364,13 @@ __device__ __forceinline__ float sigm_(float z) { return 1.f / (1.f + expf(-z));
 __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
   extern __shared__ float sm[];
   const int B = a.B, H = a.H, n = a.n, R = a.R, K2 = a.K2;
-  const int npad = n + 4, kp = K2 + 4;
+  const int npad = lstm_npad(n), n8 = (n + 7) / 8 * 8, R8 = (R + 7) / 8 * 8, kp = K2 + 4;
   const int rgs = (B + 15) / 16;
   const int unitsP = 4 * a.s * rgs, unitsB = 4 * ((H + 63) / 64);
   const int64_t BH = (int64_t)B * H;
   // one P unit and one gate-tile unit per CTA when the grid covers them: their factor operands
   // (wf_g, and the 64-column XF2_g block) stay resident in shared memory for all T steps
-  float *hs = sm, *ws = hs + 16 * npad, *ps = ws + R * npad;
+  float *hs = sm, *ws = hs + 16 * npad, *red = ws + R8 * npad, *ps = red + 128 * R8;
   ps += (4 - ((ps - sm) & 3)) & 3;  // 16-byte alignment for the staged tiles
   float *xs = ps + 64 * kp;
   const bool resP = unitsP <= (int)gridDim.x, resB = unitsB <= (int)gridDim.x;
@@ -324,6 +381,8 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
     stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, nj, K2);
     for (int i = nj * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) xs[i] = 0.f;
   };
+  zero_smem(sm, (16 + R8) * npad);  // padding rows/columns of the P tile's operands stay zero
+  __syncthreads();
   if (resP && (int)blockIdx.x < unitsP) stage_rows(ws, npad, wf_of((int)blockIdx.x / (a.s * rgs)), n, R, n);
   if (resB && (int)blockIdx.x < unitsB) stage_xs((int)blockIdx.x);
   unsigned target = 0;
@@ -359,20 +418,9 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       if (!resP) stage_rows(ws, npad, wf_of(g), n, R, n);
       stage_rows<true>(hs, npad, a.h + (size_t)b0 * H + seg * n, H, nb, n);
       __syncthreads();
-      for (int o = threadIdx.x; o < nb * R; o += blockDim.x) {
-        const int b = o / R, k = o % R;
-        const float *hr = hs + b * npad, *wr = ws + k * npad;
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int tt = 0; tt < n; tt += 4) {
-          const float4 hv = *reinterpret_cast<const float4 *>(hr + tt);
-          const float4 wv = *reinterpret_cast<const float4 *>(wr + tt);
-          acc[0] = fmaf(hv.x, wv.x, acc[0]);
-          acc[1] = fmaf(hv.y, wv.y, acc[1]);
-          acc[2] = fmaf(hv.z, wv.z, acc[2]);
-          acc[3] = fmaf(hv.w, wv.w, acc[3]);
-        }
-        a.P[((size_t)g * B + b0 + b) * K2 + seg * R + k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      }
+      p_tile_3xtf32(hs, ws, npad, n8, R8, red);
+      __syncthreads();
+      p_tile_sum(red, R8, R, nb, a.P + ((size_t)g * B + b0) * K2 + seg * R, K2);
     }
     stamp(t, 0);
     grid_barrier(a.bar, target);
@@ -402,9 +450,14 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
 
 }  // namespace
 
+// hs (16 rows) | ws (R8 rows) | P-tile partials (8 x 16 x R8) | align | ps, xs (64 rows each)
+static size_t lstm_seq_smem(const Geo &g) {
+  const size_t r8 = (g.rank + 7) / 8 * 8, npad = (g.n + 7) / 8 * 8 + 4;
+  return ((16 + r8) * npad + 128 * r8 + 4 + (size_t)128 * (g.s * g.rank + 4)) * 4;
+}
 bool lstm_seq_ok(const Geo &g, int64_t batch) {
   return lstm_gates_ok(g) && batch >= 1 && batch <= 64 && g.n <= 1024 &&
-         ((size_t)(16 + g.rank) * (g.n + 4) + 4 + (size_t)128 * (g.s * g.rank + 4)) * 4 <= 227 * 1024;
+         lstm_seq_smem(g) <= 227 * 1024;
 }
 size_t lstm_seq_ws(const Geo &g, int64_t batch) {
   return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * g.s * g.rank * 4 + (size_t)2 * batch * g.q * 4 + 256;
@@ -430,7 +483,7 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   a.out = reinterpret_cast<__nv_bfloat16 *>(out);
   DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));  // c(-1) = h(-1) = 0
   DT_CUDA_CHECK(cudaMemsetAsync(a.bar, 0, 256, st));
-  const size_t smem = ((size_t)(16 + a.R) * (a.n + 4) + 4 + (size_t)128 * (a.K2 + 4)) * 4;
+  const size_t smem = lstm_seq_smem(g);
   static bool attr = false;
   if (!attr) {
     DT_CUDA_CHECK(cudaFuncSetAttribute(k_lstm_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));

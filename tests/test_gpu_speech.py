@@ -88,8 +88,8 @@ def test_speech_graph_equals_eager_and_repeats(model):
 
 
 def test_lstm_gates_match_oracle(model):
-    """dt_lstm_gates (the four recurrent contractions of one step, exact fp32) against the
-    oracle's layer_forward per gate: rel_error <= 1e-5 (the FFMA contract)."""
+    """dt_lstm_gates (the four recurrent contractions of one step, 3xTF32 tensor-core tiles,
+    ~fp32 accuracy) against the oracle's layer_forward per gate: rel_error <= 1e-5."""
     import ctypes as C
     from paper_1802_06944_b200 import _lib
     m, orc = model
@@ -116,3 +116,60 @@ def test_speech_shape_errors(model):
     m, _ = model
     with pytest.raises(D.DimensionError):
         m.forward(torch.zeros(3, 2, 100, device="cuda"))
+
+
+@pytest.mark.parametrize("H,n,R,B,T", [(300, 60, 8, 5, 6), (256, 128, 4, 33, 4), (96, 12, 2, 64, 5),
+                                       (512, 256, 12, 17, 3)])
+def test_lstm_padded_geometries(H, n, R, B, T):
+    """Gate geometries off config 4's shape: n % 8 != 0 (segment dots padded to n8 with zeros),
+    rank % 8 != 0 (the P tile's rank rows padded), odd batch. Per gate against the oracle
+    (<= 1e-5), and the persistent recurrence (dt_lstm_sequence) bit-equal to the per-step form
+    (dt_lstm_gates + dt_lstm_cell) and within 1e-4 of the f64 cell recursion on its own gx."""
+    import ctypes as C
+    from paper_1802_06944_b200 import _lib
+    from test_gpu_forward import make_case
+    lib = _lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    cases = [make_case(H, H, R, n, H * H // n, 1, seed=40 + g, bias_sd=0.1) for g in range(4)]
+    ps = _lib.plan_struct(cases[0][2].plan)
+    P = lambda ts: (C.c_void_p * 4)(*[t.data_ptr() for t in ts])
+    xfs, wfs = P([c[2].xf for c in cases]), P([c[2].wf for c in cases])
+    bs_t = [torch.tensor(c[1]["bias"], dtype=torch.float32, device="cuda") for c in cases]
+    bs = P(bs_t)
+    rng = np.random.default_rng(H + B)
+    # gates of one step
+    h = rng.standard_normal((B, H)).astype(np.float32)
+    ht = torch.tensor(h, device="cuda")
+    gh = [torch.empty((B, H), device="cuda") for _ in range(4)]
+    wsg = torch.empty(lib.dt_lstm_gates_workspace_bytes(C.byref(ps), B), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.dt_lstm_gates(C.byref(ps), B, ht.data_ptr(), xfs, wfs, bs, P(gh), wsg.data_ptr(),
+                                 wsg.numel(), st))
+    for g, (plan, d, _) in enumerate(cases):
+        want = O.layer_forward(h.astype(np.float64), d["xf"], d["wf"], plan, d["bias"])
+        assert O.rel_error(gh[g].double().cpu().numpy(), want) <= 1e-5, g
+    # the recurrence: persistent kernel vs per-step kernels vs f64
+    gx = [torch.tensor(O.round_bf16(rng.standard_normal((T * B, H))), dtype=torch.float32,
+                       device="cuda").to(torch.bfloat16) for _ in range(4)]
+    need = lib.dt_lstm_sequence_workspace_bytes(C.byref(ps), B)
+    assert need > 0
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    out = torch.empty((T * B, H), dtype=torch.bfloat16, device="cuda")
+    _lib.check(lib.dt_lstm_sequence(C.byref(ps), T, B, P(gx), xfs, wfs, bs, out.data_ptr(),
+                                    ws.data_ptr(), ws.numel(), st))
+    c = torch.zeros((B, H), device="cuda")
+    h32 = torch.zeros((B, H), device="cuda")
+    steps = torch.empty_like(out)
+    for t in range(T):
+        _lib.check(lib.dt_lstm_gates(C.byref(ps), B, h32.data_ptr(), xfs, wfs, bs, P(gh),
+                                     wsg.data_ptr(), wsg.numel(), st))
+        _lib.check(lib.dt_lstm_cell(B, H, P([x[t * B:(t + 1) * B] for x in gx]), H, P(gh),
+                                    c.data_ptr(), h32.data_ptr(), steps[t * B:].data_ptr(), st))
+    torch.cuda.synchronize()
+    assert torch.equal(out, steps)
+    hh, cc = np.zeros((B, H)), np.zeros((B, H))
+    gxn = [x.double().cpu().numpy() for x in gx]
+    for t in range(T):
+        ghh = [O.layer_forward(hh, d["xf"], d["wf"], plan, d["bias"]) for plan, d, _ in cases]
+        hh, cc = O.lstm_cell([x[t * B:(t + 1) * B] for x in gxn], ghh, cc)
+        got = out[t * B:(t + 1) * B].double().cpu().numpy()
+        assert np.max(np.abs(got - hh)) <= 2 ** -8 + 1e-4, t  # bf16 output rounding
