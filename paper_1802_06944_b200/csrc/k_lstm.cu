@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "dt_internal.h"
+#include "sm100_ptx.cuh"
 
 namespace dt {
 namespace {
@@ -339,6 +340,7 @@ struct SeqArgs {
   unsigned *bar;               // grid barrier counter (zeroed before launch)
   unsigned long long *trace;   // DEEPTHIN_LSTM_TRACE: globaltimer stamps (block 0, first steps)
   int T, B, H, n, R, s, K2;
+  int vec;  // gx pointers 8-byte aligned (H % 4 == 0 always): vectorized cell
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
@@ -359,7 +361,32 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
   __syncthreads();
 }
 
+using namespace ptx;
+
 __device__ __forceinline__ float sigm_(float z) { return 1.f / (1.f + expf(-z)); }
+
+// Stage rows x cols fp32 (row pitch ld) into shared memory (row pitch sp) with 1-D bulk copies
+// (one per row, issued by the lanes of warp 0), completion counted on `bar`; every thread
+// waits. For data other CTAs wrote before the last grid barrier (P, h): the copies read L2
+// through the async proxy, ordered after the barrier's acquire by fence.proxy.async. Many
+// more bytes in flight than per-thread loads, so the 32-readers-per-line P broadcast no longer
+// waits on two serial L2 round trips.
+__device__ __forceinline__ void bulk_stage(float *dst, int sp, const float *src, int64_t ld, int rows,
+                                           int cols, uint64_t *bar, uint32_t &phase) {
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async_global();
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(bar, (uint32_t)(rows * cols * 4));
+    }
+    __syncwarp();
+    fence_proxy_async_global();
+    for (int r = threadIdx.x; r < rows; r += 32) bulk_load(dst + (size_t)r * sp, src + r * ld, cols * 4, bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+}
+
 
 __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
   extern __shared__ float sm[];
@@ -381,6 +408,13 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
     stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, nj, K2);
     for (int i = nj * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) xs[i] = 0.f;
   };
+  __shared__ uint64_t sbar[2];  // bulk_stage completion: [0] h rows (phase P), [1] P_g (phase G)
+  uint32_t sph[2] = {0u, 0u};
+  if (threadIdx.x == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+    fence_mbar_init();
+  }
   zero_smem(sm, (16 + R8) * npad);  // padding rows/columns of the P tile's operands stay zero
   __syncthreads();
   if (resP && (int)blockIdx.x < unitsP) stage_rows(ws, npad, wf_of((int)blockIdx.x / (a.s * rgs)), n, R, n);
@@ -390,12 +424,52 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 8) {
       unsigned long long v;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-      a.trace[t * 6 + k] = v;
+      a.trace[t * 8 + k] = v;
     }
   };
   // phase C: the cell of step t (all of B x H, grid-strided; each element owned by one thread)
   auto cell = [&](int t) {
     const size_t gxo0 = (size_t)t * BH;
+    if (a.vec) {  // 4 consecutive elements per thread: all nine loads in flight at once
+      const int64_t BH4 = BH / 4;
+      for (int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < BH4;
+           e4 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = 4 * e4;
+        float4 z[4];
+        uint2 xg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          z[q] = __ldcg(reinterpret_cast<const float4 *>(a.gh + q * BH + e));
+          xg[q] = __ldg(reinterpret_cast<const uint2 *>(a.gx[q] + gxo0 + e));
+        }
+        const float4 c4 = *reinterpret_cast<const float4 *>(a.c + e);
+        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+        float zz[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162 *>(&xg[q].x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162 *>(&xg[q].y);
+          zz[q][0] = __low2float(lo) + z[q].x;
+          zz[q][1] = __high2float(lo) + z[q].y;
+          zz[q][2] = __low2float(hi) + z[q].z;
+          zz[q][3] = __high2float(hi) + z[q].w;
+        }
+        float cn[4], hn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          cn[k] = sigm_(zz[1][k]) * cv[k] + sigm_(zz[0][k]) * tanhf(zz[2][k]);
+          hn[k] = sigm_(zz[3][k]) * tanhf(cn[k]);
+        }
+        *reinterpret_cast<float4 *>(a.c + e) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+        *reinterpret_cast<float4 *>(a.h + e) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+        __nv_bfloat162 o0 = __floats2bfloat162_rn(hn[0], hn[1]), o1 = __floats2bfloat162_rn(hn[2], hn[3]);
+        uint2 ov;
+        ov.x = *reinterpret_cast<uint32_t *>(&o0);
+        ov.y = *reinterpret_cast<uint32_t *>(&o1);
+        *reinterpret_cast<uint2 *>(a.out + gxo0 + e) = ov;
+      }
+      return;
+    }
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < BH;
          e += (int64_t)gridDim.x * blockDim.x) {
       const float zi = __bfloat162float(a.gx[0][gxo0 + e]) + a.gh[e];
@@ -416,7 +490,7 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       const int b0 = rg * 16, nb = min(16, B - b0);
       __syncthreads();
       if (!resP) stage_rows(ws, npad, wf_of(g), n, R, n);
-      stage_rows<true>(hs, npad, a.h + (size_t)b0 * H + seg * n, H, nb, n);
+      bulk_stage(hs, npad, a.h + (size_t)b0 * H + seg * n, H, nb, n, &sbar[0], sph[0]);
       __syncthreads();
       p_tile_3xtf32(hs, ws, npad, n8, R8, red);
       __syncthreads();
@@ -431,11 +505,14 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
       __syncthreads();
       if (!resB) stage_xs(u);
-      stage_rows<true>(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2);
+      bulk_stage(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2, &sbar[1], sph[1]);
       for (int i = B * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) ps[i] = 0.f;
       __syncthreads();
+      stamp(t, 6);
       float acc[4][4];
       tile64_3xtf32(ps, xs, kp, K2, acc);
+      __syncwarp();
+      stamp(t, 7);
       tile64_store(acc, a.gh + (size_t)g * BH, H, 0, B, j0, nj, bg);
     }
     stamp(t, 2);
@@ -457,7 +534,7 @@ static size_t lstm_seq_smem(const Geo &g) {
 }
 bool lstm_seq_ok(const Geo &g, int64_t batch) {
   return lstm_gates_ok(g) && batch >= 1 && batch <= 64 && g.n <= 1024 &&
-         lstm_seq_smem(g) <= 227 * 1024;
+         lstm_seq_smem(g) <= 226 * 1024;  // (+ the static mbarriers)
 }
 size_t lstm_seq_ws(const Geo &g, int64_t batch) {
   return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * g.s * g.rank * 4 + (size_t)2 * batch * g.q * 4 + 256;
@@ -474,6 +551,8 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   }
   a.T = (int)T; a.B = (int)batch; a.H = (int)g.q; a.n = (int)g.n; a.R = (int)g.rank;
   a.s = (int)g.s; a.K2 = (int)(g.s * g.rank);
+  a.vec = 1;
+  for (int i = 0; i < 4; ++i) a.vec &= (reinterpret_cast<uintptr_t>(gx[i]) & 7) == 0;
   char *cur = ws;
   a.gh = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * g.q * 4;
   a.P = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * a.K2 * 4;
@@ -486,7 +565,7 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   const size_t smem = lstm_seq_smem(g);
   static bool attr = false;
   if (!attr) {
-    DT_CUDA_CHECK(cudaFuncSetAttribute(k_lstm_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    DT_CUDA_CHECK(cudaFuncSetAttribute(k_lstm_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     attr = true;
   }
   int nsm = 148, dev = 0;
@@ -507,20 +586,21 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   static const bool tracing = getenv("DEEPTHIN_LSTM_TRACE") != nullptr;
   a.trace = nullptr;
   if (tracing) {
-    DT_CUDA_CHECK(cudaMalloc(&a.trace, 48 * 8));
-    DT_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 48 * 8, st));
+    DT_CUDA_CHECK(cudaMalloc(&a.trace, 64 * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 64 * 8, st));
   }
   DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_lstm_seq, a));
   if (tracing) {
-    unsigned long long h[48];
+    unsigned long long h[64];
     DT_CUDA_CHECK(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st));
     DT_CUDA_CHECK(cudaStreamSynchronize(st));
     cudaFree(a.trace);
     for (int t = 0; t < 8; ++t)
-      fprintf(stderr, "lstm step %d: P %.2f  bar %.2f  G %.2f  bar %.2f  cell %.2f  bar %.2f us\n", t,
-              t ? (h[t * 6] - h[t * 6 - 1]) * 1e-3 : 0.0, (h[t * 6 + 1] - h[t * 6]) * 1e-3,
-              (h[t * 6 + 2] - h[t * 6 + 1]) * 1e-3, (h[t * 6 + 3] - h[t * 6 + 2]) * 1e-3,
-              (h[t * 6 + 4] - h[t * 6 + 3]) * 1e-3, (h[t * 6 + 5] - h[t * 6 + 4]) * 1e-3);
+      fprintf(stderr, "lstm step %d: P %.2f  bar %.2f  G %.2f (stage %.2f tile %.2f)  bar %.2f  cell %.2f  bar %.2f us\n", t,
+              t ? (h[t * 8] - h[t * 8 - 3]) * 1e-3 : 0.0, (h[t * 8 + 1] - h[t * 8]) * 1e-3,
+              (h[t * 8 + 2] - h[t * 8 + 1]) * 1e-3, (h[t * 8 + 6] - h[t * 8 + 1]) * 1e-3,
+              (h[t * 8 + 7] - h[t * 8 + 6]) * 1e-3, (h[t * 8 + 3] - h[t * 8 + 2]) * 1e-3,
+              (h[t * 8 + 4] - h[t * 8 + 3]) * 1e-3, (h[t * 8 + 5] - h[t * 8 + 4]) * 1e-3);
   }
   return check_launch("lstm_seq");
 }
