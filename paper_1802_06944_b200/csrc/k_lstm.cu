@@ -353,8 +353,9 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
   __syncthreads();
   target += gridDim.x;
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    // release-add (cumulative over the CTA's writes ordered by the __syncthreads above); no
+    // separate fence and no returned value to wait for
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     while (ld_acquire_gpu(bar) < target) {
     }
   }
