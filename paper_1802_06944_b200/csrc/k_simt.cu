@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(256) k_reuse_small(int64_t batch, int64_t q, i
                                                      const XT *x, const float *xf, const float *wf,
                                                      const float *bias, int act, float act_arg,
                                                      void *y, int y_dtype) {
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) float sm[];
   // rows padded to a multiple of 4 floats + 4: 16-byte-aligned for cp.async, and the padding
   // staggers the banks of consecutive rows
   const int SR = s * rank, SRP = (SR + 3) / 4 * 4 + 4;
@@ -598,16 +598,25 @@ __global__ void __launch_bounds__(256) k_reuse_small(int64_t batch, int64_t q, i
     }
   }
   __syncthreads();
-  // 3) outputs j0 + jj: a thread per column, sequential SR-long dot, 4 partial sums
+  // 3) outputs j0 + jj: a thread per column, sequential SR-long dot, 4 partial sums. The
+  //    tile row and P are read as float4: consecutive threads' rows are SRP (= 4 mod 32) floats
+  //    apart, so scalar loads were 8-way bank conflicts; 16-byte loads of 8 threads cover 8
+  //    distinct 16-byte bank groups. Partial sum kk still takes k = kk mod 4 in order.
   for (int jj = tid; jj < RC; jj += 256) {
     const int64_t j = j0 + jj;
     if (j >= r_dim) break;
     const float *xr = X2 + jj * SRP;
+    const float4 *xr4 = reinterpret_cast<const float4 *>(xr);
+    const float4 *p4 = reinterpret_cast<const float4 *>(Ps);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     int k = 0;
-    for (; k + 4 <= SR; k += 4)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) acc[kk] = fmaf(Ps[k + kk], xr[k + kk], acc[kk]);
+    for (; k + 4 <= SR; k += 4) {
+      const float4 pv = p4[k >> 2], xv = xr4[k >> 2];
+      acc[0] = fmaf(pv.x, xv.x, acc[0]);
+      acc[1] = fmaf(pv.y, xv.y, acc[1]);
+      acc[2] = fmaf(pv.z, xv.z, acc[2]);
+      acc[3] = fmaf(pv.w, xv.w, acc[3]);
+    }
     for (; k < SR; ++k) acc[0] = fmaf(Ps[k], xr[k], acc[0]);
     float v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + (bias ? __ldg(bias + j) : 0.f);
     v = act_apply(act, v, act_arg);
