@@ -1,3 +1,4 @@
+#include <cstdlib>
 // fp32 CUDA-core (FFMA) kernels of the DeepThin hot path — the rtol-1e-5 path.
 //
 // Everything here is exact-fp32 arithmetic on CUDA cores. The contractions are
@@ -639,10 +640,18 @@ static bool reuse_small(const Geo &g, int64_t batch, const XT *x, const float *x
     return (size_t)((g.q + 3) / 4 * 4 + g.rank * ((g.n + 3) / 4 * 4 + 4) +
                     rc * ((SR + 3) / 4 * 4 + 4) + SR) * 4;
   };
-  int RC = 256;
-  while (RC > 32 && smem_for(RC) > 100 * 1024) RC /= 2;
+  // output columns per CTA (DEEPTHIN_REUSE_RC overrides the cap, for tuning sweeps)
+  static const int rc_cap = [] {
+    const char *e = getenv("DEEPTHIN_REUSE_RC");
+    const int v = e ? atoi(e) : 0;
+    return (v >= 32 && v <= 512) ? v : 256;
+  }();
+  // up to 256 columns: <= 100 KB so two CTAs share an SM; 512 columns: one CTA per SM
+  const size_t lim = rc_cap > 256 ? 200 * 1024 : 100 * 1024;
+  int RC = rc_cap;
+  while (RC > 32 && smem_for(RC) > lim) RC /= 2;
   const size_t smem = smem_for(RC);
-  if (smem > 100 * 1024) return false;
+  if (smem > lim) return false;
   const dim3 grid((unsigned)batch, (unsigned)((g.r_dim + RC - 1) / RC));
   cudaFuncSetAttribute(k_reuse_small<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_reuse_small<XT><<<grid, 256, smem, st>>>(batch, g.q, g.r_dim, (int)g.rank, g.n, (int)g.s, RC,
