@@ -409,7 +409,7 @@ def run_ours(args, cfg, key):
     # GEMM (programmatic dependent launch, W^T alternating between two workspace slots); every
     # step still regenerates its own W^T and the factors are constant. --no-pipeline disables.
     pipelined = mma == "bf16" and not args.no_pipeline
-    lib.dt_set_forward_pipeline(1 if pipelined else 0)
+    lib.dt_set_forward_pipeline(_lib.DT_PIPELINE_EXTERNAL_X if pipelined else 0)
     # clock ramp + sampler (the sampler runs through warm-up and the timed region)
     sampler = ClockSampler(local).__enter__()
     t0 = time.perf_counter()

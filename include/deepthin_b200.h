@@ -98,7 +98,12 @@ int dt_profile_kernel_kind(int kind);
  * dependent launch; W^T alternates between two workspace slots). The caller promises that the
  * factor buffers are not written while pipelined calls are in flight on the stream (a forward
  * never waits for a factor update launched after the previous forward). Every call still
- * regenerates its own W^T. Default 0. No reference counterpart (kernel.py has no pipelining). */
+ * regenerates its own W^T. Default 0. No reference counterpart (kernel.py has no pipelining).
+ * Mode 1 makes no promise about x: a call whose x is the previous call's output (a layer chain)
+ * waits for that call before loading x. Mode DT_PIPELINE_EXTERNAL_X also promises that no x
+ * is written by a call still in flight (independent inputs), so each call's first x stages load
+ * while the previous call is still running. */
+enum { DT_PIPELINE_OFF = 0, DT_PIPELINE_ON = 1, DT_PIPELINE_EXTERNAL_X = 2 };
 int dt_set_forward_pipeline(int enable);
 
 /* ---- geometry (host-only, no GPU needed) ---------------------------------- */

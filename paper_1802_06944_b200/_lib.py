@@ -18,6 +18,7 @@ DT_OK, DT_E_DIM, DT_E_ARG, DT_E_UNSUPPORTED, DT_E_CUDA, DT_E_FORMAT = range(6)
 DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64, DT_FACTORS_ROWS = 0, 1, 2, 3, 4
 DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
 DT_PROF_ANY, DT_PROF_GEMM, DT_PROF_ROWS = 0, 1, 2
+DT_PIPELINE_OFF, DT_PIPELINE_ON, DT_PIPELINE_EXTERNAL_X = 0, 1, 2
 ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
 
 # Every symbol the header declares (checked by tests/test_abi.py).

@@ -80,7 +80,7 @@ int check_act(int act) {
 thread_local void *const *g_prof_before = nullptr;
 thread_local void *const *g_prof_after = nullptr;
 thread_local int g_prof_n = 0, g_prof_used = 0, g_prof_kind = 0;
-thread_local bool g_pipeline = false;
+thread_local int g_pipeline = 0;
 
 }  // namespace
 
@@ -94,7 +94,8 @@ void dt::profile_next(cudaEvent_t *before, cudaEvent_t *after, int kind) {
   }
 }
 
-bool dt::forward_pipeline() { return g_pipeline; }
+bool dt::forward_pipeline() { return g_pipeline != 0; }
+bool dt::forward_pipeline_external_x() { return g_pipeline == DT_PIPELINE_EXTERNAL_X; }
 
 extern "C" {
 
@@ -105,7 +106,11 @@ const char *dt_last_error(void) { return g_last_error.c_str(); }
 int64_t dt_launch_counter(void) { return launch_count(); }
 
 int dt_set_forward_pipeline(int enable) {
-  g_pipeline = enable != 0;
+  if (enable < 0 || enable > DT_PIPELINE_EXTERNAL_X) {
+    set_error("dt_set_forward_pipeline: mode must be 0, 1 or DT_PIPELINE_EXTERNAL_X");
+    return DT_E_ARG;
+  }
+  g_pipeline = enable;
   return DT_OK;
 }
 

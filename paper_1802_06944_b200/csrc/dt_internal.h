@@ -131,6 +131,26 @@ size_t tc_backward_ws(const Geo &g, int64_t batch);
 void profile_next(cudaEvent_t *before, cudaEvent_t *after, int kind);
 // dt_set_forward_pipeline state of this thread.
 bool forward_pipeline();
+bool forward_pipeline_external_x();
+
+// Raise fn's dynamic shared-memory limit to at least `bytes` on the CURRENT device (function
+// attributes are per device context: a process driving several GPUs sets them on each).
+// Cached per (device, fn), thread-safe.
+int set_smem_limit(const void *fn, int bytes);
+// Allow non-portable cluster sizes for fn on the current device (once per (device, fn)).
+int allow_nonportable_clusters(const void *fn);
+
+// Timing-experiment switches (DEEPTHIN_DBG_*, DEEPTHIN_*_TRACE, DEEPTHIN_REGEN_SERIAL): some
+// drop work (stores, loads, a phase) and produce wrong outputs, so they exist only in builds
+// made with -DDEEPTHIN_TIMING_SWITCHES (python -m paper_1802_06944_b200.build --timing). The
+// product library reads none of them: DT_DBG_ENV is the constant 0 there.
+#ifdef DEEPTHIN_TIMING_SWITCHES
+#define DT_DBG_ENV(name) (getenv(name) ? atoi(getenv(name)) : 0)
+constexpr bool kTimingSwitches = true;
+#else
+#define DT_DBG_ENV(name) 0
+constexpr bool kTimingSwitches = false;
+#endif
 
 // Every kernel launch goes through check_launch, which also counts it (dt_launch_counter).
 int check_launch(const char *what);

@@ -302,12 +302,8 @@ int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *
   const int R8 = (R + 7) / 8 * 8;
   const size_t smp = ((size_t)(kPB + R8) * ((n + 7) / 8 * 8 + 4) + (size_t)8 * 16 * R8) * 4;
   const size_t smy = (size_t)(kGB + 64) * (K2 + 4) * 4;
-  static bool attr = false;
-  if (!attr) {
-    DT_CUDA_CHECK(cudaFuncSetAttribute(k_gates_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    DT_CUDA_CHECK(cudaFuncSetAttribute(k_gates_y, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(k_gates_p), 227 * 1024)) return rc;
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(k_gates_y), 227 * 1024)) return rc;
   k_gates_p<<<dim3((unsigned)s, 4, (unsigned)((batch + kPB - 1) / kPB)), 256, smp, st>>>(batch, H, n, R, h, a, P);
   if (int rc = check_launch("lstm_gates_p")) return rc;
   k_gates_y<<<dim3((unsigned)((H + 63) / 64), 4), 256, smy, st>>>(batch, H, K2, P, a);
@@ -564,11 +560,7 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));  // c(-1) = h(-1) = 0
   DT_CUDA_CHECK(cudaMemsetAsync(a.bar, 0, 256, st));
   const size_t smem = lstm_seq_smem(g);
-  static bool attr = false;
-  if (!attr) {
-    DT_CUDA_CHECK(cudaFuncSetAttribute(k_lstm_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
-    attr = true;
-  }
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(k_lstm_seq), 226 * 1024)) return rc;
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -584,7 +576,7 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  static const bool tracing = getenv("DEEPTHIN_LSTM_TRACE") != nullptr;
+  static const bool tracing = DT_DBG_ENV("DEEPTHIN_LSTM_TRACE") != 0;
   a.trace = nullptr;
   if (tracing) {
     DT_CUDA_CHECK(cudaMalloc(&a.trace, 64 * 8));

@@ -21,6 +21,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <set>
+
 #include <algorithm>
 #include <atomic>
 #include <type_traits>
@@ -675,6 +679,33 @@ int check_launch(const char *what) {
 }
 
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void *>, int> g_smem_set;       // (device, fn) -> bytes set
+std::set<std::pair<int, const void *>> g_nonportable_set;     // (device, fn)
+}  // namespace
+
+int set_smem_limit(const void *fn, int bytes) {
+  int dev = 0;
+  DT_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  int &have = g_smem_set[{dev, fn}];
+  if (have < bytes) {
+    DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+  }
+  return DT_OK;
+}
+
+int allow_nonportable_clusters(const void *fn) {
+  int dev = 0;
+  DT_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  if (g_nonportable_set.insert({dev, fn}).second)
+    DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  return DT_OK;
+}
 
 // ---- forward ------------------------------------------------------------------------
 static size_t ffma_forward_carve(const Geo &g, int64_t batch, char *base, float **P, float **part,

@@ -70,6 +70,7 @@ struct RegenArgs {
   int64_t q, r_dim, ldw;
   int rank, n, a_rows, f_dtype;
   int chain;  // pipelined forward: complete only after the previous grid (griddepcontrol.wait)
+  int x_ext;  // pipelined forward with external inputs: x is never written by an in-flight grid
   const void *xf, *wf;
   __nv_bfloat16 *wt;
 };
@@ -113,6 +114,11 @@ struct GemmParams {
   uint32_t off_fs;
   RegenArgs rg;
   int chain;  // pipelined forward: let the next call's phase 1 launch right away
+  // x may be loaded before griddepcontrol.wait: not chained (the grids ahead of phase 1 have
+  // completed), or chained with inputs the caller declared external (DT_PIPELINE_EXTERNAL_X).
+  // A chained forward whose x is the previous layer's output waits first: that layer's GEMM
+  // may still be writing it (it signals its dependents right after its prologue).
+  int x_early;
   int dbg;  // DEEPTHIN_DBG_GEMM (timing experiments only): 1 skip y stores, 2 x loads after the first S stages skipped, 4 skip TMEM loads
   unsigned long long *trace;  // DEEPTHIN_TC_TRACE: per-CTA globaltimer stamps
 };
@@ -427,7 +433,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t slice_rows = GN / cs, slice_bytes = kXBytes / cs;
       int stage = 0, jg_cur = -1, u = 0;
       uint32_t phase = 0, wf_phase = 0;
-      // x does not depend on phase 1: the first stages' x loads go out before griddep_wait.
+      // x does not depend on phase 1: the first stages' x loads go out before griddep_wait
+      // (unless x may still be in flight from a chained predecessor, see x_early).
+      if (!p.x_early) griddep_wait();
       const int pre = min(p.S, p.KB);
       for (int it = beg; it < end; ++it) {
         const int jg = it / p.n_bt, j0 = jb_of(it) * GM, b0 = b0_of(it);
@@ -535,13 +543,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int c32 = part; c32 < GN / 32; c32 += kEpiParts) {
         if (32 * c32 >= nrows) break;
         uint32_t v[32];
-        if (p.dbg & 4) {
+        if (kTimingSwitches && (p.dbg & 4)) {
           for (int r = 0; r < 32; ++r) v[r] = 0;
         } else {
           tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
           tmem_ld_wait();
         }
-        if (jok && !(p.dbg & 1)) {
+        if (jok && !(kTimingSwitches && (p.dbg & 1))) {
           OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - 32 * c32;
           if constexpr (YDT == YDT_MSE) {  // grad = scale * (z - t), sum (z - t)^2
@@ -893,7 +901,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   };
   auto issue_x = [&](int it, int kb) {
     const int xb0 = b0_of(it) + (int)crank * (GN / 2);
-    if ((p.dbg & 2) && pu >= p.S) {  // timing experiment: stale x, no L2 traffic
+    if (kTimingSwitches && (p.dbg & 2) && pu >= p.S) {  // timing experiment: stale x, no L2 traffic
       if (leader) mbar_arrive(&full[pstage]);
     } else {
       if (leader) mbar_arrive_expect_tx(&full[pstage], 2 * kXHalf);
@@ -902,8 +910,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ++pu;
     if (++pstage == p.S) { pstage = 0; pphase ^= 1; }
   };
-  if (producer && beg < end)
+  if (producer && beg < end) {
+    if (!p.x_early && !p.wgen && !p.fused) griddep_wait();  // x may be a chained predecessor's output
     for (int kb = 0; kb < pre; ++kb) issue_x(beg, kb);  // fresh stages: no empty wait
+  }
 
   if (p.fused) {
     // ---------------- phase 1 inside the kernel: W^T tiles on the epilogue warps ----------
@@ -1045,13 +1055,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int c32 = part; c32 < GN / 32; c32 += kEpiParts) {
         if (32 * c32 >= nrows) break;
         uint32_t v[32];
-        if (p.dbg & 4) {
+        if (kTimingSwitches && (p.dbg & 4)) {
           for (int r = 0; r < 32; ++r) v[r] = 0;
         } else {
           tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(acc * GN + c32 * 32), v);
           tmem_ld_wait();
         }
-        if (jok && !(p.dbg & 1)) {
+        if (jok && !(kTimingSwitches && (p.dbg & 1))) {
           OutT *yp = reinterpret_cast<OutT *>(p.y) + (b0 + 32 * c32) * p.ldy + j;
           const int rmax = nrows - 32 * c32;
           if constexpr (YDT == YDT_MSE) {  // grad = scale * (z - t), sum (z - t)^2
@@ -1287,7 +1297,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   p.cpj = p.ncl >= p.n_jg ? std::min(p.ncl / p.n_jg, p.n_bt) : 0;
   if (p.cpj > 0) p.ncl = p.cpj * p.n_jg;
   const int grid = p.ncl * p.csize;
-  static const bool tracing = getenv("DEEPTHIN_TC_TRACE") != nullptr;
+  static const bool tracing = DT_DBG_ENV("DEEPTHIN_TC_TRACE") != 0;
   unsigned long long *tbuf = nullptr;
   if (tracing) {
     DT_CUDA_CHECK(cudaMalloc(&tbuf, (size_t)grid * kTrace * 8));
@@ -1296,7 +1306,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
 
   // DEEPTHIN_DBG_PHASE=1 / 2: launch only phase 1 / phase 2 (timing experiments only — the
   // output is wrong).
-  static const int dbg_phase = getenv("DEEPTHIN_DBG_PHASE") ? atoi(getenv("DEEPTHIN_DBG_PHASE")) : 0;
+  static const int dbg_phase = DT_DBG_ENV("DEEPTHIN_DBG_PHASE");
   // DEEPTHIN_GEMM_FUSED=1: phase 1 inside the (cooperatively launched) pair kernel, a grid
   // barrier between the phases (a refused cooperative launch falls back to two kernels).
   // Measured slower than the two-kernel form at BASELINE config 2 (20.2 vs 18.7 us/step: the
@@ -1315,7 +1325,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   p.r_dim = (int)c.cols;
   p.ldy = (int)c.ldy;
   p.trace = tbuf;
-  static const int dbg_gemm = getenv("DEEPTHIN_DBG_GEMM") ? atoi(getenv("DEEPTHIN_DBG_GEMM")) : 0;
+  static const int dbg_gemm = DT_DBG_ENV("DEEPTHIN_DBG_GEMM");
   p.dbg = dbg_gemm;
   p.bias = c.bias;
   p.y = c.y;
@@ -1333,6 +1343,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
     rgrid = dim3((unsigned)((rg.a_rows + RG_R - 1) / RG_R), (unsigned)((rg.n + RG_C - 1) / RG_C));
     p.rg = rg;
     p.chain = rg.chain;
+    p.x_early = (!rg.chain || rg.x_ext) ? 1 : 0;
     // fused phase 1: 64-row tiles when that makes one tile per CTA, else 32-row tiles
     p.rg_rows = ((rg.a_rows + 63) / 64) * (int64_t)rgrid.y <= (int64_t)grid ? 64 : 32;
     p.rg_ux = (int)((rg.a_rows + p.rg_rows - 1) / p.rg_rows);
@@ -1340,9 +1351,9 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   }
   const int eact = c.act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : c.act;
   GemmFn fn = pick_gemm(c.y_dtype, eact, pair, c.el);
-  DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(fn), (int)smem_bytes)) return rc;
   if (p.csize > 8)
-    DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (int rc = allow_nonportable_clusters(reinterpret_cast<const void *>(fn))) return rc;
 
   static const int use_pdl = getenv("DEEPTHIN_PDL") ? atoi(getenv("DEEPTHIN_PDL")) : 1;
   cudaLaunchConfig_t cfg{};
@@ -1672,6 +1683,7 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
   rg.f_dtype = f_dtype;
   rg.xf = xf; rg.wf = wf; rg.wt = wt;
   rg.chain = pipe ? 1 : 0;
+  rg.x_ext = forward_pipeline_external_x() ? 1 : 0;
   GemmCall c{xt, ldx, batch, g.q, wt, ldw, g.r_dim, bias, act, act_arg,
              y, g.r_dim, y_dtype, &rg, true};
   if (mse) {

@@ -285,7 +285,7 @@ __device__ void regen_readout(const TcParams &p, int cb, uint32_t w_s, uint64_t 
     const int a = b.a_first + 128 * pass + L;
     const int a_warp = b.a_first + 128 * pass + 32 * wq;  // this warp's rows: a_warp .. +31
     const uint32_t tcol = tbase + ((uint32_t)(32 * wq) << 16) + (uint32_t)(slot * p.Nc);
-    if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo && p.dbg_regen != 3) {  // skip all-invalid warps
+    if (a_warp <= b.a_hi && a_warp + 31 >= b.a_lo && (!kTimingSwitches || p.dbg_regen != 3)) {  // skip all-invalid warps
       // this warp's column groups: part, part + kParts, ... (32 columns each)
       const int f0 = (int)((int64_t)a * n + c0 + 32 * part - b.fbeg);
       int jj = f0 >= 0 ? f0 / q : -((-f0 + q - 1) / q);
@@ -300,7 +300,7 @@ __device__ void regen_readout(const TcParams &p, int cb, uint32_t w_s, uint64_t 
           asm volatile("" ::"r"(v[0] ^ v[31]));
           trace(p, 32 + 2 * g);
         }
-        if (row_ok && col0 < cols && p.dbg_regen != 1)
+        if (row_ok && col0 < cols && (!kTimingSwitches || p.dbg_regen != 1))
           scatter32<MODE>(v, w_s, p.w_sbo, jj, i, q, cols - col0, b.jrows);
         if (p.trace && et == 0 && s == 0 && g < 3) trace(p, 33 + 2 * g);
         i += 32 * kParts;
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           regen_pending = true;
         }
         for (int kb = 0; kb < p.KB; ++kb) {
-          if ((stage >= p.S_ded || p.dbg_regen == 4) && regen_pending) {
+          if ((stage >= p.S_ded || (kTimingSwitches && p.dbg_regen == 4)) && regen_pending) {
             // this stage aliases the regeneration operands of every CTA it multicasts into
             mbar_wait_sleepy(cregen, (uint32_t)(n_cbs - 1) & 1u);
             regen_pending = false;
@@ -1144,9 +1144,9 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   p.bias = bias;
   p.y = y;
   p.arg = act_arg;
-  static const int dbg_serial = getenv("DEEPTHIN_REGEN_SERIAL") != nullptr;
+  static const int dbg_serial = DT_DBG_ENV("DEEPTHIN_REGEN_SERIAL");
   p.dbg_serial = dbg_serial;
-  static const int dbg_regen = getenv("DEEPTHIN_DBG_REGEN") ? atoi(getenv("DEEPTHIN_DBG_REGEN")) : 0;
+  static const int dbg_regen = DT_DBG_ENV("DEEPTHIN_DBG_REGEN");
   p.dbg_regen = dbg_regen;
   p.off_w = L.off_w; p.off_x = L.off_x; p.off_ar = L.off_ar; p.off_br = L.off_br;
   p.off_bar = L.off_bar;
@@ -1157,7 +1157,7 @@ int tc_general_forward(const Geo &g, int64_t batch, const void *x, int x_dtype,
   DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
 
   // Debug: DEEPTHIN_TC_TRACE=1 records per-CTA globaltimer stamps and prints a phase summary.
-  static const bool tracing = getenv("DEEPTHIN_TC_TRACE") != nullptr;
+  static const bool tracing = DT_DBG_ENV("DEEPTHIN_TC_TRACE") != 0;
   unsigned long long *tbuf = nullptr;
   if (tracing) {
     DT_CUDA_CHECK(cudaMalloc(&tbuf, (size_t)grid * kTraceSlots * 8));

@@ -30,6 +30,9 @@
 
 #include <algorithm>
 #include <unordered_map>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 
@@ -854,14 +857,8 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
                                     (uint64_t)p.k2 * 4, 32, kNc, true))
     return rc;
   RowsFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(act) : pick_act<DT_F32>(act);
-  {  // the opt-in shared-memory size once per kernel instance (host cost per call otherwise)
-    thread_local std::unordered_map<const void *, uint32_t> set_smem;
-    uint32_t &have = set_smem[reinterpret_cast<const void *>(fn)];
-    if (have < smem_bytes) {
-      DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-      have = smem_bytes;
-    }
-  }
+  // the opt-in shared-memory size once per (device, kernel instance)
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(fn), (int)smem_bytes)) return rc;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kRowsThreads);
   cfg.dynamicSmemBytes = smem_bytes;
@@ -876,21 +873,29 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   // persistent: as many clusters as fit at once (each loops over row tiles)
-  static int max_cl[9] = {0};
-  if (!max_cl[p.cs]) {
-    if (p.cs > 1)
-      DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    cfg.gridDim = dim3((unsigned)(p.cs * 64));
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl <= 0) {
-      (void)cudaGetLastError();
-      ncl = g_nsm() / p.cs;
+  // (occupancy per (device, kernel instance, cluster size), queried once)
+  static std::mutex occ_mu;
+  static std::map<std::tuple<int, const void *, int>, int> occ;
+  int max_cl = 0;
+  {
+    int dev = 0;
+    DT_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(occ_mu);
+    int &slot = occ[std::make_tuple(dev, reinterpret_cast<const void *>(fn), p.cs)];
+    if (!slot) {
+      cfg.gridDim = dim3((unsigned)(p.cs * 64));
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n <= 0) {
+        (void)cudaGetLastError();
+        n = g_nsm() / p.cs;
+      }
+      slot = n;
     }
-    max_cl[p.cs] = ncl;
+    max_cl = slot;
   }
-  const int ncl = std::max(1, std::min(p.n_tiles, max_cl[p.cs]));
+  const int ncl = std::max(1, std::min(p.n_tiles, max_cl));
   cfg.gridDim = dim3((unsigned)(ncl * p.cs));
-  static const bool tracing = getenv("DEEPTHIN_ROWS_TRACE") != nullptr;
+  static const bool tracing = DT_DBG_ENV("DEEPTHIN_ROWS_TRACE") != 0;
   if (tracing) {
     DT_CUDA_CHECK(cudaMalloc(&p.trace, 8 * kTr * 8));
     DT_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 8 * kTr * 8, st));

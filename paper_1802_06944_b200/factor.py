@@ -32,6 +32,14 @@ class FactorPair:
 
     def __post_init__(self):
         host = not isinstance(self.xf, torch.Tensor)
+        # the reference keeps float64 factors as float64 (core.as_matrix, factor.py:42-50) and
+        # serializes them as such (model_io.py:100-110): remember the source dtype, and for
+        # float64 sources a host float64 copy, so an untrained pair round-trips bit-exactly
+        src = _source_dtype(self.xf, self.wf)
+        if src == np.float64:
+            self._cache["source64"] = tuple(
+                np.array(_host64(a), dtype=np.float64, copy=True) for a in (self.xf, self.wf))
+        self._cache["source_dtype"] = src
         xf, _ = as_device_matrix(self.xf, name="xf", keep_bf16=False)
         wf, _ = as_device_matrix(self.wf, name="wf", keep_bf16=False)
         p = self.plan
@@ -123,8 +131,22 @@ class FactorPair:
             self._cache[key] = (buf, bias)
         return self._cache[key][0]
 
+    @property
+    def source_dtype(self) -> np.dtype:
+        """The dtype the reference would hold these factors in (float32 or float64)."""
+        return np.dtype(self._cache.get("source_dtype", np.float32))
+
+    def host_values(self) -> tuple[np.ndarray, np.ndarray]:
+        """(xf, wf) in source_dtype for serialization: the untouched float64 source while the
+        device masters were never updated, else the device values widened."""
+        if "source64" in self._cache:
+            return self._cache["source64"]
+        dt = self.source_dtype
+        return tuple(t.detach().float().cpu().numpy().astype(dt) for t in (self.xf, self.wf))
+
     def refresh_derived(self) -> None:
         """Re-derive the cached bf16 / packed copies after the fp32 masters changed (SGD)."""
+        self._cache.pop("source64", None)  # the masters moved on from the float64 source
         lib = _lib.lib()
         if "bf16" in self._cache:
             for src, dst in zip((self.xf, self.wf), self._cache["bf16"]):
@@ -188,3 +210,21 @@ def decompress(fp: FactorPair):
     _lib.check(_lib.lib().dt_decompress(C.byref(_lib.plan_struct(p)), fp.xf.data_ptr(),
                                         fp.wf.data_ptr(), w.data_ptr(), stream_handle()))
     return w.cpu().numpy() if fp.from_numpy else w
+
+
+def _source_dtype(*arrays) -> np.dtype:
+    """core.as_matrix's dtype rule (core.py:21-36): float32 stays float32 only when every
+    input is float32 (bf16 tensors count as float32), anything else is float64."""
+    f32 = True
+    for a in arrays:
+        if isinstance(a, torch.Tensor):
+            f32 &= a.dtype in (torch.float32, torch.bfloat16)
+        else:
+            f32 &= np.asarray(a).dtype == np.float32
+    return np.dtype(np.float32 if f32 else np.float64)
+
+
+def _host64(a) -> np.ndarray:
+    if isinstance(a, torch.Tensor):
+        return a.detach().cpu().numpy()
+    return np.asarray(a)

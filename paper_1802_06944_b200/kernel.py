@@ -5,8 +5,13 @@ meaning and errors, and route to the sm_100a kernels through dt_forward:
 
 * reuse path (n | q): every distinct run dot is computed once per input row
   (P = x.view(B*s, n) @ wf^T) and combined with xf (scale-after-dot);
-* general path (straddling rows): W tiles are regenerated from the factors
-  on chip and contracted without W ever touching HBM.
+* general path (straddling rows): W^T is regenerated from the factors on
+  every call and contracted on tcgen05. The default two-phase form writes the
+  bf16 W^T (2*q*r_dim bytes, 1.8 MB at config 2) to a workspace slot that
+  stays L2-resident between the two kernels (it does reach HBM on write-back);
+  the opt-in in-CTA form (DEEPTHIN_GEMM_WGEN=1) keeps every W block inside the
+  SM. Nothing dense persists across calls: the layer's parameters in HBM are
+  the factors.
 
 Deliberate extensions: every rank is fused (the reference's rank-1 limit,
 kernel.py:238-240, and its decompress fallback warning, :313-319, are
@@ -114,13 +119,17 @@ def resolve_mma(mma, x: torch.Tensor, plan) -> int:
 class forward_pipeline:
     """Context manager / switch for inference pipelining on this thread (dt_set_forward_pipeline):
     consecutive bf16 tensor-core forwards on one stream overlap each call's W regeneration with
-    the previous call's GEMM. Only for factors that are not updated while the calls run."""
+    the previous call's GEMM. Only for factors that are not updated while the calls run.
+    ``external_x=True`` also promises that no call's input is produced by a call still in
+    flight (independent batches, not a layer chain): the first x stages then load early too."""
 
-    def __init__(self, enable: bool = True):
+    def __init__(self, enable: bool = True, external_x: bool = False):
         self.enable = enable
+        self.external_x = external_x
 
     def __enter__(self):
-        _lib.lib().dt_set_forward_pipeline(1 if self.enable else 0)
+        mode = (_lib.DT_PIPELINE_EXTERNAL_X if self.external_x else 1) if self.enable else 0
+        _lib.check(_lib.lib().dt_set_forward_pipeline(mode))
         return self
 
     def __exit__(self, *exc):

@@ -169,8 +169,13 @@ class DeviceModel:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 y = self.forward(x, out_dtype)
-            graphs[key] = (g, y)
-        g, y = graphs[key]
+            # the graph holds raw pointers into the workspaces (and chain buffers) it captured:
+            # keep those tensors alive with it, so a later call that grows and replaces a
+            # workspace cannot hand the old memory to the allocator while the graph may replay
+            refs = [w for w in self._ws if w is not None] + list(self.__dict__.get("_bufs", []))
+            refs += list(self.__dict__.get("_flags", []))
+            graphs[key] = (g, y, refs)
+        g, y, _ = graphs[key]
         g.replay()
         return y
 

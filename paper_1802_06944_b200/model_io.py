@@ -102,6 +102,10 @@ class CompressedModel:
     def _image_current(self) -> bool:
         if getattr(self, "_stamp", None) != self._snapshot():
             return False
+        # only read-only factors can be trusted unchanged (device FactorPairs are updated in
+        # place by SGD under the same Python object)
+        if not all(isinstance(fp, StoredFactors) for fp in self.factors):
+            return False
         for rec, bias in zip(self._index, self.biases):
             dt = _STORED[rec.dtype_code]
             stored = np.frombuffer(self._image, dtype=dt, count=rec.bias_len, offset=rec.bias_offset)
@@ -124,7 +128,13 @@ def _host(a) -> np.ndarray:
 
 
 def _stored_dtype(fp) -> np.dtype:
+    if hasattr(fp, "source_dtype"):  # device FactorPair: the dtype its source had
+        return fp.source_dtype
     return np.dtype(_host(fp.xf[:0]).dtype) if hasattr(fp.xf, "detach") else np.dtype(fp.dtype)
+
+
+def _factor_values(fp):
+    return fp.host_values() if hasattr(fp, "host_values") else (fp.xf, fp.wf)
 
 
 def _layer_bytes(name: str, plan: LayerPlan, item: int, bias_len: int) -> int:
@@ -181,8 +191,9 @@ def serialize(model: CompressedModel) -> bytes:
         struct.pack_into("<5QBBQ", buf, pos, plan.q, plan.r_dim, plan.rank, plan.m, plan.n,
                          _STORED.index(dt), int(name in floors), bias.size)
         pos += 5 * 8 + 2 + 8
-        put_array(fp.xf, dt)
-        put_array(fp.wf, dt)
+        xv, wv = _factor_values(fp)
+        put_array(xv, dt)
+        put_array(wv, dt)
         put_array(bias, dt)
     assert pos == len(buf)
     struct.pack_into("<4sIIQd", buf, 0, MAGIC, model.format_version, len(model.factors),

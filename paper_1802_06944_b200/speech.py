@@ -175,6 +175,9 @@ class SpeechRNN:
             with torch.cuda.graph(cg):
                 self._steps(st, T, B)
             st["graph"] = cg
+            # the graph keeps raw pointers into these workspaces: hold them with it (a later
+            # eager call with a larger batch replaces self._ws entries, never these tensors)
+            st["ws_refs"] = list(self._ws.values())
             st["c"].zero_()
             st["h"].zero_()
         if graph:

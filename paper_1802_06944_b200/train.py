@@ -44,6 +44,10 @@ class DeepThinLayer:
         self.param_flat[ob:ob + plan.r_dim].copy_(b)
         self.fp = FactorPair.adopt(self.param_flat[ox:ox + nx].view(plan.m, plan.rank),
                                    self.param_flat[ow:ow + nw].view(plan.rank, plan.n), plan)
+        # serialization keeps the source's dtype (and, until the first step, its exact values)
+        self.fp._cache["source_dtype"] = src.source_dtype
+        if "source64" in src._cache:
+            self.fp._cache["source64"] = src._cache["source64"]
         self.bias = self.param_flat[ob:ob + plan.r_dim]
         self.d_xf = self.grad_flat[ox:ox + nx].view(plan.m, plan.rank)
         self.d_wf = self.grad_flat[ow:ow + nw].view(plan.rank, plan.n)

@@ -192,3 +192,93 @@ def test_graph_forward_equals_eager():
     x.copy_(torch.randn(700, 440, device="cuda").to(torch.bfloat16))  # same buffer, new data
     want2 = dm.forward(x, out_dtype=torch.bfloat16)
     assert torch.equal(dm.forward(x, out_dtype=torch.bfloat16, graph=True), want2)
+
+
+def chain_model(dims, ns, seed=7):
+    rng = np.random.default_rng(seed)
+    entries, factors, biases = [], [], []
+    for i, n in enumerate(ns):
+        q, r_dim = dims[i], dims[i + 1]
+        m = -(-(q * r_dim) // n)
+        plan = D.LayerPlan(q=q, r_dim=r_dim, rank=3, m=m, n=n)
+        entries.append((f"fc{i}", plan))
+        factors.append(mi.StoredFactors(rng.normal(0, 3 ** -0.5, (m, 3)).astype(np.float32),
+                                        rng.normal(0, 3 ** -0.5, (3, n)).astype(np.float32), plan))
+        biases.append(rng.normal(0, 0.01, r_dim).astype(np.float32))
+    plans = D.NetworkPlan(layers=tuple(entries), target_ratio=0.01, achieved_total_ratio=0.0,
+                          floor_hits=())
+    return mi.CompressedModel(plans=plans, factors=factors, biases=biases)
+
+
+@pytest.mark.parametrize("rows", [300, 8192])
+def test_pipelined_chain_with_back_to_back_general_layers_is_exact(rows):
+    """with inference pipelining a layer's GEMM signals its dependents right
+    after its prologue, so the next layer (W regeneration, then its GEMM) starts while the
+    current one still writes its output. A general-path GEMM whose x is that output must wait
+    before loading x. Chain: general -> general -> row-tile reuse -> general, pipelined vs
+    serial, bit for bit, repeated (a race shows up as a mismatch on some call)."""
+    model = chain_model([440, 560, 2048, 2048, 1000], [320, 320, 256, 320])
+    assert [p.reuse_path for _, p in model.plans.layers] == [False, False, True, False]
+    acts = ["sigmoid", "tanh", "sigmoid", "identity"]
+    serial = model.to_device(acts, mma="bf16", pipeline=False)
+    piped = model.to_device(acts, mma="bf16", pipeline=True)
+    x = torch.randn(rows, 440, device="cuda").to(torch.bfloat16)
+    want = serial.forward(x)
+    for _ in range(6):
+        got = piped.forward(x)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
+    for _ in range(3):  # graph replay of the pipelined chain
+        got = piped.forward(x, graph=True)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
+
+
+def test_external_x_pipeline_mode_matches_serial():
+    """DT_PIPELINE_EXTERNAL_X (independent inputs, the bench's mode): back-to-back forwards of
+    one layer over rotating buffers give the serial bits."""
+    plan = D.LayerPlan(q=440, r_dim=2048, rank=24, m=2816, n=320)
+    rng = np.random.default_rng(1)
+    fp = D.FactorPair(rng.normal(0, 0.2, (2816, 24)), rng.normal(0, 0.2, (24, 320)), plan)
+    bias = rng.normal(0, 0.01, 2048)
+    xs = [torch.randn(4096, 440, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    want = [D.layer_forward(x, fp, bias, mma="bf16") for x in xs]
+    from paper_1802_06944_b200.kernel import forward_pipeline
+    with forward_pipeline(True, external_x=True):
+        got = [D.layer_forward(x, fp, bias, mma="bf16") for x in xs * 3]
+    torch.cuda.synchronize()
+    for k, g in enumerate(got):
+        assert torch.equal(g, want[k % 3])
+
+
+def test_gpu_factor_pair_float64_round_trips_through_dthn():
+    """a model whose layers are device FactorPairs built from float64
+    factors serializes them as float64 (dtype code 1), bit-exact, like the reference
+    (model_io.py:100-110); after an SGD step the file carries the updated values, not a
+    stale image."""
+    rng = np.random.default_rng(11)
+    plan = D.LayerPlan(q=12, r_dim=40, rank=2, m=40, n=12)
+    xf, wf = rng.standard_normal((40, 2)), rng.standard_normal((2, 12))
+    fp = D.FactorPair(xf, wf, plan)
+    assert fp.source_dtype == np.float64
+    bias = rng.standard_normal(40)
+    model = mi.CompressedModel(plans=D.NetworkPlan(layers=(("fc0", plan),), target_ratio=1.0,
+                                                   achieved_total_ratio=0.0, floor_hits=()),
+                               factors=[fp], biases=[bias])
+    back = mi.deserialize(mi.serialize(model))
+    assert back.factors[0].xf.dtype == np.float64
+    assert np.array_equal(back.factors[0].xf, xf) and np.array_equal(back.factors[0].wf, wf)
+    assert mi.expected_file_size(model) == len(mi.serialize(model))
+    img0 = model.image()[0]
+    layer = D.DeepThinLayer(plan, xf, wf, bias, mma="ffma")
+    model2 = mi.CompressedModel(plans=model.plans, factors=[layer.fp], biases=[bias])
+    img_a = model2.image()[0]
+    x = torch.randn(8, 12, device="cuda")
+    t = torch.randn(8, 40, device="cuda")
+    D.train_step(layer, x, t, 0.1)
+    torch.cuda.synchronize()
+    img_b = model2.image()[0]
+    assert img_a == img0 and img_b != img_a
+    moved = mi.deserialize(img_b).factors[0]
+    assert moved.xf.dtype == np.float64
+    assert np.array_equal(moved.xf, layer.fp.xf.cpu().numpy().astype(np.float64))
