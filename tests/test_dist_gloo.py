@@ -88,3 +88,23 @@ def test_two_rank_gradient_allreduce_equals_full_batch(tmp_path):
     # the sharded forward concatenates to the full-batch forward exactly
     ys = np.concatenate([np.load(tmp_path / f"y{r}.npy") for r in range(world)])
     assert np.array_equal(ys, y)
+
+
+def test_bench_self_launches_ranks_dry_run():
+    """bench.py --gpus 2 without a torchrun environment launches two ranks itself
+    (torch.distributed.run on 127.0.0.1); rank 0 reports n_gpus 2 and both ranks took part in
+    a collective (rank_sum = 1 + 2)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--dry-run"], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["rank_sum"] == 3.0
+    assert "world_size=2" in r.stderr
