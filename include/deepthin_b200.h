@@ -199,6 +199,18 @@ int dt_forward_mse_ex(const dt_plan *plan, int64_t batch, const void *x, int x_d
                       double norm_count, float *grad, double *loss_sum, float *d_bias,
                       float *p_out, void *workspace, size_t workspace_bytes, dt_stream stream);
 
+/* core.py:63-77 matmul (np.matmul after as_matrix) on the tensor cores, for the transposed views
+ * the backward contracts (grad.py:86-94): c (M x N fp32, pitch ldc) = op(a) @ op(b), op(a) M x K,
+ * op(b) K x N. a_trans = 0: a stored M x K (pitch lda); 1: a stored K x M. b_trans = 0: b stored
+ * K x N (pitch ldb); 1: b stored N x K. dtype DT_F32 (tf32 products, fp32 accumulate) or DT_BF16
+ * (bf16 products, fp32 accumulate). Pitches are in elements and 16-byte aligned. The transposed
+ * orders need no copy (tcgen05 reads either major order). Deterministic: split-K partials are
+ * summed in a fixed order. */
+size_t dt_matmul_workspace_bytes(int64_t M, int64_t N, int64_t K, int dtype);
+int dt_matmul(int64_t M, int64_t N, int64_t K, const void *a, int64_t lda, int a_trans,
+              const void *b, int64_t ldb, int b_trans, int dtype, float *c, int64_t ldc,
+              void *workspace, size_t workspace_bytes, dt_stream stream);
+
 /* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);
 /* Row-tile reuse kernel operands derived once per factor pair (the analogue of the reference's

@@ -114,3 +114,65 @@ def stream_handle() -> int:
 
 def workspace(nbytes: int) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device())
+
+
+def _operand_view(t: torch.Tensor):
+    """(base tensor, pitch in elements, transposed?) of a 2-D CUDA view the tensor cores can read
+    in place: row-major (stride (ld, 1)) or a transposed row-major view (stride (1, ld))."""
+    if t.stride(1) == 1 and t.stride(0) >= max(1, t.shape[1]):
+        return t, t.stride(0), False
+    if t.stride(0) == 1 and t.stride(1) >= max(1, t.shape[0]):
+        return t, t.stride(1), True
+    t = t.contiguous()
+    return t, t.shape[1], False
+
+
+def matmul(a, b, *, mma: str = "tf32"):
+    """core.py:63-77 matmul on the tcgen05 tensor cores (dt_matmul): 2-D operands, shape check
+    with the reference's DimensionError text, fp32 accumulate. ``mma="tf32"`` multiplies in tf32
+    (fp32 inputs), ``"bf16"`` in bf16. Transposed views (``x.t()``) are read in place — the
+    backward's gᵀ·P and H'ᵀ·x' contractions need no transpose copy. numpy inputs return numpy
+    (float32); CUDA tensors return a CUDA float32 tensor."""
+    from . import _lib
+    host = not isinstance(a, torch.Tensor) or not isinstance(b, torch.Tensor)
+    at = a if isinstance(a, torch.Tensor) else as_device_matrix(a, name="left operand")[0]
+    bt = b if isinstance(b, torch.Tensor) else as_device_matrix(b, name="right operand")[0]
+    if at.dim() != 2 or bt.dim() != 2:
+        raise DimensionError("matmul operands must be 2-D")
+    if at.shape[1] != bt.shape[0]:
+        raise DimensionError(f"cannot multiply {at.shape[0]}x{at.shape[1]} by "
+                             f"{bt.shape[0]}x{bt.shape[1]}")
+    if mma not in ("tf32", "bf16"):
+        raise ArgumentError(f"mma must be 'tf32' or 'bf16', got {mma!r}")
+    dt = torch.float32 if mma == "tf32" else torch.bfloat16
+    code = _lib.DT_F32 if mma == "tf32" else _lib.DT_BF16
+    at = at.to(device=device(), dtype=dt)
+    bt = bt.to(device=device(), dtype=dt)
+    M, K = at.shape
+    N = bt.shape[1]
+    av, lda, ta = _operand_view(at)
+    bv, ldb, tb = _operand_view(bt)
+    esz = 4 if mma == "tf32" else 2
+    # TMA needs 16-byte pitches and bases: re-pack the rare operand that is not
+    if (lda * esz) % 16 or av.data_ptr() % 16:
+        av = _padded(at, esz)
+        lda, ta = av.stride(0), False
+    if (ldb * esz) % 16 or bv.data_ptr() % 16:
+        bv = _padded(bt, esz)
+        ldb, tb = bv.stride(0), False
+    ldc = -(-N * 4 // 16) * 16 // 4
+    c = torch.empty((M, ldc), dtype=torch.float32, device=device())
+    lib = _lib.lib()
+    ws = workspace(lib.dt_matmul_workspace_bytes(M, N, K, code))
+    _lib.check(lib.dt_matmul(M, N, K, av.data_ptr(), lda, int(ta), bv.data_ptr(), ldb, int(tb), code,
+                             c.data_ptr(), ldc, ws.data_ptr(), ws.numel(), stream_handle()))
+    c = c[:, :N]
+    return c.cpu().numpy() if host else c
+
+
+def _padded(t: torch.Tensor, esz: int) -> torch.Tensor:
+    """Row-major copy of t with a 16-byte-aligned pitch (zero padding)."""
+    cols = -(-t.shape[1] * esz // 16) * 16 // esz
+    out = torch.zeros((t.shape[0], cols), dtype=t.dtype, device=t.device)
+    out[:, : t.shape[1]].copy_(t)
+    return out

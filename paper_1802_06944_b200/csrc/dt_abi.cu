@@ -449,6 +449,65 @@ int dt_mse_grad(int64_t rows, int64_t cols, const float *y, const float *target,
                          workspace_bytes, (cudaStream_t)stream);
 }
 
+namespace {
+XGemm matmul_desc(int64_t M, int64_t N, int64_t K, const void *a, int64_t lda, int a_trans,
+                  const void *b, int64_t ldb, int b_trans, int dtype) {
+  XGemm x;
+  x.M = M; x.N = N; x.K = K;
+  x.A = a; x.lda = lda; x.a_mn = a_trans ? 1 : 0;      // a stored K x M: M contiguous
+  x.B = b; x.ldb = ldb; x.b_mn = b_trans ? 0 : 1;      // b stored K x N: N contiguous
+  x.el = dtype == DT_F32 ? 1 : 0;
+  x.BN = N > 128 ? 256 : (N > 64 || (x.b_mn && x.el == 0) ? 128 : 64);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  x.splits = xgemm_splits(M, N, K, x.BN, x.el, nsm);
+  return x;
+}
+}  // namespace
+
+size_t dt_matmul_workspace_bytes(int64_t M, int64_t N, int64_t K, int dtype) {
+  if (M < 0 || N < 0 || K < 0) return 0;
+  return xgemm_ws(matmul_desc(M, N, K, nullptr, 0, 0, nullptr, 0, 0, dtype)) + 256;
+}
+
+int dt_matmul(int64_t M, int64_t N, int64_t K, const void *a, int64_t lda, int a_trans,
+              const void *b, int64_t ldb, int b_trans, int dtype, float *c, int64_t ldc,
+              void *workspace, size_t workspace_bytes, dt_stream stream) {
+  if (M < 0 || N < 0 || K < 0) {
+    set_error("dt_matmul: negative shape");
+    return DT_E_DIM;
+  }
+  if (dtype != DT_F32 && dtype != DT_BF16) {
+    set_error("dt_matmul: dtype must be DT_F32 or DT_BF16");
+    return DT_E_ARG;
+  }
+  const int esz = dtype == DT_F32 ? 4 : 2;
+  if ((lda * esz) % 16 || (ldb * esz) % 16 || (ldc * 4) % 16 ||
+      (reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+       reinterpret_cast<uintptr_t>(c)) % 16) {
+    set_error("dt_matmul: pointers and pitches must be 16-byte aligned");
+    return DT_E_ARG;
+  }
+  if (M == 0 || N == 0) return DT_OK;
+  if (K == 0) {
+    for (int64_t i = 0; i < M; ++i)
+      DT_CUDA_CHECK(cudaMemsetAsync(c + i * ldc, 0, (size_t)N * 4, (cudaStream_t)stream));
+    return DT_OK;
+  }
+  XGemm x = matmul_desc(M, N, K, a, lda, a_trans, b, ldb, b_trans, dtype);
+  x.out = c;
+  x.ldo = ldc;
+  if (x.splits > 1) {
+    if (workspace_bytes < xgemm_ws(x)) {
+      set_error("dt_matmul: workspace too small (dt_matmul_workspace_bytes)");
+      return DT_E_ARG;
+    }
+    x.part = reinterpret_cast<float *>(workspace);
+  }
+  return xgemm(x, (cudaStream_t)stream);
+}
+
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream) {
   if (count < 0) {
     set_error("count must be >= 0");

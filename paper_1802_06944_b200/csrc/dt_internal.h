@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -80,6 +81,11 @@ int launch_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, int x_dt
 int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
                          uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
                          bool swizzle128);
+// ... with an explicit CUtensorMapSwizzle mode (e.g. CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, the
+// layout tcgen05 requires for MN-major tf32 operands)
+int encode_tensor_map_2d_sw(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
+                            uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                            int swizzle);
 
 // ---- row-tile tensor-core forward for reuse geometries: k_tc_rows.cu ------------------
 // One persistent kernel: P = x_seg @ wf^T (bf16, TMEM) -> tf32 A operand -> y = act(P XF2^T + b),
@@ -96,6 +102,45 @@ void rows_chain(const unsigned *wait, unsigned target, unsigned *post);
 int rows_posts_per_tile(const Geo &g);
 int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float *bias, int act,
                     int y_dtype, char *ws, cudaStream_t st);
+
+// ---- any-major tcgen05 GEMM on CTA pairs: k_tc_xgemm.cu ------------------------------------
+// D[M x N] = sum_k A(m, k) B(n, k); A stored K-major (A[m*lda + k]) or MN-major (A[k*lda + m]),
+// B likewise; tf32 (el = 1, fp32 in memory) or bf16 (el = 0). Epilogue `epi`: 0 store
+// (alpha * D + bias[n]), 1 fused MSE gradient, 2 hi + lo column-half sum, 3 H -> [hi | lo]
+// bf16 re-laid rows. splits > 1: split-K into `part` (xgemm_ws bytes) then a fixed-order sum
+// into out (optionally transposed / hi + lo row halves added).
+struct XGemm {
+  int64_t M = 0, N = 0, K = 0;
+  const void *A = nullptr;
+  int64_t lda = 0;
+  int a_mn = 0;
+  const void *B = nullptr;
+  int64_t ldb = 0;
+  int b_mn = 0;
+  int64_t b_wrap_k = 0;  // > 0: B's rows (K) wrap modulo this (A = [hi; lo] stacked along K)
+  int el = 1;
+  int BN = 256;
+  int splits = 1;
+  float *part = nullptr;
+  int reduce_transpose = 0, reduce_pair_half = 0;
+  int epi = 0;
+  float *out = nullptr;
+  int64_t ldo = 0;
+  float alpha = 1.f;
+  const float *bias = nullptr;
+  const float *target = nullptr;  // epi 1
+  int64_t ldt = 0;
+  float scale = 1.f;
+  double *loss_part = nullptr;
+  int64_t *n_loss_part = nullptr;
+  float *colsum_part = nullptr;   // epi 1: [2 * ceil(M / 256)][N]
+  __nv_bfloat16 *out16 = nullptr; // epi 3
+  int h_r = 0, h_s = 0;
+};
+size_t xgemm_ws(const XGemm &g);
+int xgemm_splits(int64_t M, int64_t N, int64_t K, int BN, int el, int nsm);
+int xgemm(const XGemm &g, cudaStream_t st);
+int xgemm_colsum(int rows, int64_t N, const float *part, float *out, cudaStream_t st);
 
 // ---- two-phase tensor-core path: k_tc_gemm.cu ---------------------------------------
 // W^T (r_dim x round_up(q, 8), bf16) regenerated from the factors (f_dtype DT_F32 or DT_BF16)

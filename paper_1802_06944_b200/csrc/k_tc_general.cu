@@ -1209,6 +1209,14 @@ int launch_pack_x(int64_t batch, int64_t q, int64_t ldx, const void *x, int x_dt
 int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
                          uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
                          bool swizzle128) {
+  return encode_tensor_map_2d_sw(tm, dtype, base, inner, outer, pitch_bytes, box_inner, box_outer,
+                                 swizzle128 ? (int)CU_TENSOR_MAP_SWIZZLE_128B
+                                            : (int)CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+int encode_tensor_map_2d_sw(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
+                            uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                            int swizzle) {
   PFN_encode_tiled enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable from the driver");
@@ -1220,7 +1228,7 @@ int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner,
   cuuint32_t estr[2] = {1, 1};
   CUresult cr = enc(tm, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                     2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    (CUtensorMapSwizzle)swizzle,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));

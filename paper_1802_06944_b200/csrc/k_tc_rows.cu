@@ -365,20 +365,24 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       // per 4 K values
       int j = 0;
       for (int seg = crank; seg < p.s; seg += cs, ++j) {
-        for (int g = 0; g < p.np; g += 32) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(ab * p.pcols + j * p.np + g), v);
-          tmem_ld_wait();
+        // columns [0, rank) hold x . wf_hi, [rank, 2 rank) x . wf_lo: two loads, the second
+        // offset by rank columns, so P = hi + lo pairs up register by register
+        const uint32_t pcol = tbase + lane_t + (uint32_t)(ab * p.pcols + j * p.np);
+        uint32_t vh[32], vl[32];
+        tmem_ld_32x32b_x32(pcol, vh);
+        tmem_ld_32x32b_x32(pcol + (uint32_t)p.rank, vl);
+        tmem_ld_wait();
 #pragma unroll
-          for (int k0 = 0; k0 < 32; k0 += 4) {
-            if (g + k0 < p.rp) {
-              uint32_t w[4];
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+          if (k0 < p.rp) {
+            uint32_t w[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                w[i] = (g + k0 + i < p.rank) ? v[k0 + i]
-                       : (seg == 0 && g + k0 + i == p.bslot) ? 0x3f800000u : 0u;  // 1.0f
-              st_shared_v4(a2b + a2n_off(row, seg * p.rp + g + k0), w[0], w[1], w[2], w[3]);
+            for (int i = 0; i < 4; ++i) {
+              const int k = k0 + i;
+              w[i] = (k < p.rank) ? __float_as_uint(__uint_as_float(vh[k]) + __uint_as_float(vl[k]))
+                     : (seg == 0 && k == p.bslot) ? 0x3f800000u : 0u;  // 1.0f
             }
+            st_shared_v4(a2b + a2n_off(row, seg * p.rp + k0), w[0], w[1], w[2], w[3]);
           }
         }
       }
@@ -681,6 +685,14 @@ int g_nsm() {
 
 }  // namespace
 
+// wf enters phase A as a bf16 hi + lo pair (rows [0, rank) = bf16(wf), rows [rank, 2 rank) =
+// bf16(wf - hi)): the P columns of the two halves are added in fp32 before phase B, so P carries
+// ~16 significant bits of wf instead of 8 — the bf16 rounding of fp32 factors (~2^-9 relative
+// per product, 1.7-2.1e-3 rel_error at config 3) drops to the tf32 level. The extra N columns
+// are free while 2 * rank <= 16 (the UMMA N floor). np = 2 * rank padded to 16.
+static inline int64_t rows_np(const Geo &g) { return (2 * g.rank + 15) / 16 * 16; }
+static inline int64_t rows_wf_bytes(const Geo &g) { return (2 * g.rank * g.n * 2 + 255) / 256 * 256; }
+
 // Cluster size: CTAs sharing one row tile (segments and output chunks split among them).
 static int rows_cluster(const Geo &g) {
   static const int want = getenv("DEEPTHIN_ROWS_CS") ? atoi(getenv("DEEPTHIN_ROWS_CS")) : 8;
@@ -695,8 +707,9 @@ static int rows_cluster(const Geo &g) {
 bool tc_rows_ok(const Geo &g, int x_dtype, int y_dtype) {
   static const int want = getenv("DEEPTHIN_ROWS") ? atoi(getenv("DEEPTHIN_ROWS")) : 1;
   if (!want || !g.reuse || g.n % 64 != 0 || x_dtype != DT_BF16) return false;
-  const int64_t np = (g.rank + 15) / 16 * 16;
+  const int64_t np = rows_np(g);
   const int64_t rp = (g.rank + 3) / 4 * 4;
+  if (np > 32) return false;  // the P exchange reads all np columns of a segment in one x32 load
   if (g.s * rp > 32 || (g.s / rows_cluster(g)) * np > 128) return false;
   if ((g.n / 64) * np * 128 > 32 * 1024) return false;
   const int E = y_dtype == DT_BF16 ? 2 : 4;
@@ -708,7 +721,7 @@ static int64_t rows_k2(const Geo &g) { return (g.s * ((g.rank + 3) / 4 * 4) + 7)
 
 size_t tc_rows_ws(const Geo &g) {
   if (!g.reuse) return 0;
-  return (size_t)((g.rank * g.n * 2 + 255) / 256 * 256) + (size_t)((g.r_dim * rows_k2(g) * 4 + 255) / 256 * 256);
+  return (size_t)rows_wf_bytes(g) + (size_t)((g.r_dim * rows_k2(g) * 4 + 255) / 256 * 256);
 }
 
 namespace {
@@ -723,8 +736,11 @@ __global__ void k_rows_prep(int64_t wf_count, const float *wf, __nv_bfloat16 *wf
   const int64_t tot = wf_count + (int64_t)r_dim * k2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < wf_count) {
-      wf16[i] = __float2bfloat16_rn(wf[i]);
+    if (i < wf_count) {  // hi (rows 0..rank-1) and lo (rows rank..2 rank-1) parts of wf
+      const float v = wf[i];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      wf16[i] = hi;
+      wf16[wf_count + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
     } else {
       const int64_t e = i - wf_count;
       const int64_t j = e / k2;
@@ -743,7 +759,7 @@ int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float 
   const int bslot = !bias ? -1 : (g.rank < rp ? (int)g.rank : (k2 > g.s * rp ? (int)(g.s * rp) : -1));
   const float scale = (y_dtype == DT_BF16 && act == DT_ACT_SIGMOID) ? 0.5f : 1.f;
   __nv_bfloat16 *wf16 = reinterpret_cast<__nv_bfloat16 *>(ws);
-  float *xf2p = reinterpret_cast<float *>(ws + (g.rank * g.n * 2 + 255) / 256 * 256);
+  float *xf2p = reinterpret_cast<float *>(ws + rows_wf_bytes(g));
   const int64_t tot = g.rank * g.n + g.r_dim * (int64_t)k2;
   cudaLaunchConfig_t pc{};
   pc.gridDim = dim3((unsigned)std::min<int64_t>((tot + 255) / 256, 4 * g_nsm()));
@@ -787,7 +803,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.n_tiles = (int)((batch + kTM - 1) / kTM);
   p.s = (int)g.s;
   p.nkb = (int)(g.n / 64);
-  p.np = (int)((g.rank + 15) / 16 * 16);
+  p.np = (int)rows_np(g);
   p.rank = (int)g.rank;
   p.rp = (int)((g.rank + 3) / 4 * 4);
   p.k2 = (int)rows_k2(g);
@@ -841,7 +857,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   const uint32_t smem_bytes = p.off_bar + kTail;
 
   __nv_bfloat16 *wf16 = reinterpret_cast<__nv_bfloat16 *>(ws);
-  float *xf2p = reinterpret_cast<float *>(ws + (g.rank * g.n * 2 + 255) / 256 * 256);
+  float *xf2p = reinterpret_cast<float *>(ws + rows_wf_bytes(g));
   // operands derived once per factor pair (dt_rows_prepare) or here, per call
   if (!prepared)
     if (int rc = tc_rows_prepare(g, wf, xf, bias, act, y_dtype, ws, st)) return rc;
@@ -850,7 +866,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(x), (uint64_t)g.q,
                                     (uint64_t)batch, (uint64_t)g.q * 2, 64, kTM, true))
     return rc;
-  if (int rc = encode_tensor_map_2d(&tm_wf, DT_BF16, wf16, (uint64_t)g.n, (uint64_t)g.rank,
+  if (int rc = encode_tensor_map_2d(&tm_wf, DT_BF16, wf16, (uint64_t)g.n, (uint64_t)(2 * g.rank),
                                     (uint64_t)g.n * 2, 64, (uint32_t)p.np, true))
     return rc;
   if (int rc = encode_tensor_map_2d(&tm_xf2, DT_F32, xf2p, (uint64_t)p.k2, (uint64_t)g.r_dim,

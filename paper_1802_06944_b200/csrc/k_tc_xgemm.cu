@@ -1,0 +1,584 @@
+// Any-major tcgen05 GEMM on CTA pairs — the contractions of the tensor-core training step and of
+// the general-geometry backward (grad.py:63-95, train.py:86-117), which the reference runs as
+// numpy matmuls over transposed views:
+//
+//   D[M x N] = sum_k A(m, k) * B(n, k)          (fp32 accumulate in TMEM)
+//
+// A is stored K-major (A[m * lda + k]) or MN-major (A[k * lda + m]); B likewise. Both major
+// orders feed tcgen05 directly (instruction-descriptor bits 15/16): a transposed view costs
+// nothing — no transpose kernel and no copy. Operands: tf32 (fp32 in memory, kind::tf32) or
+// bf16 (kind::f16), TMA-staged with 128-byte swizzle.
+//
+// Tile: a cluster of two CTAs computes 256 rows (128 per CTA: TMEM lanes) x BN columns
+// (BN in {64, 128, 256}; each CTA stages half of the B tile, cta_group::2 MMA M = 256). The leader
+// CTA's single thread issues every MMA; commits multicast to both CTAs. Accumulators are
+// double-buffered in TMEM (2 x BN columns) so the epilogue of unit u overlaps the MMAs of u + 1.
+// Work units are (row block, column block, K split), persistent over the clusters. Split-K
+// writes fixed-size partial slices that k_xg_reduce sums in split order: results never depend
+// on timing or on the number of SMs (no float atomics).
+//
+// Epilogues (one per template instance):
+//   XE_STORE   out = alpha * D (+ bias[n]), fp32, TMA-stored (split-K: the partial slice)
+//   XE_MSE     g = scale * (D + bias[n] - target), TMA-stored; per-warp fp64 loss partials of
+//              sum (D + bias - target)^2 and fixed-order per-CTA column sums of g (d_bias)
+//              (grad.py:98-103 and :85 fused into the forward's last contraction)
+//   XE_PAIRSUM out[m, k] = D[m, k] + D[m, k + BN/2]: the hi + lo halves of a bf16-split operand
+//   XE_SPLITH  H (fp32, B x s*r) -> H2 (B*s x 2r bf16, [hi | lo] per row of the re-laid view)
+//
+// Roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (leader CTA), warps 2-9 epilogue
+// (TMEM lane quarter = warp % 4, column half = (warp - 2) / 4).
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "dt_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dt {
+namespace {
+
+using namespace ptx;
+
+constexpr int XEPI = 8;                       // epilogue warps
+constexpr int XTHREADS = 64 + 32 * XEPI;
+constexpr uint32_t XA_BYTES = 128 * 128;      // A half-tile stage: 128 rows x 128 B (16 KB)
+constexpr uint32_t XSTG = 32 * 128;           // one 32 x 32 fp32 staging box (4 KB)
+constexpr int XSMEM_MAX = 227 * 1024;
+
+enum { XE_STORE = 0, XE_MSE = 1, XE_PAIRSUM = 2, XE_SPLITH = 3 };
+
+struct XgParams {
+  int M, N, BN, nhalf;        // nhalf = BN / 2 columns staged per CTA
+  int n_mb, n_nb, splits, units, kb_total, kb_per;
+  int a_mn, b_mn;             // 1: MN-major operand
+  int b_wrap;                 // > 0: B's k-block index wraps modulo b_wrap (K-stacked hi/lo A)
+  int S;
+  uint32_t off_b, stage_bytes, off_stg, off_bar;
+  int Mp;                     // rows per split slice of the partial buffer (multiple of 256)
+  // epilogue
+  float alpha;
+  const float *bias;
+  int ldo;
+  float scale;
+  double *loss_part;
+  float *colsum_part;         // [2 * n_mb][N]
+  __nv_bfloat16 *out16;       // XE_SPLITH
+  int h_r, h_s;
+};
+
+// K-major: rows of 128 B (the k-block), 8-row swizzle atoms 1024 B apart (SWIZZLE_128B).
+// MN-major: 128-byte chunks along M/N, each BKE K-rows x 128 B, chunk stride LBO = BKE * 128.
+//   bf16: SWIZZLE_128B, 8-row atoms (SBO 1024); tf32: tcgen05 takes MN-major tf32 only in the
+//   128B_BASE32B layout (32-byte swizzle atoms, 4-row groups: SBO 512), which TMA writes with
+//   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t xdesc(uint32_t base, int mn, int k, int el) {
+  if (!mn) return smem_desc(base + (uint32_t)k * 32u, 16, 1024, SL_SW128);
+  const uint32_t bke = el ? 32u : 64u;
+  const uint32_t step = el ? 1024u : 2048u;  // one MMA's K rows (8 tf32 / 16 bf16) x 128 B
+  if (el) return smem_desc(base + (uint32_t)k * step, bke * 128u, 512, 1u /* 128B_BASE32B */);
+  return smem_desc(base + (uint32_t)k * step, bke * 128u, 1024, SL_SW128);
+}
+
+// Stage one operand half-tile (rows = 128 for A, nhalf for B) of k-block kb.
+__device__ __forceinline__ void xload(uint8_t *dst, const CUtensorMap *tm, uint64_t *bar, int mn,
+                                      int el, int row0, int rows, int kb) {
+  const int bke = el ? 32 : 64;
+  if (!mn) {
+    tma_load_2d_pair(dst, tm, bar, kb * bke, row0);
+  } else {
+    const int ce = 128 / (el ? 4 : 2);  // elements per 128-byte chunk along M/N
+    for (int c = 0; c * ce < rows; ++c)
+      tma_load_2d_pair(dst + c * (uint32_t)bke * 128u, tm, bar, row0 + c * ce, kb * bke);
+  }
+}
+
+__device__ __forceinline__ uint32_t stg_off(int r, int c16) {  // SW128 32 x 128 B box
+  return (uint32_t)r * 128u + ((uint32_t)(c16 ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ void arrive_leader_x(uint64_t *bar, uint32_t crank) {
+  if (crank == 0)
+    mbar_arrive(bar);
+  else
+    mbar_arrive_remote(bar, 0);
+}
+
+template <int EL, int EPI>
+__global__ void __launch_bounds__(XTHREADS, 1)
+    k_tc_xgemm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+               const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_t,
+               const XgParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+  uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
+  uint64_t *tload = tempty + 2;  // [XEPI][2] target boxes (XE_MSE)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tload + 2 * XEPI);
+  float *red = reinterpret_cast<float *>(tslot + 4);  // XE_MSE colsum exchange [2][4][32]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int cid = (int)blockIdx.x / 2, ncl = (int)gridDim.x / 2;
+  const int BN = p.BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * XEPI); }
+    for (int i = 0; i < 2 * XEPI; ++i) mbar_init(&tload[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a);
+    tma_prefetch_desc(&tm_b);
+    tma_prefetch_desc(&tm_o);
+    if (EPI == XE_MSE) tma_prefetch_desc(&tm_t);
+  }
+  if (warp == 1) tmem_alloc_pair(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  griddep_wait();  // operands may come from the previous kernel on the stream
+
+  auto unit_of = [&](int u, int &mb, int &nb, int &ks) {
+    ks = u % p.splits;
+    const int t = u / p.splits;
+    nb = t % p.n_nb;
+    mb = t / p.n_nb;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own A rows, own half of the B columns) -------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t bytes = 2u * (XA_BYTES + (uint32_t)p.nhalf * 128u);
+      for (int u = cid; u < p.units; u += ncl) {
+        int mb, nb, ks;
+        unit_of(u, mb, nb, ks);
+        const int kb0 = ks * p.kb_per, kb1 = min(p.kb_total, kb0 + p.kb_per);
+        const int m0 = mb * 256 + (int)crank * 128, n0 = nb * BN + (int)crank * p.nhalf;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+          uint8_t *st = smem + stage * p.stage_bytes;
+          xload(st, &tm_a, &full[stage], p.a_mn, EL, m0, 128, kb);
+          xload(st + XA_BYTES, &tm_b, &full[stage], p.b_mn, EL, n0, p.nhalf,
+                p.b_wrap > 0 ? kb % p.b_wrap : kb);
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (lane == 0 && leader) {
+      const uint32_t idesc = idesc_f32acc(256, (uint32_t)BN, EL ? 2 : 1) |
+                             ((uint32_t)p.a_mn << 15) | ((uint32_t)p.b_mn << 16);
+      const uint32_t s0 = smem_u32(smem);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int u = cid; u < p.units; u += ncl) {
+        int mb, nb, ks;
+        unit_of(u, mb, nb, ks);
+        const int kb0 = ks * p.kb_per, kb1 = min(p.kb_total, kb0 + p.kb_per);
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_s = s0 + (uint32_t)stage * p.stage_bytes, b_s = a_s + XA_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t da = xdesc(a_s, p.a_mn, k, EL), db = xdesc(b_s, p.b_mn, k, EL);
+            if constexpr (EL)
+              mma_tf32_ss_pair(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else
+              mma_bf16_ss_pair(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit_pair(&empty[stage]);
+          if (++stage == p.S) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (both CTAs: 128 rows x BN columns each) ----------------
+    const int e = warp - 2, q = warp & 3, h = e / 4;
+    const uint32_t lane_t = (uint32_t)(32 * q) << 16;
+    const uint32_t stg0 = smem_u32(smem) + p.off_stg + (uint32_t)e * 2u * XSTG;
+    uint8_t *stg0p = smem + p.off_stg + e * 2 * XSTG;
+    int acc = 0, sb = 0;
+    uint32_t aphase = 0;
+    uint32_t tph[2] = {0u, 0u};
+    for (int u = cid; u < p.units; u += ncl) {
+      int mb, nb, ks;
+      unit_of(u, mb, nb, ks);
+      const int row = mb * 256 + (int)crank * 128 + 32 * q + lane;  // this thread's D row
+      const int r0 = mb * 256 + (int)crank * 128 + 32 * q;           // the warp's first row
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      double sq = 0.0;
+      const int nch = EPI == XE_PAIRSUM ? BN / 64 : BN / 32;
+      for (int c = h; c < nch; c += 2) {
+        const int col0 = nb * BN + 32 * c;  // first D column of this chunk
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(acc * BN + 32 * c), v);
+        if constexpr (EPI == XE_PAIRSUM) {
+          uint32_t w[32];
+          tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(acc * BN + 32 * c + BN / 2), w);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(w[i]));
+        } else {
+          tmem_ld_wait();
+        }
+        if constexpr (EPI == XE_SPLITH) {
+          // H[row, col0 .. col0+31] -> H2 row (row * s + col0 / r), [hi | lo]
+          if (row < p.M) {
+            const int seg = col0 / p.h_r, k0 = col0 % p.h_r;
+            __nv_bfloat16 *hp = p.out16 + ((int64_t)row * p.h_s + seg) * (2 * p.h_r) + k0;
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
+              const __nv_bfloat16 ha = __float2bfloat16_rn(a), hb = __float2bfloat16_rn(b);
+              __nv_bfloat162 hh, ll;
+              hh.x = ha; hh.y = hb;
+              ll = __floats2bfloat162_rn(a - __bfloat162float(ha), b - __bfloat162float(hb));
+              hi[i] = *reinterpret_cast<uint32_t *>(&hh);
+              lo[i] = *reinterpret_cast<uint32_t *>(&ll);
+            }
+            uint4 *dh = reinterpret_cast<uint4 *>(hp), *dl = reinterpret_cast<uint4 *>(hp + p.h_r);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              dh[i] = make_uint4(hi[4 * i], hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
+              dl[i] = make_uint4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+            }
+          }
+          continue;
+        } else {
+          // staging buffer sb of this warp: free once its previous TMA store read it
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+          const uint32_t sbase = stg0 + (uint32_t)sb * XSTG;
+          uint8_t *sptr = stg0p + sb * XSTG;
+          if constexpr (EPI == XE_MSE) {
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&tload[2 * e + sb], XSTG);
+              tma_load_2d(sptr, &tm_t, &tload[2 * e + sb], col0, r0);
+            }
+            mbar_wait(&tload[2 * e + sb], tph[sb]);
+            tph[sb] ^= 1;
+          }
+          float bias_v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) bias_v[i] = 0.f;
+          if (p.bias) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bias_v[i] = (col0 + i < p.N) ? __ldg(p.bias + col0 + i) : 0.f;
+          }
+          float csq = 0.f;
+#pragma unroll
+          for (int c16 = 0; c16 < 8; ++c16) {
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 4 * c16 + j;
+              const float z = __uint_as_float(v[i]);
+              if constexpr (EPI == XE_MSE) {
+                const float t = reinterpret_cast<const float *>(sptr + stg_off(lane, c16))[j];
+                const float dz = (z + bias_v[i]) - t;
+                const bool ok = row < p.M && col0 + i < p.N;
+                csq = ok ? fmaf(dz, dz, csq) : csq;
+                o[j] = ok ? p.scale * dz : 0.f;
+              } else {
+                o[j] = fmaf(p.alpha, z, bias_v[i]);
+              }
+            }
+            sts_v4(sbase + stg_off(lane, c16), __float_as_uint(o[0]), __float_as_uint(o[1]),
+                         __float_as_uint(o[2]), __float_as_uint(o[3]));
+          }
+          if constexpr (EPI == XE_MSE) {
+            sq += (double)csq;
+            // column sums of g over this warp's 32 rows (transposed read of the staging box:
+            // thread = column), then over the CTA's four lane quarters in quarter order
+            __syncwarp();
+            float cs = 0.f;
+            for (int r = 0; r < 32; ++r)
+              cs += reinterpret_cast<const float *>(sptr + stg_off(r, lane >> 2))[lane & 3];
+            red[(h * 4 + q) * 32 + lane] = cs;
+            named_bar_sync(1 + h, 128);
+            if (q == 0 && col0 + lane < p.N)
+              p.colsum_part[(int64_t)(mb * 2 + (int)crank) * p.N + col0 + lane] =
+                  ((red[(h * 4 + 0) * 32 + lane] + red[(h * 4 + 1) * 32 + lane]) +
+                   red[(h * 4 + 2) * 32 + lane]) + red[(h * 4 + 3) * 32 + lane];
+            named_bar_sync(1 + h, 128);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int ocol = EPI == XE_PAIRSUM ? nb * (BN / 2) + 32 * c : col0;
+            const int orow = r0 + (p.splits > 1 ? ks * p.Mp : 0);
+            tma_store_2d(&tm_o, sptr, ocol, orow);
+            bulk_commit_group();
+          }
+          sb ^= 1;
+        }
+      }
+      if constexpr (EPI == XE_MSE) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) p.loss_part[((int64_t)u * 2 + crank) * XEPI + e] = sq;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader_x(&tempty[acc], crank);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (lane == 0) bulk_wait_group<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tbase, 512);
+  }
+}
+
+typedef void (*XgFn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, XgParams);
+
+template <int EL>
+XgFn pick_x(int epi) {
+  switch (epi) {
+    case XE_MSE: return k_tc_xgemm<EL, XE_MSE>;
+    case XE_PAIRSUM: return k_tc_xgemm<EL, XE_PAIRSUM>;
+    case XE_SPLITH: return k_tc_xgemm<EL, XE_SPLITH>;
+    default: return k_tc_xgemm<EL, XE_STORE>;
+  }
+}
+
+// out (or out^T) = sum over splits (fixed order) of the partial slices, optionally the hi + lo
+// row halves added (pair_half > 0: rows [0, pair_half) + rows [pair_half, 2 pair_half)).
+__global__ void k_xg_reduce(int splits, int M, int N, int Mp, const float *part, float *out,
+                            int ldo, int transpose, int pair_half, float alpha) {
+  const int rows = pair_half > 0 ? pair_half : M;
+  const int64_t total = (int64_t)rows * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N), n = (int)(i - (int64_t)m * N);
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) {
+      const float *sl = part + (int64_t)k * Mp * N;
+      s += sl[(int64_t)m * N + n];
+      if (pair_half > 0) s += sl[(int64_t)(m + pair_half) * N + n];
+    }
+    s *= alpha;
+    if (transpose)
+      out[(int64_t)n * ldo + m] = s;
+    else
+      out[(int64_t)m * ldo + n] = s;
+  }
+}
+
+// column sums over the [rows][N] partials in row order (d_bias from XE_MSE's per-CTA sums)
+__global__ void k_colsum_rows(int rows, int N, const float *part, float *out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int r = 0; r < rows; ++r) s += part[(int64_t)r * N + n];
+  out[n] = s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+size_t xgemm_ws(const XGemm &g) {
+  if (g.splits <= 1) return 0;
+  const int64_t Mp = (g.M + 255) / 256 * 256;
+  return (size_t)g.splits * Mp * g.N * 4;
+}
+
+int xgemm_splits(int64_t M, int64_t N, int64_t K, int BN, int el, int nsm) {
+  const int64_t tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int64_t kb = (K + (el ? 31 : 63)) / (el ? 32 : 64);
+  const int64_t ncl = nsm / 2;
+  if (tiles >= ncl) return 1;
+  // enough units for every cluster, several waves when that balances better, >= 8 k-blocks each
+  int best = 1;
+  double best_eff = (double)tiles / ncl;
+  for (int s = 2; s <= 64 && kb / s >= 8; ++s) {
+    const double units = (double)tiles * s;
+    const double waves = std::ceil(units / ncl);
+    const double eff = units / (waves * ncl) - 0.002 * s;  // partial-slice traffic
+    if (eff > best_eff) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
+int xgemm(const XGemm &g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return DT_OK;
+  const int el = g.el;
+  const int esz = el ? 4 : 2, bke = el ? 32 : 64;
+  int BN = g.BN;
+  if (BN != 64 && BN != 128 && BN != 256) {
+    set_error("xgemm: BN must be 64, 128 or 256");
+    return DT_E_ARG;
+  }
+  const int nhalf = BN / 2;
+  if (g.b_mn && nhalf * esz < 128) {
+    set_error("xgemm: an MN-major B needs BN/2 * element size >= 128 bytes");
+    return DT_E_ARG;
+  }
+  if (g.epi == XE_PAIRSUM && (g.N != BN || g.splits > 1)) {
+    set_error("xgemm: the pair-sum epilogue needs one column block (N == BN), no split");
+    return DT_E_ARG;
+  }
+  if (g.epi == XE_SPLITH && (g.h_r % 32 != 0 || g.splits > 1)) {
+    set_error("xgemm: the H split epilogue needs rank % 32 == 0, no split");
+    return DT_E_ARG;
+  }
+  int dev = 0, nsm = 148;
+  DT_CUDA_CHECK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+
+  XgParams p{};
+  p.M = (int)g.M;
+  p.N = (int)g.N;
+  p.BN = BN;
+  p.nhalf = nhalf;
+  p.n_mb = (int)((g.M + 255) / 256);
+  p.n_nb = (int)((g.N + BN - 1) / BN);
+  p.kb_total = (int)((g.K + bke - 1) / bke);
+  p.splits = std::max(1, std::min(g.splits, p.kb_total));
+  p.kb_per = (p.kb_total + p.splits - 1) / p.splits;
+  p.splits = (p.kb_total + p.kb_per - 1) / p.kb_per;  // no empty split
+  p.units = p.n_mb * p.n_nb * p.splits;
+  p.a_mn = g.a_mn;
+  p.b_mn = g.b_mn;
+  p.b_wrap = g.b_wrap_k > 0 ? (int)(g.b_wrap_k / bke) : 0;
+  if (g.b_wrap_k > 0 && g.b_wrap_k % bke) {
+    set_error("xgemm: the B wrap length must be a multiple of the k-block");
+    return DT_E_ARG;
+  }
+  p.Mp = p.n_mb * 256;
+  p.alpha = g.alpha;
+  p.bias = g.bias;
+  p.ldo = (int)g.ldo;
+  p.scale = g.scale;
+  p.loss_part = g.loss_part;
+  p.colsum_part = g.colsum_part;
+  p.out16 = g.out16;
+  p.h_r = g.h_r;
+  p.h_s = g.h_s;
+  p.stage_bytes = XA_BYTES + (uint32_t)nhalf * 128u;
+  const uint32_t stg_bytes = (g.epi == XE_SPLITH) ? 0u : (uint32_t)XEPI * 2u * XSTG;
+  const uint32_t tail = 1024 + 512;  // barriers, TMEM slot, colsum exchange, alignment slack
+  p.S = (int)std::min<uint32_t>(8, (XSMEM_MAX - stg_bytes - tail - 1024) / p.stage_bytes);
+  p.off_stg = (uint32_t)p.S * p.stage_bytes;
+  p.off_bar = p.off_stg + stg_bytes;
+  const uint32_t smem_bytes = p.off_bar + tail + 1024;  // + the in-kernel 1024-B alignment
+  if (p.S < 2) {
+    set_error("xgemm: shared memory too small");
+    return DT_E_UNSUPPORTED;
+  }
+
+  CUtensorMap tm_a, tm_b, tm_o, tm_t;
+  const int tdt = el ? DT_F32 : DT_BF16;
+  void *A = const_cast<void *>(g.A), *B = const_cast<void *>(g.B);
+  // A: K-major [M][lda] box (bke, 128); MN-major [K][lda] box (128 B of M, bke)
+  const int mn_sw = el ? (int)CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : (int)CU_TENSOR_MAP_SWIZZLE_128B;
+  if (int rc = g.a_mn ? encode_tensor_map_2d_sw(&tm_a, tdt, A, (uint64_t)g.M, (uint64_t)g.K,
+                                                (uint64_t)g.lda * esz, 128 / esz, bke, mn_sw)
+                      : encode_tensor_map_2d(&tm_a, tdt, A, (uint64_t)g.K, (uint64_t)g.M,
+                                             (uint64_t)g.lda * esz, bke, 128, true))
+    return rc;
+  const uint64_t kb_rows = g.b_wrap_k > 0 ? (uint64_t)g.b_wrap_k : (uint64_t)g.K;
+  if (int rc = g.b_mn ? encode_tensor_map_2d_sw(&tm_b, tdt, B, (uint64_t)g.N, kb_rows,
+                                                (uint64_t)g.ldb * esz, 128 / esz, bke, mn_sw)
+                      : encode_tensor_map_2d(&tm_b, tdt, B, kb_rows, (uint64_t)g.N,
+                                             (uint64_t)g.ldb * esz, bke, (uint32_t)nhalf, true))
+    return rc;
+  float *out = g.out;
+  int64_t out_rows = g.M, out_cols = g.epi == XE_PAIRSUM ? g.N / 2 : g.N, ldo = g.ldo;
+  if (p.splits > 1) {
+    if (!g.part) {
+      set_error("xgemm: split-K needs a partial buffer (xgemm_ws bytes)");
+      return DT_E_ARG;
+    }
+    out = g.part;
+    out_rows = (int64_t)p.splits * p.Mp;
+    out_cols = g.N;
+    ldo = g.N;
+    p.ldo = (int)g.N;
+  }
+  if (g.epi != XE_SPLITH) {
+    if (int rc = encode_tensor_map_2d(&tm_o, DT_F32, out, (uint64_t)out_cols, (uint64_t)out_rows,
+                                      (uint64_t)ldo * 4, 32, 32, true))
+      return rc;
+  } else {
+    tm_o = tm_a;  // unused
+  }
+  if (g.epi == XE_MSE) {
+    if (int rc = encode_tensor_map_2d(&tm_t, DT_F32, const_cast<float *>(g.target), (uint64_t)g.N,
+                                      (uint64_t)g.M, (uint64_t)g.ldt * 4, 32, 32, true))
+      return rc;
+  } else {
+    tm_t = tm_a;  // unused
+  }
+  if (g.epi == XE_MSE && g.loss_part)
+    DT_CUDA_CHECK(cudaMemsetAsync(g.loss_part, 0, (size_t)p.units * 2 * XEPI * 8, st));
+
+  XgFn fn = el ? pick_x<1>(g.epi) : pick_x<0>(g.epi);
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(fn), (int)smem_bytes)) return rc;
+  const int ncl = std::max(1, std::min(p.units, nsm / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * ncl));
+  cfg.blockDim = dim3(XTHREADS);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_a, tm_b, tm_o, tm_t, p));
+  if (int rc = check_launch("tc_xgemm")) return rc;
+  if (g.n_loss_part) *g.n_loss_part = (int64_t)p.units * 2 * XEPI;
+
+  if (p.splits > 1) {
+    const int pair = g.reduce_pair_half;
+    const int64_t rows = pair > 0 ? pair : g.M;
+    const int64_t total = rows * g.N;
+    k_xg_reduce<<<(unsigned)std::min<int64_t>((total + 255) / 256, 8 * nsm), 256, 0, st>>>(
+        p.splits, (int)g.M, (int)g.N, p.Mp, g.part, g.out, (int)g.ldo, g.reduce_transpose ? 1 : 0,
+        pair, 1.0f);
+    if (int rc = check_launch("xg_reduce")) return rc;
+  }
+  return DT_OK;
+}
+
+int xgemm_colsum(int rows, int64_t N, const float *part, float *out, cudaStream_t st) {
+  k_colsum_rows<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rows, (int)N, part, out);
+  return check_launch("colsum_rows");
+}
+
+}  // namespace dt

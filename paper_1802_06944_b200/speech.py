@@ -217,23 +217,30 @@ class SpeechRNN:
                                         st["out"].data_ptr() + t * B * H * esz, stream_handle()))
 
     # ---- forward ------------------------------------------------------------------------
-    def forward(self, x, graph: bool = True, persistent: bool = True):
+    def forward(self, x, graph: bool = True, persistent: bool = True, trace: dict | None = None):
         """x: (T, B, n_in) CUDA tensor (bf16 or fp32), time-major. Returns fp32 logits
         (T, B, n_out). The recurrence runs as one persistent kernel (``persistent``, batch <= 64)
-        or as a CUDA graph of per-step launches (``graph``) or eagerly."""
+        or as a CUDA graph of per-step launches (``graph``) or eagerly. ``trace`` (a dict)
+        receives the stored intermediate activations by stage name (parity tests)."""
         if not isinstance(x, torch.Tensor) or x.dim() != 3 or x.shape[2] != self.n_in:
             raise DimensionError(f"input must be (T, B, {self.n_in}), got "
                                  f"{tuple(x.shape) if hasattr(x, 'shape') else type(x)}")
         T, B = int(x.shape[0]), int(x.shape[1])
         h = x.to(device()).reshape(T * B, self.n_in).to(torch.bfloat16).contiguous()
+        keep = (lambda k, v: trace.__setitem__(k, v)) if trace is not None else (lambda k, v: None)
+        keep("x", h)
         for name in ("fc1", "fc2", "fc3"):
             h = self._dense(name, h, "clipped_relu")
+            keep(name, h)
         gx = [self._dense(f"x_{g}", h, "identity") for g in GATES]
+        keep("gx", gx)
         self._last_gx = gx  # kept for measurement (bench.py times the recurrence alone)
         seq = self._sequence(gx, T, B) if persistent else None
         if seq is None:
             seq = self._recurrence(gx, T, B, graph=graph)
+        keep("seq", seq if trace is None else seq.clone())
         h = self._dense("fc4", seq, "clipped_relu")
+        keep("fc4", h)
         y = self._dense("out", h, "identity", out_dtype=torch.float32)
         return y.reshape(T, B, self.n_out)
 
