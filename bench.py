@@ -63,6 +63,13 @@ CONFIGS = {
 }
 
 
+def kname(full):
+    """Short kernel name from a demangled signature: the k_* identifier with its template args."""
+    import re
+    m = re.search(r"(k_\w+)(<[^()]*>)?", full)
+    return (m.group(1) + (m.group(2) or "")) if m else full.split("(")[0][-60:]
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -202,7 +209,7 @@ def cupti_kernels(run, name_filter):
         excl = max(excl, 0.0)
         prev_end = t1 if prev_end is None else max(prev_end, t1)
         total += excl
-        names.add(e.name.split("(")[0][-80:])
+        names.add(kname(e.name))
         if any(f in e.name for f in name_filter):
             sel.append(excl)
             raw.append(t1 - t0)

@@ -82,7 +82,7 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(compile_one, _sources()))
     tmp = lib + ".tmp"
-    r = subprocess.run([cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcublasLt",
+    r = subprocess.run([cc, *ARCH, "-shared", "-o", tmp, *objs,
                         "-Xlinker", "-rpath,/usr/local/cuda/lib64"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

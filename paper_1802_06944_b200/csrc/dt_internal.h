@@ -107,8 +107,8 @@ int tc_rows_prepare(const Geo &g, const float *wf, const float *xf, const float 
 // D[M x N] = sum_k A(m, k) B(n, k); A stored K-major (A[m*lda + k]) or MN-major (A[k*lda + m]),
 // B likewise; tf32 (el = 1, fp32 in memory) or bf16 (el = 0). Epilogue `epi`: 0 store
 // (alpha * D + bias[n]), 1 fused MSE gradient, 2 hi + lo column-half sum, 3 H -> [hi | lo]
-// bf16 re-laid rows. splits > 1: split-K into `part` (xgemm_ws bytes) then a fixed-order sum
-// into out (optionally transposed / hi + lo row halves added).
+// bf16 re-laid rows. splits > 1 (or a transposed / column-paired result, store epilogue
+// only): partial slices into `part` (xgemm_ws bytes), then a fixed-order sum into out.
 struct XGemm {
   int64_t M = 0, N = 0, K = 0;
   const void *A = nullptr;
@@ -136,11 +136,29 @@ struct XGemm {
   float *colsum_part = nullptr;   // epi 1: [2 * ceil(M / 256)][N]
   __nv_bfloat16 *out16 = nullptr; // epi 3
   int h_r = 0, h_s = 0;
+  int pair_half = 0;              // epi 2
+  int ks_major = 0;               // units ordered with the K split slowest (operand reuse in L2)
 };
 size_t xgemm_ws(const XGemm &g);
 int xgemm_splits(int64_t M, int64_t N, int64_t K, int BN, int el, int nsm);
 int xgemm(const XGemm &g, cudaStream_t st);
-int xgemm_colsum(int rows, int64_t N, const float *part, float *out, cudaStream_t st);
+// fixed-order reductions of XE_MSE's partials (scratch: xgemm_reduce_scratch bytes)
+size_t xgemm_reduce_scratch(int rows, int64_t N);
+int xgemm_colsum(int rows, int64_t N, const float *part, float *out, void *scratch, cudaStream_t st);
+int xgemm_sum_f64(int64_t count, const double *part, double *out, void *scratch, cudaStream_t st);
+
+// ---- tensor-core training step of reuse geometries: k_train.cu -------------------------------
+bool xtrain_ok(const Geo &g);
+size_t xtrain_forward_mse_ws(const Geo &g, int64_t batch);
+int xtrain_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                       const float *wf, const float *bias, const float *target, double scale,
+                       float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st,
+                       float *d_bias, float *p_out);
+size_t xtrain_backward_ws(const Geo &g, int64_t batch);
+int xtrain_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                    const float *wf, const float *bias, int act, float act_arg, const float *up,
+                    float *d_xf, float *d_wf, float *d_bias, float *d_input, char *ws,
+                    size_t ws_bytes, cudaStream_t st, const float *p_in);
 
 // ---- two-phase tensor-core path: k_tc_gemm.cu ---------------------------------------
 // W^T (r_dim x round_up(q, 8), bf16) regenerated from the factors (f_dtype DT_F32 or DT_BF16)

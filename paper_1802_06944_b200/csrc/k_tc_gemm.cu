@@ -33,7 +33,6 @@
 #include <vector>
 
 #include <cooperative_groups.h>
-#include <cublasLt.h>
 
 #include "act.cuh"
 #include "dt_internal.h"
@@ -1501,22 +1500,6 @@ static int64_t mse_parts_bound(const Geo &g, int64_t batch) {
   return ((g.r_dim + GM - 1) / GM + 2) * ((batch + GN - 1) / GN) * kEpiWarps;
 }
 
-namespace {
-int lt_gemm_ep(cudaStream_t st, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
-               const float *B, int64_t ldb, const float *C, float *D, int64_t ldd, float alpha,
-               float beta, const float *bias, void *ws, size_t ws_bytes);
-__global__ void k_scale_vec(int64_t n, const float *a, float s, float *out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = a ? s * a[i] : 0.f;
-}
-constexpr size_t kLtWsFwd = 32u << 20;
-// the MSE through cuBLASLt's epilogue (C = target) once the tf32 GEMM is large enough that the
-// stream-scheduled single-CTA tf32 kernel is L2-operand-bound (config 5: K = s*rank = 512)
-bool mse_lt_ok(const Geo &g, int64_t batch) {
-  static const int want = getenv("DEEPTHIN_MSE_LT") ? atoi(getenv("DEEPTHIN_MSE_LT")) : 1;
-  return want && g.s * g.rank >= 256 && batch >= 1024 && g.r_dim >= 1024;
-}
-}  // namespace
 
 static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dtype,
                            const void *xf, const void *wf, int f_dtype, const float *bias,
@@ -1531,15 +1514,25 @@ int tc_gemm_forward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
 }
 
 size_t tc_forward_mse_ws(const Geo &g, int64_t batch) {
-  return tc_gemm_ws(g, batch) + (size_t)round_up(mse_parts_bound(g, batch) * 8, 256) +
-         (size_t)round_up(g.r_dim * 4, 256) + (size_t)round_up(1184 * 8, 256) + kLtWsFwd +
-         (size_t)round_up(colsum_ws(batch, g.r_dim), 256);
+  const size_t own = tc_gemm_ws(g, batch) + (size_t)round_up(mse_parts_bound(g, batch) * 8, 256) +
+                     (size_t)round_up(g.r_dim * 4, 256) + (size_t)round_up(1184 * 8, 256) +
+                     (size_t)round_up(colsum_ws(batch, g.r_dim), 256);
+  return std::max(own, xtrain_ok(g) ? xtrain_forward_mse_ws(g, batch) : (size_t)0);
 }
 
 int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
                    const float *wf, const float *bias, const float *target, double scale,
                    float *grad, double *loss_sum, char *ws, size_t ws_bytes, cudaStream_t st,
                    float *d_bias, float *p_out) {
+  if (xtrain_ok(g) && x_dtype == DT_BF16) {  // k_train.cu: our tcgen05 GEMMs, fused MSE + d_bias
+    if (batch == 0) {
+      if (loss_sum) DT_CUDA_CHECK(cudaMemsetAsync(loss_sum, 0, sizeof(double), st));
+      if (d_bias) DT_CUDA_CHECK(cudaMemsetAsync(d_bias, 0, (size_t)g.r_dim * 4, st));
+      return DT_OK;
+    }
+    return xtrain_forward_mse(g, batch, x, x_dtype, xf, wf, bias, target, scale, grad, loss_sum,
+                              ws, ws_bytes, st, d_bias, p_out);
+  }
   if (p_out && !(reuse_factored_ok(g))) {
     set_error("forward_mse: P is kept only on reuse geometries (factored path)");
     return DT_E_UNSUPPORTED;
@@ -1625,33 +1618,6 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     GemmCall c1{xt, g.n, batch * g.s, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
                 P, g.rank, DT_F32, nullptr, false, 0};
     if (int rc = run_gemm(c1, st)) return rc;
-    if (mse && mse_lt_ok(g, batch)) {
-      // grad = scale * (P XF2^T + b - t) in one cuBLASLt tf32 GEMM: alpha = scale, C = target,
-      // beta = -scale, bias epilogue with scale * b; then the fixed-order fp64 loss from grad
-      char *tail = reinterpret_cast<char *>(mse->part) + round_up(mse_parts_bound(g, batch) * 8, 256);
-      float *bs = reinterpret_cast<float *>(tail);
-      double *sq_part = reinterpret_cast<double *>(tail + round_up(g.r_dim * 4, 256));
-      void *lws = tail + round_up(g.r_dim * 4, 256) + round_up(1184 * 8, 256);
-      const float sc = (float)mse->scale;
-      k_scale_vec<<<(unsigned)((g.r_dim + 255) / 256), 256, 0, st>>>(g.r_dim, bias, sc, bs);
-      if (int rc = check_launch("scale_vec")) return rc;
-      if (int rc = lt_gemm_ep(st, batch, g.r_dim, SR, P, SR, reinterpret_cast<const float *>(xf), SR,
-                              mse->target, reinterpret_cast<float *>(y), g.r_dim, sc, -sc, bs, lws,
-                              kLtWsFwd))
-        return rc;
-      if (mse->d_bias) {  // one pass over grad: column sums (d_bias) and the loss
-        float *cpart = reinterpret_cast<float *>(reinterpret_cast<char *>(lws) + kLtWsFwd);
-        const int rc = launch_colsum_sumsq(batch, g.r_dim, reinterpret_cast<const float *>(y),
-                                           1.0 / mse->scale, mse->d_bias, cpart, sq_part,
-                                           mse->loss_sum, st);
-        if (rc != DT_E_UNSUPPORTED) {
-          const_cast<MseArgs *>(mse)->d_bias = nullptr;  // done (no separate pass)
-          return rc;
-        }
-      }
-      return launch_sumsq(batch * g.r_dim, reinterpret_cast<const float *>(y), 1.0 / mse->scale,
-                          sq_part, mse->loss_sum, st);
-    }
     GemmCall c2{P, SR, batch, SR, xf, SR, g.r_dim, bias, act, act_arg,
                 y, g.r_dim, y_dtype, nullptr, true, 1};
     if (mse) {
@@ -1694,279 +1660,21 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
 }
 
 
-// =============================================================================================
-// Backward of reuse geometries on the tensor cores, factored (SURVEY.md §8(a) backward (reuse);
-// grad.py:63-95 restated without W):
-//   g      = upstream (.* act'(pre), pre recomputed)           (grad.py:81-83)
-//   d_bias = sum_b g                                            (grad.py:85)
-//   P      = x.view(B*s, n) @ wf^T                  (our GEMM, fp32 P, as in the forward)
-//   dXF2   = g^T @ P.view(B, s*rank)  -> d_xf rows [0, r_dim*s), zero tail   (grad.py:92)
-//   H      = g @ XF2                  (B x s*rank)
-//   d_wf   = H.view(B*s, rank)^T @ x.view(B*s, n)                           (grad.py:93)
-//   d_in   = (H.view(B*s, rank) @ wf).view(B, q)                            (grad.py:94)
-// The four products over transposed views are plain GEMMs: cuBLASLt, kind TF32 for the fp32
-// operands; d_wf runs in bf16 on x with H split into bf16 hi + lo parts (two accumulating
-// GEMMs: H's rounding would otherwise reach ~2^-9 of the gradient).
-// =============================================================================================
-namespace {
+// Backward of reuse geometries on the tensor cores: k_train.cu (our tcgen05 GEMMs throughout).
+bool tc_backward_ok(const Geo &g) { return xtrain_ok(g); }
 
-// H (rows x r fp32) -> H2 (rows x 2r bf16): row i = [hi(H[i, :]) | lo(H[i, :])] (one GEMM then
-// contracts both halves against x in a single read of x)
-__global__ void k_split_bf16_rows(int64_t rows, int r, const float *src, __nv_bfloat16 *h2) {
-  const int64_t count = rows * r;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / r, k = i - row * r;
-    const float v = src[i];
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    h2[row * 2 * r + k] = h;
-    h2[row * 2 * r + r + k] = __float2bfloat16_rn(v - __bfloat162float(h));
-  }
-}
-__global__ void k_add_halves(int64_t count, const float *d2, float *out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < count) out[i] = d2[i] + d2[count + i];
-}
-
-__global__ void k_split_bf16(int64_t count, const float *src, __nv_bfloat16 *hi, __nv_bfloat16 *lo) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = src[i];
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    hi[i] = h;
-    lo[i] = __float2bfloat16_rn(v - __bfloat162float(h));
-  }
-}
-
-cublasLtHandle_t lt_handle() {
-  thread_local cublasLtHandle_t h = nullptr;
-  if (!h) cublasLtCreate(&h);
-  return h;
-}
-
-// Row-major C[M x N] (ldc) = op(A)[M x K] @ op(B)[K x N] + beta*C. A is stored M x K (lda) or,
-// with ta, K x M; B is stored K x N (ldb) or, with tb, N x K. Column-major cuBLASLt computes the
-// transpose: C^T = op(B)^T op(A)^T.
-int lt_gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, const void *A, bool ta, int64_t lda,
-            const void *B, bool tb, int64_t ldb, float *C, int64_t ldc, cudaDataType_t dt,
-            float beta, void *ws, size_t ws_bytes) {
-  cublasLtHandle_t h = lt_handle();
-  if (!h) {
-    set_error("cublasLtCreate failed");
-    return DT_E_CUDA;
-  }
-  const cublasComputeType_t ct = dt == CUDA_R_32F ? CUBLAS_COMPUTE_32F_FAST_TF32 : CUBLAS_COMPUTE_32F;
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-  cublasLtMatmulPreference_t pref = nullptr;
-  int rc = DT_OK;
-  cublasStatus_t e = cublasLtMatmulDescCreate(&op, ct, CUDA_R_32F);
-  const cublasOperation_t opa = tb ? CUBLAS_OP_T : CUBLAS_OP_N;  // cuBLAS A-slot = our B
-  const cublasOperation_t opb = ta ? CUBLAS_OP_T : CUBLAS_OP_N;  // cuBLAS B-slot = our A
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &opa, sizeof(opa));
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &opb, sizeof(opb));
-  // column-major shapes of the stored matrices
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatrixLayoutCreate(&la, dt, tb ? K : N, tb ? N : K, ldb);
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatrixLayoutCreate(&lb, dt, ta ? M : K, ta ? K : M, lda);
-  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, N, M, ldc);
-  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatmulPreferenceCreate(&pref);
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
-                                             &ws_bytes, sizeof(ws_bytes));
-  cublasLtMatmulHeuristicResult_t heur{};
-  int found = 0;
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, lc, pref, 1, &heur, &found);
-  const float alpha = 1.f;
-  if (e == CUBLAS_STATUS_SUCCESS && found > 0)
-    e = cublasLtMatmul(h, op, &alpha, B, la, A, lb, &beta, C, lc, C, lc, &heur.algo, ws, ws_bytes,
-                       st);
-  if (e != CUBLAS_STATUS_SUCCESS || found == 0) {
-    set_error("cuBLASLt matmul failed (status " + std::to_string((int)e) + ")");
-    rc = DT_E_CUDA;
-  }
-  if (pref) cublasLtMatmulPreferenceDestroy(pref);
-  if (lc) cublasLtMatrixLayoutDestroy(lc);
-  if (lb) cublasLtMatrixLayoutDestroy(lb);
-  if (la) cublasLtMatrixLayoutDestroy(la);
-  if (op) cublasLtMatmulDescDestroy(op);
-  return rc;
-}
-
-constexpr size_t kLtWs = 32u << 20;
-
-}  // namespace
-
-namespace {
-// Row-major D[M x N] (ldd) = alpha * A[M x K] (lda) @ B^T (B stored N x K, ldb) + beta * C + bias
-// (bias over the N columns; C same layout as D, nullable with beta = 0), tf32 compute.
-int lt_gemm_ep(cudaStream_t st, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
-               const float *B, int64_t ldb, const float *C, float *D, int64_t ldd, float alpha,
-               float beta, const float *bias, void *ws, size_t ws_bytes) {
-  cublasLtHandle_t h = lt_handle();
-  if (!h) {
-    set_error("cublasLtCreate failed");
-    return DT_E_CUDA;
-  }
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-  cublasLtMatmulPreference_t pref = nullptr;
-  cublasStatus_t e = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F);
-  // column-major: D^T (N x M) = B (N x K, i.e. B^T stored K x N -> op T) * A^T (K x M, op N)
-  const cublasOperation_t opa = CUBLAS_OP_T, opb = CUBLAS_OP_N;
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &opa, sizeof(opa));
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &opb, sizeof(opb));
-  if (e == CUBLAS_STATUS_SUCCESS && bias) {
-    const cublasLtEpilogue_t ep = CUBLASLT_EPILOGUE_BIAS;
-    e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &ep, sizeof(ep));
-    if (e == CUBLAS_STATUS_SUCCESS)
-      e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
-  }
-  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&la, CUDA_R_32F, K, N, ldb);
-  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&lb, CUDA_R_32F, K, M, lda);
-  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, N, M, ldd);
-  if (e == CUBLAS_STATUS_SUCCESS) e = cublasLtMatmulPreferenceCreate(&pref);
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
-                                             &ws_bytes, sizeof(ws_bytes));
-  cublasLtMatmulHeuristicResult_t heur{};
-  int found = 0;
-  if (e == CUBLAS_STATUS_SUCCESS)
-    e = cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, lc, pref, 1, &heur, &found);
-  if (e == CUBLAS_STATUS_SUCCESS && found > 0)
-    e = cublasLtMatmul(h, op, &alpha, B, la, A, lb, &beta, C ? C : D, lc, D, lc, &heur.algo, ws,
-                       ws_bytes, st);
-  int rc = DT_OK;
-  if (e != CUBLAS_STATUS_SUCCESS || found == 0) {
-    set_error("cuBLASLt matmul (epilogue) failed (status " + std::to_string((int)e) + ")");
-    rc = DT_E_CUDA;
-  }
-  if (pref) cublasLtMatmulPreferenceDestroy(pref);
-  if (lc) cublasLtMatrixLayoutDestroy(lc);
-  if (lb) cublasLtMatrixLayoutDestroy(lb);
-  if (la) cublasLtMatrixLayoutDestroy(la);
-  if (op) cublasLtMatmulDescDestroy(op);
-  return rc;
-}
-}  // namespace
-
-bool tc_backward_ok(const Geo &g) {
-  return reuse_factored_ok(g) && g.m * g.rank < INT32_MAX && g.q * g.r_dim < ((int64_t)1 << 40);
-}
-
-size_t tc_backward_ws(const Geo &g, int64_t batch) {
-  const int64_t SR = g.s * g.rank;
-  return (size_t)round_up(batch * g.r_dim * 4, 256) * 2 /*pre, g*/ +
-         (size_t)round_up(batch * SR * 4, 256) * 2 /*P, H*/ +
-         (size_t)round_up(batch * SR * 2, 256) * 2 /*H hi, lo*/ +
-         (size_t)round_up(g.rank * g.n * 2, 256) + (size_t)round_up(batch * g.q * 2, 256) +
-         (size_t)round_up(colsum_ws(batch, g.r_dim), 256) +
-         std::max(tc_gemm_ws(g, batch), ffma_forward_ws(g, batch)) + kLtWs +
-         (size_t)round_up(2 * g.rank * g.n * 4, 256);
-}
+size_t tc_backward_ws(const Geo &g, int64_t batch) { return xtrain_backward_ws(g, batch); }
 
 int tc_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
                 const float *wf, const float *bias, int act, float act_arg,
                 const float *up, float *d_xf, float *d_wf, float *d_bias, float *d_input,
                 char *ws, size_t ws_bytes, cudaStream_t st, const float *p_in) {
   if (!tc_backward_ok(g)) {
-    set_error("tensor-core backward: reuse geometries with n % 8 == 0 and s*rank % 4 == 0");
+    set_error("tensor-core backward: reuse geometries with n % 8 == 0, rank % 4 == 0, rank <= 128");
     return DT_E_UNSUPPORTED;
   }
-  if (ws_bytes < tc_backward_ws(g, batch)) {
-    set_error("backward workspace too small: need " + std::to_string(tc_backward_ws(g, batch)));
-    return DT_E_ARG;
-  }
-  const int64_t SR = g.s * g.rank, Bs = batch * g.s;
-  if (batch == 0) {  // zero gradients of an empty batch
-    DT_CUDA_CHECK(cudaMemsetAsync(d_xf, 0, (size_t)g.m * g.rank * 4, st));
-    DT_CUDA_CHECK(cudaMemsetAsync(d_wf, 0, (size_t)g.rank * g.n * 4, st));
-    if (d_bias) DT_CUDA_CHECK(cudaMemsetAsync(d_bias, 0, (size_t)g.r_dim * 4, st));
-    return DT_OK;
-  }
-  char *cur = ws;
-  auto take = [&](int64_t bytes) {
-    char *r = cur;
-    cur += round_up(bytes, 256);
-    return r;
-  };
-  float *pre = reinterpret_cast<float *>(take(batch * g.r_dim * 4));
-  float *gbuf = reinterpret_cast<float *>(take(batch * g.r_dim * 4));
-  float *P = reinterpret_cast<float *>(take(batch * SR * 4));
-  float *H = reinterpret_cast<float *>(take(batch * SR * 4));
-  __nv_bfloat16 *Hhi = reinterpret_cast<__nv_bfloat16 *>(take(batch * SR * 2));
-  __nv_bfloat16 *Hlo = reinterpret_cast<__nv_bfloat16 *>(take(batch * SR * 2));
-  (void)Hlo;  // second half of the [hi | lo] operand that starts at Hhi
-  float *d2buf = reinterpret_cast<float *>(take(2 * g.rank * g.n * 4));
-  char *wf16 = take(g.rank * g.n * 2);
-  char *x16 = take(batch * g.q * 2);
-  float *cpart = reinterpret_cast<float *>(take(colsum_ws(batch, g.r_dim)));
-  char *fws = take(std::max(tc_gemm_ws(g, batch), ffma_forward_ws(g, batch)));
-  char *ltws = take(kLtWs);
-
-  const float *gp = up;
-  if (act != DT_ACT_IDENTITY) {
-    // g = up * act'(pre). pre is recomputed in exact fp32 (FFMA): act' is sensitive where
-    // |pre| ~ 1 while a tf32 forward's error scales with max|pre| (measured: tanh gradients off
-    // by 7e-3 with a tensor-core recompute at config 3's hidden layer, max|pre| = 132).
-    if (int rc = ffma_forward(g, batch, x, x_dtype, xf, wf, bias, DT_ACT_IDENTITY, 0.f, pre,
-                              DT_F32, fws, std::max(tc_gemm_ws(g, batch), ffma_forward_ws(g, batch)),
-                              st))
-      return rc;
-    if (int rc = launch_act_grad(batch * g.r_dim, up, pre, act, act_arg, gbuf, st)) return rc;
-    gp = gbuf;
-  }
-  if (d_bias)
-    if (int rc = launch_colsum(batch, g.r_dim, gp, d_bias, cpart, st)) return rc;
-  // bf16 x (the GEMM-1 / d_wf operand) and wf
-  const void *xt = x;
-  if (x_dtype != DT_BF16 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
-    if (int rc = launch_pack_x(batch, g.q, g.q, x, x_dtype, x16, st)) return rc;
-    xt = x16;
-  }
-  if (int rc = launch_cast_bf16(g.rank * g.n, wf, reinterpret_cast<uint16_t *>(wf16), st)) return rc;
-  if (p_in) {  // P kept by the forward (dt_forward_mse_ex)
-    P = const_cast<float *>(p_in);
-  } else {
-    GemmCall c1{xt, g.n, Bs, g.n, wf16, g.n, g.rank, nullptr, DT_ACT_IDENTITY, 0.f,
-                P, g.rank, DT_F32, nullptr, false, 0};
-    if (int rc = run_gemm(c1, st)) return rc;
-  }
-  // dXF2 (r_dim x SR) = g^T @ P'  -> d_xf's first r_dim*s rows; the discarded tail gets 0
-  if (int rc = lt_gemm(st, g.r_dim, SR, batch, gp, true, g.r_dim, P, false, SR, d_xf, SR,
-                       CUDA_R_32F, 0.f, ltws, kLtWs))
-    return rc;
-  const int64_t tail = (g.m - g.r_dim * g.s) * g.rank;
-  if (tail > 0)
-    DT_CUDA_CHECK(cudaMemsetAsync(d_xf + g.r_dim * SR, 0, (size_t)tail * 4, st));
-  // H (B x SR) = g @ XF2, XF2 = xf viewed (r_dim x SR)
-  if (int rc = lt_gemm(st, batch, SR, g.r_dim, gp, false, g.r_dim, xf, false, SR, H, SR, CUDA_R_32F,
-                       0.f, ltws, kLtWs))
-    return rc;
-  // d_wf (rank x n) = H'^T @ x'  with H = hi + lo in bf16: one GEMM over [hi | lo] (2*rank
-  // rows, x read once), then the two halves added (fixed order hi + lo)
-  __nv_bfloat16 *H2 = Hhi;  // Bs x 2*rank bf16: spans the adjacent Hhi and Hlo regions
-  float *D2 = d2buf;        // 2*rank x n fp32
-  k_split_bf16_rows<<<std::min<int64_t>((batch * SR + 255) / 256, 4096), 256, 0, st>>>(Bs, (int)g.rank,
-                                                                                    H, H2);
-  if (int rc = check_launch("split_bf16_rows")) return rc;
-  if (int rc = lt_gemm(st, 2 * g.rank, g.n, Bs, H2, true, 2 * g.rank, xt, false, g.n, D2, g.n,
-                       CUDA_R_16BF, 0.f, ltws, kLtWs))
-    return rc;
-  k_add_halves<<<(unsigned)((g.rank * g.n + 255) / 256), 256, 0, st>>>(g.rank * g.n, D2, d_wf);
-  if (int rc = check_launch("add_halves")) return rc;
-  // d_input (B*s x n) = H' @ wf
-  if (d_input)
-    if (int rc = lt_gemm(st, Bs, g.n, g.rank, H, false, g.rank, wf, false, g.n, d_input, g.n,
-                         CUDA_R_32F, 0.f, ltws, kLtWs))
-      return rc;
-  return DT_OK;
+  return xtrain_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, up, d_xf, d_wf, d_bias,
+                         d_input, ws, ws_bytes, st, p_in);
 }
 
 }  // namespace dt

@@ -70,6 +70,8 @@ struct XgParams {
   float *colsum_part;         // [2 * n_mb][N]
   __nv_bfloat16 *out16;       // XE_SPLITH
   int h_r, h_s;
+  int pair_half;              // XE_PAIRSUM: out[:, k] = D[:, k] + D[:, k + pair_half]
+  int ks_major;               // unit order: K split slowest (tiles of one split run together)
 };
 
 // K-major: rows of 128 B (the k-block), 8-row swizzle atoms 1024 B apart (SWIZZLE_128B).
@@ -118,9 +120,9 @@ __global__ void __launch_bounds__(XTHREADS, 1)
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *full = bars, *empty = bars + p.S, *tfull = bars + 2 * p.S, *tempty = tfull + 2;
-  uint64_t *tload = tempty + 2;  // [XEPI][2] target boxes (XE_MSE)
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(tload + 2 * XEPI);
-  float *red = reinterpret_cast<float *>(tslot + 4);  // XE_MSE colsum exchange [2][4][32]
+  uint64_t *tload = tempty + 2;  // [XEPI][3] target boxes (XE_MSE)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tload + 3 * XEPI);
+  float *red = reinterpret_cast<float *>(smem + p.off_bar + 512);  // XE_MSE [2][4][256] colsums
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * XEPI); }
-    for (int i = 0; i < 2 * XEPI; ++i) mbar_init(&tload[i], 1);
+    for (int i = 0; i < 3 * XEPI; ++i) mbar_init(&tload[i], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -148,8 +150,15 @@ __global__ void __launch_bounds__(XTHREADS, 1)
   griddep_wait();  // operands may come from the previous kernel on the stream
 
   auto unit_of = [&](int u, int &mb, int &nb, int &ks) {
-    ks = u % p.splits;
-    const int t = u / p.splits;
+    int t;
+    if (p.ks_major) {
+      const int tiles = p.n_mb * p.n_nb;
+      ks = u / tiles;
+      t = u - ks * tiles;
+    } else {
+      ks = u % p.splits;
+      t = u / p.splits;
+    }
     nb = t % p.n_nb;
     mb = t / p.n_nb;
   };
@@ -216,11 +225,32 @@ __global__ void __launch_bounds__(XTHREADS, 1)
     // ---------------- epilogue (both CTAs: 128 rows x BN columns each) ----------------
     const int e = warp - 2, q = warp & 3, h = e / 4;
     const uint32_t lane_t = (uint32_t)(32 * q) << 16;
-    const uint32_t stg0 = smem_u32(smem) + p.off_stg + (uint32_t)e * 2u * XSTG;
-    uint8_t *stg0p = smem + p.off_stg + e * 2 * XSTG;
-    int acc = 0, sb = 0;
+    constexpr int NBUF = EPI == XE_MSE ? 3 : 2;  // staging boxes per warp
+    const uint32_t stg0 = smem_u32(smem) + p.off_stg + (uint32_t)e * NBUF * XSTG;
+    uint8_t *stg0p = smem + p.off_stg + e * NBUF * XSTG;
+    const int nch = EPI == XE_PAIRSUM ? (p.pair_half + 31) / 32 : BN / 32;
+    int acc = 0, jb = 0;  // jb: this warp's running chunk count (staging buffer = jb % NBUF)
     uint32_t aphase = 0;
-    uint32_t tph[2] = {0u, 0u};
+    uint32_t tph = 0;     // XE_MSE: parity bit per staging buffer (bit b)
+    // XE_MSE target prefetch: the warp's chunk sequence (unit, chunk) walked two chunks ahead of
+    // the one being processed, across unit boundaries (the target does not depend on the MMAs)
+    int lu = cid, lc = h, nload = 0;
+    auto load_next = [&]() {
+      if (lu >= p.units) return;
+      int mb, nb, ks;
+      unit_of(lu, mb, nb, ks);
+      const int b = nload % NBUF;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&tload[NBUF * e + b], XSTG);
+        tma_load_2d(stg0p + b * XSTG, &tm_t, &tload[NBUF * e + b], nb * BN + 32 * lc,
+                    mb * 256 + (int)crank * 128 + 32 * q);
+      }
+      ++nload;
+      lc += 2;
+      if (lc >= nch) { lc = h; lu += ncl; }
+    };
+    if constexpr (EPI == XE_MSE) { load_next(); load_next(); }
+    int par = 0;  // XE_MSE: column-sum exchange buffer parity (by unit)
     for (int u = cid; u < p.units; u += ncl) {
       int mb, nb, ks;
       unit_of(u, mb, nb, ks);
@@ -229,14 +259,13 @@ __global__ void __launch_bounds__(XTHREADS, 1)
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       double sq = 0.0;
-      const int nch = EPI == XE_PAIRSUM ? BN / 64 : BN / 32;
       for (int c = h; c < nch; c += 2) {
         const int col0 = nb * BN + 32 * c;  // first D column of this chunk
         uint32_t v[32];
         tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(acc * BN + 32 * c), v);
         if constexpr (EPI == XE_PAIRSUM) {
           uint32_t w[32];
-          tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(acc * BN + 32 * c + BN / 2), w);
+          tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(acc * BN + 32 * c + p.pair_half), w);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -246,7 +275,19 @@ __global__ void __launch_bounds__(XTHREADS, 1)
         }
         if constexpr (EPI == XE_SPLITH) {
           // H[row, col0 .. col0+31] -> H2 row (row * s + col0 / r), [hi | lo]
-          if (row < p.M) {
+          if (row < p.M && (p.h_r & 31)) {  // a chunk may cross a segment: element stores
+#pragma unroll 4
+            for (int i = 0; i < 32; ++i) {
+              const int cc = col0 + i;
+              if (cc >= p.N) break;
+              const int seg = cc / p.h_r, k = cc - seg * p.h_r;
+              const float a = __uint_as_float(v[i]);
+              const __nv_bfloat16 ha = __float2bfloat16_rn(a);
+              __nv_bfloat16 *hp = p.out16 + ((int64_t)row * p.h_s + seg) * (2 * p.h_r) + k;
+              hp[0] = ha;
+              hp[p.h_r] = __float2bfloat16_rn(a - __bfloat162float(ha));
+            }
+          } else if (row < p.M) {
             const int seg = col0 / p.h_r, k0 = col0 % p.h_r;
             __nv_bfloat16 *hp = p.out16 + ((int64_t)row * p.h_s + seg) * (2 * p.h_r) + k0;
             uint32_t hi[16], lo[16];
@@ -269,18 +310,16 @@ __global__ void __launch_bounds__(XTHREADS, 1)
           }
           continue;
         } else {
-          // staging buffer sb of this warp: free once its previous TMA store read it
-          if (lane == 0) bulk_wait_group_read<1>();
-          __syncwarp();
-          const uint32_t sbase = stg0 + (uint32_t)sb * XSTG;
-          uint8_t *sptr = stg0p + sb * XSTG;
-          if constexpr (EPI == XE_MSE) {
-            if (lane == 0) {
-              mbar_arrive_expect_tx(&tload[2 * e + sb], XSTG);
-              tma_load_2d(sptr, &tm_t, &tload[2 * e + sb], col0, r0);
-            }
-            mbar_wait(&tload[2 * e + sb], tph[sb]);
-            tph[sb] ^= 1;
+          const int b = jb % NBUF;
+          ++jb;
+          const uint32_t sbase = stg0 + (uint32_t)b * XSTG;
+          uint8_t *sptr = stg0p + b * XSTG;
+          if constexpr (EPI == XE_MSE) {  // this chunk's target box (loaded two chunks ago)
+            mbar_wait(&tload[NBUF * e + b], (tph >> b) & 1u);
+            tph ^= 1u << b;
+          } else {  // the box's previous TMA store has read it
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
           }
           float bias_v[32];
 #pragma unroll
@@ -308,33 +347,32 @@ __global__ void __launch_bounds__(XTHREADS, 1)
               }
             }
             sts_v4(sbase + stg_off(lane, c16), __float_as_uint(o[0]), __float_as_uint(o[1]),
-                         __float_as_uint(o[2]), __float_as_uint(o[3]));
+                   __float_as_uint(o[2]), __float_as_uint(o[3]));
           }
           if constexpr (EPI == XE_MSE) {
             sq += (double)csq;
-            // column sums of g over this warp's 32 rows (transposed read of the staging box:
-            // thread = column), then over the CTA's four lane quarters in quarter order
+            // column sums of g over this warp's 32 rows (transposed read of the box: thread =
+            // column) into the unit's exchange row of this lane quarter
             __syncwarp();
             float cs = 0.f;
             for (int r = 0; r < 32; ++r)
               cs += reinterpret_cast<const float *>(sptr + stg_off(r, lane >> 2))[lane & 3];
-            red[(h * 4 + q) * 32 + lane] = cs;
-            named_bar_sync(1 + h, 128);
-            if (q == 0 && col0 + lane < p.N)
-              p.colsum_part[(int64_t)(mb * 2 + (int)crank) * p.N + col0 + lane] =
-                  ((red[(h * 4 + 0) * 32 + lane] + red[(h * 4 + 1) * 32 + lane]) +
-                   red[(h * 4 + 2) * 32 + lane]) + red[(h * 4 + 3) * 32 + lane];
-            named_bar_sync(1 + h, 128);
+            red[(par * 4 + q) * 256 + 32 * c + lane] = cs;
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int ocol = EPI == XE_PAIRSUM ? nb * (BN / 2) + 32 * c : col0;
+            const int ocol = EPI == XE_PAIRSUM ? 32 * c : col0;
             const int orow = r0 + (p.splits > 1 ? ks * p.Mp : 0);
             tma_store_2d(&tm_o, sptr, ocol, orow);
             bulk_commit_group();
           }
-          sb ^= 1;
+          if constexpr (EPI == XE_MSE) {
+            // the store of the previous chunk has read its box: prefetch two chunks ahead into it
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
+            load_next();
+          }
         }
       }
       if constexpr (EPI == XE_MSE) {
@@ -346,6 +384,16 @@ __global__ void __launch_bounds__(XTHREADS, 1)
       __syncwarp();
       if (lane == 0) arrive_leader_x(&tempty[acc], crank);
       if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if constexpr (EPI == XE_MSE) {
+        // the CTA's column sums of the unit: four lane quarters added in quarter order
+        named_bar_sync(1, 32 * XEPI);
+        const int t = threadIdx.x - 64;
+        if (t < BN && nb * BN + t < p.N)
+          p.colsum_part[(int64_t)(mb * 2 + (int)crank) * p.N + nb * BN + t] =
+              ((red[(par * 4 + 0) * 256 + t] + red[(par * 4 + 1) * 256 + t]) +
+               red[(par * 4 + 2) * 256 + t]) + red[(par * 4 + 3) * 256 + t];
+        par ^= 1;
+      }
     }
     if (lane == 0) bulk_wait_group<0>();
     __syncwarp();
@@ -373,21 +421,27 @@ XgFn pick_x(int epi) {
 }
 
 // out (or out^T) = sum over splits (fixed order) of the partial slices, optionally the hi + lo
-// row halves added (pair_half > 0: rows [0, pair_half) + rows [pair_half, 2 pair_half)).
+// column halves added (pair_half > 0: columns [0, pair_half) + [pair_half, 2 pair_half)).
 __global__ void k_xg_reduce(int splits, int M, int N, int Mp, const float *part, float *out,
-                            int ldo, int transpose, int pair_half, float alpha) {
-  const int rows = pair_half > 0 ? pair_half : M;
-  const int64_t total = (int64_t)rows * N;
+                            int ldo, int transpose, int pair_half) {
+  const int cols = pair_half > 0 ? pair_half : N;
+  const int64_t total = (int64_t)M * cols;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int m = (int)(i / N), n = (int)(i - (int64_t)m * N);
+    int m, n;
+    if (transpose) {  // consecutive threads walk m: coalesced writes of out[n][m]
+      n = (int)(i / M);
+      m = (int)(i - (int64_t)n * M);
+    } else {
+      m = (int)(i / cols);
+      n = (int)(i - (int64_t)m * cols);
+    }
     float s = 0.f;
     for (int k = 0; k < splits; ++k) {
-      const float *sl = part + (int64_t)k * Mp * N;
-      s += sl[(int64_t)m * N + n];
-      if (pair_half > 0) s += sl[(int64_t)(m + pair_half) * N + n];
+      const float *sl = part + ((int64_t)k * Mp + m) * N;
+      s += sl[n];
+      if (pair_half > 0) s += sl[n + pair_half];
     }
-    s *= alpha;
     if (transpose)
       out[(int64_t)n * ldo + m] = s;
     else
@@ -395,20 +449,56 @@ __global__ void k_xg_reduce(int splits, int M, int N, int Mp, const float *part,
   }
 }
 
-// column sums over the [rows][N] partials in row order (d_bias from XE_MSE's per-CTA sums)
-__global__ void k_colsum_rows(int rows, int N, const float *part, float *out) {
+// column sums over the [rows][N] partials (d_bias from XE_MSE's per-CTA sums), two fixed-order
+// levels: block (x, y) sums rows [y*kRowsPer, ...) of its columns into mid[y][n], then k_colsum_mid
+// adds the mid rows in order
+constexpr int kRowsPer = 32;
+__global__ void k_colsum_rows(int rows, int N, const float *part, float *mid) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int r0 = blockIdx.y * kRowsPer, r1 = min(rows, r0 + kRowsPer);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += part[(int64_t)r * N + n];
+  mid[(int64_t)blockIdx.y * N + n] = s;
+}
+__global__ void k_colsum_mid(int chunks, int N, const float *mid, float *out) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += part[(int64_t)r * N + n];
+  for (int c = 0; c < chunks; ++c) s += mid[(int64_t)c * N + n];
   out[n] = s;
+}
+
+// fixed-order fp64 sum of many partials: block b sums its contiguous slice (strided per thread,
+// tree in shared memory), then one block adds the block sums in order
+__global__ void __launch_bounds__(256) k_sum_f64_blocks(int64_t count, const double *part,
+                                                        double *mid) {
+  __shared__ double red[256];
+  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(count, b0 + per);
+  double s = 0.0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += 256) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = 128; h; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mid[blockIdx.x] = red[0];
+}
+__global__ void k_sum_f64_final(int n, const double *mid, double *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += mid[i];
+    out[0] = s;
+  }
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
 size_t xgemm_ws(const XGemm &g) {
-  if (g.splits <= 1) return 0;
+  if (g.splits <= 1 && !g.reduce_transpose && g.reduce_pair_half <= 0) return 0;
   const int64_t Mp = (g.M + 255) / 256 * 256;
   return (size_t)g.splits * Mp * g.N * 4;
 }
@@ -444,12 +534,12 @@ int xgemm(const XGemm &g, cudaStream_t st) {
     set_error("xgemm: an MN-major B needs BN/2 * element size >= 128 bytes");
     return DT_E_ARG;
   }
-  if (g.epi == XE_PAIRSUM && (g.N != BN || g.splits > 1)) {
-    set_error("xgemm: the pair-sum epilogue needs one column block (N == BN), no split");
+  if (g.epi == XE_PAIRSUM && (g.N > BN || 2 * g.pair_half > g.N || g.pair_half <= 0 || g.splits > 1)) {
+    set_error("xgemm: the pair-sum epilogue needs one column block (N <= BN), no split");
     return DT_E_ARG;
   }
-  if (g.epi == XE_SPLITH && (g.h_r % 32 != 0 || g.splits > 1)) {
-    set_error("xgemm: the H split epilogue needs rank % 32 == 0, no split");
+  if (g.epi == XE_SPLITH && g.splits > 1) {
+    set_error("xgemm: the H split epilogue takes no split");
     return DT_E_ARG;
   }
   int dev = 0, nsm = 148;
@@ -485,9 +575,13 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   p.out16 = g.out16;
   p.h_r = g.h_r;
   p.h_s = g.h_s;
+  p.pair_half = g.pair_half;
+  p.ks_major = g.ks_major;
   p.stage_bytes = XA_BYTES + (uint32_t)nhalf * 128u;
-  const uint32_t stg_bytes = (g.epi == XE_SPLITH) ? 0u : (uint32_t)XEPI * 2u * XSTG;
-  const uint32_t tail = 1024 + 512;  // barriers, TMEM slot, colsum exchange, alignment slack
+  const uint32_t stg_bytes = (g.epi == XE_SPLITH) ? 0u
+                             : (uint32_t)XEPI * (g.epi == XE_MSE ? 3u : 2u) * XSTG;
+  // barriers + TMEM slot (512 B), then the XE_MSE column-sum exchange [2][4][256] floats
+  const uint32_t tail = 512 + (g.epi == XE_MSE ? 8192u : 0u);
   p.S = (int)std::min<uint32_t>(8, (XSMEM_MAX - stg_bytes - tail - 1024) / p.stage_bytes);
   p.off_stg = (uint32_t)p.S * p.stage_bytes;
   p.off_bar = p.off_stg + stg_bytes;
@@ -514,8 +608,15 @@ int xgemm(const XGemm &g, cudaStream_t st) {
                                              (uint64_t)g.ldb * esz, bke, (uint32_t)nhalf, true))
     return rc;
   float *out = g.out;
-  int64_t out_rows = g.M, out_cols = g.epi == XE_PAIRSUM ? g.N / 2 : g.N, ldo = g.ldo;
-  if (p.splits > 1) {
+  int64_t out_rows = g.M, out_cols = g.epi == XE_PAIRSUM ? g.pair_half : g.N, ldo = g.ldo;
+  // partial slices (then the fixed-order reduce) for split-K, and for a transposed or
+  // column-paired result
+  const bool use_part = p.splits > 1 || g.reduce_transpose || g.reduce_pair_half > 0;
+  if (use_part && g.epi != XE_STORE) {
+    set_error("xgemm: split / transposed / paired results need the store epilogue");
+    return DT_E_ARG;
+  }
+  if (use_part) {
     if (!g.part) {
       set_error("xgemm: split-K needs a partial buffer (xgemm_ws bytes)");
       return DT_E_ARG;
@@ -564,21 +665,38 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   if (int rc = check_launch("tc_xgemm")) return rc;
   if (g.n_loss_part) *g.n_loss_part = (int64_t)p.units * 2 * XEPI;
 
-  if (p.splits > 1) {
+  if (use_part) {
     const int pair = g.reduce_pair_half;
-    const int64_t rows = pair > 0 ? pair : g.M;
-    const int64_t total = rows * g.N;
+    const int64_t total = g.M * (pair > 0 ? pair : g.N);
     k_xg_reduce<<<(unsigned)std::min<int64_t>((total + 255) / 256, 8 * nsm), 256, 0, st>>>(
         p.splits, (int)g.M, (int)g.N, p.Mp, g.part, g.out, (int)g.ldo, g.reduce_transpose ? 1 : 0,
-        pair, 1.0f);
+        pair);
     if (int rc = check_launch("xg_reduce")) return rc;
   }
   return DT_OK;
 }
 
-int xgemm_colsum(int rows, int64_t N, const float *part, float *out, cudaStream_t st) {
-  k_colsum_rows<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rows, (int)N, part, out);
-  return check_launch("colsum_rows");
+size_t xgemm_reduce_scratch(int rows, int64_t N) {
+  return (size_t)((rows + kRowsPer - 1) / kRowsPer) * N * 4 + 64 * 8;
+}
+
+int xgemm_colsum(int rows, int64_t N, const float *part, float *out, void *scratch, cudaStream_t st) {
+  const int chunks = (rows + kRowsPer - 1) / kRowsPer;
+  float *mid = reinterpret_cast<float *>(scratch);
+  k_colsum_rows<<<dim3((unsigned)((N + 255) / 256), (unsigned)chunks), 256, 0, st>>>(rows, (int)N,
+                                                                                   part, mid);
+  if (int rc = check_launch("colsum_rows")) return rc;
+  k_colsum_mid<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(chunks, (int)N, mid, out);
+  return check_launch("colsum_mid");
+}
+
+int xgemm_sum_f64(int64_t count, const double *part, double *out, void *scratch, cudaStream_t st) {
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(64, (count + 2047) / 2048));
+  double *mid = reinterpret_cast<double *>(scratch);
+  k_sum_f64_blocks<<<nb, 256, 0, st>>>(count, part, mid);
+  if (int rc = check_launch("sum_f64_blocks")) return rc;
+  k_sum_f64_final<<<1, 32, 0, st>>>(nb, mid, out);
+  return check_launch("sum_f64_final");
 }
 
 }  // namespace dt

@@ -1,0 +1,77 @@
+"""Per-kernel device-time table of one workload step, from CUPTI activity records (torch.profiler).
+
+    python scripts/prof_kernels.py c5 [steps]      # config-5 training step (global batch 65536)
+    python scripts/prof_kernels.py c3 [steps]      # config-3 network forward
+    python scripts/prof_kernels.py c2 [steps]      # config-2 layer forward
+
+Prints: kernel, launches, mean us, total us per step, share of the step's kernel time.
+"""
+import collections
+import math
+import os
+import sys
+
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1802_06944_b200 as D  # noqa: E402
+
+
+def kname(full):
+    """Short kernel name from a demangled signature: the k_* identifier with its template args."""
+    import re
+    m = re.search(r"(k_\w+)(<[^()]*>)?", full)
+    return (m.group(1) + (m.group(2) or "")) if m else full.split("(")[0][-60:]
+
+
+def c5_step(rows=65536):
+    q = r_dim = 8192
+    plan = D.LayerPlan(q=q, r_dim=r_dim, rank=64, m=65536, n=1024)
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    xf = (torch.randn(65536, 64, device="cuda", generator=g) / 8).cpu().numpy()
+    wf = (torch.randn(64, 1024, device="cuda", generator=g) / 8).cpu().numpy()
+    bias = (torch.randn(r_dim, device="cuda", generator=g) * 0.01).cpu().numpy()
+    layer = D.DeepThinLayer(plan, xf, wf, bias, mma="bf16")
+    x = torch.randn(rows, q, device="cuda", generator=g).to(torch.bfloat16)
+    t = torch.randn(rows, r_dim, device="cuda", generator=g)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    return lambda: D.train_step(layer, x, t, 1e-4, loss_out=loss)
+
+
+def main():
+    key = sys.argv[1] if len(sys.argv) > 1 else "c5"
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    rows = int(sys.argv[3]) if len(sys.argv) > 3 else 65536
+    if key == "c5":
+        step = c5_step(rows)
+    else:
+        import bench
+        raise SystemExit("use bench.py for c2/c3 (roofline line); this script covers c5")
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            step()
+        torch.cuda.synchronize()
+    agg = collections.defaultdict(list)
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA:
+            agg[kname(e.name)].append(e.time_range.end - e.time_range.start)
+    tot = sum(sum(v) for v in agg.values()) / steps
+    print(f"{key}: {ms * 1e3:.1f} us per step (events), kernels {tot:.1f} us per step")
+    for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        print(f"{sum(v) / steps:9.1f} us  {len(v) / steps:5.1f}x  {sum(v) / len(v):8.1f} us  "
+              f"{sum(v) / steps / tot:6.1%}  {name}")
+
+
+if __name__ == "__main__":
+    main()

@@ -145,7 +145,11 @@ def test_new_entry_points_validate_before_touching_the_gpu():
     assert lib.dt_lstm_sequence(C.byref(lstm), 10, 65, P4(), P4(), P4(), P4(), None, None, 0,
                                 None) == _lib.DT_E_UNSUPPORTED
     assert lib.dt_lstm_cell(4, 8, None, 4, None, None, None, None, None) == _lib.DT_E_DIM  # ld < hidden
-    assert lib.dt_forward_p_bytes(C.byref(reuse), 128) == 128 * 8 * 3 * 4
+    # P is kept for the tensor-core backward (k_train.cu): reuse geometries with rank % 4 == 0
+    # (TMA pitches of P and of H's bf16 hi | lo rows); rank 3 trains on the FFMA backward
+    assert lib.dt_forward_p_bytes(C.byref(reuse), 128) == 0
+    c5 = _lib.Plan(8192, 8192, 64, 65536, 1024)
+    assert lib.dt_forward_p_bytes(C.byref(c5), 128) == 128 * 8 * 64 * 4
     assert lib.dt_forward_p_bytes(C.byref(general), 128) == 0
     assert lib.dt_profile_kernel_kind(7) == _lib.DT_E_ARG
 
