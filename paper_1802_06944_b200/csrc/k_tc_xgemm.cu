@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
             for (int i = 0; i < 32; ++i) bias_v[i] = (col0 + i < p.N) ? __ldg(p.bias + col0 + i) : 0.f;
           }
           float csq = 0.f;
+          float go[32];  // XE_MSE: this chunk's g values (column sums below)
 #pragma unroll
           for (int c16 = 0; c16 < 8; ++c16) {
             float o[4];
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
                 const bool ok = row < p.M && col0 + i < p.N;
                 csq = ok ? fmaf(dz, dz, csq) : csq;
                 o[j] = ok ? p.scale * dz : 0.f;
+                go[i] = o[j];
               } else {
                 o[j] = fmaf(p.alpha, z, bias_v[i]);
               }
@@ -351,13 +353,22 @@ __global__ void __launch_bounds__(XTHREADS, 1)
           }
           if constexpr (EPI == XE_MSE) {
             sq += (double)csq;
-            // column sums of g over this warp's 32 rows (transposed read of the box: thread =
-            // column) into the unit's exchange row of this lane quarter
-            __syncwarp();
-            float cs = 0.f;
-            for (int r = 0; r < 32; ++r)
-              cs += reinterpret_cast<const float *>(sptr + stg_off(r, lane >> 2))[lane & 3];
-            red[(par * 4 + q) * 256 + 32 * c + lane] = cs;
+            // column sums of g over this warp's 32 rows: a shuffle transpose-reduce (5 halving
+            // rounds, fixed order) leaves column `lane`'s sum in lane `lane`
+            float cs[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cs[i] = go[i];
+#pragma unroll
+            for (int w = 16; w >= 1; w >>= 1) {
+              const bool upper = (lane & w) != 0;
+#pragma unroll
+              for (int i = 0; i < w; ++i) {
+                const float send = upper ? cs[i] : cs[i + w];
+                const float keep = upper ? cs[i + w] : cs[i];
+                cs[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+              }
+            }
+            red[(par * 4 + q) * 256 + 32 * c + lane] = cs[0];
           }
           fence_proxy_async_smem();
           __syncwarp();
