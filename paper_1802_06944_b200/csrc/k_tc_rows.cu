@@ -694,8 +694,10 @@ static inline int64_t rows_np(const Geo &g) { return (2 * g.rank + 15) / 16 * 16
 static inline int64_t rows_wf_bytes(const Geo &g) { return (2 * g.rank * g.n * 2 + 255) / 256 * 256; }
 
 // Cluster size: CTAs sharing one row tile (segments and output chunks split among them).
+// Default 4: clusters of 4 fill all 148 SMs (37 clusters; clusters of 8 fit only 15 times =
+// 120 SMs), measured 298 vs 316 us per config-3 forward.
 static int rows_cluster(const Geo &g) {
-  static const int want = getenv("DEEPTHIN_ROWS_CS") ? atoi(getenv("DEEPTHIN_ROWS_CS")) : 8;
+  static const int want = getenv("DEEPTHIN_ROWS_CS") ? atoi(getenv("DEEPTHIN_ROWS_CS")) : 4;
   for (int cs : {8, 4, 2})
     if (cs <= want && g.s % cs == 0) return cs;
   return 1;

@@ -39,15 +39,35 @@ def c5_step(rows=65536):
     return lambda: D.train_step(layer, x, t, 1e-4, loss_out=loss)
 
 
+def c3_step(rows=16384):
+    import numpy as np
+    import bench
+    from paper_1802_06944_b200 import model_io as mi
+    layers, params, rx = bench.c3_params()
+    entries, factors, biases = [], [], []
+    for i, ((q, r_dim, rk, n, m), (xf, wf, b)) in enumerate(zip(layers, params)):
+        plan = D.LayerPlan(q=q, r_dim=r_dim, rank=rk, m=m, n=n)
+        entries.append((f"fc{i}", plan))
+        factors.append(mi.StoredFactors(xf, wf, plan))
+        biases.append(b)
+    model = mi.CompressedModel(plans=D.NetworkPlan(layers=tuple(entries), target_ratio=0.01,
+                                                   achieved_total_ratio=0.0, floor_hits=()),
+                               factors=factors, biases=biases)
+    dm = model.to_device(bench.C3_ACTS, mma="bf16")
+    x = torch.randn(rows, 440, device="cuda").to(torch.bfloat16)
+    return lambda: dm.forward(x, out_dtype=torch.bfloat16, graph=True)
+
+
 def main():
     key = sys.argv[1] if len(sys.argv) > 1 else "c5"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     rows = int(sys.argv[3]) if len(sys.argv) > 3 else 65536
     if key == "c5":
         step = c5_step(rows)
+    elif key == "c3":
+        step = c3_step(rows if len(sys.argv) > 3 else 16384)
     else:
-        import bench
-        raise SystemExit("use bench.py for c2/c3 (roofline line); this script covers c5")
+        raise SystemExit("configs: c5, c3")
     for _ in range(3):
         step()
     torch.cuda.synchronize()

@@ -136,7 +136,7 @@ def test_new_entry_points_validate_before_touching_the_gpu():
         == _lib.DT_E_UNSUPPORTED
     assert lib.dt_rows_prepare(C.byref(reuse), 0, _lib.DT_BF16, None, None, None, None, None) \
         == _lib.DT_E_ARG
-    assert lib.dt_rows_posts_per_tile(C.byref(reuse)) == 8 * 16
+    assert lib.dt_rows_posts_per_tile(C.byref(reuse)) == 4 * 16  # cluster of 4 x 16 epilogue warps
     lstm = _lib.Plan(2048, 2048, 32, 16384, 256)
     assert lib.dt_lstm_sequence_workspace_bytes(C.byref(lstm), 64) > 0
     assert lib.dt_lstm_sequence_workspace_bytes(C.byref(lstm), 65) == 0   # batch <= 64
