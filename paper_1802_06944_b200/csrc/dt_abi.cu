@@ -339,6 +339,7 @@ size_t dt_backward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) 
   Geo g;
   if (make_geo(plan, &g) || batch < 0) return 0;
   if (mma == DT_MMA_BF16 && tc_backward_ok(g)) return tc_backward_ws(g, batch);
+  if (mma == DT_MMA_BF16 && xback_general_ok(g)) return xback_general_ws(g, batch);
   return ffma_backward_ws(g, batch);
 }
 
@@ -384,6 +385,10 @@ int dt_backward_ex(const dt_plan *plan, int64_t batch, int mma, const void *x, i
     set_error("backward: a kept P applies to the tensor-core backward of reuse geometries only");
     return DT_E_UNSUPPORTED;
   }
+  // general (straddling) geometries on the tensor cores (k_train.cu)
+  if (mma == DT_MMA_BF16 && xback_general_ok(g))
+    return xback_general(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
+                         d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
   return ffma_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
                        d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
 }

@@ -118,6 +118,8 @@ struct XGemm {
   int64_t ldb = 0;
   int b_mn = 0;
   int64_t b_wrap_k = 0;  // > 0: B's rows (K) wrap modulo this (A = [hi; lo] stacked along K)
+  int64_t b_rows = 0;    // with b_wrap_k: rows B actually stores (< wrap: zero fill past them)
+  int force_part = 0;    // result through the partial buffer + reduce (any output pitch)
   int el = 1;
   int BN = 256;
   int splits = 1;
@@ -159,6 +161,14 @@ int xtrain_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
                     const float *wf, const float *bias, int act, float act_arg, const float *up,
                     float *d_xf, float *d_wf, float *d_bias, float *d_input, char *ws,
                     size_t ws_bytes, cudaStream_t st, const float *p_in);
+// general (straddling) geometries: d_W^T = g^T x on tcgen05 (bf16 x, g hi | lo), the flat
+// inverse re-layout as a view, then d_xf / d_wf / d_input as tf32 GEMMs (k_train.cu)
+bool xback_general_ok(const Geo &g);
+size_t xback_general_ws(const Geo &g, int64_t batch);
+int xback_general(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                  const float *wf, const float *bias, int act, float act_arg, const float *up,
+                  float *d_xf, float *d_wf, float *d_bias, float *d_input, char *ws,
+                  size_t ws_bytes, cudaStream_t st);
 
 // ---- two-phase tensor-core path: k_tc_gemm.cu ---------------------------------------
 // W^T (r_dim x round_up(q, 8), bf16) regenerated from the factors (f_dtype DT_F32 or DT_BF16)

@@ -509,7 +509,7 @@ __global__ void k_sum_f64_final(int n, const double *mid, double *out) {
 
 // ---------------------------------------------------------------------------------------------
 size_t xgemm_ws(const XGemm &g) {
-  if (g.splits <= 1 && !g.reduce_transpose && g.reduce_pair_half <= 0) return 0;
+  if (g.splits <= 1 && !g.reduce_transpose && g.reduce_pair_half <= 0 && !g.force_part) return 0;
   const int64_t Mp = (g.M + 255) / 256 * 256;
   return (size_t)g.splits * Mp * g.N * 4;
 }
@@ -612,7 +612,10 @@ int xgemm(const XGemm &g, cudaStream_t st) {
                       : encode_tensor_map_2d(&tm_a, tdt, A, (uint64_t)g.K, (uint64_t)g.M,
                                              (uint64_t)g.lda * esz, bke, 128, true))
     return rc;
-  const uint64_t kb_rows = g.b_wrap_k > 0 ? (uint64_t)g.b_wrap_k : (uint64_t)g.K;
+  // rows of B along K: the wrap length, or the stored extent when shorter (zero fill past it)
+  const uint64_t kb_rows = g.b_wrap_k > 0 ? (uint64_t)(g.b_rows > 0 ? std::min(g.b_rows, g.b_wrap_k)
+                                                                   : g.b_wrap_k)
+                                          : (uint64_t)g.K;
   if (int rc = g.b_mn ? encode_tensor_map_2d_sw(&tm_b, tdt, B, (uint64_t)g.N, kb_rows,
                                                 (uint64_t)g.ldb * esz, 128 / esz, bke, mn_sw)
                       : encode_tensor_map_2d(&tm_b, tdt, B, kb_rows, (uint64_t)g.N,
@@ -622,7 +625,8 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   int64_t out_rows = g.M, out_cols = g.epi == XE_PAIRSUM ? g.pair_half : g.N, ldo = g.ldo;
   // partial slices (then the fixed-order reduce) for split-K, and for a transposed or
   // column-paired result
-  const bool use_part = p.splits > 1 || g.reduce_transpose || g.reduce_pair_half > 0;
+  const bool use_part = p.splits > 1 || g.reduce_transpose || g.reduce_pair_half > 0 ||
+                        g.force_part;
   if (use_part && g.epi != XE_STORE) {
     set_error("xgemm: split / transposed / paired results need the store epilogue");
     return DT_E_ARG;

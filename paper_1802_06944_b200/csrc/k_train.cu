@@ -304,4 +304,184 @@ int xtrain_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
   return DT_OK;
 }
 
+
+// =============================================================================================
+// Backward of general (straddling) geometries on the tensor cores (grad.py:63-95):
+//   g       = upstream (.* act'(pre), pre recomputed in exact fp32)
+//   d_bias  = sum_b g
+//   d_W^T   = g^T @ x   (r_dim x q)   = d_v[0 : q*r_dim], the flat inverse re-layout: row j of
+//             d_W^T is v[j*q : (j+1)*q] (factor.py:87-93), so the row-major product IS d_v and
+//             d_aux = d_v viewed (m x n) with a zero tail — no scatter kernel
+//             bf16 x (exact) against g split hi | lo and stacked along K (two bf16 products in
+//             one GEMM: B's rows wrap), fp32 accumulate
+//   d_xf    = d_aux @ wf^T                    (tf32)
+//   d_wf    = xf^T @ d_aux = (d_aux^T @ xf)^T (tf32, both MN-major, transposed reduce)
+//   d_input = g @ W^T                         (tf32, W = decompress(fp) in fp32; only if asked)
+// =============================================================================================
+namespace {
+
+__global__ void k_split_g_rows(int64_t rows, int64_t cols, int64_t rows_p, const float *g,
+                               __nv_bfloat16 *g2) {
+  // g2 rows [0, rows_p): hi (zero past rows), rows [rows_p, 2 rows_p): lo
+  const int64_t tot = rows_p * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols;
+    const float v = r < rows ? g[i] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    g2[i] = h;
+    g2[tot + i] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+XGemm gemm_dwt(const Geo &g, int64_t batch) {  // d_W^T (r_dim x q) = [g_hi; g_lo]^T @ [x; x]
+  XGemm x;
+  const int64_t bp = rup(batch, 64);
+  x.M = g.r_dim; x.N = g.q; x.K = 2 * bp;
+  x.a_mn = 1; x.b_mn = 1; x.el = 0;
+  x.b_wrap_k = bp; x.b_rows = batch;
+  x.BN = g.q > 128 ? 256 : 128;
+  x.splits = xgemm_splits(x.M, x.N, x.K, x.BN, 0, num_sms());
+  x.ks_major = 1;
+  x.force_part = (g.q % 4) ? 1 : 0;
+  return x;
+}
+XGemm gemm_gdxf(const Geo &g) {  // d_xf (m x r) = d_aux (m x n) @ wf^T
+  XGemm x;
+  x.M = g.m; x.N = g.rank; x.K = g.n;
+  x.a_mn = 0; x.b_mn = 0; x.el = 1;
+  x.BN = g.rank <= 64 ? 64 : (g.rank <= 128 ? 128 : 256);
+  x.splits = xgemm_splits(x.M, x.N, x.K, x.BN, 1, num_sms());
+  x.force_part = 1;  // any rank: output pitch r
+  return x;
+}
+XGemm gemm_gdwf(const Geo &g) {  // D' (n x r) = d_aux^T @ xf, reduced transposed into d_wf
+  XGemm x;
+  x.M = g.n; x.N = g.rank; x.K = g.m;
+  x.a_mn = 1; x.b_mn = 1; x.el = 1;
+  x.BN = g.rank <= 64 ? 64 : (g.rank <= 128 ? 128 : 256);
+  x.splits = xgemm_splits(x.M, x.N, x.K, x.BN, 1, num_sms());
+  x.reduce_transpose = 1;
+  return x;
+}
+XGemm gemm_gdin(const Geo &g, int64_t batch) {  // d_input (B x q) = g @ W^T, W (q x r_dim)
+  XGemm x;
+  x.M = batch; x.N = g.q; x.K = g.r_dim;
+  x.a_mn = 0; x.b_mn = 0; x.el = 1;
+  x.BN = g.q > 128 ? 256 : (g.q > 64 ? 128 : 64);
+  x.force_part = (g.q % 4) ? 1 : 0;
+  return x;
+}
+
+struct GenWs {
+  size_t pre, gbuf, g2, x16, dwt, w, part, cols, ffma, total;
+  GenWs(const Geo &g, int64_t batch) {
+    const int64_t bp = rup(batch, 64), ldx = rup(g.q, 8);
+    pre = 0;
+    gbuf = pre + rup(batch * g.r_dim * 4, 256);
+    g2 = gbuf + rup(batch * g.r_dim * 4, 256);
+    x16 = g2 + rup(2 * bp * g.r_dim * 2, 256);
+    dwt = x16 + rup(batch * ldx * 2, 256);
+    w = dwt + rup(g.m * g.n * 4, 256);
+    part = w + rup(g.q * g.r_dim * 4, 256);
+    const size_t pb = std::max(std::max(xgemm_ws(gemm_dwt(g, batch)), xgemm_ws(gemm_gdxf(g))),
+                               std::max(xgemm_ws(gemm_gdwf(g)), xgemm_ws(gemm_gdin(g, batch))));
+    cols = part + rup(pb, 256);
+    ffma = cols + rup(colsum_ws(batch, g.r_dim), 256);
+    total = ffma + rup(ffma_forward_ws(g, batch), 256);
+  }
+};
+
+}  // namespace
+
+bool xback_general_ok(const Geo &g) {
+  return !g.reuse && g.r_dim % 8 == 0 && g.n % 4 == 0 && g.rank % 4 == 0 && g.rank <= 256 &&
+         g.m * g.n < ((int64_t)1 << 31) && g.q * g.r_dim < ((int64_t)1 << 31);
+}
+
+size_t xback_general_ws(const Geo &g, int64_t batch) { return GenWs(g, batch).total; }
+
+int xback_general(const Geo &g, int64_t batch, const void *x, int x_dtype, const float *xf,
+                  const float *wf, const float *bias, int act, float act_arg, const float *up,
+                  float *d_xf, float *d_wf, float *d_bias, float *d_input, char *ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  const GenWs L(g, batch);
+  if (ws_bytes < L.total) {
+    set_error("backward workspace too small: need " + std::to_string(L.total));
+    return DT_E_ARG;
+  }
+  if (batch == 0) {
+    DT_CUDA_CHECK(cudaMemsetAsync(d_xf, 0, (size_t)g.m * g.rank * 4, st));
+    DT_CUDA_CHECK(cudaMemsetAsync(d_wf, 0, (size_t)g.rank * g.n * 4, st));
+    if (d_bias) DT_CUDA_CHECK(cudaMemsetAsync(d_bias, 0, (size_t)g.r_dim * 4, st));
+    return DT_OK;
+  }
+  const float *gp = up;
+  if (act != DT_ACT_IDENTITY) {
+    float *pre = reinterpret_cast<float *>(ws + L.pre);
+    float *gbuf = reinterpret_cast<float *>(ws + L.gbuf);
+    if (int rc = ffma_forward(g, batch, x, x_dtype, xf, wf, bias, DT_ACT_IDENTITY, 0.f, pre,
+                              DT_F32, ws + L.ffma, ffma_forward_ws(g, batch), st))
+      return rc;
+    if (int rc = launch_act_grad(batch * g.r_dim, up, pre, act, act_arg, gbuf, st)) return rc;
+    gp = gbuf;
+  }
+  if (d_bias)
+    if (int rc = launch_colsum(batch, g.r_dim, gp, d_bias, reinterpret_cast<float *>(ws + L.cols), st))
+      return rc;
+  // bf16 x with a 16-byte pitch (TMA)
+  const int64_t ldx = rup(g.q, 8);
+  const void *xt = x;
+  if (x_dtype != DT_BF16 || ldx != g.q || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
+    if (int rc = launch_pack_x(batch, g.q, ldx, x, x_dtype, ws + L.x16, st)) return rc;
+    xt = ws + L.x16;
+  }
+  // g -> [g_hi; g_lo] (bf16, K-stacked)
+  const int64_t bp = rup(batch, 64);
+  __nv_bfloat16 *g2 = reinterpret_cast<__nv_bfloat16 *>(ws + L.g2);
+  k_split_g_rows<<<(unsigned)std::min<int64_t>((bp * g.r_dim + 255) / 256, 4 * 1184), 256, 0, st>>>(
+      batch, g.r_dim, bp, gp, g2);
+  if (int rc = check_launch("split_g_rows")) return rc;
+  float *part = reinterpret_cast<float *>(ws + L.part);
+  // d_v = d_W^T flat; zero tail of the aux matrix
+  float *dv = reinterpret_cast<float *>(ws + L.dwt);
+  {
+    XGemm d = gemm_dwt(g, batch);
+    d.A = g2; d.lda = g.r_dim;
+    d.B = xt; d.ldb = ldx;
+    d.out = dv; d.ldo = g.q;
+    d.part = part;
+    if (int rc = xgemm(d, st)) return rc;
+    const int64_t tail = g.m * g.n - g.q * g.r_dim;
+    if (tail > 0) DT_CUDA_CHECK(cudaMemsetAsync(dv + g.q * g.r_dim, 0, (size_t)tail * 4, st));
+  }
+  {
+    XGemm d = gemm_gdxf(g);
+    d.A = dv; d.lda = g.n;
+    d.B = wf; d.ldb = g.n;
+    d.out = d_xf; d.ldo = g.rank;
+    d.part = part;
+    if (int rc = xgemm(d, st)) return rc;
+  }
+  {
+    XGemm d = gemm_gdwf(g);
+    d.A = dv; d.lda = g.n;
+    d.B = xf; d.ldb = g.rank;
+    d.out = d_wf; d.ldo = g.n;
+    d.part = part;
+    if (int rc = xgemm(d, st)) return rc;
+  }
+  if (d_input) {
+    float *w = reinterpret_cast<float *>(ws + L.w);
+    if (int rc = launch_decompress(g, xf, wf, w, st)) return rc;
+    XGemm d = gemm_gdin(g, batch);
+    d.A = gp; d.lda = g.r_dim;
+    d.B = w; d.ldb = g.r_dim;
+    d.out = d_input; d.ldo = g.q;
+    d.part = part;
+    if (int rc = xgemm(d, st)) return rc;
+  }
+  return DT_OK;
+}
+
 }  // namespace dt

@@ -218,3 +218,32 @@ def test_forward_mse_keep_for_backward_is_exact(geo):
     db0, db1 = out[0][1][ob:ob + r_dim], out[1][1][ob:ob + r_dim]
     assert torch.allclose(db0, db1, rtol=1e-5, atol=1e-6 * float(db0.abs().max()))
     assert out[1][2] == pytest.approx(out[0][2], rel=1e-12)
+
+
+@pytest.mark.parametrize("geo", [
+    (440, 2048, 24, 320, 2816, 512),    # config 2 geometry (straddling rows, period 8)
+    (96, 136, 4, 40, 327, 70),          # discarded tail (m*n > q*r_dim), ragged batch
+    (1000, 512, 8, 384, 1334, 200),     # q % 8 == 0, q not a multiple of n
+])
+@pytest.mark.parametrize("act", ["identity", "tanh"])
+def test_tc_backward_general_geometry(geo, act):
+    """the tensor-core backward of straddling geometries (k_train.cu xback_general:
+    d_W^T = g^T x on tcgen05 with g split bf16 hi | lo, the flat inverse re-layout as a view,
+    d_xf / d_wf / d_input as tf32 GEMMs) against the oracle's layer_backward (grad.py:63-95) on
+    the same bf16-rounded inputs: <= 2e-3; bitwise repeatable (fixed-order split-K)."""
+    q, r_dim, rank, n, m, batch = geo
+    op = O.Plan(q=q, r_dim=r_dim, rank=rank, m=m, n=n)
+    assert q % n != 0
+    d = {k: O.round_bf16(v) for k, v in O.baseline_inputs(op, batch, seed=6, bias_sd=0.3).items()}
+    fp = D.FactorPair(d["xf"], d["wf"], D.LayerPlan(q=q, r_dim=r_dim, rank=rank, m=m, n=n))
+    up = O.round_bf16(O.make_rng(3).standard_normal((batch, r_dim)))
+    ref = O.layer_backward(d["x"], d["xf"], d["wf"], op, d["bias"], act, up)
+    x = torch.tensor(d["x"], dtype=torch.float32, device="cuda").to(torch.bfloat16)
+    gr = D.layer_backward(x, fp, d["bias"], act, up, mma="bf16")
+    for mine, want, k in ((gr.d_xf, ref.d_xf, "dxf"), (gr.d_wf, ref.d_wf, "dwf"),
+                          (gr.d_input, ref.d_input, "dx"), (gr.d_bias, ref.d_bias, "db")):
+        assert O.rel_error(mine, want) <= BF16_TOL, (k, O.rel_error(mine, want))
+    gr2 = D.layer_backward(x, fp, d["bias"], act, up, mma="bf16")
+    for a, b in ((gr.d_xf, gr2.d_xf), (gr.d_wf, gr2.d_wf), (gr.d_input, gr2.d_input)):
+        assert np.array_equal(np.asarray(a.cpu() if hasattr(a, "cpu") else a),
+                              np.asarray(b.cpu() if hasattr(b, "cpu") else b))
