@@ -199,6 +199,20 @@ int dt_forward_mse_ex(const dt_plan *plan, int64_t batch, const void *x, int x_d
                       double norm_count, float *grad, double *loss_sum, float *d_bias,
                       float *p_out, void *workspace, size_t workspace_bytes, dt_stream stream);
 
+/* A run of consecutive reuse layers of a network (model_io.py:46-63 CompressedModel, each layer
+ * kernel.py:296-320 layer_forward) fused into ONE persistent kernel: every 128-row tile goes
+ * through all n_layers layers with the hidden activations kept in shared memory (only the run's
+ * input and its last layer's output touch HBM). Eligible: n_layers in [2, 8], every plan a reuse
+ * geometry taking the row-tile kernel (dt_rows_prepared_bytes > 0 with bf16 x and y), all sharing
+ * n, rank and q/n, plans[l].q == plans[l-1].r_dim (dt_chain_ok). x: batch x plans[0].q bf16; y:
+ * batch x plans[n_layers-1].r_dim bf16. prepared[l]: dt_rows_prepare of layer l with hidden_act
+ * (l < n_layers-1) or DT_ACT_IDENTITY (the last layer), y_dtype DT_BF16, and the layer's bias.
+ * last_act: DT_ACT_IDENTITY, or DT_ACT_SOFTMAX (a row softmax over y after the chain). */
+int dt_chain_ok(const dt_plan *plans, int n_layers);
+int dt_chain_forward(const dt_plan *plans, int n_layers, int64_t batch, const void *x,
+                     void *const *prepared, int hidden_act, float act_arg, int last_act, void *y,
+                     dt_stream stream);
+
 /* core.py:63-77 matmul (np.matmul after as_matrix) on the tensor cores, for the transposed views
  * the backward contracts (grad.py:86-94): c (M x N fp32, pitch ldc) = op(a) @ op(b), op(a) M x K,
  * op(b) K x N. a_trans = 0: a stored M x K (pitch lda); 1: a stored K x M. b_trans = 0: b stored

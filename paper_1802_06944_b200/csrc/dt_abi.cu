@@ -454,6 +454,48 @@ int dt_mse_grad(int64_t rows, int64_t cols, const float *y, const float *target,
                          workspace_bytes, (cudaStream_t)stream);
 }
 
+int dt_chain_ok(const dt_plan *plans, int n_layers) {
+  if (!plans || n_layers < 2 || n_layers > 8) return 0;
+  Geo g[8];
+  for (int l = 0; l < n_layers; ++l)
+    if (make_geo(&plans[l], &g[l])) return 0;
+  return tc_chain_ok(g, n_layers) ? 1 : 0;
+}
+
+int dt_chain_forward(const dt_plan *plans, int n_layers, int64_t batch, const void *x,
+                     void *const *prepared, int hidden_act, float act_arg, int last_act, void *y,
+                     dt_stream stream) {
+  if (!plans || n_layers < 2 || n_layers > 8) {
+    set_error("dt_chain_forward: 2 to 8 layers");
+    return DT_E_ARG;
+  }
+  Geo g[8];
+  for (int l = 0; l < n_layers; ++l)
+    if (int rc = make_geo(&plans[l], &g[l])) return rc;
+  if (batch < 0) {
+    set_error("batch must be >= 0");
+    return DT_E_DIM;
+  }
+  if (int rc = check_act(hidden_act)) return rc;
+  if (hidden_act == DT_ACT_SOFTMAX || (last_act != DT_ACT_IDENTITY && last_act != DT_ACT_SOFTMAX)) {
+    set_error("dt_chain_forward: hidden_act must be elementwise, last_act identity or softmax");
+    return DT_E_ARG;
+  }
+  if (batch > 0 && (!x || !y || !prepared)) {
+    set_error("NULL operand pointer");
+    return DT_E_ARG;
+  }
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) {
+    set_error("dt_chain_forward: x and y must be 16-byte aligned");
+    return DT_E_ARG;
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (int rc = tc_chain_forward(g, n_layers, batch, x, prepared, hidden_act, act_arg, y, st)) return rc;
+  if (last_act == DT_ACT_SOFTMAX && batch > 0)
+    return launch_row_softmax(batch, g[n_layers - 1].r_dim, y, DT_BF16, st);
+  return DT_OK;
+}
+
 namespace {
 XGemm matmul_desc(int64_t M, int64_t N, int64_t K, const void *a, int64_t lda, int a_trans,
                   const void *b, int64_t ldb, int b_trans, int dtype) {

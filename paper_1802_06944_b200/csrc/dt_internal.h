@@ -97,6 +97,12 @@ size_t tc_rows_ws(const Geo &g);
 int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
                     const float *bias, int act, float act_arg, void *y, int y_dtype, char *ws,
                     cudaStream_t st, bool prepared = false);
+// Fused layer chain (k_tc_chain.cu): L reuse layers sharing n, s and rank in one persistent
+// kernel; hidden activations stay in shared memory. prepared[l]: tc_rows_prepare output of layer
+// l (hidden layers with hidden_act / bf16 output, the last with identity / bf16 output).
+bool tc_chain_ok(const Geo *g, int L);
+int tc_chain_forward(const Geo *g, int L, int64_t batch, const void *x, void *const *prepared,
+                     int hidden_act, float act_arg, void *y, cudaStream_t st);
 // layer chaining for the next tc_rows_forward on this thread (prepared operands only)
 void rows_chain(const unsigned *wait, unsigned target, unsigned *post);
 int rows_posts_per_tile(const Geo &g);

@@ -94,6 +94,13 @@ class DeviceModel:
         # then polls flags instead of a single grid dependency): off by default
         self.chain = False
         self._chain_key = None
+        # fused layer chains (dt_chain_forward, k_tc_chain.cu): runs of reuse layers as ONE
+        # kernel with the hidden activations kept in shared memory. Exact (bit-identical to the
+        # layer-by-layer kernels) but measured slower at config 3 (314 vs ~213 us for layers
+        # 1-6): a tile's six layers are a serial ~10 us-per-layer chain (phase A, cluster P
+        # exchange, phase B + epilogue) that one tile in flight per cluster cannot hide, while
+        # the per-layer kernel pipelines tiles. Opt-in.
+        self.fuse = False
 
     @property
     def plans(self):
@@ -130,8 +137,21 @@ class DeviceModel:
         bufs = flags = None
         if any(rows[i] and rows[i - 1] for i in range(1, last + 1)):
             bufs, flags = self._chain_state(batch, mid)
+        runs = self._fused_runs(out_dtype) if (code == _lib.DT_MMA_BF16 and self.fuse and
+                                               bufs is None) else {}
         with forward_pipeline(self.pipeline and self.mma == "bf16"):
+            skip_to = 0
             for i, (fp, bias) in enumerate(zip(self.factors, self.biases)):
+                if i < skip_to:
+                    continue
+                if i in runs and xt.dtype == torch.bfloat16 and xt.is_contiguous():
+                    j = runs[i]
+                    y = torch.empty((batch, self.factors[j].plan.r_dim), device=xt.device,
+                                    dtype=torch.bfloat16)
+                    self._run_chain(i, j, xt, y)
+                    xt = y
+                    skip_to = j + 1
+                    continue
                 need = lib.dt_forward_workspace_bytes(C.byref(_lib.plan_struct(fp.plan)), batch,
                                                       code)
                 if self._ws[i] is None or self._ws[i].numel() < need:
@@ -154,6 +174,62 @@ class DeviceModel:
         if bufs is not None:
             self._epoch += 1
         return xt.float().cpu().numpy() if host else xt
+
+    def _fused_runs(self, out_dtype):
+        """{first: last} of the layer runs dt_chain_forward takes: >= 2 consecutive reuse layers
+        on the row-tile kernel sharing n, rank and q/n, one elementwise activation on all but the
+        last, the last identity or softmax (bf16 output, so the network's final layer only when
+        out_dtype is bf16)."""
+        key = ("runs", out_dtype)
+        cache = self.__dict__.setdefault("_run_cache", {})
+        if key in cache:
+            return cache[key]
+        lib = _lib.lib()
+        last = len(self.factors) - 1
+        sm, ident = _act_code("softmax"), _act_code("identity")
+
+        def rows_ok(i):
+            return lib.dt_rows_prepared_bytes(C.byref(_lib.plan_struct(self.factors[i].plan)),
+                                              _lib.DT_BF16, _lib.DT_BF16) > 0
+
+        runs, i = {}, 0
+        while i <= last:
+            best = None
+            j = i + 1
+            while j <= last and j - i < 8:
+                hid = self.codes[i:j]
+                if not (all(c == hid[0] for c in hid) and hid[0] not in (sm,)):
+                    break
+                ends_ok = self.codes[j] in (ident, sm) and (j < last or out_dtype == torch.bfloat16)
+                plans = (_lib.Plan * (j - i + 1))(*[_lib.plan_struct(f.plan)
+                                                   for f in self.factors[i:j + 1]])
+                if ends_ok and all(rows_ok(k) for k in range(i, j + 1)) and \
+                        lib.dt_chain_ok(plans, j - i + 1):
+                    best = j
+                j += 1
+            if best is not None:
+                runs[i] = best
+                i = best + 1
+            else:
+                i += 1
+        cache[key] = runs
+        return runs
+
+    def _run_chain(self, i, j, x, y):
+        lib = _lib.lib()
+        L = j - i + 1
+        hidden = self.codes[i]
+        ident = _act_code("identity")
+        bufs = []
+        for k in range(i, j + 1):
+            act = hidden if k < j else ident
+            buf = self.factors[k].rows_prepared(self.biases[k], act, _lib.DT_BF16)
+            bufs.append(buf)
+        plans = (_lib.Plan * L)(*[_lib.plan_struct(f.plan) for f in self.factors[i:j + 1]])
+        ptrs = (C.c_void_p * L)(*[b.data_ptr() for b in bufs])
+        _lib.check(lib.dt_chain_forward(plans, L, x.shape[0], x.data_ptr(), ptrs, hidden,
+                                        self.act_args[i], self.codes[j], y.data_ptr(),
+                                        stream_handle()))
 
     def _graph_forward(self, x, out_dtype):
         key = (x.data_ptr(), tuple(x.shape), x.dtype, out_dtype)

@@ -39,7 +39,7 @@ def c5_step(rows=65536):
     return lambda: D.train_step(layer, x, t, 1e-4, loss_out=loss)
 
 
-def c3_step(rows=16384):
+def c3_step(rows=16384, graph=True):
     import numpy as np
     import bench
     from paper_1802_06944_b200 import model_io as mi
@@ -55,7 +55,7 @@ def c3_step(rows=16384):
                                factors=factors, biases=biases)
     dm = model.to_device(bench.C3_ACTS, mma="bf16")
     x = torch.randn(rows, 440, device="cuda").to(torch.bfloat16)
-    return lambda: dm.forward(x, out_dtype=torch.bfloat16, graph=True)
+    return lambda: dm.forward(x, out_dtype=torch.bfloat16, graph=graph)
 
 
 def main():

@@ -282,3 +282,28 @@ def test_gpu_factor_pair_float64_round_trips_through_dthn():
     moved = mi.deserialize(img_b).factors[0]
     assert moved.xf.dtype == np.float64
     assert np.array_equal(moved.xf, layer.fp.xf.cpu().numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("rows", [1000, 4096, 128])
+def test_fused_layer_chain_matches_layer_by_layer(rows):
+    """dt_chain_forward (k_tc_chain.cu): the config-3 hidden layers + output layer as ONE kernel
+    with the activations kept in shared memory give the bits of the layer-by-layer row-tile
+    kernels (same per-layer arithmetic and summation order), with bf16 output (the chain runs
+    through the softmax head) and fp32 output (the last layer runs on its own)."""
+    model = mi.deserialize(mi.serialize(config3_like(layers=5)))
+    acts = ["sigmoid"] * 5 + ["softmax"]
+    dm = model.to_device(acts, mma="bf16")
+    x = torch.randn(rows, 440, device="cuda").to(torch.bfloat16)
+    assert dm._fused_runs(torch.bfloat16) == {1: 5}
+    assert dm._fused_runs(torch.float32) == {}  # layers 1-4: the run would end on a sigmoid
+    for out in (torch.bfloat16, torch.float32):
+        dm.fuse = False
+        want = dm.forward(x, out_dtype=out).clone()
+        dm.fuse = True
+        got = dm.forward(x, out_dtype=out)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (out, (got.float() - want.float()).abs().max().item())
+    got = dm.forward(x, out_dtype=torch.bfloat16, graph=True)
+    torch.cuda.synchronize()
+    dm.fuse = False
+    assert torch.equal(got, dm.forward(x, out_dtype=torch.bfloat16))
