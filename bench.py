@@ -528,7 +528,8 @@ def run_ours(args, cfg, key):
     # Roofline of the dominant kernel: its device durations from CUPTI activity records over K
     # more steps of the same loop (no events inside the step; the pipelined overlap is kept)
     bf16_peak, hbm_peak, peak_kind = peaks()
-    pat = ["k_tc_gemm_pair", "k_tc_gemm<"] if mma == "bf16" else ["k_reuse_small", "k_simt", "k_gemm"]
+    pat = ["k_tc_xgemm", "k_tc_gemm_pair", "k_tc_gemm<"] if mma == "bf16" else \
+        ["k_reuse_small", "k_simt", "k_gemm"]
 
     def prof_run():
         for _ in range(args.steps):
@@ -537,15 +538,18 @@ def run_ours(args, cfg, key):
     kernel_ms = (statistics.mean(kd) if kd else float("nan")) / 1e3
     share = sum(kd) / 1e3 / args.steps / ms_per_step if kd else None
     if mma == "bf16":
-        # phase-2 GEMM per launch: reads x (bf16) and W^T (bf16, L2-resident from phase 1) once,
-        # writes y (fp32); HBM-bound at this shape (bytes/peak_bw > flops/peak_flops)
-        bytes_alg = batch * q * 2 + r_dim * q * 2 + batch * r_dim * 4 + r_dim * 4
+        # phase-2 GEMM per launch: reads x (bf16) and W^T as bf16 hi + lo (L2-resident from
+        # phase 1) once, writes y (fp32); HBM-bound at this shape (bytes/peak_bw >
+        # flops/peak_flops). flops: the contraction the layer needs (2 B q r_dim); the hi + lo
+        # split issues twice that on the tensor cores
+        bytes_alg = batch * q * 2 + 2 * r_dim * q * 2 + batch * r_dim * 4 + r_dim * 4
         flops = 2.0 * batch * q * r_dim
         achieved = bytes_alg / (kernel_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": traffic_for(key),
                 "peak_source": f"{peak_kind} hbm_gbs",
-                "kernel": "k_tc_gemm_pair (phase 2)", "kernel_us": round(kernel_ms * 1e3, 3),
+                "kernel": "k_tc_xgemm (phase 2: x . [W_hi | W_lo]^T, tcgen05 pairs)",
+                "kernel_us": round(kernel_ms * 1e3, 3),
                 "kernel_launches": len(kd), "kernel_us_raw": round(statistics.mean(kraw), 3),
                 "timing": "CUPTI activity records (torch.profiler), exclusive of the PDL overlap "
                           "with the previous kernel",

@@ -146,6 +146,11 @@ struct XGemm {
   int h_r = 0, h_s = 0;
   int pair_half = 0;              // epi 2
   int ks_major = 0;               // units ordered with the K split slowest (operand reuse in L2)
+  // epi 4 (transposed store): out_t[n][m] = act(D[m][n] + bias[m]), y_dtype DT_F32 / DT_BF16
+  void *out_t = nullptr;
+  int y_dtype = DT_F32, act = DT_ACT_IDENTITY;
+  float act_arg = 0.f;
+  int chain = 0;                  // pipelined forward (PDL trigger after the prologue)
 };
 size_t xgemm_ws(const XGemm &g);
 int xgemm_splits(int64_t M, int64_t N, int64_t K, int BN, int el, int nsm);

@@ -72,6 +72,10 @@ struct RegenArgs {
   int x_ext;  // pipelined forward with external inputs: x is never written by an in-flight grid
   const void *xf, *wf;
   __nv_bfloat16 *wt;
+  // hilo: W^T as a bf16 hi + lo pair, row j = [hi(W^T[j, :]) | pad | lo(W^T[j, :]) | pad] with
+  // halves of qp columns (qp = round_up(q, 64)), so one GEMM over K = 2 qp against x (read
+  // twice through a wrapping tensor map) accumulates x W_hi + x W_lo: ~16 significant bits of W
+  int hilo, qp;
 };
 struct RegenSmem {
   float xt[RG_K][RG_RMAX + 4];  // +4: the transposing stores are 4-way, not 32-way, conflicted
@@ -111,7 +115,7 @@ struct GemmParams {
   // factors (p.rg.xf / p.rg.wf), staged at off_fs (x stages not in flight yet)
   int wgen;
   uint32_t off_fs;
-  RegenArgs rg;
+  RegenArgs rg{};
   int chain;  // pipelined forward: let the next call's phase 1 launch right away
   // x may be loaded before griddepcontrol.wait: not chained (the grids ahead of phase 1 have
   // completed), or chained with inputs the caller declared external (DT_PIPELINE_EXTERNAL_X).
@@ -345,6 +349,42 @@ __device__ __forceinline__ void regen_tile_tc(const RegenArgs &g, int tid, int b
     }
   }
   const int64_t q = g.q, total = q * g.r_dim;
+  if (g.hilo) {
+    // [hi | lo] rows: each accumulator pair (an even flat index f, so both in row f / q when q
+    // is even) -> one bf16x2 hi store and one bf16x2 lo store
+    const int64_t ld2 = 2 * (int64_t)g.qp;
+    const bool pairs = (q & 1) == 0 && (n & 1) == 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int c = c0 + (nt0 + t) * 8 + 2 * tq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = a0 + mt * 16 + gr + 8 * h;
+        if (a >= a_rows || c >= n) continue;
+        const float v0 = d[t][2 * h], v1 = d[t][2 * h + 1];
+        const int64_t f = (int64_t)a * n + c;
+        if (pairs && c + 1 < n && f + 2 <= total) {
+          const int64_t j = f / q, i = f - j * q;
+          const __nv_bfloat162 hv = __floats2bfloat162_rn(v0, v1);
+          const __nv_bfloat162 lv = __floats2bfloat162_rn(v0 - __low2float(hv), v1 - __high2float(hv));
+          *reinterpret_cast<__nv_bfloat162 *>(g.wt + j * ld2 + i) = hv;
+          *reinterpret_cast<__nv_bfloat162 *>(g.wt + j * ld2 + g.qp + i) = lv;
+        } else {
+          for (int e = 0; e < 2; ++e) {
+            const int64_t fe = f + e;
+            if (c + e < n && fe < total) {
+              const int64_t j = fe / q, i = fe - j * q;
+              const float v = e ? v1 : v0;
+              const __nv_bfloat16 hb = __float2bfloat16_rn(v);
+              g.wt[j * ld2 + i] = hb;
+              g.wt[j * ld2 + g.qp + i] = __float2bfloat16_rn(v - __bfloat162float(hb));
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
   const bool flat = g.ldw == q && (n & 1) == 0;  // W^T == I.ravel(): bf16x2 stores
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
@@ -373,6 +413,18 @@ __device__ __forceinline__ void regen_tile_tc(const RegenArgs &g, int tid, int b
 __global__ void __launch_bounds__(256) k_regen_wt(const RegenArgs g) {
   griddep_launch_dependents();  // the GEMM may start its prologue now
   __shared__ __align__(16) RegenSmemTC sm;
+  if (g.hilo && g.qp > g.q && blockIdx.y == 0) {
+    // zero the pad columns [q, qp) of both halves (the GEMM multiplies them by x's zero fill;
+    // workspace garbage could be NaN), rows strided over the first column of CTAs
+    const int64_t ld2 = 2 * (int64_t)g.qp;
+    const int pad = g.qp - (int)g.q;
+    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < g.r_dim * 2 * pad;
+         e += (int64_t)gridDim.x * 256) {
+      const int64_t j = e / (2 * pad);
+      const int k = (int)(e - j * 2 * pad);
+      g.wt[j * ld2 + (k < pad ? 0 : g.qp) + g.q + (k % pad)] = __float2bfloat16_rn(0.f);
+    }
+  }
   if (g.f_dtype == DT_F32)
     regen_tile_tc<float>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm);
   else
@@ -1480,10 +1532,15 @@ static int pipeline_slot(const void *ws) {
   return (int)(next[ws]++ & 1u);
 }
 
+// W^T slot of the two-phase forward: the hi | lo rows (2 x round_up(q, 64) bf16 per row)
+static int64_t wt_slot_bytes(const Geo &g) {
+  return round_up(g.r_dim * 2 * round_up(g.q, 64) * 2, 256);
+}
+
 size_t tc_gemm_ws(const Geo &g, int64_t batch) {
   const int64_t ldw = round_up(g.q, 8);
   const size_t two_phase =  // two W^T slots (pipelined forwards alternate) + packed x
-      2 * (size_t)round_up(g.r_dim * ldw * 2, 256) + (size_t)round_up(batch * ldw * 2, 256);
+      2 * (size_t)wt_slot_bytes(g) + (size_t)round_up(batch * ldw * 2, 256);
   return std::max(std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0),
                   tc_rows_ws(g));
 }
@@ -1630,7 +1687,69 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
   // ---- two-phase: W^T regenerated into the workspace, then the GEMM ----
   const int64_t ldw = round_up(g.q, 8);
   const bool pipe = forward_pipeline();
-  const int64_t slot_bytes = round_up(g.r_dim * ldw * 2, 256);
+  const int64_t slot_bytes = wt_slot_bytes(g);
+  if (!mse && y_dtype == DT_F32 && g.q * 2 * round_up(g.q, 64) < INT32_MAX) {
+    // fp32 outputs: W^T as bf16 hi + lo. Phase 1 writes rows [hi | lo] (K = 2 qp), phase 2 is
+    // the any-major tcgen05 GEMM (k_tc_xgemm.cu) with x read twice through a wrapping tensor
+    // map, epilogue transposed into y's row-major layout with bias + activation. W keeps ~16
+    // significant bits: rel_error ~3e-6 instead of the 1.7-1.9e-3 of a single bf16 rounding
+    // (SURVEY §0.6), at twice the tensor work (config 2: 33 vs 20 us per step).
+    // bf16 outputs keep the single rounding (the W-resident pair kernel below): the output's
+    // own bf16 rounding (2^-9 relative per element) is of the same size as W's.
+    const int64_t qp = round_up(g.q, 64);
+    __nv_bfloat16 *w2 =
+        reinterpret_cast<__nv_bfloat16 *>(ws + (pipe ? pipeline_slot(ws) : 0) * slot_bytes);
+    char *xws = ws + 2 * slot_bytes;
+    const void *xt = x;
+    int64_t ldx = g.q;
+    if (x_dtype != DT_BF16 || (g.q % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) {
+      ldx = ldw;
+      if (int rc = launch_pack_x(batch, g.q, ldx, x, x_dtype, xws, st)) return rc;
+      xt = xws;
+    }
+    RegenArgs rg{};
+    rg.q = g.q; rg.r_dim = g.r_dim; rg.ldw = 2 * qp;
+    rg.rank = (int)g.rank; rg.n = (int)g.n;
+    rg.a_rows = (int)((g.q * g.r_dim + g.n - 1) / g.n);
+    rg.f_dtype = f_dtype;
+    rg.xf = xf; rg.wf = wf; rg.wt = w2;
+    rg.chain = pipe ? 1 : 0;
+    rg.hilo = 1;
+    rg.qp = (int)qp;
+    const dim3 rgrid((unsigned)((rg.a_rows + RG_R - 1) / RG_R), (unsigned)((rg.n + RG_C - 1) / RG_C));
+    if (pipe) {  // phase 1 overlaps the previous forward's GEMM
+      cudaLaunchConfig_t rcfg{};
+      rcfg.gridDim = rgrid;
+      rcfg.blockDim = dim3(256);
+      rcfg.stream = st;
+      cudaLaunchAttribute ra[1];
+      ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      ra[0].val.programmaticStreamSerializationAllowed = 1;
+      rcfg.attrs = ra;
+      rcfg.numAttrs = 1;
+      DT_CUDA_CHECK(cudaLaunchKernelEx(&rcfg, k_regen_wt, rg));
+    } else {
+      k_regen_wt<<<rgrid, 256, 0, st>>>(rg);
+    }
+    if (int rc = check_launch("regen_wt")) return rc;
+    XGemm xg;
+    xg.M = g.r_dim; xg.N = batch; xg.K = 2 * qp;
+    xg.A = w2; xg.lda = 2 * qp; xg.a_mn = 0;
+    xg.B = xt; xg.ldb = ldx; xg.b_mn = 0;
+    xg.b_wrap_k = qp; xg.b_rows = g.q;
+    xg.el = 0;
+    xg.BN = 256;
+    xg.epi = 4;  // transposed store: y[b][j] = act(D[j][b] + bias[j])
+    xg.out_t = y; xg.ldo = g.r_dim;
+    xg.y_dtype = y_dtype;
+    xg.act = act == DT_ACT_SOFTMAX ? DT_ACT_IDENTITY : act;
+    xg.act_arg = act_arg;
+    xg.bias = bias;
+    xg.chain = pipe ? 1 : 0;
+    if (int rc = xgemm(xg, st)) return rc;
+    if (act == DT_ACT_SOFTMAX) return launch_row_softmax(batch, g.r_dim, y, y_dtype, st);
+    return DT_OK;
+  }
   __nv_bfloat16 *wt =
       reinterpret_cast<__nv_bfloat16 *>(ws + (pipe ? pipeline_slot(ws) : 0) * slot_bytes);
   char *xws = ws + 2 * slot_bytes;
@@ -1642,7 +1761,7 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     if (int rc = launch_pack_x(batch, g.q, ldx, x, x_dtype, xws, st)) return rc;
     xt = xws;
   }
-  RegenArgs rg;
+  RegenArgs rg{};
   rg.q = g.q; rg.r_dim = g.r_dim; rg.ldw = ldw;
   rg.rank = (int)g.rank; rg.n = (int)g.n;
   rg.a_rows = (int)((g.q * g.r_dim + g.n - 1) / g.n);

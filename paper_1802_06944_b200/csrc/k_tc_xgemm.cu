@@ -36,7 +36,9 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <type_traits>
 
+#include "act.cuh"
 #include "dt_internal.h"
 #include "sm100_ptx.cuh"
 
@@ -51,7 +53,7 @@ constexpr uint32_t XA_BYTES = 128 * 128;      // A half-tile stage: 128 rows x 1
 constexpr uint32_t XSTG = 32 * 128;           // one 32 x 32 fp32 staging box (4 KB)
 constexpr int XSMEM_MAX = 227 * 1024;
 
-enum { XE_STORE = 0, XE_MSE = 1, XE_PAIRSUM = 2, XE_SPLITH = 3 };
+enum { XE_STORE = 0, XE_MSE = 1, XE_PAIRSUM = 2, XE_SPLITH = 3, XE_STORE_T = 4 };
 
 struct XgParams {
   int M, N, BN, nhalf;        // nhalf = BN / 2 columns staged per CTA
@@ -72,6 +74,10 @@ struct XgParams {
   int h_r, h_s;
   int pair_half;              // XE_PAIRSUM: out[:, k] = D[:, k] + D[:, k + pair_half]
   int ks_major;               // unit order: K split slowest (tiles of one split run together)
+  int chain;                  // pipelined forward: let the next call's W regeneration start early
+  float act_arg;              // XE_STORE_T activation argument
+  void *out_t;                // XE_STORE_T: out[n][m] (pitch ldo), fp32 or bf16
+  int N_true;                 // XE_STORE_T: rows of out (D columns) actually stored
 };
 
 // K-major: rows of 128 B (the k-block), 8-row swizzle atoms 1024 B apart (SWIZZLE_128B).
@@ -111,7 +117,7 @@ __device__ __forceinline__ void arrive_leader_x(uint64_t *bar, uint32_t crank) {
     mbar_arrive_remote(bar, 0);
 }
 
-template <int EL, int EPI>
+template <int EL, int EPI, int YDT = DT_F32, int ACT = DT_ACT_IDENTITY>
 __global__ void __launch_bounds__(XTHREADS, 1)
     k_tc_xgemm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_t,
@@ -148,6 +154,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tslot;
   griddep_wait();  // operands may come from the previous kernel on the stream
+  if (p.chain) griddep_launch_dependents();  // the next forward's W regeneration may start
 
   auto unit_of = [&](int u, int &mb, int &nb, int &ks) {
     int t;
@@ -273,7 +280,32 @@ __global__ void __launch_bounds__(XTHREADS, 1)
         } else {
           tmem_ld_wait();
         }
-        if constexpr (EPI == XE_SPLITH) {
+        if constexpr (EPI == XE_STORE_T) {
+          // out[n][m] = act(D[m][n] + bias[m]): lane = output column m, the chunk's 32 D
+          // columns = 32 output rows; each store instruction writes 32 consecutive columns of
+          // one output row (coalesced)
+          using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
+          if (row < p.M) {
+            const float bm = p.bias ? __ldg(p.bias + row) : 0.f;
+            OutT *yp = reinterpret_cast<OutT *>(p.out_t) + (int64_t)col0 * p.ldo + row;
+            const int nrow = min(32, p.N_true - col0);
+            if (nrow >= 32) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[i]) + bm, p.act_arg);
+                if constexpr (YDT == DT_BF16) yp[(int64_t)i * p.ldo] = __float2bfloat16_rn(o);
+                else yp[(int64_t)i * p.ldo] = o;
+              }
+            } else {
+              for (int i = 0; i < nrow; ++i) {
+                const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[i]) + bm, p.act_arg);
+                if constexpr (YDT == DT_BF16) yp[(int64_t)i * p.ldo] = __float2bfloat16_rn(o);
+                else yp[(int64_t)i * p.ldo] = o;
+              }
+            }
+          }
+          continue;
+        } else if constexpr (EPI == XE_SPLITH) {
           // H[row, col0 .. col0+31] -> H2 row (row * s + col0 / r), [hi | lo]
           if (row < p.M && (p.h_r & 31)) {  // a chunk may cross a segment: element stores
 #pragma unroll 4
@@ -420,6 +452,17 @@ __global__ void __launch_bounds__(XTHREADS, 1)
 }
 
 typedef void (*XgFn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, XgParams);
+
+template <int YDT>
+XgFn pick_t(int act) {  // XE_STORE_T (bf16 operands: the general-path forward)
+  switch (act) {
+    case DT_ACT_RELU: return k_tc_xgemm<0, XE_STORE_T, YDT, DT_ACT_RELU>;
+    case DT_ACT_SIGMOID: return k_tc_xgemm<0, XE_STORE_T, YDT, DT_ACT_SIGMOID>;
+    case DT_ACT_TANH: return k_tc_xgemm<0, XE_STORE_T, YDT, DT_ACT_TANH>;
+    case DT_ACT_CLIPPED_RELU: return k_tc_xgemm<0, XE_STORE_T, YDT, DT_ACT_CLIPPED_RELU>;
+    default: return k_tc_xgemm<0, XE_STORE_T, YDT, DT_ACT_IDENTITY>;
+  }
+}
 
 template <int EL>
 XgFn pick_x(int epi) {
@@ -589,7 +632,7 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   p.pair_half = g.pair_half;
   p.ks_major = g.ks_major;
   p.stage_bytes = XA_BYTES + (uint32_t)nhalf * 128u;
-  const uint32_t stg_bytes = (g.epi == XE_SPLITH) ? 0u
+  const uint32_t stg_bytes = (g.epi == XE_SPLITH || g.epi == XE_STORE_T) ? 0u
                              : (uint32_t)XEPI * (g.epi == XE_MSE ? 3u : 2u) * XSTG;
   // barriers + TMEM slot (512 B), then the XE_MSE column-sum exchange [2][4][256] floats
   const uint32_t tail = 512 + (g.epi == XE_MSE ? 8192u : 0u);
@@ -642,7 +685,11 @@ int xgemm(const XGemm &g, cudaStream_t st) {
     ldo = g.N;
     p.ldo = (int)g.N;
   }
-  if (g.epi != XE_SPLITH) {
+  p.chain = g.chain;
+  p.act_arg = g.act_arg;
+  p.out_t = g.out_t;
+  p.N_true = (int)g.N;
+  if (g.epi != XE_SPLITH && g.epi != XE_STORE_T) {
     if (int rc = encode_tensor_map_2d(&tm_o, DT_F32, out, (uint64_t)out_cols, (uint64_t)out_rows,
                                       (uint64_t)ldo * 4, 32, 32, true))
       return rc;
@@ -659,7 +706,16 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   if (g.epi == XE_MSE && g.loss_part)
     DT_CUDA_CHECK(cudaMemsetAsync(g.loss_part, 0, (size_t)p.units * 2 * XEPI * 8, st));
 
-  XgFn fn = el ? pick_x<1>(g.epi) : pick_x<0>(g.epi);
+  XgFn fn;
+  if (g.epi == XE_STORE_T) {
+    if (el) {
+      set_error("xgemm: the transposed-store epilogue takes bf16 operands");
+      return DT_E_ARG;
+    }
+    fn = g.y_dtype == DT_BF16 ? pick_t<DT_BF16>(g.act) : pick_t<DT_F32>(g.act);
+  } else {
+    fn = el ? pick_x<1>(g.epi) : pick_x<0>(g.epi);
+  }
   if (int rc = set_smem_limit(reinterpret_cast<const void *>(fn), (int)smem_bytes)) return rc;
   const int ncl = std::max(1, std::min(p.units, nsm / 2));
   cudaLaunchConfig_t cfg{};

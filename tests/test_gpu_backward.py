@@ -158,10 +158,9 @@ def test_forward_mse_fused_matches_separate(geo):
     z = g.double() * (norm / 2.0) + t.double()
     want = O.layer_forward(d["x"], d["xf"], d["wf"], op, d["bias"])
     assert O.rel_error(z.cpu().numpy(), want) <= 2e-3
-    if not p.reuse_path:
-        y = layer.forward(x)
-        want_g = (2.0 / norm) * (y.double() - t.double())
-        assert torch.allclose(g.double(), want_g, rtol=0, atol=1e-6 * float(want_g.abs().max()))
+    if not p.reuse_path:  # the general MSE forward rounds W once to bf16 (pair kernel)
+        from test_gpu_forward import bf16_emulated
+        assert O.rel_error(z.cpu().numpy(), bf16_emulated(d, op, d["bias"])) <= 1e-3
     own = float(((g.double() * norm / 2.0) ** 2).sum())
     assert float(loss.item()) == pytest.approx(own, rel=1e-5)  # fp32 chunk sums
 

@@ -97,8 +97,12 @@ def test_config3_all_layers_stage_by_stage(c3):
         out = D.layer_forward(h, fp, b, act, mma="bf16",
                               out_dtype=torch.float32 if last else torch.bfloat16)
         a_ref = O.apply_activation(act, host(z))
-        tol = 1e-6 + (0 if last else ULP16)   # sigmoid in (0, 1): one bf16 ulp <= 2^-8
-        assert np.max(np.abs(host(out) - a_ref)) <= tol, (i, act)
+        # the stored (bf16) activation comes from the bf16-output launch, whose logits meet the
+        # same 2e-3 contract on their own (W rounded once to bf16 on the general path): sigmoid
+        # is 1/4-Lipschitz, plus one bf16 ulp of the stored value (<= 2^-8 in (0, 1))
+        tol = 1e-6 if last else ULP16 + 0.25 * BF16_TOL * float(np.max(np.abs(want)))
+        diff = float(np.max(np.abs(host(out) - a_ref)))
+        assert diff <= tol, (i, act, diff, tol)
         h = out
     # the chain: same kernels, prepared operands, one graph
     y = dm.forward(torch.tensor(x, dtype=torch.float32, device="cuda").to(torch.bfloat16),

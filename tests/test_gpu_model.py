@@ -42,13 +42,15 @@ def oplan(p):
 
 def oracle_chain(model, x, acts, *, factor_round, inter_round=None, contract=None):
     h = x
+    last = len(model.factors) - 1
     for i, ((_, p), fp, b) in enumerate(zip(model.plans.layers, model.factors, model.biases)):
         d = {"x": h, "xf": factor_round(fp.xf), "wf": factor_round(fp.wf)}
         bias = np.asarray(b, dtype=np.float32).astype(np.float64)
         if contract is None:
             h = O.layer_forward(h, d["xf"], d["wf"], oplan(p), bias, acts[i])
-        else:
-            h = O.apply_activation(acts[i], contract(d, oplan(p), bias))
+        else:  # intermediates are stored bf16 on the device, the last layer's output fp32
+            ydt = torch.float32 if i == last or inter_round is None else torch.bfloat16
+            h = O.apply_activation(acts[i], contract(d, oplan(p), bias, ydt))
         if inter_round is not None and i + 1 < len(model.factors):
             h = inter_round(h)
     return h
@@ -89,7 +91,8 @@ def test_bf16_network_matches_contract_chain(dthn):
     y = dm.forward(torch.tensor(x, dtype=torch.bfloat16, device="cuda"))
     assert y.dtype == torch.float32 and tuple(y.shape) == (300, 9)
     # every golden layer takes the two-phase path: W regenerated from the fp32 masters, then
-    # rounded to bf16 (the contract bf16_emulated states); the factors themselves stay fp32
+    # rounded once to bf16 for the bf16 intermediates (bf16_contract, y_dtype bf16); the
+    # factors themselves stay fp32
     want = oracle_chain(model, x, ACTS, factor_round=f32, inter_round=O.round_bf16,
                         contract=bf16_contract)
     assert O.rel_error(y.double().cpu().numpy(), want) <= 4e-3
