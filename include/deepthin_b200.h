@@ -225,6 +225,13 @@ int dt_matmul(int64_t M, int64_t N, int64_t K, const void *a, int64_t lda, int a
               const void *b, int64_t ldb, int b_trans, int dtype, float *c, int64_t ldc,
               void *workspace, size_t workspace_bytes, dt_stream stream);
 
+/* Data-parallel overlap hook (this thread): the next dt_backward / dt_backward_ex records
+ * `event` (a cudaEvent_t) on its stream as soon as d_xf and d_bias are final — on the
+ * tensor-core path right after d_xf's GEMM, before H and d_wf — so a caller can start their
+ * all-reduce on another stream while the backward still runs; at the latest when the call's
+ * work is enqueued. One-shot. No reference counterpart (the reference is single-process). */
+int dt_set_backward_event(void *event);
+
 /* train.py:107-111 DeepThinWeights.step: param -= lr * grad (fp32 masters). */
 int dt_sgd_step(int64_t count, float *param, const float *grad, float lr, dt_stream stream);
 /* Row-tile reuse kernel operands derived once per factor pair (the analogue of the reference's

@@ -27,7 +27,7 @@ EXPORTS = (
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
     "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
-    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_forward_mse_ex", "dt_forward_p_bytes", "dt_backward_ex", "dt_sgd_step", "dt_matmul_workspace_bytes", "dt_matmul", "dt_chain_ok", "dt_chain_forward", "dt_rows_prepared_bytes", "dt_rows_prepare", "dt_rows_chain", "dt_rows_posts_per_tile", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_sequence_workspace_bytes", "dt_lstm_sequence", "dt_lstm_cell", "dt_session_create",
+    "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_forward_mse_ex", "dt_forward_p_bytes", "dt_backward_ex", "dt_sgd_step", "dt_matmul_workspace_bytes", "dt_matmul", "dt_chain_ok", "dt_chain_forward", "dt_set_backward_event", "dt_rows_prepared_bytes", "dt_rows_prepare", "dt_rows_chain", "dt_rows_posts_per_tile", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_sequence_workspace_bytes", "dt_lstm_sequence", "dt_lstm_cell", "dt_session_create",
     "dt_session_forward", "dt_session_destroy", "dt_model_parse", "dt_unpack_values",
 )
 
@@ -111,6 +111,7 @@ def _declare(lib):
         "dt_sgd_step": ([I64, VP, VP, F, VP], i),
         "dt_matmul_workspace_bytes": ([I64, I64, I64, i], SZ),
         "dt_chain_ok": ([P, i], i),
+        "dt_set_backward_event": ([VP], i),
         "dt_chain_forward": ([P, i, I64, VP, C.POINTER(VP), i, F, i, VP, VP], i),
         "dt_matmul": ([I64, I64, I64, VP, I64, i, VP, I64, i, i, VP, I64, VP, SZ, VP], i),
         "dt_rows_prepared_bytes": ([P, i, i], SZ),

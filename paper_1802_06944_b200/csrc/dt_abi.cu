@@ -95,6 +95,18 @@ void dt::profile_next(cudaEvent_t *before, cudaEvent_t *after, int kind) {
 }
 
 bool dt::forward_pipeline() { return g_pipeline != 0; }
+
+namespace {
+thread_local cudaEvent_t g_bwd_event = nullptr;
+}  // namespace
+// The backward records the pending event as soon as d_xf (and d_bias) are final, once.
+int dt::backward_event_record(cudaStream_t st) {
+  if (!g_bwd_event) return DT_OK;
+  cudaEvent_t e = g_bwd_event;
+  g_bwd_event = nullptr;
+  DT_CUDA_CHECK(cudaEventRecord(e, st));
+  return DT_OK;
+}
 bool dt::forward_pipeline_external_x() { return g_pipeline == DT_PIPELINE_EXTERNAL_X; }
 
 extern "C" {
@@ -104,6 +116,11 @@ const char *dt_version(void) { return "deepthin_b200 0.1.0 (sm_100a)"; }
 const char *dt_last_error(void) { return g_last_error.c_str(); }
 
 int64_t dt_launch_counter(void) { return launch_count(); }
+
+int dt_set_backward_event(void *event) {
+  g_bwd_event = reinterpret_cast<cudaEvent_t>(event);
+  return DT_OK;
+}
 
 int dt_set_forward_pipeline(int enable) {
   if (enable < 0 || enable > DT_PIPELINE_EXTERNAL_X) {
@@ -376,21 +393,23 @@ int dt_backward_ex(const dt_plan *plan, int64_t batch, int mma, const void *x, i
     return DT_E_ARG;
   }
   // bf16 / tf32 tensor cores for reuse geometries (factored); every other case runs the exact
-  // fp32 FFMA backward
+  // fp32 FFMA backward. A pending dt_set_backward_event is recorded when d_xf is final (the
+  // factored path: after its first GEMM), at the latest when the call's work is enqueued.
+  const cudaStream_t st = (cudaStream_t)stream;
+  auto done = [&](int rc) { return rc ? rc : backward_event_record(st); };
   if (mma == DT_MMA_BF16 && tc_backward_ok(g))
-    return tc_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
-                       d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream,
-                       p_in);
+    return done(tc_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf,
+                            d_wf, d_bias, d_input, (char *)workspace, workspace_bytes, st, p_in));
   if (p_in) {
     set_error("backward: a kept P applies to the tensor-core backward of reuse geometries only");
     return DT_E_UNSUPPORTED;
   }
   // general (straddling) geometries on the tensor cores (k_train.cu)
   if (mma == DT_MMA_BF16 && xback_general_ok(g))
-    return xback_general(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
-                         d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
-  return ffma_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf, d_wf,
-                       d_bias, d_input, (char *)workspace, workspace_bytes, (cudaStream_t)stream);
+    return done(xback_general(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf,
+                              d_wf, d_bias, d_input, (char *)workspace, workspace_bytes, st));
+  return done(ffma_backward(g, batch, x, x_dtype, xf, wf, bias, act, act_arg, upstream, d_xf,
+                            d_wf, d_bias, d_input, (char *)workspace, workspace_bytes, st));
 }
 
 size_t dt_forward_mse_workspace_bytes(const dt_plan *plan, int64_t batch) {

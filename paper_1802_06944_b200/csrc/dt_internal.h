@@ -124,7 +124,7 @@ struct XGemm {
   int64_t ldb = 0;
   int b_mn = 0;
   int64_t b_wrap_k = 0;  // > 0: B's rows (K) wrap modulo this (A = [hi; lo] stacked along K)
-  int64_t b_rows = 0;    // with b_wrap_k: rows B actually stores (< wrap: zero fill past them)
+  int64_t b_rows = 0;    // K extent B actually stores (zero fill past it; with b_wrap_k: < wrap)
   int force_part = 0;    // result through the partial buffer + reduce (any output pitch)
   int el = 1;
   int BN = 256;
@@ -151,6 +151,9 @@ struct XGemm {
   int y_dtype = DT_F32, act = DT_ACT_IDENTITY;
   float act_arg = 0.f;
   int chain = 0;                  // pipelined forward (PDL trigger after the prologue)
+  // > 0: every stage also multiplies A at K offset dual_k (a K-major A whose rows hold two
+  // halves, e.g. [W_hi | W_lo]) by the same B tile; K is then the length of ONE half
+  int64_t dual_k = 0;
 };
 size_t xgemm_ws(const XGemm &g);
 int xgemm_splits(int64_t M, int64_t N, int64_t K, int BN, int el, int nsm);
@@ -216,6 +219,8 @@ void profile_next(cudaEvent_t *before, cudaEvent_t *after, int kind);
 // dt_set_forward_pipeline state of this thread.
 bool forward_pipeline();
 bool forward_pipeline_external_x();
+// records (once) the event set by dt_set_backward_event on st; no-op when none is pending
+int backward_event_record(cudaStream_t st);
 
 // Raise fn's dynamic shared-memory limit to at least `bytes` on the CURRENT device (function
 // attributes are per device context: a process driving several GPUs sets them on each).

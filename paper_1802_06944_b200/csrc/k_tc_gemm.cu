@@ -1733,10 +1733,11 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     }
     if (int rc = check_launch("regen_wt")) return rc;
     XGemm xg;
-    xg.M = g.r_dim; xg.N = batch; xg.K = 2 * qp;
+    // K = qp with the lo half riding in the same stages (dual A): x is read once per tile
+    xg.M = g.r_dim; xg.N = batch; xg.K = qp;
     xg.A = w2; xg.lda = 2 * qp; xg.a_mn = 0;
-    xg.B = xt; xg.ldb = ldx; xg.b_mn = 0;
-    xg.b_wrap_k = qp; xg.b_rows = g.q;
+    xg.dual_k = qp;
+    xg.B = xt; xg.ldb = ldx; xg.b_mn = 0; xg.b_rows = g.q;
     xg.el = 0;
     xg.BN = 256;
     xg.epi = 4;  // transposed store: y[b][j] = act(D[j][b] + bias[j])

@@ -78,6 +78,8 @@ struct XgParams {
   float act_arg;              // XE_STORE_T activation argument
   void *out_t;                // XE_STORE_T: out[n][m] (pitch ldo), fp32 or bf16
   int N_true;                 // XE_STORE_T: rows of out (D columns) actually stored
+  int dual_kb;                // > 0: each stage also carries A at k-block kb + dual_kb (a second
+                              // A half, e.g. W_lo beside W_hi) multiplied by the same B tile
 };
 
 // K-major: rows of 128 B (the k-block), 8-row swizzle atoms 1024 B apart (SWIZZLE_128B).
@@ -175,7 +177,8 @@ __global__ void __launch_bounds__(XTHREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t bytes = 2u * (XA_BYTES + (uint32_t)p.nhalf * 128u);
+      const uint32_t abytes = p.dual_kb > 0 ? 2u * XA_BYTES : XA_BYTES;
+      const uint32_t bytes = 2u * (abytes + (uint32_t)p.nhalf * 128u);
       for (int u = cid; u < p.units; u += ncl) {
         int mb, nb, ks;
         unit_of(u, mb, nb, ks);
@@ -186,7 +189,9 @@ __global__ void __launch_bounds__(XTHREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
           uint8_t *st = smem + stage * p.stage_bytes;
           xload(st, &tm_a, &full[stage], p.a_mn, EL, m0, 128, kb);
-          xload(st + XA_BYTES, &tm_b, &full[stage], p.b_mn, EL, n0, p.nhalf,
+          if (p.dual_kb > 0) xload(st + abytes - XA_BYTES, &tm_a, &full[stage], p.a_mn, EL, m0, 128,
+                                   kb + p.dual_kb);
+          xload(st + abytes, &tm_b, &full[stage], p.b_mn, EL, n0, p.nhalf,
                 p.b_wrap > 0 ? kb % p.b_wrap : kb);
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
@@ -211,7 +216,8 @@ __global__ void __launch_bounds__(XTHREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_s = s0 + (uint32_t)stage * p.stage_bytes, b_s = a_s + XA_BYTES;
+          const uint32_t a_s = s0 + (uint32_t)stage * p.stage_bytes;
+          const uint32_t b_s = a_s + (p.dual_kb > 0 ? 2u * XA_BYTES : XA_BYTES);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t da = xdesc(a_s, p.a_mn, k, EL), db = xdesc(b_s, p.b_mn, k, EL);
@@ -219,6 +225,14 @@ __global__ void __launch_bounds__(XTHREADS, 1)
               mma_tf32_ss_pair(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             else
               mma_bf16_ss_pair(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          if (p.dual_kb > 0) {  // the second A half against the same B stage
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t da = xdesc(a_s + XA_BYTES, p.a_mn, k, EL), db = xdesc(b_s, p.b_mn, k, EL);
+              if constexpr (EL) mma_tf32_ss_pair(d, da, db, idesc, 1u);
+              else mma_bf16_ss_pair(d, da, db, idesc, 1u);
+            }
           }
           mma_commit_pair(&empty[stage]);
           if (++stage == p.S) { stage = 0; phase ^= 1; }
@@ -631,7 +645,12 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   p.h_s = g.h_s;
   p.pair_half = g.pair_half;
   p.ks_major = g.ks_major;
-  p.stage_bytes = XA_BYTES + (uint32_t)nhalf * 128u;
+  p.dual_kb = g.dual_k > 0 ? (int)(g.dual_k / bke) : 0;
+  if (g.dual_k > 0 && (g.dual_k % bke || g.a_mn)) {
+    set_error("xgemm: the dual-A offset must be whole k-blocks of a K-major A");
+    return DT_E_ARG;
+  }
+  p.stage_bytes = (p.dual_kb > 0 ? 2u : 1u) * XA_BYTES + (uint32_t)nhalf * 128u;
   const uint32_t stg_bytes = (g.epi == XE_SPLITH || g.epi == XE_STORE_T) ? 0u
                              : (uint32_t)XEPI * (g.epi == XE_MSE ? 3u : 2u) * XSTG;
   // barriers + TMEM slot (512 B), then the XE_MSE column-sum exchange [2][4][256] floats
@@ -652,13 +671,13 @@ int xgemm(const XGemm &g, cudaStream_t st) {
   const int mn_sw = el ? (int)CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : (int)CU_TENSOR_MAP_SWIZZLE_128B;
   if (int rc = g.a_mn ? encode_tensor_map_2d_sw(&tm_a, tdt, A, (uint64_t)g.M, (uint64_t)g.K,
                                                 (uint64_t)g.lda * esz, 128 / esz, bke, mn_sw)
-                      : encode_tensor_map_2d(&tm_a, tdt, A, (uint64_t)g.K, (uint64_t)g.M,
+                      : encode_tensor_map_2d(&tm_a, tdt, A, (uint64_t)(g.K + g.dual_k), (uint64_t)g.M,
                                              (uint64_t)g.lda * esz, bke, 128, true))
     return rc;
   // rows of B along K: the wrap length, or the stored extent when shorter (zero fill past it)
   const uint64_t kb_rows = g.b_wrap_k > 0 ? (uint64_t)(g.b_rows > 0 ? std::min(g.b_rows, g.b_wrap_k)
                                                                    : g.b_wrap_k)
-                                          : (uint64_t)g.K;
+                                          : (uint64_t)(g.b_rows > 0 ? std::min(g.b_rows, g.K) : g.K);
   if (int rc = g.b_mn ? encode_tensor_map_2d_sw(&tm_b, tdt, B, (uint64_t)g.N, kb_rows,
                                                 (uint64_t)g.ldb * esz, 128 / esz, bke, mn_sw)
                       : encode_tensor_map_2d(&tm_b, tdt, B, kb_rows, (uint64_t)g.N,

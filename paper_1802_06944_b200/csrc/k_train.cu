@@ -271,6 +271,9 @@ int xtrain_backward(const Geo &g, int64_t batch, const void *x, int x_dtype, con
     const int64_t tail = (g.m - g.r_dim * g.s) * g.rank;
     if (tail > 0) DT_CUDA_CHECK(cudaMemsetAsync(d_xf + g.r_dim * SR, 0, (size_t)tail * 4, st));
   }
+  // d_xf and d_bias are final: a data-parallel caller's all-reduce of them may start now
+  // (dist.GradReducer), overlapping H and d_wf below
+  if (int rc = backward_event_record(st)) return rc;
   // H = g @ XF2, written re-laid as H2 = [hi | lo] (B*s x 2r bf16)
   {
     XGemm h = gemm_h(g, batch, 3);

@@ -9,6 +9,8 @@ inverse re-layout, all-reduce, SGD (train.py:107-111).
 
 from __future__ import annotations
 
+from ctypes import c_void_p as ctypes_void_p
+
 import ctypes as C
 from dataclasses import dataclass
 
@@ -103,6 +105,17 @@ class DeepThinLayer:
         self._p = None
         return d_in
 
+    def reducer(self, group=None):
+        """dist.GradReducer over grad_flat with buckets [d_xf] then [d_wf | d_bias] (the order
+        the tensor-core backward finalises them), cached per process group."""
+        from .dist import GradReducer
+        key = id(group)
+        cache = self.__dict__.setdefault("_reducers", {})
+        if key not in cache:
+            ow = -(-(self.plan.m * self.plan.rank) // 64) * 64
+            cache[key] = GradReducer(self.grad_flat, [(0, ow), (ow, self.grad_flat.numel())], group)
+        return cache[key]
+
     def grad_buffers(self):
         """train.py:226-227: the gradient buffers the global-norm clip sees."""
         return [self.d_xf, self.d_wf, self.d_bias]
@@ -129,8 +142,18 @@ def train_step(layer: DeepThinLayer, x: torch.Tensor, target: torch.Tensor, lr: 
         y = layer.forward(x)
         g = torch.empty_like(y)
         mse_grad_into(y, target, g, norm, ls)
-    layer.backward(g)
-    allreduce_grads(layer.grad_flat, group)
+    red = layer.reducer(group)
+    if red.active:
+        # d_xf is final after the backward's first GEMM: its all-reduce overlaps the rest
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())  # cudaEvent_t created; re-recorded in the backward
+        _lib.check(_lib.lib().dt_set_backward_event(ctypes_void_p(ev.cuda_event)))
+        layer.backward(g)
+        red.launch(0, ev)
+        red.launch(1)
+        red.wait()
+    else:
+        layer.backward(g)
     layer.step(lr)
     return ls
 

@@ -66,8 +66,10 @@ def main():
         step = c5_step(rows)
     elif key == "c3":
         step = c3_step(rows if len(sys.argv) > 3 else 16384)
+    elif key == "c2":
+        step = c2_step(rows if len(sys.argv) > 3 else 4096)
     else:
-        raise SystemExit("configs: c5, c3")
+        raise SystemExit("configs: c5, c3, c2")
     for _ in range(3):
         step()
     torch.cuda.synchronize()
@@ -91,6 +93,24 @@ def main():
     for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         print(f"{sum(v) / steps:9.1f} us  {len(v) / steps:5.1f}x  {sum(v) / len(v):8.1f} us  "
               f"{sum(v) / steps / tot:6.1%}  {name}")
+
+
+
+def c2_step(rows=4096):
+    import numpy as np
+    plan = D.LayerPlan(q=440, r_dim=2048, rank=24, m=2816, n=320)
+    rng = np.random.default_rng(0)
+    fp = D.FactorPair(rng.normal(0, 24 ** -0.5, (2816, 24)), rng.normal(0, 24 ** -0.5, (24, 320)), plan)
+    b = torch.tensor(rng.normal(0, 0.01, 2048), dtype=torch.float32, device="cuda")
+    xs = [torch.randn(rows, 440, device="cuda").to(torch.bfloat16) for _ in range(8)]
+    from paper_1802_06944_b200.kernel import forward_pipeline
+    it = [0]
+
+    def step():
+        with forward_pipeline(True, external_x=True):
+            D.layer_forward(xs[it[0] % 8], fp, b, mma="bf16")
+        it[0] += 1
+    return step
 
 
 if __name__ == "__main__":

@@ -108,3 +108,43 @@ def test_bench_self_launches_ranks_dry_run():
     assert len(lines) == 1
     assert lines[0]["n_gpus"] == 2 and lines[0]["rank_sum"] == 3.0
     assert "world_size=2" in r.stderr
+
+
+def _reducer_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1802_06944_b200.dist import GradReducer, allreduce_grads
+    rng = np.random.default_rng(10 + rank)
+    flat = torch.tensor(rng.standard_normal(1000))
+    ref = flat.clone()
+    allreduce_grads(ref)
+    red = GradReducer(flat, [(0, 384), (384, 1000)])
+    assert red.active
+    red.launch(0)        # the d_xf bucket first (final before d_wf / d_bias)
+    red.launch(1)
+    red.wait()
+    np.save(os.path.join(out_dir, f"red{rank}.npy"), flat.numpy())
+    np.save(os.path.join(out_dir, f"ref{rank}.npy"), ref.numpy())
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_bucketed_overlapped_reducer_equals_one_allreduce(tmp_path):
+    """dist.GradReducer (bucketed, asynchronous; on GPUs each bucket waits only on the event the
+    backward records when it is final) reduces to the same buffer as one all-reduce."""
+    world = 2
+    mp.spawn(_reducer_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"red{r}.npy"), np.load(tmp_path / f"ref{r}.npy"))
+
+
+def test_reducer_single_process_is_noop():
+    from paper_1802_06944_b200.dist import GradReducer
+    t = torch.arange(6.0)
+    red = GradReducer(t, [(0, 2), (2, 6)])
+    assert not red.active
+    red.launch(0)
+    red.launch(1)
+    red.wait()
+    assert torch.equal(t, torch.arange(6.0))
