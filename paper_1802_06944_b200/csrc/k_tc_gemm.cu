@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);  // this warp's TMEM reads are done
+      if (lane == 0) mbar_arrive_relaxed(&tempty[acc]);  // this warp's TMEM reads are done
       if (threadIdx.x == 64) gtrace(p, 12 + min(it - beg, 7));
       if (threadIdx.x == kGemmThreads - 32 && it - beg < 2) gtrace(p, 46 + (it - beg));
       if (++acc == 2) { acc = 0; aphase ^= 1; }
@@ -893,6 +893,13 @@ __device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t crank) {
     mbar_arrive(bar);
   else
     mbar_arrive_remote(bar, 0);
+}
+// "TMEM read" signals of the epilogue: relaxed (see mbar_arrive_relaxed)
+__device__ __forceinline__ void arrive_leader_tmem(uint64_t *bar, uint32_t crank) {
+  if (crank == 0)
+    mbar_arrive_relaxed(bar);
+  else
+    mbar_arrive_remote_relaxed(bar, 0);
 }
 
 template <int YDT, int ACT, int EL>
@@ -1162,7 +1169,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_leader(&tempty[acc], crank);  // the leader's MMAs reuse it
+      if (lane == 0) arrive_leader_tmem(&tempty[acc], crank);  // the leader's MMAs reuse it
       if (threadIdx.x == 64) gtrace(p, 12 + min(it - beg, 7));
       if (threadIdx.x == kGemmThreads - 32 && it - beg < 2) gtrace(p, 46 + (it - beg));
       if (++acc == 2) { acc = 0; aphase ^= 1; }

@@ -112,11 +112,12 @@ __device__ __forceinline__ uint32_t stg_off(int r, int c16) {  // SW128 32 x 128
   return (uint32_t)r * 128u + ((uint32_t)(c16 ^ (r & 7)) << 4);
 }
 
+// the epilogue's "TMEM read" signal: relaxed (see mbar_arrive_relaxed)
 __device__ __forceinline__ void arrive_leader_x(uint64_t *bar, uint32_t crank) {
   if (crank == 0)
-    mbar_arrive(bar);
+    mbar_arrive_relaxed(bar);
   else
-    mbar_arrive_remote(bar, 0);
+    mbar_arrive_remote_relaxed(bar, 0);
 }
 
 template <int EL, int EPI, int YDT = DT_F32, int ACT = DT_ACT_IDENTITY>

@@ -151,6 +151,18 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
     }
   }
 }
+// Relaxed arrives (no memory ordering): for "this warp's TMEM reads are done" signals. The
+// reads completed at tcgen05.wait::ld, so nothing needs releasing — and a release arrive would
+// make the warp wait for its outstanding global stores (MEMBAR) before signalling.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t *bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
 // Shared-memory address of the same offset in cluster CTA `cta` (for st.shared::cluster).
 __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t cta) {
   uint32_t r;
