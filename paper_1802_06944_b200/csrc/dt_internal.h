@@ -83,6 +83,8 @@ int encode_tensor_map_2d(CUtensorMap *tm, int dtype, void *base, uint64_t inner,
                          bool swizzle128);
 // ... with an explicit CUtensorMapSwizzle mode (e.g. CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, the
 // layout tcgen05 requires for MN-major tf32 operands)
+int encode_tensor_map_mn3d(CUtensorMap *tm, int dtype, void *base, uint64_t mn, uint64_t k,
+                           uint64_t pitch_bytes, uint32_t bk, uint32_t nchunks, int swizzle);
 int encode_tensor_map_2d_sw(CUtensorMap *tm, int dtype, void *base, uint64_t inner, uint64_t outer,
                             uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
                             int swizzle);

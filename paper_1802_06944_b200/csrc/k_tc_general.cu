@@ -1237,4 +1237,30 @@ int encode_tensor_map_2d_sw(CUtensorMap *tm, int dtype, void *base, uint64_t inn
   return DT_OK;
 }
 
+// 3-D map for an MN-major operand: dims (elements of one 128-byte chunk along M/N, K rows,
+// chunks along M/N), so ONE box of (chunk, bk, nchunks) lands in shared memory as the UMMA
+// canonical MN-major layout [chunk][K row][128 B] (instead of one 2-D box per chunk).
+int encode_tensor_map_mn3d(CUtensorMap *tm, int dtype, void *base, uint64_t mn, uint64_t k,
+                           uint64_t pitch_bytes, uint32_t bk, uint32_t nchunks, int swizzle) {
+  PFN_encode_tiled enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return DT_E_CUDA;
+  }
+  const uint64_t esz = dtype == DT_BF16 ? 2 : 4, ce = 128 / esz;
+  cuuint64_t dims[3] = {(cuuint64_t)ce, (cuuint64_t)k, (cuuint64_t)(mn / ce)};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch_bytes, (cuuint64_t)128};
+  cuuint32_t box[3] = {(cuuint32_t)ce, bk, nchunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(tm, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                    3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    (CUtensorMapSwizzle)swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)cr));
+    return DT_E_CUDA;
+  }
+  return DT_OK;
+}
+
 }  // namespace dt
