@@ -151,6 +151,21 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
                float act_arg, void *y, int y_dtype, void *workspace, size_t workspace_bytes,
                dt_stream stream);
 
+/* Which kernel family dt_forward takes for (plan, mma, x/f/y dtypes) with 16-byte-aligned
+ * operands (misaligned pointers fall back to the staged two-phase forms). Each family states its
+ * own arithmetic contract; tests pick the matching emulation from it.
+ * Returns a DT_PATH_* value, or a negative dt_status on a bad plan / argument. */
+enum dt_path {
+  DT_PATH_FFMA = 1,     /* fp32 FFMA                                               */
+  DT_PATH_ROWS = 2,     /* one-kernel row-tile reuse form (k_tc_rows.cu)           */
+  DT_PATH_FACTORED = 3, /* factored reuse, two GEMMs (P = x wf^T, y = P XF2^T)     */
+  DT_PATH_RUNS = 4,     /* memoized runs, low-rank straddling layers (k_tc_runs.cu) */
+  DT_PATH_HILO = 5,     /* two-phase, W^T as bf16 hi + lo (fp32 outputs)           */
+  DT_PATH_PAIR = 6,     /* two-phase, W^T rounded once to bf16                     */
+  DT_PATH_FUSED = 7     /* single kernel, W regenerated in-kernel (packed factors) */
+};
+int dt_forward_path(const dt_plan *plan, int mma, int x_dtype, int f_dtype, int y_dtype);
+
 size_t dt_backward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma);
 
 /* Replaces grad.py:63-95 layer_backward: gradients through activation, bias,

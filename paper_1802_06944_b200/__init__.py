@@ -12,7 +12,7 @@ from .errors import (ArgumentError, CudaError, DeepThinError, DimensionError, In
                      UnsupportedConfigurationError)
 from .factor import FactorPair, decompress, init_factors, phase, phase_count, relayout_index
 from .grad import Gradients, layer_backward, loss_and_grad
-from .kernel import (ACTIVATIONS, OpCount, ReuseTable, forward_pipeline, fused_matmul,
+from .kernel import (ACTIVATIONS, OpCount, ReuseTable, forward_path, forward_pipeline, fused_matmul,
                      layer_forward, op_count, predict_reuse)
 from .model import DeviceModel
 from .model_io import (CompressedModel, deserialize, expected_file_size, load_model, save_model,
@@ -28,7 +28,7 @@ __all__ = [
     "DeepThinLayer", "DeviceModel", "DimensionError", "FactorPair", "Gradients", "LayerPlan",
     "ModelFormatError", "NetworkPlan", "OpCount", "ReuseTable",
     "UnsupportedConfigurationError", "baseline_plan", "decompress", "deserialize",
-    "expected_file_size", "forward_pipeline", "fused_matmul", "load_model", "save_model",
+    "expected_file_size", "forward_path", "forward_pipeline", "fused_matmul", "load_model", "save_model",
     "serialize",
     "init_factors", "layer_backward", "layer_forward", "loss_and_grad", "make_rng",
     "max_abs_diff", "op_count", "phase", "phase_count", "predict_reuse", "rel_error",

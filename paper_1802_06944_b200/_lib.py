@@ -19,6 +19,8 @@ DT_F32, DT_BF16, DT_FACTORS_PACKED, DT_F64, DT_FACTORS_ROWS = 0, 1, 2, 3, 4
 DT_MMA_FFMA, DT_MMA_BF16 = 0, 1
 DT_PROF_ANY, DT_PROF_GEMM, DT_PROF_ROWS = 0, 1, 2
 DT_PIPELINE_OFF, DT_PIPELINE_ON, DT_PIPELINE_EXTERNAL_X = 0, 1, 2
+# dt_forward_path results (include/deepthin_b200.h enum dt_path)
+PATHS = {1: "ffma", 2: "rows", 3: "factored", 4: "runs", 5: "hilo", 6: "pair", 7: "fused"}
 ACT_CODES = {"identity": 0, "relu": 1, "sigmoid": 2, "tanh": 3, "clipped_relu": 4, "softmax": 5}
 
 # Every symbol the header declares (checked by tests/test_abi.py).
@@ -26,7 +28,7 @@ EXPORTS = (
     "dt_version", "dt_last_error", "dt_launch_counter", "dt_profile_kernel_events", "dt_profile_kernel_kind", "dt_set_forward_pipeline", "dt_plan_validate", "dt_plan_query", "dt_phase",
     "dt_relayout_index", "dt_predict_reuse", "dt_op_count", "dt_decompress", "dt_cast_bf16",
     "dt_packed_factors_bytes", "dt_pack_factors",
-    "dt_forward_workspace_bytes", "dt_forward", "dt_backward_workspace_bytes", "dt_backward",
+    "dt_forward_workspace_bytes", "dt_forward", "dt_forward_path", "dt_backward_workspace_bytes", "dt_backward",
     "dt_mse_grad", "dt_mse_workspace_bytes", "dt_forward_mse", "dt_forward_mse_workspace_bytes", "dt_forward_mse_ex", "dt_forward_p_bytes", "dt_backward_ex", "dt_sgd_step", "dt_matmul_workspace_bytes", "dt_matmul", "dt_chain_ok", "dt_chain_forward", "dt_set_backward_event", "dt_rows_prepared_bytes", "dt_rows_prepare", "dt_rows_chain", "dt_rows_posts_per_tile", "dt_lstm_gates_workspace_bytes", "dt_lstm_gates", "dt_lstm_sequence_workspace_bytes", "dt_lstm_sequence", "dt_lstm_cell", "dt_session_create",
     "dt_session_forward", "dt_session_destroy", "dt_model_parse", "dt_unpack_values",
 )
@@ -113,6 +115,7 @@ def _declare(lib):
         "dt_chain_ok": ([P, i], i),
         "dt_set_backward_event": ([VP], i),
         "dt_chain_forward": ([P, i, I64, VP, C.POINTER(VP), i, F, i, VP, VP], i),
+        "dt_forward_path": ([P, i, i, i, i], i),
         "dt_matmul": ([I64, I64, I64, VP, I64, i, VP, I64, i, i, VP, I64, VP, SZ, VP], i),
         "dt_rows_prepared_bytes": ([P, i, i], SZ),
         "dt_rows_chain": ([VP, C.c_uint, VP], i),

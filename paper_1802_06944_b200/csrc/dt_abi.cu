@@ -352,6 +352,27 @@ int dt_forward(const dt_plan *plan, int64_t batch, int mma, const void *x, int x
   return DT_E_ARG;
 }
 
+int dt_forward_path(const dt_plan *plan, int mma, int x_dtype, int f_dtype, int y_dtype) {
+  Geo g;
+  if (int rc = make_geo(plan, &g)) return -rc;
+  if (int rc = check_dtype(x_dtype, "x")) return -rc;
+  if (int rc = check_dtype(y_dtype, "y")) return -rc;
+  if (mma == DT_MMA_FFMA) {
+    if (f_dtype == DT_F32) return DT_PATH_FFMA;
+    set_error("the FFMA path takes fp32 factors");
+    return -DT_E_ARG;
+  }
+  if (mma != DT_MMA_BF16) {
+    set_error("unknown mma kind " + std::to_string(mma));
+    return -DT_E_ARG;
+  }
+  if (f_dtype == DT_FACTORS_ROWS) return tc_rows_ok(g, x_dtype, y_dtype) ? DT_PATH_ROWS : -DT_E_UNSUPPORTED;
+  static const int want_fused = getenv("DEEPTHIN_TC_FUSED") ? atoi(getenv("DEEPTHIN_TC_FUSED")) : 0;
+  if (f_dtype == DT_FACTORS_PACKED || (want_fused && f_dtype == DT_BF16 && !g.reuse))
+    return g.reuse ? -DT_E_UNSUPPORTED : DT_PATH_FUSED;
+  return tc_forward_path(g, x_dtype, f_dtype, y_dtype);
+}
+
 size_t dt_backward_workspace_bytes(const dt_plan *plan, int64_t batch, int mma) {
   Geo g;
   if (make_geo(plan, &g) || batch < 0) return 0;

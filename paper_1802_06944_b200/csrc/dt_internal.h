@@ -105,6 +105,14 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
 bool tc_chain_ok(const Geo *g, int L);
 int tc_chain_forward(const Geo *g, int L, int64_t batch, const void *x, void *const *prepared,
                      int hidden_act, float act_arg, void *y, cudaStream_t st);
+// Low-rank straddling layers as the reference's memoized runs (k_tc_runs.cu): bf16 in / out,
+// P' = x . Wruns^T (wf hi + lo), y = act(P' . XFfull^T + b); W never exists.
+bool tc_runs_ok(const Geo &g, int x_dtype, int y_dtype);
+// dt_forward_path for the two-phase entry (tc_forward_impl's own choice, aligned operands)
+int tc_forward_path(const Geo &g, int x_dtype, int f_dtype, int y_dtype);
+size_t tc_runs_ws(const Geo &g);
+int tc_runs_forward(const Geo &g, int64_t batch, const void *x, const float *wf, const float *xf,
+                    const float *bias, int act, float act_arg, void *y, char *ws, cudaStream_t st);
 // layer chaining for the next tc_rows_forward on this thread (prepared operands only)
 void rows_chain(const unsigned *wait, unsigned target, unsigned *post);
 int rows_posts_per_tile(const Geo &g);

@@ -1521,6 +1521,12 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
 // rounding (P stays fp32; rounding it to bf16 measured 2.5e-3 rel_error at config 1 — over the
 // 2e-3 contract — while tf32 products keep the two-GEMM error at the operand-rounding level).
 // Needs aligned views: n % 8 == 0 (bf16 rows), s*rank % 4 == 0 (fp32 rows); fp32 factors.
+// DEEPTHIN_RUNS=0 routes low-rank straddling layers to the two-phase path instead (comparisons)
+static bool runs_disabled() {
+  static const bool off = getenv("DEEPTHIN_RUNS") && atoi(getenv("DEEPTHIN_RUNS")) == 0;
+  return off;
+}
+
 static bool reuse_factored_ok(const Geo &g) {
   const int want = getenv("DEEPTHIN_REUSE_FACTORED") ? atoi(getenv("DEEPTHIN_REUSE_FACTORED")) : 1;
   return want && g.reuse && g.n % 8 == 0 && (g.s * g.rank) % 4 == 0;
@@ -1548,8 +1554,10 @@ size_t tc_gemm_ws(const Geo &g, int64_t batch) {
   const int64_t ldw = round_up(g.q, 8);
   const size_t two_phase =  // two W^T slots (pipelined forwards alternate) + packed x
       2 * (size_t)wt_slot_bytes(g) + (size_t)round_up(batch * ldw * 2, 256);
-  return std::max(std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch) : (size_t)0),
-                  tc_rows_ws(g));
+  return std::max(std::max(std::max(two_phase, reuse_factored_ok(g) ? reuse_factored_ws(g, batch)
+                                                                     : (size_t)0),
+                           tc_rows_ws(g)),
+                  tc_runs_ws(g));
 }
 
 struct MseArgs {
@@ -1621,6 +1629,17 @@ int tc_forward_mse(const Geo &g, int64_t batch, const void *x, int x_dtype, cons
   return rc;
 }
 
+int tc_forward_path(const Geo &g, int x_dtype, int f_dtype, int y_dtype) {
+  // mirrors tc_forward_impl's order below (non-MSE launch, 16-byte-aligned operands)
+  if (f_dtype != DT_F32 && f_dtype != DT_BF16) return -DT_E_ARG;
+  if (g.m * g.n > INT32_MAX || g.r_dim > INT32_MAX / 2) return -DT_E_UNSUPPORTED;
+  if (f_dtype == DT_F32 && tc_rows_ok(g, x_dtype, y_dtype)) return DT_PATH_ROWS;
+  if (reuse_factored_ok(g) && f_dtype == DT_F32) return DT_PATH_FACTORED;
+  if (f_dtype == DT_F32 && tc_runs_ok(g, x_dtype, y_dtype) && !runs_disabled()) return DT_PATH_RUNS;
+  if (y_dtype == DT_F32 && g.q * 2 * round_up(g.q, 64) < INT32_MAX) return DT_PATH_HILO;
+  return DT_PATH_PAIR;
+}
+
 static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dtype,
                            const void *xf, const void *wf, int f_dtype, const float *bias,
                            int act, float act_arg, void *y, int y_dtype, char *ws,
@@ -1690,6 +1709,12 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     }
     return finish_mse(run_gemm(c2, st));
   }
+
+  // ---- low-rank straddling layers, bf16 in / out: the memoized runs (k_tc_runs.cu) ----
+  if (!mse && f_dtype == DT_F32 && tc_runs_ok(g, x_dtype, y_dtype) && !runs_disabled() &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0)
+    return tc_runs_forward(g, batch, x, reinterpret_cast<const float *>(wf),
+                           reinterpret_cast<const float *>(xf), bias, act, act_arg, y, ws, st);
 
   // ---- two-phase: W^T regenerated into the workspace, then the GEMM ----
   const int64_t ldw = round_up(g.q, 8);

@@ -73,6 +73,7 @@ XGemm gemm_z(const Geo &g, int64_t batch) {  // z = P2 @ XF2^T (+ b), MSE epilog
   x.M = batch; x.N = g.r_dim; x.K = g.s * g.rank;
   x.a_mn = 0; x.b_mn = 0; x.el = 1; x.BN = 256;
   x.epi = 1;
+  if (int bn = DT_DBG_ENV("DEEPTHIN_MSE_BN")) x.BN = bn;  // timing builds: tile experiments
   return x;
 }
 XGemm gemm_dxf(const Geo &g, int64_t batch) {  // dXF2 = g^T @ P2

@@ -88,6 +88,24 @@ def op_count(plan, batch: int) -> OpCount:
     return OpCount(multiplies=mul.value, adds=add.value)
 
 
+def forward_path(plan, mma: str = "bf16", x_dtype=torch.bfloat16, y_dtype=torch.float32,
+                 factors: str = "f32") -> str:
+    """Kernel family layer_forward takes (dt_forward_path): "ffma", "rows", "factored", "runs",
+    "hilo", "pair" or "fused" — each with its own arithmetic contract."""
+    dt = {torch.bfloat16: _lib.DT_BF16, torch.float32: _lib.DT_F32}
+    fd = {"f32": _lib.DT_F32, "bf16": _lib.DT_BF16, "packed": _lib.DT_FACTORS_PACKED,
+          "rows": _lib.DT_FACTORS_ROWS}
+    mk = {"ffma": _lib.DT_MMA_FFMA, "bf16": _lib.DT_MMA_BF16}
+    if x_dtype not in dt or y_dtype not in dt or factors not in fd or mma not in mk:
+        raise ArgumentError("forward_path: x/y dtype bf16|fp32, factors f32|bf16|packed|rows, "
+                            "mma ffma|bf16")
+    rc = _lib.lib().dt_forward_path(C.byref(_lib.plan_struct(plan)), mk[mma], dt[x_dtype],
+                                    fd[factors], dt[y_dtype])
+    if rc < 0:
+        _lib.check(-rc)
+    return _lib.PATHS[rc]
+
+
 def _resolve_threads(threads):
     """kernel.py:208-214 — accepted for signature parity; GPU results never depend on it."""
     if threads is None:

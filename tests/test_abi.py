@@ -161,3 +161,19 @@ def test_no_cpu_fallback_without_gpu():
     p = D.LayerPlan(q=8, r_dim=8, rank=1, m=8, n=8)
     with pytest.raises(D.CudaError):
         D.FactorPair(np.ones((8, 1)), np.ones((1, 8)), p)
+
+
+def test_forward_path_selection():
+    """dt_forward_path (host-only): the kernel family per geometry and dtypes."""
+    import torch
+    cases = {(440, 2048, 3, 320): ("runs", "hilo"), (2048, 2048, 3, 256): ("rows", "rows"),
+             (8192, 8192, 64, 1024): ("factored", "factored"), (440, 512, 4, 320): ("pair", "hilo")}
+    for (q, r, k, n), want in cases.items():
+        p = D.LayerPlan(q=q, r_dim=r, rank=k, m=-(-(q * r) // n), n=n)
+        got = tuple(D.forward_path(p, "bf16", torch.bfloat16, y) for y in (torch.bfloat16, torch.float32))
+        assert got == want, (q, r, k, n, got)
+        assert D.forward_path(p, "ffma", torch.float32, torch.float32) == "ffma"
+        # a fp32 x disqualifies the bf16-only kernels (rows / runs); the staged forms remain
+        assert D.forward_path(p, "bf16", torch.float32, torch.bfloat16) in ("factored", "pair")
+    with pytest.raises(D.ArgumentError):
+        D.forward_path(p, "ffma", torch.float32, torch.float32, factors="bf16")

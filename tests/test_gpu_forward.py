@@ -60,23 +60,13 @@ def path_contract(path, d, plan, bias):
 
 
 def factored_path(plan, y_dtype=torch.float32):
-    """The bf16 tensor-core path computes reuse geometries in factored form when the views are
-    16-byte aligned (k_tc_gemm.cu reuse_factored_ok) or the row-tile kernel takes them (bf16 x,
-    k_tc_rows.cu tc_rows_ok, which pads each segment's rank and so has no s*rank % 4 rule)."""
-    if plan.q % plan.n:
-        return False
-    s = plan.q // plan.n
-    if plan.n % 8 == 0 and (s * plan.rank) % 4 == 0:
-        return True
-    return rows_path(plan, y_dtype)
+    """The bf16 tensor-core path computes reuse geometries in factored form: the row-tile kernel
+    (k_tc_rows.cu) or the two-GEMM factored form (dt_forward_path)."""
+    return D.forward_path(plan, "bf16", torch.bfloat16, y_dtype) in ("rows", "factored")
 
 
 def rows_path(plan, y_dtype=torch.float32):
-    import ctypes as C
-    from paper_1802_06944_b200 import _lib
-    ps = _lib.plan_struct(plan)
-    yd = _lib.DT_BF16 if y_dtype == torch.bfloat16 else _lib.DT_F32
-    return _lib.lib().dt_rows_prepared_bytes(C.byref(ps), _lib.DT_BF16, yd) > 0
+    return D.forward_path(plan, "bf16", torch.bfloat16, y_dtype) == "rows"
 
 
 def bf16_factored_emulated(d, plan, bias):
@@ -92,11 +82,14 @@ def bf16_factored_emulated(d, plan, bias):
 
 
 def bf16_contract(d, plan, bias, y_dtype=torch.float32):
-    """Reuse geometries: the factored contract. Two-phase geometries: W as bf16 hi + lo for fp32
-    outputs, W rounded once to bf16 for bf16 outputs (k_tc_gemm.cu tc_forward_impl)."""
-    if factored_path(plan, y_dtype):
+    """Reuse geometries: the factored contract. Straddling geometries: the memoized runs and the
+    fp32-output two-phase form carry wf / W as bf16 hi + lo (the runs' tf32 rounding of P and xf,
+    2^-11 relative, is inside the bound); the bf16-output two-phase form rounds W once to bf16
+    (k_tc_gemm.cu tc_forward_impl, dt_forward_path)."""
+    path = D.forward_path(plan, "bf16", torch.bfloat16, y_dtype)
+    if path in ("rows", "factored"):
         return bf16_factored_emulated(d, plan, bias)
-    if y_dtype == torch.bfloat16:
+    if path == "pair":
         return bf16_emulated(d, plan, bias)
     return bf16_hilo_emulated(d, plan, bias)
 
@@ -384,3 +377,31 @@ def test_tc_forward_pipeline_matches_serial():
     torch.cuda.synchronize()
     for k, x in enumerate(xs):
         assert torch.equal(piped[2 * k], serial[k]) and torch.equal(piped[2 * k + 1], serial[k]), k
+
+
+@pytest.mark.parametrize("geo", [
+    (440, 2048, 3, 320, 2816, 1000),    # config 3 layer 0: period 8, 18 distinct runs
+    (440, 2048, 3, 320, 2816, 5),       # fewer rows than one tile
+    (120, 200, 2, 48, 503, 300),        # period 2, discarded tail rows
+    (64, 96, 5, 40, 157, 70),           # rank 5, 12 runs, ragged batch
+    (256, 1024, 1, 96, 2734, 129),      # rank 1 (the reference's own fused_matmul case)
+    (16, 64, 3, 24, 46, 33),            # q below one K block
+])
+@pytest.mark.parametrize("act", ["identity", "sigmoid", "relu"])
+def test_runs_path_low_rank_general_bf16(geo, act):
+    """k_tc_runs.cu: low-rank straddling layers with bf16 in/out as the reference's memoized
+    runs (kernel.py:99-164) — x . Wruns^T (wf hi + lo) then the tiny per-column combine with xf
+    (tf32) — against the oracle on the same bf16 inputs: logits <= 2e-3 + one bf16 ulp; the
+    fused activation on those logits."""
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=13, bias_sd=0.3)
+    assert D.forward_path(fp.plan, "bf16", torch.bfloat16, torch.bfloat16) == "runs"
+    x = gpu_x(O.round_bf16(d["x"]), torch.bfloat16)
+    ref = O.layer_forward(O.round_bf16(d["x"]), d["xf"], d["wf"], plan, d["bias"], "identity")
+    z = D.layer_forward(x, fp, d["bias"], "identity", mma="bf16", out_dtype=torch.bfloat16)
+    assert O.rel_error(z.double().cpu().numpy(), ref) <= BF16_TOL + 2 ** -8
+    y = D.layer_forward(x, fp, d["bias"], act, mma="bf16", out_dtype=torch.bfloat16)
+    want = O.apply_activation(act, ref)
+    tol = 2 ** -8 * max(1.0, float(np.max(np.abs(want)))) + (0.25 if act == "sigmoid" else 1.0) * \
+        BF16_TOL * float(np.max(np.abs(ref)))
+    assert np.max(np.abs(y.double().cpu().numpy() - want)) <= tol
