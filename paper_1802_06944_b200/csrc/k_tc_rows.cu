@@ -18,14 +18,17 @@
 // its P values into the tf32 A operand of every cluster CTA through distributed shared memory,
 // then computes and stores output chunks c, c+cs, ... Clusters are persistent over tiles.
 //
-// Warp roles (480 threads, one CTA per SM):
-//   warp 0  TMA producer of x k-blocks (128 rows x 64 bf16, SW128) into a 4-deep ring
+// Warp roles (768 threads, one CTA per SM):
+//   warp 0  TMA producer of x k-blocks (128 rows x 64 bf16, SW128) into a ring sized to the
+//           shared memory left (5-8 deep)
 //   warp 1  TMA producer of XF2 chunks (128 output columns x 32 fp32, SW128), 2-deep ring
-//   warp 2  TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 3-6  P exchange: P (TMEM) -> tf32 A operand of every cluster CTA (DSMEM stores)
-//   warps 7-14 epilogue: D chunks (TMEM, double-buffered 2 x 128 columns) -> bias +
+//   warp 2  TMEM allocator + single-thread tcgen05.mma issuer of phase A
+//   warps 3-6  P exchange: P (TMEM) -> tf32 A operand of every cluster CTA (DSMEM bulk copies)
+//   warps 7-22 epilogue: D chunks (TMEM, double-buffered 2 x 128 columns) -> bias +
 //           activation -> bf16/fp32 -> swizzled shared staging -> TMA store (each warp its
-//           own 32 rows x 128 B boxes).
+//           own 32 x 32 box)
+//   warp 23 single-thread tcgen05.mma issuer of phase B (decoupled from phase A: B of tile i
+//           never waits for tile i+1's x, A of tile i+1 never waits for the epilogue)
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -33,7 +36,9 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include "act.cuh"
@@ -51,7 +56,8 @@ constexpr int kXSMax = 8;          // x ring depth cap (the launcher sizes it to
 constexpr int kBS = 2;             // XF2 chunk ring depth (resident when a CTA has <= 2 chunks)
 constexpr int kPW = 4;             // P-exchange warps (one per TMEM lane quarter)
 constexpr int kEpi = 16;           // epilogue warps (four per TMEM lane quarter)
-constexpr int kRowsThreads = 32 * (3 + kPW + kEpi);
+constexpr int kBWarp = 3 + kPW + kEpi;  // the phase-B MMA issuer (last warp)
+constexpr int kRowsThreads = 32 * (4 + kPW + kEpi);
 constexpr uint32_t kXBytes = kTM * 128;   // 128 rows x 64 bf16
 constexpr uint32_t kBBytes = kNc * 128;   // 128 columns x 32 fp32
 constexpr uint32_t kA2Bytes = kTM * 128;  // 128 rows x 32 fp32 (k2 <= 32)
@@ -66,6 +72,7 @@ struct RowsParams {
   void *y;
   float arg;
   int softmax;         // fused row softmax over the full output width (see the epilogue)
+  int tma_y;           // epilogue stores through TMA (tm_y, 32 x 32 boxes) instead of st.global
   uint32_t off_sm;     // softmax: 2 x cs x 128 (max, sum) partials
   int bslot;  // K slot carrying the bias (P = 1 there, XF2p = bias * scale), -1: epilogue adds it
   uint32_t off_x, off_a2, off_wf, off_b, off_out, off_bar;
@@ -89,7 +96,7 @@ __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
 
 constexpr int kTr = 64;  // trace slots per CTA
 __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
-  if (p.trace && blockIdx.x < 8 && slot < kTr) {
+  if (p.trace && slot < kTr) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[blockIdx.x * kTr + slot] = t;
@@ -158,7 +165,7 @@ __device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta,
 template <int YDT, int ACT>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     k_tc_rows_reuse(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_wf,
-                    const __grid_constant__ CUtensorMap tm_xf2,
+                    const __grid_constant__ CUtensorMap tm_xf2, const __grid_constant__ CUtensorMap tm_y,
                     const RowsParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -169,7 +176,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   uint64_t *a2_full = d_empty + 2, *a2_free = a2_full + 2;
   uint64_t *p_full = a2_free + 2, *wf_full = p_full + 2;
   uint64_t *sm_full = wf_full + 1;  // softmax partials of every cluster CTA landed (2, by tile)
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(sm_full + 2);
+  uint64_t *p_free = sm_full + 2;   // the P warps read P[i & 1] out of TMEM (2, by tile)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(p_free + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int cs = p.cs;
   const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
@@ -187,6 +195,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       mbar_init(&a2_full[i], 1);   // local arm (expect_tx of the peers' bytes)
       mbar_init(&a2_free[i], cs);  // every cluster CTA's MMAs on this buffer done
       mbar_init(&p_full[i], 1);
+      mbar_init(&p_free[i], 1);
     }
     mbar_init(wf_full, 1);
     mbar_init(&sm_full[0], 1);
@@ -197,6 +206,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     tma_prefetch_desc(&tm_x);
     tma_prefetch_desc(&tm_wf);
     tma_prefetch_desc(&tm_xf2);
+    if (p.tma_y) tma_prefetch_desc(&tm_y);
   }
   if (warp == 2) tmem_alloc(tslot, 512);
   tc_fence_before();
@@ -210,6 +220,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   // (chained layers wait per row tile on the previous layer's flags instead, in the x producer)
   if (!p.wait_flags) griddep_wait();
   griddep_launch_dependents();
+  if (threadIdx.x == 0) rtrace(p, 1);
 
   const int n = p.nkb * 64;
   if (warp == 0) {
@@ -267,79 +278,89 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     __syncwarp();
   } else if (warp == 2) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- phase-A MMA issuer: P[i & 1] = x_seg . [wf_hi | wf_lo] ----------------
+    // (phase B runs on its own issuer warp, so A of the next tiles never waits behind the
+    // epilogue's D buffers, and B never waits for the next tile's x)
     if (lane == 0) {
       const uint32_t s0 = smem_u32(smem);
       const uint32_t wf_s = s0 + p.off_wf;
       const uint32_t idA = idesc_f32acc(kTM, (uint32_t)p.np, 1);
-      const uint32_t idB = idesc_f32acc(kTM, kNc, 2);
       mbar_wait(wf_full, 0);
       const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
-      int xs = 0, bs = 0, db = 0;
-      uint32_t xph = 0, bph = 0, dph = 0;
-      for (int i = 0; i <= ntl; ++i) {
-        if (i < ntl) {
-          // phase A of tile i into P[i & 1] (read out by the P warps before they armed
-          // a2_full of tile i-2, which phase B of tile i-2 below waited on)
-          const uint32_t pc = tbase + (uint32_t)((i & 1) * p.pcols);
-          int j = 0;
-          for (int seg = crank; seg < p.s; seg += cs, ++j) {
-            const uint32_t d = pc + (uint32_t)(j * p.np);
-            for (int kb = 0; kb < p.nkb; ++kb) {
-              mbar_wait(&x_full[xs], xph);
-              if (kb == 0 && j == 0) rtrace(p, 1 + 4 * min(i, 7));
-              tc_fence_after();
-              const uint32_t a = s0 + p.off_x + (uint32_t)xs * kXBytes;
-              const uint32_t b = wf_s + (uint32_t)(kb * p.np * 128);
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int i = 0; i < ntl; ++i) {
+        mbar_wait(&p_free[i & 1], ((uint32_t)(i >> 1) & 1u) ^ 1u);  // P warps read tile i-2
+        tc_fence_after();
+        const uint32_t pc = tbase + (uint32_t)((i & 1) * p.pcols);
+        int j = 0;
+        for (int seg = crank; seg < p.s; seg += cs, ++j) {
+          const uint32_t d = pc + (uint32_t)(j * p.np);
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(&x_full[xs], xph);
+            if (kb == 0 && j == 0) rtrace(p, 2 + 5 * min(i, 9));
+            if (kb == p.nkb - 1 && seg + cs >= p.s) rtrace(p, 3 + 5 * min(i, 9));
+            tc_fence_after();
+            const uint32_t a = s0 + p.off_x + (uint32_t)xs * kXBytes;
+            const uint32_t b = wf_s + (uint32_t)(kb * p.np * 128);
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16_ss(d, smem_desc(a + k * 32, 16, 1024, SL_SW128),
-                            smem_desc(b + k * 32, 16, 1024, SL_SW128), idA, (kb | k) != 0);
-              mma_commit(&x_empty[xs]);
-              if (++xs == p.xs) { xs = 0; xph ^= 1; }
-            }
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss(d, smem_desc(a + k * 32, 16, 1024, SL_SW128),
+                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idA, (kb | k) != 0);
+            mma_commit(&x_empty[xs]);
+            if (++xs == p.xs) { xs = 0; xph ^= 1; }
           }
-          mma_commit(&p_full[i & 1]);
         }
-        if (i >= 1) {
-          // phase B of tile i-1: every cluster CTA's P landed in A2[(i-1) & 1]
-          const int tb = i - 1, ab = tb & 1;
-          mbar_wait_cluster(&a2_full[ab], (uint32_t)(tb >> 1) & 1u);
-          rtrace(p, 2 + 4 * min(tb, 7));
+        mma_commit(&p_full[i & 1]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kBWarp) {
+    // ---------------- phase-B MMA issuer: D = A2 . XF2 chunk (tf32) ----------------
+    if (lane == 0) {
+      const uint32_t s0 = smem_u32(smem);
+      const uint32_t idB = idesc_f32acc(kTM, kNc, 2);
+      const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
+      int bs = 0, db = 0;
+      uint32_t bph = 0, dph = 0;
+      for (int tb = 0; tb < ntl; ++tb) {
+        // every cluster CTA's P landed in A2[tb & 1]
+        const int ab = tb & 1;
+        mbar_wait_cluster(&a2_full[ab], (uint32_t)(tb >> 1) & 1u);
+        rtrace(p, 4 + 5 * min(tb, 9));
+        tc_fence_after();
+        const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)ab * kA2Bytes;
+        int ci = 0;
+        if (p.softmax) {  // the whole tile's chunks live in TMEM together (row softmax)
+          mbar_wait(&d_empty[0], dph ^ 1);
           tc_fence_after();
-          const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)ab * kA2Bytes;
-          int ci = 0;
-          if (p.softmax) {  // the whole tile's chunks live in TMEM together (row softmax)
-            mbar_wait(&d_empty[0], dph ^ 1);
-            tc_fence_after();
-          }
-          for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
-            const int slot = b_res ? ci : bs;
-            mbar_wait(&b_full[slot], b_res ? 0u : bph);
-            if (!p.softmax) mbar_wait(&d_empty[db], dph ^ 1);
-            tc_fence_after();
-            const uint32_t d = p.softmax ? tbase + 128u + (uint32_t)(ci * kNc)
-                                         : tbase + kDCol + (uint32_t)(db * kNc);
-            const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
-            for (int k = 0; k < p.k2 / 8; ++k)
-              mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
-                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
-            if (!b_res) {
-              mma_commit(&b_empty[bs]);
-              if (++bs == kBS) { bs = 0; bph ^= 1; }
-            }
-            if (!p.softmax) {
-              mma_commit(&d_full[db]);
-              if (++db == 2) { db = 0; dph ^= 1; }
-            }
-          }
-          if (p.softmax) {
-            mma_commit(&d_full[0]);
-            dph ^= 1;
-          }
-          // this CTA's reads of A2[ab] are done when these MMAs complete: tell every writer
-          if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
         }
+        for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
+          const int slot = b_res ? ci : bs;
+          mbar_wait(&b_full[slot], b_res ? 0u : bph);
+          if (!p.softmax) mbar_wait(&d_empty[db], dph ^ 1);
+          tc_fence_after();
+          const uint32_t d = p.softmax ? tbase + 128u + (uint32_t)(ci * kNc)
+                                       : tbase + kDCol + (uint32_t)(db * kNc);
+          const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
+          for (int k = 0; k < p.k2 / 8; ++k)
+            mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
+                        smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
+          if (!b_res) {
+            mma_commit(&b_empty[bs]);
+            if (++bs == kBS) { bs = 0; bph ^= 1; }
+          }
+          if (!p.softmax) {
+            mma_commit(&d_full[db]);
+            if (++db == 2) { db = 0; dph ^= 1; }
+          }
+        }
+        if (p.softmax) {
+          mma_commit(&d_full[0]);
+          dph ^= 1;
+        }
+        // this CTA's reads of A2[ab] are done when these MMAs complete: tell every writer
+        if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
       }
     }
     __syncwarp();
@@ -358,8 +379,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       mbar_wait(&p_full[ab], (it >> 1) & 1);
       tc_fence_after();
       mbar_wait(&a2_free[ab], ((it >> 1) & 1) ^ 1);  // all readers of tile it-2 finished
-      const bool trp = false;
-      if (trp) rtrace(p, 44 + 4 * (int)it);
       const uint32_t a2b = a2_local + (uint32_t)ab * kA2Bytes;
       // own P values (rank padded to rp with zeros) into this CTA's A2[ab], one 16-byte store
       // per 4 K values
@@ -386,10 +405,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           }
         }
       }
-      if (trp) rtrace(p, 45 + 4 * (int)it);
       tc_fence_before();
       fence_proxy_async_smem();  // visible to the local MMAs and to the bulk-copy engine
       named_bar_sync(1, 32 * kPW);
+      if (warp == 3 && lane == 0) mbar_arrive(&p_free[ab]);  // P[ab] read out of TMEM
       if (warp == 3) {
         // lane r (1..cs-1) pushes this CTA's blocks into peer (crank + r) % cs, completion
         // counted on the peer's a2_full[ab]; lane 0 arms the local barrier for the peers' bytes
@@ -406,11 +425,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           const int own = ((p.s - crank + cs - 1) / cs) * (p.rp / 4);
           mbar_arrive_expect_tx(&a2_full[ab], (uint32_t)(p.s * p.rp / 4 - own) * 2048u);
         }
-        if (trp) rtrace(p, 46 + 4 * (int)it);
         __syncwarp();
       }
     }
-  } else {
+  } else if (warp < kBWarp) {
     // ---------------- epilogue ----------------
     if (p.softmax) {
       // Fused row softmax (the output layer of config 3): the tile's chunks of this CTA sit in
@@ -579,7 +597,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const int64_t row0 = (int64_t)t * kTM + 32 * sp;
       for (int c = crank; c < p.n_chunks; c += cs) {
         mbar_wait(&d_full[db], dph);
-        if (warp == 3 + kPW && c == crank) rtrace(p, 3 + 4 * (int)min(it, 7u));
+        if (warp == 3 + kPW && c == crank) rtrace(p, 5 + 5 * (int)min(it, 9u));
         tc_fence_after();
         const int col0 = c * kNc + 32 * qc;
         uint32_t v[32];
@@ -601,8 +619,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]), p.arg);
         }
-        // this lane's row (RB bytes) into the warp's swizzled staging box, then read back
-        // RPI rows per instruction (LPR lanes per row) and store whole rows with st.global.v4
+        // this lane's row (RB bytes) into the warp's swizzled staging box (the TMA SW64 / SW128
+        // pattern: 16-byte chunk ch of row r at ch ^ (r >> 1 & 3) / ch ^ (r & 7)), then either one
+        // TMA store of the 32 x 32 box or, read back RPI rows per instruction, st.global.v4
+        if (p.tma_y) {  // the staging box's previous TMA store has read it
+          if (lane == 0) bulk_wait_group_read<0>();
+          __syncwarp();
+        }
         const uint32_t rb = out_s + (uint32_t)lane * RB;
 #pragma unroll
         for (int ch = 0; ch < RB / 16; ++ch) {
@@ -618,6 +641,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           }
           const int sw = E == 2 ? ((lane >> 1) & SWM) : (lane & SWM);
           st_shared_v4(rb + ((uint32_t)(ch ^ sw) << 4), w0, w1, w2, w3);
+        }
+        if (p.tma_y) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm_y, smem + (out_s - s0), col0, (int32_t)row0);
+            bulk_commit_group();
+          }
+          continue;
         }
         __syncwarp();
         const int ch = lane % LPR;
@@ -642,12 +674,18 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       if (p.post_flags) {  // this warp's stores of tile t are done: release them to the next layer
         __syncwarp();
         if (lane == 0) {
+          if (p.tma_y) {
+            bulk_wait_group<0>();
+            fence_proxy_async_global();
+          }
           __threadfence();
           red_release_add(p.post_flags + t, 1u);
         }
       }
+      if (warp == 3 + kPW) rtrace(p, 6 + 5 * (int)min(it, 9u));
     }
-    if (warp == 3 + kPW) rtrace(p, 40);
+    if (p.tma_y && lane == 0) bulk_wait_group<0>();  // staging read + y written before exit
+    if (warp == 3 + kPW) rtrace(p, 60);
     }
   }
 
@@ -660,7 +698,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   }
 }
 
-using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
+using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
 
 template <int YDT>
 RowsFn pick_act(int act) {
@@ -874,6 +912,17 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   if (int rc = encode_tensor_map_2d(&tm_xf2, DT_F32, xf2p, (uint64_t)p.k2, (uint64_t)g.r_dim,
                                     (uint64_t)p.k2 * 4, 32, kNc, true))
     return rc;
+  // TMA stores of the epilogue's 32 x 32 boxes (DEEPTHIN_ROWS_TMA_Y=0: st.global.v4, A/B runs)
+  static const int want_tma_y = getenv("DEEPTHIN_ROWS_TMA_Y") ? atoi(getenv("DEEPTHIN_ROWS_TMA_Y")) : 1;
+  CUtensorMap tm_y;
+  memset(&tm_y, 0, sizeof(tm_y));
+  p.tma_y = (want_tma_y && !p.softmax) ? 1 : 0;
+  if (p.tma_y)
+    if (int rc = encode_tensor_map_2d_sw(&tm_y, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
+                                         (uint64_t)g.r_dim * (y_dtype == DT_BF16 ? 2 : 4), 32, 32,
+                                         y_dtype == DT_BF16 ? (int)CU_TENSOR_MAP_SWIZZLE_64B
+                                                            : (int)CU_TENSOR_MAP_SWIZZLE_128B))
+      return rc;
   RowsFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(act) : pick_act<DT_F32>(act);
   // the opt-in shared-memory size once per (device, kernel instance)
   if (int rc = set_smem_limit(reinterpret_cast<const void *>(fn), (int)smem_bytes)) return rc;
@@ -915,28 +964,26 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   cfg.gridDim = dim3((unsigned)(ncl * p.cs));
   static const bool tracing = DT_DBG_ENV("DEEPTHIN_ROWS_TRACE") != 0;
   if (tracing) {
-    DT_CUDA_CHECK(cudaMalloc(&p.trace, 8 * kTr * 8));
-    DT_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 8 * kTr * 8, st));
+    DT_CUDA_CHECK(cudaMalloc(&p.trace, (size_t)ncl * p.cs * kTr * 8));
+    DT_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, (size_t)ncl * p.cs * kTr * 8, st));
   }
   cudaEvent_t ev_b = nullptr, ev_a = nullptr;  // dt_profile_kernel_events
   profile_next(&ev_b, &ev_a, DT_PROF_ROWS);
   if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
-  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, p));
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, tm_y, p));
   if (ev_a) DT_CUDA_CHECK(cudaEventRecord(ev_a, st));
-  if (tracing) {
-    unsigned long long h[8 * kTr];
-    DT_CUDA_CHECK(cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (tracing) {  // every CTA's stamps, raw, to DEEPTHIN_ROWS_TRACE_FILE (scripts/rows_trace.py)
+    const int nb = ncl * p.cs;
+    std::vector<unsigned long long> h((size_t)nb * kTr);
+    DT_CUDA_CHECK(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
     DT_CUDA_CHECK(cudaStreamSynchronize(st));
     cudaFree(p.trace);
-    unsigned long long t0 = ~0ull;
-    for (int i = 0; i < 8 * kTr; ++i) if (h[i] && h[i] < t0) t0 = h[i];
-    fprintf(stderr, "rows trace: grid %d clusters x %d, tiles %d, chunks %d, s %d\n", ncl, p.cs,
-            p.n_tiles, p.n_chunks, p.s);
-    for (int b = 0; b < std::min(8, ncl * p.cs); ++b) {
-      fprintf(stderr, " cta %d:", b);
-      for (int i = 0; i < kTr; ++i)
-        if (h[b * kTr + i]) fprintf(stderr, " %d:%.2f", i, (h[b * kTr + i] - t0) * 1e-3);
-      fprintf(stderr, "\n");
+    const char *fn = getenv("DEEPTHIN_ROWS_TRACE_FILE");
+    if (FILE *f = fopen(fn ? fn : "rows_trace.bin", "wb")) {
+      const int hdr[6] = {nb, kTr, p.cs, p.n_tiles, p.n_chunks, p.s};
+      fwrite(hdr, sizeof(hdr), 1, f);
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
     }
   }
   if (int rc = check_launch("tc_rows_reuse")) return rc;
