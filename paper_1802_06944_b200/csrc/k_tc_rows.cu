@@ -61,7 +61,6 @@ constexpr int kRowsThreads = 32 * (4 + kPW + kEpi);
 constexpr uint32_t kXBytes = kTM * 128;   // 128 rows x 64 bf16
 constexpr uint32_t kBBytes = kNc * 128;   // 128 columns x 32 fp32
 constexpr uint32_t kA2Bytes = kTM * 128;  // 128 rows x 32 fp32 (k2 <= 32)
-constexpr uint32_t kDCol = 256;           // TMEM column of the first D buffer (P below it)
 // A2 descriptor strides (see a2n_off)
 constexpr uint32_t kA2Lbo = 2048, kA2Sbo = 128;
 
@@ -73,7 +72,11 @@ struct RowsParams {
   float arg;
   int softmax;         // fused row softmax over the full output width (see the epilogue)
   int tma_y;           // epilogue stores through TMA (tm_y, 32 x 32 boxes) instead of st.global
-  uint32_t off_sm;     // softmax: 2 x cs x 128 (max, sum) partials
+  int nd;              // D buffers in TMEM (2-3, 128 columns each, from column dcol0)
+  uint32_t dcol0;
+  int nstage;          // output staging boxes per epilogue warp (1-2, TMA stores in flight)
+  uint32_t off_sm;     // softmax: 2 x cs x 128 (max, sum) cluster partials
+  uint32_t off_red;    // softmax: [4][128] column-warp partials
   int bslot;  // K slot carrying the bias (P = 1 there, XF2p = bias * scale), -1: epilogue adds it
   uint32_t off_x, off_a2, off_wf, off_b, off_out, off_bar;
   unsigned long long *trace;  // DEEPTHIN_ROWS_TRACE: globaltimer stamps of cluster 0
@@ -172,8 +175,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *x_full = bars, *x_empty = bars + kXSMax;
   uint64_t *b_full = bars + 2 * kXSMax, *b_empty = b_full + kBS;
-  uint64_t *d_full = b_empty + kBS, *d_empty = d_full + 2;
-  uint64_t *a2_full = d_empty + 2, *a2_free = a2_full + 2;
+  uint64_t *d_full = b_empty + kBS, *d_empty = d_full + 4;
+  uint64_t *a2_full = d_empty + 4, *a2_free = a2_full + 2;
   uint64_t *p_full = a2_free + 2, *wf_full = p_full + 2;
   uint64_t *sm_full = wf_full + 1;  // softmax partials of every cluster CTA landed (2, by tile)
   uint64_t *p_free = sm_full + 2;   // the P warps read P[i & 1] out of TMEM (2, by tile)
@@ -189,9 +192,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.xs; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < kBS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&d_full[i], 1);
       mbar_init(&d_empty[i], kEpi);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&a2_full[i], 1);   // local arm (expect_tx of the peers' bytes)
       mbar_init(&a2_free[i], cs);  // every cluster CTA's MMAs on this buffer done
       mbar_init(&p_full[i], 1);
@@ -268,6 +273,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         int st = 0;
         uint32_t ph = 0;
         for (int t = cid; t < p.n_tiles; t += ncl)
+          for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass)
           for (int c = crank; c < p.n_chunks; c += cs) {
             mbar_wait(&b_empty[st], ph ^ 1);
             mbar_arrive_expect_tx(&b_full[st], kBBytes);
@@ -330,34 +336,27 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         rtrace(p, 4 + 5 * min(tb, 9));
         tc_fence_after();
         const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)ab * kA2Bytes;
-        int ci = 0;
-        if (p.softmax) {  // the whole tile's chunks live in TMEM together (row softmax)
-          mbar_wait(&d_empty[0], dph ^ 1);
-          tc_fence_after();
-        }
-        for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
-          const int slot = b_res ? ci : bs;
-          mbar_wait(&b_full[slot], b_res ? 0u : bph);
-          if (!p.softmax) mbar_wait(&d_empty[db], dph ^ 1);
-          tc_fence_after();
-          const uint32_t d = p.softmax ? tbase + 128u + (uint32_t)(ci * kNc)
-                                       : tbase + kDCol + (uint32_t)(db * kNc);
-          const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
-          for (int k = 0; k < p.k2 / 8; ++k)
-            mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
-                        smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
-          if (!b_res) {
-            mma_commit(&b_empty[bs]);
-            if (++bs == kBS) { bs = 0; bph ^= 1; }
-          }
-          if (!p.softmax) {
+        // softmax: two passes over the chunks (statistics, then normalised stores), the tf32
+        // MMA recomputed from the A2 tile still resident — no logits round trip through HBM
+        for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass) {
+          int ci = 0;
+          for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
+            const int slot = b_res ? ci : bs;
+            mbar_wait(&b_full[slot], b_res ? 0u : bph);
+            mbar_wait(&d_empty[db], dph ^ 1);
+            tc_fence_after();
+            const uint32_t d = tbase + p.dcol0 + (uint32_t)(db * kNc);
+            const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
+            for (int k = 0; k < p.k2 / 8; ++k)
+              mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
+                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
+            if (!b_res) {
+              mma_commit(&b_empty[bs]);
+              if (++bs == kBS) { bs = 0; bph ^= 1; }
+            }
             mma_commit(&d_full[db]);
-            if (++db == 2) { db = 0; dph ^= 1; }
+            if (++db == p.nd) { db = 0; dph ^= 1; }
           }
-        }
-        if (p.softmax) {
-          mma_commit(&d_full[0]);
-          dph ^= 1;
         }
         // this CTA's reads of A2[ab] are done when these MMAs complete: tell every writer
         if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
@@ -431,60 +430,53 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   } else if (warp < kBWarp) {
     // ---------------- epilogue ----------------
     if (p.softmax) {
-      // Fused row softmax (the output layer of config 3): the tile's chunks of this CTA sit in
-      // TMEM together. Pass 1: per-row (max, sum exp) over this warp's 32 columns of each chunk,
-      // combined over the CTA's four column warps through shared memory, then over the cluster:
-      // each CTA bulk-copies its 128 (max, sum) pairs into every peer (completion counted on the
-      // peer's sm_full), and every CTA combines the cs partials in rank order. Pass 2: reload,
-      // p = exp(z - M) / L, bf16 out. Fixed reduction order: deterministic.
+      // Fused row softmax (the output layer of config 3), two passes over the tile's chunks with
+      // the tf32 contraction recomputed in between (the B issuer runs it twice):
+      //   pass 1: per row, the online (max, sum 2^((z - max) log2 e)) over this warp's 32
+      //           columns of every chunk of this CTA, combined over the four column warps in
+      //           shared memory, then over the cluster: each CTA bulk-copies its 128 partials
+      //           into every peer (completion on the peer's sm_full) and every CTA combines the
+      //           cs partials in rank order (fixed order: deterministic);
+      //   pass 2: p = 2^((z - M) log2 e) / L, staged and TMA-stored like the logits path.
+      // The logits never leave the SM (one HBM write of p instead of z written, read, rewritten).
       const int sp = warp & 3, e = warp - 3 - kPW, qc = e / 4, row = 32 * sp + lane;
       const uint32_t s0 = smem_u32(smem);
       const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
       constexpr int E = YDT == DT_BF16 ? 2 : 4;
-      constexpr int RB = 32 * E, LPR = RB / 16, RPI = 32 / LPR, SWM = RB / 16 - 1;
+      constexpr int RB = 32 * E, SWM = RB / 16 - 1;
       const uint32_t out_s = s0 + p.off_out + (uint32_t)e * (32u * RB);
-      float2 *red = reinterpret_cast<float2 *>(smem + p.off_out + kEpi * 32u * RB);  // [4][128]
+      float2 *red = reinterpret_cast<float2 *>(smem + p.off_red);  // [4][128]
       const float l2e = 1.4426950408889634f;
-      uint32_t it = 0;
+      int db = 0;
+      uint32_t dph = 0, it = 0;
       for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
         const int sb = (int)(it & 1);
         float2 *part = reinterpret_cast<float2 *>(smem + p.off_sm) + sb * cs * kTM;  // [cs][128]
-        mbar_wait(&d_full[0], it & 1);
-        tc_fence_after();
-        // pass 1: per chunk e = 2^((z - m_c) log2 e) written back over z in TMEM, with the
-        // chunk's (m_c, l_c); one MUFU op per element
-        float mc[3] = {-INFINITY, -INFINITY, -INFINITY}, lc[3] = {0.f, 0.f, 0.f};
-        int ci = 0;
-        for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
-          const int col0 = c * kNc + 32 * qc;
-          const uint32_t ta = tbase + lane_t + 128u + (uint32_t)(ci * kNc + 32 * qc);
+        float m = -INFINITY, l = 0.f;
+        for (int c = crank; c < p.n_chunks; c += cs) {
+          mbar_wait(&d_full[db], dph);
+          tc_fence_after();
           uint32_t v[32];
-          tmem_ld_32x32b_x32(ta, v);
+          tmem_ld_32x32b_x32(tbase + lane_t + p.dcol0 + (uint32_t)(db * kNc + 32 * qc), v);
           tmem_ld_wait();
-          const int nv = min(32, p.r_dim - col0);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[db]);
+          if (++db == p.nd) { db = 0; dph ^= 1; }
+          const int nv = min(32, p.r_dim - (c * kNc + 32 * qc));
+          if (nv <= 0) continue;
           float cm = -INFINITY;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (i < nv) cm = fmaxf(cm, __uint_as_float(v[i]));
+          const float nm = fmaxf(m, cm);
           float cl = 0.f;
-          if (nv > 0) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float ev = i < nv ? ex2_approx((__uint_as_float(v[i]) - cm) * l2e) : 0.f;
-              cl += ev;
-              v[i] = __float_as_uint(ev);
-            }
-            tmem_st_32x32b_x32(ta, v);
-          }
-          if (ci < 3) { mc[ci] = cm; lc[ci] = cl; }
+          for (int i = 0; i < 32; ++i)
+            if (i < nv) cl += ex2_approx((__uint_as_float(v[i]) - nm) * l2e);
+          l = (m > -INFINITY ? l * ex2_approx((m - nm) * l2e) : 0.f) + cl;
+          m = nm;
         }
-        tmem_st_wait();
-        float m = -INFINITY, l = 0.f;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) m = fmaxf(m, mc[k]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          if (mc[k] > -INFINITY) l += lc[k] * ex2_approx((mc[k] - m) * l2e);
         red[qc * kTM + row] = make_float2(m, l);
         named_bar_sync(2, 32 * kEpi);
         if (qc == 0) {  // the CTA's partial for this row, column warps in order
@@ -511,7 +503,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           if (lane == 0) mbar_arrive_expect_tx(&sm_full[sb], (uint32_t)(cs - 1) * kTM * 8u);
           __syncwarp();
         }
-        mbar_wait_cluster(&sm_full[sb], (it >> 1) & 1);
+        if (cs > 1) mbar_wait_cluster(&sm_full[sb], (it >> 1) & 1);
         float M = -INFINITY, L = 0.f;
         for (int k = 0; k < cs; ++k) {
           const float2 q = part[k * kTM + row];
@@ -521,23 +513,26 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             M = nm;
           }
         }
-        const float inv = 1.f / L;
-        float fc[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) fc[k] = mc[k] > -INFINITY ? ex2_approx((mc[k] - M) * l2e) * inv : 0.f;
-        // pass 2: p = e * 2^((m_c - M) log2 e) / L
+        const float inv = 1.f / L;  // the difference first below: exact near the max
+        // pass 2: the recomputed chunks, normalised, through the staging box and TMA stores
         const int64_t row0 = (int64_t)t * kTM + 32 * sp;
-        ci = 0;
-        for (int c = crank; c < p.n_chunks; c += cs, ++ci) {
-          const int col0 = c * kNc + 32 * qc;
+        for (int c = crank; c < p.n_chunks; c += cs) {
+          mbar_wait(&d_full[db], dph);
+          tc_fence_after();
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + lane_t + 128u + (uint32_t)(ci * kNc + 32 * qc), v);
+          tmem_ld_32x32b_x32(tbase + lane_t + p.dcol0 + (uint32_t)(db * kNc + 32 * qc), v);
           tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[db]);
+          if (++db == p.nd) { db = 0; dph ^= 1; }
+          const int col0 = c * kNc + 32 * qc;
           if (col0 >= p.r_dim) continue;
-          const float f = fc[ci < 3 ? ci : 2];
           float o[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f;
+          for (int i = 0; i < 32; ++i) o[i] = ex2_approx((__uint_as_float(v[i]) - M) * l2e) * inv;
+          if (lane == 0) bulk_wait_group_read<0>();
+          __syncwarp();
           const uint32_t rb = out_s + (uint32_t)lane * RB;
 #pragma unroll
           for (int ch = 0; ch < RB / 16; ++ch) {
@@ -554,30 +549,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             const int sw = E == 2 ? ((lane >> 1) & SWM) : (lane & SWM);
             st_shared_v4(rb + ((uint32_t)(ch ^ sw) << 4), w0, w1, w2, w3);
           }
+          fence_proxy_async_smem();
           __syncwarp();
-          const int chl = lane % LPR;
-          const int cb = col0 + chl * (16 / E);
-          uint32_t w[RPI == 8 ? 4 : 8][4];
-#pragma unroll
-          for (int i = 0; i < 32 / RPI; ++i) {
-            const int r = RPI * i + lane / LPR;
-            const int sw = E == 2 ? ((r >> 1) & SWM) : (r & SWM);
-            ld_shared_v4(out_s + (uint32_t)r * RB + ((uint32_t)(chl ^ sw) << 4), w[i][0], w[i][1],
-                         w[i][2], w[i][3]);
+          if (lane == 0) {
+            tma_store_2d(&tm_y, smem + (out_s - s0), col0, (int32_t)row0);
+            bulk_commit_group();
           }
-#pragma unroll
-          for (int i = 0; i < 32 / RPI; ++i) {
-            const int r = RPI * i + lane / LPR;
-            if (row0 + r < p.batch && cb < p.r_dim)
-              st_global_v4(reinterpret_cast<uint8_t *>(p.y) + ((row0 + r) * p.r_dim + cb) * E, w[i][0],
-                           w[i][1], w[i][2], w[i][3]);
-          }
-          __syncwarp();
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&d_empty[0]);
       }
+      if (lane == 0) bulk_wait_group<0>();
     } else {
     // 16 warps: four per TMEM lane quarter, each owning 32 of the chunk's 128 columns
     const int sp = warp & 3;           // TMEM lane quarter this warp may access
@@ -590,8 +570,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     constexpr int LPR = RB / 16;       // lanes per row when storing (4 or 8)
     constexpr int RPI = 32 / LPR;      // rows per store instruction (8 or 4)
     constexpr int SWM = RB / 16 - 1;   // swizzle mask over the row's 16-byte chunks
-    const uint32_t out_s = s0 + p.off_out + (uint32_t)e * (32u * RB);
-    int db = 0;
+    const uint32_t out_s0 = s0 + p.off_out + (uint32_t)(e * p.nstage) * (32u * RB);
+    int db = 0, sb = 0;
     uint32_t dph = 0, it = 0;
     for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
       const int64_t row0 = (int64_t)t * kTM + 32 * sp;
@@ -601,12 +581,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tc_fence_after();
         const int col0 = c * kNc + 32 * qc;
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + lane_t + kDCol + (uint32_t)(db * kNc + 32 * qc), v);
+        tmem_ld_32x32b_x32(tbase + lane_t + p.dcol0 + (uint32_t)(db * kNc + 32 * qc), v);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[db]);
-        if (++db == 2) { db = 0; dph ^= 1; }
+        if (++db == p.nd) { db = 0; dph ^= 1; }
         if (col0 >= p.r_dim) continue;
         float o[32];
         if (p.bias && p.bslot < 0) {
@@ -622,8 +602,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // this lane's row (RB bytes) into the warp's swizzled staging box (the TMA SW64 / SW128
         // pattern: 16-byte chunk ch of row r at ch ^ (r >> 1 & 3) / ch ^ (r & 7)), then either one
         // TMA store of the 32 x 32 box or, read back RPI rows per instruction, st.global.v4
+        const uint32_t out_s = out_s0 + (uint32_t)sb * (32u * RB);
+        if (p.nstage == 2) sb ^= 1;
         if (p.tma_y) {  // the staging box's previous TMA store has read it
-          if (lane == 0) bulk_wait_group_read<0>();
+          if (lane == 0) {
+            if (p.nstage == 2) bulk_wait_group_read<1>(); else bulk_wait_group_read<0>();
+          }
           __syncwarp();
         }
         const uint32_t rb = out_s + (uint32_t)lane * RB;
@@ -864,17 +848,13 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   // a zero K slot for the bias: the rank padding of segment 0, else an all-zero pad chunk
   p.bslot = !bias ? -1 : (g.rank < p.rp ? (int)g.rank : (p.k2 > g.s * p.rp ? (int)(g.s * p.rp) : -1));
   p.pcols = (int)((g.s / p.cs) * p.np);
-  // row softmax fused into the epilogue when every CTA's chunks of a tile fit in TMEM next to
-  // P (<= 3 chunks, 2 * pcols <= 128) and the bias rides in the contraction; else a post pass
+  // row softmax fused into the epilogue (two passes, the contraction recomputed: see the
+  // kernel) when the bias rides in the contraction; DEEPTHIN_ROWS_SOFTMAX=0: logits, then the
+  // separate register softmax kernel (A/B runs)
   const bool want_sm = act == DT_ACT_SOFTMAX;
-  // Opt-in (DEEPTHIN_ROWS_SOFTMAX=1, read per call): with every chunk of a tile held in TMEM
-  // there is no D double buffering, so tile t+1's MMAs wait for tile t's whole two-pass
-  // epilogue and its cluster exchange (~9.5 us per tile at config 3's output layer vs ~4 us
-  // for logits + the separate register softmax kernel) — measured slower end to end.
-  const char *fenv = getenv("DEEPTHIN_ROWS_SOFTMAX");
-  const int fuse_sm = fenv ? atoi(fenv) : 0;
-  p.softmax = (want_sm && fuse_sm && (p.n_chunks + p.cs - 1) / p.cs <= 3 && 2 * p.pcols <= 128 &&
-               (!bias || p.bslot >= 0)) ? 1 : 0;
+  const char *fenv = getenv("DEEPTHIN_ROWS_SOFTMAX");  // read per call (tests flip it)
+  const int fuse_sm = fenv ? atoi(fenv) : 1;
+  p.softmax = (want_sm && fuse_sm && (!bias || p.bslot >= 0)) ? 1 : 0;
   if (want_sm) act = DT_ACT_IDENTITY;
   // bf16 sigmoid runs as 1/2 + tanh(z/2)/2: the contraction (and bias) pre-scaled by 1/2
   const float scale = (y_dtype == DT_BF16 && act == DT_ACT_SIGMOID) ? 0.5f : 1.f;
@@ -884,15 +864,25 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.off_wf = 2 * kA2Bytes;
   p.off_b = (p.off_wf + wf_bytes + 1023) & ~1023u;
   p.off_out = p.off_b + kBS * kBBytes;
-  p.off_x = p.off_out + kEpi * 32u * 32u * (uint32_t)(y_dtype == DT_BF16 ? 2 : 4);
+  // TMEM: P double buffer in columns [0, 2 pcols), nd D buffers of 128 columns at the top;
+  // output staging: nstage boxes per epilogue warp (DEEPTHIN_ROWS_ND / _STG: A/B runs)
+  static const int want_nd = getenv("DEEPTHIN_ROWS_ND") ? atoi(getenv("DEEPTHIN_ROWS_ND")) : 2;
+  static const int want_stg = getenv("DEEPTHIN_ROWS_STG") ? atoi(getenv("DEEPTHIN_ROWS_STG")) : 1;
+  p.nd = std::max(2, std::min(want_nd, (int)(512 - (2 * p.pcols + 127) / 128 * 128) / (int)kNc));
+  p.dcol0 = 512u - (uint32_t)p.nd * kNc;
+  p.nstage = (want_stg == 2 && !p.softmax) ? 2 : 1;
+  p.off_x = p.off_out + (uint32_t)p.nstage * kEpi * 32u * 32u * (uint32_t)(y_dtype == DT_BF16 ? 2 : 4);
   if (p.softmax) {  // [4][128] column-warp partials, then 2 x cs x 128 cluster partials
+    p.off_red = p.off_x;
     p.off_x += 4 * kTM * 8;
     p.off_sm = p.off_x;
     p.off_x += 2u * (uint32_t)p.cs * kTM * 8;
     p.off_x = (p.off_x + 1023) & ~1023u;
   }
   constexpr uint32_t kSmemMax = 227 * 1024, kTail = 512 + 1024;
-  p.xs = (int)std::min<uint32_t>(kXSMax, (kSmemMax - kTail - p.off_x) / kXBytes);
+  static const int want_xs = getenv("DEEPTHIN_ROWS_XS") ? atoi(getenv("DEEPTHIN_ROWS_XS")) : kXSMax;
+  p.xs = (int)std::min<uint32_t>((uint32_t)std::max(2, std::min(want_xs, kXSMax)),
+                                 (kSmemMax - kTail - p.off_x) / kXBytes);
   p.off_bar = p.off_x + (uint32_t)p.xs * kXBytes;
   const uint32_t smem_bytes = p.off_bar + kTail;
 
@@ -916,7 +906,7 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   static const int want_tma_y = getenv("DEEPTHIN_ROWS_TMA_Y") ? atoi(getenv("DEEPTHIN_ROWS_TMA_Y")) : 1;
   CUtensorMap tm_y;
   memset(&tm_y, 0, sizeof(tm_y));
-  p.tma_y = (want_tma_y && !p.softmax) ? 1 : 0;
+  p.tma_y = (want_tma_y || p.softmax) ? 1 : 0;  // the softmax epilogue stores through TMA
   if (p.tma_y)
     if (int rc = encode_tensor_map_2d_sw(&tm_y, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
                                          (uint64_t)g.r_dim * (y_dtype == DT_BF16 ? 2 : 4), 32, 32,

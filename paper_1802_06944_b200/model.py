@@ -178,8 +178,8 @@ class DeviceModel:
     def _fused_runs(self, out_dtype):
         """{first: last} of the layer runs dt_chain_forward takes: >= 2 consecutive reuse layers
         on the row-tile kernel sharing n, rank and q/n, one elementwise activation on all but the
-        last, the last identity or softmax (bf16 output, so the network's final layer only when
-        out_dtype is bf16)."""
+        last, the last identity (bf16 output, so the network's final layer only when out_dtype is
+        bf16)."""
         key = ("runs", out_dtype)
         cache = self.__dict__.setdefault("_run_cache", {})
         if key in cache:
@@ -200,7 +200,9 @@ class DeviceModel:
                 hid = self.codes[i:j]
                 if not (all(c == hid[0] for c in hid) and hid[0] not in (sm,)):
                     break
-                ends_ok = self.codes[j] in (ident, sm) and (j < last or out_dtype == torch.bfloat16)
+                # an identity head only: a softmax head runs on the row-tile kernel, whose fused
+                # epilogue normalises the fp32 logits (the chain would store bf16 logits first)
+                ends_ok = self.codes[j] == ident and (j < last or out_dtype == torch.bfloat16)
                 plans = (_lib.Plan * (j - i + 1))(*[_lib.plan_struct(f.plan)
                                                    for f in self.factors[i:j + 1]])
                 if ends_ok and all(rows_ok(k) for k in range(i, j + 1)) and \

@@ -292,13 +292,15 @@ def test_fused_layer_chain_matches_layer_by_layer(rows):
     """dt_chain_forward (k_tc_chain.cu): the config-3 hidden layers + output layer as ONE kernel
     with the activations kept in shared memory give the bits of the layer-by-layer row-tile
     kernels (same per-layer arithmetic and summation order), with bf16 output (the chain runs
-    through the softmax head) and fp32 output (the last layer runs on its own)."""
+    through the identity head) and fp32 output (the last layer runs on its own). A softmax head
+    is never chained: the row-tile kernel fuses it on the fp32 logits."""
     model = mi.deserialize(mi.serialize(config3_like(layers=5)))
-    acts = ["sigmoid"] * 5 + ["softmax"]
+    acts = ["sigmoid"] * 5 + ["identity"]
     dm = model.to_device(acts, mma="bf16")
     x = torch.randn(rows, 440, device="cuda").to(torch.bfloat16)
     assert dm._fused_runs(torch.bfloat16) == {1: 5}
     assert dm._fused_runs(torch.float32) == {}  # layers 1-4: the run would end on a sigmoid
+    assert model.to_device(["sigmoid"] * 5 + ["softmax"], mma="bf16")._fused_runs(torch.bfloat16) == {}
     for out in (torch.bfloat16, torch.float32):
         dm.fuse = False
         want = dm.forward(x, out_dtype=out).clone()
