@@ -67,9 +67,6 @@ constexpr uint32_t kA2Lbo = 2048, kA2Sbo = 128;
 struct RowsParams {
   int64_t batch;
   int r_dim, n_tiles, s, nkb, np, rank, rp, k2, n_chunks, cs, xs, pcols;
-  // work units: n_full whole 128-row tiles, then the rest of the batch in pieces of `piece` rows
-  // (a multiple of 32, <= 128) so that the last round gives every cluster an equal short share
-  int n_units, n_full, piece;
   const float *bias;
   void *y;
   float arg;
@@ -99,12 +96,6 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
 __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-// first batch row / row count of work unit u
-__device__ __forceinline__ int unit_row0(const RowsParams &p, int u) {
-  return u < p.n_full ? u * kTM : p.n_full * kTM + (u - p.n_full) * p.piece;
-}
-__device__ __forceinline__ int unit_rows(const RowsParams &p, int u) { return u < p.n_full ? kTM : p.piece; }
 
 constexpr int kTr = 64;  // trace slots per CTA
 __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
@@ -176,9 +167,9 @@ __device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta,
 // before phase B of tile i (P double-buffered in TMEM), so the exchange latency is hidden.
 template <int YDT, int ACT>
 __global__ void __launch_bounds__(kRowsThreads, 1)
-    k_tc_rows_reuse(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_xp,
-                    const __grid_constant__ CUtensorMap tm_wf, const __grid_constant__ CUtensorMap tm_xf2,
-                    const __grid_constant__ CUtensorMap tm_y, const RowsParams p) {
+    k_tc_rows_reuse(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_wf,
+                    const __grid_constant__ CUtensorMap tm_xf2, const __grid_constant__ CUtensorMap tm_y,
+                    const RowsParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
@@ -218,7 +209,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_x);
-    if (p.n_units > p.n_full) tma_prefetch_desc(&tm_xp);
     tma_prefetch_desc(&tm_wf);
     tma_prefetch_desc(&tm_xf2);
     if (p.tma_y) tma_prefetch_desc(&tm_y);
@@ -249,13 +239,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tma_load_2d(wf_s + kb * p.np * 128, &tm_wf, wf_full, kb * 64, 0);
       int st = 0;
       uint32_t ph = 0;
-      for (int t = cid; t < p.n_units; t += ncl) {
-        // a short unit of the last round loads only its own `piece` rows (the MMAs still run
-        // M = 128 over the stage: rows are independent, the rest is never stored)
-        const bool whole = t < p.n_full;
-        const CUtensorMap *tm = whole ? &tm_x : &tm_xp;
-        const uint32_t xbytes = whole ? kXBytes : (uint32_t)p.piece * 128u;
-        const int row0 = unit_row0(p, t);
+      for (int t = cid; t < p.n_tiles; t += ncl) {
         if (p.wait_flags) {  // rows of tile t written (and released) by the previous layer
           uint32_t spins = 0;
           while (ld_acquire_u32(p.wait_flags + t) < p.wait_target) {
@@ -269,8 +253,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         for (int seg = crank; seg < p.s; seg += cs)
           for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(&x_empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&x_full[st], xbytes);
-            tma_load_2d(smem + p.off_x + st * kXBytes, tm, &x_full[st], seg * n + kb * 64, row0);
+            mbar_arrive_expect_tx(&x_full[st], kXBytes);
+            tma_load_2d(smem + p.off_x + st * kXBytes, &tm_x, &x_full[st], seg * n + kb * 64, t * kTM);
             if (++st == p.xs) { st = 0; ph ^= 1; }
           }
       }
@@ -288,7 +272,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       } else {
         int st = 0;
         uint32_t ph = 0;
-        for (int t = cid; t < p.n_units; t += ncl)
+        for (int t = cid; t < p.n_tiles; t += ncl)
           for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass)
           for (int c = crank; c < p.n_chunks; c += cs) {
             mbar_wait(&b_empty[st], ph ^ 1);
@@ -308,7 +292,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const uint32_t wf_s = s0 + p.off_wf;
       const uint32_t idA = idesc_f32acc(kTM, (uint32_t)p.np, 1);
       mbar_wait(wf_full, 0);
-      const int ntl = cid < p.n_units ? (p.n_units - cid + ncl - 1) / ncl : 0;
+      const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
       int xs = 0;
       uint32_t xph = 0;
       for (int i = 0; i < ntl; ++i) {
@@ -342,7 +326,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     if (lane == 0) {
       const uint32_t s0 = smem_u32(smem);
       const uint32_t idB = idesc_f32acc(kTM, kNc, 2);
-      const int ntl = cid < p.n_units ? (p.n_units - cid + ncl - 1) / ncl : 0;
+      const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
       int bs = 0, db = 0;
       uint32_t bph = 0, dph = 0;
       for (int tb = 0; tb < ntl; ++tb) {
@@ -389,7 +373,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         st_shared_v4(a2_local + (uint32_t)b * kA2Bytes + a2n_off(row, kk),
                      kk == p.bslot ? 0x3f800000u : 0u, 0u, 0u, 0u);
     uint32_t it = 0;
-    for (int t = cid; t < p.n_units; t += ncl, ++it) {
+    for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
       const int ab = (int)(it & 1);
       mbar_wait(&p_full[ab], (it >> 1) & 1);
       tc_fence_after();
@@ -465,9 +449,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const float l2e = 1.4426950408889634f;
       int db = 0;
       uint32_t dph = 0, it = 0;
-      for (int t = cid; t < p.n_units; t += ncl, ++it) {
+      for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
         const int sb = (int)(it & 1);
-        const bool live = 32 * sp < unit_rows(p, t);  // this warp's rows belong to the unit
         float2 *part = reinterpret_cast<float2 *>(smem + p.off_sm) + sb * cs * kTM;  // [cs][128]
         float m = -INFINITY, l = 0.f;
         for (int c = crank; c < p.n_chunks; c += cs) {
@@ -532,7 +515,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         const float inv = 1.f / L;  // the difference first below: exact near the max
         // pass 2: the recomputed chunks, normalised, through the staging box and TMA stores
-        const int64_t row0 = (int64_t)unit_row0(p, t) + 32 * sp;
+        const int64_t row0 = (int64_t)t * kTM + 32 * sp;
         for (int c = crank; c < p.n_chunks; c += cs) {
           mbar_wait(&d_full[db], dph);
           tc_fence_after();
@@ -544,7 +527,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           if (lane == 0) mbar_arrive(&d_empty[db]);
           if (++db == p.nd) { db = 0; dph ^= 1; }
           const int col0 = c * kNc + 32 * qc;
-          if (col0 >= p.r_dim || !live) continue;
+          if (col0 >= p.r_dim) continue;
           float o[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = ex2_approx((__uint_as_float(v[i]) - M) * l2e) * inv;
@@ -590,9 +573,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const uint32_t out_s0 = s0 + p.off_out + (uint32_t)(e * p.nstage) * (32u * RB);
     int db = 0, sb = 0;
     uint32_t dph = 0, it = 0;
-    for (int t = cid; t < p.n_units; t += ncl, ++it) {
-      const int64_t row0 = (int64_t)unit_row0(p, t) + 32 * sp;
-      const bool live = 32 * sp < unit_rows(p, t);  // this warp's rows belong to the unit
+    for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
+      const int64_t row0 = (int64_t)t * kTM + 32 * sp;
       for (int c = crank; c < p.n_chunks; c += cs) {
         mbar_wait(&d_full[db], dph);
         if (warp == 3 + kPW && c == crank) rtrace(p, 5 + 5 * (int)min(it, 9u));
@@ -605,7 +587,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[db]);
         if (++db == p.nd) { db = 0; dph ^= 1; }
-        if (col0 >= p.r_dim || !live) continue;
+        if (col0 >= p.r_dim) continue;
         float o[32];
         if (p.bias && p.bslot < 0) {
           constexpr float bsc = (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) ? 0.5f : 1.f;
@@ -700,7 +682,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   }
 }
 
-using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
+using RowsFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, RowsParams);
 
 template <int YDT>
 RowsFn pick_act(int act) {
