@@ -43,12 +43,14 @@
 
 #include "act.cuh"
 #include "dt_internal.h"
+#include "rows_common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace dt {
 namespace {
 
 using namespace ptx;
+using namespace rowsdev;
 
 constexpr int kTM = 128;           // batch rows per tile (UMMA M = TMEM lanes)
 constexpr int kNc = 128;           // output columns per D chunk (UMMA N of phase B)
@@ -88,15 +90,6 @@ struct RowsParams {
   unsigned *post_flags;
 };
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 constexpr int kTr = 64;  // trace slots per CTA
 __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
   if (p.trace && slot < kTr) {
@@ -106,41 +99,6 @@ __device__ __forceinline__ void rtrace(const RowsParams &p, int slot) {
   }
 }
 
-// bf16 outputs: one MUFU op per element (act.cuh tanh_approx); the launcher pre-scales XF2p and
-// the bias by 1/2 for the bf16 sigmoid, so z here is already z/2
-template <int YDT, int ACT>
-__device__ __forceinline__ float act_out(float z, float arg) {
-  if constexpr (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) return fmaf(0.5f, tanh_approx(z), 0.5f);
-  return act_out_bf16<YDT, ACT>(z, arg);
-}
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t *>(&h);
-}
-__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c,
-                                             uint32_t &d) {
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
-               : "r"(addr)
-               : "memory");
-}
-__device__ __forceinline__ void st_global_v4(void *ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d)
-               : "memory");
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
-                                             uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-               "r"(d)
-               : "memory");
-}
 // No-swizzle K-major layout of the 128-row x k2 tf32 A operand: core matrices of 8 rows x 16 B
 // (4 K values); M-adjacent core matrices 128 B apart (SBO), K-adjacent 2 KB apart (LBO) — so
 // every 4-K column block of all 128 rows is one contiguous 2 KB run (bulk-copyable).
@@ -891,6 +849,19 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   // operands derived once per factor pair (dt_rows_prepare) or here, per call
   if (!prepared)
     if (int rc = tc_rows_prepare(g, wf, xf, bias, act, y_dtype, ws, st)) return rc;
+
+  // The slab kernel (k_tc_slab.cu: no clusters, every SM a contiguous slab of rows) takes the
+  // layer when s is a power of two and no per-tile chaining was requested
+  // (DEEPTHIN_ROWS_SLAB=0: the clustered row-tile kernel below, A/B runs and tests)
+  {
+    const char *senv = getenv("DEEPTHIN_ROWS_SLAB");  // read per call (tests flip it)
+    if ((senv ? atoi(senv) != 0 : false) && !p.wait_flags && !p.post_flags && tc_slab_ok(g, batch)) {
+      if (int rc = tc_slab_forward(g, batch, x, wf16, xf2p, bias, p.bslot, act, act_arg, p.softmax, y,
+                                   y_dtype, st))
+        return rc;
+      return want_sm && !p.softmax ? launch_row_softmax(batch, g.r_dim, y, y_dtype, st) : DT_OK;
+    }
+  }
 
   CUtensorMap tm_x, tm_wf, tm_xf2;
   if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(x), (uint64_t)g.q,

@@ -32,9 +32,30 @@ def main():
     os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
     for _ in range(3):
         D.layer_forward(x, fp, b, os.environ.get("ACT", "sigmoid"), mma="bf16",
-                        out_dtype=torch.bfloat16)
+                        out_dtype=torch.float32 if os.environ.get("OUT") == "f32" else torch.bfloat16)
     torch.cuda.synchronize()
     summarise(out)
+
+
+def summarise_slab(us, nb, slab, n_chunks, s):
+    """Slab kernel (k_tc_slab.cu strace): 0 set-up, 1 after griddepcontrol.wait, 2 first x block
+    landed; per group g: 3+8g last phase-A unit issued, 4+8g phase B start (A2 complete), 5+8g
+    first D chunk ready, 6+8g the group's stores issued; 62 the CTA's stores complete."""
+    print(f"slab kernel: grid {nb} CTAs, {slab} rows per CTA, {n_chunks} chunks, s {s}")
+
+    def col(k):
+        v = us[:, k]
+        v = v[~np.isnan(v)]
+        return f"{np.median(v):7.2f} / {v.min():7.2f} .. {v.max():7.2f} (n={v.size:3d})" if v.size else "      -"
+    print(f"  setup done         {col(0)}")
+    print(f"  griddep_wait done  {col(1)}")
+    print(f"  first x landed     {col(2)}")
+    for g in range(7):
+        if np.all(np.isnan(us[:, 3 + 8 * g])):
+            break
+        for k, nm in enumerate(["A issued", "B start", "epi start", "epi issued"]):
+            print(f"  group {g} {nm:10s} {col(3 + 8 * g + k)}")
+    print(f"  CTA end            {col(62)}")
 
 
 def summarise(path):
@@ -43,6 +64,8 @@ def summarise(path):
     h = np.frombuffer(raw[24:], dtype=np.uint64).reshape(nb, ktr).astype(np.float64)
     t0 = h[:, 0][h[:, 0] > 0].min()
     us = np.where(h > 0, (h - t0) * 1e-3, np.nan)
+    if cs == 1 and np.any(~np.isnan(us[:, 62])):
+        return summarise_slab(us, nb, n_tiles, n_chunks, s)
     print(f"grid {nb} CTAs (clusters of {cs}), {n_tiles} tiles, {n_chunks} chunks, s {s}")
 
     def col(k):

@@ -22,6 +22,14 @@ from test_gpu_forward import bf16_factored_emulated, gpu_x, make_case, rows_path
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, params=["slab", "cluster"])
+def rows_kernel(request, monkeypatch):
+    """Every test here runs on both row kernels: the slab kernel (k_tc_slab.cu, the default
+    where s is a power of two) and the clustered row-tile kernel (DEEPTHIN_ROWS_SLAB=0)."""
+    monkeypatch.setenv("DEEPTHIN_ROWS_SLAB", "1" if request.param == "slab" else "0")
+    return request.param
+
 GEOS = [
     # q, r_dim, rank, n, m, batch
     (2048, 2048, 3, 256, 16384, 1000),   # config 3 hidden layer, ragged batch
@@ -173,3 +181,27 @@ def test_rows_random_geometries(geo):
         y = D.layer_forward(x, fp, d["bias"], mma="bf16", out_dtype=out).double().cpu().numpy()
         extra = 2 ** -8 if out == torch.bfloat16 else 0.0
         assert O.rel_error(y, bf16_factored_emulated(d, plan, d["bias"])) <= 1e-3 + extra, geo
+
+
+@pytest.mark.parametrize("geo", [(2048, 2048, 3, 256, 16384, 16384 + 40), (2048, 3000, 3, 256, 24000, 2500),
+                                 (512, 640, 4, 64, 5120, 4099), (256, 512, 5, 128, 1024, 700),
+                                 (256, 384, 9, 256, 384, 333)])
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+def test_slab_kernel_bits_equal_cluster_kernel(geo, out, monkeypatch):
+    """The slab kernel performs the clustered kernel's arithmetic row by row (same MMA shapes
+    along K, same hi + lo sum, same epilogue): the outputs are bit-identical (the fused softmax
+    to rounding: its partials combine in another order), at slab sizes with partial groups and
+    16-row tails."""
+    q, r_dim, rank, n, m, batch = geo
+    plan, d, fp = make_case(q, r_dim, rank, n, m, batch, seed=8, rnd=O.round_bf16, bias_sd=0.2)
+    x = gpu_x(d["x"], torch.bfloat16)
+    for act in ("identity", "sigmoid", "softmax"):
+        ys = {}
+        for k in ("1", "0"):
+            monkeypatch.setenv("DEEPTHIN_ROWS_SLAB", k)
+            ys[k] = D.layer_forward(x, fp, d["bias"], act, mma="bf16", out_dtype=out)
+        if act == "softmax":  # the partial (max, sum) pairs combine in a different fixed order
+            rtol = 1e-5 if out == torch.float32 else 2.0 ** -7
+            assert torch.allclose(ys["1"].float(), ys["0"].float(), rtol=rtol, atol=1e-30), (geo, act)
+        else:
+            assert torch.equal(ys["1"], ys["0"]), (geo, act)
