@@ -57,6 +57,10 @@ def _fingerprint(extra=()) -> str:
 def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
     os.makedirs(OUTDIR, exist_ok=True)
     extra = ["-DDEEPTHIN_TIMING_SWITCHES"] if timing else []
+    if os.environ.get("DEEPTHIN_TEST_WAIT", "0") not in ("", "0"):
+        extra.append("-DDEEPTHIN_TEST_WAIT")  # experiment: non-blocking mbarrier.test_wait polls
+    if os.environ.get("DEEPTHIN_BOUNDED_WAITS", "0") not in ("", "0"):
+        extra.append("-DDEEPTHIN_BOUNDED_WAITS")  # trap on an mbarrier protocol bug (slower waits)
     lib = LIB.replace(".so", "_timing.so") if timing else LIB
     stamp = os.path.join(OUTDIR, "build_timing.stamp" if timing else "build.stamp")
     fp = _fingerprint(extra)

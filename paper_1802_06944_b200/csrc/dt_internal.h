@@ -102,10 +102,10 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
 // Row-slab variant (k_tc_slab.cu): no clusters, every CTA a contiguous slab of batch rows, x
 // viewed (batch * s) x n so one UMMA covers whole batch rows; same prepared operands (wf16 /
 // xf2p / bslot as tc_rows_prepare lays them out). Dispatched from tc_rows_forward.
-bool tc_slab_ok(const Geo &g, int64_t batch);
+bool tc_slab_ok(const Geo &g, int64_t batch, int softmax);
 int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16, const void *xf2p,
-                    const float *bias, int bslot, int act, float act_arg, int softmax, void *y,
-                    int y_dtype, cudaStream_t st);
+                    const float *bias, int bslot, int act, float act_arg, void *y, int y_dtype,
+                    cudaStream_t st);
 // Fused layer chain (k_tc_chain.cu): L reuse layers sharing n, s and rank in one persistent
 // kernel; hidden activations stay in shared memory. prepared[l]: tc_rows_prepare output of layer
 // l (hidden layers with hidden_act / bf16 output, the last with identity / bf16 output).

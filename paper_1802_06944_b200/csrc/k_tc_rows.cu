@@ -855,9 +855,8 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   // (DEEPTHIN_ROWS_SLAB=0: the clustered row-tile kernel below, A/B runs and tests)
   {
     const char *senv = getenv("DEEPTHIN_ROWS_SLAB");  // read per call (tests flip it)
-    if ((senv ? atoi(senv) != 0 : false) && !p.wait_flags && !p.post_flags && tc_slab_ok(g, batch)) {
-      if (int rc = tc_slab_forward(g, batch, x, wf16, xf2p, bias, p.bslot, act, act_arg, p.softmax, y,
-                                   y_dtype, st))
+    if ((senv ? atoi(senv) != 0 : false) && !p.wait_flags && !p.post_flags && tc_slab_ok(g, batch, p.softmax)) {
+      if (int rc = tc_slab_forward(g, batch, x, wf16, xf2p, bias, p.bslot, act, act_arg, y, y_dtype, st))
         return rc;
       return want_sm && !p.softmax ? launch_row_softmax(batch, g.r_dim, y, y_dtype, st) : DT_OK;
     }

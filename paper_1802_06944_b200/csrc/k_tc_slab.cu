@@ -12,24 +12,29 @@
 //             (bf16 x bf16 -> fp32 in TMEM; wf as bf16 hi | lo in the two N halves)
 //   re-lay:   TMEM lane (b*s + seg) -> row b, K slots [seg*rp, seg*rp + rank) of the tf32 A
 //             operand of phase B (128-byte swizzled K-major rows in shared memory)
-//   phase B:  y[b, j] = act(sum_kk A2[b, kk] XF2p[j, kk])   (kind::tf32, bias in a K pad slot)
-//             per group of up to 64 batch rows, 128 output columns per D buffer, XF2p chunks
-//             streamed from L2. A group's rows sit in TMEM lanes 32 q + (0..15), q = 0..3 (the
-//             re-lay chooses the A2 row): every epilogue warp reads its quarter's 16 live lanes
-//             with the 16-lane tcgen05.ld shape, so all 32 threads hold live values (the
-//             epilogue is MUFU-bound: one tanh per output) although the UMMA runs M = 128.
-//             Groups of 64 let a slab's first stores overlap its later loads.
-//   epilogue: D (TMEM) -> activation -> bf16/fp32 -> swizzled staging -> TMA store (16 x 32
-//             boxes); the fused row softmax (two passes, the contraction recomputed) needs no
-//             exchange: a CTA holds whole rows.
+//   phase B:  TRANSPOSED, output columns on the UMMA M axis (= TMEM lanes), batch rows on N:
+//             D^T[j, b] = sum_kk XF2p[j, kk] A2[b, kk]   (kind::tf32, bias in a K pad slot)
+//             per group of up to 64 batch rows (N = 64) and chunk of 128 output columns, XF2p
+//             chunks streamed from L2. TMEM reads (64 B/clk per SM) and MUFU (one tanh per
+//             output) bound the epilogue at 16 outputs per clock per SM; with the columns on
+//             the lanes every lane and every thread is live whatever the group's row count, so
+//             slabs split into small groups and a group's stores overlap the next group's loads.
+//             (Rows on the lanes — measured — need 128-row groups to keep the lanes busy: one
+//             group per slab, all loads before all stores.)
+//   epilogue: D^T (TMEM; thread = output column, registers = 32 batch rows) -> activation ->
+//             bf16/fp32 -> transposed into a swizzled 32 x 32 staging box -> TMA store.
+//             The row softmax is not fused here (per-row statistics would cross lanes):
+//             softmax layers stay on the clustered row-tile kernel.
 //
 // Warp roles (768 threads, one CTA per SM):
 //   warp 0  TMA producer of x' k-blocks (128 x' rows x 64 bf16, SW128)
 //   warp 1  TMA producer of XF2p chunks (128 output columns x 32 fp32, SW128)
 //   warp 2  TMEM allocator + single-thread tcgen05.mma issuer of phase A (P ring of 8 units)
-//   warp 3  single-thread tcgen05.mma issuer of phase B
+//   warps 3, 24  single-thread tcgen05.mma issuers of phase B, one per team (team t = chunks t,
+//               t + 2, ... with its own XF2p ring, D buffers and epilogue warps)
 //   warps 4-7   P re-lay (one per TMEM lane quarter)
-//   warps 8-23  epilogue (four per lane quarter, each 32 of a chunk's 128 columns)
+//   warps 8-23  epilogue, 8 warps per team: quarter (warp % 4) = 32 of a chunk's 128 output
+//               columns, ((warp - 8) / 4) % 2 = 32 of the group's 64 rows
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -49,18 +54,20 @@ namespace {
 using namespace ptx;
 using namespace rowsdev;
 
-constexpr int kGM = 64;            // batch rows per phase-B group (16 live lanes per TMEM quarter)
-constexpr int kMM = 128;           // UMMA M of phase B (= A2 rows = TMEM lanes)
-constexpr int kNc = 128;           // output columns per D chunk (UMMA N of phase B)
+constexpr int kGM = 64;            // batch rows per phase-B group (UMMA N = TMEM columns per D buffer)
+constexpr int kNc = 128;           // output columns per D chunk (UMMA M of phase B = TMEM lanes)
+constexpr int kTeams = 2;          // independent phase-B pipelines (issuer + 8 epilogue warps each)
+constexpr int kND = 2;             // D buffers in TMEM per team (kGM columns each)
 constexpr int kXSMax = 8;          // x ring depth cap
-constexpr int kBSMax = 4;          // XF2p chunk ring depth cap
+constexpr int kBSMax = 4;          // XF2p chunk ring depth cap (per team)
 constexpr int kPS = 8;             // P ring: phase-A units in TMEM
 constexpr int kPW = 4;             // re-lay warps
 constexpr int kEpi = 16;           // epilogue warps
-constexpr int kSlabThreads = 32 * (4 + kPW + kEpi);
+constexpr int kIssuer1 = 4 + kPW + kEpi;  // the second phase-B issuer (last warp)
+constexpr int kSlabThreads = 32 * (5 + kPW + kEpi);
 constexpr uint32_t kXBytes = 128 * 128;   // 128 x' rows x 64 bf16
 constexpr uint32_t kBBytes = kNc * 128;   // 128 columns x 32 fp32
-constexpr uint32_t kA2Bytes = kMM * 128;  // 128 rows x 32 fp32
+constexpr uint32_t kA2Bytes = kGM * 128;  // 64 rows x 32 fp32
 constexpr int kTr = 64;                   // trace slots per CTA
 
 struct SlabParams {
@@ -68,12 +75,11 @@ struct SlabParams {
   int r_dim, s, ls, nkb, np, rank, rp, k2, n_chunks;
   int ur;       // batch rows per phase-A unit (128 / s)
   int slab;     // batch rows per CTA (a multiple of max(ur, 16))
-  int xs, bs, nd;
+  int xs, bs;
   int nstage;   // output staging boxes per epilogue warp (TMA stores in flight)
   int dbg;      // timing build only (DEEPTHIN_DBG_SLAB): 1 no TMA store, 2 no staging, 3 no act
   uint32_t dcol0;
   int bslot;    // K slot carrying the bias (A2 = 1 there), -1: the epilogue adds it
-  int softmax;
   const float *bias;
   float arg;
   uint32_t off_a2, off_wf, off_b, off_out, off_red, off_x, off_bar;
@@ -95,28 +101,32 @@ __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t
   asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 
-// this warp's 16 x 32 outputs in the 16x256b register layout (o[4i], o[4i+1]: row lane/4,
-// columns 8i + 2(lane%4) + {0,1}; o[4i+2], o[4i+3]: row 8 + lane/4) into its swizzled staging
-// box (the TMA SW64 / SW128 pattern: 16-byte chunk ch of row r at ch ^ (r >> 1 & 3) / ch ^ (r & 7))
+// this warp's 16 x 32 outputs, o[i] = row i of output column `lane`, transposed into its
+// swizzled row-major staging box (the TMA SW64 / SW128 pattern: 16-byte chunk ch of row r at
+// ch ^ (r >> 1 & 3) / ch ^ (r & 7)). bf16: lane pairs exchange so that the even lane holds
+// columns (lane, lane + 1) of the even rows and the odd lane those of the odd rows — one 4-byte
+// store per two outputs, 128 contiguous bytes per instruction (rows r, r + 1 are adjacent).
 template <int E>
-__device__ __forceinline__ void stage_16x32(uint32_t out_s, int lane, const float (&o)[16]) {
-  const int r = lane >> 2, cp = lane & 3;
-  if constexpr (E == 2) {  // rows of 64 bytes; (r + 8) >> 1 & 3 == r >> 1 & 3
-    const uint32_t lo = out_s + (uint32_t)r * 64u + (uint32_t)cp * 4u, hi = lo + 8u * 64u;
-    const int sw = (r >> 1) & 3;
+__device__ __forceinline__ void stage_t16x32(uint32_t out_s, int lane, const float *o) {
+  if constexpr (E == 2) {
+    const int odd = lane & 1;
+    const uint32_t base = out_s + (uint32_t)odd * 64u + (uint32_t)((lane >> 1) & 3) * 4u;
+    const int ch = lane >> 3;  // 16-byte chunk of columns lane - odd, lane - odd + 1
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      st_shared_b32(lo + ((uint32_t)(i ^ sw) << 4), pack_bf16(o[4 * i], o[4 * i + 1]));
-      st_shared_b32(hi + ((uint32_t)(i ^ sw) << 4), pack_bf16(o[4 * i + 2], o[4 * i + 3]));
+    for (int i = 0; i < 16; i += 2) {
+      // send the row the partner keeps, receive the partner's value of the row this lane keeps
+      const float give = odd ? o[i] : o[i + 1], keep = odd ? o[i + 1] : o[i];
+      const float got = __shfl_xor_sync(0xffffffffu, give, 1);
+      const uint32_t w = odd ? pack_bf16(got, keep) : pack_bf16(keep, got);
+      const int r = i;  // even row of the pair; this lane stores row r + odd (same swizzle)
+      st_shared_b32(base + (uint32_t)r * 64u + ((uint32_t)(ch ^ ((r >> 1) & 3)) << 4), w);
     }
-  } else {  // rows of 128 bytes; (r + 8) & 7 == r
-    const uint32_t lo = out_s + (uint32_t)r * 128u + (uint32_t)(cp & 1) * 8u, hi = lo + 8u * 128u;
+  } else {
+    const uint32_t base = out_s + (uint32_t)(lane & 3) * 4u;
+    const int ch = lane >> 2;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t ch = (uint32_t)((2 * i + (cp >> 1)) ^ r) << 4;
-      st_shared_v2(lo + ch, __float_as_uint(o[4 * i]), __float_as_uint(o[4 * i + 1]));
-      st_shared_v2(hi + ch, __float_as_uint(o[4 * i + 2]), __float_as_uint(o[4 * i + 3]));
-    }
+    for (int i = 0; i < 16; ++i)
+      st_shared_b32(base + (uint32_t)i * 128u + ((uint32_t)(ch ^ (i & 7)) << 4), __float_as_uint(o[i]));
   }
 }
 
@@ -124,13 +134,13 @@ template <int YDT, int ACT>
 __global__ void __launch_bounds__(kSlabThreads, 1)
     k_tc_rows_slab(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_wf,
                    const __grid_constant__ CUtensorMap tm_xf2, const __grid_constant__ CUtensorMap tm_y,
-                   const SlabParams p) {
+                   const __grid_constant__ CUtensorMap tm_y16, const SlabParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *x_full = bars, *x_empty = x_full + kXSMax;
-  uint64_t *b_full = x_empty + kXSMax, *b_empty = b_full + kBSMax;
-  uint64_t *d_full = b_empty + kBSMax, *d_empty = d_full + 4;
+  uint64_t *b_full = x_empty + kXSMax, *b_empty = b_full + kTeams * kBSMax;  // [team][slot]
+  uint64_t *d_full = b_empty + kTeams * kBSMax, *d_empty = d_full + 4;        // [team][buffer]
   uint64_t *p_full = d_empty + 4, *p_free = p_full + kPS;
   uint64_t *a2_full = p_free + kPS, *a2_free = a2_full + 2;
   uint64_t *wf_full = a2_free + 2;
@@ -144,17 +154,18 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
   const int n_groups = (rows + kGM - 1) / kGM;
   // Every CTA streams every XF2p chunk: CTA i starts at chunk i mod n_chunks, so that at any
   // time the CTAs read n_chunks different chunks (all of them on the same 128 lines at once
-  // serialise on a few L2 slices: measured 0.53 us per chunk with nothing else running). The
-  // softmax passes keep the natural order: their sums run in chunk order, which must not
-  // depend on the CTA a row falls in.
-  const int rot = p.softmax ? 0 : (int)(blockIdx.x % (unsigned)p.n_chunks);
+  // would hit the same few L2 slices).
+  const int rot = (int)(blockIdx.x % (unsigned)p.n_chunks);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.xs; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
-    for (int i = 0; i < p.bs; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < 4; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], kEpi); }
+    for (int i = 0; i < kTeams * kBSMax; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+    for (int i = 0; i < kTeams * kND; ++i) {
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], kEpi / kTeams);
+    }
     for (int i = 0; i < kPS; ++i) { mbar_init(&p_full[i], 1); mbar_init(&p_free[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&a2_full[i], 1); mbar_init(&a2_free[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&a2_full[i], 1); mbar_init(&a2_free[i], kTeams); }
     mbar_init(wf_full, 1);
     fence_mbar_init();
   }
@@ -163,6 +174,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     tma_prefetch_desc(&tm_wf);
     tma_prefetch_desc(&tm_xf2);
     tma_prefetch_desc(&tm_y);
+    tma_prefetch_desc(&tm_y16);
   }
   if (warp == 2) tmem_alloc(tslot, 512);
   tc_fence_before();
@@ -201,19 +213,28 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- XF2p chunk producer (every chunk once per group and pass) ----------------
+    // ---------------- XF2p chunk producer: chunk ci of a group goes to team ci % 2 ----------------
     if (lane == 0) {
-      int st = 0;
-      uint32_t ph = 0;
+      int st0 = 0, st1 = 0;  // per-team ring positions (scalars: no dynamically indexed arrays)
+      uint32_t ph0 = 0, ph1 = 0;
       for (int g = 0; g < n_groups; ++g)
-        for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass)
-          for (int ci = 0; ci < p.n_chunks; ++ci) {
-            const int c = ci + rot < p.n_chunks ? ci + rot : ci + rot - p.n_chunks;
-            mbar_wait(&b_empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&b_full[st], kBBytes);
-            tma_load_2d(smem + p.off_b + st * kBBytes, &tm_xf2, &b_full[st], 0, c * kNc);
-            if (++st == p.bs) { st = 0; ph ^= 1; }
+        for (int ci = 0; ci < p.n_chunks; ++ci) {
+          const int t = ci & 1;
+          const int c = ci + rot < p.n_chunks ? ci + rot : ci + rot - p.n_chunks;
+          const int st = t ? st1 : st0;
+          const uint32_t ph = t ? ph1 : ph0;
+          const int slot = t * kBSMax + st;
+          mbar_wait(&b_empty[slot], ph ^ 1);
+          if (kTimingSwitches && p.dbg >= 5) {  // no XF2p loads (stale operand)
+            mbar_arrive(&b_full[slot]);
+          } else {
+            mbar_arrive_expect_tx(&b_full[slot], kBBytes);
+            tma_load_2d(smem + p.off_b + (t * p.bs + st) * kBBytes, &tm_xf2, &b_full[slot], 0, c * kNc);
           }
+          const int nst = st + 1 == p.bs ? 0 : st + 1;
+          const uint32_t nph = st + 1 == p.bs ? ph ^ 1 : ph;
+          if (t) { st1 = nst; ph1 = nph; } else { st0 = nst; ph0 = nph; }
+        }
     }
     __syncwarp();
   } else if (warp == 2) {
@@ -252,35 +273,43 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 3) {
-    // ---------------- phase-B MMA issuer: D = A2[group] . XF2p chunk^T (tf32) ----------------
+  } else if (warp == 3 || warp == kIssuer1) {
+    // ---------------- phase-B MMA issuers: D^T = XF2p chunk . A2[group]^T (tf32) ----------------
+    // two independent pipelines (teams): issuer t takes chunks t, t + 2, ... of every group, its
+    // own XF2p ring, its own two D buffers and its own eight epilogue warps — two handshake
+    // loops in flight instead of one (measured: one loop costs ~0.5 us per chunk)
     if (lane == 0) {
+      const int t = warp == 3 ? 0 : 1;
       const uint32_t s0 = smem_u32(smem);
-      const uint32_t idB = idesc_f32acc(kMM, kNc, 2);
+      const uint32_t idB = idesc_f32acc(kNc, kGM, 2);
       int bs = 0, db = 0;
       uint32_t bph = 0, dph = 0;
       for (int g = 0; g < n_groups; ++g) {
         const int gb = g & 1;
         mbar_wait(&a2_full[gb], (uint32_t)(g >> 1) & 1u);
-        strace(p, 4 + 8 * min(g, 6));
+        if (t == 0) strace(p, 4 + 8 * min(g, 6));
         tc_fence_after();
         const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)gb * kA2Bytes;
-        for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass)
-          for (int c = 0; c < p.n_chunks; ++c) {
-            mbar_wait(&b_full[bs], bph);
-            mbar_wait(&d_empty[db], dph ^ 1);
-            tc_fence_after();
-            const uint32_t d = tbase + p.dcol0 + (uint32_t)(db * kNc);
-            const uint32_t b = s0 + p.off_b + (uint32_t)bs * kBBytes;
-            for (int k = 0; k < p.k2 / 8; ++k)
-              mma_tf32_ss(d, smem_desc(a2_s + k * 32, 16, 1024, SL_SW128),
-                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
-            mma_commit(&b_empty[bs]);
-            if (++bs == p.bs) { bs = 0; bph ^= 1; }
-            mma_commit(&d_full[db]);
-            if (++db == p.nd) { db = 0; dph ^= 1; }
-          }
-        mma_commit(&a2_free[gb]);  // this group's reads of A2[gb] are done when these complete
+        for (int ci = t; ci < p.n_chunks; ci += kTeams) {
+          mbar_wait(&b_full[t * kBSMax + bs], bph);
+          mbar_wait(&d_empty[t * kND + db], dph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tbase + p.dcol0 + (uint32_t)((t * kND + db) * kGM);
+          const uint32_t b = s0 + p.off_b + (uint32_t)(t * p.bs + bs) * kBBytes;
+          const int nk = (kTimingSwitches && p.dbg >= 7) ? 0 : (kTimingSwitches && p.dbg >= 6) ? 1 : p.k2 / 8;
+          for (int k = 0; k < nk; ++k)
+            mma_tf32_ss(d, smem_desc(b + k * 32, 16, 1024, SL_SW128),
+                        smem_desc(a2_s + k * 32, 16, 1024, SL_SW128), idB, k != 0);
+          if (kTimingSwitches && p.dbg >= 8) mbar_arrive(&b_empty[t * kBSMax + bs]); else
+          mma_commit(&b_empty[t * kBSMax + bs]);
+          if (++bs == p.bs) { bs = 0; bph ^= 1; }
+          if (kTimingSwitches && p.dbg >= 9) mbar_arrive(&d_full[t * kND + db]); else
+          mma_commit(&d_full[t * kND + db]);
+          if (++db == kND) { db = 0; dph ^= 1; }
+        }
+        // this team's reads of A2[gb] are done when these complete (both teams: count 2)
+        if (kTimingSwitches && p.dbg >= 9) mbar_arrive(&a2_free[gb]); else
+        mma_commit(&a2_free[gb]);
       }
     }
     __syncwarp();
@@ -292,11 +321,12 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     const int seg = lrow & (p.s - 1), bq = lrow >> p.ls;
     const int cpr = p.rp / 4;  // 16-byte chunks per segment
     // K padding of the tf32 operand (never overwritten): zero, 1.0 in a bias slot past s*rp
-    for (int b = 0; b < 2; ++b)
-      for (int kk = p.s * p.rp; kk < p.k2; kk += 4)
-        st_shared_v4(a2_local + (uint32_t)b * kA2Bytes + (uint32_t)lrow * 128u +
-                         ((uint32_t)((kk >> 2) ^ (lrow & 7)) << 4),
-                     kk == p.bslot ? 0x3f800000u : 0u, 0u, 0u, 0u);
+    if (lrow < kGM)
+      for (int b = 0; b < 2; ++b)
+        for (int kk = p.s * p.rp; kk < p.k2; kk += 4)
+          st_shared_v4(a2_local + (uint32_t)b * kA2Bytes + (uint32_t)lrow * 128u +
+                           ((uint32_t)((kk >> 2) ^ (lrow & 7)) << 4),
+                       kk == p.bslot ? 0x3f800000u : 0u, 0u, 0u, 0u);
     uint32_t seq = 0;
     for (int g = 0; g < n_groups; ++g) {
       const int gb = g & 1;
@@ -315,9 +345,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         tmem_ld_32x32b_x32(pcol, vh);
         tmem_ld_32x32b_x32(pcol + (uint32_t)p.rank, vl);
         tmem_ld_wait();
-        // batch row u*ur + bq of the group -> A2 row (= TMEM lane) 32 (r / 16) + r % 16
-        const int grow = u * p.ur + bq;
-        const int row = 32 * (grow >> 4) + (grow & 15);
+        const int row = u * p.ur + bq;  // batch row within the group = A2 row
         const uint32_t rbase = a2b + (uint32_t)row * 128u;
 #pragma unroll
         for (int k0 = 0; k0 < 32; k0 += 4) {
@@ -343,160 +371,81 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue: 16 warps, four per TMEM lane quarter ----------------
-    // quarter sp holds group rows 16 sp .. 16 sp + 15 in its lanes 0..15; warp (sp, qc) takes
-    // columns 32 qc .. 32 qc + 31 of every 128-column chunk in the 16x256b register layout:
-    // this thread has rows ra = lane/4 and ra + 8, columns 8i + 2(lane%4) + {0,1}, i = 0..3
+    // ---------------- epilogue: 2 teams of 8 warps ----------------
+    // team t = chunks t, t + 2, ...; within a team quarter sp = output columns 32 sp .. 32 sp + 31
+    // of the chunk (lane = column), h = rows 32 h .. 32 h + 31 of the group (32 TMEM columns)
     const int sp = warp & 3;
     const int e = warp - 4 - kPW;      // 0..15
-    const int qc = e / 4;
-    const int ra = lane >> 2, cp = lane & 3;
+    const int t = e >> 3, h = (e >> 2) & 1;
     const uint32_t s0 = smem_u32(smem);
     const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
     constexpr int E = YDT == DT_BF16 ? 2 : 4;
     constexpr int RB = 32 * E;         // bytes per row of this warp's 32 columns (64 or 128)
-    const uint32_t out_s0 = s0 + p.off_out + (uint32_t)(e * p.nstage) * (16u * RB);
+    const uint32_t out_s0 = s0 + p.off_out + (uint32_t)(e * p.nstage) * (32u * RB);
     int sb = 0;
     const int64_t slab_end = row_begin + rows;
-    const float l2e = 1.4426950408889634f;
     int db = 0;
     uint32_t dph = 0;
     for (int g = 0; g < n_groups; ++g) {
-      const int64_t row0 = row_begin + g * kGM + 16 * sp;
-      // this quarter's 16 rows lie inside the slab (slabs end on multiples of 16; the batch end
-      // is clipped by TMA) or past it (no store)
-      const bool live = row0 < slab_end;
-      float Ma = 0.f, Mb = 0.f, inva = 1.f, invb = 1.f;
-      if (p.softmax) {
-        // pass 1: per row, the online (max, sum 2^((z - max) log2 e)) over this warp's columns of
-        // every chunk (the four threads of a row combined by shuffles), then the four column
-        // warps combined in a fixed order (deterministic)
-        float2 *red = reinterpret_cast<float2 *>(smem + p.off_red) + (g & 1) * 4 * kGM;  // [4][64]
-        float ma = -INFINITY, la = 0.f, mb = -INFINITY, lb = 0.f;
-        for (int c = 0; c < p.n_chunks; ++c) {
-          mbar_wait(&d_full[db], dph);
-          tc_fence_after();
-          uint32_t v[16];
-          tmem_ld_16x256b_x4(tbase + lane_t + p.dcol0 + (uint32_t)(db * kNc + 32 * qc), v);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[db]);
-          if (++db == p.nd) { db = 0; dph ^= 1; }
-          const int col0 = c * kNc + 32 * qc;
-          if (col0 >= p.r_dim) continue;  // (uniform over the warp)
-          float ca = -INFINITY, cb = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (col0 + 8 * i + 2 * cp < p.r_dim) {  // r_dim is even: the pair is in or out
-              ca = fmaxf(ca, fmaxf(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])));
-              cb = fmaxf(cb, fmaxf(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])));
-            }
-          ca = fmaxf(ca, __shfl_xor_sync(0xffffffffu, ca, 1));
-          ca = fmaxf(ca, __shfl_xor_sync(0xffffffffu, ca, 2));
-          cb = fmaxf(cb, __shfl_xor_sync(0xffffffffu, cb, 1));
-          cb = fmaxf(cb, __shfl_xor_sync(0xffffffffu, cb, 2));
-          const float na = fmaxf(ma, ca), nb = fmaxf(mb, cb);
-          float sa = 0.f, sb = 0.f;
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (col0 + 8 * i + 2 * cp < p.r_dim) {
-              sa += ex2_approx((__uint_as_float(v[4 * i]) - na) * l2e) +
-                    ex2_approx((__uint_as_float(v[4 * i + 1]) - na) * l2e);
-              sb += ex2_approx((__uint_as_float(v[4 * i + 2]) - nb) * l2e) +
-                    ex2_approx((__uint_as_float(v[4 * i + 3]) - nb) * l2e);
-            }
-          sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-          sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-          sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-          sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-          la = (ma > -INFINITY ? la * ex2_approx((ma - na) * l2e) : 0.f) + sa;
-          lb = (mb > -INFINITY ? lb * ex2_approx((mb - nb) * l2e) : 0.f) + sb;
-          ma = na;
-          mb = nb;
-        }
-        if (cp == 0) {
-          red[qc * kGM + 16 * sp + ra] = make_float2(ma, la);
-          red[qc * kGM + 16 * sp + ra + 8] = make_float2(mb, lb);
-        }
-        named_bar_sync(2, 32 * kEpi);
-        float La = 0.f, Lb = 0.f;
-        Ma = Mb = -INFINITY;
-        for (int k = 0; k < 4; ++k) {
-          const float2 qa = red[k * kGM + 16 * sp + ra], qb = red[k * kGM + 16 * sp + ra + 8];
-          if (qa.x > -INFINITY) {
-            const float nm = fmaxf(Ma, qa.x);
-            La = La * exp2f((Ma - nm) * l2e) + qa.y * exp2f((qa.x - nm) * l2e);
-            Ma = nm;
-          }
-          if (qb.x > -INFINITY) {
-            const float nm = fmaxf(Mb, qb.x);
-            Lb = Lb * exp2f((Mb - nm) * l2e) + qb.y * exp2f((qb.x - nm) * l2e);
-            Mb = nm;
-          }
-        }
-        inva = 1.f / La;
-        invb = 1.f / Lb;
-      }
-      // (softmax: pass 2 over the recomputed chunks)
-      for (int ci = 0; ci < p.n_chunks; ++ci) {
+      const int64_t row0 = row_begin + g * kGM + 32 * h;
+      // rows of this warp inside the slab: all 32 (or the batch end, which TMA clips) -> the
+      // 32-row box; 16 -> the 16-row box (slabs end on multiples of 16); none -> nothing to do
+      const int live = (int)min((int64_t)32, slab_end - row0);
+      const CUtensorMap *tmy = (live >= 32 || slab_end == p.batch) ? &tm_y : &tm_y16;
+      for (int ci = t; ci < p.n_chunks; ci += kTeams) {
         const int c = ci + rot < p.n_chunks ? ci + rot : ci + rot - p.n_chunks;
-        mbar_wait(&d_full[db], dph);
+        mbar_wait(&d_full[t * kND + db], dph);
         if (e == 0 && ci == 0) strace(p, 5 + 8 * min(g, 6));
         tc_fence_after();
-        const int col0 = c * kNc + 32 * qc;
-        uint32_t v[16];
-        tmem_ld_16x256b_x4(tbase + lane_t + p.dcol0 + (uint32_t)(db * kNc + 32 * qc), v);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&d_empty[db]);
-        if (++db == p.nd) { db = 0; dph ^= 1; }
-        if (col0 >= p.r_dim || !live) continue;
-        if (kTimingSwitches && p.dbg >= 3) continue;
-        float o[16];
-        if (p.softmax) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            o[4 * i] = ex2_approx((__uint_as_float(v[4 * i]) - Ma) * l2e) * inva;
-            o[4 * i + 1] = ex2_approx((__uint_as_float(v[4 * i + 1]) - Ma) * l2e) * inva;
-            o[4 * i + 2] = ex2_approx((__uint_as_float(v[4 * i + 2]) - Mb) * l2e) * invb;
-            o[4 * i + 3] = ex2_approx((__uint_as_float(v[4 * i + 3]) - Mb) * l2e) * invb;
-          }
-        } else if (p.bias && p.bslot < 0) {
-          constexpr float bsc = (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) ? 0.5f : 1.f;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int col = col0 + 8 * i + 2 * cp;
-            const float b0 = col < p.r_dim ? bsc * __ldg(p.bias + col) : 0.f;
-            const float b1 = col + 1 < p.r_dim ? bsc * __ldg(p.bias + col + 1) : 0.f;
-            o[4 * i] = act_out<YDT, ACT>(__uint_as_float(v[4 * i]) + b0, p.arg);
-            o[4 * i + 1] = act_out<YDT, ACT>(__uint_as_float(v[4 * i + 1]) + b1, p.arg);
-            o[4 * i + 2] = act_out<YDT, ACT>(__uint_as_float(v[4 * i + 2]) + b0, p.arg);
-            o[4 * i + 3] = act_out<YDT, ACT>(__uint_as_float(v[4 * i + 3]) + b1, p.arg);
-          }
-        } else {  // bias folded into the tf32 contraction (or absent)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]), p.arg);
-        }
-        if (kTimingSwitches && p.dbg >= 2) {
-          if (o[0] == 1234.5f) strace(p, 63);
-          continue;
-        }
+        const int col0 = c * kNc + 32 * sp;
+        const bool work = live > 0 && col0 < p.r_dim && !(kTimingSwitches && p.dbg >= 4);
         // the staging box's previous store (nstage stores ago) has read it
-        const uint32_t out_s = out_s0 + (uint32_t)sb * (16u * RB);
-        if (++sb == p.nstage) sb = 0;
-        if (lane == 0) {
-          if (p.nstage == 4) bulk_wait_group_read<3>();
-          else if (p.nstage == 2) bulk_wait_group_read<1>();
-          else bulk_wait_group_read<0>();
+        const uint32_t out_s = out_s0 + (uint32_t)sb * (32u * RB);
+        if (work) {
+          if (++sb == p.nstage) sb = 0;
+          if (lane == 0) {
+            if (p.nstage == 2) bulk_wait_group_read<1>();
+            else bulk_wait_group_read<0>();
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        stage_16x32<E>(out_s, lane, o);
+        // two halves of 16 rows (16 live registers each: 32 at once spill at 800 threads)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t v[16];
+          if (work) {
+            tmem_ld_32x32b_x16(
+                tbase + lane_t + p.dcol0 + (uint32_t)((t * kND + db) * kGM + 32 * h + 16 * hh), v);
+            tmem_ld_wait();
+          }
+          if (hh == 1) {  // both halves read: the D buffer may be overwritten
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_empty[t * kND + db]);
+          }
+          if (!work || (kTimingSwitches && p.dbg >= 3)) continue;
+          float o[16];
+          if (p.bias && p.bslot < 0) {
+            constexpr float bsc = (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) ? 0.5f : 1.f;
+            const float bj = col0 + lane < p.r_dim ? bsc * __ldg(p.bias + col0 + lane) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]) + bj, p.arg);
+          } else {  // bias folded into the tf32 contraction (or absent)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]), p.arg);
+          }
+          if (kTimingSwitches && p.dbg >= 2) {
+            if (o[0] == 1234.5f) strace(p, 63);
+            continue;
+          }
+          stage_t16x32<E>(out_s + (uint32_t)hh * (16u * RB), lane, o);
+        }
+        if (++db == kND) { db = 0; dph ^= 1; }
+        if (!work || (kTimingSwitches && p.dbg >= 2)) continue;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && !(kTimingSwitches && p.dbg >= 1)) {
-          tma_store_2d(&tm_y, smem + (out_s - s0), col0, (int32_t)row0);
+          tma_store_2d(tmy, smem + (out_s - s0), col0, (int32_t)row0);
           bulk_commit_group();
         }
       }
@@ -514,7 +463,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
   }
 }
 
-using SlabFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, SlabParams);
+using SlabFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, SlabParams);
 
 template <int YDT>
 SlabFn pick_act(int act) {
@@ -542,15 +491,16 @@ int slab_nsm() {
 // Geometries the slab kernel takes among those tc_rows_ok accepts: s = 2, 4 or 8 (a unit of
 // 128 x' rows holds 64 / 32 / 16 whole batch rows, a group of 64 whole units), batch * s within
 // the tensor map's 32-bit coordinates.
-bool tc_slab_ok(const Geo &g, int64_t batch) {
+bool tc_slab_ok(const Geo &g, int64_t batch, int softmax) {
+  if (softmax) return false;  // per-row statistics would cross lanes: the clustered kernel fuses it
   if (g.s < 2 || g.s > 8 || (g.s & (g.s - 1)) != 0) return false;  // units of 16 / 32 / 64 rows
   if (batch * g.s >= (int64_t)1 << 31) return false;
   return true;
 }
 
 int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16, const void *xf2p,
-                    const float *bias, int bslot, int act, float act_arg, int softmax, void *y,
-                    int y_dtype, cudaStream_t st) {
+                    const float *bias, int bslot, int act, float act_arg, void *y, int y_dtype,
+                    cudaStream_t st) {
   SlabParams p{};
   p.batch = batch;
   p.r_dim = (int)g.r_dim;
@@ -567,7 +517,6 @@ int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16
   p.bias = bias;
   p.bslot = bslot;
   p.arg = act_arg;
-  p.softmax = softmax;
   p.dbg = DT_DBG_ENV("DEEPTHIN_DBG_SLAB");
   // slab: the batch split evenly over the SMs, rounded up to whole units and to the 16-row
   // store box (DEEPTHIN_SLAB_CTAS: A/B runs with fewer CTAs)
@@ -577,23 +526,22 @@ int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16
   const int64_t per = (batch + nsm - 1) / nsm;
   p.slab = (int)((per + gran - 1) / gran * gran);
   const int ncta = (int)((batch + p.slab - 1) / p.slab);
-  // TMEM: P ring of kPS units in columns [0, kPS * np), nd D buffers of 128 columns at the top
-  p.nd = std::min(3, (512 - (kPS * p.np + 127) / 128 * 128) / kNc);
-  p.dcol0 = 512u - (uint32_t)p.nd * kNc;
+  // TMEM: P ring of kPS units in columns [0, kPS * np), kTeams x kND D buffers of kGM columns
+  // at the top
+  p.dcol0 = 512u - (uint32_t)(kTeams * kND * kGM);
   // shared memory: A2 x 2 | wf | XF2p ring | output staging | softmax partials | x ring | barriers
   const int E = y_dtype == DT_BF16 ? 2 : 4;
   const uint32_t wf_bytes = (uint32_t)(p.nkb * p.np * 128);
   static const int want_bs = getenv("DEEPTHIN_SLAB_BS") ? atoi(getenv("DEEPTHIN_SLAB_BS")) : 0;
-  p.bs = want_bs > 0 ? std::max(2, std::min(want_bs, kBSMax)) : 3;
+  p.bs = want_bs > 0 ? std::max(2, std::min(want_bs, kBSMax)) : 2;  // per team
   p.off_a2 = 0;
   p.off_wf = 2 * kA2Bytes;
   p.off_b = (p.off_wf + wf_bytes + 1023) & ~1023u;
-  p.off_out = p.off_b + (uint32_t)p.bs * kBBytes;
-  static const int want_stg = getenv("DEEPTHIN_SLAB_STG") ? atoi(getenv("DEEPTHIN_SLAB_STG")) : 2;
-  p.nstage = want_stg >= 4 ? 4 : want_stg >= 2 ? 2 : 1;
-  p.off_red = p.off_out + (uint32_t)(kEpi * p.nstage) * 16u * 32u * (uint32_t)E;
-  p.off_x = p.off_red + (softmax ? 2u * 4u * kGM * 8u : 0u);
-  p.off_x = (p.off_x + 1023) & ~1023u;
+  p.off_out = p.off_b + (uint32_t)(kTeams * p.bs) * kBBytes;
+  static const int want_stg = getenv("DEEPTHIN_SLAB_STG") ? atoi(getenv("DEEPTHIN_SLAB_STG")) : 1;
+  p.nstage = want_stg >= 2 ? 2 : 1;
+  p.off_red = p.off_out + (uint32_t)(kEpi * p.nstage) * 32u * 32u * (uint32_t)E;
+  p.off_x = (p.off_red + 1023) & ~1023u;
   constexpr uint32_t kSmemMax = 227 * 1024, kTail = 512 + 1024;
   static const int want_xs = getenv("DEEPTHIN_SLAB_XS") ? atoi(getenv("DEEPTHIN_SLAB_XS")) : kXSMax;
   if (kSmemMax - kTail < p.off_x + 2 * kXBytes) {
@@ -605,7 +553,7 @@ int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16
   p.off_bar = p.off_x + (uint32_t)p.xs * kXBytes;
   const uint32_t smem_bytes = p.off_bar + kTail;
 
-  CUtensorMap tm_x, tm_wf, tm_xf2, tm_y;
+  CUtensorMap tm_x, tm_wf, tm_xf2, tm_y, tm_y16;
   // x viewed (batch * s) x n: every 128 x' rows are 128 / s batch rows with all their segments
   if (int rc = encode_tensor_map_2d(&tm_x, DT_BF16, const_cast<void *>(x), (uint64_t)g.n,
                                     (uint64_t)(batch * g.s), (uint64_t)g.n * 2, 64, 128, true))
@@ -618,6 +566,9 @@ int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16
     return rc;
   const int sw = y_dtype == DT_BF16 ? (int)CU_TENSOR_MAP_SWIZZLE_64B : (int)CU_TENSOR_MAP_SWIZZLE_128B;
   if (int rc = encode_tensor_map_2d_sw(&tm_y, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
+                                       (uint64_t)g.r_dim * E, 32, 32, sw))
+    return rc;
+  if (int rc = encode_tensor_map_2d_sw(&tm_y16, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
                                        (uint64_t)g.r_dim * E, 32, 16, sw))
     return rc;
   SlabFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(act) : pick_act<DT_F32>(act);
@@ -640,7 +591,7 @@ int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16
   cudaEvent_t ev_b = nullptr, ev_a = nullptr;  // dt_profile_kernel_events
   profile_next(&ev_b, &ev_a, DT_PROF_ROWS);
   if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
-  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, tm_y, p));
+  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tm_x, tm_wf, tm_xf2, tm_y, tm_y16, p));
   if (ev_a) DT_CUDA_CHECK(cudaEventRecord(ev_a, st));
   if (tracing) {  // every CTA's stamps, raw, to DEEPTHIN_ROWS_TRACE_FILE (scripts/rows_trace.py)
     std::vector<unsigned long long> h((size_t)ncta * kTr);

@@ -34,15 +34,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
+#ifdef DEEPTHIN_TEST_WAIT
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a protocol bug traps (launch error) instead of hanging the GPU.
+// Wait for the phase with the given parity. The loop must stay the bare `while (!try_wait)`:
+// measured on B200 (scripts/microbench_mbar2.cu, the row kernels' issuer / producer / 16
+// epilogue-warp handshake), ANY extra exit in the polling loop — a spin counter with trap or
+// printf, a clock bound, an unrolled counter, the same loop written in PTX — makes ptxas emit
+// YIELD + reconvergence code around the TRYWAIT and the handshake costs 380-480 clocks per
+// iteration instead of 173, whatever the ring depth. Builds with -DDEEPTHIN_BOUNDED_WAITS
+// (DEEPTHIN_BOUNDED_WAITS=1 python -m paper_1802_06944_b200.build --force) keep the bounded
+// loop: a protocol bug then traps (launch error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef DEEPTHIN_BOUNDED_WAITS
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins == (1u << 26)) {
@@ -50,6 +62,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       __trap();
     }
   }
+#else
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
 }
 
 // Wait with nanosleep back-off: for long waits of otherwise idle warps (keeps their issue
@@ -133,23 +149,30 @@ __device__ __forceinline__ void cluster_sync() {
 }
 // Wait with cluster-scope acquire (the arrivals come from other CTAs of the cluster, released
 // at cluster scope after their distributed-shared-memory stores).
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+#ifdef DEEPTHIN_BOUNDED_WAITS
   uint32_t spins = 0;
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) return;
+  while (!mbar_try_wait_cluster(bar, parity)) {
     if (++spins == (1u << 26)) {
       printf("deepthin: cluster mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
       __trap();
     }
   }
+#else
+  while (!mbar_try_wait_cluster(bar, parity)) {  // bare loop: see mbar_wait
+  }
+#endif
 }
 // Relaxed arrives (no memory ordering): for "this warp's TMEM reads are done" signals. The
 // reads completed at tcgen05.wait::ld, so nothing needs releasing — and a release arrive would
@@ -285,6 +308,17 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)
         "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
         "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit columns: thread t of the warp gets lane (base+t).
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
       : "r"(taddr)
       : "memory");
 }

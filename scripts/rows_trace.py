@@ -65,6 +65,11 @@ def summarise(path):
     t0 = h[:, 0][h[:, 0] > 0].min()
     us = np.where(h > 0, (h - t0) * 1e-3, np.nan)
     if cs == 1 and np.any(~np.isnan(us[:, 62])):
+        for g in range(2):  # clock64 around the phase-B loop of group g (slots 56+g / 58+g)
+            d = h[:, 58 + g] - h[:, 56 + g]
+            d = d[h[:, 58 + g] > 0]
+            if d.size:
+                print(f"  phase-B loop of group {g}: median {np.median(d):.0f} SM clocks")
         return summarise_slab(us, nb, n_tiles, n_chunks, s)
     print(f"grid {nb} CTAs (clusters of {cs}), {n_tiles} tiles, {n_chunks} chunks, s {s}")
 
