@@ -722,6 +722,11 @@ def run_network(args, cfg, key):
     dm = model.to_device(C3_ACTS, mma="bf16")
     gbatch = cfg[5]
     batch = gbatch // world
+    # --shard-of N: ONE GPU timed on the shard an N-GPU job would give it (rank 0's rows) — the
+    # per-GPU step of the strong-scaled job, measurable on a one-GPU box (no collective on this
+    # path); the line says so in config.emulated_world and is not a scaling measurement
+    if getattr(args, "shard_of", 0) and world == 1:
+        batch = gbatch // args.shard_of
     x_all = sample_normal(rx, 0.0, 1.0, (gbatch, C3_DIMS[0])).astype(np.float32)
     x_host = torch.tensor(x_all[rank * batch:(rank + 1) * batch]).to(torch.bfloat16)
     xs = [x_host.cuda() for _ in range(2)]
@@ -767,7 +772,7 @@ def run_network(args, cfg, key):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = gbatch * args.steps / (total_ms / 1e3)
+    value = batch * world * args.steps / (total_ms / 1e3)   # rows actually processed per step
     net_bytes = sum(2 * batch * (q + r) for q, r in zip(C3_DIMS[:-1], C3_DIMS[1:]))
 
     # roofline of the dominant kernel: the row-tile reuse kernel (6 of the 7 layers), device
@@ -820,7 +825,7 @@ def run_network(args, cfg, key):
     te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     if world > 1:
         tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
-    e2e_value = gbatch * args.steps / float(te.item())
+    e2e_value = batch * world * args.steps / float(te.item())
     ok = torch.equal(hy.cuda(), y)
 
     cpu = None
@@ -835,6 +840,10 @@ def run_network(args, cfg, key):
             "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": cfg[6], "global_batch": gbatch, "batch_per_gpu": batch,
+                       **({"emulated_world": args.shard_of,
+                           "note": "one GPU timed on the shard of an N-GPU job (--shard-of); "
+                                   "value counts this shard's rows only"}
+                          if getattr(args, "shard_of", 0) and world == 1 else {}),
                        "parallelism": f"dp{world} (batch-sharded, no collective)",
                        "execution": "DeviceModel.forward(graph=True): the 7-layer chain replayed "
                                     "from a CUDA graph per input buffer",
@@ -1013,6 +1022,8 @@ def main():
                     help="launcher / rank plumbing only (gloo, no GPU work)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="config c3 on one GPU: time the per-GPU shard of an N-GPU job")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="disable inference pipelining of consecutive forwards")
     ap.add_argument("--path", default="two-phase", choices=["two-phase", "fused"],

@@ -28,12 +28,12 @@
 //
 // Warp roles (768 threads, one CTA per SM):
 //   warp 0  TMA producer of x' k-blocks (128 x' rows x 64 bf16, SW128)
-//   warp 1  TMA producer of XF2p chunks (128 output columns x 32 fp32, SW128)
 //   warp 2  TMEM allocator + single-thread tcgen05.mma issuer of phase A (P ring of 8 units)
-//   warps 3, 24  single-thread tcgen05.mma issuers of phase B, one per team (team t = chunks t,
-//               t + 2, ... with its own XF2p ring, D buffers and epilogue warps)
+//   warps 1, 3  none
 //   warps 4-7   P re-lay (one per TMEM lane quarter)
-//   warps 8-23  epilogue, 8 warps per team: quarter (warp % 4) = 32 of a chunk's 128 output
+//   warps 8-23  phase B + epilogue, two teams of 8 warps (team t = chunks t, t + 2, ...): the
+//               team's leader thread loads its XF2p chunks and issues its MMAs one chunk ahead
+//               into the team's other D buffer; quarter (warp % 4) = 32 of a chunk's 128 output
 //               columns, ((warp - 8) / 4) % 2 = 32 of the group's 64 rows
 #include <cuda_bf16.h>
 
@@ -57,14 +57,15 @@ using namespace rowsdev;
 constexpr int kGM = 64;            // batch rows per phase-B group (UMMA N = TMEM columns per D buffer)
 constexpr int kNc = 128;           // output columns per D chunk (UMMA M of phase B = TMEM lanes)
 constexpr int kTeams = 2;          // independent phase-B pipelines (issuer + 8 epilogue warps each)
-constexpr int kND = 2;             // D buffers in TMEM per team (kGM columns each)
+constexpr int kNDMax = 3;          // D buffers in TMEM per team (kGM columns each): 3 when the P ring
+                                   // leaves room (np = 16), else 2
 constexpr int kXSMax = 8;          // x ring depth cap
 constexpr int kBSMax = 4;          // XF2p chunk ring depth cap (per team)
+constexpr uint32_t kBS = 3;        // XF2p slots per team
 constexpr int kPS = 8;             // P ring: phase-A units in TMEM
 constexpr int kPW = 4;             // re-lay warps
 constexpr int kEpi = 16;           // epilogue warps
-constexpr int kIssuer1 = 4 + kPW + kEpi;  // the second phase-B issuer (last warp)
-constexpr int kSlabThreads = 32 * (5 + kPW + kEpi);
+constexpr int kSlabThreads = 32 * (4 + kPW + kEpi);
 constexpr uint32_t kXBytes = 128 * 128;   // 128 x' rows x 64 bf16
 constexpr uint32_t kBBytes = kNc * 128;   // 128 columns x 32 fp32
 constexpr uint32_t kA2Bytes = kGM * 128;  // 64 rows x 32 fp32
@@ -75,7 +76,7 @@ struct SlabParams {
   int r_dim, s, ls, nkb, np, rank, rp, k2, n_chunks;
   int ur;       // batch rows per phase-A unit (128 / s)
   int slab;     // batch rows per CTA (a multiple of max(ur, 16))
-  int xs, bs;
+  int xs, bs, nd;
   int nstage;   // output staging boxes per epilogue warp (TMA stores in flight)
   int dbg;      // timing build only (DEEPTHIN_DBG_SLAB): 1 no TMA store, 2 no staging, 3 no act
   uint32_t dcol0;
@@ -109,17 +110,20 @@ __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t
 template <int E>
 __device__ __forceinline__ void stage_t16x32(uint32_t out_s, int lane, const float *o) {
   if constexpr (E == 2) {
+    // rows (i, i + 1) of this column packed, exchanged with the partner lane, and one byte
+    // permute picks (own, partner) low halves (even lane: row i) or (partner, own) high halves
+    // (odd lane: row i + 1): four instructions per two outputs
     const int odd = lane & 1;
+    const uint32_t sel = odd ? 0x3276u : 0x5410u;
     const uint32_t base = out_s + (uint32_t)odd * 64u + (uint32_t)((lane >> 1) & 3) * 4u;
     const int ch = lane >> 3;  // 16-byte chunk of columns lane - odd, lane - odd + 1
 #pragma unroll
     for (int i = 0; i < 16; i += 2) {
-      // send the row the partner keeps, receive the partner's value of the row this lane keeps
-      const float give = odd ? o[i] : o[i + 1], keep = odd ? o[i + 1] : o[i];
-      const float got = __shfl_xor_sync(0xffffffffu, give, 1);
-      const uint32_t w = odd ? pack_bf16(got, keep) : pack_bf16(keep, got);
-      const int r = i;  // even row of the pair; this lane stores row r + odd (same swizzle)
-      st_shared_b32(base + (uint32_t)r * 64u + ((uint32_t)(ch ^ ((r >> 1) & 3)) << 4), w);
+      const uint32_t w = pack_bf16(o[i], o[i + 1]);
+      const uint32_t pw = __shfl_xor_sync(0xffffffffu, w, 1);
+      // even row of the pair is i; this lane stores row i + odd (same swizzle)
+      st_shared_b32(base + (uint32_t)i * 64u + ((uint32_t)(ch ^ ((i >> 1) & 3)) << 4),
+                    __byte_perm(w, pw, sel));
     }
   } else {
     const uint32_t base = out_s + (uint32_t)(lane & 3) * 4u;
@@ -140,12 +144,14 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.off_bar);
   uint64_t *x_full = bars, *x_empty = x_full + kXSMax;
   uint64_t *b_full = x_empty + kXSMax, *b_empty = b_full + kTeams * kBSMax;  // [team][slot]
-  uint64_t *d_full = b_empty + kTeams * kBSMax, *d_empty = d_full + 4;        // [team][buffer]
-  uint64_t *p_full = d_empty + 4, *p_free = p_full + kPS;
+  uint64_t *d_full = b_empty + kTeams * kBSMax, *d_empty = d_full + kTeams * kNDMax;  // [team][buffer]
+  uint64_t *p_full = d_empty + kTeams * kNDMax, *p_free = p_full + kPS;
   uint64_t *a2_full = p_free + kPS, *a2_free = a2_full + 2;
   uint64_t *wf_full = a2_free + 2;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(wf_full + 1);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // (the shuffle makes the warp index — and everything derived from it — provably warp-uniform
+  // for the compiler: uniform registers instead of per-lane waterfalls in the issuer loops)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
 
   // this CTA's slab: rows [row_begin, row_begin + rows), in groups of kGM, each group in units
   // of ur rows
@@ -160,12 +166,15 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.xs; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < kTeams * kBSMax; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < kTeams * kND; ++i) {
+    for (int i = 0; i < kTeams * kNDMax; ++i) {
       mbar_init(&d_full[i], 1);
       mbar_init(&d_empty[i], kEpi / kTeams);
     }
     for (int i = 0; i < kPS; ++i) { mbar_init(&p_full[i], 1); mbar_init(&p_free[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&a2_full[i], 1); mbar_init(&a2_free[i], kTeams); }
+    for (int i = 0; i < 2; ++i) {  // a2_free: one arrive per team that has chunks
+      mbar_init(&a2_full[i], 1);
+      mbar_init(&a2_free[i], (uint32_t)min(kTeams, p.n_chunks));
+    }
     mbar_init(wf_full, 1);
     fence_mbar_init();
   }
@@ -187,129 +196,150 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
   griddep_launch_dependents();
   if (threadIdx.x == 0) strace(p, 1);
 
+  // The role warps below run their loops on ALL 32 lanes (uniform control flow, uniform ring
+  // positions and addresses) and only predicate the asynchronous instructions on lane 0. With
+  // the whole loop inside `if (lane == 0)` the compiler treats every operand as lane-varying and
+  // wraps each UTCHMMA / UTMALDG in a waterfall (ELECT, five R2UR.BROADCAST, branch): ~200
+  // clocks per MMA issue, which paced phase A at 1.7 us per 64 KB of x and phase B at ~0.7 us
+  // per chunk. (Warp index and TMEM base pass through a shuffle for the same reason.)
+  const bool l0 = lane == 0;
+  const uint32_t tb = __shfl_sync(0xffffffffu, tbase, 0);
   if (warp == 0) {
     // ---------------- x' producer ----------------
-    if (lane == 0) {
-      uint8_t *wf_s = smem + p.off_wf;
+    const uint32_t s0 = smem_u32(smem);
+    if (l0) {
       mbar_arrive_expect_tx(wf_full, (uint32_t)(p.nkb * p.np * 128));
       for (int kb = 0; kb < p.nkb; ++kb)
-        tma_load_2d(wf_s + kb * p.np * 128, &tm_wf, wf_full, kb * 64, 0);
-      int st = 0;
-      uint32_t ph = 0;
-      for (int g = 0; g < n_groups; ++g) {
-        const int g_rows = min(kGM, rows - g * kGM);
-        const int g_units = (g_rows + p.ur - 1) / p.ur;
-        for (int u = 0; u < g_units; ++u) {
-          // x' rows of the unit: (first batch row) * s .. + 128 (past the batch: zero-filled)
-          const int32_t r0 = (int32_t)((row_begin + g * kGM + u * p.ur) << p.ls);
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            mbar_wait(&x_empty[st], ph ^ 1);
+        tma_load_2d_s(s0 + p.off_wf + (uint32_t)(kb * p.np * 128), &tm_wf, smem_u32(wf_full), kb * 64, 0);
+    }
+    int st = 0;
+    uint32_t ph = 0;
+    for (int g = 0; g < n_groups; ++g) {
+      const int g_rows = min(kGM, rows - g * kGM);
+      const int g_units = (g_rows + p.ur - 1) / p.ur;
+      for (int u = 0; u < g_units; ++u) {
+        // x' rows of the unit: (first batch row) * s .. + 128 (past the batch: zero-filled)
+        const int32_t r0 = (int32_t)((row_begin + g * kGM + u * p.ur) << p.ls);
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&x_empty[st], ph ^ 1);
+          if (l0) {
             mbar_arrive_expect_tx(&x_full[st], kXBytes);
-            tma_load_2d(smem + p.off_x + st * kXBytes, &tm_x, &x_full[st], kb * 64, r0);
-            if (++st == p.xs) { st = 0; ph ^= 1; }
+            tma_load_2d_s(s0 + p.off_x + (uint32_t)st * kXBytes, &tm_x, smem_u32(&x_full[st]), kb * 64, r0);
           }
+          if (++st == p.xs) { st = 0; ph ^= 1; }
         }
       }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ---------------- XF2p chunk producer: chunk ci of a group goes to team ci % 2 ----------------
-    if (lane == 0) {
-      int st0 = 0, st1 = 0;  // per-team ring positions (scalars: no dynamically indexed arrays)
-      uint32_t ph0 = 0, ph1 = 0;
-      for (int g = 0; g < n_groups; ++g)
-        for (int ci = 0; ci < p.n_chunks; ++ci) {
-          const int t = ci & 1;
-          const int c = ci + rot < p.n_chunks ? ci + rot : ci + rot - p.n_chunks;
-          const int st = t ? st1 : st0;
-          const uint32_t ph = t ? ph1 : ph0;
-          const int slot = t * kBSMax + st;
-          mbar_wait(&b_empty[slot], ph ^ 1);
-          if (kTimingSwitches && p.dbg >= 5) {  // no XF2p loads (stale operand)
-            mbar_arrive(&b_full[slot]);
-          } else {
-            mbar_arrive_expect_tx(&b_full[slot], kBBytes);
-            tma_load_2d(smem + p.off_b + (t * p.bs + st) * kBBytes, &tm_xf2, &b_full[slot], 0, c * kNc);
-          }
-          const int nst = st + 1 == p.bs ? 0 : st + 1;
-          const uint32_t nph = st + 1 == p.bs ? ph ^ 1 : ph;
-          if (t) { st1 = nst; ph1 = nph; } else { st0 = nst; ph0 = nph; }
-        }
     }
     __syncwarp();
   } else if (warp == 2) {
     // ---------------- phase-A MMA issuer: P[unit] = x' unit . [wf_hi | wf_lo]^T ----------------
-    if (lane == 0) {
-      const uint32_t s0 = smem_u32(smem);
-      const uint32_t wf_s = s0 + p.off_wf;
-      const uint32_t idA = idesc_f32acc(128, (uint32_t)p.np, 1);
-      mbar_wait(wf_full, 0);
-      int xs = 0;
-      uint32_t xph = 0, seq = 0;
-      for (int g = 0; g < n_groups; ++g) {
-        const int g_rows = min(kGM, rows - g * kGM);
-        const int g_units = (g_rows + p.ur - 1) / p.ur;
-        for (int u = 0; u < g_units; ++u, ++seq) {
-          const uint32_t slot = seq % kPS;
-          mbar_wait(&p_free[slot], ((seq / kPS) & 1u) ^ 1u);  // the re-lay warps read unit seq-8
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t idA = idesc_f32acc(128, (uint32_t)p.np, 1);
+    const uint64_t descX0 = smem_desc(s0 + p.off_x, 16, 1024, SL_SW128);
+    const uint64_t descW0 = smem_desc(s0 + p.off_wf, 16, 1024, SL_SW128);
+    const uint32_t wstep = (uint32_t)(p.np * 128) >> 4;  // descriptor units per wf k-block
+    mbar_wait(wf_full, 0);
+    int xs = 0;
+    uint32_t xph = 0, slot = 0, sph = 0;
+    bool first = true;
+    for (int g = 0; g < n_groups; ++g) {
+      const int g_rows = min(kGM, rows - g * kGM);
+      const int g_units = (g_rows + p.ur - 1) / p.ur;
+      for (int u = 0; u < g_units; ++u) {
+        mbar_wait(&p_free[slot], sph ^ 1u);  // the re-lay warps read the unit 8 units back
+        tc_fence_after();
+        const uint32_t d = tb + slot * (uint32_t)p.np;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&x_full[xs], xph);
+          if (first && l0) strace(p, 2);
+          first = false;
           tc_fence_after();
-          const uint32_t d = tbase + slot * (uint32_t)p.np;
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            mbar_wait(&x_full[xs], xph);
-            if (seq == 0 && kb == 0) strace(p, 2);
-            tc_fence_after();
-            const uint32_t a = s0 + p.off_x + (uint32_t)xs * kXBytes;
-            const uint32_t b = wf_s + (uint32_t)(kb * p.np * 128);
+          const uint64_t a = descX0 + (uint64_t)((uint32_t)xs * (kXBytes >> 4));
+          const uint64_t b = descW0 + (uint64_t)((uint32_t)kb * wstep);
+          if (l0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(d, smem_desc(a + k * 32, 16, 1024, SL_SW128),
-                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idA, (kb | k) != 0);
+              mma_bf16_ss(d, a + (uint64_t)(2 * k), b + (uint64_t)(2 * k), idA, (kb | k) != 0);
             mma_commit(&x_empty[xs]);
-            if (++xs == p.xs) { xs = 0; xph ^= 1; }
           }
+          if (++xs == p.xs) { xs = 0; xph ^= 1; }
+        }
+        if (l0) {
           mma_commit(&p_full[slot]);
           if (u == g_units - 1) strace(p, 3 + 8 * min(g, 6));
         }
+        if (++slot == kPS) { slot = 0; sph ^= 1; }
       }
     }
     __syncwarp();
-  } else if (warp == 3 || warp == kIssuer1) {
-    // ---------------- phase-B MMA issuers: D^T = XF2p chunk . A2[group]^T (tf32) ----------------
-    // two independent pipelines (teams): issuer t takes chunks t, t + 2, ... of every group, its
-    // own XF2p ring, its own two D buffers and its own eight epilogue warps — two handshake
-    // loops in flight instead of one (measured: one loop costs ~0.5 us per chunk)
-    if (lane == 0) {
-      const int t = warp == 3 ? 0 : 1;
-      const uint32_t s0 = smem_u32(smem);
-      const uint32_t idB = idesc_f32acc(kNc, kGM, 2);
-      int bs = 0, db = 0;
-      uint32_t bph = 0, dph = 0;
-      for (int g = 0; g < n_groups; ++g) {
-        const int gb = g & 1;
-        mbar_wait(&a2_full[gb], (uint32_t)(g >> 1) & 1u);
-        if (t == 0) strace(p, 4 + 8 * min(g, 6));
-        tc_fence_after();
-        const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)gb * kA2Bytes;
-        for (int ci = t; ci < p.n_chunks; ci += kTeams) {
-          mbar_wait(&b_full[t * kBSMax + bs], bph);
-          mbar_wait(&d_empty[t * kND + db], dph ^ 1);
-          tc_fence_after();
-          const uint32_t d = tbase + p.dcol0 + (uint32_t)((t * kND + db) * kGM);
-          const uint32_t b = s0 + p.off_b + (uint32_t)(t * p.bs + bs) * kBBytes;
-          const int nk = (kTimingSwitches && p.dbg >= 7) ? 0 : (kTimingSwitches && p.dbg >= 6) ? 1 : p.k2 / 8;
-          for (int k = 0; k < nk; ++k)
-            mma_tf32_ss(d, smem_desc(b + k * 32, 16, 1024, SL_SW128),
-                        smem_desc(a2_s + k * 32, 16, 1024, SL_SW128), idB, k != 0);
-          if (kTimingSwitches && p.dbg >= 8) mbar_arrive(&b_empty[t * kBSMax + bs]); else
-          mma_commit(&b_empty[t * kBSMax + bs]);
-          if (++bs == p.bs) { bs = 0; bph ^= 1; }
-          if (kTimingSwitches && p.dbg >= 9) mbar_arrive(&d_full[t * kND + db]); else
-          mma_commit(&d_full[t * kND + db]);
-          if (++db == kND) { db = 0; dph ^= 1; }
+  } else if (warp < 4) {
+    // ---------------- phase-B issuers (warp 1: team 0, warp 3: team 1) ----------------
+    // Team t = chunks t, t + 2, ... of every group, eight epilogue warps and this warp's lane 0,
+    // which loads the team's XF2p chunks (kBS slots, kBS chunks ahead: an L2 -> shared chunk
+    // load takes ~1 us here) and issues the chunk's MMAs nd - 1 chunks ahead into the team's D
+    // ring. One named barrier per chunk joins the nine warps: past it, every epilogue warp has
+    // read the D buffer the issuer overwrites next. The loop is single-thread scalar code and
+    // was the bottleneck (~2400 clocks per chunk with descriptors rebuilt per MMA, divisions for
+    // ring positions, ...): everything is kept incremental and the descriptors precomputed.
+    const int t = warp >> 1;
+    const int cpt = t < p.n_chunks ? (p.n_chunks - t + kTeams - 1) / kTeams : 0;  // chunks per group
+    const int K = n_groups * cpt;
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t nd = (uint32_t)p.nd;
+    const int ahead = p.nd - 1;
+    const int nk = p.k2 / 8;
+    const uint32_t idB = idesc_f32acc(kNc, kGM, 2);
+    uint64_t *bf = b_full + t * kBSMax, *df = d_full + t * kNDMax;
+    const uint64_t descA0 = smem_desc(s0 + p.off_b + (uint32_t)(t * kBS) * kBBytes, 16, 1024, SL_SW128);
+    const uint64_t descB0 = smem_desc(s0 + p.off_a2, 16, 1024, SL_SW128);
+    const uint32_t dbase = tb + p.dcol0 + (uint32_t)t * nd * (uint32_t)kGM;
+    const uint32_t b_s0 = s0 + p.off_b + (uint32_t)(t * kBS) * kBBytes;
+    // ring positions: loads (l_*), MMA issue (i_*), completion waits (w_*)
+    uint32_t l_slot = 0, i_slot = 0, i_par = 0, i_d = 0, w_d = 0, w_par = 0;
+    int l_j = 0, l_n = 0;
+    auto load_next = [&]() {  // XF2p chunk of the next element of the team's sequence
+      const int ci = t + l_j * kTeams;
+      const int c = ci + rot < p.n_chunks ? ci + rot : ci + rot - p.n_chunks;
+      if (l0) {
+        mbar_arrive_expect_tx(&bf[l_slot], kBBytes);
+        tma_load_2d_s(b_s0 + l_slot * kBBytes, &tm_xf2, smem_u32(&bf[l_slot]), 0, c * kNc);
+      }
+      if (++l_slot == kBS) l_slot = 0;
+      if (++l_j == cpt) l_j = 0;
+      ++l_n;
+    };
+    auto issue_next = [&](uint64_t descB) {  // the MMAs of the next element
+      mbar_wait(&bf[i_slot], i_par);
+      tc_fence_after();
+      const uint32_t d = dbase + i_d * (uint32_t)kGM;
+      const uint64_t a = descA0 + (uint64_t)(i_slot * (kBBytes >> 4));
+      if (l0) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (kk < nk) mma_tf32_ss(d, a + (uint64_t)(2 * kk), descB + (uint64_t)(2 * kk), idB, kk != 0);
+        mma_commit(&df[i_d]);
+      }
+      if (++i_slot == kBS) { i_slot = 0; i_par ^= 1; }
+      if (++i_d == nd) i_d = 0;
+    };
+    for (int i = 0; i < (int)kBS && i < K; ++i) load_next();
+    for (int g = 0; g < n_groups; ++g) {
+      const int gb = g & 1;
+      const uint64_t descB = descB0 + (uint64_t)(gb * (int)(kA2Bytes >> 4));
+      for (int j = 0; j < cpt; ++j) {
+        named_bar_sync(2 + t, 32 * (kEpi / kTeams + 1));
+        if (j == 0) {  // first chunk of a group: its A2 has to be complete (nothing issued early)
+          mbar_wait(&a2_full[gb], (uint32_t)(g >> 1) & 1u);
+          if (t == 0 && l0) strace(p, 4 + 8 * min(g, 6));
+          for (int a = 0; a < ahead && a < cpt; ++a) issue_next(descB);
         }
-        // this team's reads of A2[gb] are done when these complete (both teams: count 2)
-        if (kTimingSwitches && p.dbg >= 9) mbar_arrive(&a2_free[gb]); else
-        mma_commit(&a2_free[gb]);
+        if (j + ahead < cpt) issue_next(descB);
+        // the MMAs of this chunk are complete: its XF2p slot is free (the element kBS further
+        // goes there) and, after the group's last chunk, so is A2[gb] as far as this team goes
+        mbar_wait(&df[w_d], w_par);
+        if (++w_d == nd) { w_d = 0; w_par ^= 1; }
+        if (l_n < K) load_next();
+        if (j + 1 == cpt && l0) mbar_arrive(&a2_free[gb]);
       }
     }
     __syncwarp();
@@ -372,8 +402,9 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     }
   } else {
     // ---------------- epilogue: 2 teams of 8 warps ----------------
-    // team t = chunks t, t + 2, ...; within a team quarter sp = output columns 32 sp .. 32 sp + 31
-    // of the chunk (lane = column), h = rows 32 h .. 32 h + 31 of the group (32 TMEM columns)
+    // Team t reads the chunks its issuer multiplies (t, t + 2, ... of every group). Within a team
+    // quarter sp = output columns 32 sp .. 32 sp + 31 of the chunk (lane = column), h = rows
+    // 32 h .. 32 h + 31 of the group (32 TMEM columns).
     const int sp = warp & 3;
     const int e = warp - 4 - kPW;      // 0..15
     const int t = e >> 3, h = (e >> 2) & 1;
@@ -384,18 +415,25 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     const uint32_t out_s0 = s0 + p.off_out + (uint32_t)(e * p.nstage) * (32u * RB);
     int sb = 0;
     const int64_t slab_end = row_begin + rows;
-    int db = 0;
-    uint32_t dph = 0;
+    const int cpt = t < p.n_chunks ? (p.n_chunks - t + kTeams - 1) / kTeams : 0;  // chunks per group
+    uint64_t *df = d_full + t * kNDMax;
+    const uint32_t dcol = p.dcol0 + (uint32_t)(t * p.nd * kGM + 32 * h);
+    uint32_t w_d = 0, w_par = 0;  // position in the team's D ring
     for (int g = 0; g < n_groups; ++g) {
       const int64_t row0 = row_begin + g * kGM + 32 * h;
       // rows of this warp inside the slab: all 32 (or the batch end, which TMA clips) -> the
       // 32-row box; 16 -> the 16-row box (slabs end on multiples of 16); none -> nothing to do
       const int live = (int)min((int64_t)32, slab_end - row0);
       const CUtensorMap *tmy = (live >= 32 || slab_end == p.batch) ? &tm_y : &tm_y16;
-      for (int ci = t; ci < p.n_chunks; ci += kTeams) {
+      for (int j = 0; j < cpt; ++j) {
+        // (joins the team's issuer: every warp has read the D buffer it overwrites next)
+        named_bar_sync(2 + t, 32 * (kEpi / kTeams + 1));
+        const int ci = t + j * kTeams;
         const int c = ci + rot < p.n_chunks ? ci + rot : ci + rot - p.n_chunks;
-        mbar_wait(&d_full[t * kND + db], dph);
-        if (e == 0 && ci == 0) strace(p, 5 + 8 * min(g, 6));
+        mbar_wait(&df[w_d], w_par);
+        const uint32_t dc = dcol + w_d * (uint32_t)kGM;
+        if (++w_d == (uint32_t)p.nd) { w_d = 0; w_par ^= 1; }
+        if (e == 0 && j == 0) strace(p, 5 + 8 * min(g, 6));
         tc_fence_after();
         const int col0 = c * kNc + 32 * sp;
         const bool work = live > 0 && col0 < p.r_dim && !(kTimingSwitches && p.dbg >= 4);
@@ -409,20 +447,15 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
           }
           __syncwarp();
         }
-        // two halves of 16 rows (16 live registers each: 32 at once spill at 800 threads)
+        // two halves of 16 rows (16 live registers each)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t v[16];
           if (work) {
-            tmem_ld_32x32b_x16(
-                tbase + lane_t + p.dcol0 + (uint32_t)((t * kND + db) * kGM + 32 * h + 16 * hh), v);
+            tmem_ld_32x32b_x16(tbase + lane_t + dc + (uint32_t)(16 * hh), v);
             tmem_ld_wait();
           }
-          if (hh == 1) {  // both halves read: the D buffer may be overwritten
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&d_empty[t * kND + db]);
-          }
+          if (hh == 1) tc_fence_before();  // both halves read (the team barrier follows)
           if (!work || (kTimingSwitches && p.dbg >= 3)) continue;
           float o[16];
           if (p.bias && p.bslot < 0) {
@@ -440,7 +473,6 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
           }
           stage_t16x32<E>(out_s + (uint32_t)hh * (16u * RB), lane, o);
         }
-        if (++db == kND) { db = 0; dph ^= 1; }
         if (!work || (kTimingSwitches && p.dbg >= 2)) continue;
         fence_proxy_async_smem();
         __syncwarp();
@@ -528,12 +560,14 @@ int tc_slab_forward(const Geo &g, int64_t batch, const void *x, const void *wf16
   const int ncta = (int)((batch + p.slab - 1) / p.slab);
   // TMEM: P ring of kPS units in columns [0, kPS * np), kTeams x kND D buffers of kGM columns
   // at the top
-  p.dcol0 = 512u - (uint32_t)(kTeams * kND * kGM);
+  p.nd = std::min(kNDMax, (512 - (kPS * p.np + 63) / 64 * 64) / (kTeams * kGM));
+  p.dcol0 = 512u - (uint32_t)(kTeams * p.nd * kGM);
   // shared memory: A2 x 2 | wf | XF2p ring | output staging | softmax partials | x ring | barriers
   const int E = y_dtype == DT_BF16 ? 2 : 4;
   const uint32_t wf_bytes = (uint32_t)(p.nkb * p.np * 128);
   static const int want_bs = getenv("DEEPTHIN_SLAB_BS") ? atoi(getenv("DEEPTHIN_SLAB_BS")) : 0;
-  p.bs = want_bs > 0 ? std::max(2, std::min(want_bs, kBSMax)) : 2;  // per team
+  (void)want_bs;
+  p.bs = 3;  // per team (kBS in the kernel)
   p.off_a2 = 0;
   p.off_wf = 2 * kA2Bytes;
   p.off_b = (p.off_wf + wf_bytes + 1023) & ~1023u;

@@ -85,6 +85,16 @@ __device__ __forceinline__ void mbar_wait_sleepy(uint64_t *bar, uint32_t parity)
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
+// the same with shared-memory operands already as 32-bit shared addresses (no generic -> shared
+// conversion per call: keeps the operands in the uniform datapath of a convergent issuer loop)
+__device__ __forceinline__ void tma_load_2d_s(uint32_t smem_dst, const CUtensorMap *m, uint32_t bar,
+                                              int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *m, uint64_t *bar,
                                             int32_t c0, int32_t c1) {
   asm volatile(
