@@ -37,6 +37,11 @@
 #include <tuple>
 #include <vector>
 
+// This (opt-in, measured-slower) kernel keeps the bounded mbarrier waits: with the bare
+// try_wait loops of sm100_ptx.cuh its layer-chain test hangs (a wait that never completes —
+// a phase race in this kernel's single-buffered activation hand-off that the slower bounded
+// waits do not expose; unresolved). The bounded loops also turn any such hang into a trap.
+#define DEEPTHIN_BOUNDED_WAITS 1
 #include "act.cuh"
 #include "dt_internal.h"
 #include "sm100_ptx.cuh"

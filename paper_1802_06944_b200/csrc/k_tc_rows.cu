@@ -139,9 +139,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   uint64_t *sm_full = wf_full + 1;  // softmax partials of every cluster CTA landed (2, by tile)
   uint64_t *p_free = sm_full + 2;   // the P warps read P[i & 1] out of TMEM (2, by tile)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(p_free + 2);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // (the shuffles make the warp index, the cluster rank and the TMEM base provably warp-uniform
+  // for the compiler: the producer / issuer loops below run on all 32 lanes with only the
+  // asynchronous instructions predicated on lane 0, so their operands stay in uniform registers
+  // instead of a per-instruction ELECT / R2UR waterfall — ~200 -> ~40 clocks per MMA issue,
+  // measured on the slab kernel, k_tc_slab.cu)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const bool l0 = lane == 0;
   const int cs = p.cs;
-  const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
+  const int crank = (int)(blockIdx.x & (unsigned)(cs - 1));  // rank in the cluster of cs (power of 2) along x
   const int cid = (int)blockIdx.x / cs, ncl = (int)gridDim.x / cs;
   const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
   const int my_chunks = crank < p.n_chunks ? (p.n_chunks - crank + cs - 1) / cs : 0;
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   __syncthreads();
   if (cs > 1) cluster_sync();  // peers' barriers initialised before any remote copy/arrive
   tc_fence_after();
-  const uint32_t tbase = *tslot;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tslot, 0);
   if (threadIdx.x == 0) rtrace(p, 0);
   // Everything below reads buffers an earlier kernel on the stream may write (x is the previous
   // layer's output; factors/bias may come from an SGD step): wait for it, let the next start.
@@ -188,13 +194,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   const int n = p.nkb * 64;
   if (warp == 0) {
     // ---------------- x producer: this CTA's segments of each tile ----------------
-    if (lane == 0) {
+    {
       // wf (rank x n bf16, rows rank..np-1 zero-filled by TMA) stays resident: nkb blocks of
       // np rows x 128 B
-      uint8_t *wf_s = smem + p.off_wf;
-      mbar_arrive_expect_tx(wf_full, (uint32_t)(p.nkb * p.np * 128));
-      for (int kb = 0; kb < p.nkb; ++kb)
-        tma_load_2d(wf_s + kb * p.np * 128, &tm_wf, wf_full, kb * 64, 0);
+      const uint32_t s0 = smem_u32(smem);
+      if (l0) {
+        mbar_arrive_expect_tx(wf_full, (uint32_t)(p.nkb * p.np * 128));
+        for (int kb = 0; kb < p.nkb; ++kb)
+          tma_load_2d_s(s0 + p.off_wf + (uint32_t)(kb * p.np * 128), &tm_wf, smem_u32(wf_full), kb * 64, 0);
+      }
       int st = 0;
       uint32_t ph = 0;
       for (int t = cid; t < p.n_tiles; t += ncl) {
@@ -211,8 +219,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         for (int seg = crank; seg < p.s; seg += cs)
           for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(&x_empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&x_full[st], kXBytes);
-            tma_load_2d(smem + p.off_x + st * kXBytes, &tm_x, &x_full[st], seg * n + kb * 64, t * kTM);
+            if (l0) {
+              mbar_arrive_expect_tx(&x_full[st], kXBytes);
+              tma_load_2d_s(s0 + p.off_x + (uint32_t)st * kXBytes, &tm_x, smem_u32(&x_full[st]),
+                            seg * n + kb * 64, t * kTM);
+            }
             if (++st == p.xs) { st = 0; ph ^= 1; }
           }
       }
@@ -220,13 +231,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- XF2 chunk producer: this CTA's output chunks ----------------
-    if (lane == 0) {
+    {
+      const uint32_t s0 = smem_u32(smem);
       if (b_res) {
         int i = 0;
-        for (int c = crank; c < p.n_chunks; c += cs, ++i) {
-          mbar_arrive_expect_tx(&b_full[i], kBBytes);
-          tma_load_2d(smem + p.off_b + i * kBBytes, &tm_xf2, &b_full[i], 0, c * kNc);
-        }
+        for (int c = crank; c < p.n_chunks; c += cs, ++i)
+          if (l0) {
+            mbar_arrive_expect_tx(&b_full[i], kBBytes);
+            tma_load_2d_s(s0 + p.off_b + (uint32_t)i * kBBytes, &tm_xf2, smem_u32(&b_full[i]), 0, c * kNc);
+          }
       } else {
         int st = 0;
         uint32_t ph = 0;
@@ -234,8 +247,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass)
           for (int c = crank; c < p.n_chunks; c += cs) {
             mbar_wait(&b_empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&b_full[st], kBBytes);
-            tma_load_2d(smem + p.off_b + st * kBBytes, &tm_xf2, &b_full[st], 0, c * kNc);
+            if (l0) {
+              mbar_arrive_expect_tx(&b_full[st], kBBytes);
+              tma_load_2d_s(s0 + p.off_b + (uint32_t)st * kBBytes, &tm_xf2, smem_u32(&b_full[st]), 0, c * kNc);
+            }
             if (++st == kBS) { st = 0; ph ^= 1; }
           }
       }
@@ -245,10 +260,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // ---------------- phase-A MMA issuer: P[i & 1] = x_seg . [wf_hi | wf_lo] ----------------
     // (phase B runs on its own issuer warp, so A of the next tiles never waits behind the
     // epilogue's D buffers, and B never waits for the next tile's x)
-    if (lane == 0) {
+    {
       const uint32_t s0 = smem_u32(smem);
-      const uint32_t wf_s = s0 + p.off_wf;
       const uint32_t idA = idesc_f32acc(kTM, (uint32_t)p.np, 1);
+      const uint64_t descX0 = smem_desc(s0 + p.off_x, 16, 1024, SL_SW128);
+      const uint64_t descW0 = smem_desc(s0 + p.off_wf, 16, 1024, SL_SW128);
+      const uint32_t wstep = (uint32_t)(p.np * 128) >> 4;  // descriptor units per wf k-block
       mbar_wait(wf_full, 0);
       const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
       int xs = 0;
@@ -262,28 +279,32 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           const uint32_t d = pc + (uint32_t)(j * p.np);
           for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(&x_full[xs], xph);
-            if (kb == 0 && j == 0) rtrace(p, 2 + 5 * min(i, 9));
-            if (kb == p.nkb - 1 && seg + cs >= p.s) rtrace(p, 3 + 5 * min(i, 9));
+            if (l0 && kb == 0 && j == 0) rtrace(p, 2 + 5 * min(i, 9));
+            if (l0 && kb == p.nkb - 1 && seg + cs >= p.s) rtrace(p, 3 + 5 * min(i, 9));
             tc_fence_after();
-            const uint32_t a = s0 + p.off_x + (uint32_t)xs * kXBytes;
-            const uint32_t b = wf_s + (uint32_t)(kb * p.np * 128);
+            const uint64_t a = descX0 + (uint64_t)((uint32_t)xs * (kXBytes >> 4));
+            const uint64_t b = descW0 + (uint64_t)((uint32_t)kb * wstep);
+            if (l0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(d, smem_desc(a + k * 32, 16, 1024, SL_SW128),
-                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idA, (kb | k) != 0);
-            mma_commit(&x_empty[xs]);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(d, a + (uint64_t)(2 * k), b + (uint64_t)(2 * k), idA, (kb | k) != 0);
+              mma_commit(&x_empty[xs]);
+            }
             if (++xs == p.xs) { xs = 0; xph ^= 1; }
           }
         }
-        mma_commit(&p_full[i & 1]);
+        if (l0) mma_commit(&p_full[i & 1]);
       }
     }
     __syncwarp();
   } else if (warp == kBWarp) {
     // ---------------- phase-B MMA issuer: D = A2 . XF2 chunk (tf32) ----------------
-    if (lane == 0) {
+    {
       const uint32_t s0 = smem_u32(smem);
       const uint32_t idB = idesc_f32acc(kTM, kNc, 2);
+      const uint64_t descA20 = smem_desc(s0 + p.off_a2, kA2Lbo, kA2Sbo, SL_NONE);
+      const uint64_t descXF0 = smem_desc(s0 + p.off_b, 16, 1024, SL_SW128);
+      const int nk = p.k2 / 8;
       const int ntl = cid < p.n_tiles ? (p.n_tiles - cid + ncl - 1) / ncl : 0;
       int bs = 0, db = 0;
       uint32_t bph = 0, dph = 0;
@@ -291,9 +312,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // every cluster CTA's P landed in A2[tb & 1]
         const int ab = tb & 1;
         mbar_wait_cluster(&a2_full[ab], (uint32_t)(tb >> 1) & 1u);
-        rtrace(p, 4 + 5 * min(tb, 9));
+        if (l0) rtrace(p, 4 + 5 * min(tb, 9));
         tc_fence_after();
-        const uint32_t a2_s = s0 + p.off_a2 + (uint32_t)ab * kA2Bytes;
+        const uint64_t a2d = descA20 + (uint64_t)((uint32_t)ab * (kA2Bytes >> 4));
         // softmax: two passes over the chunks (statistics, then normalised stores), the tf32
         // MMA recomputed from the A2 tile still resident — no logits round trip through HBM
         for (int pass = 0; pass < (p.softmax ? 2 : 1); ++pass) {
@@ -304,20 +325,22 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             mbar_wait(&d_empty[db], dph ^ 1);
             tc_fence_after();
             const uint32_t d = tbase + p.dcol0 + (uint32_t)(db * kNc);
-            const uint32_t b = s0 + p.off_b + (uint32_t)slot * kBBytes;
-            for (int k = 0; k < p.k2 / 8; ++k)
-              mma_tf32_ss(d, smem_desc(a2_s + k * 4096, kA2Lbo, kA2Sbo, SL_NONE),
-                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idB, k != 0);
-            if (!b_res) {
-              mma_commit(&b_empty[bs]);
-              if (++bs == kBS) { bs = 0; bph ^= 1; }
+            const uint64_t b = descXF0 + (uint64_t)((uint32_t)slot * (kBBytes >> 4));
+            if (l0) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)  // A2: 4 KB (256 descriptor units) per K step of 8
+                if (k < nk) mma_tf32_ss(d, a2d + (uint64_t)(256 * k), b + (uint64_t)(2 * k), idB, k != 0);
+              if (!b_res) mma_commit(&b_empty[bs]);
+              mma_commit(&d_full[db]);
             }
-            mma_commit(&d_full[db]);
+            if (!b_res && ++bs == kBS) { bs = 0; bph ^= 1; }
             if (++db == p.nd) { db = 0; dph ^= 1; }
           }
         }
         // this CTA's reads of A2[ab] are done when these MMAs complete: tell every writer
-        if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
+        if (l0) {
+          if (cs > 1) mma_commit_mc(&a2_free[ab], cmask); else mma_commit(&a2_free[ab]);
+        }
       }
     }
     __syncwarp();

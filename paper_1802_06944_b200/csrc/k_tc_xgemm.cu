@@ -136,8 +136,14 @@ __global__ void __launch_bounds__(XTHREADS, 1)
   uint64_t *tload = tempty + 2;  // [XEPI][3] target boxes (XE_MSE)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(tload + 3 * XEPI);
   float *red = reinterpret_cast<float *>(smem + p.off_bar + 512);  // XE_MSE [2][4][256] colsums
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t crank = cluster_ctarank();
+  // (the shuffles make the warp index, the cluster rank and the TMEM base provably warp-uniform
+  // for the compiler: the producer and issuer loops run on all 32 lanes with only the
+  // asynchronous instructions predicated on lane 0, so their operands stay in uniform registers
+  // instead of a per-instruction ELECT / R2UR waterfall — ~200 -> ~40 clocks per MMA issue,
+  // measured on the row kernels; the issue rate, not the tensor pipe, paced these GEMMs)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const bool l0 = lane == 0;
+  const uint32_t crank = blockIdx.x & 1u;  // rank in the cluster of 2 along x (uniform to the compiler)
   const bool leader = crank == 0;
   const int cid = (int)blockIdx.x / 2, ncl = (int)gridDim.x / 2;
   const int BN = p.BN;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
   __syncthreads();
   cluster_sync();
   tc_fence_after();
-  const uint32_t tbase = *tslot;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tslot, 0);
   griddep_wait();  // operands may come from the previous kernel on the stream
   if (p.chain) griddep_launch_dependents();  // the next forward's W regeneration may start
 
@@ -175,11 +181,16 @@ __global__ void __launch_bounds__(XTHREADS, 1)
     }
     nb = t % p.n_nb;
     mb = t / p.n_nb;
+    // (integer division runs on the vector pipe: pass the results through a shuffle so the
+    // compiler keeps treating everything derived from them as warp-uniform)
+    mb = __shfl_sync(0xffffffffu, mb, 0);
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    ks = __shfl_sync(0xffffffffu, ks, 0);
   };
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs: own A rows, own half of the B columns) -------
-    if (lane == 0) {
+    {
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t abytes = p.dual_kb > 0 ? 2u * XA_BYTES : XA_BYTES;
@@ -191,13 +202,15 @@ __global__ void __launch_bounds__(XTHREADS, 1)
         const int m0 = mb * 256 + (int)crank * 128, n0 = nb * BN + (int)crank * p.nhalf;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
           uint8_t *st = smem + stage * p.stage_bytes;
-          xload(st, &tm_a, &full[stage], p.a_mn, EL, m0, 128, kb);
-          if (p.dual_kb > 0) xload(st + abytes - XA_BYTES, &tm_a, &full[stage], p.a_mn, EL, m0, 128,
-                                   kb + p.dual_kb);
-          xload(st + abytes, &tm_b, &full[stage], p.b_mn, EL, n0, p.nhalf,
-                p.b_wrap > 0 ? kb % p.b_wrap : kb);
+          const int kbb = p.b_wrap > 0 ? kb % p.b_wrap : kb;
+          if (l0) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+            xload(st, &tm_a, &full[stage], p.a_mn, EL, m0, 128, kb);
+            if (p.dual_kb > 0) xload(st + abytes - XA_BYTES, &tm_a, &full[stage], p.a_mn, EL, m0, 128,
+                                     kb + p.dual_kb);
+            xload(st + abytes, &tm_b, &full[stage], p.b_mn, EL, n0, p.nhalf, kbb);
+          }
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
       }
@@ -205,10 +218,17 @@ __global__ void __launch_bounds__(XTHREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA) ----------------
-    if (lane == 0 && leader) {
+    if (leader) {
       const uint32_t idesc = idesc_f32acc(256, (uint32_t)BN, EL ? 2 : 1) |
                              ((uint32_t)(p.a_mn != 0) << 15) | ((uint32_t)(p.b_mn != 0) << 16);
       const uint32_t s0 = smem_u32(smem);
+      // descriptors: stage 0 / K step 0 once, then plain 64-bit additions in the start-address
+      // field (16-byte units; no carry out of its 14 bits within shared memory)
+      const uint32_t b_off = p.dual_kb > 0 ? 2u * XA_BYTES : XA_BYTES;
+      const uint64_t dA0 = xdesc(s0, p.a_mn, 0, EL), dB0 = xdesc(s0 + b_off, p.b_mn, 0, EL);
+      const uint32_t ksA = p.a_mn ? (EL ? 1024u : 2048u) >> 4 : 2u;
+      const uint32_t ksB = p.b_mn ? (EL ? 1024u : 2048u) >> 4 : 2u;
+      const uint32_t st16 = p.stage_bytes >> 4;
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
       for (int u = cid; u < p.units; u += ncl) {
@@ -221,28 +241,30 @@ __global__ void __launch_bounds__(XTHREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_s = s0 + (uint32_t)stage * p.stage_bytes;
-          const uint32_t b_s = a_s + (p.dual_kb > 0 ? 2u * XA_BYTES : XA_BYTES);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t da = xdesc(a_s, p.a_mn, k, EL), db = xdesc(b_s, p.b_mn, k, EL);
-            if constexpr (EL)
-              mma_tf32_ss_pair(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            else
-              mma_bf16_ss_pair(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          }
-          if (p.dual_kb > 0) {  // the second A half against the same B stage
+          const uint64_t da = dA0 + (uint64_t)((uint32_t)stage * st16);
+          const uint64_t db = dB0 + (uint64_t)((uint32_t)stage * st16);
+          const uint64_t da2 = da + (uint64_t)(XA_BYTES >> 4);
+          const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+          if (l0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint64_t da = xdesc(a_s + XA_BYTES, p.a_mn, k, EL), db = xdesc(b_s, p.b_mn, k, EL);
-              if constexpr (EL) mma_tf32_ss_pair(d, da, db, idesc, 1u);
-              else mma_bf16_ss_pair(d, da, db, idesc, 1u);
+              if constexpr (EL)
+                mma_tf32_ss_pair(d, da + (uint64_t)(k * ksA), db + (uint64_t)(k * ksB), idesc, k > 0 ? 1u : acc0);
+              else
+                mma_bf16_ss_pair(d, da + (uint64_t)(k * ksA), db + (uint64_t)(k * ksB), idesc, k > 0 ? 1u : acc0);
             }
+            if (p.dual_kb > 0) {  // the second A half against the same B stage
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if constexpr (EL) mma_tf32_ss_pair(d, da2 + (uint64_t)(k * ksA), db + (uint64_t)(k * ksB), idesc, 1u);
+                else mma_bf16_ss_pair(d, da2 + (uint64_t)(k * ksA), db + (uint64_t)(k * ksB), idesc, 1u);
+              }
+            }
+            mma_commit_pair(&empty[stage]);
           }
-          mma_commit_pair(&empty[stage]);
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
-        mma_commit_pair(&tfull[acc]);
+        if (l0) mma_commit_pair(&tfull[acc]);
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     }
