@@ -88,7 +88,11 @@ __global__ void __launch_bounds__(uThreads, 1)
   uint64_t *d_full = b_empty + uBS, *d_empty = d_full + 2;
   uint64_t *p_full = d_empty + 2, *a2_full = p_full + 2, *a2_free = a2_full + 1;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(a2_free + 1);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // (warp index and TMEM base through a shuffle: provably warp-uniform for the compiler, so the
+  // producer / issuer loops — run on all 32 lanes, only the asynchronous instructions predicated
+  // on lane 0 — keep their operands in uniform registers: no per-MMA ELECT / R2UR waterfall)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const bool l0 = lane == 0;
   const int ntl = (int)blockIdx.x < p.n_tiles
                       ? (p.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   const uint32_t bbytes = (uint32_t)p.ka * uNc * 128u;
@@ -114,14 +118,14 @@ __global__ void __launch_bounds__(uThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tslot;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tslot, 0);
   griddep_wait();  // x is the previous layer's output; the operands come from the prep kernel
   griddep_launch_dependents();
   const uint32_t s0 = smem_u32(smem);
 
   if (warp == 0) {
     // ---------------- x + Wruns producer: per tile, nkb stages of (x k-block, Wruns k-block) ----
-    if (lane == 0) {
+    {
       int st = 0;
       uint32_t ph = 0;
       const uint32_t wbytes = (uint32_t)p.np * 128u;
@@ -129,10 +133,12 @@ __global__ void __launch_bounds__(uThreads, 1)
         const int t = (int)blockIdx.x + i * (int)gridDim.x;
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&x_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&x_full[st], (uint32_t)(uTM * 128) + wbytes);
-          uint8_t *sb = smem + p.off_x + st * p.stage_bytes;
-          tma_load_2d(sb, &tm_x, &x_full[st], kb * 64, t * uTM);
-          tma_load_2d(sb + uTM * 128, &tm_w, &x_full[st], kb * 64, 0);
+          const uint32_t sb = s0 + p.off_x + (uint32_t)st * p.stage_bytes;
+          if (l0) {
+            mbar_arrive_expect_tx(&x_full[st], (uint32_t)(uTM * 128) + wbytes);
+            tma_load_2d_s(sb, &tm_x, smem_u32(&x_full[st]), kb * 64, t * uTM);
+            tma_load_2d_s(sb + uTM * 128, &tm_w, smem_u32(&x_full[st]), kb * 64, 0);
+          }
           if (++st == uXS) { st = 0; ph ^= 1; }
         }
       }
@@ -140,25 +146,33 @@ __global__ void __launch_bounds__(uThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- XFfull chunk producer ----------------
-    if (lane == 0) {
+    {
       int st = 0;
       uint32_t ph = 0;
       for (int i = 0; i < ntl; ++i)
         for (int c = 0; c < p.n_chunks; ++c) {
           mbar_wait(&b_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&b_full[st], bbytes);
-          for (int a = 0; a < p.ka; ++a)
-            tma_load_2d(smem + p.off_b + st * bbytes + a * uNc * 128, &tm_xf, &b_full[st], a * 32,
-                        c * uNc);
+          if (l0) {
+            mbar_arrive_expect_tx(&b_full[st], bbytes);
+            for (int a = 0; a < p.ka; ++a)
+              tma_load_2d_s(s0 + p.off_b + (uint32_t)st * bbytes + (uint32_t)(a * uNc * 128), &tm_xf,
+                            smem_u32(&b_full[st]), a * 32, c * uNc);
+          }
           if (++st == uBS) { st = 0; ph ^= 1; }
         }
     }
     __syncwarp();
   } else if (warp == 2) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    {
       const uint32_t idA = idesc_f32acc(uTM, (uint32_t)p.np, 1);
       const uint32_t idB = idesc_f32acc(uTM, uNc, 2);
+      // descriptors once, then 64-bit additions in the start-address field (16-byte units)
+      const uint64_t dX0 = smem_desc(s0 + p.off_x, 16, 1024, SL_SW128);
+      const uint64_t dA20 = smem_desc(s0 + p.off_a2, 2048, 128, SL_NONE);
+      const uint64_t dB0 = smem_desc(s0 + p.off_b, 16, 1024, SL_SW128);
+      const uint32_t st16 = p.stage_bytes >> 4, bb16 = bbytes >> 4;
+      const int nk8 = p.k2 / 8;
       int xs = 0, bs = 0, db = 0;
       uint32_t xph = 0, bph = 0, dph = 0;
       for (int i = 0; i <= ntl; ++i) {
@@ -167,38 +181,39 @@ __global__ void __launch_bounds__(uThreads, 1)
           for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(&x_full[xs], xph);
             tc_fence_after();
-            const uint32_t a = s0 + p.off_x + (uint32_t)xs * p.stage_bytes;
-            const uint32_t b = a + uTM * 128;
+            const uint64_t a = dX0 + (uint64_t)((uint32_t)xs * st16);
+            const uint64_t b = a + (uint64_t)((uTM * 128) >> 4);
+            if (l0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(d, smem_desc(a + k * 32, 16, 1024, SL_SW128),
-                          smem_desc(b + k * 32, 16, 1024, SL_SW128), idA, (kb | k) != 0);
-            mma_commit(&x_empty[xs]);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(d, a + (uint64_t)(2 * k), b + (uint64_t)(2 * k), idA, (kb | k) != 0);
+              mma_commit(&x_empty[xs]);
+            }
             if (++xs == uXS) { xs = 0; xph ^= 1; }
           }
-          mma_commit(&p_full[i & 1]);
+          if (l0) mma_commit(&p_full[i & 1]);
         }
         if (i >= 1) {  // phase B of tile i-1: A2 (tf32 P') against every XFfull chunk
           mbar_wait(a2_full, (uint32_t)(i - 1) & 1u);
           tc_fence_after();
-          const uint32_t a2_s = s0 + p.off_a2;
           for (int c = 0; c < p.n_chunks; ++c) {
             mbar_wait(&b_full[bs], bph);
             mbar_wait(&d_empty[db], dph ^ 1);
             tc_fence_after();
             const uint32_t d = tbase + uDCol + (uint32_t)(db * uNc);
-            const uint32_t b = s0 + p.off_b + (uint32_t)bs * bbytes;
-            for (int k8 = 0; k8 < p.k2 / 8; ++k8)
-              mma_tf32_ss(d, smem_desc(a2_s + k8 * 4096, 2048, 128, SL_NONE),
-                          smem_desc(b + (uint32_t)(k8 >> 2) * uNc * 128u + (uint32_t)(k8 & 3) * 32u,
-                                    16, 1024, SL_SW128),
-                          idB, k8 != 0);
-            mma_commit(&b_empty[bs]);
+            const uint64_t b = dB0 + (uint64_t)((uint32_t)bs * bb16);
+            if (l0) {
+              for (int k8 = 0; k8 < nk8; ++k8)  // A2: 4 KB per K step; XFfull: 32 B, next atom every 4
+                mma_tf32_ss(d, dA20 + (uint64_t)(256 * k8),
+                            b + (uint64_t)((uint32_t)(k8 >> 2) * ((uNc * 128u) >> 4) + (uint32_t)(k8 & 3) * 2u),
+                            idB, k8 != 0);
+              mma_commit(&b_empty[bs]);
+              mma_commit(&d_full[db]);
+            }
             if (++bs == uBS) { bs = 0; bph ^= 1; }
-            mma_commit(&d_full[db]);
             if (++db == 2) { db = 0; dph ^= 1; }
           }
-          mma_commit(a2_free);  // the P warps may overwrite A2 with the next tile's P'
+          if (l0) mma_commit(a2_free);  // the P warps may overwrite A2 with the next tile's P'
         }
       }
     }

@@ -6,7 +6,7 @@ set -u
 mkdir -p gpurun_out/r02
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/r02/gpu.txt
 if [ "${SKIP_TESTS:-0}" != "1" ]; then
-  timeout -s KILL 1500 python -m pytest tests -m gpu -q --tb=short -rf > gpurun_out/r02/tests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/r02/tests.log
+  timeout -s KILL 1200 python -m pytest tests -m gpu -q --tb=short -rf --timeout 180 > gpurun_out/r02/tests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/r02/tests.log
   python __graft_entry__.py --smoke > gpurun_out/r02/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/r02/smoke.log
 fi
 for c in ${CONFIGS:-c3 c2 c1 c4 c5}; do
