@@ -77,6 +77,8 @@ struct RowsParams {
   int nd;              // D buffers in TMEM (2-3, 128 columns each, from column dcol0)
   uint32_t dcol0;
   int nstage;          // output staging boxes per epilogue warp (1-2, TMA stores in flight)
+  int wide;            // bf16 TMA epilogue in two teams of 8 warps on alternate chunks, each warp
+                       // 32 rows x 64 columns per chunk: 128-byte rows per TMA store request
   uint32_t off_sm;     // softmax: 2 x cs x 128 (max, sum) cluster partials
   uint32_t off_red;    // softmax: [4][128] column-warp partials
   int bslot;  // K slot carrying the bias (P = 1 there, XF2p = bias * scale), -1: epilogue adds it
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     for (int i = 0; i < kBS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], kEpi);
+      mbar_init(&d_empty[i], p.wide ? kEpi / 2 : kEpi);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&a2_full[i], 1);   // local arm (expect_tx of the peers' bytes)
@@ -539,6 +541,77 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
       }
       if (lane == 0) bulk_wait_group<0>();
+    } else if (p.wide) {
+      // bf16 outputs through TMA, two teams of 8 warps: team (n & 1) takes the CTA's n-th chunk
+      // (= D buffer n & 1, nd == 2), a warp 32 rows (its TMEM lane quarter) x 64 columns of it in
+      // two 32-column steps, staged as ONE 32 x 64 box of 128-byte rows: half the TMA store
+      // requests of the 32-column boxes (fp32 outputs — 128-byte rows, twice the bytes — take
+      // only 1.4x as long, which suggested a per-request cost), and the teams run out of phase
+      // (one reads TMEM while the other computes and stores). Opt-in (DEEPTHIN_ROWS_WIDE=1):
+      // measured no faster than the 32-column epilogue.
+      const int sp = warp & 3;
+      const int e = warp - 3 - kPW;      // 0..15
+      const int team = (e >> 2) & 1, half = e >> 3;
+      const uint32_t s0 = smem_u32(smem);
+      const uint32_t lane_t = (uint32_t)(32 * sp) << 16;
+      const uint32_t out_s = s0 + p.off_out + (uint32_t)e * 4096u;  // 32 rows x 128 bytes
+      const uint32_t rb = out_s + (uint32_t)lane * 128u;
+      const uint32_t dcol = p.dcol0 + (uint32_t)(team * kNc + 64 * half);
+      uint32_t n = 0, dph = 0, it = 0;
+      for (int t = cid; t < p.n_tiles; t += ncl, ++it) {
+        const int64_t row0 = (int64_t)t * kTM + 32 * sp;
+        for (int c = crank; c < p.n_chunks; c += cs, ++n) {
+          if ((int)(n & 1u) != team) continue;
+          mbar_wait(&d_full[team], dph);
+          dph ^= 1;
+          if (warp == 3 + kPW && c == crank) rtrace(p, 5 + 5 * (int)min(it, 9u));
+          tc_fence_after();
+          const int col0 = c * kNc + 64 * half;
+          if (lane == 0) bulk_wait_group_read<0>();  // the staging box's previous store has read it
+          __syncwarp();
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tbase + lane_t + dcol + (uint32_t)(32 * h2), v);
+            tmem_ld_wait();
+            if (h2 == 1) {  // both halves read: the D buffer may be overwritten
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&d_empty[team]);
+            }
+            const int colh = col0 + 32 * h2;
+            if (colh >= p.r_dim) continue;
+            float o[32];
+            if (p.bias && p.bslot < 0) {
+              constexpr float bsc = (YDT == DT_BF16 && ACT == DT_ACT_SIGMOID) ? 0.5f : 1.f;
+              const float bl = colh + lane < p.r_dim ? bsc * __ldg(p.bias + colh + lane) : 0.f;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]) + __shfl_sync(0xffffffffu, bl, i), p.arg);
+            } else {  // bias folded into the tf32 contraction (or absent)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = act_out<YDT, ACT>(__uint_as_float(v[i]), p.arg);
+            }
+            // this lane's row: 16-byte chunk ch of the 128-byte row at ch ^ (row & 7) (TMA SW128)
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+              const float *f = o + ch * 8;
+              st_shared_v4(rb + ((uint32_t)((4 * h2 + ch) ^ (lane & 7)) << 4), pack_bf16(f[0], f[1]),
+                           pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+            }
+          }
+          if (col0 >= p.r_dim) continue;
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm_y, smem + (out_s - s0), col0, (int32_t)row0);
+            bulk_commit_group();
+          }
+        }
+        if (warp == 3 + kPW) rtrace(p, 6 + 5 * (int)min(it, 9u));
+      }
+      if (lane == 0) bulk_wait_group<0>();  // staging read + y written before exit
+      if (warp == 3 + kPW) rtrace(p, 60);
     } else {
     // 16 warps: four per TMEM lane quarter, each owning 32 of the chunk's 128 columns
     const int sp = warp & 3;           // TMEM lane quarter this warp may access
@@ -852,7 +925,16 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.nd = std::max(2, std::min(want_nd, (int)(512 - (2 * p.pcols + 127) / 128 * 128) / (int)kNc));
   p.dcol0 = 512u - (uint32_t)p.nd * kNc;
   p.nstage = (want_stg == 2 && !p.softmax) ? 2 : 1;
-  p.off_x = p.off_out + (uint32_t)p.nstage * kEpi * 32u * 32u * (uint32_t)(y_dtype == DT_BF16 ? 2 : 4);
+  // wide bf16 epilogue (see the kernel), opt-in with DEEPTHIN_ROWS_WIDE=1: measured 28.96 vs
+  // 28.50 us per config-3 hidden layer — halving the TMA store requests does not pay, the x
+  // ring it shrinks (7 -> 5 stages) costs as much
+  static const int want_wide = getenv("DEEPTHIN_ROWS_WIDE") ? atoi(getenv("DEEPTHIN_ROWS_WIDE")) : 0;
+  static const int want_tma_y0 = getenv("DEEPTHIN_ROWS_TMA_Y") ? atoi(getenv("DEEPTHIN_ROWS_TMA_Y")) : 1;
+  p.wide = (want_wide && want_tma_y0 && y_dtype == DT_BF16 && !p.softmax && p.nd == 2 &&
+            !p.wait_flags && !p.post_flags && (g.r_dim * 2) % 16 == 0) ? 1 : 0;
+  if (p.wide) p.nstage = 1;
+  p.off_x = p.off_out + (p.wide ? (uint32_t)kEpi * 4096u
+                                : (uint32_t)p.nstage * kEpi * 32u * 32u * (uint32_t)(y_dtype == DT_BF16 ? 2 : 4));
   if (p.softmax) {  // [4][128] column-warp partials, then 2 x cs x 128 cluster partials
     p.off_red = p.off_x;
     p.off_x += 4 * kTM * 8;
@@ -902,9 +984,10 @@ int tc_rows_forward(const Geo &g, int64_t batch, const void *x, const float *wf,
   p.tma_y = (want_tma_y || p.softmax) ? 1 : 0;  // the softmax epilogue stores through TMA
   if (p.tma_y)
     if (int rc = encode_tensor_map_2d_sw(&tm_y, y_dtype, y, (uint64_t)g.r_dim, (uint64_t)batch,
-                                         (uint64_t)g.r_dim * (y_dtype == DT_BF16 ? 2 : 4), 32, 32,
-                                         y_dtype == DT_BF16 ? (int)CU_TENSOR_MAP_SWIZZLE_64B
-                                                            : (int)CU_TENSOR_MAP_SWIZZLE_128B))
+                                         (uint64_t)g.r_dim * (y_dtype == DT_BF16 ? 2 : 4),
+                                         p.wide ? 64 : 32, 32,
+                                         y_dtype == DT_BF16 && !p.wide ? (int)CU_TENSOR_MAP_SWIZZLE_64B
+                                                                       : (int)CU_TENSOR_MAP_SWIZZLE_128B))
       return rc;
   RowsFn fn = y_dtype == DT_BF16 ? pick_act<DT_BF16>(act) : pick_act<DT_F32>(act);
   // the opt-in shared-memory size once per (device, kernel instance)

@@ -1,7 +1,13 @@
-// Row-slab tensor-core forward for reuse geometries (n_f | q, s = q / n_f a power of two): the
+// Row-slab tensor-core forward for reuse geometries (n_f | q, s = q / n_f in {2, 4, 8}): the
 // factored DeepThin layer in ONE persistent kernel without clusters. Every CTA owns a contiguous
 // slab of batch rows (batch / #SMs, rounded to the phase-A unit), reads those rows of x once and
 // writes those rows of y once: all SMs stream, no P exchange between CTAs, no tail round.
+// OPT-IN (DEEPTHIN_ROWS_SLAB=1): on config 3 it measures 30.5 us per hidden layer against
+// 28.2 us for the clustered row-tile kernel (k_tc_rows.cu) — its transposed epilogue costs more
+// instructions per output than the exchange it removes. Bit-identical outputs
+// (test_slab_kernel_bits_equal_cluster_kernel). Its traces are where this round's two
+// library-wide findings came from: the cost of bounded mbarrier wait loops (sm100_ptx.cuh
+// mbar_wait) and of issuing tcgen05 / TMA instructions from inside `if (lane == 0)` (below).
 //
 // Reference: kernel.py:1-16 / 99-164 (the reuse identity: every output column reads s = q/n
 // whole rows of I = xf @ wf, so each distinct run dot x_seg . wf[k] is computed once) and
@@ -15,26 +21,29 @@
 //   phase B:  TRANSPOSED, output columns on the UMMA M axis (= TMEM lanes), batch rows on N:
 //             D^T[j, b] = sum_kk XF2p[j, kk] A2[b, kk]   (kind::tf32, bias in a K pad slot)
 //             per group of up to 64 batch rows (N = 64) and chunk of 128 output columns, XF2p
-//             chunks streamed from L2. TMEM reads (64 B/clk per SM) and MUFU (one tanh per
-//             output) bound the epilogue at 16 outputs per clock per SM; with the columns on
-//             the lanes every lane and every thread is live whatever the group's row count, so
-//             slabs split into small groups and a group's stores overlap the next group's loads.
-//             (Rows on the lanes — measured — need 128-row groups to keep the lanes busy: one
-//             group per slab, all loads before all stores.)
-//   epilogue: D^T (TMEM; thread = output column, registers = 32 batch rows) -> activation ->
-//             bf16/fp32 -> transposed into a swizzled 32 x 32 staging box -> TMA store.
-//             The row softmax is not fused here (per-row statistics would cross lanes):
-//             softmax layers stay on the clustered row-tile kernel.
+//             chunks streamed from L2. With the columns on the lanes every lane and every
+//             thread is live whatever the group's row count, so slabs split into small groups
+//             and a group's stores overlap the next group's loads. (Rows on the lanes —
+//             measured — need 128-row groups to keep lanes, TMEM reads and MUFU busy: one group
+//             per slab, all loads before all stores; 64-row groups read through the 16-lane
+//             tcgen05.ld shape halve the TMEM read efficiency.)
+//   epilogue: D^T (TMEM; thread = output column, registers = 2 x 16 batch rows) -> activation
+//             -> bf16/fp32 -> transposed (lane-pair shuffle + byte permute) into a swizzled
+//             32 x 32 staging box -> TMA store. The row softmax is not fused here (per-row
+//             statistics would cross lanes): softmax layers stay on the clustered kernel.
 //
 // Warp roles (768 threads, one CTA per SM):
-//   warp 0  TMA producer of x' k-blocks (128 x' rows x 64 bf16, SW128)
-//   warp 2  TMEM allocator + single-thread tcgen05.mma issuer of phase A (P ring of 8 units)
-//   warps 1, 3  none
+//   warp 0      TMA producer of x' k-blocks (128 x' rows x 64 bf16, SW128)
+//   warp 2      TMEM allocator + tcgen05.mma issuer of phase A (P ring of 8 units)
+//   warps 1, 3  phase-B issuers, one per team (team t = chunks t, t + 2, ... of every group):
+//               XF2p chunk loads (3 slots, 3 chunks ahead: an L2 -> shared chunk load takes
+//               ~1 us) and the chunk's MMAs nd - 1 chunks ahead into the team's D ring; one
+//               named barrier per chunk joins the issuer and the team's eight epilogue warps
 //   warps 4-7   P re-lay (one per TMEM lane quarter)
-//   warps 8-23  phase B + epilogue, two teams of 8 warps (team t = chunks t, t + 2, ...): the
-//               team's leader thread loads its XF2p chunks and issues its MMAs one chunk ahead
-//               into the team's other D buffer; quarter (warp % 4) = 32 of a chunk's 128 output
+//   warps 8-23  epilogue, 8 warps per team: quarter (warp % 4) = 32 of a chunk's 128 output
 //               columns, ((warp - 8) / 4) % 2 = 32 of the group's 64 rows
+// All producer / issuer loops run warp-convergent with the asynchronous instructions predicated
+// on lane 0 (see the comment at their head).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -78,7 +87,8 @@ struct SlabParams {
   int slab;     // batch rows per CTA (a multiple of max(ur, 16))
   int xs, bs, nd;
   int nstage;   // output staging boxes per epilogue warp (TMA stores in flight)
-  int dbg;      // timing build only (DEEPTHIN_DBG_SLAB): 1 no TMA store, 2 no staging, 3 no act
+  int dbg;      // timing build only (DEEPTHIN_DBG_SLAB): >= 1 no TMA store, >= 2 no staging, >= 3
+                // no activation, >= 4 no TMEM reads (wrong outputs: a ladder for the traces)
   uint32_t dcol0;
   int bslot;    // K slot carrying the bias (A2 = 1 there), -1: the epilogue adds it
   const float *bias;
