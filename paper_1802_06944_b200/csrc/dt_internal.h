@@ -243,6 +243,9 @@ int backward_event_record(cudaStream_t st);
 // attributes are per device context: a process driving several GPUs sets them on each).
 // Cached per (device, fn), thread-safe.
 int set_smem_limit(const void *fn, int bytes);
+// Ask for the maximum shared-memory carveout for fn on the current device (once per (device,
+// fn)): a small kernel meant to run on the same SMs as a large-shared-memory one.
+int prefer_max_smem_carveout(const void *fn);
 // Allow non-portable cluster sizes for fn on the current device (once per (device, fn)).
 int allow_nonportable_clusters(const void *fn);
 

@@ -684,6 +684,7 @@ namespace {
 std::mutex g_attr_mu;
 std::map<std::pair<int, const void *>, int> g_smem_set;       // (device, fn) -> bytes set
 std::set<std::pair<int, const void *>> g_nonportable_set;     // (device, fn)
+std::set<std::pair<int, const void *>> g_carveout_set;        // (device, fn)
 }  // namespace
 
 int set_smem_limit(const void *fn, int bytes) {
@@ -695,6 +696,16 @@ int set_smem_limit(const void *fn, int bytes) {
     DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     have = bytes;
   }
+  return DT_OK;
+}
+
+int prefer_max_smem_carveout(const void *fn) {
+  int dev = 0;
+  DT_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  if (g_carveout_set.insert({dev, fn}).second)
+    DT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
   return DT_OK;
 }
 

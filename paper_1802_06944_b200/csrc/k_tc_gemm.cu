@@ -76,6 +76,7 @@ struct RegenArgs {
   // halves of qp columns (qp = round_up(q, 64)), so one GEMM over K = 2 qp against x (read
   // twice through a wrapping tensor map) accumulates x W_hi + x W_lo: ~16 significant bits of W
   int hilo, qp;
+  int tiles_x, tiles_y;  // phase-1 tile grid (filled by launch_regen_wt)
 };
 struct RegenSmem {
   float xt[RG_K][RG_RMAX + 4];  // +4: the transposing stores are 4-way, not 32-way, conflicted
@@ -410,12 +411,17 @@ __device__ __forceinline__ void regen_tile_tc(const RegenArgs &g, int tid, int b
   }
 }
 
+// Persistent over the tiles (1-D grid, tile t -> (t % tiles_x, t / tiles_x)): a pipelined launch
+// caps the grid at one CTA per SM, so every CTA of this grid is resident beside the previous
+// forward's GEMM (22 KB of shared memory fit next to its stages). With more CTAs than SMs the
+// second wave could only start once the first wave left — which waits for that GEMM's end
+// (griddepcontrol.wait below) — and ran exposed between the two GEMMs (config 2: ~7 us a step).
 __global__ void __launch_bounds__(256) k_regen_wt(const RegenArgs g) {
   griddep_launch_dependents();  // the GEMM may start its prologue now
   __shared__ __align__(16) RegenSmemTC sm;
-  if (g.hilo && g.qp > g.q && blockIdx.y == 0) {
+  if (g.hilo && g.qp > g.q) {
     // zero the pad columns [q, qp) of both halves (the GEMM multiplies them by x's zero fill;
-    // workspace garbage could be NaN), rows strided over the first column of CTAs
+    // workspace garbage could be NaN), rows strided over the CTAs
     const int64_t ld2 = 2 * (int64_t)g.qp;
     const int pad = g.qp - (int)g.q;
     for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < g.r_dim * 2 * pad;
@@ -425,14 +431,48 @@ __global__ void __launch_bounds__(256) k_regen_wt(const RegenArgs g) {
       g.wt[j * ld2 + (k < pad ? 0 : g.qp) + g.q + (k % pad)] = __float2bfloat16_rn(0.f);
     }
   }
-  if (g.f_dtype == DT_F32)
-    regen_tile_tc<float>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm);
-  else
-    regen_tile_tc<__nv_bfloat16>(g, threadIdx.x, blockIdx.x, blockIdx.y, sm);
+  const int tiles = g.tiles_x * g.tiles_y;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    if (t != (int)blockIdx.x) __syncthreads();  // the previous tile's fragments are read
+    const int by = t / g.tiles_x, bx = t - by * g.tiles_x;
+    if (g.f_dtype == DT_F32)
+      regen_tile_tc<float>(g, threadIdx.x, bx, by, sm);
+    else
+      regen_tile_tc<__nv_bfloat16>(g, threadIdx.x, bx, by, sm);
+  }
   // pipelined: this grid overlapped the previous forward's GEMM (it writes the other W^T
   // slot); completing only after that grid keeps the next GEMM — which waits on this grid —
   // ordered after it, so W^T slots and outputs are reused safely.
   if (g.chain) griddep_wait();
+}
+
+// Launch phase 1 (fills g.tiles_x / tiles_y; see k_regen_wt for the grid cap when pipelined).
+int launch_regen_wt(RegenArgs rg, cudaStream_t st) {
+  rg.tiles_x = (rg.a_rows + RG_R - 1) / RG_R;
+  rg.tiles_y = (rg.n + RG_C - 1) / RG_C;
+  int tiles = rg.tiles_x * rg.tiles_y;
+  if (rg.chain) {
+    int dev = 0, nsm = 148;
+    DT_CUDA_CHECK(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // the same shared-memory carveout as the GEMM it runs beside (an SM switches its L1 /
+    // shared split only when idle: with the default carveout these CTAs waited for the GEMM's
+    // CTAs to leave)
+    if (int rc = prefer_max_smem_carveout(reinterpret_cast<const void *>(k_regen_wt))) return rc;
+    cudaLaunchConfig_t rcfg{};
+    rcfg.gridDim = dim3((unsigned)std::max(1, std::min(tiles, nsm)));
+    rcfg.blockDim = dim3(256);
+    rcfg.stream = st;
+    cudaLaunchAttribute ra[1];
+    ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ra[0].val.programmaticStreamSerializationAllowed = 1;
+    rcfg.attrs = ra;
+    rcfg.numAttrs = 1;
+    DT_CUDA_CHECK(cudaLaunchKernelEx(&rcfg, k_regen_wt, rg));
+  } else {
+    k_regen_wt<<<(unsigned)std::max(1, tiles), 256, 0, st>>>(rg);
+  }
+  return check_launch("regen_wt");
 }
 
 // ---- phase 2 --------------------------------------------------------------------------------
@@ -1480,21 +1520,7 @@ static int run_gemm(const GemmCall &c, cudaStream_t st) {
   }
   if (!done) {
     if (c.rg && dbg_phase != 2) {
-      if (c.rg->chain) {  // pipelined: phase 1 overlaps the previous forward's GEMM
-        cudaLaunchConfig_t rcfg{};
-        rcfg.gridDim = rgrid;
-        rcfg.blockDim = dim3(256);
-        rcfg.stream = st;
-        cudaLaunchAttribute ra[1];
-        ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        ra[0].val.programmaticStreamSerializationAllowed = 1;
-        rcfg.attrs = ra;
-        rcfg.numAttrs = 1;
-        DT_CUDA_CHECK(cudaLaunchKernelEx(&rcfg, k_regen_wt, *c.rg));
-      } else {
-        k_regen_wt<<<rgrid, 256, 0, st>>>(*c.rg);
-      }
-      if (int rc = check_launch("regen_wt")) return rc;
+      if (int rc = launch_regen_wt(*c.rg, st)) return rc;
     }
     if (c.rg && dbg_phase == 1) return DT_OK;
     if (ev_b) DT_CUDA_CHECK(cudaEventRecord(ev_b, st));
@@ -1748,22 +1774,7 @@ static int tc_forward_impl(const Geo &g, int64_t batch, const void *x, int x_dty
     rg.chain = pipe ? 1 : 0;
     rg.hilo = 1;
     rg.qp = (int)qp;
-    const dim3 rgrid((unsigned)((rg.a_rows + RG_R - 1) / RG_R), (unsigned)((rg.n + RG_C - 1) / RG_C));
-    if (pipe) {  // phase 1 overlaps the previous forward's GEMM
-      cudaLaunchConfig_t rcfg{};
-      rcfg.gridDim = rgrid;
-      rcfg.blockDim = dim3(256);
-      rcfg.stream = st;
-      cudaLaunchAttribute ra[1];
-      ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      ra[0].val.programmaticStreamSerializationAllowed = 1;
-      rcfg.attrs = ra;
-      rcfg.numAttrs = 1;
-      DT_CUDA_CHECK(cudaLaunchKernelEx(&rcfg, k_regen_wt, rg));
-    } else {
-      k_regen_wt<<<rgrid, 256, 0, st>>>(rg);
-    }
-    if (int rc = check_launch("regen_wt")) return rc;
+    if (int rc = launch_regen_wt(rg, st)) return rc;  // pipelined: overlaps the previous forward's GEMM
     XGemm xg;
     // K = qp with the lo half riding in the same stages (dual A): x is read once per tile
     xg.M = g.r_dim; xg.N = batch; xg.K = qp;

@@ -78,6 +78,8 @@ struct XgParams {
   float act_arg;              // XE_STORE_T activation argument
   void *out_t;                // XE_STORE_T: out[n][m] (pitch ldo), fp32 or bf16
   int N_true;                 // XE_STORE_T: rows of out (D columns) actually stored
+  int tma_t;                  // XE_STORE_T, fp32 out: transposed through shared staging + TMA stores
+  int dbg;                    // timing build only (DEEPTHIN_DBG_XG): 1 no y stores, 2 no MMAs, 4 no TMEM reads, 8 no dual-A loads
   int dual_kb;                // > 0: each stage also carries A at k-block kb + dual_kb (a second
                               // A half, e.g. W_lo beside W_hi) multiplied by the same B tile
 };
@@ -194,7 +196,8 @@ __global__ void __launch_bounds__(XTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t abytes = p.dual_kb > 0 ? 2u * XA_BYTES : XA_BYTES;
-      const uint32_t bytes = 2u * (abytes + (uint32_t)p.nhalf * 128u);
+      const bool skip_dual = kTimingSwitches && (p.dbg & 8);  // traffic experiment: no A_lo loads
+      const uint32_t bytes = 2u * ((skip_dual ? XA_BYTES : abytes) + (uint32_t)p.nhalf * 128u);
       for (int u = cid; u < p.units; u += ncl) {
         int mb, nb, ks;
         unit_of(u, mb, nb, ks);
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
           if (l0) {
             if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
             xload(st, &tm_a, &full[stage], p.a_mn, EL, m0, 128, kb);
-            if (p.dual_kb > 0) xload(st + abytes - XA_BYTES, &tm_a, &full[stage], p.a_mn, EL, m0, 128,
+            if (p.dual_kb > 0 && !skip_dual) xload(st + abytes - XA_BYTES, &tm_a, &full[stage], p.a_mn, EL, m0, 128,
                                      kb + p.dual_kb);
             xload(st + abytes, &tm_b, &full[stage], p.b_mn, EL, n0, p.nhalf, kbb);
           }
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
           const uint64_t db = dB0 + (uint64_t)((uint32_t)stage * st16);
           const uint64_t da2 = da + (uint64_t)(XA_BYTES >> 4);
           const uint32_t acc0 = kb > kb0 ? 1u : 0u;
-          if (l0) {
+          if (l0 && !(kTimingSwitches && (p.dbg & 2))) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               if constexpr (EL)
@@ -260,8 +263,8 @@ __global__ void __launch_bounds__(XTHREADS, 1)
                 else mma_bf16_ss_pair(d, da2 + (uint64_t)(k * ksA), db + (uint64_t)(k * ksB), idesc, 1u);
               }
             }
-            mma_commit_pair(&empty[stage]);
           }
+          if (l0) mma_commit_pair(&empty[stage]);
           if (++stage == p.S) { stage = 0; phase ^= 1; }
         }
         if (l0) mma_commit_pair(&tfull[acc]);
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(XTHREADS, 1)
     // ---------------- epilogue (both CTAs: 128 rows x BN columns each) ----------------
     const int e = warp - 2, q = warp & 3, h = e / 4;
     const uint32_t lane_t = (uint32_t)(32 * q) << 16;
-    constexpr int NBUF = EPI == XE_MSE ? 3 : 2;  // staging boxes per warp
+    constexpr int NBUF = EPI == XE_MSE ? 3 : EPI == XE_STORE_T ? 1 : 2;  // staging boxes per warp
     const uint32_t stg0 = smem_u32(smem) + p.off_stg + (uint32_t)e * NBUF * XSTG;
     uint8_t *stg0p = smem + p.off_stg + e * NBUF * XSTG;
     const int nch = EPI == XE_PAIRSUM ? (p.pair_half + 31) / 32 : BN / 32;
@@ -310,6 +313,10 @@ __global__ void __launch_bounds__(XTHREADS, 1)
       for (int c = h; c < nch; c += 2) {
         const int col0 = nb * BN + 32 * c;  // first D column of this chunk
         uint32_t v[32];
+        if (kTimingSwitches && (p.dbg & 4)) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        } else
         tmem_ld_32x32b_x32(tbase + lane_t + (uint32_t)(acc * BN + 32 * c), v);
         if constexpr (EPI == XE_PAIRSUM) {
           uint32_t w[32];
@@ -326,7 +333,41 @@ __global__ void __launch_bounds__(XTHREADS, 1)
           // columns = 32 output rows; each store instruction writes 32 consecutive columns of
           // one output row (coalesced)
           using OutT = typename std::conditional<YDT == DT_BF16, __nv_bfloat16, float>::type;
-          if (row < p.M) {
+          if constexpr (YDT == DT_F32) {
+            if (p.tma_t) {
+              // Transposed through shared memory: the chunk is staged as two 16 x 32 fp32 half
+              // boxes (batch row i = one 128-byte line, this lane's output column at word `lane`,
+              // 16-byte units XOR-swizzled by i & 7 as the SW128 tensor map expects: every
+              // st.shared covers 32 distinct banks), each stored by ONE bulk tensor copy instead
+              // of 16 st.global instructions through L1 (TMA clips the ragged edges of y). The
+              // half boxes alternate, so a half is rewritten only after the store two back read it.
+              const float bm = (p.bias && row < p.M) ? __ldg(p.bias + row) : 0.f;
+#pragma unroll
+              for (int hb = 0; hb < 2; ++hb) {
+                if (lane == 0) bulk_wait_group_read<1>();
+                __syncwarp();
+                const uint32_t sb = stg0 + (uint32_t)hb * 2048u;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const float o = act_out_bf16<YDT, ACT>(__uint_as_float(v[16 * hb + i]) + bm, p.act_arg);
+                  asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + (uint32_t)i * 128u +
+                                                                 ((uint32_t)((lane >> 2) ^ (i & 7)) << 4) +
+                                                                 (uint32_t)(lane & 3) * 4u),
+                               "f"(o)
+                               : "memory");
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  if (col0 + 16 * hb < p.N_true && r0 < p.M)
+                    tma_store_2d(&tm_o, stg0p + hb * 2048, r0, col0 + 16 * hb);
+                  bulk_commit_group();  // (an empty group keeps the wait above counting halves)
+                }
+              }
+              continue;
+            }
+          }
+          if (row < p.M && !(kTimingSwitches && (p.dbg & 1) && v[0] != 0x7fc12345u)) {
             const float bm = p.bias ? __ldg(p.bias + row) : 0.f;
             OutT *yp = reinterpret_cast<OutT *>(p.out_t) + (int64_t)col0 * p.ldo + row;
             const int nrow = min(32, p.N_true - col0);
@@ -678,11 +719,23 @@ int xgemm(const XGemm &g, cudaStream_t st) {
     return DT_E_ARG;
   }
   p.stage_bytes = (p.dual_kb > 0 ? 2u : 1u) * XA_BYTES + (uint32_t)nhalf * 128u;
-  const uint32_t stg_bytes = (g.epi == XE_SPLITH || g.epi == XE_STORE_T) ? 0u
+  // XE_STORE_T with fp32 outputs stores through TMA when y's base and pitch allow a tensor map
+  // (one 4 KB box per epilogue warp, used as two alternating 16-row halves)
+  const bool tma_t = g.epi == XE_STORE_T && g.y_dtype == DT_F32 && g.ldo % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(g.out_t) & 15) == 0 &&
+                     !DT_DBG_ENV("DEEPTHIN_DBG_XG_NOTMA");
+  p.tma_t = tma_t ? 1 : 0;
+  const uint32_t stg_bytes = g.epi == XE_SPLITH ? 0u
+                             : g.epi == XE_STORE_T ? (tma_t ? (uint32_t)XEPI * XSTG : 0u)
                              : (uint32_t)XEPI * (g.epi == XE_MSE ? 3u : 2u) * XSTG;
   // barriers + TMEM slot (512 B), then the XE_MSE column-sum exchange [2][4][256] floats
   const uint32_t tail = 512 + (g.epi == XE_MSE ? 8192u : 0u);
-  p.S = (int)std::min<uint32_t>(8, (XSMEM_MAX - stg_bytes - tail - 1024) / p.stage_bytes);
+  // A pipelined forward (chain) leaves room for one CTA of the next call's W regeneration
+  // (k_regen_wt: 22 KB static + 1 KB reserved) beside this kernel on every SM, so that grid
+  // runs under this GEMM instead of after it.
+  const uint32_t smem_cap = g.chain ? XSMEM_MAX - 26 * 1024 : XSMEM_MAX;
+  p.S = (int)std::min<uint32_t>(8, (smem_cap - stg_bytes - tail - 1024) / p.stage_bytes);
+  if (DT_DBG_ENV("DEEPTHIN_DBG_XG_S") > 0) p.S = DT_DBG_ENV("DEEPTHIN_DBG_XG_S");
   p.off_stg = (uint32_t)p.S * p.stage_bytes;
   p.off_bar = p.off_stg + stg_bytes;
   const uint32_t smem_bytes = p.off_bar + tail + 1024;  // + the in-kernel 1024-B alignment
@@ -744,12 +797,17 @@ int xgemm(const XGemm &g, cudaStream_t st) {
     p.ldo = (int)g.N;
   }
   p.chain = g.chain;
+  p.dbg = DT_DBG_ENV("DEEPTHIN_DBG_XG");
   p.act_arg = g.act_arg;
   p.out_t = g.out_t;
   p.N_true = (int)g.N;
   if (g.epi != XE_SPLITH && g.epi != XE_STORE_T) {
     if (int rc = encode_tensor_map_2d(&tm_o, DT_F32, out, (uint64_t)out_cols, (uint64_t)out_rows,
                                       (uint64_t)ldo * 4, 32, 32, true))
+      return rc;
+  } else if (tma_t) {  // y[batch][r_dim]: boxes of 32 output columns x 16 batch rows
+    if (int rc = encode_tensor_map_2d(&tm_o, DT_F32, g.out_t, (uint64_t)g.M, (uint64_t)g.N,
+                                      (uint64_t)g.ldo * 4, 32, 16, true))
       return rc;
   } else {
     tm_o = tm_a;  // unused
