@@ -175,6 +175,61 @@ class DeviceModel:
             self._epoch += 1
         return xt.float().cpu().numpy() if host else xt
 
+    def forward_host(self, hx, hy=None, *, chunks: int = 4, out_dtype=torch.bfloat16):
+        """Pinned host x -> pinned host y with the copies overlapped: the batch is cut into
+        `chunks` row blocks (multiples of 128 rows) and block i's host->device copy, forward
+        (CUDA-graph replay on its own static buffers) and device->host copy run on three streams,
+        so the PCIe transfers of one block hide the compute of its neighbours and the two copy
+        directions run concurrently. Rows are independent (kernel.py:296-320 applied per row;
+        the kernels' bits do not depend on the batch sharding), so the result equals
+        forward(x). Returns hy (allocated pinned when None); synchronises before returning.
+
+        hx: pinned CPU tensor (batch x q) of the dtype the first layer reads (bf16 on the
+        tensor-core path)."""
+        if not (isinstance(hx, torch.Tensor) and hx.device.type == "cpu" and hx.dim() == 2):
+            raise ArgumentError("forward_host takes a 2-D CPU tensor (pinned for overlap)")
+        if hx.shape[1] != self.factors[0].plan.q:
+            raise DimensionError(f"input has {hx.shape[1]} columns, the first layer takes "
+                                 f"{self.factors[0].plan.q}")
+        batch, width = hx.shape[0], self.factors[-1].plan.r_dim
+        if hy is None:
+            hy = torch.empty((batch, width), dtype=out_dtype, pin_memory=True)
+        if tuple(hy.shape) != (batch, width) or hy.dtype != out_dtype:
+            raise DimensionError(f"output buffer must be {batch} x {width} {out_dtype}")
+        if batch == 0:
+            return hy
+        per = -(-batch // max(1, chunks))
+        per = -(-per // 128) * 128
+        bounds = [(r, min(batch, r + per)) for r in range(0, batch, per)]
+        key = (batch, hx.dtype, out_dtype, len(bounds))
+        st = self.__dict__.get("_host_pipe")
+        if st is None or st["key"] != key:
+            dev = self.factors[0].xf.device
+            st = {"key": key, "s_in": torch.cuda.Stream(), "s_out": torch.cuda.Stream(),
+                  "xd": [torch.empty((b - a, hx.shape[1]), dtype=hx.dtype, device=dev)
+                         for a, b in bounds],
+                  "ev_in": [torch.cuda.Event() for _ in bounds],
+                  "ev_c": [torch.cuda.Event() for _ in bounds],
+                  "ev_out": [torch.cuda.Event() for _ in bounds]}
+            self._host_pipe = st
+        cur = torch.cuda.current_stream()
+        st["s_in"].wait_stream(cur)
+        for i, (a, b) in enumerate(bounds):
+            with torch.cuda.stream(st["s_in"]):
+                st["s_in"].wait_event(st["ev_c"][i])   # the previous call's forward read xd[i]
+                st["xd"][i].copy_(hx[a:b], non_blocking=True)
+                st["ev_in"][i].record()
+            cur.wait_event(st["ev_in"][i])
+            cur.wait_event(st["ev_out"][i])            # the graph's static output was copied out
+            yd = self.forward(st["xd"][i], out_dtype=out_dtype, graph=True)
+            st["ev_c"][i].record(cur)
+            with torch.cuda.stream(st["s_out"]):
+                st["s_out"].wait_event(st["ev_c"][i])
+                hy[a:b].copy_(yd, non_blocking=True)
+                st["ev_out"][i].record()
+        st["s_out"].synchronize()
+        return hy
+
     def _fused_runs(self, out_dtype):
         """{first: last} of the layer runs dt_chain_forward takes: >= 2 consecutive reuse layers
         on the row-tile kernel sharing n, rank and q/n, one elementwise activation on all but the
@@ -237,7 +292,7 @@ class DeviceModel:
         key = (x.data_ptr(), tuple(x.shape), x.dtype, out_dtype)
         graphs = self.__dict__.setdefault("_graphs", {})
         if key not in graphs:
-            if len(graphs) >= 8:
+            if len(graphs) >= 16:
                 graphs.clear()
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())

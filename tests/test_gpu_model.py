@@ -146,6 +146,25 @@ def test_config3_shaped_network_bf16_and_pipeline():
     assert np.max(np.abs(got - O.apply_activation("softmax", logits))) <= 1e-6
 
 
+@pytest.mark.parametrize("rows,chunks", [(1000, 3), (4096, 4), (100, 4)])
+def test_forward_host_pipeline_equals_device_forward(rows, chunks):
+    """forward_host (row blocks pipelined over copy / compute / copy streams) returns the bits
+    of one forward over the whole batch, also when its static buffers are reused by a second
+    call on other inputs and when the last block is ragged."""
+    model = config3_like(layers=2)
+    dm = model.to_device(["sigmoid"] * 2 + ["softmax"], mma="bf16")
+    g = torch.Generator().manual_seed(rows)
+    hy = None
+    for call in range(2):
+        hx = torch.randn(rows, 440, generator=g).to(torch.bfloat16).pin_memory()
+        want = dm.forward(hx.cuda(), out_dtype=torch.bfloat16).cpu()
+        hy = dm.forward_host(hx, hy, chunks=chunks)
+        assert hy.dtype == torch.bfloat16 and tuple(hy.shape) == (rows, 3000)
+        assert torch.equal(hy, want), call
+    with pytest.raises(D.DimensionError):
+        dm.forward_host(torch.zeros(4, 441, dtype=torch.bfloat16))
+
+
 def test_chain_and_argument_errors(dthn):
     model = mi.deserialize(dthn["f32_bytes"].tobytes())
     with pytest.raises(D.ArgumentError):
