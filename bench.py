@@ -79,6 +79,23 @@ def peaks():
         return 1590.0, 6650.0, "fallback"
 
 
+def write_roofline(bytes_written, seconds):
+    """The write direction of an HBM-bound kernel beside the copy-bandwidth roofline: HBM3e on
+    this pool's B200 sustains ~3.9 TB/s of pure writes (torch fill_ / memset over 2 GiB) against
+    ~6.45 TB/s of reads or of a copy's read + write (scripts/hbm_rw_probe.py ->
+    profiles/r02_hbm_rw.json), so a kernel that mostly writes is bounded by the former."""
+    peak = 3911.7
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_hbm_rw.json")) as f:
+            peak = float(json.load(f)["write_gbs_fill"])
+    except (OSError, ValueError, KeyError):
+        pass
+    ach = bytes_written / seconds / 1e9
+    return {"bytes_written": int(bytes_written), "achieved": round(ach, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(ach / peak, 4),
+            "peak_source": "measured pure-write bandwidth (profiles/r02_hbm_rw.json)"}
+
+
 def traffic_for(key):
     """dram bytes per launch of the dominant kernel from the committed ncu capture, else None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -550,14 +567,16 @@ def run_ours(args, cfg, key):
                 "peak_source": f"{peak_kind} hbm_gbs",
                 "kernel": "k_tc_xgemm (phase 2: x . [W_hi | W_lo]^T, tcgen05 pairs)",
                 "kernel_us": round(kernel_ms * 1e3, 3),
-                "kernel_launches": len(kd), "kernel_us_raw": round(statistics.mean(kraw), 3),
+                "kernel_launches": len(kd),
+                "kernel_us_raw": round(statistics.mean(kraw), 3) if kraw else None,
                 "timing": "CUPTI activity records (torch.profiler), exclusive of the PDL overlap "
                           "with the previous kernel",
                 "kernel_share_of_step": round(share, 3) if share else None,
                 "all_kernels_share_of_step": round(ktotal / 1e3 / args.steps / ms_per_step, 3),
                 "algorithmic_bytes": bytes_alg,
                 "tensor_tflops": round(flops / (kernel_ms * 1e-3) / 1e12, 1),
-                "tensor_frac": round(flops / (kernel_ms * 1e-3) / 1e12 / bf16_peak, 4)}
+                "tensor_frac": round(flops / (kernel_ms * 1e-3) / 1e12 / bf16_peak, 4),
+                "hbm_write": write_roofline(batch * r_dim * 4, kernel_ms * 1e-3)}
     else:
         bytes_alg = 4 * (batch * q + batch * r_dim + m * rank_r + rank_r * n + r_dim)
         achieved = bytes_alg / (kernel_ms * 1e-3) / 1e9
@@ -803,6 +822,9 @@ def run_network(args, cfg, key):
             "all_kernels_share_of_step": round(ktotal / 1e3 / args.steps / ms_per_step, 3),
             "algorithmic_bytes": int(statistics.mean(per_launch)),
             "algorithmic_bytes_per_layer": per_launch}
+    if kd:  # y written per launch (bf16): the direction that bounds this kernel
+        wbytes = sum(batch * reuse[i % len(reuse)][1] * 2 for i in range(nl))
+        roof["hbm_write"] = write_roofline(wbytes / nl, statistics.mean(kd) * 1e-6)
 
     # e2e through the public API: pinned host x -> device -> DeviceModel.forward -> pinned host y
     hx = x_host.pin_memory()
