@@ -313,8 +313,9 @@ int lstm_gates(const Geo &g, int64_t batch, const float *h, const float *const *
 }  // namespace dt
 
 // =============================================================================================
-// The whole LSTM recurrence in ONE persistent kernel (config 4): T steps, three grid-wide
-// barriers per step, no host launches inside the loop. Work units (3xTF32 tiles, fp32 cell):
+// The whole LSTM recurrence in ONE persistent kernel (config 4): T steps, two grid-wide
+// barriers per step in the fused gate-cluster form (three in the general form), no host
+// launches inside the loop. Work units (3xTF32 tiles, fp32 cell):
 //   phase P, unit (gate g, segment seg, 16-row group rg):
 //     P_g[rows, seg*R + k] = h[rows, seg cols] . wf_g[k, :]        (p_tile_3xtf32)
 //   phase G, unit (gate g, 64-column block): gh_g[:, cols] = P_g @ XF2_g[cols]^T + b_hg
@@ -329,7 +330,8 @@ struct SeqArgs {
   const float *xf[4], *wf[4], *bias[4];
   const __nv_bfloat16 *gx[4];  // T*B x H each (biases of the input projections included)
   float *gh;                   // 4 x B x H
-  float *P;                    // 4 x B x K2
+  float *P;                    // 4 x B x Pld (rows at the staged pitch K2 + 4: one bulk copy per gate tile)
+  int Pld;
   float *c;                    // B x H cell state
   float *h;                    // B x H hidden state (fp32, the recurrent contractions' input)
   __nv_bfloat16 *out;          // T*B x H
@@ -370,7 +372,14 @@ __device__ __forceinline__ float sigm_(float z) { return 1.f / (1.f + expf(-z));
 // waits on two serial L2 round trips.
 __device__ __forceinline__ void bulk_stage(float *dst, int sp, const float *src, int64_t ld, int rows,
                                            int cols, uint64_t *bar, uint32_t &phase) {
-  if (threadIdx.x < 32) {
+  if (ld == sp) {  // source rows already at the staged pitch: ONE copy of the whole block
+    if (threadIdx.x == 0) {
+      fence_proxy_async_global();
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(bar, (uint32_t)(rows * sp * 4));
+      bulk_load(dst, src, (uint32_t)(rows * sp * 4), bar);
+    }
+  } else if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
       fence_proxy_async_global();
       fence_proxy_async_smem();
@@ -385,6 +394,13 @@ __device__ __forceinline__ void bulk_stage(float *dst, int sp, const float *src,
 }
 
 
+// FUSED: the four gate tiles of one 64-column block sit in one cluster of four CTAs (gate =
+// cluster rank). After its tile each CTA scatters its gate's pre-activations into the peers'
+// shared memory (DSMEM), 16 columns of the block per peer, and after one cluster barrier every
+// CTA runs the cell for its 64 rows x 16 columns with c held in registers for the whole
+// sequence: no gh round trip through L2, no separate cell phase and two grid barriers per step
+// instead of three. Same arithmetic and order per element as the unfused phases (same bits).
+template <bool FUSED>
 __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
   extern __shared__ float sm[];
   const int B = a.B, H = a.H, n = a.n, R = a.R, K2 = a.K2;
@@ -397,11 +413,16 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
   float *hs = sm, *ws = hs + 16 * npad, *red = ws + R8 * npad, *ps = red + 128 * R8;
   ps += (4 - ((ps - sm) & 3)) & 3;  // 16-byte alignment for the staged tiles
   float *xs = ps + 64 * kp;
+  float *g4 = xs + 64 * kp;  // FUSED: [4 gates][64 rows][16 columns] gate pre-activations
+  const int nblk = (H + 63) / 64;
+  // G unit -> (gate, column block): gate-major, or cluster rank = gate when fused
+  auto unit_gate = [&](int u) { return FUSED ? (u & 3) : u / nblk; };
+  auto unit_j0 = [&](int u) { return (FUSED ? (u >> 2) : u % nblk) * 64; };
   const bool resP = unitsP <= (int)gridDim.x, resB = unitsB <= (int)gridDim.x;
   auto wf_of = [&](int g) { return g == 0 ? a.wf[0] : g == 1 ? a.wf[1] : g == 2 ? a.wf[2] : a.wf[3]; };
   auto xf_of = [&](int g) { return g == 0 ? a.xf[0] : g == 1 ? a.xf[1] : g == 2 ? a.xf[2] : a.xf[3]; };
   auto stage_xs = [&](int u) {
-    const int g = u / ((H + 63) / 64), j0 = (u % ((H + 63) / 64)) * 64, nj = min(64, H - j0);
+    const int g = unit_gate(u), j0 = unit_j0(u), nj = min(64, H - j0);
     stage_rows(xs, kp, xf_of(g) + (size_t)j0 * K2, K2, nj, K2);
     for (int i = nj * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) xs[i] = 0.f;
   };
@@ -480,6 +501,7 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       a.out[gxo0 + e] = __float2bfloat16_rn(hn);
     }
   };
+  float creg[4] = {0.f, 0.f, 0.f, 0.f};  // FUSED: this thread's four cell states, c(-1) = 0
   for (int t = 0; t < a.T; ++t) {
     // ---------------- phase P: P_g[rows, seg*R + k] = h[rows, seg] . wf_g[k, :] ----------------
     for (int u = blockIdx.x; u < unitsP; u += gridDim.x) {
@@ -491,18 +513,95 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
       __syncthreads();
       p_tile_3xtf32(hs, ws, npad, n8, R8, red);
       __syncthreads();
-      p_tile_sum(red, R8, R, nb, a.P + ((size_t)g * B + b0) * K2 + seg * R, K2);
+      p_tile_sum(red, R8, R, nb, a.P + ((size_t)g * B + b0) * a.Pld + seg * R, a.Pld);
     }
     stamp(t, 0);
     grid_barrier(a.bar, target);
     stamp(t, 1);
     // ---------------- phase G: gh_g[:, 64-column block] = P_g XF2_g^T + b (3xTF32 mma) -----------
+    if constexpr (FUSED) {
+      // one unit per CTA (launcher: gridDim.x == unitsB, H % 64 == 0, clusters of 4)
+      const int g = (int)blockIdx.x & 3, j0 = ((int)blockIdx.x >> 2) * 64;
+      const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
+      // this thread's cell elements: row cb, block columns 16 g + 4 cq .. + 3; their input
+      // projections are independent of the recurrence: fetched before the tile
+      const int cb = threadIdx.x >> 2, cq = threadIdx.x & 3, cj = j0 + 16 * g + 4 * cq;
+      const size_t gxo = ((size_t)t * B + cb) * H + cj;
+      uint2 xg[4];
+      if (cb < B) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xg[q] = __ldg(reinterpret_cast<const uint2 *>(a.gx[q] + gxo));
+      }
+      bulk_stage(ps, kp, a.P + (size_t)g * B * a.Pld, a.Pld, B, K2, &sbar[1], sph[1]);
+      if (t == 0) {
+        for (int i = B * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) ps[i] = 0.f;
+      }
+      __syncthreads();
+      stamp(t, 6);
+      float acc[4][4];
+      tile64_3xtf32(ps, xs, kp, K2, acc);
+      __syncwarp();
+      stamp(t, 7);
+      {  // scatter: block column j -> peer j / 16, slot [g][row][j % 16] (column pairs: 8 bytes)
+        const int w = threadIdx.x / 32, lane = threadIdx.x % 32, gid = lane >> 2, tig = lane & 3;
+        const int r0 = 16 * (w & 3), c0 = 32 * (w >> 2);
+        const uint32_t base = smem_u32(g4) + (uint32_t)(g * 64 * 16) * 4u;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int j = c0 + nt * 8 + 2 * tig;
+          const uint32_t peer = (uint32_t)(j >> 4);
+          const float b0v = bg ? __ldg(bg + j0 + j) : 0.f, b1v = bg ? __ldg(bg + j0 + j + 1) : 0.f;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int b = r0 + gid + 8 * hh;
+            const uint32_t dst = mapa_shared(base + (uint32_t)(b * 16 + (j & 15)) * 4u, peer);
+            asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(dst),
+                         "f"(acc[nt][2 * hh] + b0v), "f"(acc[nt][2 * hh + 1] + b1v)
+                         : "memory");
+          }
+        }
+      }
+      cluster_sync();  // release / acquire at cluster scope: every peer's scatter has landed
+      stamp(t, 2);
+      stamp(t, 3);
+      if (cb < B) {
+        float4 z[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          z[q] = *reinterpret_cast<const float4 *>(g4 + (q * 64 + cb) * 16 + 4 * cq);
+        float zz[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162 *>(&xg[q].x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162 *>(&xg[q].y);
+          zz[q][0] = __low2float(lo) + z[q].x;
+          zz[q][1] = __high2float(lo) + z[q].y;
+          zz[q][2] = __low2float(hi) + z[q].z;
+          zz[q][3] = __high2float(hi) + z[q].w;
+        }
+        float hn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          creg[k] = sigm_(zz[1][k]) * creg[k] + sigm_(zz[0][k]) * tanhf(zz[2][k]);
+          hn[k] = sigm_(zz[3][k]) * tanhf(creg[k]);
+        }
+        *reinterpret_cast<float4 *>(a.h + (size_t)cb * H + cj) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+        __nv_bfloat162 o0 = __floats2bfloat162_rn(hn[0], hn[1]), o1 = __floats2bfloat162_rn(hn[2], hn[3]);
+        uint2 ov;
+        ov.x = *reinterpret_cast<uint32_t *>(&o0);
+        ov.y = *reinterpret_cast<uint32_t *>(&o1);
+        *reinterpret_cast<uint2 *>(a.out + gxo) = ov;
+      }
+      stamp(t, 4);
+      grid_barrier(a.bar, target);
+      stamp(t, 5);
+    } else {
     for (int u = blockIdx.x; u < unitsB; u += gridDim.x) {
-      const int g = u / ((H + 63) / 64), j0 = (u % ((H + 63) / 64)) * 64, nj = min(64, H - j0);
+      const int g = unit_gate(u), j0 = unit_j0(u), nj = min(64, H - j0);
       const float *bg = g == 0 ? a.bias[0] : g == 1 ? a.bias[1] : g == 2 ? a.bias[2] : a.bias[3];
       __syncthreads();
       if (!resB) stage_xs(u);
-      bulk_stage(ps, kp, a.P + (size_t)g * B * K2, K2, B, K2, &sbar[1], sph[1]);
+      bulk_stage(ps, kp, a.P + (size_t)g * B * a.Pld, a.Pld, B, K2, &sbar[1], sph[1]);
       for (int i = B * kp + threadIdx.x; i < 64 * kp; i += blockDim.x) ps[i] = 0.f;
       __syncthreads();
       stamp(t, 6);
@@ -519,7 +618,9 @@ __global__ void __launch_bounds__(256, 1) k_lstm_seq(SeqArgs a) {
     stamp(t, 4);
     grid_barrier(a.bar, target);
     stamp(t, 5);
+    }
   }
+  if constexpr (FUSED) cluster_sync();  // no CTA exits while a peer may still address its memory
 }
 
 }  // namespace
@@ -534,8 +635,8 @@ bool lstm_seq_ok(const Geo &g, int64_t batch) {
          lstm_seq_smem(g) <= 226 * 1024;  // (+ the static mbarriers)
 }
 size_t lstm_seq_ws(const Geo &g, int64_t batch) {
-  return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * g.s * g.rank * 4 + (size_t)2 * batch * g.q * 4 + 256;
-  // gh (4 B H) | P (4 B K2) | c, h (2 B H) | barrier
+  return (size_t)4 * batch * g.q * 4 + (size_t)4 * batch * (g.s * g.rank + 4) * 4 + (size_t)2 * batch * g.q * 4 + 256;
+  // gh (4 B H) | P (4 B (K2 + 4)) | c, h (2 B H) | barrier
 }
 
 int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, const float *const *xf,
@@ -552,37 +653,74 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   for (int i = 0; i < 4; ++i) a.vec &= (reinterpret_cast<uintptr_t>(gx[i]) & 7) == 0;
   char *cur = ws;
   a.gh = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * g.q * 4;
-  a.P = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * a.K2 * 4;
+  a.Pld = a.K2 + 4;
+  a.P = reinterpret_cast<float *>(cur); cur += (size_t)4 * batch * a.Pld * 4;
   a.c = reinterpret_cast<float *>(cur); cur += (size_t)batch * g.q * 4;
   a.h = reinterpret_cast<float *>(cur); cur += (size_t)batch * g.q * 4;
   a.bar = reinterpret_cast<unsigned *>(cur);
   a.out = reinterpret_cast<__nv_bfloat16 *>(out);
   DT_CUDA_CHECK(cudaMemsetAsync(a.c, 0, (size_t)2 * batch * g.q * 4, st));  // c(-1) = h(-1) = 0
   DT_CUDA_CHECK(cudaMemsetAsync(a.bar, 0, 256, st));
-  const size_t smem = lstm_seq_smem(g);
-  if (int rc = set_smem_limit(reinterpret_cast<const void *>(k_lstm_seq), 226 * 1024)) return rc;
+  size_t smem = lstm_seq_smem(g);
+  if (int rc = set_smem_limit(reinterpret_cast<const void *>(k_lstm_seq<false>), 226 * 1024)) return rc;
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int unitsP = 4 * a.s * ((a.B + 15) / 16), unitsB = 4 * ((a.H + 63) / 64);
-  const int grid = std::min(nsm, std::max(unitsP, unitsB));
+  int grid = std::min(nsm, std::max(unitsP, unitsB));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: grid barriers are safe
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  // Fused gate-cluster form (k_lstm_seq<true>): one gate tile per CTA, the four gates of a
+  // 64-column block in one cluster. Needs whole blocks, a CTA per unit, vectorizable gx, the
+  // 16 KB exchange buffer, and every cluster resident at once (the grid barriers spin).
+  // DEEPTHIN_LSTM_FUSED=0 keeps the three-phase form (A/B runs; both are complete).
+  static const bool want_fused = !(getenv("DEEPTHIN_LSTM_FUSED") && atoi(getenv("DEEPTHIN_LSTM_FUSED")) == 0);
+  bool fused = want_fused && a.H % 64 == 0 && unitsB <= nsm && unitsP <= unitsB && a.vec &&
+               smem + 16384 <= 226 * 1024;
+  if (fused) {
+    if (int rc = set_smem_limit(reinterpret_cast<const void *>(k_lstm_seq<true>), 226 * 1024)) return rc;
+    cudaLaunchConfig_t fc = cfg;
+    fc.gridDim = dim3((unsigned)unitsB);
+    fc.dynamicSmemBytes = smem + 16384;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 4;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    fc.numAttrs = 2;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_lstm_seq<true>, &fc) != cudaSuccess || ncl < unitsB / 4) {
+      cudaGetLastError();
+      fused = false;
+    } else {
+      cfg = fc;
+      grid = unitsB;
+      smem += 16384;
+    }
+  }
   static const bool tracing = DT_DBG_ENV("DEEPTHIN_LSTM_TRACE") != 0;
   a.trace = nullptr;
   if (tracing) {
     DT_CUDA_CHECK(cudaMalloc(&a.trace, 64 * 8));
     DT_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 64 * 8, st));
   }
-  DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_lstm_seq, a));
+  if (fused) {
+    if (cudaLaunchKernelEx(&cfg, k_lstm_seq<true>, a) != cudaSuccess) {
+      cudaGetLastError();  // cooperative + cluster launch refused: the three-phase form
+      fused = false;
+      cfg.gridDim = dim3((unsigned)std::min(nsm, std::max(unitsP, unitsB)));
+      cfg.dynamicSmemBytes = lstm_seq_smem(g);
+      cfg.numAttrs = 1;
+    }
+  }
+  if (!fused) DT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_lstm_seq<false>, a));
   if (tracing) {
     unsigned long long h[64];
     DT_CUDA_CHECK(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st));
