@@ -682,7 +682,8 @@ int lstm_seq(const Geo &g, int64_t T, int64_t batch, const void *const *gx, cons
   // 64-column block in one cluster. Needs whole blocks, a CTA per unit, vectorizable gx, the
   // 16 KB exchange buffer, and every cluster resident at once (the grid barriers spin).
   // DEEPTHIN_LSTM_FUSED=0 keeps the three-phase form (A/B runs; both are complete).
-  static const bool want_fused = !(getenv("DEEPTHIN_LSTM_FUSED") && atoi(getenv("DEEPTHIN_LSTM_FUSED")) == 0);
+  const char *fenv = getenv("DEEPTHIN_LSTM_FUSED");  // read per call (tests flip it)
+  const bool want_fused = !(fenv && atoi(fenv) == 0);
   bool fused = want_fused && a.H % 64 == 0 && unitsB <= nsm && unitsP <= unitsB && a.vec &&
                smem + 16384 <= 226 * 1024;
   if (fused) {

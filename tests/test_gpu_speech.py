@@ -173,3 +173,39 @@ def test_lstm_padded_geometries(H, n, R, B, T):
         hh, cc = O.lstm_cell([x[t * B:(t + 1) * B] for x in gxn], ghh, cc)
         got = out[t * B:(t + 1) * B].double().cpu().numpy()
         assert np.max(np.abs(got - hh)) <= 2 ** -8 + 1e-4, t  # bf16 output rounding
+
+
+@pytest.mark.parametrize("H,n,R,B,T", [(512, 256, 12, 17, 4), (1024, 256, 8, 64, 3)])
+def test_lstm_sequence_fused_gate_clusters_equal_three_phase_form(H, n, R, B, T, monkeypatch):
+    """The fused gate-cluster recurrence (four gates of a 64-column block in a cluster of four,
+    DSMEM scatter, cell state in registers, two grid barriers per step: the default when the
+    geometry allows) gives the bits of the three-phase form (DEEPTHIN_LSTM_FUSED=0), also with
+    ragged batch rows and when called twice on the same workspace."""
+    import ctypes as C
+    from paper_1802_06944_b200 import _lib
+    from test_gpu_forward import make_case
+    lib = _lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    cases = [make_case(H, H, R, n, H * H // n, 1, seed=70 + g, bias_sd=0.1) for g in range(4)]
+    ps = _lib.plan_struct(cases[0][2].plan)
+    P = lambda ts: (C.c_void_p * 4)(*[t.data_ptr() for t in ts])
+    xfs, wfs = P([c[2].xf for c in cases]), P([c[2].wf for c in cases])
+    bs_t = [torch.tensor(c[1]["bias"], dtype=torch.float32, device="cuda") for c in cases]
+    bs = P(bs_t)
+    rng = np.random.default_rng(H + B)
+    gx = [torch.tensor(rng.standard_normal((T * B, H)), dtype=torch.float32,
+                       device="cuda").to(torch.bfloat16) for _ in range(4)]
+    ws = torch.empty(lib.dt_lstm_sequence_workspace_bytes(C.byref(ps), B), dtype=torch.uint8,
+                     device="cuda")
+    outs = {}
+    for mode in ("0", "1", "1"):
+        monkeypatch.setenv("DEEPTHIN_LSTM_FUSED", mode)
+        out = torch.empty((T * B, H), dtype=torch.bfloat16, device="cuda")
+        _lib.check(lib.dt_lstm_sequence(C.byref(ps), T, B, P(gx), xfs, wfs, bs, out.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), st))
+        torch.cuda.synchronize()
+        if mode in outs:
+            assert torch.equal(out, outs[mode])
+        outs[mode] = out
+    assert torch.equal(outs["0"], outs["1"])
+    assert float(outs["1"].float().abs().max()) > 0.05
