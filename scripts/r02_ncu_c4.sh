@@ -2,6 +2,7 @@
 # Round-2 ncu evidence for config 4's recurrence (fused gate-cluster k_lstm_seq) at T = 8.
 set -u
 mkdir -p gpurun_out/r02
+
 T=8 python scripts/c4_probe.py > gpurun_out/r02/plain_c4.log 2>&1 || { cat gpurun_out/r02/plain_c4.log; exit 1; }
 cat gpurun_out/r02/plain_c4.log
 T=8 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
