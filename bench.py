@@ -879,7 +879,9 @@ def run_network(args, cfg, key):
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 1), "unit": "samples/s",
                     "h2d_bytes_per_step": int(hx.numel() * 2),
-                    "d2h_bytes_per_step": int(hy.numel() * 2), "matches_device_path": bool(ok)},
+                    "d2h_bytes_per_step": int(hy.numel() * 2), "matches_device_path": bool(ok),
+                    "path": f"DeviceModel.forward_host: {e2e_chunks} row blocks pipelined over "
+                            "H2D / forward (CUDA graph per block) / D2H streams, pinned buffers"},
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
